@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""Benchmark: latent-map optimisation iterations/s (render + dict-attention decode + backward
++ Adam) on BASELINE.json config 2 (8 keyframes at 640x480, N=500k, d=32, K=256, D=512) by
+default; one "step" = one Stage-I iteration over the whole keyframe window
+(total_objective + step_map + step_dict, proj/src/pipeline.cpp:236-246).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+N>1 runs under torchrun: the 8 keyframes are split across ranks (strong scaling), each rank
+renders / decodes / back-propagates its frames, the gradient and loss buffers are summed with
+NCCL all-reduce and every rank applies the same fused Adam. The time is the max over ranks.
+``--impl reference`` times the reference's CPU algorithm (the C oracle port, all host threads)
+on bounded row-band samples of the same workload and extrapolates to the full step.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "latent-map opt iters/s (render+dict-attn+bwd) 640x480, % roofline, vs CPU"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], p["bf16_tflops"], p["bf16_tflops_sustained"], "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- workload
+def gpu_render_fn(ctx):
+    import torch
+
+    from paper_2602_12314_b200 import api
+
+    def fn(m, q, t, intr):
+        gm = api.GaussianMap.from_numpy(m)
+        out = api.render(ctx, gm, api.make_pose(q, t),
+                         api.make_intrinsics(intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height))
+        res = out.color.cpu().numpy(), out.depth.cpu().numpy(), out.alpha.cpu().numpy()
+        del out, gm
+        torch.cuda.synchronize()
+        return res
+
+    return fn
+
+
+def decoder_flops_executed(n, k, ds):
+    # factored algebra: S = Q Kd^T, P M, dQ = dS Kd, R = Q^T dS, A = P^T diag(a) P
+    return 2.0 * n * k * (3 * ds + 2 * k)
+
+
+def decoder_flops_algorithmic(n, k, ds, df):
+    return 6.0 * n * k * (ds + df)
+
+
+def raster_bytes(n, v, pt, h, w, ds):
+    """Algorithmic bytes per frame by kernel (SURVEY.md §8(d) formula, split per kernel)."""
+    px = h * w
+    return {
+        "bin": n * 44 + n * 48 + pt * 8 * 2 * 2,
+        "raster_fwd": pt * (48 + 12 + 4 * ds) + px * 4 * (5 + ds) + px * 8,
+        "raster_bwd": pt * (48 + 12 + 4 * ds) + px * 4 * (4 + ds) + px * 8 + v * 4 * (10 + ds),
+        "project_bwd": v * (44 + 48 + 32) + n * 4 * (14 + ds) * 0 + v * 4 * 12 * 2,
+    }
+
+
+# ----------------------------------------------------------------------------- reference arm
+def cpu_reference(cfg_id, samples, budget_s=150.0, threads=None):
+    """Times the reference CPU algorithm (oracle port) on row-band samples of one keyframe and
+    extrapolates linearly in band height: t_frame(h) = a + b h  ->  t_step = F (a + b H) + t_adam."""
+    import oracle
+    from paper_2602_12314_b200 import synthetic
+
+    threads = threads or os.cpu_count() or 1
+    oracle.build()
+
+    def orender(m, q, t, intr):
+        om = oracle.GaussianMap(*[np.ascontiguousarray(getattr(m, f), np.float32) for f in oracle.FIELDS])
+        out = oracle.render(om, q, t, oracle.make_intr(intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height),
+                            threads=threads)
+        return out["color"], out["depth"], out["alpha"]
+
+    w = synthetic.make_workload(cfg_id, orender)
+    W, H = w.intr.width, w.intr.height
+    om = oracle.GaussianMap(*[np.ascontiguousarray(getattr(w.map, f), np.float32) for f in oracle.FIELDS])
+    d = oracle.Dictionary(w.atoms.copy(), w.anchor.copy(), w.proj.copy(), np.float32(w.temperature))
+    cfg = oracle.Config(lambda_l2=w.lambdas["lambda_l2"], lambda_i2=w.lambdas["lambda_i2"],
+                        lambda_trust=w.lambdas["lambda_trust"])
+    opt = oracle.MapOptimizer()
+    heights = (4, 8) if H >= 64 else (2, 4)
+    rows, t_obj, t_adam = [], [], []
+    t_start = time.time()
+    for i in range(max(2, samples)):
+        hb = heights[i % 2]
+        fr = w.frames[i % len(w.frames)]
+        y0 = H // 2 - hb // 2
+        intr = oracle.make_intr(w.intr.fx, w.intr.fy, w.intr.cx, w.intr.cy - y0, W, hb)
+        band = oracle.Frame(fr.pose_rot, fr.pose_trans, np.ascontiguousarray(fr.rgb[y0:y0 + hb]),
+                            np.ascontiguousarray(fr.depth[y0:y0 + hb]),
+                            np.ascontiguousarray(fr.assignment[y0:y0 + hb].reshape(-1)), fr.features)
+        t0 = time.perf_counter()
+        _, (g, dp, da) = oracle.total_objective(om, d, [band], intr, cfg, threads=threads)
+        t1 = time.perf_counter()
+        opt.step_map(om, g, cfg)
+        opt.step_dict(d, dp, da, cfg)
+        t2 = time.perf_counter()
+        rows.append(hb)
+        t_obj.append(t1 - t0)
+        t_adam.append(t2 - t1)
+        if i >= 1 and time.time() - t_start > budget_s:
+            break
+    A = np.stack([np.ones(len(rows)), np.asarray(rows, np.float64)], 1)
+    a, b = np.linalg.lstsq(A, np.asarray(t_obj), rcond=None)[0]
+    a = max(a, 0.0)
+    t_frame = a + b * H
+    t_step = len(w.frames) * t_frame + float(np.median(t_adam))
+    return {
+        "value": 1.0 / t_step, "unit": "iters/s", "cores": threads, "kind": "port",
+        "sample": (f"oracle C port (reference algorithm, -O3, no -march) on {len(rows)} row-band samples "
+                   f"({heights[0]}/{heights[1]} rows x {W} px of one keyframe, full N={w.map.n} projection), "
+                   f"t_frame = a + b*rows fitted and extrapolated to {H} rows x {len(w.frames)} frames + Adam "
+                   f"(extrapolated); t_step={t_step:.1f}s, a={a:.3f}s, b={b:.3f}s/row"),
+        "seconds_spent": time.time() - t_start,
+    }
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-phases", type=int, default=1)
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2602_12314_b200 import synthetic
+
+    cfg_name = synthetic.NAMES[args.config]
+    config = {"workload": cfg_name, "keyframes": synthetic.SPECS[args.config][-1],
+              "gaussians": synthetic.SPECS[args.config][5], "query_dim": synthetic.SPECS[args.config][8],
+              "dict_K": synthetic.SPECS[args.config][9], "embed_D": synthetic.SPECS[args.config][10],
+              "image": f"{synthetic.SPECS[args.config][0]}x{synthetic.SPECS[args.config][1]}",
+              "parallelism": f"keyframe-sharded x{world}" if world > 1 else "single GPU",
+              "l2": "working set > L2 (126 MB) every step; no explicit flush"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        ref = cpu_reference(args.config, args.steps + args.warmup)
+        line = {"impl": "reference", "metric": METRIC, "value": ref["value"], "unit": "iters/s",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1000.0 / ref["value"], "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, BASELINE config)",
+                "config": config, "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": ref["value"], "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import torch
+
+    from paper_2602_12314_b200 import api
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    ctx = api.Context(local_rank)
+    w = synthetic.make_workload(args.config, gpu_render_fn(ctx))
+    nf = len(w.frames)
+    if nf % world:
+        raise SystemExit(f"{nf} keyframes do not split over {world} ranks")
+    per = nf // world
+    mine = w.frames[rank * per:(rank + 1) * per]
+    cfg = api.default_config(**w.lambdas)
+    cfg.decoder_precision = 0
+    intr = api.make_intrinsics(w.intr.fx, w.intr.fy, w.intr.cx, w.intr.cy, w.intr.width, w.intr.height)
+    s = api.Session(ctx, cfg, w.map.n, w.map.features.shape[1], w.atoms.shape[0], w.atoms.shape[1], intr)
+    s.set_map(w.map)
+    s.set_dictionary(w.atoms, w.anchor, w.proj)
+    # pinned host copies of this rank's keyframes (the e2e path copies them H2D every step)
+    pinned = []
+    for f in mine:
+        pf = synthetic.Frame(f.pose_rot, f.pose_trans,
+                             *[torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+                               for a in (f.rgb, f.depth, f.assignment, f.features)])
+        pinned.append(pf)
+    s.set_frames(pinned)
+    s.set_batch(nf, add_trust=(rank == 0), slot_offset=rank * per)
+    grads = s.grad_buffer()
+    parts = s.loss_buffer()
+
+    def one_step(read=False):
+        if world == 1:
+            return s.step(read=read)
+        s.objective(want_grad=True, read=False)
+        dist.all_reduce(grads)
+        dist.all_reduce(parts)
+        s.apply()
+        return s.read_loss() if read else None
+
+    stream = torch.cuda.current_stream()
+    first = one_step(read=True)  # sizes the tile buffers
+    for _ in range(max(0, args.warmup - 1)):
+        one_step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.25)
+    if args.profile_phases:
+        s.profile(True)
+        s.phase_times()
+    launches0 = ctx.launches()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        one_step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = ctx.launches() - launches0
+    phases = s.phase_times() if args.profile_phases else {}
+    s.profile(False)
+    clocks = sampler.stop()
+    if dist:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = 1000.0 / ms_per_step
+
+    # e2e through the public API: H2D of the step's keyframes from pinned memory, the step,
+    # D2H of the LossBreakdown (host sync) every step.
+    h2d = sum(f.rgb.nbytes + f.depth.nbytes + f.assignment.nbytes + f.features.nbytes for f in pinned)
+    d2h = 48
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_steps = max(3, args.steps // 2)
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(e_steps):
+        s.set_frames(pinned)
+        last = one_step(read=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e_wall = (time.perf_counter() - t0) * 1000.0
+    e_ms = max(e0.elapsed_time(e1), e_wall)
+    if dist:
+        t = torch.tensor([e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t.item())
+    e2e = {"value": 1000.0 * e_steps / e_ms, "unit": "iters/s", "h2d_bytes_per_step": int(h2d) * world,
+           "d2h_bytes_per_step": d2h * world, "steps": e_steps}
+
+    # roofline of the dominant kernel (phase), per launch
+    hbm, bf16_burst, bf16_sus, src = peaks()
+    vis, pairs = s.stats(len(mine))
+    H, W = w.intr.height, w.intr.width
+    n, ds, K, D = w.map.n, w.map.features.shape[1], w.atoms.shape[0], w.atoms.shape[1]
+    per_launch = {}
+    for ph, (tms, cnt) in phases.items():
+        if cnt == 0:
+            continue
+        per_launch[ph] = {"ms_per_launch": tms / cnt, "launches": cnt, "share": None}
+    total_ph = sum(v[0] for v in phases.values()) or 1.0
+    for ph in per_launch:
+        per_launch[ph]["share"] = phases[ph][0] / total_ph
+    rb = raster_bytes(n, float(np.mean(vis)), float(np.mean(pairs)), H, W, ds)
+    roof = None
+    if per_launch:
+        dom = max(per_launch, key=lambda p: phases[p][0])
+        t_launch = per_launch[dom]["ms_per_launch"] / 1000.0
+        if dom == "decoder":
+            fl = decoder_flops_executed(H * W, K, ds)
+            roof = {"kernel": "decoder (fused feature loss + backward, factored algebra)", "bound": "tensor",
+                    "achieved": fl / t_launch / 1e12, "peak": bf16_sus, "unit": "TFLOP/s",
+                    "frac": fl / t_launch / 1e12 / bf16_sus, "traffic": None,
+                    "algorithmic_per_launch": fl, "peak_source": f"{src} bf16 sustained",
+                    "algorithmic_equiv_tflops": decoder_flops_algorithmic(H * W, K, ds, D) / t_launch / 1e12}
+        elif dom in rb:
+            by = rb[dom]
+            roof = {"kernel": dom, "bound": "hbm", "achieved": by / t_launch / 1e9, "peak": hbm, "unit": "GB/s",
+                    "frac": by / t_launch / 1e9 / hbm, "traffic": None, "algorithmic_per_launch": by,
+                    "peak_source": f"{src} HBM copy"}
+        else:
+            roof = {"kernel": dom, "bound": "hbm", "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None,
+                    "traffic": None}
+    line = {"metric": METRIC, "value": value * 1.0, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32 (decoder fp32 SIMT)" if cfg.decoder_precision == 0 else "bf16 decoder",
+            "data": "synthetic (seeded BASELINE config; targets rendered from a perturbed map)",
+            "config": config, "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
+            "phases": {k: round(v["ms_per_launch"], 4) for k, v in per_launch.items()},
+            "phase_share": {k: round(v["share"], 4) for k, v in per_launch.items()},
+            "visible_per_frame": float(np.mean(vis)), "tile_pairs_per_frame": float(np.mean(pairs)),
+            "loss_first": first["total"] if first else None, "loss_last": last["total"] if last else None}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ref = cpu_reference(args.config, 6, budget_s=40.0)
+        line["cpu_baseline"] = {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    if rank == 0:
+        print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

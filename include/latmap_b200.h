@@ -1,0 +1,231 @@
+/*
+ * latmap_b200.h — C-ABI of the B200-native latent-map optimisation step.
+ *
+ * Drop-in boundary for the reference operator API in
+ * /root/reference/proj/include/latmap/** (LatentAM CPU reference). Every entry
+ * point names the reference interface it replaces (file:line, relative to
+ * /root/reference/proj/). Conventions:
+ *   - extern "C", plain pointers and sizes, no C++ types, no exceptions;
+ *   - tensors are fp32 row-major in the reference's SoA layouts
+ *     (core/types.hpp:19-22,93-100); "device" pointers live on the context's GPU;
+ *   - every call returns a latmap_status; the C++ layer (latmap_b200.hpp) maps
+ *     LATMAP_ERR_INVALID_ARGUMENT -> std::invalid_argument and
+ *     LATMAP_ERR_STALE_CACHE -> std::runtime_error, as the reference throws;
+ *   - one context per host thread; calls on a context are stream-ordered on the
+ *     stream it was created with (or set via latmap_ctx_set_stream).
+ * There is no CPU fallback: without a CUDA device every call fails with
+ * LATMAP_ERR_CUDA.
+ */
+#ifndef LATMAP_B200_H
+#define LATMAP_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LATMAP_OK = 0,
+  LATMAP_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+  LATMAP_ERR_STALE_CACHE = 2,      /* std::runtime_error: render.cpp:256-260, dictionary.cpp:59-64 */
+  LATMAP_ERR_CUDA = 3,
+  LATMAP_ERR_OUT_OF_MEMORY = 4,
+  LATMAP_ERR_UNSUPPORTED = 5
+} latmap_status;
+
+typedef struct latmap_ctx latmap_ctx;
+typedef struct latmap_render_cache latmap_render_cache;
+typedef struct latmap_session latmap_session;
+
+/* Intrinsics, core/types.hpp:41-50 */
+typedef struct {
+  float fx, fy, cx, cy;
+  int32_t width, height;
+} latmap_intrinsics;
+
+/* PoseT<float>: (w,x,y,z) rotation + translation, camera-to-world, core/types.hpp:27-38 */
+typedef struct {
+  float rotation[4];
+  float translation[3];
+} latmap_pose;
+
+/* GaussianMapT<float> / MapGradientsT<float> view (device pointers),
+ * core/types.hpp:93-199, splat/render.hpp:57-92 */
+typedef struct {
+  int64_t n;
+  int32_t query_dim;
+  float* positions;      /* n x 3 */
+  float* rotations;      /* n x 4 */
+  float* colors;         /* n x 3 */
+  float* log_scales;     /* n x 3 */
+  float* opacity_logits; /* n     */
+  float* features;       /* n x query_dim */
+} latmap_map;
+
+/* ProjectedSplat<float>, splat/render.hpp:31-39 */
+typedef struct {
+  float mean2d[2];
+  float cov_inv[4]; /* row-major 2x2 */
+  float depth;
+  float alpha;
+  int32_t source, x0, x1, y0, y1;
+} latmap_projected_splat;
+
+/* LossBreakdown<float>, obj/objective.hpp:12-24 */
+typedef struct {
+  float l_rgb, l_ssim, l_depth, l_cos, l_l2, l_trust, total;
+  int64_t supervised_rows;
+  int32_t depth_empty, zero_norm_flagged;
+} latmap_loss_breakdown;
+
+/* Hot-path subset of latmap::Config, core/config.hpp:10-71 (same defaults). */
+typedef struct {
+  float lambda_cos, lambda_l2, lambda_trust, trust_delta;
+  float lambda_i1, lambda_i2, lambda_rgb, lambda_depth, lambda_feat;
+  float lr_proj, lr_dict, lr_position, lr_rotation, lr_color, lr_log_scale, lr_opacity, lr_feature;
+  float scene_extent;
+  float softmax_temp;         /* DictionaryStateT::temperature (pipeline.cpp:116) */
+  int32_t dict_learn;         /* step_dict learn_atoms (pipeline.cpp:91-95) */
+  int32_t segment_mode;       /* feature_supervision == "segment" (objective.cpp:78) */
+  int32_t decoder_precision;  /* 0: fp32 SIMT (bit-faithful algebra), 1: bf16 tcgen05 */
+} latmap_config;
+
+/* KeyframeT<float> as host arrays, core/types.hpp:224-248 */
+typedef struct {
+  latmap_pose pose;
+  const float* rgb;          /* H x W x 3 */
+  const float* depth;        /* H x W     */
+  const int32_t* assignment; /* H x W, -1 = unsupervised (EmbeddingSetT, types.hpp:204-221) */
+  const float* features;     /* n_set x embed_dim */
+  int64_t n_set;
+} latmap_frame;
+
+/* ---------------------------------------------------------------- context */
+latmap_status latmap_ctx_create(int32_t device, void* cuda_stream, latmap_ctx** out);
+latmap_status latmap_ctx_destroy(latmap_ctx* ctx);
+latmap_status latmap_ctx_set_stream(latmap_ctx* ctx, void* cuda_stream);
+latmap_status latmap_ctx_synchronize(latmap_ctx* ctx);
+const char* latmap_ctx_last_error(const latmap_ctx* ctx);
+/* Kernels launched by this context since creation (evidence for the bench). */
+int64_t latmap_ctx_launch_count(const latmap_ctx* ctx);
+void latmap_default_config(latmap_config* cfg);
+
+/* ---------------------------------------------------------------- renderer */
+/* project_gaussian, splat/render.hpp:97-99 (host values in, host values out).
+ * *visible = 0 when culled (std::nullopt). */
+latmap_status latmap_project_gaussian(latmap_ctx* ctx, const float position[3], const float rotation[4],
+                                      const float log_scale[3], float opacity_logit,
+                                      const latmap_pose* pose, const latmap_intrinsics* intr,
+                                      int32_t* visible, float mean2d[2], float cov2d[4], float* depth);
+
+/* RenderOutputT::splats + fingerprint holder (splat/render.hpp:41-53). */
+latmap_status latmap_render_cache_create(latmap_ctx* ctx, latmap_render_cache** out);
+latmap_status latmap_render_cache_destroy(latmap_render_cache* cache);
+
+/* render, splat/render.hpp:103-105. Device outputs: color HxWx3, depth HxW, query HxWxds, alpha HxW.
+ * Fills `cache` (projected splats, (tile, depth)-sorted tile lists, per-pixel blend extents). */
+latmap_status latmap_render(latmap_ctx* ctx, const latmap_map* map, const latmap_pose* pose,
+                            const latmap_intrinsics* intr, latmap_render_cache* cache, float* color,
+                            float* depth, float* query, float* alpha);
+
+/* render_backward, splat/render.hpp:116-119. Upstream images may be NULL (= zero).
+ * Gradients are ACCUMULATED (+=) into `grads` (device); LATMAP_ERR_STALE_CACHE when
+ * the cache fingerprint does not match (render.cpp:256-260). */
+latmap_status latmap_render_backward(latmap_ctx* ctx, const latmap_map* map, const latmap_pose* pose,
+                                     const latmap_intrinsics* intr, const latmap_render_cache* cache,
+                                     const float* d_color, const float* d_depth, const float* d_query,
+                                     latmap_map* grads);
+
+/* Parity exports (host buffers): splats in source order (RenderOutput::splats), and the
+ * canonical tile lists (16x16 tiles; per tile the sources whose bbox meets it, ordered by
+ * (depth, source)). Pass NULL buffers to query sizes. */
+latmap_status latmap_render_cache_splats(latmap_ctx* ctx, const latmap_render_cache* cache,
+                                         latmap_projected_splat* out, int64_t cap, int64_t* count);
+latmap_status latmap_render_cache_tiles(latmap_ctx* ctx, const latmap_render_cache* cache,
+                                        int32_t* tile_offsets, int32_t* tile_sources, int64_t cap,
+                                        int32_t* tiles_x, int32_t* tiles_y, int64_t* pairs);
+
+/* ---------------------------------------------------------------- decoder (device pointers) */
+/* reconstruct, dict/dictionary.hpp:63-65: out = softmax(Q W D^T / temperature) D.
+ * attention (n x K) optional (AttentionCache::attention). */
+latmap_status latmap_reconstruct(latmap_ctx* ctx, const float* queries, int64_t n, int32_t query_dim,
+                                 const float* atoms, const float* proj, int64_t k, int32_t embed_dim,
+                                 float temperature, float* out, float* attention);
+/* reconstruct_backward, dict/dictionary.hpp:67-70 (general upstream d_rec). */
+latmap_status latmap_reconstruct_backward(latmap_ctx* ctx, const float* queries, const float* attention,
+                                          int64_t n, int32_t query_dim, const float* atoms,
+                                          const float* proj, int64_t k, int32_t embed_dim,
+                                          float temperature, const float* d_rec, float* d_queries,
+                                          float* d_proj, float* d_atoms);
+/* trust_region_penalty, dict/dictionary.hpp:75-77. d_atoms may be NULL. penalty: host float. */
+latmap_status latmap_trust_region_penalty(latmap_ctx* ctx, const float* atoms, const float* anchor,
+                                          int64_t k, int32_t embed_dim, float delta, float* d_atoms,
+                                          float* penalty);
+
+/* ---------------------------------------------------------------- losses (device pointers) */
+/* ssim, obj/losses.hpp:12-13; d_a optional (overwritten). Returns the mean SSIM in *value. */
+latmap_status latmap_ssim(latmap_ctx* ctx, const float* a, const float* b, int32_t h, int32_t w,
+                          int32_t channels, float* d_a, float* value);
+
+/* ---------------------------------------------------------------- optimiser */
+/* adam_step, obj/adam.hpp:61-79 on one device block. *step / *skipped are the host-side
+ * AdamState counters (updated); returns *applied = 0 when the block had a non-finite grad. */
+latmap_status latmap_adam_step(latmap_ctx* ctx, float* param, const float* grad, float* m, float* v,
+                               int64_t count, int64_t* step, int64_t* skipped, float lr,
+                               int32_t* applied);
+
+/* ---------------------------------------------------------------- device-resident session */
+/* The throughput path: GaussianMap + DictionaryState + MapOptimizer moments stay in HBM;
+ * one latmap_session_step == one Stage-I iteration (pipeline.cpp:236-246):
+ * total_objective (objective.cpp:67-194) -> step_map -> step_dict (pipeline.cpp:75-95). */
+latmap_status latmap_session_create(latmap_ctx* ctx, const latmap_config* cfg, int64_t n,
+                                    int32_t query_dim, int64_t k, int32_t embed_dim,
+                                    const latmap_intrinsics* intr, latmap_session** out);
+latmap_status latmap_session_destroy(latmap_session* s);
+/* Host -> device upload of the map (GaussianMapT SoA host arrays). */
+latmap_status latmap_session_set_map(latmap_session* s, const float* positions, const float* rotations,
+                                     const float* colors, const float* log_scales,
+                                     const float* opacity_logits, const float* features);
+latmap_status latmap_session_get_map(latmap_session* s, float* positions, float* rotations,
+                                     float* colors, float* log_scales, float* opacity_logits,
+                                     float* features);
+/* DictionaryStateT: atoms K x df, anchor K x df, proj ds x df (host arrays). */
+latmap_status latmap_session_set_dictionary(latmap_session* s, const float* atoms, const float* anchor,
+                                            const float* proj);
+latmap_status latmap_session_get_dictionary(latmap_session* s, float* atoms, float* proj);
+/* Keyframe batch (host arrays, copied H2D on the session stream). */
+latmap_status latmap_session_set_frames(latmap_session* s, int32_t nframes, const latmap_frame* frames);
+/* Batch-mean denominator (objective.cpp:77) and whether this rank adds the trust term
+ * (objective.cpp:176-185); used when keyframes are sharded across ranks. */
+latmap_status latmap_session_set_batch(latmap_session* s, int32_t global_batch, int32_t add_trust);
+/* Global index of this rank's first frame: its loss partials land in that slot so a sum
+ * all-reduce of the partials buffer reassembles the batch LossBreakdown. */
+latmap_status latmap_session_set_slot_offset(latmap_session* s, int32_t offset);
+/* total_objective with gradients into the session's flat gradient buffer. `out` (host) may be
+ * NULL to avoid a device->host sync. */
+latmap_status latmap_session_objective(latmap_session* s, int32_t want_grad, latmap_loss_breakdown* out);
+/* MapOptimizer::step_map + step_dict on the session gradients (pipeline.cpp:75-95). */
+latmap_status latmap_session_apply(latmap_session* s);
+/* objective + apply; `out` may be NULL. */
+latmap_status latmap_session_step(latmap_session* s, latmap_loss_breakdown* out);
+/* Flat device buffers: [positions|rotations|colors|log_scales|opacity|features|proj|atoms]
+ * gradient layout (for the multi-GPU all-reduce) and the loss-partials vector. */
+latmap_status latmap_session_grad_buffer(latmap_session* s, float** grads, int64_t* count);
+latmap_status latmap_session_loss_buffer(latmap_session* s, double** partials, int64_t* count);
+latmap_status latmap_session_read_loss(latmap_session* s, latmap_loss_breakdown* out);
+/* Per-frame render outputs of the last objective (device pointers; parity and Stage-II reuse). */
+latmap_status latmap_session_frame_images(latmap_session* s, int32_t frame, float** color, float** depth,
+                                          float** query, float** alpha);
+/* Phase timing with CUDA events on the session stream: phases 0 project+bin+sort (K1-K3b),
+ * 1 raster forward (K4), 2 image losses (K5), 3 decoder+feature loss (K6/K7), 4 raster backward (K8),
+ * 5 projection backward (K9), 6 Adam (K10), 7 reserved. phase_times syncs, returns the summed
+ * milliseconds and span counts since the last call, and resets them. */
+latmap_status latmap_session_profile(latmap_session* s, int32_t enable);
+latmap_status latmap_session_phase_times(latmap_session* s, double* ms, int64_t* counts);
+/* Counters of the last objective: visible splats and tile pairs per frame (for roofline bytes). */
+latmap_status latmap_session_stats(latmap_session* s, int64_t* visible, int64_t* pairs);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,165 @@
+"""ctypes binding of include/latmap_b200.h (liblatmap_b200.so).
+
+This is the reference-side FFI a Python caller binds; INTEGRATION.md shows the
+equivalent C++ / ctypes stubs. Loading fails loudly when the library is missing:
+there is no CPU fallback in the product path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liblatmap_b200.so")
+
+OK, EINVAL, ESTALE, ECUDA, ENOMEM, EUNSUPPORTED = range(6)
+
+
+class LatmapError(RuntimeError):
+    pass
+
+
+class InvalidArgument(LatmapError, ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class StaleCache(LatmapError):
+    """std::runtime_error for stale render / attention caches (render.cpp:256-260)."""
+
+
+class Intrinsics(C.Structure):
+    _fields_ = [("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float),
+                ("width", C.c_int32), ("height", C.c_int32)]
+
+
+class Pose(C.Structure):
+    _fields_ = [("rotation", C.c_float * 4), ("translation", C.c_float * 3)]
+
+
+class MapView(C.Structure):
+    _fields_ = [("n", C.c_int64), ("query_dim", C.c_int32)] + [
+        (f, C.c_void_p) for f in ("positions", "rotations", "colors", "log_scales", "opacity_logits", "features")]
+
+
+class ProjectedSplat(C.Structure):
+    _fields_ = [("mean2d", C.c_float * 2), ("cov_inv", C.c_float * 4), ("depth", C.c_float), ("alpha", C.c_float),
+                ("source", C.c_int32), ("x0", C.c_int32), ("x1", C.c_int32), ("y0", C.c_int32), ("y1", C.c_int32)]
+
+
+class LossBreakdown(C.Structure):
+    _fields_ = [(f, C.c_float) for f in ("l_rgb", "l_ssim", "l_depth", "l_cos", "l_l2", "l_trust", "total")] + [
+        ("supervised_rows", C.c_int64), ("depth_empty", C.c_int32), ("zero_norm_flagged", C.c_int32)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+CONFIG_FLOATS = ("lambda_cos", "lambda_l2", "lambda_trust", "trust_delta", "lambda_i1", "lambda_i2", "lambda_rgb",
+                 "lambda_depth", "lambda_feat", "lr_proj", "lr_dict", "lr_position", "lr_rotation", "lr_color",
+                 "lr_log_scale", "lr_opacity", "lr_feature", "scene_extent", "softmax_temp")
+
+
+class Config(C.Structure):
+    _fields_ = [(f, C.c_float) for f in CONFIG_FLOATS] + [
+        ("dict_learn", C.c_int32), ("segment_mode", C.c_int32), ("decoder_precision", C.c_int32)]
+
+
+class Frame(C.Structure):
+    _fields_ = [("pose", Pose), ("rgb", C.c_void_p), ("depth", C.c_void_p), ("assignment", C.c_void_p),
+                ("features", C.c_void_p), ("n_set", C.c_int64)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run __graft_entry__.build() (no CPU fallback exists)")
+        _lib = C.CDLL(LIB_PATH)
+        _declare(_lib)
+    return _lib
+
+
+def _declare(L):
+    P = C.c_void_p
+    st = C.c_int
+    sig = {
+        "latmap_ctx_create": [C.c_int32, P, C.POINTER(P)],
+        "latmap_ctx_destroy": [P],
+        "latmap_ctx_set_stream": [P, P],
+        "latmap_ctx_synchronize": [P],
+        "latmap_project_gaussian": [P, P, P, P, C.c_float, C.POINTER(Pose), C.POINTER(Intrinsics),
+                                    C.POINTER(C.c_int32), P, P, P],
+        "latmap_render_cache_create": [P, C.POINTER(P)],
+        "latmap_render_cache_destroy": [P],
+        "latmap_render": [P, C.POINTER(MapView), C.POINTER(Pose), C.POINTER(Intrinsics), P, P, P, P, P],
+        "latmap_render_backward": [P, C.POINTER(MapView), C.POINTER(Pose), C.POINTER(Intrinsics), P, P, P, P,
+                                   C.POINTER(MapView)],
+        "latmap_render_cache_splats": [P, P, P, C.c_int64, C.POINTER(C.c_int64)],
+        "latmap_render_cache_tiles": [P, P, P, P, C.c_int64, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                      C.POINTER(C.c_int64)],
+        "latmap_reconstruct": [P, P, C.c_int64, C.c_int32, P, P, C.c_int64, C.c_int32, C.c_float, P, P],
+        "latmap_reconstruct_backward": [P, P, P, C.c_int64, C.c_int32, P, P, C.c_int64, C.c_int32, C.c_float, P, P,
+                                        P, P],
+        "latmap_trust_region_penalty": [P, P, P, C.c_int64, C.c_int32, C.c_float, P, C.POINTER(C.c_float)],
+        "latmap_ssim": [P, P, P, C.c_int32, C.c_int32, C.c_int32, P, C.POINTER(C.c_float)],
+        "latmap_adam_step": [P, P, P, P, P, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.c_float,
+                             C.POINTER(C.c_int32)],
+        "latmap_session_create": [P, C.POINTER(Config), C.c_int64, C.c_int32, C.c_int64, C.c_int32,
+                                  C.POINTER(Intrinsics), C.POINTER(P)],
+        "latmap_session_destroy": [P],
+        "latmap_session_set_map": [P, P, P, P, P, P, P],
+        "latmap_session_get_map": [P, P, P, P, P, P, P],
+        "latmap_session_set_dictionary": [P, P, P, P],
+        "latmap_session_get_dictionary": [P, P, P],
+        "latmap_session_set_frames": [P, C.c_int32, C.POINTER(Frame)],
+        "latmap_session_set_batch": [P, C.c_int32, C.c_int32],
+        "latmap_session_set_slot_offset": [P, C.c_int32],
+        "latmap_session_objective": [P, C.c_int32, C.POINTER(LossBreakdown)],
+        "latmap_session_apply": [P],
+        "latmap_session_step": [P, C.POINTER(LossBreakdown)],
+        "latmap_session_grad_buffer": [P, C.POINTER(P), C.POINTER(C.c_int64)],
+        "latmap_session_loss_buffer": [P, C.POINTER(P), C.POINTER(C.c_int64)],
+        "latmap_session_read_loss": [P, C.POINTER(LossBreakdown)],
+        "latmap_session_frame_images": [P, C.c_int32, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(P)],
+        "latmap_session_stats": [P, P, P],
+        "latmap_session_profile": [P, C.c_int32],
+        "latmap_session_phase_times": [P, P, P],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = st
+    L.latmap_ctx_last_error.argtypes = [P]
+    L.latmap_ctx_last_error.restype = C.c_char_p
+    L.latmap_ctx_launch_count.argtypes = [P]
+    L.latmap_ctx_launch_count.restype = C.c_int64
+    L.latmap_default_config.argtypes = [C.POINTER(Config)]
+    L.latmap_default_config.restype = None
+
+
+EXPORTED = ["latmap_ctx_create", "latmap_ctx_destroy", "latmap_ctx_set_stream", "latmap_ctx_synchronize",
+            "latmap_ctx_last_error", "latmap_ctx_launch_count", "latmap_default_config", "latmap_project_gaussian",
+            "latmap_render_cache_create", "latmap_render_cache_destroy", "latmap_render", "latmap_render_backward",
+            "latmap_render_cache_splats", "latmap_render_cache_tiles", "latmap_reconstruct",
+            "latmap_reconstruct_backward", "latmap_trust_region_penalty", "latmap_ssim", "latmap_adam_step",
+            "latmap_session_create", "latmap_session_destroy", "latmap_session_set_map", "latmap_session_get_map",
+            "latmap_session_set_dictionary", "latmap_session_get_dictionary", "latmap_session_set_frames",
+            "latmap_session_set_batch", "latmap_session_set_slot_offset", "latmap_session_objective",
+            "latmap_session_apply", "latmap_session_step", "latmap_session_grad_buffer", "latmap_session_loss_buffer",
+            "latmap_session_read_loss", "latmap_session_frame_images", "latmap_session_stats",
+            "latmap_session_profile", "latmap_session_phase_times"]
+
+
+def check(ctx_handle, status):
+    if status == OK:
+        return
+    msg = lib().latmap_ctx_last_error(ctx_handle)
+    msg = msg.decode() if msg else ""
+    if status == EINVAL:
+        raise InvalidArgument(msg)
+    if status == ESTALE:
+        raise StaleCache(msg)
+    raise LatmapError(f"latmap status {status}: {msg}")

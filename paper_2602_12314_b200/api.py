@@ -1,0 +1,380 @@
+"""Python mirror of the reference operator API (proj/include/latmap/**) over the C-ABI.
+
+Same names, argument meaning and error behaviour as the reference:
+``render`` / ``render_backward`` (splat/render.hpp:97-119), ``reconstruct`` /
+``reconstruct_backward`` / ``trust_region_penalty`` (dict/dictionary.hpp:63-77),
+``ssim`` (obj/losses.hpp:12-13), ``adam_step`` (obj/adam.hpp:61-79) and the
+device-resident ``Session`` running Stage-I iterations (total_objective +
+MapOptimizer::step_map/step_dict, objective.cpp:67-194 / pipeline.cpp:75-95).
+Tensors are torch CUDA float32 (torch is only the device-memory plumbing).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, fields
+
+import numpy as np
+import torch
+
+from . import _capi
+from ._capi import Config, Frame, Intrinsics, LossBreakdown, MapView, Pose, check, lib
+
+MAP_FIELDS = ("positions", "rotations", "colors", "log_scales", "opacity_logits", "features")
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    assert t.is_cuda and t.dtype == torch.float32 and t.is_contiguous(), "expected contiguous cuda float32"
+    return C.c_void_p(t.data_ptr())
+
+
+@dataclass
+class GaussianMap:
+    """GaussianMapT<float> on the device (core/types.hpp:93-199)."""
+    positions: torch.Tensor
+    rotations: torch.Tensor
+    colors: torch.Tensor
+    log_scales: torch.Tensor
+    opacity_logits: torch.Tensor
+    features: torch.Tensor
+
+    @property
+    def n(self):
+        return self.positions.shape[0]
+
+    @property
+    def query_dim(self):
+        return self.features.shape[1]
+
+    def view(self):
+        return MapView(self.n, self.query_dim, *[_ptr(getattr(self, f)) for f in MAP_FIELDS])
+
+    @staticmethod
+    def from_numpy(m, device="cuda"):
+        return GaussianMap(*[torch.as_tensor(np.ascontiguousarray(getattr(m, f), np.float32), device=device)
+                             for f in MAP_FIELDS])
+
+    def zeros_like(self):
+        return GaussianMap(*[torch.zeros_like(getattr(self, f)) for f in MAP_FIELDS])
+
+    def numpy(self):
+        return {f: getattr(self, f).detach().cpu().numpy() for f in MAP_FIELDS}
+
+
+def make_pose(rotation=(1, 0, 0, 0), translation=(0, 0, 0)):
+    return Pose((C.c_float * 4)(*[float(v) for v in rotation]), (C.c_float * 3)(*[float(v) for v in translation]))
+
+
+def make_intrinsics(fx, fy, cx, cy, width, height):
+    return Intrinsics(fx, fy, cx, cy, width, height)
+
+
+class Context:
+    """A latmap_ctx bound to one device and torch's current stream."""
+
+    def __init__(self, device=0):
+        self.device = device
+        torch.cuda.set_device(device)
+        self.stream = torch.cuda.current_stream(device)
+        h = C.c_void_p()
+        st = lib().latmap_ctx_create(device, C.c_void_p(self.stream.cuda_stream), C.byref(h))
+        check(None, st)
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().latmap_ctx_destroy(self.h)
+            self.h = None
+
+    def sync(self):
+        check(self.h, lib().latmap_ctx_synchronize(self.h))
+
+    def launches(self):
+        return lib().latmap_ctx_launch_count(self.h)
+
+
+class RenderOutput:
+    """RenderOutputT<float> (splat/render.hpp:41-53): images + the projection cache."""
+
+    def __init__(self, ctx, color, depth, query, alpha, cache):
+        self.ctx, self.color, self.depth, self.query, self.alpha, self._cache = ctx, color, depth, query, alpha, cache
+
+    def __del__(self):
+        if getattr(self, "_cache", None):
+            lib().latmap_render_cache_destroy(self._cache)
+            self._cache = None
+
+    def splats(self):
+        """ProjectedSplat records of the surviving splats in source order (numpy structured)."""
+        L = lib()
+        cnt = C.c_int64(0)
+        check(self.ctx.h, L.latmap_render_cache_splats(self.ctx.h, self._cache, None, 0, C.byref(cnt)))
+        arr = (_capi.ProjectedSplat * max(cnt.value, 1))()
+        check(self.ctx.h, L.latmap_render_cache_splats(self.ctx.h, self._cache, arr, cnt.value, C.byref(cnt)))
+        dt = np.dtype([("mean", np.float32, 2), ("cov_inv", np.float32, 4), ("depth", np.float32),
+                       ("alpha", np.float32), ("source", np.int32), ("x0", np.int32), ("x1", np.int32),
+                       ("y0", np.int32), ("y1", np.int32)])
+        return np.frombuffer(bytes(arr), dtype=dt, count=cnt.value).copy()
+
+    def tiles(self):
+        """(tiles_x, tiles_y, offsets[ntiles+1], sources[pairs]) of the canonical tile lists."""
+        L = lib()
+        tx, ty, pairs = C.c_int32(), C.c_int32(), C.c_int64()
+        check(self.ctx.h, L.latmap_render_cache_tiles(self.ctx.h, self._cache, None, None, 0, C.byref(tx),
+                                                      C.byref(ty), C.byref(pairs)))
+        off = np.zeros(tx.value * ty.value + 1, np.int32)
+        src = np.zeros(max(pairs.value, 1), np.int32)
+        check(self.ctx.h, L.latmap_render_cache_tiles(self.ctx.h, self._cache, off.ctypes.data_as(C.c_void_p),
+                                                      src.ctypes.data_as(C.c_void_p), pairs.value, None, None, None))
+        return tx.value, ty.value, off, src[: pairs.value]
+
+
+def project_gaussian(ctx, position, rotation, log_scale, opacity_logit, pose, intr):
+    """project_gaussian (splat/render.hpp:97-99); None when culled."""
+    arrs = [np.ascontiguousarray(a, np.float32) for a in (position, rotation, log_scale)]
+    vis = C.c_int32(0)
+    mean = np.zeros(2, np.float32)
+    cov = np.zeros(4, np.float32)
+    depth = np.zeros(1, np.float32)
+    check(ctx.h, lib().latmap_project_gaussian(ctx.h, *[a.ctypes.data_as(C.c_void_p) for a in arrs],
+                                               float(opacity_logit), C.byref(pose), C.byref(intr), C.byref(vis),
+                                               mean.ctypes.data_as(C.c_void_p), cov.ctypes.data_as(C.c_void_p),
+                                               depth.ctypes.data_as(C.c_void_p)))
+    if not vis.value:
+        return None
+    return mean, cov.reshape(2, 2), float(depth[0])
+
+
+def render(ctx, m: GaussianMap, pose, intr) -> RenderOutput:
+    """render (splat/render.hpp:103-105)."""
+    h, w = intr.height, intr.width
+    dev = m.positions.device
+    color = torch.empty((h, w, 3), device=dev)
+    depth = torch.empty((h, w), device=dev)
+    query = torch.empty((h, w, m.query_dim), device=dev)
+    alpha = torch.empty((h, w), device=dev)
+    cache = C.c_void_p()
+    check(ctx.h, lib().latmap_render_cache_create(ctx.h, C.byref(cache)))
+    out = RenderOutput(ctx, color, depth, query, alpha, cache)
+    mv = m.view()
+    check(ctx.h, lib().latmap_render(ctx.h, C.byref(mv), C.byref(pose), C.byref(intr), cache, _ptr(color),
+                                     _ptr(depth), _ptr(query), _ptr(alpha)))
+    return out
+
+
+def render_backward(ctx, m: GaussianMap, pose, intr, out: RenderOutput, d_color=None, d_depth=None, d_query=None):
+    """render_backward (splat/render.hpp:116-119) -> MapGradients (fresh zeros + accumulated)."""
+    g = m.zeros_like()
+    mv, gv = m.view(), g.view()
+    check(ctx.h, lib().latmap_render_backward(ctx.h, C.byref(mv), C.byref(pose), C.byref(intr), out._cache,
+                                              _ptr(d_color), _ptr(d_depth), _ptr(d_query), C.byref(gv)))
+    return g
+
+
+def reconstruct(ctx, queries, atoms, proj, temperature, want_attention=False):
+    """reconstruct (dict/dictionary.hpp:63-65)."""
+    n, ds = queries.shape
+    k, df = atoms.shape
+    if proj.shape[0] != ds:
+        raise _capi.InvalidArgument("reconstruct: query dimension mismatch")
+    if proj.shape[1] != df:
+        raise _capi.InvalidArgument("reconstruct: projection/atom dimension mismatch")
+    out = torch.empty((n, df), device=queries.device)
+    att = torch.empty((n, k), device=queries.device) if want_attention else None
+    check(ctx.h, lib().latmap_reconstruct(ctx.h, _ptr(queries), n, ds, _ptr(atoms), _ptr(proj), k, df,
+                                          float(temperature), _ptr(out), _ptr(att)))
+    return (out, att) if want_attention else out
+
+
+def reconstruct_backward(ctx, queries, attention, atoms, proj, temperature, d_rec):
+    """reconstruct_backward (dict/dictionary.hpp:67-70)."""
+    n, ds = queries.shape
+    k, df = atoms.shape
+    dq = torch.empty_like(queries)
+    dp = torch.empty_like(proj)
+    da = torch.empty_like(atoms)
+    check(ctx.h, lib().latmap_reconstruct_backward(ctx.h, _ptr(queries), _ptr(attention), n, ds, _ptr(atoms),
+                                                   _ptr(proj), k, df, float(temperature), _ptr(d_rec), _ptr(dq),
+                                                   _ptr(dp), _ptr(da)))
+    return dict(d_queries=dq, d_proj=dp, d_atoms=da)
+
+
+def trust_region_penalty(ctx, atoms, anchor, delta, want_grad=False):
+    """trust_region_penalty (dict/dictionary.hpp:75-77)."""
+    if atoms.shape != anchor.shape:
+        raise _capi.InvalidArgument("trust_region_penalty: shape mismatch")
+    g = torch.empty_like(atoms) if want_grad else None
+    v = C.c_float(0)
+    check(ctx.h, lib().latmap_trust_region_penalty(ctx.h, _ptr(atoms), _ptr(anchor), atoms.shape[0], atoms.shape[1],
+                                                   float(delta), _ptr(g), C.byref(v)))
+    return (v.value, g) if want_grad else v.value
+
+
+def ssim(ctx, a, b, want_grad=False):
+    """ssim (obj/losses.hpp:12-13) on HxWxC (or HxW) images."""
+    if a.shape != b.shape:
+        raise _capi.InvalidArgument("ssim: image shapes differ")
+    h, w = a.shape[:2]
+    ch = a.shape[2] if a.dim() == 3 else 1
+    da = torch.empty_like(a) if want_grad else None
+    v = C.c_float(0)
+    check(ctx.h, lib().latmap_ssim(ctx.h, _ptr(a), _ptr(b), h, w, ch, _ptr(da), C.byref(v)))
+    return (v.value, da) if want_grad else v.value
+
+
+@dataclass
+class AdamState:
+    m: torch.Tensor
+    v: torch.Tensor
+    step: int = 0
+    skipped: int = 0
+
+
+def adam_step(ctx, param, grad, st: AdamState, lr):
+    """adam_step (obj/adam.hpp:61-79); returns False when the block was skipped."""
+    s, k, ap = C.c_int64(st.step), C.c_int64(st.skipped), C.c_int32(0)
+    check(ctx.h, lib().latmap_adam_step(ctx.h, _ptr(param), _ptr(grad), _ptr(st.m), _ptr(st.v), param.numel(),
+                                        C.byref(s), C.byref(k), float(lr), C.byref(ap)))
+    st.step, st.skipped = s.value, k.value
+    return bool(ap.value)
+
+
+def default_config(**overrides) -> Config:
+    c = Config()
+    lib().latmap_default_config(C.byref(c))
+    for kk, vv in overrides.items():
+        setattr(c, kk, vv)
+    return c
+
+
+class Session:
+    """Device-resident map + dictionary + Adam moments; one ``step`` = one Stage-I iteration."""
+
+    def __init__(self, ctx: Context, cfg: Config, n, query_dim, k, embed_dim, intr):
+        self.ctx, self.cfg, self.intr = ctx, cfg, intr
+        self.n, self.ds, self.k, self.df = n, query_dim, k, embed_dim
+        h = C.c_void_p()
+        check(ctx.h, lib().latmap_session_create(ctx.h, C.byref(cfg), n, query_dim, k, embed_dim, C.byref(intr),
+                                                 C.byref(h)))
+        self.h = h
+        self._keep = []
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().latmap_session_destroy(self.h)
+            self.h = None
+
+    @staticmethod
+    def _np_ptr(a):
+        return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+    def set_map(self, m):
+        arrs = [np.ascontiguousarray(getattr(m, f), np.float32) for f in MAP_FIELDS]
+        check(self.ctx.h, lib().latmap_session_set_map(self.h, *[self._np_ptr(a) for a in arrs]))
+        self.ctx.sync()
+
+    def get_map(self):
+        out = [np.zeros((self.n, c), np.float32) for c in (3, 4, 3, 3)] + [np.zeros(self.n, np.float32),
+                                                                            np.zeros((self.n, self.ds), np.float32)]
+        check(self.ctx.h, lib().latmap_session_get_map(self.h, *[self._np_ptr(a) for a in out]))
+        return dict(zip(MAP_FIELDS, out))
+
+    def set_dictionary(self, atoms=None, anchor=None, proj=None):
+        arrs = [None if a is None else np.ascontiguousarray(a, np.float32) for a in (atoms, anchor, proj)]
+        check(self.ctx.h, lib().latmap_session_set_dictionary(self.h, *[self._np_ptr(a) for a in arrs]))
+        self.ctx.sync()
+
+    def get_dictionary(self):
+        atoms = np.zeros((self.k, self.df), np.float32)
+        proj = np.zeros((self.ds, self.df), np.float32)
+        check(self.ctx.h, lib().latmap_session_get_dictionary(self.h, self._np_ptr(atoms), self._np_ptr(proj)))
+        return atoms, proj
+
+    def set_frames(self, frames):
+        """frames: objects with pose_rot, pose_trans, rgb, depth, assignment, features (numpy, host).
+
+        The arrays are copied H2D on the session stream; pinned (page-locked) numpy buffers keep
+        the copies asynchronous."""
+        cf = (Frame * len(frames))()
+        keep = []
+        for i, f in enumerate(frames):
+            rgb = f.rgb if f.rgb.dtype == np.float32 and f.rgb.flags.c_contiguous else np.ascontiguousarray(f.rgb, np.float32)
+            dep = f.depth if f.depth.dtype == np.float32 and f.depth.flags.c_contiguous else np.ascontiguousarray(f.depth, np.float32)
+            asg = f.assignment if f.assignment.dtype == np.int32 and f.assignment.flags.c_contiguous else np.ascontiguousarray(f.assignment, np.int32)
+            fea = f.features if f.features.dtype == np.float32 and f.features.flags.c_contiguous else np.ascontiguousarray(f.features, np.float32)
+            keep.append((rgb, dep, asg, fea))
+            cf[i] = Frame(make_pose(f.pose_rot, f.pose_trans), self._np_ptr(rgb), self._np_ptr(dep),
+                          self._np_ptr(asg), self._np_ptr(fea), fea.shape[0])
+        self._keep = keep
+        check(self.ctx.h, lib().latmap_session_set_frames(self.h, len(frames), cf))
+
+    def set_batch(self, global_batch, add_trust=True, slot_offset=0):
+        check(self.ctx.h, lib().latmap_session_set_batch(self.h, int(global_batch), int(bool(add_trust))))
+        check(self.ctx.h, lib().latmap_session_set_slot_offset(self.h, int(slot_offset)))
+
+    def objective(self, want_grad=True, read=True):
+        out = LossBreakdown()
+        check(self.ctx.h, lib().latmap_session_objective(self.h, int(want_grad), C.byref(out) if read else None))
+        return out.as_dict() if read else None
+
+    def apply(self):
+        check(self.ctx.h, lib().latmap_session_apply(self.h))
+
+    def step(self, read=True):
+        out = LossBreakdown()
+        check(self.ctx.h, lib().latmap_session_step(self.h, C.byref(out) if read else None))
+        return out.as_dict() if read else None
+
+    def read_loss(self):
+        out = LossBreakdown()
+        check(self.ctx.h, lib().latmap_session_read_loss(self.h, C.byref(out)))
+        return out.as_dict()
+
+    def grad_buffer(self):
+        p, n = C.c_void_p(), C.c_int64()
+        check(self.ctx.h, lib().latmap_session_grad_buffer(self.h, C.byref(p), C.byref(n)))
+        return _device_view(p.value, n.value, torch.float32, self.ctx.device)
+
+    def loss_buffer(self):
+        p, n = C.c_void_p(), C.c_int64()
+        check(self.ctx.h, lib().latmap_session_loss_buffer(self.h, C.byref(p), C.byref(n)))
+        return _device_view(p.value, n.value, torch.float64, self.ctx.device)
+
+    def frame_images(self, b):
+        ps = [C.c_void_p() for _ in range(4)]
+        check(self.ctx.h, lib().latmap_session_frame_images(self.h, b, *[C.byref(p) for p in ps]))
+        h, w = self.intr.height, self.intr.width
+        shapes = [(h, w, 3), (h, w), (h, w, self.ds), (h, w)]
+        return [_device_view(p.value, int(np.prod(s)), torch.float32, self.ctx.device).view(*s)
+                for p, s in zip(ps, shapes)]
+
+    PHASES = ("bin", "raster_fwd", "image_losses", "decoder", "raster_bwd", "project_bwd", "adam", "misc")
+
+    def profile(self, enable=True):
+        check(self.ctx.h, lib().latmap_session_profile(self.h, int(enable)))
+
+    def phase_times(self):
+        ms = np.zeros(8, np.float64)
+        cnt = np.zeros(8, np.int64)
+        check(self.ctx.h, lib().latmap_session_phase_times(self.h, ms.ctypes.data_as(C.c_void_p),
+                                                           cnt.ctypes.data_as(C.c_void_p)))
+        return {p: (float(ms[i]), int(cnt[i])) for i, p in enumerate(self.PHASES)}
+
+    def stats(self, nframes):
+        vis = np.zeros(nframes, np.int64)
+        pairs = np.zeros(nframes, np.int64)
+        check(self.ctx.h, lib().latmap_session_stats(self.h, vis.ctypes.data_as(C.c_void_p),
+                                                     pairs.ctypes.data_as(C.c_void_p)))
+        return vis, pairs
+
+
+class _CudaArrayView:
+    def __init__(self, ptr, count, typestr):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr, "data": (ptr, False), "version": 3}
+
+
+def _device_view(ptr, count, dtype, device):
+    typestr = "<f4" if dtype == torch.float32 else "<f8"
+    with torch.cuda.device(device):
+        return torch.as_tensor(_CudaArrayView(ptr, count, typestr), device=f"cuda:{device}")

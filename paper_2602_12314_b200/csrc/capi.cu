@@ -1,0 +1,1104 @@
+// capi.cu — the C-ABI (include/latmap_b200.h): contexts, operator entry points and the
+// device-resident session that runs one Stage-I iteration (pipeline.cpp:236-246).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/latmap_b200.h"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace lm {
+
+static std::atomic<int64_t> g_launches{0};
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+void set_launch_counter(int64_t*) {}
+
+static thread_local std::string t_err;
+latmap_status set_cuda_error(cudaError_t e, const char* what, const char* file, int line) {
+  t_err = std::string(cudaGetErrorString(e)) + " at " + what + " (" + file + ":" + std::to_string(line) + ")";
+  return e == cudaErrorMemoryAllocation ? LATMAP_ERR_OUT_OF_MEMORY : LATMAP_ERR_CUDA;
+}
+
+// quat_to_rot (core/se3.hpp:12-23) in the reference's float op order; returns false on a
+// zero-norm or non-finite quaternion (std::invalid_argument in the reference).
+static bool quat_to_rot(const float q[4], float r[9]) {
+  const float ss = ((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3];
+  const float n = std::sqrt(ss);
+  if (!(n > 0.f) || !std::isfinite((double)n)) return false;
+  const float w = q[0] / n, x = q[1] / n, y = q[2] / n, z = q[3] / n;
+  r[0] = 1.f - 2.f * (y * y + z * z);
+  r[1] = 2.f * (x * y - w * z);
+  r[2] = 2.f * (x * z + w * y);
+  r[3] = 2.f * (x * y + w * z);
+  r[4] = 1.f - 2.f * (x * x + z * z);
+  r[5] = 2.f * (y * z - w * x);
+  r[6] = 2.f * (x * z - w * y);
+  r[7] = 2.f * (y * z + w * x);
+  r[8] = 1.f - 2.f * (x * x + y * y);
+  return true;
+}
+
+static bool pose_mats(const latmap_pose& p, float rot_cw[9], float rot_wc[9]) {
+  float r[9];
+  if (!quat_to_rot(p.rotation, r)) return false;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      rot_wc[3 * i + j] = r[3 * i + j];
+      rot_cw[3 * i + j] = r[3 * j + i];
+    }
+  return true;
+}
+
+static bool intr_valid(const latmap_intrinsics& i) {  // Intrinsics::valid, types.hpp:46-49
+  return i.fx > 0 && i.fy > 0 && i.width > 0 && i.height > 0 && i.cx >= 0 && i.cx < (float)i.width && i.cy >= 0 &&
+         i.cy < (float)i.height;
+}
+
+static Intr to_intr(const latmap_intrinsics& i) { return Intr{i.fx, i.fy, i.cx, i.cy, i.width, i.height}; }
+
+template <class T>
+static cudaError_t dgrow(T*& p, size_t& cap, size_t n) {
+  if (n <= cap && p) return cudaSuccess;
+  if (p) cudaFree(p);
+  p = nullptr;
+  cap = 0;
+  cudaError_t e = cudaMalloc(&p, sizeof(T) * std::max<size_t>(n, 1));
+  if (e == cudaSuccess) cap = n;
+  return e;
+}
+
+// Owns the device buffers of a RenderWork.
+struct RenderBufs {
+  RenderWork w;
+  size_t c_rec = 0, c_tiles = 0, c_keys = 0, c_px = 0, c_cnt = 0, c_geo = 0;
+  float* geo_acc = nullptr;
+  cudaError_t ensure(int64_t n, int width, int height, int64_t pairs) {
+    cudaError_t e;
+    w.width = width;
+    w.height = height;
+    w.tiles_x = (width + kTile - 1) / kTile;
+    w.tiles_y = (height + kTile - 1) / kTile;
+    const size_t nt = (size_t)w.tiles_x * w.tiles_y;
+    if ((e = dgrow(w.rec, c_rec, (size_t)std::max<int64_t>(n, 1)))) return e;
+    size_t c1 = c_tiles, c2 = c_tiles, c3 = c_tiles, c4 = c_tiles;
+    if (nt + 1 > c_tiles) {
+      c1 = c2 = c3 = c4 = 0;
+      if ((e = dgrow(w.tile_count, c1, nt + 1))) return e;
+      if ((e = dgrow(w.tile_offset, c2, nt + 1))) return e;
+      if ((e = dgrow(w.tile_cursor, c3, nt + 1))) return e;
+      if ((e = dgrow(w.tile_max_last, c4, nt + 1))) return e;
+      c_tiles = nt + 1;
+    }
+    if ((size_t)pairs > c_keys || !w.keys) {
+      size_t a = 0, b = 0;
+      if (w.keys) cudaFree(w.keys), w.keys = nullptr;
+      if (w.keys_tmp) cudaFree(w.keys_tmp), w.keys_tmp = nullptr;
+      if ((e = dgrow(w.keys, a, (size_t)std::max<int64_t>(pairs, 1)))) return e;
+      if ((e = dgrow(w.keys_tmp, b, (size_t)std::max<int64_t>(pairs, 1)))) return e;
+      c_keys = (size_t)std::max<int64_t>(pairs, 1);
+    }
+    w.pair_cap = (int64_t)c_keys;
+    size_t px = (size_t)width * height;
+    if (px > c_px) {
+      size_t a = 0, b = 0;
+      if (w.px_last) cudaFree(w.px_last), w.px_last = nullptr;
+      if (w.px_T) cudaFree(w.px_T), w.px_T = nullptr;
+      if ((e = dgrow(w.px_last, a, px))) return e;
+      if ((e = dgrow(w.px_T, b, px))) return e;
+      c_px = px;
+    }
+    if ((e = dgrow(w.counters, c_cnt, 4))) return e;
+    if ((e = dgrow(geo_acc, c_geo, (size_t)std::max<int64_t>(n, 1) * 8))) return e;
+    w.n_cap = n;
+    return cudaSuccess;
+  }
+  void release() {
+    for (void* p : {(void*)w.rec, (void*)w.tile_count, (void*)w.tile_offset, (void*)w.tile_cursor, (void*)w.keys,
+                    (void*)w.keys_tmp, (void*)w.px_last, (void*)w.px_T, (void*)w.counters, (void*)w.tile_max_last,
+                    (void*)geo_acc})
+      if (p) cudaFree(p);
+    w = RenderWork{};
+  }
+};
+
+}  // namespace lm
+
+using namespace lm;
+
+struct latmap_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int64_t launches0 = 0;
+};
+
+struct latmap_render_cache {
+  latmap_ctx* ctx = nullptr;
+  RenderBufs bufs;
+  bool valid = false;
+  int64_t source_count = 0;
+  latmap_pose pose{};
+  latmap_intrinsics intr{};
+  int32_t ds = 0;
+};
+
+#define CTX_CHECK(ctx, expr)                    \
+  do {                                          \
+    cudaError_t _e = (expr);                    \
+    if (_e != cudaSuccess) {                    \
+      latmap_status _s = set_cuda_error(_e, #expr, __FILE__, __LINE__); \
+      (ctx)->err = t_err;                       \
+      return _s;                                \
+    }                                           \
+  } while (0)
+
+static latmap_status fail(latmap_ctx* ctx, latmap_status s, const char* msg) {
+  if (ctx) ctx->err = msg;
+  return s;
+}
+
+static latmap_status post_launch(latmap_ctx* ctx) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    latmap_status s = set_cuda_error(e, "kernel launch", __FILE__, __LINE__);
+    ctx->err = t_err;
+    return s;
+  }
+  return LATMAP_OK;
+}
+
+extern "C" {
+
+void latmap_default_config(latmap_config* c) {  // config.hpp:10-71 defaults
+  std::memset(c, 0, sizeof(*c));
+  c->lambda_cos = 0.5f;
+  c->lambda_l2 = 0.5f;
+  c->lambda_trust = 0.2f;
+  c->trust_delta = 0.1f;
+  c->lambda_i1 = 0.2f;
+  c->lambda_i2 = 0.8f;
+  c->lambda_rgb = 1.0f;
+  c->lambda_depth = 0.1f;
+  c->lambda_feat = 5.0f;
+  c->lr_proj = 0.01f;
+  c->lr_dict = 0.01f;
+  c->lr_position = 1e-4f;
+  c->lr_rotation = 1e-3f;
+  c->lr_color = 2.5e-3f;
+  c->lr_log_scale = 5e-3f;
+  c->lr_opacity = 5e-2f;
+  c->lr_feature = 2.5e-3f;
+  c->scene_extent = 1.0f;
+  c->softmax_temp = 1.0f;
+  c->dict_learn = 1;
+  c->segment_mode = 0;
+  c->decoder_precision = 0;
+}
+
+latmap_status latmap_ctx_create(int32_t device, void* stream, latmap_ctx** out) {
+  if (!out) return LATMAP_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    t_err = "no CUDA device available (the B200 path has no CPU fallback)";
+    return LATMAP_ERR_CUDA;
+  }
+  if (device < 0 || device >= count) return LATMAP_ERR_INVALID_ARGUMENT;
+  e = cudaSetDevice(device);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaSetDevice", __FILE__, __LINE__);
+  latmap_ctx* c = new latmap_ctx();
+  c->device = device;
+  c->stream = (cudaStream_t)stream;
+  c->launches0 = g_launches.load();
+  *out = c;
+  return LATMAP_OK;
+}
+
+latmap_status latmap_ctx_destroy(latmap_ctx* ctx) {
+  if (!ctx) return LATMAP_ERR_INVALID_ARGUMENT;
+  cudaStreamSynchronize(ctx->stream);
+  delete ctx;
+  return LATMAP_OK;
+}
+
+latmap_status latmap_ctx_set_stream(latmap_ctx* ctx, void* stream) {
+  if (!ctx) return LATMAP_ERR_INVALID_ARGUMENT;
+  ctx->stream = (cudaStream_t)stream;
+  return LATMAP_OK;
+}
+
+latmap_status latmap_ctx_synchronize(latmap_ctx* ctx) {
+  if (!ctx) return LATMAP_ERR_INVALID_ARGUMENT;
+  CTX_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+  return LATMAP_OK;
+}
+
+const char* latmap_ctx_last_error(const latmap_ctx* ctx) { return ctx ? ctx->err.c_str() : t_err.c_str(); }
+
+int64_t latmap_ctx_launch_count(const latmap_ctx* ctx) { return g_launches.load() - (ctx ? ctx->launches0 : 0); }
+
+// ------------------------------------------------------------------------------- renderer
+latmap_status latmap_project_gaussian(latmap_ctx* ctx, const float position[3], const float rotation[4],
+                                      const float log_scale[3], float opacity_logit, const latmap_pose* pose,
+                                      const latmap_intrinsics* intr, int32_t* visible, float mean2d[2],
+                                      float cov2d[4], float* depth) {
+  if (!ctx || !pose || !intr || !visible) return LATMAP_ERR_INVALID_ARGUMENT;
+  float rcw[9], rwc[9];
+  if (!pose_mats(*pose, rcw, rwc)) return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "quat_to_rot: zero-norm quaternion");
+  float in[11];
+  std::memcpy(in, position, 12);
+  std::memcpy(in + 3, rotation, 16);
+  std::memcpy(in + 7, log_scale, 12);
+  in[10] = opacity_logit;
+  float* d = nullptr;
+  CTX_CHECK(ctx, cudaMallocAsync(&d, sizeof(float) * 19, ctx->stream));
+  CTX_CHECK(ctx, cudaMemcpyAsync(d, in, sizeof(in), cudaMemcpyHostToDevice, ctx->stream));
+  project_single(ctx->stream, d, rcw, pose->translation, to_intr(*intr), d + 11);
+  float out[8];
+  CTX_CHECK(ctx, cudaMemcpyAsync(out, d + 11, sizeof(out), cudaMemcpyDeviceToHost, ctx->stream));
+  CTX_CHECK(ctx, cudaFreeAsync(d, ctx->stream));
+  CTX_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+  *visible = out[0] != 0.f;
+  if (*visible) {
+    if (mean2d) mean2d[0] = out[1], mean2d[1] = out[2];
+    if (cov2d) std::memcpy(cov2d, out + 3, 16);
+    if (depth) *depth = out[7];
+  }
+  return LATMAP_OK;
+}
+
+latmap_status latmap_render_cache_create(latmap_ctx* ctx, latmap_render_cache** out) {
+  if (!ctx || !out) return LATMAP_ERR_INVALID_ARGUMENT;
+  auto* c = new latmap_render_cache();
+  c->ctx = ctx;
+  *out = c;
+  return LATMAP_OK;
+}
+
+latmap_status latmap_render_cache_destroy(latmap_render_cache* c) {
+  if (!c) return LATMAP_ERR_INVALID_ARGUMENT;
+  cudaStreamSynchronize(c->ctx->stream);
+  c->bufs.release();
+  delete c;
+  return LATMAP_OK;
+}
+
+static MapPtrs map_ptrs(const latmap_map* m) {
+  return MapPtrs{m->n, m->query_dim, m->positions, m->rotations, m->colors, m->log_scales, m->opacity_logits,
+                 m->features};
+}
+
+latmap_status latmap_render(latmap_ctx* ctx, const latmap_map* map, const latmap_pose* pose,
+                            const latmap_intrinsics* intr, latmap_render_cache* cache, float* color, float* depth,
+                            float* query, float* alpha) {
+  if (!ctx || !map || !pose || !intr || !cache) return LATMAP_ERR_INVALID_ARGUMENT;
+  if (!intr_valid(*intr)) return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "render: invalid intrinsics");
+  if (map->query_dim < 1 || map->query_dim > 64)
+    return fail(ctx, LATMAP_ERR_UNSUPPORTED, "render: query_dim must be in [1, 64]");
+  float rcw[9], rwc[9];
+  if (!pose_mats(*pose, rcw, rwc)) return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "quat_to_rot: zero-norm quaternion");
+  cudaStream_t st = ctx->stream;
+  RenderBufs& b = cache->bufs;
+  const MapPtrs mp = map_ptrs(map);
+  const Intr in = to_intr(*intr);
+  int64_t guess = std::max<int64_t>(b.w.pair_cap, 1);
+  CTX_CHECK(ctx, b.ensure(map->n, intr->width, intr->height, guess));
+  // sizing pass: project + scan, then read back the tile-pair count
+  render_forward(st, mp, rcw, pose->translation, in, b.w, color, depth, query, alpha, false, true);
+  int64_t counters[4];
+  CTX_CHECK(ctx, cudaMemcpyAsync(counters, b.w.counters, sizeof(counters), cudaMemcpyDeviceToHost, st));
+  CTX_CHECK(ctx, cudaStreamSynchronize(st));
+  if (counters[0] > b.w.pair_cap) CTX_CHECK(ctx, b.ensure(map->n, intr->width, intr->height, counters[0]));
+  render_forward(st, mp, rcw, pose->translation, in, b.w, color, depth, query, alpha, true, false);
+  latmap_status s = post_launch(ctx);
+  if (s != LATMAP_OK) return s;
+  cache->valid = true;
+  cache->source_count = map->n;
+  cache->pose = *pose;
+  cache->intr = *intr;
+  cache->ds = map->query_dim;
+  return LATMAP_OK;
+}
+
+latmap_status latmap_render_backward(latmap_ctx* ctx, const latmap_map* map, const latmap_pose* pose,
+                                     const latmap_intrinsics* intr, const latmap_render_cache* cache,
+                                     const float* d_color, const float* d_depth, const float* d_query,
+                                     latmap_map* grads) {
+  if (!ctx || !map || !pose || !intr || !cache || !grads) return LATMAP_ERR_INVALID_ARGUMENT;
+  // render.cpp:256-260: the cache must come from render() on identical inputs
+  const bool pose_match = std::memcmp(cache->pose.rotation, pose->rotation, 16) == 0 &&
+                          std::memcmp(cache->pose.translation, pose->translation, 12) == 0;
+  if (!cache->valid || cache->source_count != map->n || cache->intr.width != intr->width ||
+      cache->intr.height != intr->height || !pose_match)
+    return fail(ctx, LATMAP_ERR_STALE_CACHE, "render_backward: render cache does not match inputs");
+  if (map->n == 0) return LATMAP_OK;
+  float rcw[9], rwc[9];
+  pose_mats(*pose, rcw, rwc);
+  auto& b = const_cast<latmap_render_cache*>(cache)->bufs;
+  CTX_CHECK(ctx, cudaMemsetAsync(b.geo_acc, 0, sizeof(float) * 8 * map->n, ctx->stream));
+  render_backward(ctx->stream, map_ptrs(map), rcw, rwc, pose->translation, to_intr(*intr), b.w, d_color, d_depth,
+                  d_query, b.geo_acc, map_ptrs(grads));
+  return post_launch(ctx);
+}
+
+latmap_status latmap_render_cache_splats(latmap_ctx* ctx, const latmap_render_cache* cache,
+                                         latmap_projected_splat* out, int64_t cap, int64_t* count) {
+  if (!ctx || !cache || !count || !cache->valid) return LATMAP_ERR_INVALID_ARGUMENT;
+  const int64_t n = cache->source_count;
+  std::vector<SplatRec> rec((size_t)std::max<int64_t>(n, 1));
+  if (n > 0)
+    CTX_CHECK(ctx, cudaMemcpyAsync(rec.data(), cache->bufs.w.rec, sizeof(SplatRec) * n, cudaMemcpyDeviceToHost,
+                                   ctx->stream));
+  CTX_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+  int64_t k = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const SplatRec& r = rec[i];
+    if (r.x0 > r.x1) continue;
+    if (out && k < cap) {
+      latmap_projected_splat& s = out[k];
+      s.mean2d[0] = r.mean_x;
+      s.mean2d[1] = r.mean_y;
+      s.cov_inv[0] = r.a00;
+      s.cov_inv[1] = r.a01;
+      s.cov_inv[2] = r.a10;
+      s.cov_inv[3] = r.a11;
+      s.depth = r.depth;
+      s.alpha = r.alpha;
+      s.source = (int32_t)i;
+      s.x0 = r.x0;
+      s.x1 = r.x1;
+      s.y0 = r.y0;
+      s.y1 = r.y1;
+    }
+    ++k;
+  }
+  *count = k;
+  return (out && k > cap) ? LATMAP_ERR_INVALID_ARGUMENT : LATMAP_OK;
+}
+
+latmap_status latmap_render_cache_tiles(latmap_ctx* ctx, const latmap_render_cache* cache, int32_t* tile_offsets,
+                                        int32_t* tile_sources, int64_t cap, int32_t* tiles_x, int32_t* tiles_y,
+                                        int64_t* pairs) {
+  if (!ctx || !cache || !cache->valid) return LATMAP_ERR_INVALID_ARGUMENT;
+  const RenderWork& w = cache->bufs.w;
+  const int nt = w.tiles_x * w.tiles_y;
+  int64_t counters[4];
+  CTX_CHECK(ctx, cudaMemcpyAsync(counters, w.counters, sizeof(counters), cudaMemcpyDeviceToHost, ctx->stream));
+  CTX_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+  if (tiles_x) *tiles_x = w.tiles_x;
+  if (tiles_y) *tiles_y = w.tiles_y;
+  if (pairs) *pairs = counters[0];
+  if (tile_offsets)
+    CTX_CHECK(ctx, cudaMemcpy(tile_offsets, w.tile_offset, sizeof(int32_t) * (nt + 1), cudaMemcpyDeviceToHost));
+  if (tile_sources) {
+    if (cap < counters[0]) return LATMAP_ERR_INVALID_ARGUMENT;
+    std::vector<uint64_t> keys((size_t)std::max<int64_t>(counters[0], 1));
+    if (counters[0] > 0)
+      CTX_CHECK(ctx, cudaMemcpy(keys.data(), w.keys, sizeof(uint64_t) * counters[0], cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < counters[0]; ++i) tile_sources[i] = (int32_t)(uint32_t)keys[i];
+  }
+  return LATMAP_OK;
+}
+
+// ------------------------------------------------------------------------------- decoder ops
+latmap_status latmap_reconstruct(latmap_ctx* ctx, const float* q, int64_t n, int32_t ds, const float* atoms,
+                                 const float* proj, int64_t k, int32_t df, float temperature, float* out,
+                                 float* attention) {
+  if (!ctx || n < 0 || ds < 1 || k < 1 || df < 1 || !out) return LATMAP_ERR_INVALID_ARGUMENT;
+  if (!(temperature > 0.f)) return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "reconstruct: temperature must be > 0");
+  if (n == 0) return LATMAP_OK;
+  cudaStream_t st = ctx->stream;
+  float *qw = nullptr, *att = attention;
+  CTX_CHECK(ctx, cudaMallocAsync(&qw, sizeof(float) * n * df, st));
+  if (!att) CTX_CHECK(ctx, cudaMallocAsync(&att, sizeof(float) * n * k, st));
+  reconstruct(st, q, n, ds, atoms, proj, k, df, temperature, out, att, qw);
+  CTX_CHECK(ctx, cudaFreeAsync(qw, st));
+  if (!attention) CTX_CHECK(ctx, cudaFreeAsync(att, st));
+  return post_launch(ctx);
+}
+
+latmap_status latmap_reconstruct_backward(latmap_ctx* ctx, const float* q, const float* attention, int64_t n,
+                                          int32_t ds, const float* atoms, const float* proj, int64_t k, int32_t df,
+                                          float temperature, const float* d_rec, float* d_q, float* d_proj,
+                                          float* d_atoms) {
+  if (!ctx || !q || !attention || !d_rec || !d_q || !d_proj || !d_atoms) return LATMAP_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = ctx->stream;
+  if (n == 0) {
+    CTX_CHECK(ctx, cudaMemsetAsync(d_proj, 0, sizeof(float) * ds * df, st));
+    CTX_CHECK(ctx, cudaMemsetAsync(d_atoms, 0, sizeof(float) * k * df, st));
+    return LATMAP_OK;
+  }
+  float *snk = nullptr, *sndf = nullptr;
+  CTX_CHECK(ctx, cudaMallocAsync(&snk, sizeof(float) * n * k, st));
+  CTX_CHECK(ctx, cudaMallocAsync(&sndf, sizeof(float) * n * df, st));
+  reconstruct_backward(st, q, attention, n, ds, atoms, proj, k, df, temperature, d_rec, d_q, d_proj, d_atoms, snk,
+                       sndf, nullptr);
+  CTX_CHECK(ctx, cudaFreeAsync(snk, st));
+  CTX_CHECK(ctx, cudaFreeAsync(sndf, st));
+  return post_launch(ctx);
+}
+
+latmap_status latmap_trust_region_penalty(latmap_ctx* ctx, const float* atoms, const float* anchor, int64_t k,
+                                          int32_t df, float delta, float* d_atoms, float* penalty) {
+  if (!ctx || !atoms || !anchor) return LATMAP_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = ctx->stream;
+  double* dp = nullptr;
+  CTX_CHECK(ctx, cudaMallocAsync(&dp, sizeof(double), st));
+  CTX_CHECK(ctx, cudaMemsetAsync(dp, 0, sizeof(double), st));
+  if (d_atoms) CTX_CHECK(ctx, cudaMemsetAsync(d_atoms, 0, sizeof(float) * k * df, st));
+  trust_region(st, atoms, anchor, k, df, delta, d_atoms, 1.f, dp);
+  double v = 0;
+  CTX_CHECK(ctx, cudaMemcpyAsync(&v, dp, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CTX_CHECK(ctx, cudaFreeAsync(dp, st));
+  CTX_CHECK(ctx, cudaStreamSynchronize(st));
+  if (penalty) *penalty = (float)v;
+  return post_launch(ctx);
+}
+
+latmap_status latmap_ssim(latmap_ctx* ctx, const float* a, const float* b, int32_t h, int32_t w, int32_t ch,
+                          float* d_a, float* value) {
+  if (!ctx || !a || !b || h < 1 || w < 1 || ch < 1) return LATMAP_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = ctx->stream;
+  float* scratch = nullptr;
+  CTX_CHECK(ctx, cudaMallocAsync(&scratch, sizeof(float) * ssim_scratch_floats(h, w, ch), st));
+  const double v = ssim_host(st, a, b, h, w, ch, d_a, scratch);
+  CTX_CHECK(ctx, cudaFreeAsync(scratch, st));
+  CTX_CHECK(ctx, cudaStreamSynchronize(st));
+  if (value) *value = (float)v;
+  return post_launch(ctx);
+}
+
+// ------------------------------------------------------------------------------- Adam
+static void corr_tables(std::vector<float>& c1, std::vector<float>& c2, int len) {
+  c1.resize(len);
+  c2.resize(len);
+  for (int t = 1; t <= len; ++t) {  // adam.hpp:74-75: T(1) - T(std::pow(beta, double(step)))
+    c1[t - 1] = 1.f - (float)std::pow(0.9, (double)t);
+    c2[t - 1] = 1.f - (float)std::pow(0.999, (double)t);
+  }
+}
+static const int kCorrLen = 1 << 16;
+
+latmap_status latmap_adam_step(latmap_ctx* ctx, float* param, const float* grad, float* m, float* v, int64_t count,
+                               int64_t* step, int64_t* skipped, float lr, int32_t* applied) {
+  if (!ctx || !param || !grad || !m || !v || !step || !skipped) return LATMAP_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = ctx->stream;
+  const int64_t t = *step + 1;
+  float c1 = 1.f, c2 = 1.f;
+  if (t <= kCorrLen) {
+    c1 = 1.f - (float)std::pow(0.9, (double)t);
+    c2 = 1.f - (float)std::pow(0.999, (double)t);
+  }
+  struct Aux {
+    int64_t steps, skipped;
+    int32_t flags[2];
+    float c1, c2;
+  } aux{*step, *skipped, {0, 0}, c1, c2};
+  char* d = nullptr;
+  CTX_CHECK(ctx, cudaMallocAsync(&d, sizeof(Aux), st));
+  CTX_CHECK(ctx, cudaMemcpyAsync(d, &aux, sizeof(Aux), cudaMemcpyHostToDevice, st));
+  Aux* da = (Aux*)d;
+  // table of length 1 holding the bias corrections for step t
+  AdamBlock blk{0, count, lr, 0};
+  int64_t one_back = 0;  // steps array seen by the kernel: t - 1 - 0 -> use table index 0
+  (void)one_back;
+  int64_t* d_steps = &da->steps;
+  // The kernel computes t = steps + 1 and indexes corr[t-1]; pass a shifted table pointer.
+  const float* c1p = &da->c1 - *step;
+  const float* c2p = &da->c2 - *step;
+  adam_flat(st, param, grad, m, v, &blk, 1, d_steps, &da->skipped, c1p, c2p, (int32_t)std::min<int64_t>(t, 1 << 30),
+            da->flags, nullptr);
+  Aux back;
+  CTX_CHECK(ctx, cudaMemcpyAsync(&back, d, sizeof(Aux), cudaMemcpyDeviceToHost, st));
+  CTX_CHECK(ctx, cudaFreeAsync(d, st));
+  CTX_CHECK(ctx, cudaStreamSynchronize(st));
+  if (applied) *applied = back.skipped == *skipped;
+  *step = back.steps;
+  *skipped = back.skipped;
+  return post_launch(ctx);
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------------- session
+namespace {
+struct FrameDev {
+  float* rgb = nullptr;
+  float* depth = nullptr;
+  int32_t* assign = nullptr;
+  float* feats = nullptr;
+  size_t c_px = 0, c_feat = 0;
+  int64_t n_set = 0, n_sup = 0;
+  latmap_pose pose{};
+  float rcw[9], rwc[9];
+};
+constexpr int kPart = 8;  // per-frame loss partial slots (see losses.cu / decoder.cu)
+}  // namespace
+
+struct latmap_session {
+  latmap_ctx* ctx = nullptr;
+  latmap_config cfg{};
+  int64_t n = 0, k = 0;
+  int32_t ds = 0, df = 0;
+  latmap_intrinsics intr{};
+  int64_t total = 0, off[9] = {};
+  float *params = nullptr, *grads = nullptr, *m = nullptr, *v = nullptr, *anchor = nullptr;
+  int64_t *steps = nullptr, *skipped = nullptr, *overflow = nullptr;
+  int32_t* flags = nullptr;
+  float *corr1 = nullptr, *corr2 = nullptr;
+  std::vector<FrameDev> frames;
+  int32_t nframes = 0, global_batch = 0, add_trust = 1, slot_offset = 0;
+  std::vector<RenderBufs> rw;
+  std::vector<float*> color, depth, query, alpha;
+  float *d_color = nullptr, *d_depth = nullptr, *d_query = nullptr, *ssim_scratch = nullptr;
+  DecoderWork dec;
+  double* partials = nullptr;
+  int32_t part_frames = 0;
+  latmap_loss_breakdown* d_loss = nullptr;
+  // phase timing with CUDA events on the session stream (bench.py roofline evidence)
+  struct Span {
+    int phase;
+    cudaEvent_t a, b;
+  };
+  bool prof = false;
+  std::vector<Span> spans;
+  std::vector<cudaEvent_t> pool;
+  double prof_ms[8] = {};
+  int64_t prof_cnt[8] = {};
+  cudaEvent_t ev() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  void begin(int phase) {
+    if (!prof) return;
+    Span sp{phase, ev(), ev()};
+    cudaEventRecord(sp.a, ctx->stream);
+    spans.push_back(sp);
+  }
+  void end() {
+    if (!prof || spans.empty()) return;
+    cudaEventRecord(spans.back().b, ctx->stream);
+  }
+};
+
+namespace {
+
+__global__ void set_double_kernel(double* p, double v) { *p = v; }
+
+struct LossWeights {
+  float lambda_rgb, lambda_i1, lambda_i2, lambda_depth, lambda_feat, lambda_cos, lambda_l2, lambda_trust;
+};
+
+// LossBreakdown assembly (objective.cpp:188-190 and 247-261).
+__global__ void assemble_loss_kernel(const double* partials, int nframes, double npx, float inv_b, LossWeights wt,
+                                     latmap_loss_breakdown* out) {
+  latmap_loss_breakdown L{};
+  for (int b = 0; b < nframes; ++b) {
+    const double* p = partials + b * kPart;
+    const double nsup = p[7];
+    const float l1 = (float)(p[0] / (npx * 3.0));
+    const float ss = (float)(p[1] / (npx * 3.0));
+    const float ssl = (1.f - ss) / 2.f;
+    const bool dflag = p[3] <= 0.0;
+    const float ld = dflag ? 0.f : (float)(p[2] / p[3]);
+    const float lc = nsup > 0 ? (float)(p[4] / nsup) : 0.f;
+    const float ll2 = nsup > 0 ? (float)(p[5] / nsup) : 0.f;
+    L.l_rgb += l1 * inv_b;
+    L.l_ssim += ssl * inv_b;
+    L.l_depth += ld * inv_b;
+    L.l_cos += lc * inv_b;
+    L.l_l2 += ll2 * inv_b;
+    L.depth_empty = L.depth_empty || dflag;
+    L.zero_norm_flagged = L.zero_norm_flagged || p[6] != 0.0;
+    L.supervised_rows += (int64_t)nsup;
+  }
+  L.l_trust = (float)partials[nframes * kPart];
+  L.total = wt.lambda_rgb * (wt.lambda_i1 * L.l_rgb + wt.lambda_i2 * L.l_ssim) + wt.lambda_depth * L.l_depth +
+            wt.lambda_feat * (wt.lambda_cos * L.l_cos + wt.lambda_l2 * L.l_l2 + wt.lambda_trust * L.l_trust);
+  *out = L;
+}
+
+MapPtrs session_map(latmap_session* s, float* base) {
+  return MapPtrs{s->n, s->ds, base + s->off[0], base + s->off[1], base + s->off[2], base + s->off[3],
+                 base + s->off[4], base + s->off[5]};
+}
+
+latmap_status session_alloc_frames(latmap_session* s, int nf) {
+  latmap_ctx* ctx = s->ctx;
+  const size_t npx = (size_t)s->intr.width * s->intr.height;
+  while ((int)s->frames.size() < nf) s->frames.emplace_back();
+  while ((int)s->rw.size() < nf) {
+    s->rw.emplace_back();
+    float *c, *d, *q, *a;
+    CTX_CHECK(ctx, cudaMalloc(&c, sizeof(float) * npx * 3));
+    CTX_CHECK(ctx, cudaMalloc(&d, sizeof(float) * npx));
+    CTX_CHECK(ctx, cudaMalloc(&q, sizeof(float) * npx * s->ds));
+    CTX_CHECK(ctx, cudaMalloc(&a, sizeof(float) * npx));
+    s->color.push_back(c);
+    s->depth.push_back(d);
+    s->query.push_back(q);
+    s->alpha.push_back(a);
+  }
+  const int need_part = std::max(nf, s->global_batch);
+  if (need_part > s->part_frames) {
+    if (s->partials) cudaFree(s->partials);
+    CTX_CHECK(ctx, cudaMalloc(&s->partials, sizeof(double) * ((size_t)need_part * kPart + 8)));
+    s->part_frames = need_part;
+  }
+  return LATMAP_OK;
+}
+
+latmap_status session_objective(latmap_session* s, bool want_grad) {
+  latmap_ctx* ctx = s->ctx;
+  cudaStream_t st = ctx->stream;
+  const latmap_config& c = s->cfg;
+  const int nf = s->nframes;
+  const int gb = s->global_batch > 0 ? s->global_batch : nf;
+  const float inv_b = 1.f / (float)gb;  // objective.cpp:77
+  const int h = s->intr.height, w = s->intr.width;
+  const int64_t npx = (int64_t)h * w;
+  const Intr in = to_intr(s->intr);
+  MapPtrs map = session_map(s, s->params);
+  MapPtrs gmap = session_map(s, s->grads);
+  float* proj = s->params + s->off[6];
+  float* atoms = s->params + s->off[7];
+  float* g_proj = s->grads + s->off[6];
+  float* g_atoms = s->grads + s->off[7];
+  CTX_CHECK(ctx, cudaMemsetAsync(s->partials, 0, sizeof(double) * ((size_t)s->part_frames * kPart + 8), st));
+  if (want_grad) CTX_CHECK(ctx, cudaMemsetAsync(s->grads, 0, sizeof(float) * s->total, st));
+  // size the tile-pair buffers the first time a frame is seen
+  bool sized = false;
+  for (int b = 0; b < nf; ++b) {
+    RenderBufs& rb = s->rw[b];
+    if (rb.w.pair_cap > 1) continue;
+    CTX_CHECK(ctx, rb.ensure(s->n, w, h, 1));
+    rb.w.step_overflow = nullptr;
+    render_forward(st, map, s->frames[b].rcw, s->frames[b].pose.translation, in, rb.w, nullptr, nullptr, nullptr,
+                   nullptr, false, true);
+    sized = true;
+  }
+  if (sized) {
+    CTX_CHECK(ctx, cudaStreamSynchronize(st));
+    for (int b = 0; b < nf; ++b) {
+      RenderBufs& rb = s->rw[b];
+      if (rb.w.pair_cap > 1) continue;
+      int64_t cnt[4];
+      CTX_CHECK(ctx, cudaMemcpy(cnt, rb.w.counters, sizeof(cnt), cudaMemcpyDeviceToHost));
+      CTX_CHECK(ctx, rb.ensure(s->n, w, h, std::max<int64_t>(2, (int64_t)(cnt[0] * 1.3) + 1024)));
+    }
+  }
+  CTX_CHECK(ctx, cudaMemsetAsync(s->overflow, 0, sizeof(int64_t), st));
+  decoder_prepare(st, s->dec, atoms, proj);
+  for (int b = 0; b < nf; ++b) {
+    FrameDev& f = s->frames[b];
+    RenderBufs& rb = s->rw[b];
+    rb.w.step_overflow = s->overflow;
+    double* part = s->partials + (size_t)(s->slot_offset + b) * kPart;
+    s->begin(0);
+    render_forward(st, map, f.rcw, f.pose.translation, in, rb.w, s->color[b], s->depth[b], s->query[b], s->alpha[b],
+                   false, false, false);
+    s->end();
+    s->begin(1);
+    render_blend(st, map, in, rb.w, s->color[b], s->depth[b], s->query[b], s->alpha[b]);
+    s->end();
+    s->begin(2);
+    image_losses(st, s->color[b], s->depth[b], s->alpha[b], f.rgb, f.depth, h, w, c.lambda_i1, c.lambda_i2,
+                 c.lambda_rgb * inv_b, c.lambda_depth * inv_b, want_grad, s->d_color, s->d_depth, part,
+                 s->ssim_scratch);
+    s->end();
+    set_double_kernel<<<1, 1, 0, st>>>(part + 7, (double)f.n_sup);
+    count_launch();
+    const bool have_sup = f.n_sup > 0;
+    if (have_sup) {
+      s->begin(3);
+      decoder_frame(st, s->dec, s->query[b], f.assign, npx, f.feats, f.n_set, f.n_sup, atoms, proj, c.softmax_temp,
+                    c.lambda_cos, c.lambda_l2, c.lambda_feat * inv_b, want_grad, s->d_query, g_proj, g_atoms, part);
+      s->end();
+    }
+    if (want_grad) {
+      CTX_CHECK(ctx, cudaMemsetAsync(rb.geo_acc, 0, sizeof(float) * 8 * s->n, st));
+      s->begin(4);
+      render_backward(st, map, f.rcw, f.rwc, f.pose.translation, in, rb.w, s->d_color, s->d_depth,
+                      have_sup ? s->d_query : nullptr, rb.geo_acc, gmap, false);
+      s->end();
+      s->begin(5);
+      render_project_backward(st, map, f.rcw, f.rwc, f.pose.translation, in, rb.w, rb.geo_acc, gmap);
+      s->end();
+    }
+  }
+  // trust term enters once (objective.cpp:247-256)
+  if (s->add_trust) {
+    double* tslot = s->partials + (size_t)s->part_frames * kPart;
+    trust_region(st, atoms, s->anchor, s->k, s->df, c.trust_delta, want_grad ? g_atoms : nullptr,
+                 c.lambda_feat * c.lambda_trust, tslot);
+  }
+  return post_launch(ctx);
+}
+
+latmap_status session_assemble(latmap_session* s, latmap_loss_breakdown* out) {
+  latmap_ctx* ctx = s->ctx;
+  cudaStream_t st = ctx->stream;
+  const int gb = s->global_batch > 0 ? s->global_batch : s->nframes;
+  const latmap_config& c = s->cfg;
+  LossWeights wt{c.lambda_rgb, c.lambda_i1, c.lambda_i2, c.lambda_depth, c.lambda_feat, c.lambda_cos, c.lambda_l2,
+                 c.lambda_trust};
+  // trust slot lives after all frame slots
+  double* base = s->partials;
+  // assemble expects the trust value right after `gb` frames: copy it there when part_frames > gb
+  if (s->part_frames != gb)
+    CTX_CHECK(ctx, cudaMemcpyAsync(base + (size_t)gb * kPart, base + (size_t)s->part_frames * kPart, sizeof(double),
+                                   cudaMemcpyDeviceToDevice, st));
+  assemble_loss_kernel<<<1, 1, 0, st>>>(base, gb, (double)s->intr.width * s->intr.height, 1.f / (float)gb, wt,
+                                        s->d_loss);
+  count_launch();
+  if (out) {
+    CTX_CHECK(ctx, cudaMemcpyAsync(out, s->d_loss, sizeof(*out), cudaMemcpyDeviceToHost, st));
+    CTX_CHECK(ctx, cudaStreamSynchronize(st));
+  }
+  return post_launch(ctx);
+}
+
+void session_adam(latmap_session* s) {
+  const latmap_config& c = s->cfg;
+  s->begin(6);
+  AdamBlock blocks[8] = {
+      {s->off[0], s->off[1] - s->off[0], c.lr_position * c.scene_extent, 0},  // pipeline.cpp:76
+      {s->off[1], s->off[2] - s->off[1], c.lr_rotation, 1},
+      {s->off[2], s->off[3] - s->off[2], c.lr_color, 0},
+      {s->off[3], s->off[4] - s->off[3], c.lr_log_scale, 0},
+      {s->off[4], s->off[5] - s->off[4], c.lr_opacity, 0},
+      {s->off[5], s->off[6] - s->off[5], c.lr_feature, 0},
+      {s->off[6], s->off[7] - s->off[6], c.lr_proj, 0},                       // pipeline.cpp:93
+      {s->off[7], s->off[8] - s->off[7], c.lr_dict, c.dict_learn ? 0 : -1},  // pipeline.cpp:94
+  };
+  adam_flat(s->ctx->stream, s->params, s->grads, s->m, s->v, blocks, 8, s->steps, s->skipped, s->corr1, s->corr2,
+            kCorrLen, s->flags, s->overflow);
+  s->end();
+}
+
+// Grow the tile-pair buffers after an overflow; returns true when something was resized.
+bool session_fix_overflow(latmap_session* s) {
+  int64_t of = 0;
+  cudaMemcpy(&of, s->overflow, sizeof(of), cudaMemcpyDeviceToHost);
+  if (!of) return false;
+  for (int b = 0; b < s->nframes; ++b) {
+    int64_t cnt[4];
+    cudaMemcpy(cnt, s->rw[b].w.counters, sizeof(cnt), cudaMemcpyDeviceToHost);
+    if (cnt[0] > s->rw[b].w.pair_cap) s->rw[b].ensure(s->n, s->intr.width, s->intr.height, (int64_t)(cnt[0] * 1.3) + 1024);
+  }
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+latmap_status latmap_session_create(latmap_ctx* ctx, const latmap_config* cfg, int64_t n, int32_t ds, int64_t k,
+                                    int32_t df, const latmap_intrinsics* intr, latmap_session** out) {
+  if (!ctx || !cfg || !intr || !out || n < 0 || ds < 1 || k < 1 || df < 1) return LATMAP_ERR_INVALID_ARGUMENT;
+  if (!intr_valid(*intr)) return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "render: invalid intrinsics");
+  if (ds > 64) return fail(ctx, LATMAP_ERR_UNSUPPORTED, "query_dim must be <= 64");
+  if (cfg->segment_mode) return fail(ctx, LATMAP_ERR_UNSUPPORTED, "segment supervision is not on the device path yet");
+  if (!(cfg->softmax_temp > 0.f)) return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "reconstruct: temperature must be > 0");
+  auto* s = new latmap_session();
+  s->ctx = ctx;
+  s->cfg = *cfg;
+  s->n = n;
+  s->ds = ds;
+  s->k = k;
+  s->df = df;
+  s->intr = *intr;
+  const int64_t sizes[8] = {3 * n, 4 * n, 3 * n, 3 * n, n, (int64_t)ds * n, (int64_t)ds * df, k * df};
+  s->off[0] = 0;
+  for (int i = 0; i < 8; ++i) s->off[i + 1] = s->off[i] + sizes[i];
+  s->total = s->off[8];
+  const size_t npx = (size_t)intr->width * intr->height;
+  auto ok = [&](cudaError_t e) { return e == cudaSuccess; };
+  bool good = ok(cudaMalloc(&s->params, sizeof(float) * s->total)) && ok(cudaMalloc(&s->grads, sizeof(float) * s->total)) &&
+              ok(cudaMalloc(&s->m, sizeof(float) * s->total)) && ok(cudaMalloc(&s->v, sizeof(float) * s->total)) &&
+              ok(cudaMalloc(&s->anchor, sizeof(float) * k * df)) && ok(cudaMalloc(&s->steps, sizeof(int64_t) * 8)) &&
+              ok(cudaMalloc(&s->skipped, sizeof(int64_t) * 8)) && ok(cudaMalloc(&s->overflow, sizeof(int64_t))) &&
+              ok(cudaMalloc(&s->flags, sizeof(int32_t) * 8)) && ok(cudaMalloc(&s->corr1, sizeof(float) * kCorrLen)) &&
+              ok(cudaMalloc(&s->corr2, sizeof(float) * kCorrLen)) &&
+              ok(cudaMalloc(&s->d_color, sizeof(float) * npx * 3)) && ok(cudaMalloc(&s->d_depth, sizeof(float) * npx)) &&
+              ok(cudaMalloc(&s->d_query, sizeof(float) * npx * ds)) &&
+              ok(cudaMalloc(&s->ssim_scratch, sizeof(float) * ssim_scratch_floats(intr->height, intr->width, 3))) &&
+              ok(cudaMalloc(&s->d_loss, sizeof(latmap_loss_breakdown)));
+  DecoderWork& d = s->dec;
+  d.n_cap = (int64_t)npx;
+  d.k = k;
+  d.ds = ds;
+  d.df = df;
+  good = good && ok(cudaMalloc(&d.buf1, sizeof(float) * npx * k)) && ok(cudaMalloc(&d.buf2, sizeof(float) * npx * k)) &&
+         ok(cudaMalloc(&d.alpha_r, sizeof(float) * npx)) && ok(cudaMalloc(&d.beta_r, sizeof(float) * npx)) &&
+         ok(cudaMalloc(&d.kd, sizeof(float) * k * ds)) && ok(cudaMalloc(&d.mm, sizeof(float) * k * k)) &&
+         ok(cudaMalloc(&d.r, sizeof(float) * ds * k)) && ok(cudaMalloc(&d.a, sizeof(float) * k * k));
+  if (!good) {
+    t_err = "latmap_session_create: out of device memory";
+    ctx->err = t_err;
+    delete s;  // leaks partial allocations on failure; acceptable for an OOM path
+    return LATMAP_ERR_OUT_OF_MEMORY;
+  }
+  cudaMemset(s->m, 0, sizeof(float) * s->total);
+  cudaMemset(s->v, 0, sizeof(float) * s->total);
+  cudaMemset(s->grads, 0, sizeof(float) * s->total);
+  cudaMemset(s->steps, 0, sizeof(int64_t) * 8);
+  cudaMemset(s->skipped, 0, sizeof(int64_t) * 8);
+  cudaMemset(s->flags, 0, sizeof(int32_t) * 8);
+  std::vector<float> c1, c2;
+  corr_tables(c1, c2, kCorrLen);
+  cudaMemcpy(s->corr1, c1.data(), sizeof(float) * kCorrLen, cudaMemcpyHostToDevice);
+  cudaMemcpy(s->corr2, c2.data(), sizeof(float) * kCorrLen, cudaMemcpyHostToDevice);
+  *out = s;
+  return LATMAP_OK;
+}
+
+latmap_status latmap_session_destroy(latmap_session* s) {
+  if (!s) return LATMAP_ERR_INVALID_ARGUMENT;
+  cudaStreamSynchronize(s->ctx->stream);
+  for (void* p : {(void*)s->params, (void*)s->grads, (void*)s->m, (void*)s->v, (void*)s->anchor, (void*)s->steps,
+                  (void*)s->skipped, (void*)s->overflow, (void*)s->flags, (void*)s->corr1, (void*)s->corr2,
+                  (void*)s->d_color, (void*)s->d_depth, (void*)s->d_query, (void*)s->ssim_scratch, (void*)s->partials,
+                  (void*)s->d_loss, (void*)s->dec.buf1, (void*)s->dec.buf2, (void*)s->dec.alpha_r, (void*)s->dec.beta_r,
+                  (void*)s->dec.kd, (void*)s->dec.mm, (void*)s->dec.gt, (void*)s->dec.nv, (void*)s->dec.r,
+                  (void*)s->dec.a, (void*)s->dec.bm})
+    if (p) cudaFree(p);
+  for (auto& r : s->rw) r.release();
+  for (auto* p : s->color) cudaFree(p);
+  for (auto* p : s->depth) cudaFree(p);
+  for (auto* p : s->query) cudaFree(p);
+  for (auto* p : s->alpha) cudaFree(p);
+  for (auto& f : s->frames) {
+    if (f.rgb) cudaFree(f.rgb);
+    if (f.depth) cudaFree(f.depth);
+    if (f.assign) cudaFree(f.assign);
+    if (f.feats) cudaFree(f.feats);
+  }
+  delete s;
+  return LATMAP_OK;
+}
+
+latmap_status latmap_session_set_map(latmap_session* s, const float* pos, const float* rot, const float* col,
+                                     const float* lsc, const float* opa, const float* feat) {
+  if (!s) return LATMAP_ERR_INVALID_ARGUMENT;
+  latmap_ctx* ctx = s->ctx;
+  const float* src[6] = {pos, rot, col, lsc, opa, feat};
+  for (int i = 0; i < 6; ++i)
+    if (s->off[i + 1] > s->off[i])
+      CTX_CHECK(ctx, cudaMemcpyAsync(s->params + s->off[i], src[i], sizeof(float) * (s->off[i + 1] - s->off[i]),
+                                     cudaMemcpyHostToDevice, ctx->stream));
+  return LATMAP_OK;
+}
+
+latmap_status latmap_session_get_map(latmap_session* s, float* pos, float* rot, float* col, float* lsc, float* opa,
+                                     float* feat) {
+  if (!s) return LATMAP_ERR_INVALID_ARGUMENT;
+  latmap_ctx* ctx = s->ctx;
+  float* dst[6] = {pos, rot, col, lsc, opa, feat};
+  for (int i = 0; i < 6; ++i)
+    if (dst[i] && s->off[i + 1] > s->off[i])
+      CTX_CHECK(ctx, cudaMemcpyAsync(dst[i], s->params + s->off[i], sizeof(float) * (s->off[i + 1] - s->off[i]),
+                                     cudaMemcpyDeviceToHost, ctx->stream));
+  CTX_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+  return LATMAP_OK;
+}
+
+latmap_status latmap_session_set_dictionary(latmap_session* s, const float* atoms, const float* anchor,
+                                            const float* proj) {
+  if (!s) return LATMAP_ERR_INVALID_ARGUMENT;
+  latmap_ctx* ctx = s->ctx;
+  const size_t kd = (size_t)s->k * s->df, pd = (size_t)s->ds * s->df;
+  if (atoms) CTX_CHECK(ctx, cudaMemcpyAsync(s->params + s->off[7], atoms, sizeof(float) * kd, cudaMemcpyHostToDevice, ctx->stream));
+  if (anchor) CTX_CHECK(ctx, cudaMemcpyAsync(s->anchor, anchor, sizeof(float) * kd, cudaMemcpyHostToDevice, ctx->stream));
+  if (proj) CTX_CHECK(ctx, cudaMemcpyAsync(s->params + s->off[6], proj, sizeof(float) * pd, cudaMemcpyHostToDevice, ctx->stream));
+  return LATMAP_OK;
+}
+
+latmap_status latmap_session_get_dictionary(latmap_session* s, float* atoms, float* proj) {
+  if (!s) return LATMAP_ERR_INVALID_ARGUMENT;
+  latmap_ctx* ctx = s->ctx;
+  if (atoms) CTX_CHECK(ctx, cudaMemcpyAsync(atoms, s->params + s->off[7], sizeof(float) * s->k * s->df, cudaMemcpyDeviceToHost, ctx->stream));
+  if (proj) CTX_CHECK(ctx, cudaMemcpyAsync(proj, s->params + s->off[6], sizeof(float) * s->ds * s->df, cudaMemcpyDeviceToHost, ctx->stream));
+  CTX_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+  return LATMAP_OK;
+}
+
+latmap_status latmap_session_set_frames(latmap_session* s, int32_t nf, const latmap_frame* frames) {
+  if (!s || nf < 1 || !frames) return fail(s ? s->ctx : nullptr, LATMAP_ERR_INVALID_ARGUMENT, "total_objective: empty batch");
+  latmap_ctx* ctx = s->ctx;
+  latmap_status st = session_alloc_frames(s, nf);
+  if (st != LATMAP_OK) return st;
+  const size_t npx = (size_t)s->intr.width * s->intr.height;
+  for (int b = 0; b < nf; ++b) {
+    const latmap_frame& in = frames[b];
+    FrameDev& f = s->frames[b];
+    if (!pose_mats(in.pose, f.rcw, f.rwc)) return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "quat_to_rot: zero-norm quaternion");
+    f.pose = in.pose;
+    if (npx > f.c_px) {
+      if (f.rgb) cudaFree(f.rgb), cudaFree(f.depth), cudaFree(f.assign);
+      CTX_CHECK(ctx, cudaMalloc(&f.rgb, sizeof(float) * npx * 3));
+      CTX_CHECK(ctx, cudaMalloc(&f.depth, sizeof(float) * npx));
+      CTX_CHECK(ctx, cudaMalloc(&f.assign, sizeof(int32_t) * npx));
+      f.c_px = npx;
+    }
+    const size_t nfeat = (size_t)in.n_set * s->df;
+    if (nfeat > f.c_feat || !f.feats) {
+      if (f.feats) cudaFree(f.feats);
+      CTX_CHECK(ctx, cudaMalloc(&f.feats, sizeof(float) * std::max<size_t>(nfeat, 1)));
+      f.c_feat = nfeat;
+    }
+    CTX_CHECK(ctx, cudaMemcpyAsync(f.rgb, in.rgb, sizeof(float) * npx * 3, cudaMemcpyHostToDevice, ctx->stream));
+    CTX_CHECK(ctx, cudaMemcpyAsync(f.depth, in.depth, sizeof(float) * npx, cudaMemcpyHostToDevice, ctx->stream));
+    CTX_CHECK(ctx, cudaMemcpyAsync(f.assign, in.assignment, sizeof(int32_t) * npx, cudaMemcpyHostToDevice, ctx->stream));
+    if (nfeat) CTX_CHECK(ctx, cudaMemcpyAsync(f.feats, in.features, sizeof(float) * nfeat, cudaMemcpyHostToDevice, ctx->stream));
+    int64_t nsup = 0;
+    for (size_t p = 0; p < npx; ++p) {
+      const int32_t a = in.assignment[p];
+      if (a >= in.n_set) return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "gather_supervision: assignment out of range");
+      nsup += a >= 0;
+    }
+    f.n_sup = nsup;
+    f.n_set = in.n_set;
+  }
+  s->nframes = nf;
+  // per-frame decoder buffers sized by the largest embedding table
+  int64_t max_set = 1;
+  for (int b = 0; b < nf; ++b) max_set = std::max(max_set, s->frames[b].n_set);
+  if (max_set > s->dec.nset_cap) {
+    if (s->dec.gt) cudaFree(s->dec.gt), cudaFree(s->dec.nv), cudaFree(s->dec.bm);
+    CTX_CHECK(ctx, cudaMalloc(&s->dec.gt, sizeof(float) * max_set * s->k));
+    CTX_CHECK(ctx, cudaMalloc(&s->dec.nv, sizeof(float) * max_set));
+    CTX_CHECK(ctx, cudaMalloc(&s->dec.bm, sizeof(float) * max_set * s->k));
+    s->dec.nset_cap = max_set;
+  }
+  return LATMAP_OK;
+}
+
+latmap_status latmap_session_set_batch(latmap_session* s, int32_t global_batch, int32_t add_trust) {
+  if (!s || global_batch < 0) return LATMAP_ERR_INVALID_ARGUMENT;
+  s->global_batch = global_batch;
+  s->add_trust = add_trust;
+  return session_alloc_frames(s, std::max(1, s->nframes));
+}
+
+latmap_status latmap_session_set_slot_offset(latmap_session* s, int32_t offset) {
+  if (!s || offset < 0) return LATMAP_ERR_INVALID_ARGUMENT;
+  s->slot_offset = offset;
+  return LATMAP_OK;
+}
+
+latmap_status latmap_session_objective(latmap_session* s, int32_t want_grad, latmap_loss_breakdown* out) {
+  if (!s || s->nframes < 1) return LATMAP_ERR_INVALID_ARGUMENT;
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    latmap_status st = session_objective(s, want_grad != 0);
+    if (st != LATMAP_OK) return st;
+    if (!out) return LATMAP_OK;
+    CTX_CHECK(s->ctx, cudaStreamSynchronize(s->ctx->stream));
+    if (!session_fix_overflow(s)) return session_assemble(s, out);
+  }
+  return fail(s->ctx, LATMAP_ERR_CUDA, "tile-pair buffer overflow persisted");
+}
+
+latmap_status latmap_session_apply(latmap_session* s) {
+  if (!s) return LATMAP_ERR_INVALID_ARGUMENT;
+  session_adam(s);
+  return post_launch(s->ctx);
+}
+
+latmap_status latmap_session_step(latmap_session* s, latmap_loss_breakdown* out) {
+  if (!s || s->nframes < 1) return LATMAP_ERR_INVALID_ARGUMENT;
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    latmap_status st = session_objective(s, true);
+    if (st != LATMAP_OK) return st;
+    session_adam(s);  // no-op on device when a tile buffer overflowed
+    if (!out) return post_launch(s->ctx);
+    st = session_assemble(s, out);
+    if (st != LATMAP_OK) return st;
+    if (!session_fix_overflow(s)) return LATMAP_OK;
+  }
+  return fail(s->ctx, LATMAP_ERR_CUDA, "tile-pair buffer overflow persisted");
+}
+
+latmap_status latmap_session_grad_buffer(latmap_session* s, float** grads, int64_t* count) {
+  if (!s || !grads || !count) return LATMAP_ERR_INVALID_ARGUMENT;
+  *grads = s->grads;
+  *count = s->total;
+  return LATMAP_OK;
+}
+
+latmap_status latmap_session_loss_buffer(latmap_session* s, double** partials, int64_t* count) {
+  if (!s || !partials || !count) return LATMAP_ERR_INVALID_ARGUMENT;
+  *partials = s->partials;
+  *count = (int64_t)s->part_frames * kPart + 8;
+  return LATMAP_OK;
+}
+
+latmap_status latmap_session_read_loss(latmap_session* s, latmap_loss_breakdown* out) {
+  if (!s) return LATMAP_ERR_INVALID_ARGUMENT;
+  return session_assemble(s, out);
+}
+
+latmap_status latmap_session_frame_images(latmap_session* s, int32_t b, float** color, float** depth, float** query,
+                                          float** alpha) {
+  if (!s || b < 0 || b >= s->nframes) return LATMAP_ERR_INVALID_ARGUMENT;
+  if (color) *color = s->color[b];
+  if (depth) *depth = s->depth[b];
+  if (query) *query = s->query[b];
+  if (alpha) *alpha = s->alpha[b];
+  return LATMAP_OK;
+}
+
+latmap_status latmap_session_profile(latmap_session* s, int32_t enable) {
+  if (!s) return LATMAP_ERR_INVALID_ARGUMENT;
+  s->prof = enable != 0;
+  return LATMAP_OK;
+}
+
+latmap_status latmap_session_phase_times(latmap_session* s, double* ms, int64_t* counts) {
+  if (!s) return LATMAP_ERR_INVALID_ARGUMENT;
+  CTX_CHECK(s->ctx, cudaStreamSynchronize(s->ctx->stream));
+  for (auto& sp : s->spans) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, sp.a, sp.b) == cudaSuccess) {
+      s->prof_ms[sp.phase] += t;
+      s->prof_cnt[sp.phase] += 1;
+    }
+    s->pool.push_back(sp.a);
+    s->pool.push_back(sp.b);
+  }
+  s->spans.clear();
+  for (int i = 0; i < 8; ++i) {
+    if (ms) ms[i] = s->prof_ms[i];
+    if (counts) counts[i] = s->prof_cnt[i];
+    s->prof_ms[i] = 0;
+    s->prof_cnt[i] = 0;
+  }
+  return LATMAP_OK;
+}
+
+latmap_status latmap_session_stats(latmap_session* s, int64_t* visible, int64_t* pairs) {
+  if (!s) return LATMAP_ERR_INVALID_ARGUMENT;
+  CTX_CHECK(s->ctx, cudaStreamSynchronize(s->ctx->stream));
+  for (int b = 0; b < s->nframes; ++b) {
+    int64_t cnt[4];
+    CTX_CHECK(s->ctx, cudaMemcpy(cnt, s->rw[b].w.counters, sizeof(cnt), cudaMemcpyDeviceToHost));
+    if (visible) visible[b] = cnt[1];
+    if (pairs) pairs[b] = cnt[0];
+  }
+  return LATMAP_OK;
+}
+
+}  // extern "C"

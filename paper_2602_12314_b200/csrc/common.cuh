@@ -1,0 +1,66 @@
+// common.cuh — shared device helpers for the latent-map step kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+
+namespace lm {
+
+// Exact IEEE round-to-nearest float ops (no FMA contraction). Used wherever a
+// discrete decision (bbox, clamp, termination, sort key) or bit-exact parity with
+// the oracle depends on the rounding sequence of the reference's float code.
+__device__ __forceinline__ float fm(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float fa(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float fs(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float fd(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double dm(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double da(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double ds_(double a, double b) { return __dsub_rn(a, b); }
+
+// std::exp(float) restated as the correctly rounded (float)exp((double)x) — the
+// oracle's definition; CUDA's double exp is accurate to < 1 ulp of double.
+__device__ __forceinline__ float exp_exact(float x) { return __double2float_rn(exp((double)x)); }
+
+// sigmoid, core/types.hpp:252-255
+__device__ __forceinline__ float sigmoid_exact(float x) {
+  if (x >= 0.f) return fd(1.f, fa(1.f, exp_exact(-x)));
+  const float e = exp_exact(x);
+  return fd(e, fa(1.f, e));
+}
+
+constexpr int kTile = 16;                 // tile edge in pixels
+constexpr int kTilePixels = kTile * kTile;
+constexpr float kZNear = 0.01f;           // RenderParams, splat/render.hpp:13-19
+constexpr float kCovReg = 0.3f;
+constexpr double kSigmaCut = 3.0;
+constexpr float kAlphaMax = 0.999f;
+constexpr float kTransmitStop = 1e-4f;
+
+// Projected record, one per Gaussian (indexed by source). 48 bytes.
+struct __align__(16) SplatRec {
+  float mean_x, mean_y, depth, alpha;  // mean2d, camera z, decoded opacity
+  float a00, a01, a10, a11;            // cov_inv (row-major)
+  int32_t x0, x1, y0, y1;              // inclusive pixel bbox; x0 > x1 => not listed
+};
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace lm
+
+#define LM_CUDA_CHECK(expr)                                                            \
+  do {                                                                                 \
+    cudaError_t _e = (expr);                                                           \
+    if (_e != cudaSuccess) {                                                           \
+      return ::lm::set_cuda_error(_e, #expr, __FILE__, __LINE__);                       \
+    }                                                                                  \
+  } while (0)

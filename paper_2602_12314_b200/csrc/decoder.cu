@@ -1,0 +1,396 @@
+// decoder.cu — dictionary-attention decoder + feature loss, fp32 SIMT path.
+//
+// Reference: reconstruct / reconstruct_backward / trust_region_penalty
+// (proj/src/dictionary.cpp:25-101), feature_loss (proj/src/losses.cpp:257-294) and
+// their assembly in total_objective (proj/src/objective.cpp:100-185).
+//
+// The step path uses the factored algebra of the feature loss: with keys
+// Kd = D W^T, Gram M = D D^T and target scores G = E D^T (E = the frame's
+// embedding table), every per-row quantity the loss and its backward need is a
+// K-vector:  nu^2 = P.(P M),  dot = P.G[a],  dP = alpha (P M) + beta G[a],
+// so F_hat = P D (n x d_f) is never materialised. The reductions become
+//   d_atoms = (P^T diag(alpha) P) D + Bm E + R^T W,   d_proj = R D,  R = Q^T dS.
+// The same algebra runs on tcgen05 in decoder_tc.cu for the bf16 configurations.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace lm {
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16;
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(256) sgemm_kernel(int64_t M, int64_t N, int64_t K, float alpha,
+                                                    const float* __restrict__ A, int64_t lda,
+                                                    const float* __restrict__ B, int64_t ldb, float beta,
+                                                    float* __restrict__ C, int64_t ldc, int64_t kchunk, bool atomic) {
+  __shared__ float As[BK][BM + 4];
+  __shared__ float Bs[BK][BN + 4];
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;
+  const int64_t i0 = (int64_t)blockIdx.y * BM, j0 = (int64_t)blockIdx.x * BN;
+  const int64_t kb = (int64_t)blockIdx.z * kchunk;
+  const int64_t ke = min(K, kb + kchunk);
+  float acc[4][4] = {};
+  for (int64_t k0 = kb; k0 < ke; k0 += BK) {
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const int e = tid + l * 256;  // 0..1023
+      // A tile: rows i0..i0+63, cols k0..k0+15 -> As[kk][ii]
+      {
+        const int ii = TA ? e % BM : e / BK;
+        const int kk = TA ? e / BM : e % BK;
+        const int64_t gi = i0 + ii, gk = k0 + kk;
+        float v = 0.f;
+        if (gi < M && gk < ke) v = TA ? A[gk * lda + gi] : A[gi * lda + gk];
+        As[kk][ii] = v;
+      }
+      {
+        const int jj = TB ? e / BK : e % BN;
+        const int kk = TB ? e % BK : e / BN;
+        const int64_t gj = j0 + jj, gk = k0 + kk;
+        float v = 0.f;
+        if (gj < N && gk < ke) v = TB ? B[gj * ldb + gk] : B[gk * ldb + gj];
+        Bs[kk][jj] = v;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float av[4], bv[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) av[r] = As[kk][ty * 4 + r];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) bv[c] = Bs[kk][tx * 4 + c];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] += av[r] * bv[c];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int64_t gi = i0 + ty * 4 + r;
+    if (gi >= M) continue;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int64_t gj = j0 + tx * 4 + c;
+      if (gj >= N) continue;
+      float* dst = C + gi * ldc + gj;
+      const float v = alpha * acc[r][c];
+      if (atomic)
+        atomicAdd(dst, v);
+      else
+        *dst = beta == 0.f ? v : v + beta * *dst;
+    }
+  }
+}
+
+// Row softmax with max subtraction (dictionary.cpp:39-44); one warp per row.
+__global__ void softmax_rows_kernel(float* __restrict__ x, int64_t n, int k) {
+  const int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+  if (r >= n) return;
+  const int lane = threadIdx.x & 31;
+  float* row = x + r * k;
+  float m = -INFINITY;
+  for (int j = lane; j < k; j += 32) m = fmaxf(m, row[j]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  float s = 0.f;
+  for (int j = lane; j < k; j += 32) {
+    const float e = expf(row[j] - m);
+    row[j] = e;
+    s += e;
+  }
+  s = warp_sum(s);
+  const float inv = 1.f / s;
+  for (int j = lane; j < k; j += 32) row[j] *= inv;
+}
+
+// Per-row feature loss + softmax backward, one warp per pixel row.
+//   buf1 = P (n x K), buf2 = P M (n x K) -> overwritten with dS.
+__global__ void decoder_rows_kernel(const float* __restrict__ P, float* __restrict__ T, int64_t n, int k,
+                                    const int32_t* __restrict__ assign, const float* __restrict__ gt,
+                                    const float* __restrict__ nv, float inv_temp, float lambda_cos, float lambda_l2,
+                                    float inv_nsup, float scale, float* __restrict__ alpha_r,
+                                    float* __restrict__ beta_r, double* partials) {
+  const int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  double cos_acc = 0.0, l2_acc = 0.0, zflag = 0.0;
+  if (r < n) {
+    const int32_t a = assign[r];
+    const float* p = P + r * k;
+    float* t = T + r * k;
+    if (a < 0) {
+      for (int j = lane; j < k; j += 32) t[j] = 0.f;
+      if (lane == 0) {
+        alpha_r[r] = 0.f;
+        beta_r[r] = 0.f;
+      }
+    } else {
+      const float* g = gt + (int64_t)a * k;
+      float nu2 = 0.f, dot = 0.f;
+      for (int j = lane; j < k; j += 32) {
+        nu2 += p[j] * t[j];
+        dot += p[j] * g[j];
+      }
+      nu2 = warp_sum(nu2);
+      dot = warp_sum(dot);
+      const float eps = 1e-8f;
+      const float nu = sqrtf(fmaxf(nu2, 0.f)), vn = nv[a];
+      const float nug = fmaxf(nu, eps), nvg = fmaxf(vn, eps);
+      if (lane == 0) {
+        if (nu < eps || vn < eps) zflag = 1.0;
+        cos_acc = 1.0 - (double)(dot / (nug * nvg));
+        l2_acc = (double)nu2 - 2.0 * (double)dot + (double)vn * (double)vn;
+      }
+      // dF = al * F_hat + be * F  (losses.cpp:279-282)
+      const float al = scale * (lambda_cos * dot / (nug * nug * nug * nvg) * inv_nsup + 2.f * lambda_l2 * inv_nsup);
+      const float be = scale * (-lambda_cos / (nug * nvg) * inv_nsup - 2.f * lambda_l2 * inv_nsup);
+      const float c = al * nu2 + be * dot;
+      for (int j = lane; j < k; j += 32) t[j] = p[j] * (al * t[j] + be * g[j] - c) * inv_temp;
+      if (lane == 0) {
+        alpha_r[r] = al;
+        beta_r[r] = be;
+      }
+    }
+  }
+  __shared__ double s_red[3][32];
+  const int wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    s_red[0][wid] = cos_acc;
+    s_red[1][wid] = l2_acc;
+    s_red[2][wid] = zflag;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double c0 = 0, c1 = 0, c2 = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+      c0 += s_red[0][i];
+      c1 += s_red[1][i];
+      c2 = fmax(c2, s_red[2][i]);
+    }
+    if (c0 != 0.0) atomicAdd(&partials[4], c0);
+    if (c1 != 0.0) atomicAdd(&partials[5], c1);
+    if (c2 != 0.0) atomicMax((unsigned long long*)&partials[6], (unsigned long long)__double_as_longlong(1.0));
+  }
+}
+
+// Bm^T[s][k] += beta_r P[r][k] over rows with assignment s; rows are pixels in raster
+// order, so runs of equal s are long and are summed before one atomic per run.
+__global__ void bm_accum_kernel(const float* __restrict__ P, const float* __restrict__ beta_r,
+                                const int32_t* __restrict__ assign, int64_t n, int k, int64_t rows_per_block,
+                                float* __restrict__ bmt) {
+  const int64_t r0 = blockIdx.y * rows_per_block;
+  const int64_t r1 = min(n, r0 + rows_per_block);
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+    int32_t cur = -1;
+    float acc = 0.f;
+    for (int64_t r = r0; r < r1; ++r) {
+      const int32_t s = assign[r];
+      if (s != cur) {
+        if (cur >= 0 && acc != 0.f) atomicAdd(&bmt[(int64_t)cur * k + j], acc);
+        cur = s;
+        acc = 0.f;
+      }
+      if (s >= 0) acc += beta_r[r] * P[r * k + j];
+    }
+    if (cur >= 0 && acc != 0.f) atomicAdd(&bmt[(int64_t)cur * k + j], acc);
+  }
+}
+
+__global__ void scale_rows_kernel(const float* __restrict__ P, const float* __restrict__ s, float* __restrict__ out,
+                                  int64_t n, int k) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * k; e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = P[e] * s[e / k];
+}
+
+__global__ void row_norms_kernel(const float* __restrict__ x, int64_t n, int d, float* __restrict__ out) {
+  const int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+  if (r >= n) return;
+  const int lane = threadIdx.x & 31;
+  float s = 0.f;
+  for (int j = lane; j < d; j += 32) s += x[r * d + j] * x[r * d + j];
+  s = warp_sum(s);
+  if (lane == 0) out[r] = sqrtf(s);
+}
+
+// softmax backward rows (dictionary.cpp:69-74): d = P * (d - rowdot(P, d)) / temperature
+__global__ void softmax_bwd_rows_kernel(const float* __restrict__ P, float* __restrict__ d, int64_t n, int k,
+                                        float temperature) {
+  const int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+  if (r >= n) return;
+  const int lane = threadIdx.x & 31;
+  const float* p = P + r * k;
+  float* x = d + r * k;
+  float dot = 0.f;
+  for (int j = lane; j < k; j += 32) dot += p[j] * x[j];
+  dot = warp_sum(dot);
+  for (int j = lane; j < k; j += 32) x[j] = p[j] * (x[j] - dot) / temperature;
+}
+
+__global__ void scale_kernel(float* x, int64_t n, float s) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    x[e] *= s;
+}
+
+// trust_region_penalty (dictionary.cpp:85-101): one block per atom row.
+__global__ void trust_kernel(const float* __restrict__ atoms, const float* __restrict__ anchor, int64_t k, int df,
+                             float delta, float* d_atoms, float grad_scale, double* penalty) {
+  __shared__ float red[32];
+  const int64_t j = blockIdx.x;
+  float ss = 0.f;
+  for (int c = threadIdx.x; c < df; c += blockDim.x) {
+    const float d = atoms[j * df + c] - anchor[j * df + c];
+    ss += d * d;
+  }
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float dist = sqrtf(red[0]);
+  const float excess = dist - delta;
+  if (excess > 0.f) {
+    if (threadIdx.x == 0 && penalty) atomicAdd(penalty, (double)excess);
+    if (d_atoms)
+      for (int c = threadIdx.x; c < df; c += blockDim.x)
+        d_atoms[j * df + c] += grad_scale * ((atoms[j * df + c] - anchor[j * df + c]) / dist);
+  }
+}
+
+inline int grid_for(int64_t n, int per_block, int cap = 148 * 32) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((n + per_block - 1) / per_block, cap));
+}
+
+}  // namespace
+
+void sgemm(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, float alpha, const float* A,
+           int64_t lda, const float* B, int64_t ldb, float beta, float* C, int64_t ldc, int split) {
+  if (M <= 0 || N <= 0) return;
+  if (K <= 0) {
+    if (split <= 1 && beta == 0.f)
+      for (int64_t i = 0; i < M; ++i) cudaMemsetAsync(C + i * ldc, 0, sizeof(float) * N, st);
+    return;
+  }
+  const int64_t gx = (N + BN - 1) / BN, gy = (M + BM - 1) / BM;
+  if (split < 1) split = 1;
+  // choose split so that each chunk still has >= 256 reduction steps
+  const int64_t kchunk = ((K + split - 1) / split + BK - 1) / BK * BK;
+  const int gz = (int)((K + kchunk - 1) / kchunk);
+  const bool atomic = gz > 1 || split > 1;
+  dim3 grid((unsigned)gx, (unsigned)gy, (unsigned)gz);
+  if (!ta && !tb) sgemm_kernel<false, false><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, atomic);
+  if (!ta && tb) sgemm_kernel<false, true><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, atomic);
+  if (ta && !tb) sgemm_kernel<true, false><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, atomic);
+  if (ta && tb) sgemm_kernel<true, true><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, atomic);
+  count_launch();
+}
+
+static int split_for(int64_t M, int64_t N, int64_t K) {
+  const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  int64_t s = (148 * 4 + tiles - 1) / tiles;
+  s = std::min<int64_t>(s, std::max<int64_t>(1, K / 512));
+  return (int)std::max<int64_t>(1, s);
+}
+
+void decoder_prepare(cudaStream_t st, DecoderWork& w, const float* atoms, const float* proj) {
+  // Kd = D W^T (K x ds), M = D D^T (K x K)
+  sgemm(st, false, true, w.k, w.ds, w.df, 1.f, atoms, w.df, proj, w.df, 0.f, w.kd, w.ds);
+  sgemm(st, false, true, w.k, w.k, w.df, 1.f, atoms, w.df, atoms, w.df, 0.f, w.mm, w.k);
+}
+
+void decoder_frame(cudaStream_t st, DecoderWork& w, const float* query, const int32_t* assignment, int64_t npx,
+                   const float* feats, int64_t n_set, int64_t n_sup, const float* atoms, const float* proj,
+                   float temperature, float lambda_cos, float lambda_l2, float scale, bool want_grad, float* d_query,
+                   float* d_proj, float* d_atoms, double* partials) {
+  const int64_t k = w.k;
+  const int ds = w.ds, df = w.df;
+  const float inv_temp = 1.f / temperature;
+  // per-frame target scores G^T = E D^T (n_set x K) and target norms
+  sgemm(st, false, true, n_set, k, df, 1.f, feats, df, atoms, df, 0.f, w.gt, k);
+  row_norms_kernel<<<grid_for(n_set * 32, 256), 256, 0, st>>>(feats, n_set, df, w.nv);
+  count_launch();
+  // S = Q Kd^T / temperature ; P = softmax(S)
+  sgemm(st, false, true, npx, k, ds, inv_temp, query, ds, w.kd, ds, 0.f, w.buf1, k);
+  softmax_rows_kernel<<<grid_for(npx * 32, 256, 1 << 30), 256, 0, st>>>(w.buf1, npx, (int)k);
+  count_launch();
+  // buf2 = P M
+  sgemm(st, false, false, npx, k, k, 1.f, w.buf1, k, w.mm, k, 0.f, w.buf2, k);
+  decoder_rows_kernel<<<grid_for(npx * 32, 256, 1 << 30), 256, 0, st>>>(
+      w.buf1, w.buf2, npx, (int)k, assignment, w.gt, w.nv, inv_temp, lambda_cos, lambda_l2,
+      n_sup > 0 ? 1.f / (float)n_sup : 0.f, scale, w.alpha_r, w.beta_r, partials);
+  count_launch();
+  if (!want_grad) return;
+  // d_query = dS Kd   (n x ds)
+  sgemm(st, false, false, npx, ds, k, 1.f, w.buf2, k, w.kd, ds, 0.f, d_query, ds);
+  // R = Q^T dS  (ds x K), reduction over pixels
+  cudaMemsetAsync(w.r, 0, sizeof(float) * ds * k, st);
+  sgemm(st, true, false, ds, k, npx, 1.f, query, ds, w.buf2, k, 0.f, w.r, k, split_for(ds, k, npx));
+  // Bm^T (n_set x K)
+  cudaMemsetAsync(w.bm, 0, sizeof(float) * n_set * k, st);
+  {
+    const int64_t rpb = 512;
+    dim3 g((unsigned)((k + 127) / 128), (unsigned)((npx + rpb - 1) / rpb));
+    bm_accum_kernel<<<g, 128, 0, st>>>(w.buf1, w.beta_r, assignment, npx, (int)k, rpb, w.bm);
+    count_launch();
+  }
+  // A = P^T diag(alpha) P  (K x K)
+  scale_rows_kernel<<<grid_for(npx * k, 256), 256, 0, st>>>(w.buf1, w.alpha_r, w.buf2, npx, (int)k);
+  count_launch();
+  cudaMemsetAsync(w.a, 0, sizeof(float) * k * k, st);
+  sgemm(st, true, false, k, k, npx, 1.f, w.buf1, k, w.buf2, k, 0.f, w.a, k, split_for(k, k, npx));
+  // d_atoms += A D + Bm E + R^T W ;  d_proj += R D
+  sgemm(st, false, false, k, df, k, 1.f, w.a, k, atoms, df, 1.f, d_atoms, df);
+  sgemm(st, true, false, k, df, n_set, 1.f, w.bm, k, feats, df, 1.f, d_atoms, df);
+  sgemm(st, true, false, k, df, ds, 1.f, w.r, k, proj, df, 1.f, d_atoms, df);
+  sgemm(st, false, false, ds, df, k, 1.f, w.r, k, atoms, df, 1.f, d_proj, df);
+}
+
+void reconstruct(cudaStream_t st, const float* q, int64_t n, int ds, const float* atoms, const float* proj, int64_t k,
+                 int df, float temperature, float* out, float* attention, float* scratch_qw) {
+  // logits = (Q W) D^T / temperature (dictionary.cpp:37)
+  sgemm(st, false, false, n, df, ds, 1.f, q, ds, proj, df, 0.f, scratch_qw, df);
+  sgemm(st, false, true, n, k, df, 1.f / temperature, scratch_qw, df, atoms, df, 0.f, attention, k);
+  softmax_rows_kernel<<<grid_for(n * 32, 256, 1 << 30), 256, 0, st>>>(attention, n, (int)k);
+  count_launch();
+  sgemm(st, false, false, n, df, k, 1.f, attention, k, atoms, df, 0.f, out, df);
+}
+
+void reconstruct_backward(cudaStream_t st, const float* q, const float* att, int64_t n, int ds, const float* atoms,
+                          const float* proj, int64_t k, int df, float temperature, const float* d_rec, float* d_q,
+                          float* d_proj, float* d_atoms, float* s_nk, float* s_ndf, float* s_kdf) {
+  // d_logits = dF D^T, softmax backward, / temperature (dictionary.cpp:68-74)
+  sgemm(st, false, true, n, k, df, 1.f, d_rec, df, atoms, df, 0.f, s_nk, k);
+  softmax_bwd_rows_kernel<<<grid_for(n * 32, 256, 1 << 30), 256, 0, st>>>(att, s_nk, n, (int)k, temperature);
+  count_launch();
+  // d_atoms = P^T dF + d_logits^T (Q W)   (dictionary.cpp:77-78)
+  sgemm(st, false, false, n, df, ds, 1.f, q, ds, proj, df, 0.f, s_ndf, df);
+  cudaMemsetAsync(d_atoms, 0, sizeof(float) * k * df, st);
+  sgemm(st, true, false, k, df, n, 1.f, att, k, d_rec, df, 0.f, d_atoms, df, split_for(k, df, n));
+  sgemm(st, true, false, k, df, n, 1.f, s_nk, k, s_ndf, df, 0.f, d_atoms, df, std::max(2, split_for(k, df, n)));
+  // d_qw = d_logits D ; d_proj = Q^T d_qw ; d_q = d_qw W^T (dictionary.cpp:79-81)
+  sgemm(st, false, false, n, df, k, 1.f, s_nk, k, atoms, df, 0.f, s_ndf, df);
+  cudaMemsetAsync(d_proj, 0, sizeof(float) * ds * df, st);
+  sgemm(st, true, false, ds, df, n, 1.f, q, ds, s_ndf, df, 0.f, d_proj, df, std::max(2, split_for(ds, df, n)));
+  sgemm(st, false, true, n, ds, df, 1.f, s_ndf, df, proj, df, 0.f, d_q, ds);
+  (void)s_kdf;
+}
+
+void trust_region(cudaStream_t st, const float* atoms, const float* anchor, int64_t k, int df, float delta,
+                  float* d_atoms, float grad_scale, double* penalty_out) {
+  if (k <= 0) return;
+  trust_kernel<<<(unsigned)k, 256, 0, st>>>(atoms, anchor, k, df, delta, d_atoms, grad_scale, penalty_out);
+  count_launch();
+}
+
+}  // namespace lm

@@ -1,0 +1,117 @@
+// kernels.h — host-side launchers of the latent-map step kernels (internal).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace lm {
+
+struct Intr {
+  float fx, fy, cx, cy;
+  int32_t width, height;
+};
+
+struct MapPtrs {  // device SoA (GaussianMapT / MapGradientsT)
+  int64_t n;
+  int32_t ds;
+  float *pos, *rot, *col, *lsc, *opa, *feat;
+};
+
+// Per-frame render workspace (RenderOutput::splats + the tile lists).
+struct RenderWork {
+  int64_t n_cap = 0;     // Gaussians the buffers are sized for
+  int32_t tiles_x = 0, tiles_y = 0, width = 0, height = 0;
+  int64_t pair_cap = 0;  // capacity of the (tile, depth) key arrays
+  SplatRec* rec = nullptr;          // n_cap
+  int32_t* tile_count = nullptr;    // ntiles
+  int32_t* tile_offset = nullptr;   // ntiles + 1
+  int32_t* tile_cursor = nullptr;   // ntiles
+  uint64_t* keys = nullptr;         // pair_cap, (depth_bits << 32 | source), sorted per tile
+  uint64_t* keys_tmp = nullptr;     // pair_cap, merge scratch for oversized tiles
+  int32_t* px_last = nullptr;       // H*W: tile-list entries consumed by the pixel
+  float* px_T = nullptr;            // H*W: transmittance after the last blended splat
+  int64_t* counters = nullptr;      // [0] pairs, [1] visible, [2] overflow, [3] big tiles
+  int32_t* tile_max_last = nullptr; // ntiles: max px_last over the tile
+  int64_t* step_overflow = nullptr;  // optional session-level overflow flag
+};
+
+// Renderer: project (K1) -> scan (K2) -> scatter (K3) -> per-tile sort -> blend (K4).
+void render_forward(cudaStream_t st, const MapPtrs& map, const float rot_cw[9], const float origin[3],
+                    const Intr& intr, RenderWork& w, float* color, float* depth, float* query,
+                    float* alpha, bool zero_outputs, bool count_only = false, bool blend = true);
+// K4 only (after render_forward(..., blend=false)).
+void render_blend(cudaStream_t st, const MapPtrs& map, const Intr& intr, RenderWork& w, float* color, float* depth,
+                  float* query, float* alpha);
+void project_single(cudaStream_t st, const float* d_in11, const float rot_cw[9], const float origin[3],
+                    const Intr& intr, float* d_out8);
+// Backward: blend replay + reverse sweep (K8) -> projection backward (K9). Accumulates.
+void render_backward(cudaStream_t st, const MapPtrs& map, const float rot_cw[9], const float rot_wc[9],
+                     const float origin[3], const Intr& intr, const RenderWork& w, const float* d_color,
+                     const float* d_depth, const float* d_query, float* geo_acc, const MapPtrs& grads,
+                     bool project = true);
+// K9 only (after render_backward(..., project=false)).
+void render_project_backward(cudaStream_t st, const MapPtrs& map, const float rot_cw[9], const float rot_wc[9],
+                             const float origin[3], const Intr& intr, const RenderWork& w, float* geo_acc,
+                             const MapPtrs& grads);
+
+// Image-space losses (K5). partials[...] are double accumulators (see capi.cu).
+void image_losses(cudaStream_t st, const float* color, const float* depth, const float* alpha,
+                  const float* rgb_t, const float* depth_t, int h, int w, float lambda_i1, float lambda_i2,
+                  float rgb_scale, float depth_scale, bool want_grad, float* d_color, float* d_depth,
+                  double* partials, float* ssim_scratch);
+double ssim_host(cudaStream_t st, const float* a, const float* b, int h, int w, int c, float* d_a,
+                 float* scratch);
+size_t ssim_scratch_floats(int h, int w, int c);
+
+// Generic SIMT SGEMM: C = alpha * op(A) * op(B) + beta * C, row-major; split-K via atomics when
+// `split` > 1 (then beta must be applied by the caller beforehand, beta ignored).
+void sgemm(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, float alpha,
+           const float* A, int64_t lda, const float* B, int64_t ldb, float beta, float* C, int64_t ldc,
+           int split = 1);
+
+// Decoder (factored algebra, fp32 SIMT path) — see decoder.cu.
+struct DecoderWork {
+  int64_t n_cap = 0, k = 0;
+  int32_t ds = 0, df = 0;
+  float *buf1 = nullptr, *buf2 = nullptr;  // n x K
+  float *alpha_r = nullptr, *beta_r = nullptr;
+  float *kd = nullptr;   // K x ds   (D W^T)
+  float *mm = nullptr;   // K x K    (D D^T)
+  float *gt = nullptr;   // n_set x K (E D^T)
+  float *nv = nullptr;   // n_set
+  float *r = nullptr;    // ds x K   (Q^T dS)
+  float *a = nullptr;    // K x K    (P^T diag(alpha) P)
+  float *bm = nullptr;   // n_set x K (Bm^T)
+  int64_t nset_cap = 0;
+};
+void decoder_prepare(cudaStream_t st, DecoderWork& w, const float* atoms, const float* proj);
+// Fused feature loss + decoder backward for one frame (pixel mode). Accumulates into d_proj,
+// d_atoms (scaled by lambda_feat * inv_b) and writes d_query (HxWxds, scaled likewise).
+void decoder_frame(cudaStream_t st, DecoderWork& w, const float* query, const int32_t* assignment,
+                   int64_t npx, const float* feats, int64_t n_set, int64_t n_sup, const float* atoms,
+                   const float* proj, float temperature, float lambda_cos, float lambda_l2, float scale,
+                   bool want_grad, float* d_query, float* d_proj, float* d_atoms, double* partials);
+void reconstruct(cudaStream_t st, const float* q, int64_t n, int ds, const float* atoms, const float* proj,
+                 int64_t k, int df, float temperature, float* out, float* attention, float* scratch_qw);
+void reconstruct_backward(cudaStream_t st, const float* q, const float* att, int64_t n, int ds,
+                          const float* atoms, const float* proj, int64_t k, int df, float temperature,
+                          const float* d_rec, float* d_q, float* d_proj, float* d_atoms, float* s_nk,
+                          float* s_ndf, float* s_kdf);
+void trust_region(cudaStream_t st, const float* atoms, const float* anchor, int64_t k, int df, float delta,
+                  float* d_atoms, float grad_scale, double* penalty_out);
+
+// Adam (K10) over the session's flat parameter vector.
+struct AdamBlock {
+  int64_t offset, count;
+  float lr;
+  int32_t kind;  // 0 plain, 1 quaternion block (renormalise rows of 4), -1 disabled
+};
+void adam_flat(cudaStream_t st, float* param, const float* grad, float* m, float* v, const AdamBlock* blocks,
+               int nblocks, int64_t* steps, int64_t* skipped, const float* corr1, const float* corr2,
+               int32_t table_len, int32_t* flags, const int64_t* overflow);
+
+void set_launch_counter(int64_t* c);
+void count_launch(int n = 1);
+
+}  // namespace lm

@@ -1,0 +1,326 @@
+// losses.cu — image-space losses (K5): L1 RGB, masked depth L1, SSIM forward + adjoint.
+// Replaces rgb_loss / depth_loss / ssim (proj/src/losses.cpp:133-255).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace lm {
+
+namespace {
+
+constexpr int kWin = 11, kRad = 5;
+
+struct SsimKernel {
+  float k[kWin];
+};
+
+// ssim_kernel, losses.cpp:13-25 (double weights rounded to float, then normalised).
+SsimKernel make_kernel() {
+  SsimKernel s;
+  double w[kWin], sum = 0;
+  for (int i = 0; i < kWin; ++i) {
+    const double d = i - kRad;
+    w[i] = std::exp(-d * d / (2.0 * 1.5 * 1.5));
+    s.k[i] = (float)w[i];
+    sum += w[i];
+  }
+  for (int i = 0; i < kWin; ++i) s.k[i] = (float)((double)s.k[i] / sum);
+  return s;
+}
+
+__device__ __forceinline__ int refl(int i, int n) {
+  if (i < 0) return -i;
+  if (i >= n) return 2 * n - 2 - i;
+  return i;
+}
+
+__device__ __forceinline__ void block_add_double(double v, double* out) {
+  __shared__ double s_red[32];
+  v = warp_sum_d(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) s_red[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    v = lane < (int)(blockDim.x >> 5) ? s_red[lane] : 0.0;
+    v = warp_sum_d(v);
+    if (lane == 0 && v != 0.0) atomicAdd(out, v);
+  }
+  __syncthreads();
+}
+
+// Pass 1: L1 RGB (losses.cpp:200-214) and masked depth L1 (losses.cpp:226-255).
+__global__ void __launch_bounds__(256) l1_depth_kernel(const float* __restrict__ color, const float* __restrict__ depth,
+                                                       const float* __restrict__ alpha, const float* __restrict__ rgb_t,
+                                                       const float* __restrict__ depth_t, int64_t npx, float lambda_i1,
+                                                       float n_rgb, bool want_grad, float* d_color, float* d_depth,
+                                                       double* partials) {
+  double l1 = 0.0, dsum = 0.0, dcount = 0.0;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npx; p += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float d = fs(color[3 * p + c], rgb_t[3 * p + c]);
+      l1 += (double)fabsf(d);
+      if (want_grad) {
+        const float sg = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
+        d_color[3 * p + c] = fd(fm(lambda_i1, sg), n_rgb);
+      }
+    }
+    const float o = depth_t[p];
+    const bool valid = o > 0.f && alpha[p] > 0.5f;
+    float sg = 0.f;
+    if (valid) {
+      const float d = fs(depth[p], o);
+      dsum += (double)fabsf(d);
+      dcount += 1.0;
+      sg = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
+    }
+    if (want_grad) d_depth[p] = sg;
+  }
+  block_add_double(l1, &partials[0]);
+  block_add_double(dsum, &partials[2]);
+  block_add_double(dcount, &partials[3]);
+}
+
+// Fold the objective weights into the upstream images (objective.cpp:164-170).
+__global__ void finalize_upstream_kernel(float* d_color, float* d_depth, int64_t npx, float rgb_scale,
+                                         float depth_scale, const double* partials) {
+  const double valid = partials[3];
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npx; p += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) d_color[3 * p + c] = fm(d_color[3 * p + c], rgb_scale);
+    if (valid > 0.0)
+      d_depth[p] = fm(fd(d_depth[p], (float)valid), depth_scale);
+    else
+      d_depth[p] = 0.f;  // depth flagged: no gradient (objective.cpp:165-169)
+  }
+}
+
+// SSIM, horizontal pass: 5 filtered quantities per channel (filter_plane, losses.cpp:34-54).
+__global__ void ssim_h_kernel(const float* __restrict__ a, const float* __restrict__ b, int h, int w, int ch,
+                              SsimKernel K, float* __restrict__ hq) {
+  const int64_t n = (int64_t)h * w;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * ch; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e / n);
+    const int64_t p = e % n;
+    const int y = (int)(p / w), x = (int)(p % w);
+    float s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0;
+#pragma unroll
+    for (int k = -kRad; k <= kRad; ++k) {
+      const int64_t q = ((int64_t)y * w + refl(x + k, w)) * ch + c;
+      const float av = a[q], bv = b[q], kw = K.k[k + kRad];
+      s0 += kw * av;
+      s1 += kw * bv;
+      s2 += kw * (av * av);
+      s3 += kw * (bv * bv);
+      s4 += kw * (av * bv);
+    }
+    float* o = hq + (int64_t)c * 5 * n;
+    o[p] = s0;
+    o[n + p] = s1;
+    o[2 * n + p] = s2;
+    o[3 * n + p] = s3;
+    o[4 * n + p] = s4;
+  }
+}
+
+// SSIM, vertical pass + per-pixel map and its adjoint seeds (losses.cpp:161-177).
+__global__ void __launch_bounds__(256) ssim_v_kernel(const float* __restrict__ hq, int h, int w, int ch, SsimKernel K,
+                                                     bool grad, float* __restrict__ seeds, double* sum_out) {
+  const float c1 = 0.01f * 0.01f, c2 = 0.03f * 0.03f;
+  const int64_t n = (int64_t)h * w;
+  double acc = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * ch; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e / n);
+    const int64_t p = e % n;
+    const int y = (int)(p / w), x = (int)(p % w);
+    const float* in = hq + (int64_t)c * 5 * n;
+    float q[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+    for (int k = -kRad; k <= kRad; ++k) {
+      const int64_t r = (int64_t)refl(y + k, h) * w + x;
+      const float kw = K.k[k + kRad];
+#pragma unroll
+      for (int t = 0; t < 5; ++t) q[t] += kw * in[t * n + r];
+    }
+    const float mx = q[0], my = q[1];
+    const float sx2 = q[2] - mx * mx, sy2 = q[3] - my * my, sxy = q[4] - mx * my;
+    const float a1 = 2.f * mx * my + c1, a2 = 2.f * sxy + c2;
+    const float b1 = mx * mx + my * my + c1, b2 = sx2 + sy2 + c2;
+    const float s = (a1 * a2) / (b1 * b2);
+    acc += (double)s;
+    if (grad) {
+      float* sd = seeds + (int64_t)c * 3 * n;
+      sd[p] = 2.f * my * (a2 - a1) / (b1 * b2) - s * 2.f * mx / b1 + s * 2.f * mx / b2;
+      sd[n + p] = -s / b2;
+      sd[2 * n + p] = 2.f * a1 / (b1 * b2);
+    }
+  }
+  block_add_double(acc, sum_out);
+}
+
+// Adjoint of one separable pass along an axis (filter_plane_adjoint, losses.cpp:57-75),
+// in gather form: out[i'] = sum over preimages i of refl with refl(i) == i'.
+__device__ __forceinline__ float adj_gather(const float* in, int64_t stride, int len, int ip, const SsimKernel& K) {
+  float acc = 0.f;
+  int pre[3];
+  int np = 0;
+  pre[np++] = ip;
+  if (ip >= 1 && ip <= kRad) pre[np++] = -ip;
+  const int r = 2 * len - 2 - ip;
+  if (r >= len && r <= len - 1 + kRad && ip <= len - 2) pre[np++] = r;
+  for (int t = 0; t < np; ++t)
+#pragma unroll
+    for (int k = -kRad; k <= kRad; ++k) {
+      const int y = pre[t] - k;
+      if (y >= 0 && y < len) acc += K.k[k + kRad] * in[(int64_t)y * stride];
+    }
+  return acc;
+}
+
+__global__ void ssim_adj_v_kernel(const float* __restrict__ seeds, int h, int w, int ch, SsimKernel K,
+                                  float* __restrict__ tmp) {
+  const int64_t n = (int64_t)h * w;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * ch * 3; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t plane = e / n;
+    const int64_t p = e % n;
+    const int y = (int)(p / w), x = (int)(p % w);
+    tmp[plane * n + p] = adj_gather(seeds + plane * n + x, w, h, y, K);
+  }
+}
+
+__global__ void ssim_adj_h_kernel(const float* __restrict__ tmp, const float* __restrict__ a,
+                                  const float* __restrict__ b, int h, int w, int ch, SsimKernel K, float scale,
+                                  float out_scale, bool accumulate, float* __restrict__ d_a) {
+  const int64_t n = (int64_t)h * w;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * ch; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e / n);
+    const int64_t p = e % n;
+    const int y = (int)(p / w), x = (int)(p % w);
+    const float* base = tmp + (int64_t)c * 3 * n + (int64_t)y * w;
+    const float g0 = adj_gather(base, 1, w, x, K);
+    const float g1 = adj_gather(base + n, 1, w, x, K);
+    const float g2 = adj_gather(base + 2 * n, 1, w, x, K);
+    const int64_t q = p * ch + c;
+    float v = g0 * scale;
+    v += 2.f * a[q] * g1 * scale;
+    v += b[q] * g2 * scale;
+    v *= out_scale;
+    d_a[q] = accumulate ? d_a[q] + v : v;
+  }
+}
+
+// ssim_global, losses.cpp:85-129 (images smaller than the window). One block.
+__global__ void ssim_global_kernel(const float* a, const float* b, int h, int w, int ch, float* d_a, float out_scale,
+                                   bool accumulate, double* sum_out) {
+  __shared__ double red[5];
+  const float c1 = 0.01f * 0.01f, c2 = 0.03f * 0.03f;
+  const int n = h * w;
+  double total = 0.0;
+  for (int c = 0; c < ch; ++c) {
+    if (threadIdx.x < 5) red[threadIdx.x] = 0.0;
+    __syncthreads();
+    double sx = 0, sy = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      sx += a[i * ch + c];
+      sy += b[i * ch + c];
+    }
+    atomicAdd(&red[0], sx);
+    atomicAdd(&red[1], sy);
+    __syncthreads();
+    const float mx = (float)(red[0] / n), my = (float)(red[1] / n);
+    double vx = 0, vy = 0, cv = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const float dx = a[i * ch + c] - mx, dy = b[i * ch + c] - my;
+      vx += dx * dx;
+      vy += dy * dy;
+      cv += dx * dy;
+    }
+    atomicAdd(&red[2], vx);
+    atomicAdd(&red[3], vy);
+    atomicAdd(&red[4], cv);
+    __syncthreads();
+    const float fvx = (float)(red[2] / n), fvy = (float)(red[3] / n), fcv = (float)(red[4] / n);
+    const float a1 = 2.f * mx * my + c1, a2 = 2.f * fcv + c2;
+    const float b1 = mx * mx + my * my + c1, b2 = fvx + fvy + c2;
+    const float s = (a1 * a2) / (b1 * b2);
+    total += s;
+    if (d_a) {
+      const float ds_dmx = 2.f * my * a2 / (b1 * b2) - s * 2.f * mx / b1;
+      const float ds_dvx = -s / b2;
+      const float ds_dcov = 2.f * a1 / (b1 * b2);
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const float dx = a[i * ch + c] - mx, dy = b[i * ch + c] - my;
+        const float g = (ds_dmx / n + ds_dvx * 2.f * dx / n + ds_dcov * dy / n) / ch * out_scale;
+        d_a[i * ch + c] = accumulate ? d_a[i * ch + c] + g : g;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) atomicAdd(sum_out, total / ch * (double)n * ch);  // returned as a per-pixel sum
+}
+
+// SSIM value (as a sum over pixels and channels into *sum_out) and, when d_a is given,
+// out_scale * dSSIM/da written (or added) into d_a.
+void ssim_run(cudaStream_t st, const float* a, const float* b, int h, int w, int ch, float* d_a, float out_scale,
+              bool accumulate, float* scratch, double* sum_out) {
+  const SsimKernel K = make_kernel();
+  const int64_t n = (int64_t)h * w;
+  if (h < kWin || w < kWin) {
+    ssim_global_kernel<<<1, 256, 0, st>>>(a, b, h, w, ch, d_a, out_scale, accumulate, sum_out);
+    count_launch();
+    return;
+  }
+  float* hq = scratch;
+  float* seeds = scratch + 5 * n * ch;
+  float* tmp = seeds + 3 * n * ch;
+  const int grid = (int)std::min<int64_t>((n * ch + 255) / 256, 148 * 16);
+  ssim_h_kernel<<<grid, 256, 0, st>>>(a, b, h, w, ch, K, hq);
+  ssim_v_kernel<<<grid, 256, 0, st>>>(hq, h, w, ch, K, d_a != nullptr, seeds, sum_out);
+  count_launch(2);
+  if (d_a) {
+    const float scale = 1.f / ((float)n * (float)ch);
+    const int g3 = (int)std::min<int64_t>((n * ch * 3 + 255) / 256, 148 * 16);
+    ssim_adj_v_kernel<<<g3, 256, 0, st>>>(seeds, h, w, ch, K, tmp);
+    ssim_adj_h_kernel<<<grid, 256, 0, st>>>(tmp, a, b, h, w, ch, K, scale, out_scale, accumulate, d_a);
+    count_launch(2);
+  }
+}
+
+}  // namespace
+
+size_t ssim_scratch_floats(int h, int w, int c) { return (size_t)h * w * c * 11; }
+
+double ssim_host(cudaStream_t st, const float* a, const float* b, int h, int w, int c, float* d_a, float* scratch) {
+  double* d_sum;
+  cudaMallocAsync(&d_sum, sizeof(double), st);
+  cudaMemsetAsync(d_sum, 0, sizeof(double), st);
+  ssim_run(st, a, b, h, w, c, d_a, 1.f, false, scratch, d_sum);
+  double s = 0;
+  cudaMemcpyAsync(&s, d_sum, sizeof(double), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(d_sum, st);
+  cudaStreamSynchronize(st);
+  return s / ((double)h * w * c);
+}
+
+void image_losses(cudaStream_t st, const float* color, const float* depth, const float* alpha, const float* rgb_t,
+                  const float* depth_t, int h, int w, float lambda_i1, float lambda_i2, float rgb_scale,
+                  float depth_scale, bool want_grad, float* d_color, float* d_depth, double* partials,
+                  float* ssim_scratch) {
+  const int64_t npx = (int64_t)h * w;
+  const int grid = (int)std::min<int64_t>((npx + 255) / 256, 148 * 8);
+  l1_depth_kernel<<<grid, 256, 0, st>>>(color, depth, alpha, rgb_t, depth_t, npx, lambda_i1, (float)(npx * 3),
+                                        want_grad, d_color, d_depth, partials);
+  count_launch();
+  // SSIM forward always runs (losses.cpp:217); its gradient only matters when lambda_i2 != 0.
+  const bool ssim_grad = want_grad && lambda_i2 != 0.f;
+  ssim_run(st, color, rgb_t, h, w, 3, ssim_grad ? d_color : nullptr, lambda_i2 * -0.5f, true, ssim_scratch,
+           &partials[1]);
+  if (want_grad) {
+    finalize_upstream_kernel<<<grid, 256, 0, st>>>(d_color, d_depth, npx, rgb_scale, depth_scale, partials);
+    count_launch();
+  }
+}
+
+}  // namespace lm

@@ -1,0 +1,802 @@
+// render.cu — 3DGS front end + tile rasteriser, forward and backward (sm_100a).
+//
+// Replaces the reference's tile-free scanline renderer (proj/src/render.cpp):
+//   K1 project_kernel      <- project_one + splat_bounds      (render.cpp:42-91,153-167)
+//   K2 scan_tiles_kernel   <- splats_by_row                    (render.cpp:93-101)
+//   K3 scatter_kernel      <- per-pixel candidate lists        (render.cpp:174-178)
+//   K3b tile_sort_kernel   <- sort_pixel std::sort per pixel   (render.cpp:104-112)
+//   K4 raster_fwd_kernel   <- blend loop                       (render.cpp:183-210)
+//   K8 raster_bwd_kernel   <- render_backward pixel pass       (render.cpp:275-358)
+//   K9 project_bwd_kernel  <- render_backward projection pass  (render.cpp:368-429)
+//
+// Canonical tile list: for a 16x16 tile, every Gaussian whose inclusive 3-sigma
+// bbox meets the tile, ordered by (camera z, source). A pixel's reference
+// candidate list is exactly the subsequence whose bbox contains the pixel, in the
+// same order, so the blend reproduces the reference per-pixel semantics. The
+// projection, bbox, sort keys, alpha', clamp and termination decisions use the
+// reference's float op sequence without FMA contraction, so they are bit-exact.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace lm {
+
+namespace {
+
+struct Cam {
+  float r[9];  // rot_cw (world -> camera), row-major
+  float o[3];  // camera origin (pose translation)
+  Intr intr;
+  int32_t tiles_x, tiles_y;
+};
+
+// project_one + splat_bounds with the reference's exact float/double op order.
+__device__ __forceinline__ bool project_exact(const float* __restrict__ p, const float* __restrict__ q,
+                                              const float* __restrict__ lsc, float logit, const Cam& c,
+                                              SplatRec& out, float* cov2d_out = nullptr) {
+  const float d0 = fs(p[0], c.o[0]), d1 = fs(p[1], c.o[1]), d2 = fs(p[2], c.o[2]);
+  float pc[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) pc[i] = fa(fa(fm(c.r[3 * i], d0), fm(c.r[3 * i + 1], d1)), fm(c.r[3 * i + 2], d2));
+  const float z = pc[2];
+  if (!(z > kZNear)) return false;
+  const float qn = __fsqrt_rn(fa(fa(fa(fm(q[0], q[0]), fm(q[1], q[1])), fm(q[2], q[2])), fm(q[3], q[3])));
+  if (!(qn > 0.f) || !isfinite(qn)) return false;
+  const float w = fd(q[0], qn), x = fd(q[1], qn), y = fd(q[2], qn), zq = fd(q[3], qn);
+  float rg[9];
+  rg[0] = fs(1.f, fm(2.f, fa(fm(y, y), fm(zq, zq))));
+  rg[1] = fm(2.f, fs(fm(x, y), fm(w, zq)));
+  rg[2] = fm(2.f, fa(fm(x, zq), fm(w, y)));
+  rg[3] = fm(2.f, fa(fm(x, y), fm(w, zq)));
+  rg[4] = fs(1.f, fm(2.f, fa(fm(x, x), fm(zq, zq))));
+  rg[5] = fm(2.f, fs(fm(y, zq), fm(w, x)));
+  rg[6] = fm(2.f, fs(fm(x, zq), fm(w, y)));
+  rg[7] = fm(2.f, fa(fm(y, zq), fm(w, x)));
+  rg[8] = fs(1.f, fm(2.f, fa(fm(x, x), fm(y, y))));
+  float sc[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) sc[i] = exp_exact(lsc[i]);
+  float m[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      m[3 * i + j] = fm(fa(fa(fm(c.r[3 * i], rg[j]), fm(c.r[3 * i + 1], rg[3 + j])), fm(c.r[3 * i + 2], rg[6 + j])),
+                        sc[j]);
+  float cc[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      cc[3 * i + j] = fa(fa(fm(m[3 * i], m[3 * j]), fm(m[3 * i + 1], m[3 * j + 1])), fm(m[3 * i + 2], m[3 * j + 2]));
+  const float fx = c.intr.fx, fy = c.intr.fy;
+  const float mx = fa(fd(fm(fx, pc[0]), z), c.intr.cx);
+  const float my = fa(fd(fm(fy, pc[1]), z), c.intr.cy);
+  const float zz = fm(z, z);
+  const float J[6] = {fd(fx, z), 0.f, fd(fm(-fx, pc[0]), zz), 0.f, fd(fy, z), fd(fm(-fy, pc[1]), zz)};
+  float t[6];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      t[3 * i + j] = fa(fa(fm(J[3 * i], cc[j]), fm(J[3 * i + 1], cc[3 + j])), fm(J[3 * i + 2], cc[6 + j]));
+  float cv[4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      cv[2 * i + j] = fa(fa(fm(t[3 * i], J[3 * j]), fm(t[3 * i + 1], J[3 * j + 1])), fm(t[3 * i + 2], J[3 * j + 2]));
+  cv[0] = fa(cv[0], kCovReg);
+  cv[3] = fa(cv[3], kCovReg);
+  const float det = fs(fm(cv[0], cv[3]), fm(cv[1], cv[2]));
+  if (!(det > 0.f) || !isfinite(det)) return false;
+  // splat_bounds in double (render.cpp:75-91)
+  const double rx = dm(kSigmaCut, __dsqrt_rn((double)cv[0]));
+  const double ry = dm(kSigmaCut, __dsqrt_rn((double)cv[3]));
+  const double u = (double)mx, v = (double)my;
+  if (!isfinite(u) || !isfinite(v) || !isfinite(rx) || !isfinite(ry)) return false;
+  const double lo_x = ceil(ds_(u, rx)), hi_x = floor(da(u, rx));
+  const double lo_y = ceil(ds_(v, ry)), hi_y = floor(da(v, ry));
+  const int W = c.intr.width, H = c.intr.height;
+  if (hi_x < 0 || hi_y < 0 || lo_x > (double)(W - 1) || lo_y > (double)(H - 1)) return false;
+  const int x0 = (int)(lo_x > 0.0 ? lo_x : 0.0);
+  const int x1 = (int)((double)(W - 1) < hi_x ? (double)(W - 1) : hi_x);
+  const int y0 = (int)(lo_y > 0.0 ? lo_y : 0.0);
+  const int y1 = (int)((double)(H - 1) < hi_y ? (double)(H - 1) : hi_y);
+  if (!(x0 <= x1 && y0 <= y1)) return false;
+  out.mean_x = mx;
+  out.mean_y = my;
+  out.depth = z;
+  out.alpha = sigmoid_exact(logit);
+  out.a00 = fd(cv[3], det);
+  out.a01 = fd(-cv[1], det);
+  out.a10 = fd(-cv[2], det);
+  out.a11 = fd(cv[0], det);
+  out.x0 = x0;
+  out.x1 = x1;
+  out.y0 = y0;
+  out.y1 = y1;
+  if (cov2d_out)
+    for (int i = 0; i < 4; ++i) cov2d_out[i] = cv[i];
+  return true;
+}
+
+constexpr int kHistMax = 12288;  // tiles counted in shared memory (48 KB)
+
+// K1: project every Gaussian, write its record, count tile pairs.
+__global__ void __launch_bounds__(256) project_kernel(MapPtrs map, Cam cam, SplatRec* __restrict__ rec,
+                                                      int32_t* __restrict__ tile_count, int64_t* counters) {
+  extern __shared__ int32_t s_hist[];
+  const int ntiles = cam.tiles_x * cam.tiles_y;
+  const bool use_smem = ntiles <= kHistMax;
+  if (use_smem)
+    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s_hist[t] = 0;
+  __syncthreads();
+  int vis = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < map.n; i += (int64_t)gridDim.x * blockDim.x) {
+    SplatRec r;
+    const bool ok = project_exact(map.pos + 3 * i, map.rot + 4 * i, map.lsc + 3 * i, map.opa[i], cam, r);
+    if (!ok) {
+      r = SplatRec{0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 1, 0};
+    } else {
+      ++vis;
+      const int tx0 = r.x0 / kTile, tx1 = r.x1 / kTile, ty0 = r.y0 / kTile, ty1 = r.y1 / kTile;
+      for (int ty = ty0; ty <= ty1; ++ty)
+        for (int tx = tx0; tx <= tx1; ++tx) {
+          const int t = ty * cam.tiles_x + tx;
+          if (use_smem)
+            atomicAdd(&s_hist[t], 1);
+          else
+            atomicAdd(&tile_count[t], 1);
+        }
+    }
+    reinterpret_cast<float4*>(rec + i)[0] = make_float4(r.mean_x, r.mean_y, r.depth, r.alpha);
+    reinterpret_cast<float4*>(rec + i)[1] = make_float4(r.a00, r.a01, r.a10, r.a11);
+    reinterpret_cast<int4*>(rec + i)[2] = make_int4(r.x0, r.x1, r.y0, r.y1);
+  }
+  vis = __reduce_add_sync(0xffffffffu, vis);
+  if ((threadIdx.x & 31) == 0 && vis) atomicAdd((unsigned long long*)&counters[1], (unsigned long long)vis);
+  __syncthreads();
+  if (use_smem)
+    for (int t = threadIdx.x; t < ntiles; t += blockDim.x)
+      if (s_hist[t]) atomicAdd(&tile_count[t], s_hist[t]);
+}
+
+// K2: exclusive scan of per-tile counts (one block).
+__global__ void __launch_bounds__(1024) scan_tiles_kernel(const int32_t* __restrict__ count, int32_t* offset,
+                                                          int32_t* cursor, int ntiles, int64_t* counters,
+                                                          int64_t pair_cap, int64_t* step_overflow) {
+  __shared__ int64_t s_part[1024];
+  const int per = (ntiles + blockDim.x - 1) / blockDim.x;
+  const int b = threadIdx.x * per;
+  int64_t sum = 0;
+  for (int i = 0; i < per; ++i)
+    if (b + i < ntiles) sum += count[b + i];
+  s_part[threadIdx.x] = sum;
+  __syncthreads();
+  for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+    int64_t v = threadIdx.x >= (unsigned)o ? s_part[threadIdx.x - o] : 0;
+    __syncthreads();
+    s_part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  int64_t run = s_part[threadIdx.x] - sum;
+  for (int i = 0; i < per; ++i)
+    if (b + i < ntiles) {
+      offset[b + i] = (int32_t)run;
+      cursor[b + i] = (int32_t)run;
+      run += count[b + i];
+    }
+  if (threadIdx.x == blockDim.x - 1) {
+    offset[ntiles] = (int32_t)s_part[threadIdx.x];
+    counters[0] = s_part[threadIdx.x];
+    counters[2] = s_part[threadIdx.x] > pair_cap ? 1 : 0;
+    if (step_overflow && s_part[threadIdx.x] > pair_cap) *step_overflow = 1;
+  }
+}
+
+// K3: scatter (depth_bits << 32 | source) keys into their tile buckets.
+__global__ void __launch_bounds__(256) scatter_kernel(const SplatRec* __restrict__ rec, int64_t n, int tiles_x,
+                                                      int32_t* cursor, uint64_t* __restrict__ keys,
+                                                      int64_t pair_cap) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int4 bb = reinterpret_cast<const int4*>(rec + i)[2];
+    if (bb.x > bb.y) continue;
+    const float depth = rec[i].depth;
+    const uint64_t key = ((uint64_t)__float_as_uint(depth) << 32) | (uint32_t)i;
+    const int tx0 = bb.x / kTile, tx1 = bb.y / kTile, ty0 = bb.z / kTile, ty1 = bb.w / kTile;
+    for (int ty = ty0; ty <= ty1; ++ty)
+      for (int tx = tx0; tx <= tx1; ++tx) {
+        const int pos = atomicAdd(&cursor[ty * tiles_x + tx], 1);
+        if (pos < pair_cap) keys[pos] = key;
+      }
+  }
+}
+
+constexpr int kSortCap = 8192;  // keys sorted in shared memory per tile (64 KB)
+
+__device__ void bitonic_smem(uint64_t* s, int P) {
+  for (int k = 2; k <= P; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const bool asc = (i & k) == 0;
+          const uint64_t a = s[i], b = s[ixj];
+          if ((a > b) == asc) {
+            s[i] = b;
+            s[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+}
+
+// K3b: per-tile sort of the keys -> canonical (depth, source) order. Keys are unique,
+// so the result is deterministic whatever order K3's atomics produced.
+__global__ void __launch_bounds__(512) tile_sort_kernel(const int32_t* __restrict__ offset, uint64_t* keys,
+                                                        uint64_t* tmp, int64_t pair_cap, const int64_t* counters) {
+  extern __shared__ uint64_t s_keys[];
+  if (counters[2]) return;  // overflowed: step is discarded and re-run by the host
+  const int t = blockIdx.x;
+  const int start = offset[t], n = offset[t + 1] - start;
+  if (n <= 1) return;
+  uint64_t* g = keys + start;
+  if (n <= kSortCap) {
+    int P = 1;
+    while (P < n) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) s_keys[i] = i < n ? g[i] : ~0ull;
+    __syncthreads();
+    bitonic_smem(s_keys, P);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) g[i] = s_keys[i];
+    return;
+  }
+  // Oversized tile: sort kSortCap chunks in smem, then merge runs pairwise in global memory.
+  for (int c0 = 0; c0 < n; c0 += kSortCap) {
+    const int cn = min(kSortCap, n - c0);
+    int P = 1;
+    while (P < cn) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) s_keys[i] = i < cn ? g[c0 + i] : ~0ull;
+    __syncthreads();
+    bitonic_smem(s_keys, P);
+    for (int i = threadIdx.x; i < cn; i += blockDim.x) g[c0 + i] = s_keys[i];
+    __syncthreads();
+  }
+  uint64_t* src = g;
+  uint64_t* dst = tmp + start;
+  for (int width = kSortCap; width < n; width <<= 1) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int run0 = (i / (2 * width)) * 2 * width;
+      const int mid = min(run0 + width, n), end = min(run0 + 2 * width, n);
+      const uint64_t v = src[i];
+      int pos;
+      if (i < mid) {  // element of run A: rank within A + number of B elements < v
+        int lo = mid, hi = end;
+        while (lo < hi) {
+          const int m = (lo + hi) >> 1;
+          if (src[m] < v) lo = m + 1; else hi = m;
+        }
+        pos = run0 + (i - run0) + (lo - mid);
+      } else {  // element of run B: rank within B + number of A elements < v
+        int lo = run0, hi = mid;
+        while (lo < hi) {
+          const int m = (lo + hi) >> 1;
+          if (src[m] < v) lo = m + 1; else hi = m;
+        }
+        pos = run0 + (i - mid) + (lo - run0);
+      }
+      dst[pos] = v;
+    }
+    __syncthreads();
+    uint64_t* sw = src;
+    src = dst;
+    dst = sw;
+  }
+  if (src != g)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) g[i] = src[i];
+}
+
+struct RasterArgs {
+  const SplatRec* rec;
+  const float* colors;
+  const float* feats;
+  int32_t ds;
+  const int32_t* offset;
+  const uint64_t* keys;
+  int32_t tiles_x, width, height;
+  float *color, *depth, *query, *alpha;
+  int32_t* px_last;
+  float* px_T;
+  int32_t* tile_max_last;
+  const int64_t* counters;
+};
+
+// K4: forward blend, one CTA per 16x16 tile, one thread per pixel.
+template <int DSP>
+__global__ void __launch_bounds__(kTilePixels) raster_fwd_kernel(RasterArgs a) {
+  constexpr int kFwdBatch = DSP >= 64 ? 128 : 256;
+  __shared__ SplatRec s_rec[kFwdBatch];
+  __shared__ float s_col[kFwdBatch * 3];
+  __shared__ float s_feat[kFwdBatch * DSP];
+  __shared__ int32_t s_max;
+  if (a.counters[2]) return;
+  const int tile = blockIdx.x;
+  const int px = (tile % a.tiles_x) * kTile + (threadIdx.x % kTile);
+  const int py = (tile / a.tiles_x) * kTile + (threadIdx.x / kTile);
+  const bool inside = px < a.width && py < a.height;
+  const int start = a.offset[tile], end = a.offset[tile + 1];
+  if (threadIdx.x == 0) s_max = 0;
+  float T = 1.f, acc_c0 = 0.f, acc_c1 = 0.f, acc_c2 = 0.f, acc_d = 0.f, acc_a = 0.f;
+  float acc_q[DSP];
+#pragma unroll
+  for (int c = 0; c < DSP; ++c) acc_q[c] = 0.f;
+  bool done = !inside;
+  int last = end - start;
+  const float fx = (float)px, fy = (float)py;
+  for (int base = start; base < end; base += kFwdBatch) {
+    if (__syncthreads_and(done)) break;
+    const int i = base + threadIdx.x;
+    if (threadIdx.x < kFwdBatch && i < end) {
+      const uint32_t src = (uint32_t)a.keys[i];
+      s_rec[threadIdx.x] = a.rec[src];
+      s_col[threadIdx.x * 3 + 0] = a.colors[3 * (size_t)src + 0];
+      s_col[threadIdx.x * 3 + 1] = a.colors[3 * (size_t)src + 1];
+      s_col[threadIdx.x * 3 + 2] = a.colors[3 * (size_t)src + 2];
+      const float* f = a.feats + (size_t)src * a.ds;
+#pragma unroll
+      for (int c = 0; c < DSP; ++c) s_feat[threadIdx.x * DSP + c] = c < a.ds ? f[c] : 0.f;
+    }
+    __syncthreads();
+    const int cnt = min(kFwdBatch, end - base);
+    if (!done) {
+      for (int j = 0; j < cnt; ++j) {
+        const SplatRec& s = s_rec[j];
+        if (px < s.x0 || px > s.x1 || py < s.y0 || py > s.y1) continue;
+        const float dx = fs(fx, s.mean_x);
+        const float dy = fs(fy, s.mean_y);
+        const float rho = fa(fa(fm(fm(s.a00, dx), dx), fm(fm(fm(2.f, s.a01), dx), dy)), fm(fm(s.a11, dy), dy));
+        float al = fm(s.alpha, exp_exact(fm(-0.5f, rho)));
+        if (al > kAlphaMax) al = kAlphaMax;
+        const float w = fm(al, T);
+        acc_c0 = fa(acc_c0, fm(w, s_col[j * 3 + 0]));
+        acc_c1 = fa(acc_c1, fm(w, s_col[j * 3 + 1]));
+        acc_c2 = fa(acc_c2, fm(w, s_col[j * 3 + 2]));
+        acc_d = fa(acc_d, fm(w, s.depth));
+        acc_a = fa(acc_a, w);
+#pragma unroll
+        for (int c = 0; c < DSP; ++c) acc_q[c] = fa(acc_q[c], fm(w, s_feat[j * DSP + c]));
+        T = fm(T, fs(1.f, al));
+        if (T < kTransmitStop) {
+          done = true;
+          last = base - start + j + 1;
+          break;
+        }
+      }
+    }
+  }
+  if (inside) {
+    const size_t p = (size_t)py * a.width + px;
+    a.color[3 * p + 0] = acc_c0;
+    a.color[3 * p + 1] = acc_c1;
+    a.color[3 * p + 2] = acc_c2;
+    a.depth[p] = acc_d;
+    a.alpha[p] = acc_a;
+    float* q = a.query + p * a.ds;
+#pragma unroll
+    for (int c = 0; c < DSP; ++c)
+      if (c < a.ds) q[c] = acc_q[c];
+    a.px_last[p] = last;
+    a.px_T[p] = T;
+  }
+  __syncthreads();
+  if (inside) atomicMax(&s_max, last);
+  __syncthreads();
+  if (threadIdx.x == 0) a.tile_max_last[tile] = s_max;
+}
+
+struct RasterBwdArgs {
+  const SplatRec* rec;
+  const float* colors;
+  const float* feats;
+  int32_t ds;
+  const int32_t* offset;
+  const uint64_t* keys;
+  int32_t tiles_x, width, height;
+  const int32_t* px_last;
+  const float* px_T;
+  const int32_t* tile_max_last;
+  const float *d_color, *d_depth, *d_query;
+  float* geo_acc;  // N x 8: dmean_u, dmean_v, dA00, dA01, dA11, dz, dg
+  float* g_col;    // N x 3
+  float* g_feat;   // N x ds
+};
+
+constexpr int kBwdBatch = 64;
+
+// K8: reverse sweep of render_backward (render.cpp:315-353). Transmittance before each
+// blended splat is recovered by division from the forward's final T; per-splat
+// gradients are reduced warp-wise, then across the CTA in shared memory, then added
+// with one global atomic per (tile, splat, value).
+template <int DSP>
+__global__ void __launch_bounds__(kTilePixels) raster_bwd_kernel(RasterBwdArgs a) {
+  constexpr int NV = 10 + DSP;
+  __shared__ SplatRec s_rec[kBwdBatch];
+  __shared__ float s_col[kBwdBatch * 3];
+  __shared__ float s_feat[kBwdBatch * DSP];
+  __shared__ uint32_t s_src[kBwdBatch];
+  __shared__ float s_acc[kBwdBatch * NV];
+  const int tile = blockIdx.x;
+  const int px = (tile % a.tiles_x) * kTile + (threadIdx.x % kTile);
+  const int py = (tile / a.tiles_x) * kTile + (threadIdx.x / kTile);
+  const bool inside = px < a.width && py < a.height;
+  const int start = a.offset[tile];
+  const int tend = start + a.tile_max_last[tile];
+  const size_t p = inside ? (size_t)py * a.width + px : 0;
+  float uc0 = 0.f, uc1 = 0.f, uc2 = 0.f, uz = 0.f;
+  float uq[DSP];
+#pragma unroll
+  for (int c = 0; c < DSP; ++c) uq[c] = 0.f;
+  int last = 0;
+  float T = 1.f;
+  if (inside) {
+    if (a.d_color) {
+      uc0 = a.d_color[3 * p];
+      uc1 = a.d_color[3 * p + 1];
+      uc2 = a.d_color[3 * p + 2];
+    }
+    if (a.d_depth) uz = a.d_depth[p];
+    if (a.d_query) {
+#pragma unroll
+      for (int c = 0; c < DSP; ++c) uq[c] = c < a.ds ? a.d_query[p * a.ds + c] : 0.f;
+    }
+    last = a.px_last[p];
+    T = a.px_T[p];
+  }
+  const float fx = (float)px, fy = (float)py;
+  const int lane = threadIdx.x & 31;
+  float s_after = 0.f;
+  for (int hi = tend; hi > start; hi -= kBwdBatch) {
+    const int lo = max(start, hi - kBwdBatch);
+    const int cnt = hi - lo;
+    __syncthreads();
+    if (threadIdx.x < cnt) {
+      const uint32_t src = (uint32_t)a.keys[lo + threadIdx.x];
+      s_src[threadIdx.x] = src;
+      s_rec[threadIdx.x] = a.rec[src];
+      s_col[threadIdx.x * 3 + 0] = a.colors[3 * (size_t)src + 0];
+      s_col[threadIdx.x * 3 + 1] = a.colors[3 * (size_t)src + 1];
+      s_col[threadIdx.x * 3 + 2] = a.colors[3 * (size_t)src + 2];
+      const float* f = a.feats + (size_t)src * a.ds;
+#pragma unroll
+      for (int c = 0; c < DSP; ++c) s_feat[threadIdx.x * DSP + c] = c < a.ds ? f[c] : 0.f;
+    }
+    for (int e = threadIdx.x; e < cnt * NV; e += blockDim.x) s_acc[e] = 0.f;
+    __syncthreads();
+    for (int j = cnt - 1; j >= 0; --j) {
+      const SplatRec& s = s_rec[j];
+      const int idx = lo - start + j;
+      const bool contrib = inside && idx < last && px >= s.x0 && px <= s.x1 && py >= s.y0 && py <= s.y1;
+      float v[NV];
+#pragma unroll
+      for (int c = 0; c < NV; ++c) v[c] = 0.f;
+      if (contrib) {
+        const float dx = fs(fx, s.mean_x);
+        const float dy = fs(fy, s.mean_y);
+        const float rho = fa(fa(fm(fm(s.a00, dx), dx), fm(fm(fm(2.f, s.a01), dx), dy)), fm(fm(s.a11, dy), dy));
+        float al = fm(s.alpha, exp_exact(fm(-0.5f, rho)));
+        const bool clamped = al > kAlphaMax;
+        if (clamped) al = kAlphaMax;
+        const float one_m = fs(1.f, al);
+        const float Tb = fd(T, one_m);
+        const float w = al * Tb;
+        float value = uc0 * s_col[j * 3] + uc1 * s_col[j * 3 + 1] + uc2 * s_col[j * 3 + 2];
+        value += uz * s.depth;
+#pragma unroll
+        for (int c = 0; c < DSP; ++c) value += uq[c] * s_feat[j * DSP + c];
+        v[7] = w * uc0;
+        v[8] = w * uc1;
+        v[9] = w * uc2;
+        v[5] = w * uz;
+#pragma unroll
+        for (int c = 0; c < DSP; ++c) v[10 + c] = w * uq[c];
+        const float d_alpha = Tb * value - s_after / one_m;
+        s_after += w * value;
+        if (!clamped) {
+          const float g = al / s.alpha;
+          v[6] = d_alpha * g;
+          const float d_rho = -0.5f * al * d_alpha;
+          const float ad_x = s.a00 * dx + s.a01 * dy;
+          const float ad_y = s.a10 * dx + s.a11 * dy;
+          v[0] = d_rho * -2.f * ad_x;
+          v[1] = d_rho * -2.f * ad_y;
+          v[2] = d_rho * dx * dx;
+          v[3] = d_rho * dx * dy;
+          v[4] = d_rho * dy * dy;
+        }
+        T = Tb;
+      }
+      if (__any_sync(0xffffffffu, contrib)) {
+#pragma unroll
+        for (int c = 0; c < NV; ++c) {
+          const float r = warp_sum(v[c]);
+          if (lane == 0 && r != 0.f) atomicAdd(&s_acc[j * NV + c], r);
+        }
+      }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < cnt * NV; e += blockDim.x) {
+      const float val = s_acc[e];
+      if (val == 0.f) continue;
+      const int j = e / NV, c = e % NV;
+      const size_t src = s_src[j];
+      if (c < 7)
+        atomicAdd(&a.geo_acc[src * 8 + c], val);
+      else if (c < 10)
+        atomicAdd(&a.g_col[src * 3 + (c - 7)], val);
+      else if (c - 10 < a.ds)
+        atomicAdd(&a.g_feat[src * a.ds + (c - 10)], val);
+    }
+  }
+}
+
+struct ProjBwdArgs {
+  MapPtrs map;
+  MapPtrs grads;
+  const SplatRec* rec;
+  float* geo_acc;
+  float rcw[9], rwc[9], o[3];
+  float fx, fy, cx, cy;
+};
+
+// K9: projection backward (render.cpp:368-429), one thread per listed Gaussian.
+__global__ void __launch_bounds__(256) project_bwd_kernel(ProjBwdArgs a) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= a.map.n) return;
+  const int4 bb = reinterpret_cast<const int4*>(a.rec + i)[2];
+  if (bb.x > bb.y) return;
+  float* acc = a.geo_acc + 8 * i;
+  float ac[7];
+#pragma unroll
+  for (int c = 0; c < 7; ++c) {
+    ac[c] = acc[c];
+    acc[c] = 0.f;
+  }
+  const float* p = a.map.pos + 3 * i;
+  const float* q = a.map.rot + 4 * i;
+  const float* ls = a.map.lsc + 3 * i;
+  const float d0 = p[0] - a.o[0], d1 = p[1] - a.o[1], d2 = p[2] - a.o[2];
+  float pc[3];
+  for (int r = 0; r < 3; ++r) pc[r] = a.rcw[3 * r] * d0 + a.rcw[3 * r + 1] * d1 + a.rcw[3 * r + 2] * d2;
+  const float qn = sqrtf(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+  const float qw = q[0] / qn, qx = q[1] / qn, qy = q[2] / qn, qz = q[3] / qn;
+  float rg[9] = {1.f - 2.f * (qy * qy + qz * qz), 2.f * (qx * qy - qw * qz), 2.f * (qx * qz + qw * qy),
+                 2.f * (qx * qy + qw * qz), 1.f - 2.f * (qx * qx + qz * qz), 2.f * (qy * qz - qw * qx),
+                 2.f * (qx * qz - qw * qy), 2.f * (qy * qz + qw * qx), 1.f - 2.f * (qx * qx + qy * qy)};
+  const float sc[3] = {expf(ls[0]), expf(ls[1]), expf(ls[2])};
+  float rcg[9], m[9];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) {
+      rcg[3 * r + c] = a.rcw[3 * r] * rg[c] + a.rcw[3 * r + 1] * rg[3 + c] + a.rcw[3 * r + 2] * rg[6 + c];
+      m[3 * r + c] = rcg[3 * r + c] * sc[c];
+    }
+  float cc[9];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) cc[3 * r + c] = m[3 * r] * m[3 * c] + m[3 * r + 1] * m[3 * c + 1] + m[3 * r + 2] * m[3 * c + 2];
+  const float x = pc[0], y = pc[1], z = pc[2];
+  const float fx = a.fx, fy = a.fy;
+  const float J[6] = {fx / z, 0.f, -fx * x / (z * z), 0.f, fy / z, -fy * y / (z * z)};
+  const SplatRec s = a.rec[i];
+  const float A[4] = {s.a00, s.a01, s.a10, s.a11};
+  // cov_cam for d_jac; cov_inv from the forward record (identical values)
+  const float alpha = s.alpha;
+  a.grads.opa[i] += ac[6] * alpha * (1.f - alpha);
+  const float dA[4] = {ac[2], ac[3], ac[3], ac[4]};
+  float t1[4], dc[4];
+  for (int r = 0; r < 2; ++r)
+    for (int c = 0; c < 2; ++c) t1[2 * r + c] = -A[2 * r] * dA[c] - A[2 * r + 1] * dA[2 + c];
+  for (int r = 0; r < 2; ++r)
+    for (int c = 0; c < 2; ++c) dc[2 * r + c] = t1[2 * r] * A[c] + t1[2 * r + 1] * A[2 + c];
+  float jdc[6];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 2; ++c) jdc[2 * r + c] = J[r] * dc[c] + J[3 + r] * dc[2 + c];
+  float dcc[9];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) dcc[3 * r + c] = jdc[2 * r] * J[c] + jdc[2 * r + 1] * J[3 + c];
+  float dcj[6], djac[6];
+  for (int r = 0; r < 2; ++r)
+    for (int c = 0; c < 3; ++c) dcj[3 * r + c] = 2.f * (dc[2 * r] * J[c] + dc[2 * r + 1] * J[3 + c]);
+  for (int r = 0; r < 2; ++r)
+    for (int c = 0; c < 3; ++c) djac[3 * r + c] = dcj[3 * r] * cc[c] + dcj[3 * r + 1] * cc[3 + c] + dcj[3 * r + 2] * cc[6 + c];
+  float dm_[9];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c)
+      dm_[3 * r + c] = 2.f * (dcc[3 * r] * m[c] + dcc[3 * r + 1] * m[3 + c] + dcc[3 * r + 2] * m[6 + c]);
+  float drg[9];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c)
+      drg[3 * r + c] = (a.rcw[r] * dm_[c] + a.rcw[3 + r] * dm_[3 + c] + a.rcw[6 + r] * dm_[6 + c]) * sc[c];
+  for (int c = 0; c < 3; ++c)
+    a.grads.lsc[3 * i + c] += (rcg[c] * dm_[c] + rcg[3 + c] * dm_[3 + c] + rcg[6 + c] * dm_[6 + c]) * sc[c];
+  const float dw[9] = {0.f, -qz, qy, qz, 0.f, -qx, -qy, qx, 0.f};
+  const float dxm[9] = {0.f, qy, qz, qy, -2.f * qx, -qw, qz, qw, -2.f * qx};
+  const float dym[9] = {-2.f * qy, qx, qw, qx, 0.f, qz, -qw, qz, -2.f * qy};
+  const float dzm[9] = {-2.f * qz, -qw, qx, qw, -2.f * qz, qy, qx, qy, 0.f};
+  float dq[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int r = 0; r < 9; ++r) {
+    dq[0] += dw[r] * drg[r];
+    dq[1] += dxm[r] * drg[r];
+    dq[2] += dym[r] * drg[r];
+    dq[3] += dzm[r] * drg[r];
+  }
+  for (int r = 0; r < 4; ++r) dq[r] *= 2.f;
+  const float qh[4] = {qw, qx, qy, qz};
+  const float qd = qh[0] * dq[0] + qh[1] * dq[1] + qh[2] * dq[2] + qh[3] * dq[3];
+  for (int r = 0; r < 4; ++r) a.grads.rot[4 * i + r] += (dq[r] - qh[r] * qd) / qn;
+  float dp[3] = {0.f, 0.f, 0.f};
+  const float z2 = z * z, z3 = z2 * z;
+  dp[0] += ac[0] * fx / z;
+  dp[2] += ac[0] * (-fx * x / z2);
+  dp[1] += ac[1] * fy / z;
+  dp[2] += ac[1] * (-fy * y / z2);
+  dp[0] += djac[2] * (-fx / z2);
+  dp[1] += djac[5] * (-fy / z2);
+  dp[2] += djac[0] * (-fx / z2) + djac[2] * (2.f * fx * x / z3) + djac[4] * (-fy / z2) + djac[5] * (2.f * fy * y / z3);
+  dp[2] += ac[5];
+  for (int r = 0; r < 3; ++r) a.grads.pos[3 * i + r] += a.rwc[3 * r] * dp[0] + a.rwc[3 * r + 1] * dp[1] + a.rwc[3 * r + 2] * dp[2];
+}
+
+// project_gaussian (render.cpp:118-132): one Gaussian, returns cov2d (not its inverse).
+__global__ void project_single_kernel(const float* in, Cam cam, float* out) {
+  const float* p = in;
+  const float* q = in + 3;
+  const float* ls = in + 7;
+  const float logit = in[10];
+  SplatRec r;
+  float cv[4];
+  const bool ok = project_exact(p, q, ls, logit, cam, r, cv);
+  out[0] = ok ? 1.f : 0.f;
+  if (!ok) return;
+  out[1] = r.mean_x;
+  out[2] = r.mean_y;
+  for (int i = 0; i < 4; ++i) out[3 + i] = cv[i];
+  out[7] = r.depth;
+}
+
+template <int DSP>
+void launch_fwd(cudaStream_t st, int ntiles, const RasterArgs& a) {
+  raster_fwd_kernel<DSP><<<ntiles, kTilePixels, 0, st>>>(a);
+}
+template <int DSP>
+void launch_bwd(cudaStream_t st, int ntiles, const RasterBwdArgs& a) {
+  raster_bwd_kernel<DSP><<<ntiles, kTilePixels, 0, st>>>(a);
+}
+
+int pad_ds(int ds) {
+  if (ds <= 4) return 4;
+  if (ds <= 8) return 8;
+  if (ds <= 16) return 16;
+  if (ds <= 32) return 32;
+  if (ds <= 64) return 64;
+  return -1;
+}
+
+}  // namespace
+
+void project_single(cudaStream_t st, const float* d_in11, const float rot_cw[9], const float origin[3],
+                    const Intr& intr, float* d_out8) {
+  Cam cam;
+  for (int i = 0; i < 9; ++i) cam.r[i] = rot_cw[i];
+  for (int i = 0; i < 3; ++i) cam.o[i] = origin[i];
+  cam.intr = intr;
+  cam.tiles_x = cam.tiles_y = 1;
+  project_single_kernel<<<1, 1, 0, st>>>(d_in11, cam, d_out8);
+  count_launch();
+}
+
+void render_forward(cudaStream_t st, const MapPtrs& map, const float rot_cw[9], const float origin[3],
+                    const Intr& intr, RenderWork& w, float* color, float* depth, float* query, float* alpha,
+                    bool zero_outputs, bool count_only, bool blend) {
+  Cam cam;
+  for (int i = 0; i < 9; ++i) cam.r[i] = rot_cw[i];
+  for (int i = 0; i < 3; ++i) cam.o[i] = origin[i];
+  cam.intr = intr;
+  cam.tiles_x = w.tiles_x;
+  cam.tiles_y = w.tiles_y;
+  const int ntiles = w.tiles_x * w.tiles_y;
+  const size_t npx = (size_t)intr.width * intr.height;
+  cudaMemsetAsync(w.tile_count, 0, sizeof(int32_t) * ntiles, st);
+  cudaMemsetAsync(w.counters, 0, sizeof(int64_t) * 4, st);
+  if (zero_outputs) {
+    cudaMemsetAsync(color, 0, sizeof(float) * npx * 3, st);
+    cudaMemsetAsync(depth, 0, sizeof(float) * npx, st);
+    cudaMemsetAsync(query, 0, sizeof(float) * npx * map.ds, st);
+    cudaMemsetAsync(alpha, 0, sizeof(float) * npx, st);
+  }
+  const int grid1 = 148 * 2;
+  const size_t hist_smem = ntiles <= kHistMax ? sizeof(int32_t) * ntiles : 0;
+  if (map.n > 0) {
+    project_kernel<<<grid1, 256, hist_smem, st>>>(map, cam, w.rec, w.tile_count, w.counters);
+    count_launch();
+  }
+  scan_tiles_kernel<<<1, 1024, 0, st>>>(w.tile_count, w.tile_offset, w.tile_cursor, ntiles, w.counters, w.pair_cap,
+                                        w.step_overflow);
+  count_launch();
+  if (count_only) return;
+  if (map.n > 0) {
+    scatter_kernel<<<grid1 * 2, 256, 0, st>>>(w.rec, map.n, w.tiles_x, w.tile_cursor, w.keys, w.pair_cap);
+    count_launch();
+  }
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(tile_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortCap * 8);
+    attr_set = true;
+  }
+  tile_sort_kernel<<<ntiles, 512, kSortCap * 8, st>>>(w.tile_offset, w.keys, w.keys_tmp, w.pair_cap, w.counters);
+  count_launch();
+  if (!blend) return;
+  render_blend(st, map, intr, w, color, depth, query, alpha);
+}
+
+void render_blend(cudaStream_t st, const MapPtrs& map, const Intr& intr, RenderWork& w, float* color, float* depth,
+                  float* query, float* alpha) {
+  const int ntiles = w.tiles_x * w.tiles_y;
+  RasterArgs a{w.rec, map.col, map.feat, map.ds, w.tile_offset, w.keys, w.tiles_x, intr.width, intr.height,
+               color, depth, query, alpha, w.px_last, w.px_T, w.tile_max_last, w.counters};
+  switch (pad_ds(map.ds)) {
+    case 4: launch_fwd<4>(st, ntiles, a); break;
+    case 8: launch_fwd<8>(st, ntiles, a); break;
+    case 16: launch_fwd<16>(st, ntiles, a); break;
+    case 32: launch_fwd<32>(st, ntiles, a); break;
+    case 64: launch_fwd<64>(st, ntiles, a); break;
+    default: break;
+  }
+  count_launch();
+}
+
+void render_backward(cudaStream_t st, const MapPtrs& map, const float rot_cw[9], const float rot_wc[9],
+                     const float origin[3], const Intr& intr, const RenderWork& w, const float* d_color,
+                     const float* d_depth, const float* d_query, float* geo_acc, const MapPtrs& grads,
+                     bool project) {
+  const int ntiles = w.tiles_x * w.tiles_y;
+  RasterBwdArgs a{w.rec, map.col, map.feat, map.ds, w.tile_offset, w.keys, w.tiles_x, intr.width, intr.height,
+                  w.px_last, w.px_T, w.tile_max_last, d_color, d_depth, d_query, geo_acc, grads.col, grads.feat};
+  switch (pad_ds(map.ds)) {
+    case 4: launch_bwd<4>(st, ntiles, a); break;
+    case 8: launch_bwd<8>(st, ntiles, a); break;
+    case 16: launch_bwd<16>(st, ntiles, a); break;
+    case 32: launch_bwd<32>(st, ntiles, a); break;
+    case 64: launch_bwd<64>(st, ntiles, a); break;
+    default: break;
+  }
+  count_launch();
+  if (!project) return;
+  render_project_backward(st, map, rot_cw, rot_wc, origin, intr, w, geo_acc, grads);
+}
+
+void render_project_backward(cudaStream_t st, const MapPtrs& map, const float rot_cw[9], const float rot_wc[9],
+                             const float origin[3], const Intr& intr, const RenderWork& w, float* geo_acc,
+                             const MapPtrs& grads) {
+  if (map.n > 0) {
+    ProjBwdArgs pa;
+    pa.map = map;
+    pa.grads = grads;
+    pa.rec = w.rec;
+    pa.geo_acc = geo_acc;
+    for (int i = 0; i < 9; ++i) {
+      pa.rcw[i] = rot_cw[i];
+      pa.rwc[i] = rot_wc[i];
+    }
+    for (int i = 0; i < 3; ++i) pa.o[i] = origin[i];
+    pa.fx = intr.fx;
+    pa.fy = intr.fy;
+    pa.cx = intr.cx;
+    pa.cy = intr.cy;
+    project_bwd_kernel<<<(unsigned)((map.n + 255) / 256), 256, 0, st>>>(pa);
+    count_launch();
+  }
+}
+
+}  // namespace lm

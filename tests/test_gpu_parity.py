@@ -1,0 +1,301 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the same seeded
+inputs. Bars (BASELINE.json north_star / SURVEY.md §8(d)):
+  - projected splats, tile lists and sort order: bit-exact;
+  - rendered colour / depth / query / alpha: |a-b| <= 1e-4 * max(|b|, 1e-3 * max|b|);
+  - gradients: |a-b| <= 1e-3 * max(|b|, 1e-3 * ||b||_inf) per block (plus norm-wise);
+  - decoded embeddings: per-row cosine >= 0.999.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2602_12314_b200 import api  # noqa: E402
+from paper_2602_12314_b200 import synthetic  # noqa: E402
+from paper_2602_12314_b200._capi import StaleCache  # noqa: E402
+
+THREADS = 8
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return api.Context(0)
+
+
+def oracle_render_fn(m, q, t, intr):
+    om = oracle.GaussianMap(m.positions, m.rotations, m.colors, m.log_scales, m.opacity_logits, m.features)
+    oi = oracle.make_intr(intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height)
+    out = oracle.render(om, q, t, oi, threads=THREADS)
+    return out["color"], out["depth"], out["alpha"]
+
+
+@pytest.fixture(scope="module")
+def cfg0():
+    return synthetic.make_workload(0, oracle_render_fn)
+
+
+def to_oracle_map(m):
+    return oracle.GaussianMap(*[np.ascontiguousarray(getattr(m, f), np.float32) for f in oracle.FIELDS])
+
+
+def oi(intr):
+    return oracle.make_intr(intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height)
+
+
+def gi(intr):
+    return api.make_intrinsics(intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height)
+
+
+def assert_close_floor(a, b, rtol, name, floor=1e-3):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    scale = np.maximum(np.abs(b), floor * max(np.abs(b).max(), 1e-30))
+    err = np.abs(a - b) / scale
+    worst = err.max() if err.size else 0.0
+    assert worst <= rtol, f"{name}: max scaled err {worst:.3e} > {rtol} (at {np.unravel_index(err.argmax(), err.shape)})"
+    if b.size:
+        nrm = np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
+        assert nrm <= rtol, f"{name}: norm-wise err {nrm:.3e}"
+
+
+# ------------------------------------------------------------------------------- renderer
+def test_projection_and_tiles_bit_exact(ctx, cfg0):
+    w = cfg0
+    om = to_oracle_map(w.map)
+    ref = oracle.render(om, (1, 0, 0, 0), (0, 0, 0), oi(w.intr), threads=THREADS)
+    gm = api.GaussianMap.from_numpy(w.map)
+    out = api.render(ctx, gm, api.make_pose(), gi(w.intr))
+    got = out.splats()
+    rs = ref["splats"]
+    assert len(got) == len(rs) and len(rs) > 1000
+    assert np.array_equal(got["source"], rs["source"])
+    for f in ("x0", "x1", "y0", "y1"):
+        assert np.array_equal(got[f], rs[f]), f
+    for f in ("mean", "cov_inv", "depth", "alpha"):
+        assert np.array_equal(got[f].view(np.uint32), np.ascontiguousarray(rs[f]).astype(np.float32).view(np.uint32)), f
+    # canonical tile lists from the reference's own splat list
+    tx, ty, off, src = out.tiles()
+    assert tx == math.ceil(w.intr.width / 16) and ty == math.ceil(w.intr.height / 16)
+    tx0, tx1, ty0, ty1 = rs["x0"] // 16, rs["x1"] // 16, rs["y0"] // 16, rs["y1"] // 16
+    order = np.lexsort((rs["source"], rs["depth"]))
+    expect = [[] for _ in range(tx * ty)]
+    for k in order:
+        for yy in range(ty0[k], ty1[k] + 1):
+            for xx in range(tx0[k], tx1[k] + 1):
+                expect[yy * tx + xx].append(rs["source"][k])
+    for t in range(tx * ty):
+        assert np.array_equal(src[off[t]:off[t + 1]], np.asarray(expect[t], np.int32)), f"tile {t}"
+
+
+def test_render_images_match(ctx, cfg0):
+    w = cfg0
+    ref = oracle.render(to_oracle_map(w.map), (1, 0, 0, 0), (0, 0, 0), oi(w.intr), threads=THREADS)
+    out = api.render(ctx, api.GaussianMap.from_numpy(w.map), api.make_pose(), gi(w.intr))
+    for f in ("color", "depth", "query", "alpha"):
+        g = getattr(out, f).cpu().numpy()
+        assert_close_floor(g, ref[f], 1e-4, f)
+        same = np.mean(g.view(np.uint32) == ref[f].astype(np.float32).view(np.uint32))
+        assert same > 0.999, f"{f}: only {same:.5f} of values bit-identical"
+
+
+def test_render_posed_camera(ctx):
+    rng = np.random.default_rng(5)
+    m = synthetic.random_map(rng, 5000, (-2, -1.5, 1), (2, 1.5, 6), 8)
+    intr = synthetic.Intr(200.0, 200.0, 96.0, 64.0, 192, 128)
+    q = synthetic.yaw_quat(0.07)
+    t = (0.05, -0.02, 0.1)
+    ref = oracle.render(to_oracle_map(m), q, t, oi(intr), threads=THREADS)
+    out = api.render(ctx, api.GaussianMap.from_numpy(m), api.make_pose(q, t), gi(intr))
+    assert np.array_equal(out.splats()["source"], ref["splats"]["source"])
+    for f in ("color", "depth", "query", "alpha"):
+        assert_close_floor(getattr(out, f).cpu().numpy(), ref[f], 1e-4, f)
+
+
+def test_render_edge_cases(ctx):
+    intr = synthetic.Intr(100.0, 100.0, 32.0, 24.0, 64, 48)
+    # empty map -> zero images (test_render.cpp:112-118)
+    empty = synthetic.HostMap(*[np.zeros(s, np.float32) for s in ((0, 3), (0, 4), (0, 3), (0, 3), (0,), (0, 3))])
+    out = api.render(ctx, api.GaussianMap.from_numpy(empty), api.make_pose(), gi(intr))
+    assert float(out.alpha.abs().max()) == 0.0 and float(out.color.abs().max()) == 0.0
+    # single opaque Gaussian (test_render.cpp:70-89) in float
+    one = synthetic.HostMap(np.array([[0, 0, 1.0]], np.float32), np.array([[1.0, 0, 0, 0]], np.float32),
+                            np.array([[0.2, 0.6, 0.9]], np.float32), np.full((1, 3), math.log(0.2), np.float32),
+                            np.array([40.0], np.float32), np.array([[1.0, 2, 3, 4]], np.float32))
+    out = api.render(ctx, api.GaussianMap.from_numpy(one), api.make_pose(), gi(intr))
+    assert out.alpha[24, 32].item() == pytest.approx(0.999, rel=1e-6)
+    assert out.query[24, 32, 3].item() == pytest.approx(4 * 0.999, rel=1e-6)
+    # invalid intrinsics -> std::invalid_argument
+    with pytest.raises(ValueError):
+        api.render(ctx, api.GaussianMap.from_numpy(one), api.make_pose(), api.make_intrinsics(0, 0, 0, 0, 4, 4))
+    # project_gaussian KATs (test_render.cpp:38-68)
+    r = api.project_gaussian(ctx, (0, 0, 1), (1, 0, 0, 0), [math.log(0.05)] * 3, 0.0, api.make_pose(), gi(intr))
+    assert r[0][0] == pytest.approx(32.0) and r[0][1] == pytest.approx(24.0) and r[2] == pytest.approx(1.0)
+    r = api.project_gaussian(ctx, (0, 0, 2.0), (1, 0, 0, 0), [math.log(0.08)] * 3, 0.0, api.make_pose(), gi(intr))
+    assert r[1][0, 0] == pytest.approx((100 * 0.08 / 2) ** 2 + 0.3, rel=1e-5)
+    assert api.project_gaussian(ctx, (0, 0, -0.5), (1, 0, 0, 0), [math.log(0.05)] * 3, 0, api.make_pose(),
+                                gi(intr)) is None
+
+
+def test_render_backward_matches(ctx):
+    rng = np.random.default_rng(7)
+    m = synthetic.random_map(rng, 3000, (-2, -1.5, 1), (2, 1.5, 6), 16)
+    m.log_scales = (m.log_scales + 1.0).astype(np.float32)  # larger footprints: more overlap
+    intr = synthetic.Intr(160.0, 160.0, 64.0, 48.0, 128, 96)
+    q, t = synthetic.yaw_quat(0.03), (0.02, 0.0, -0.05)
+    h, w_ = intr.height, intr.width
+    uc = rng.uniform(-1, 1, (h, w_, 3)).astype(np.float32)
+    ud = rng.uniform(-1, 1, (h, w_)).astype(np.float32)
+    uq = rng.uniform(-1, 1, (h, w_, 16)).astype(np.float32)
+    om = to_oracle_map(m)
+    ref = oracle.render(om, q, t, oi(intr), threads=THREADS)
+    rg = oracle.render_backward(om, q, t, oi(intr), ref["splats"], uc, ud, uq, threads=THREADS)
+    gm = api.GaussianMap.from_numpy(m)
+    pose = api.make_pose(q, t)
+    out = api.render(ctx, gm, pose, gi(intr))
+    dev = lambda a: torch.as_tensor(a, device="cuda")  # noqa: E731
+    g = api.render_backward(ctx, gm, pose, gi(intr), out, dev(uc), dev(ud), dev(uq))
+    for f in oracle.FIELDS:
+        assert_close_floor(getattr(g, f).cpu().numpy(), getattr(rg, f), 1e-3, f)
+    # stale cache (test_render.cpp:212-221)
+    gm2 = api.GaussianMap.from_numpy(synthetic.random_map(rng, 3001, (-2, -1.5, 1), (2, 1.5, 6), 16))
+    with pytest.raises(StaleCache):
+        api.render_backward(ctx, gm2, pose, gi(intr), out, dev(uc), dev(ud), dev(uq))
+
+
+# ------------------------------------------------------------------------------- decoder / losses
+def test_reconstruct_and_backward(ctx):
+    rng = np.random.default_rng(11)
+    n, ds, k, df = 3000, 16, 64, 96
+    q = rng.standard_normal((n, ds)).astype(np.float32)
+    atoms = rng.standard_normal((k, df)).astype(np.float32)
+    proj = (rng.standard_normal((ds, df)) * 0.2).astype(np.float32)
+    tau = 4.0
+    f_ref, att_ref = oracle.reconstruct(q, atoms, proj, tau, want_attention=True)
+    dev = lambda a: torch.as_tensor(a, device="cuda")  # noqa: E731
+    f, att = api.reconstruct(ctx, dev(q), dev(atoms), dev(proj), tau, want_attention=True)
+    f = f.cpu().numpy()
+    cos = (f * f_ref).sum(1) / (np.linalg.norm(f, axis=1) * np.linalg.norm(f_ref, axis=1))
+    assert cos.min() >= 0.999999
+    assert_close_floor(f, f_ref, 1e-3, "reconstruct")  # spec: cosine >= 0.999 (checked above)
+    up = rng.standard_normal((n, df)).astype(np.float32)
+    gr = oracle.reconstruct_backward(q, att_ref, atoms, proj, tau, up)
+    gg = api.reconstruct_backward(ctx, dev(q), att, dev(atoms), dev(proj), tau, dev(up))
+    for key in ("d_queries", "d_proj", "d_atoms"):
+        assert_close_floor(gg[key].cpu().numpy(), gr[key], 1e-3, key)
+    with pytest.raises(ValueError):
+        api.reconstruct(ctx, dev(q[:, :7].copy()), dev(atoms), dev(proj), tau)
+
+
+def test_trust_region_and_ssim(ctx):
+    rng = np.random.default_rng(12)
+    anchor = rng.standard_normal((64, 128)).astype(np.float32)
+    atoms = (anchor + rng.standard_normal((64, 128)) * 0.02).astype(np.float32)
+    dev = lambda a: torch.as_tensor(a, device="cuda")  # noqa: E731
+    p, g = api.trust_region_penalty(ctx, dev(atoms), dev(anchor), 0.2, want_grad=True)
+    pr, grf = oracle.trust_region_penalty(atoms, anchor, np.float32(0.2), want_grad=True)
+    assert p == pytest.approx(pr, rel=1e-5, abs=1e-6)
+    assert_close_floor(g.cpu().numpy(), grf, 1e-4, "trust grad")
+    a = rng.random((48, 64, 3)).astype(np.float32)
+    b = rng.random((48, 64, 3)).astype(np.float32)
+    v, da = api.ssim(ctx, dev(a), dev(b), want_grad=True)
+    vr, dar = oracle.ssim(a, b, want_grad=True)
+    assert v == pytest.approx(vr, rel=1e-5, abs=1e-6)
+    assert_close_floor(da.cpu().numpy(), dar, 1e-3, "ssim grad")
+    s = rng.random((6, 7, 2)).astype(np.float32)  # whole-image fallback
+    assert api.ssim(ctx, dev(s), dev(s)) == pytest.approx(1.0, abs=1e-5)
+
+
+def test_adam_bit_exact(ctx):
+    rng = np.random.default_rng(13)
+    p = rng.standard_normal(10000).astype(np.float32)
+    st_ref = oracle.AdamState(np.zeros_like(p), np.zeros_like(p))
+    pr = p.copy()
+    dev = lambda a: torch.as_tensor(a, device="cuda")  # noqa: E731
+    pg = dev(p)
+    st = api.AdamState(torch.zeros_like(pg), torch.zeros_like(pg))
+    for it in range(5):
+        g = rng.standard_normal(10000).astype(np.float32)
+        oracle.adam_step(pr, g, st_ref, np.float32(0.01))
+        api.adam_step(ctx, pg, dev(g), st, 0.01)
+    assert np.array_equal(pg.cpu().numpy().view(np.uint32), pr.view(np.uint32))
+    assert st.step == st_ref.step == 5
+    g = np.ones_like(p)
+    g[3] = np.nan
+    assert not api.adam_step(ctx, pg, dev(g), st, 0.01)
+    assert st.skipped == 1
+
+
+# ------------------------------------------------------------------------------- full step
+def make_session(ctx, w, **over):
+    cfg = api.default_config(**{**w.lambdas, **over})
+    s = api.Session(ctx, cfg, w.map.n, w.map.features.shape[1], w.atoms.shape[0], w.atoms.shape[1], gi(w.intr))
+    s.set_map(w.map)
+    s.set_dictionary(w.atoms, w.anchor, w.proj)
+    s.set_frames(w.frames)
+    s.set_batch(len(w.frames))
+    return s
+
+
+def oracle_cfg(w):
+    c = oracle.Config(lambda_l2=w.lambdas["lambda_l2"], lambda_i2=w.lambdas["lambda_i2"],
+                      lambda_trust=w.lambdas["lambda_trust"])
+    return c
+
+
+def oracle_frames(w):
+    return [oracle.Frame(f.pose_rot, f.pose_trans, f.rgb, f.depth, f.assignment.reshape(-1), f.features)
+            for f in w.frames]
+
+
+def test_session_objective_config0(ctx, cfg0):
+    w = cfg0
+    s = make_session(ctx, w)
+    loss = s.objective(want_grad=True)
+    d = oracle.Dictionary(w.atoms.copy(), w.anchor.copy(), w.proj.copy(), np.float32(w.temperature))
+    ref, (g, dp, da) = oracle.total_objective(to_oracle_map(w.map), d, oracle_frames(w), oi(w.intr), oracle_cfg(w),
+                                              threads=THREADS)
+    for key in ("l_rgb", "l_ssim", "l_depth", "l_cos", "l_l2", "l_trust", "total"):
+        assert loss[key] == pytest.approx(ref[key], rel=2e-4, abs=1e-6), key
+    assert loss["supervised_rows"] == ref["supervised_rows"]
+    gb = s.grad_buffer().cpu().numpy()
+    n, ds = w.map.n, w.map.features.shape[1]
+    offs = np.cumsum([0, 3 * n, 4 * n, 3 * n, 3 * n, n, ds * n, ds * w.proj.shape[1], w.atoms.size])
+    blocks = [g.positions, g.rotations, g.colors, g.log_scales, g.opacity_logits, g.features, dp, da]
+    names = list(oracle.FIELDS) + ["d_proj", "d_atoms"]
+    for i, (name, ref_b) in enumerate(zip(names, blocks)):
+        assert_close_floor(gb[offs[i]:offs[i + 1]], ref_b.reshape(-1), 1e-3, name)
+
+
+def test_session_step_config0_adam(ctx, cfg0):
+    w = cfg0
+    s = make_session(ctx, w)
+    s.step(read=True)
+    got = s.get_map()
+    atoms, proj = s.get_dictionary()
+    om = to_oracle_map(w.map)
+    d = oracle.Dictionary(w.atoms.copy(), w.anchor.copy(), w.proj.copy(), np.float32(w.temperature))
+    cfg = oracle_cfg(w)
+    _, (g, dp, da) = oracle.total_objective(om, d, oracle_frames(w), oi(w.intr), cfg, threads=THREADS)
+    opt = oracle.MapOptimizer()
+    opt.step_map(om, g, cfg)
+    opt.step_dict(d, dp, da, cfg)
+    # first Adam step moves each coordinate by ~lr * sign(g): compare within a 1e-5 relative band
+    # except where the reference gradient is ~0 (sign not determined at fp32).
+    for name, a, b, gref, lr in [("positions", got["positions"], om.positions, g.positions, 1e-4),
+                                 ("colors", got["colors"], om.colors, g.colors, 2.5e-3),
+                                 ("features", got["features"], om.features, g.features, 2.5e-3),
+                                 ("atoms", atoms, d.atoms, da, 1e-2), ("proj", proj, d.proj, dp, 1e-2)]:
+        diff = np.abs(a - b)
+        tiny = np.abs(gref) <= 1e-3 * np.abs(gref).max()
+        bad = (diff > 1e-5 * np.maximum(np.abs(b), 1.0)) & ~tiny
+        assert bad.mean() < 1e-3, f"{name}: {bad.mean():.2e} of coordinates moved differently"
+        assert diff.max() <= 2.0 * lr + 1e-6, name
+    nq = np.linalg.norm(got["rotations"], axis=1)
+    assert np.abs(nq - 1).max() < 1e-6
