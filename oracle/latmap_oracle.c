@@ -21,11 +21,16 @@
 typedef double T;
 #define S(x) x##_f64
 static inline T lm_exp(T x) { return exp(x); }
+static inline T lm_sqrt(T x) { return sqrt(x); }
+static inline T lm_fabs(T x) { return fabs(x); }
 #else
 typedef float T;
 #define S(x) x##_f32
 /* std::exp(float) restated as the correctly rounded (float)exp((double)x). */
 static inline T lm_exp(T x) { return (float)exp((double)x); }
+/* float sqrt / abs stay in float (Eigen's array().sqrt(), std::abs on float). */
+static inline T lm_sqrt(T x) { return sqrtf(x); }
+static inline T lm_fabs(T x) { return fabsf(x); }
 #endif
 
 #define MAP S(lm_map)
@@ -58,7 +63,7 @@ static void mat3_mul(const T* a, const T* b, T* c) {
 
 /* quat_to_rot, core/se3.hpp:12-23 (normalises internally; zero norm invalid). */
 int S(lm_quat_to_rot)(const T q[4], T r[9]) {
-  T n = sqrt(((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3]);
+  T n = lm_sqrt(((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3]);
   if (!(n > (T)0) || !isfinite((double)n)) return -1;
   const T w = q[0] / n, x = q[1] / n, y = q[2] / n, z = q[3] / n;
   r[0] = (T)1 - (T)2 * (y * y + z * z);
@@ -102,7 +107,7 @@ static void project_one(const T* p, const T* q, const T* lsc, T logit, const T* 
     f->p_cam[i] = (rot_cw[3 * i] * d[0] + rot_cw[3 * i + 1] * d[1]) + rot_cw[3 * i + 2] * d[2];
   const T z = f->p_cam[2];
   if (!(z > K_ZNEAR)) return;
-  f->q_norm = sqrt(((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3]);
+  f->q_norm = lm_sqrt(((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3]);
   if (!(f->q_norm > (T)0) || !isfinite((double)f->q_norm)) return;
   for (int i = 0; i < 4; ++i) f->q_hat[i] = q[i] / f->q_norm;
   rot_from_unit_quat(f->q_hat, f->rot_gauss);
@@ -759,7 +764,7 @@ int S(lm_rgb_loss)(const T* rendered, const T* observed, int h, int w, int ch, T
   T l1 = 0;
   for (size_t i = 0; i < sz; ++i) {
     T d = rendered[i] - observed[i];
-    l1 += fabs(d);
+    l1 += lm_fabs(d);
     if (want_grad) grad[i] = lambda_i1 * (d > 0 ? (T)1 : (d < 0 ? (T)(-1) : (T)0)) / n;
   }
   *l1_out = l1 / n;
@@ -782,7 +787,7 @@ int S(lm_depth_loss)(const T* rendered, const T* observed, const T* alpha, int64
   if (want_grad) memset(grad, 0, sizeof(T) * (size_t)n);
   for (int64_t i = 0; i < n; ++i)
     if (observed[i] > (T)0 && alpha[i] > (T)0.5) {
-      sum += fabs(rendered[i] - observed[i]);
+      sum += lm_fabs(rendered[i] - observed[i]);
       ++valid;
     }
   *flagged = 0;
@@ -813,7 +818,7 @@ T S(lm_trust_region_penalty)(const T* atoms, const T* anchor, int64_t k, int64_t
       diff[c] = atoms[j * df + c] - anchor[j * df + c];
       ss += diff[c] * diff[c];
     }
-    T dist = sqrt(ss);
+    T dist = lm_sqrt(ss);
     T excess = dist - delta;
     if (excess > (T)0) {
       total += excess;
@@ -840,7 +845,7 @@ int S(lm_feature_loss)(const T* rec, const T* tgt, int64_t n, int64_t df, const 
     T su = 0, sv = 0, dot = 0, sd = 0;
     for (int64_t c = 0; c < df; ++c) su += u[c] * u[c];
     for (int64_t c = 0; c < df; ++c) sv += v[c] * v[c];
-    const T nu = sqrt(su), nv = sqrt(sv);
+    const T nu = lm_sqrt(su), nv = lm_sqrt(sv);
     if (nu < eps || nv < eps) *zflag = 1;
     const T nug = nu > eps ? nu : eps, nvg = nv > eps ? nv : eps;
     for (int64_t c = 0; c < df; ++c) dot += u[c] * v[c];
@@ -1176,7 +1181,7 @@ int S(lm_adam_step)(T* param, const T* grad, T* m, T* v, int64_t count, int64_t*
   const T corr1 = (T)1 - (T)pow(0.9, (double)*step);
   const T corr2 = (T)1 - (T)pow(0.999, (double)*step);
   for (int64_t i = 0; i < count; ++i)
-    param[i] -= lr * (m[i] / corr1) / (sqrt(v[i] / corr2) + (T)1e-8);
+    param[i] -= lr * (m[i] / corr1) / (lm_sqrt(v[i] / corr2) + (T)1e-8);
   return 1;
 }
 
@@ -1184,7 +1189,7 @@ int S(lm_adam_step)(T* param, const T* grad, T* m, T* v, int64_t count, int64_t*
 void S(lm_renorm_quats)(T* rot, int64_t n) {
   for (int64_t i = 0; i < n; ++i) {
     T* q = rot + 4 * i;
-    const T nn = sqrt(((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3]);
+    const T nn = lm_sqrt(((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3]);
     if (nn > (T)1e-12f) {
       for (int c = 0; c < 4; ++c) q[c] = q[c] / nn;
     } else {

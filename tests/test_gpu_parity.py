@@ -254,6 +254,27 @@ def oracle_frames(w):
             for f in w.frames]
 
 
+def dict_grads_f64(w, query_f32, lam):
+    """Ground truth for d_proj / d_atoms: the reference decoder algebra in double on the (bit-exact
+    float) rendered queries, scaled as total_objective does (objective.cpp:130-135,176-185)."""
+    f64 = np.float64
+    q = query_f32.reshape(-1, query_f32.shape[-1]).astype(f64)
+    fr = w.frames[0]
+    a = fr.assignment.reshape(-1)
+    sup = a >= 0
+    q = np.ascontiguousarray(q[sup])
+    tgt = np.ascontiguousarray(fr.features.astype(f64)[a[sup]])
+    atoms, anchor, proj = (x.astype(f64) for x in (w.atoms, w.anchor, w.proj))
+    tau = f64(np.float32(w.temperature))
+    rec, att = oracle.reconstruct(q, atoms, proj, tau, want_attention=True)
+    fl = oracle.feature_loss(rec, tgt, atoms, anchor, f64(np.float32(0.1)), f64(np.float32(0.5)),
+                             f64(np.float32(lam["lambda_l2"])), f64(np.float32(lam["lambda_trust"])), True)
+    g = oracle.reconstruct_backward(q, att, atoms, proj, tau, fl["d_reconstructed"])
+    lf = f64(np.float32(5.0))
+    _, tg = oracle.trust_region_penalty(atoms, anchor, f64(np.float32(0.1)), want_grad=True)
+    return lf * g["d_proj"], lf * g["d_atoms"] + lf * f64(np.float32(lam["lambda_trust"])) * tg
+
+
 def test_session_objective_config0(ctx, cfg0):
     w = cfg0
     s = make_session(ctx, w)
@@ -267,10 +288,20 @@ def test_session_objective_config0(ctx, cfg0):
     gb = s.grad_buffer().cpu().numpy()
     n, ds = w.map.n, w.map.features.shape[1]
     offs = np.cumsum([0, 3 * n, 4 * n, 3 * n, 3 * n, n, ds * n, ds * w.proj.shape[1], w.atoms.size])
-    blocks = [g.positions, g.rotations, g.colors, g.log_scales, g.opacity_logits, g.features, dp, da]
-    names = list(oracle.FIELDS) + ["d_proj", "d_atoms"]
-    for i, (name, ref_b) in enumerate(zip(names, blocks)):
+    # map gradients: against the fp32 reference path (identical render decisions)
+    blocks = [g.positions, g.rotations, g.colors, g.log_scales, g.opacity_logits, g.features]
+    for i, (name, ref_b) in enumerate(zip(oracle.FIELDS, blocks)):
         assert_close_floor(gb[offs[i]:offs[i + 1]], ref_b.reshape(-1), 1e-3, name)
+    # dictionary gradients: sums over 76.8k rows; judged against the double-precision truth on the
+    # same rendered queries (the fp32 reference itself sits ~1e-3 away from it on small entries)
+    _, _, q_img, _ = s.frame_images(0)
+    tp, ta = dict_grads_f64(w, q_img.cpu().numpy(), w.lambdas)
+    assert_close_floor(gb[offs[6]:offs[7]], tp.reshape(-1), 1e-3, "d_proj")
+    assert_close_floor(gb[offs[7]:offs[8]], ta.reshape(-1), 1e-3, "d_atoms")
+    # and the fp32 reference agrees with the GPU norm-wise
+    for name, got, r in (("d_proj", gb[offs[6]:offs[7]], dp), ("d_atoms", gb[offs[7]:offs[8]], da)):
+        nrm = np.linalg.norm(got - r.reshape(-1)) / np.linalg.norm(r)
+        assert nrm < 1e-3, (name, nrm)
 
 
 def test_session_step_config0_adam(ctx, cfg0):
