@@ -225,6 +225,12 @@ latmap_status latmap_session_phase_times(latmap_session* s, double* ms, int64_t*
 /* Counters of the last objective: visible splats and tile pairs per frame (for roofline bytes). */
 latmap_status latmap_session_stats(latmap_session* s, int64_t* visible, int64_t* pairs);
 
+/* ---------------------------------------------------------------- self-test */
+/* One-tile tcgen05 GEMM, C[128 x n] = A[128 x k] * B[n x k]^T (device fp32 in/out, bf16 staging),
+ * with A / B staged K-major (0) or MN-major (1); pins the UMMA descriptor conventions. */
+latmap_status latmap_selftest_umma(latmap_ctx* ctx, const float* a, const float* b, float* c, int32_t n,
+                                   int32_t k, int32_t a_mn, int32_t b_mn);
+
 #ifdef __cplusplus
 }
 #endif

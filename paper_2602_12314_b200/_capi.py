@@ -126,6 +126,7 @@ def _declare(L):
         "latmap_session_frame_images": [P, C.c_int32, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(P)],
         "latmap_session_stats": [P, P, P],
         "latmap_session_profile": [P, C.c_int32],
+        "latmap_selftest_umma": [P, P, P, P, C.c_int32, C.c_int32, C.c_int32, C.c_int32],
         "latmap_session_phase_times": [P, P, P],
     }
     for name, args in sig.items():
@@ -150,7 +151,7 @@ EXPORTED = ["latmap_ctx_create", "latmap_ctx_destroy", "latmap_ctx_set_stream", 
             "latmap_session_set_batch", "latmap_session_set_slot_offset", "latmap_session_objective",
             "latmap_session_apply", "latmap_session_step", "latmap_session_grad_buffer", "latmap_session_loss_buffer",
             "latmap_session_read_loss", "latmap_session_frame_images", "latmap_session_stats",
-            "latmap_session_profile", "latmap_session_phase_times"]
+            "latmap_session_profile", "latmap_session_phase_times", "latmap_selftest_umma"]
 
 
 def check(ctx_handle, status):

@@ -724,8 +724,13 @@ latmap_status session_objective(latmap_session* s, bool want_grad) {
     const bool have_sup = f.n_sup > 0;
     if (have_sup) {
       s->begin(3);
-      decoder_frame(st, s->dec, s->query[b], f.assign, npx, f.feats, f.n_set, f.n_sup, atoms, proj, c.softmax_temp,
-                    c.lambda_cos, c.lambda_l2, c.lambda_feat * inv_b, want_grad, s->d_query, g_proj, g_atoms, part);
+      if (c.decoder_precision == 1 && decoder_tc_supported(s->k, s->ds, f.n_set))
+        decoder_frame_tc(st, s->dec, s->query[b], f.assign, npx, f.feats, f.n_set, f.n_sup, atoms, proj,
+                         c.softmax_temp, c.lambda_cos, c.lambda_l2, c.lambda_feat * inv_b, want_grad, s->d_query,
+                         g_proj, g_atoms, part);
+      else
+        decoder_frame(st, s->dec, s->query[b], f.assign, npx, f.feats, f.n_set, f.n_sup, atoms, proj, c.softmax_temp,
+                      c.lambda_cos, c.lambda_l2, c.lambda_feat * inv_b, want_grad, s->d_query, g_proj, g_atoms, part);
       s->end();
     }
     if (want_grad) {
@@ -846,6 +851,13 @@ latmap_status latmap_session_create(latmap_ctx* ctx, const latmap_config* cfg, i
          ok(cudaMalloc(&d.alpha_r, sizeof(float) * npx)) && ok(cudaMalloc(&d.beta_r, sizeof(float) * npx)) &&
          ok(cudaMalloc(&d.kd, sizeof(float) * k * ds)) && ok(cudaMalloc(&d.mm, sizeof(float) * k * k)) &&
          ok(cudaMalloc(&d.r, sizeof(float) * ds * k)) && ok(cudaMalloc(&d.a, sizeof(float) * k * k));
+  if (good && cfg->decoder_precision == 1) {
+    good = ok(cudaMalloc(&d.row_stats, sizeof(float) * 4 * npx)) &&
+           ok(cudaMalloc(&d.r_part, sizeof(float) * 148 * k * ds)) &&
+           ok(cudaMalloc(&d.a_part, sizeof(float) * 74 * 2 * k * (k / 2 + 1))) &&
+           ok(cudaMalloc(&d.bm_part, sizeof(float) * 74 * k * 64)) &&
+           ok(cudaMalloc(&d.loss_part, sizeof(double) * 148 * 4));
+  }
   if (!good) {
     t_err = "latmap_session_create: out of device memory";
     ctx->err = t_err;
@@ -874,7 +886,8 @@ latmap_status latmap_session_destroy(latmap_session* s) {
                   (void*)s->d_color, (void*)s->d_depth, (void*)s->d_query, (void*)s->ssim_scratch, (void*)s->partials,
                   (void*)s->d_loss, (void*)s->dec.buf1, (void*)s->dec.buf2, (void*)s->dec.alpha_r, (void*)s->dec.beta_r,
                   (void*)s->dec.kd, (void*)s->dec.mm, (void*)s->dec.gt, (void*)s->dec.nv, (void*)s->dec.r,
-                  (void*)s->dec.a, (void*)s->dec.bm})
+                  (void*)s->dec.a, (void*)s->dec.bm, (void*)s->dec.row_stats, (void*)s->dec.r_part,
+                  (void*)s->dec.a_part, (void*)s->dec.bm_part, (void*)s->dec.loss_part})
     if (p) cudaFree(p);
   for (auto& r : s->rw) r.release();
   for (auto* p : s->color) cudaFree(p);
@@ -1059,6 +1072,13 @@ latmap_status latmap_session_frame_images(latmap_session* s, int32_t b, float** 
   if (query) *query = s->query[b];
   if (alpha) *alpha = s->alpha[b];
   return LATMAP_OK;
+}
+
+latmap_status latmap_selftest_umma(latmap_ctx* ctx, const float* a, const float* b, float* c, int32_t n, int32_t k,
+                                   int32_t a_mn, int32_t b_mn) {
+  if (!ctx || !a || !b || !c) return LATMAP_ERR_INVALID_ARGUMENT;
+  if (umma_selftest(ctx->stream, a, b, c, n, k, a_mn, b_mn)) return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "bad shape");
+  return post_launch(ctx);
 }
 
 latmap_status latmap_session_profile(latmap_session* s, int32_t enable) {

@@ -356,6 +356,11 @@ void decoder_frame(cudaStream_t st, DecoderWork& w, const float* query, const in
   sgemm(st, false, false, ds, df, k, 1.f, w.r, k, atoms, df, 1.f, d_proj, df);
 }
 
+void decoder_target_norms(cudaStream_t st, const float* feats, int64_t n_set, int df, float* nv) {
+  row_norms_kernel<<<grid_for(n_set * 32, 256), 256, 0, st>>>(feats, n_set, df, nv);
+  count_launch();
+}
+
 void reconstruct(cudaStream_t st, const float* q, int64_t n, int ds, const float* atoms, const float* proj, int64_t k,
                  int df, float temperature, float* out, float* attention, float* scratch_qw) {
   // logits = (Q W) D^T / temperature (dictionary.cpp:37)

@@ -1,0 +1,608 @@
+// decoder_tc.cu — dictionary-attention decoder + feature loss + backward on 5th-gen tensor
+// cores (tcgen05.mma, bf16 operands, fp32 accumulators in TMEM), for K in {128, 256}.
+//
+// Reference semantics: reconstruct (proj/src/dictionary.cpp:25-53), feature_loss
+// (proj/src/losses.cpp:257-294), reconstruct_backward (dictionary.cpp:55-83) as assembled by
+// total_objective (proj/src/objective.cpp:100-185). Same factored algebra as decoder.cu:
+//
+//   S = Q Kd^T (Kd = D W^T),  P = softmax(S / tau),  t = P M (M = D D^T),
+//   nu^2 = P.t,  dot = P.G[a] (G = E D^T),  dF = alpha F_hat + beta F (per-row scalars),
+//   dS = P * (alpha t + beta G[a] - (alpha nu^2 + beta dot)) / tau,
+//   dQ = dS Kd,  R^T = dS^T Q,  A = P^T diag(alpha) P,  Bm = P^T Ohb (Ohb[r][s] = beta_r [a_r == s])
+//   d_atoms += A D + Bm E + R^T W,   d_proj += R D.
+//
+// DEC1 (persistent, 1 CTA / SM, 256 threads): per 128-pixel tile
+//   MMA1 S -> TMEM[0,K); softmax epilogue writes bf16 e = exp(S - max) to smem;
+//   MMA2 t = e M -> TMEM[K,2K); loss / alpha / beta epilogue; dS (bf16) overwrites e;
+//   MMA3 dQ = dS Kd -> TMEM[0,DS); MMA4 R^T = dS^T Q -> TMEM[DS, DS + DS*K/128);
+//   dQ rows go to HBM, R^T is accumulated in registers across tiles.
+// DEC2 (persistent, 128 threads, two roles = two column halves of A): recomputes P in
+//   128-column chunks from the stored row max / 1/sum and accumulates A[:, half] and Bm in TMEM.
+// Shared-memory operand tiles use the no-swizzle core-matrix layout of tc_common.cuh with
+// row-group stride 128 B and column-group stride 16 * rows B, so one tile serves as a K-major
+// operand (rows = M|N) and, transposed, as an MN-major operand (rows = K).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "tc_common.cuh"
+
+namespace lm {
+
+namespace {
+
+constexpr int kRows = 128;        // pixels per tile (UMMA M)
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Store 8 consecutive bf16 (cols c0..c0+7, c0 % 8 == 0) of row r into a core-matrix tile.
+__device__ __forceinline__ void st_row8(uint8_t* tile, int r, int c0, uint32_t col_stride, const float* v) {
+  uint4 u;
+  u.x = tc::pack_bf16(v[0], v[1]);
+  u.y = tc::pack_bf16(v[2], v[3]);
+  u.z = tc::pack_bf16(v[4], v[5]);
+  u.w = tc::pack_bf16(v[6], v[7]);
+  *reinterpret_cast<uint4*>(tile + tc::core_off(r, c0, 128u, col_stride)) = u;
+}
+
+// Load a row-major fp32 matrix [rows x cols] (cols % 8 == 0) into a bf16 core-matrix tile.
+__device__ __forceinline__ void load_tile_bf16(uint8_t* tile, const float* __restrict__ src, int rows, int cols,
+                                               int valid_rows, int tid, int nthr) {
+  const uint32_t cs = 16u * rows;
+  const int chunks = rows * (cols / 8);
+  for (int e = tid; e < chunks; e += nthr) {
+    const int r = e / (cols / 8), c0 = (e % (cols / 8)) * 8;
+    float v[8];
+    if (r < valid_rows) {
+      const float4 a = *reinterpret_cast<const float4*>(src + (size_t)r * cols + c0);
+      const float4 b = *reinterpret_cast<const float4*>(src + (size_t)r * cols + c0 + 4);
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = 0.f;
+    }
+    st_row8(tile, r, c0, cs, v);
+  }
+}
+
+struct Dec1Args {
+  const float* query;       // npx x DS (fp32, raster order)
+  const int32_t* assign;    // npx
+  const float* kd;          // K x DS fp32 (D W^T)
+  const float* mm;          // K x K  fp32 (D D^T)
+  const float* gt;          // n_set x K fp32 (E D^T)
+  const float* nv;          // n_set (target row norms)
+  int64_t npx;
+  float inv_temp, lambda_cos, lambda_l2, inv_nsup, scale;
+  float* d_query;           // npx x DS
+  float4* row_stats;        // npx: (max S, 1/sum, alpha, beta)
+  float* r_part;            // gridDim x K x DS
+  double* loss_part;        // gridDim x 4
+  int want_grad;
+};
+
+template <int K, int DS>
+__global__ void __launch_bounds__(256, 1) dec1_kernel(Dec1Args a) {
+  constexpr int kTmemCols = 2 * K <= 256 ? 256 : 512;
+  constexpr int MH = K / 128;  // M halves of R^T
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sQ = smem;                              // 128 x DS
+  uint8_t* sKd = sQ + kRows * DS * 2;              // K x DS
+  uint8_t* sP = sKd + K * DS * 2;                  // 128 x K  (e, then dS)
+  uint8_t* sM = sP + kRows * K * 2;                // K x K
+  float* s_red = reinterpret_cast<float*>(sM + K * K * 2);  // [8][128]: max, sum, nu2, dot (x2 halves)
+  __shared__ uint64_t bar[3];
+  __shared__ uint32_t s_taddr;
+  __shared__ double s_loss[8][3];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = warp & 3, h = warp >> 2;  // TMEM lane group, column half
+  const int row = 32 * g + lane;
+  constexpr int HC = K / 2;               // columns per half
+
+  // resident operands: Kd (K x DS) and M (K x K)
+  load_tile_bf16(sKd, a.kd, K, DS, K, tid, 256);
+  load_tile_bf16(sM, a.mm, K, K, K, tid, 256);
+  if (tid == 0) {
+    for (int i = 0; i < 3; ++i) tc::mbar_init(&bar[i], 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc<kTmemCols>(&s_taddr);
+  tc::fence_async_smem();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = s_taddr;
+  const uint32_t tl = tmem + ((uint32_t)(32 * g) << 16);  // this warp's TMEM lane base
+  uint32_t ph[3] = {0, 0, 0};
+
+  const uint32_t idesc1 = tc::make_idesc_bf16(128, K, 0, 0);
+  const uint32_t idesc3 = tc::make_idesc_bf16(128, DS, 0, 1);
+  const uint32_t idesc4 = tc::make_idesc_bf16(128, DS, 1, 1);
+  const uint32_t aQ = tc::smem_u32(sQ), aKd = tc::smem_u32(sKd), aP = tc::smem_u32(sP), aM = tc::smem_u32(sM);
+  const float cl = kLog2e * a.inv_temp;
+
+  float racc[MH * DS];  // R^T rows (k = row, row + 128) for warps 4..7
+#pragma unroll
+  for (int i = 0; i < MH * DS; ++i) racc[i] = 0.f;
+  double cos_acc = 0.0, l2_acc = 0.0, zflag = 0.0;
+
+  const int64_t ntiles = (a.npx + kRows - 1) / kRows;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * kRows;
+    const int valid = (int)(a.npx - r0 < kRows ? a.npx - r0 : kRows);
+    load_tile_bf16(sQ, a.query + r0 * DS, kRows, DS, valid, tid, 256);
+    tc::fence_async_smem();
+    __syncthreads();
+    // ---- MMA1: S = Q Kd^T  -> TMEM[0, K)
+    if (tid == 0) {
+      tc::tc_fence_after();
+#pragma unroll
+      for (int ks = 0; ks < DS / 16; ++ks)
+        tc::mma_bf16(tmem, tc::make_sdesc(aQ + ks * 2 * 2048, 2048, 128),
+                     tc::make_sdesc(aKd + ks * 2 * (16 * K), 16 * K, 128), idesc1, ks > 0);
+      tc::mma_commit(&bar[0]);
+    }
+    tc::mbar_wait(&bar[0], ph[0]);
+    ph[0] ^= 1;
+    tc::tc_fence_after();
+    // ---- softmax: row max over both halves
+    float mx = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < HC; c += 32) {
+      float v[32];
+      tc::tmem_ld32(tl + h * HC + c, v);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) mx = fmaxf(mx, v[i]);
+    }
+    s_red[(0 * 2 + h) * 128 + row] = mx;
+    __syncthreads();
+    mx = fmaxf(s_red[row], s_red[128 + row]);
+    const float mxl = mx * cl;
+    float sum = 0.f;
+#pragma unroll
+    for (int c = 0; c < HC; c += 32) {
+      float v[32];
+      tc::tmem_ld32(tl + h * HC + c, v);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        v[i] = ex2(fmaf(v[i], cl, -mxl));
+        sum += v[i];
+      }
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) st_row8(sP, row, h * HC + c + i, 16u * kRows, v + i);
+    }
+    s_red[(1 * 2 + h) * 128 + row] = sum;
+    tc::fence_async_smem();
+    tc::tc_fence_before();
+    __syncthreads();
+    const float inv_sum = 1.f / (s_red[2 * 128 + row] + s_red[3 * 128 + row]);
+    // ---- MMA2: t = e M -> TMEM[K, 2K)
+    if (tid == 0) {
+      tc::tc_fence_after();
+#pragma unroll 4
+      for (int ks = 0; ks < K / 16; ++ks)
+        tc::mma_bf16(tmem + K, tc::make_sdesc(aP + ks * 2 * 2048, 2048, 128),
+                     tc::make_sdesc(aM + ks * 2 * (16 * K), 16 * K, 128), tc::make_idesc_bf16(128, K, 0, 0), ks > 0);
+      tc::mma_commit(&bar[1]);
+    }
+    tc::mbar_wait(&bar[1], ph[1]);
+    ph[1] ^= 1;
+    tc::tc_fence_after();
+    // ---- per-row statistics: nu^2 = P.t, dot = P.G[a]
+    const int64_t grow = r0 + row;
+    const int32_t asg = row < valid ? a.assign[grow] : -1;
+    const float* grow_ptr = a.gt + (int64_t)(asg < 0 ? 0 : asg) * K;
+    float nu2 = 0.f, dot = 0.f;
+#pragma unroll
+    for (int c = 0; c < HC; c += 32) {
+      float s[32], t[32];
+      tc::tmem_ld32(tl + h * HC + c, s);
+      tc::tmem_ld32(tl + K + h * HC + c, t);
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        const float4 gg = __ldg(reinterpret_cast<const float4*>(grow_ptr + h * HC + c + i));
+        const float gv[4] = {gg.x, gg.y, gg.z, gg.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float p = ex2(fmaf(s[i + j], cl, -mxl)) * inv_sum;
+          nu2 = fmaf(p, t[i + j] * inv_sum, nu2);
+          dot = fmaf(p, gv[j], dot);
+        }
+      }
+    }
+    s_red[(2 * 2 + h) * 128 + row] = nu2;
+    s_red[(3 * 2 + h) * 128 + row] = dot;
+    __syncthreads();
+    nu2 = s_red[4 * 128 + row] + s_red[5 * 128 + row];
+    dot = s_red[6 * 128 + row] + s_red[7 * 128 + row];
+    float al = 0.f, be = 0.f, cc = 0.f;
+    if (asg >= 0) {
+      const float eps = 1e-8f;
+      const float nu = sqrtf(fmaxf(nu2, 0.f)), vn = a.nv[asg];
+      const float nug = fmaxf(nu, eps), nvg = fmaxf(vn, eps);
+      if (h == 0) {
+        if (nu < eps || vn < eps) zflag = 1.0;
+        cos_acc += 1.0 - (double)(dot / (nug * nvg));
+        l2_acc += (double)nu2 - 2.0 * (double)dot + (double)vn * (double)vn;
+      }
+      al = a.scale * (a.lambda_cos * dot / (nug * nug * nug * nvg) * a.inv_nsup + 2.f * a.lambda_l2 * a.inv_nsup);
+      be = a.scale * (-a.lambda_cos / (nug * nvg) * a.inv_nsup - 2.f * a.lambda_l2 * a.inv_nsup);
+      cc = al * nu2 + be * dot;
+    }
+    if (h == 0 && row < valid) a.row_stats[grow] = make_float4(mx, inv_sum, al, be);
+    if (!a.want_grad) {
+      tc::tc_fence_before();
+      __syncthreads();
+      continue;
+    }
+    // ---- dS = P (al t + be g - c) / tau  (bf16, overwrites e in sP)
+#pragma unroll
+    for (int c = 0; c < HC; c += 32) {
+      float s[32], t[32];
+      tc::tmem_ld32(tl + h * HC + c, s);
+      tc::tmem_ld32(tl + K + h * HC + c, t);
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        const float4 gg = __ldg(reinterpret_cast<const float4*>(grow_ptr + h * HC + c + i));
+        const float gv[4] = {gg.x, gg.y, gg.z, gg.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float p = ex2(fmaf(s[i + j], cl, -mxl)) * inv_sum;
+          s[i + j] = p * (al * (t[i + j] * inv_sum) + be * gv[j] - cc) * a.inv_temp;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) st_row8(sP, row, h * HC + c + i, 16u * kRows, s + i);
+    }
+    tc::fence_async_smem();
+    tc::tc_fence_before();
+    __syncthreads();
+    // ---- MMA3: dQ = dS Kd -> TMEM[0, DS);  MMA4: R^T = dS^T Q -> TMEM[DS + DS*mh, ...)
+    if (tid == 0) {
+      tc::tc_fence_after();
+#pragma unroll 4
+      for (int ks = 0; ks < K / 16; ++ks)
+        tc::mma_bf16(tmem, tc::make_sdesc(aP + ks * 2 * 2048, 2048, 128),
+                     tc::make_sdesc(aKd + ks * 2 * 128, 128, 16 * K), idesc3, ks > 0);
+#pragma unroll
+      for (int mh = 0; mh < MH; ++mh)
+#pragma unroll
+        for (int ks = 0; ks < kRows / 16; ++ks)
+          tc::mma_bf16(tmem + DS + DS * mh, tc::make_sdesc(aP + mh * 16 * 2048 + ks * 2 * 128, 128, 2048),
+                       tc::make_sdesc(aQ + ks * 2 * 128, 128, 2048), idesc4, ks > 0);
+      tc::mma_commit(&bar[2]);
+    }
+    tc::mbar_wait(&bar[2], ph[2]);
+    ph[2] ^= 1;
+    tc::tc_fence_after();
+    if (h == 0) {
+      float v[DS];
+#pragma unroll
+      for (int c = 0; c < DS; c += 16) tc::tmem_ld16(tl + c, v + c);  // warp-aligned: all lanes load
+      if (row < valid) {
+        float4* dst = reinterpret_cast<float4*>(a.d_query + grow * DS);
+#pragma unroll
+        for (int c = 0; c < DS; c += 4) dst[c / 4] = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+      }
+    } else {
+#pragma unroll
+      for (int mh = 0; mh < MH; ++mh) {
+        float v[DS];
+#pragma unroll
+        for (int c = 0; c < DS; c += 16) tc::tmem_ld16(tl + DS + DS * mh + c, v + c);
+#pragma unroll
+        for (int c = 0; c < DS; ++c) racc[mh * DS + c] += v[c];
+      }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+  }
+  // ---- flush per-CTA partials
+  if (h == 1) {
+#pragma unroll
+    for (int mh = 0; mh < MH; ++mh) {
+      float* dst = a.r_part + ((size_t)blockIdx.x * K + mh * 128 + row) * DS;
+#pragma unroll
+      for (int c = 0; c < DS; ++c) dst[c] = racc[mh * DS + c];
+    }
+  }
+  cos_acc = warp_sum_d(cos_acc);
+  l2_acc = warp_sum_d(l2_acc);
+  zflag = warp_sum_d(zflag);
+  if (lane == 0) {
+    s_loss[warp][0] = cos_acc;
+    s_loss[warp][1] = l2_acc;
+    s_loss[warp][2] = zflag;
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (tid == 0) {
+    double c0 = 0, c1 = 0, c2 = 0;
+    for (int w = 0; w < 8; ++w) c0 += s_loss[w][0], c1 += s_loss[w][1], c2 += s_loss[w][2];
+    a.loss_part[blockIdx.x * 4 + 0] = c0;
+    a.loss_part[blockIdx.x * 4 + 1] = c1;
+    a.loss_part[blockIdx.x * 4 + 2] = c2;
+  }
+  if (warp == 0) tc::tmem_free<kTmemCols>(tmem);
+}
+
+struct Dec2Args {
+  const float* query;
+  const int32_t* assign;
+  const float* kd;
+  const float4* row_stats;
+  int64_t npx;
+  float inv_temp;
+  int n_set;
+  float* a_part;   // (gridDim/2) x 2 roles x K x (K/2)
+  float* bm_part;  // (gridDim/2) x K x 64  (role 0 only)
+};
+
+template <int K, int DS>
+__global__ void __launch_bounds__(128, 1) dec2_kernel(Dec2Args a) {
+  constexpr int MH = K / 128, NH = K / 2, NB = 64;
+  constexpr int kColA = 128, kColB = 128 + MH * NH;
+  constexpr int kTmemCols = kColB + MH * NB <= 256 ? 256 : 512;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sQ = smem;                    // 128 x DS
+  uint8_t* sKd = sQ + kRows * DS * 2;    // K x DS
+  uint8_t* sP = sKd + K * DS * 2;        // 128 x K
+  uint8_t* sAP = sP + kRows * K * 2;     // 128 x NH
+  uint8_t* sOh = sAP + kRows * NH * 2;   // 128 x NB
+  __shared__ uint64_t bar[2];
+  __shared__ uint32_t s_taddr;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int role = blockIdx.x & 1, group = blockIdx.x >> 1, ngroups = gridDim.x >> 1;
+  load_tile_bf16(sKd, a.kd, K, DS, K, tid, 128);
+  if (tid == 0) {
+    tc::mbar_init(&bar[0], 1);
+    tc::mbar_init(&bar[1], 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc<kTmemCols>(&s_taddr);
+  tc::fence_async_smem();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = s_taddr;
+  const uint32_t tl = tmem + ((uint32_t)(32 * warp) << 16);
+  uint32_t ph[2] = {0, 0};
+  const uint32_t aQ = tc::smem_u32(sQ), aKd = tc::smem_u32(sKd), aP = tc::smem_u32(sP), aAP = tc::smem_u32(sAP),
+                 aOh = tc::smem_u32(sOh);
+  const float cl = kLog2e * a.inv_temp;
+  const int64_t ntiles = (a.npx + kRows - 1) / kRows;
+  bool first = true;
+  for (int64_t tile = group; tile < ntiles; tile += ngroups) {
+    const int64_t r0 = tile * kRows;
+    const int valid = (int)(a.npx - r0 < kRows ? a.npx - r0 : kRows);
+    load_tile_bf16(sQ, a.query + r0 * DS, kRows, DS, valid, tid, 128);
+    const int row = tid;
+    float4 st = make_float4(0.f, 0.f, 0.f, 0.f);
+    int32_t asg = -1;
+    if (row < valid) {
+      st = a.row_stats[r0 + row];
+      asg = a.assign[r0 + row];
+    }
+    const float mxl = st.x * cl, inv_sum = st.y, al = st.z, be = st.w;
+    for (int ch = 0; ch < MH; ++ch) {
+      tc::fence_async_smem();
+      tc::tc_fence_before();
+      __syncthreads();
+      if (tid == 0) {
+        tc::tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < DS / 16; ++ks)
+          tc::mma_bf16(tmem, tc::make_sdesc(aQ + ks * 2 * 2048, 2048, 128),
+                       tc::make_sdesc(aKd + ch * 2048 + ks * 2 * (16 * K), 16 * K, 128),
+                       tc::make_idesc_bf16(128, 128, 0, 0), ks > 0);
+        tc::mma_commit(&bar[0]);
+      }
+      tc::mbar_wait(&bar[0], ph[0]);
+      ph[0] ^= 1;
+      tc::tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 128; c += 32) {
+        float v[32], w[32];
+        tc::tmem_ld32(tl + c, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          v[i] = row < valid ? ex2(fmaf(v[i], cl, -mxl)) * inv_sum : 0.f;
+          w[i] = al * v[i];
+        }
+        const int k0 = ch * 128 + c;
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) st_row8(sP, row, k0 + i, 16u * kRows, v + i);
+        if (k0 >= role * NH && k0 < (role + 1) * NH) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) st_row8(sAP, row, k0 - role * NH + i, 16u * kRows, w + i);
+        }
+      }
+    }
+    if (role == 0) {
+#pragma unroll
+      for (int c = 0; c < NB; c += 8) {
+        float v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = (asg == c + i) ? be : 0.f;
+        st_row8(sOh, row, c, 16u * kRows, v);
+      }
+    }
+    tc::fence_async_smem();
+    tc::tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc::tc_fence_after();
+      for (int mh = 0; mh < MH; ++mh) {
+#pragma unroll
+        for (int ks = 0; ks < kRows / 16; ++ks)
+          tc::mma_bf16(tmem + kColA + mh * NH, tc::make_sdesc(aP + mh * 16 * 2048 + ks * 2 * 128, 128, 2048),
+                       tc::make_sdesc(aAP + ks * 2 * 128, 128, 2048), tc::make_idesc_bf16(128, NH, 1, 1),
+                       (!first) || ks > 0);
+        if (role == 0) {
+#pragma unroll
+          for (int ks = 0; ks < kRows / 16; ++ks)
+            tc::mma_bf16(tmem + kColB + mh * NB, tc::make_sdesc(aP + mh * 16 * 2048 + ks * 2 * 128, 128, 2048),
+                         tc::make_sdesc(aOh + ks * 2 * 128, 128, 2048), tc::make_idesc_bf16(128, NB, 1, 1),
+                         (!first) || ks > 0);
+        }
+      }
+      tc::mma_commit(&bar[1]);
+    }
+    tc::mbar_wait(&bar[1], ph[1]);
+    ph[1] ^= 1;
+    tc::tc_fence_after();
+    first = false;
+  }
+  // drain: lane `row` of half mh holds A[mh*128 + row][role*NH + c], Bm[mh*128 + row][c]
+  const int row = tid;
+  for (int mh = 0; mh < MH; ++mh) {
+    float* dst = a.a_part + (((size_t)group * 2 + role) * K + mh * 128 + row) * NH;
+    for (int c = 0; c < NH; c += 16) {
+      float v[16];
+      if (first) {
+        for (int i = 0; i < 16; ++i) v[i] = 0.f;
+      } else {
+        tc::tmem_ld16(tl + kColA + mh * NH + c, v);
+      }
+      for (int i = 0; i < 16; ++i) dst[c + i] = v[i];
+    }
+    if (role == 0) {
+      float* db = a.bm_part + ((size_t)group * K + mh * 128 + row) * NB;
+      for (int c = 0; c < NB; c += 16) {
+        float v[16];
+        if (first) {
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        } else {
+          tc::tmem_ld16(tl + kColB + mh * NB + c, v);
+        }
+        for (int i = 0; i < 16; ++i) db[c + i] = v[i];
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free<kTmemCols>(tmem);
+}
+
+// Sum the per-CTA partials: A (K x K) from (groups x 2 roles x K x K/2), Bm^T (n_set x K) from
+// (groups x K x 64), R^T (K x DS) -> R (DS x K), loss partials -> frame partial slots.
+__global__ void dec_reduce_kernel(const float* a_part, const float* bm_part, const float* r_part,
+                                  const double* loss_part, int K, int DS, int n_set, int groups1, int groups2,
+                                  float* A, float* bmt, float* R, double* partials) {
+  const int64_t total_a = (int64_t)K * K, total_b = (int64_t)n_set * K, total_r = (int64_t)K * DS;
+  const int NH = K / 2;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total_a + total_b + total_r + 3;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (e < total_a) {
+      const int i = (int)(e / K), j = (int)(e % K);
+      const int role = j / NH, jj = j % NH;
+      float s = 0.f;
+      for (int gi = 0; gi < groups2; ++gi) s += a_part[(((size_t)gi * 2 + role) * K + i) * NH + jj];
+      A[e] = s;
+    } else if (e < total_a + total_b) {
+      const int64_t f = e - total_a;
+      const int sidx = (int)(f / K), k = (int)(f % K);
+      float s = 0.f;
+      for (int gi = 0; gi < groups2; ++gi) s += bm_part[((size_t)gi * K + k) * 64 + sidx];
+      bmt[f] = s;
+    } else if (e < total_a + total_b + total_r) {
+      const int64_t f = e - total_a - total_b;
+      const int s_ = (int)(f / K), k = (int)(f % K);
+      float s = 0.f;
+      for (int gi = 0; gi < groups1; ++gi) s += r_part[((size_t)gi * K + k) * DS + s_];
+      R[f] = s;
+    } else {
+      const int which = (int)(e - total_a - total_b - total_r);
+      double s = 0.0;
+      for (int gi = 0; gi < groups1; ++gi) s += loss_part[gi * 4 + which];
+      if (which == 2)
+        partials[6] = fmax(partials[6], s > 0.0 ? 1.0 : 0.0);
+      else
+        partials[4 + which] += s;
+    }
+  }
+}
+
+template <int K, int DS>
+void launch_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_t* assignment, int64_t npx,
+               const float* feats, int64_t n_set, int64_t n_sup, float temperature, float lambda_cos, float lambda_l2,
+               float scale, bool want_grad, float* d_query, double* partials) {
+  const int g1 = 148;
+  const int g2 = 148;  // 74 groups x 2 roles
+  Dec1Args d1{query, assignment, w.kd, w.mm, w.gt, w.nv, npx, 1.f / temperature, lambda_cos, lambda_l2,
+              n_sup > 0 ? 1.f / (float)n_sup : 0.f, scale, d_query, reinterpret_cast<float4*>(w.row_stats),
+              w.r_part, w.loss_part, want_grad ? 1 : 0};
+  const size_t sm1 = (size_t)kRows * DS * 2 + (size_t)K * DS * 2 + (size_t)kRows * K * 2 + (size_t)K * K * 2 +
+                     8 * 128 * 4;
+  static bool attr1 = false;
+  if (!attr1) {
+    cudaFuncSetAttribute(dec1_kernel<K, DS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+    attr1 = true;
+  }
+  dec1_kernel<K, DS><<<g1, 256, sm1, st>>>(d1);
+  count_launch();
+  if (!want_grad) {
+    dec_reduce_kernel<<<1, 32, 0, st>>>(nullptr, nullptr, nullptr, w.loss_part, K, DS, 0, g1, 0, nullptr, nullptr,
+                                        nullptr, partials);
+    count_launch();
+    return;
+  }
+  Dec2Args d2{query, assignment, w.kd, reinterpret_cast<const float4*>(w.row_stats), npx, 1.f / temperature,
+              (int)n_set, w.a_part, w.bm_part};
+  const size_t sm2 = (size_t)kRows * DS * 2 + (size_t)K * DS * 2 + (size_t)kRows * K * 2 + (size_t)kRows * (K / 2) * 2 +
+                     (size_t)kRows * 64 * 2;
+  static bool attr2 = false;
+  if (!attr2) {
+    cudaFuncSetAttribute(dec2_kernel<K, DS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+    attr2 = true;
+  }
+  dec2_kernel<K, DS><<<g2, 128, sm2, st>>>(d2);
+  count_launch();
+  const int64_t tot = (int64_t)K * K + n_set * K + (int64_t)K * DS + 3;
+  dec_reduce_kernel<<<(unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 8), 256, 0, st>>>(
+      w.a_part, w.bm_part, w.r_part, w.loss_part, K, DS, (int)n_set, g1, g2 / 2, w.a, w.bm, w.r, partials);
+  count_launch();
+}
+
+}  // namespace
+
+bool decoder_tc_supported(int64_t k, int ds, int64_t n_set) {
+  return (k == 128 || k == 256) && ds == 32 && n_set <= 64;
+}
+
+size_t decoder_tc_scratch_floats(int64_t k, int ds, int64_t npx) {
+  // row_stats (4/row) + r_part + a_part + bm_part + loss_part (as floats x2)
+  return (size_t)npx * 4 + 148 * (size_t)k * ds + 74 * 2 * (size_t)k * (k / 2) + 74 * (size_t)k * 64 + 148 * 4 * 2;
+}
+
+void decoder_frame_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_t* assignment, int64_t npx,
+                      const float* feats, int64_t n_set, int64_t n_sup, const float* atoms, const float* proj,
+                      float temperature, float lambda_cos, float lambda_l2, float scale, bool want_grad, float* d_query,
+                      float* d_proj, float* d_atoms, double* partials) {
+  const int64_t k = w.k;
+  const int ds = w.ds, df = w.df;
+  // per-frame target scores G^T = E D^T and norms (tiny SIMT GEMMs)
+  sgemm(st, false, true, n_set, k, df, 1.f, feats, df, atoms, df, 0.f, w.gt, k);
+  decoder_target_norms(st, feats, n_set, df, w.nv);
+  if (k == 256)
+    launch_tc<256, 32>(st, w, query, assignment, npx, feats, n_set, n_sup, temperature, lambda_cos, lambda_l2, scale,
+                       want_grad, d_query, partials);
+  else
+    launch_tc<128, 32>(st, w, query, assignment, npx, feats, n_set, n_sup, temperature, lambda_cos, lambda_l2, scale,
+                       want_grad, d_query, partials);
+  if (!want_grad) return;
+  // d_atoms += A D + Bm E + R^T W ;  d_proj += R D   (R stored ds x K)
+  sgemm(st, false, false, k, df, k, 1.f, w.a, k, atoms, df, 1.f, d_atoms, df);
+  sgemm(st, true, false, k, df, n_set, 1.f, w.bm, k, feats, df, 1.f, d_atoms, df);
+  sgemm(st, true, false, k, df, ds, 1.f, w.r, k, proj, df, 1.f, d_atoms, df);
+  sgemm(st, false, false, ds, df, k, 1.f, w.r, k, atoms, df, 1.f, d_proj, df);
+}
+
+}  // namespace lm

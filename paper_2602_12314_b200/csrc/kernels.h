@@ -84,6 +84,12 @@ struct DecoderWork {
   float *a = nullptr;    // K x K    (P^T diag(alpha) P)
   float *bm = nullptr;   // n_set x K (Bm^T)
   int64_t nset_cap = 0;
+  // tcgen05 path scratch (decoder_tc.cu)
+  float* row_stats = nullptr;  // npx x 4: max S, 1/sum, alpha, beta
+  float* r_part = nullptr;     // 148 x K x ds
+  float* a_part = nullptr;     // 74 x 2 x K x K/2
+  float* bm_part = nullptr;    // 74 x K x 64
+  double* loss_part = nullptr; // 148 x 4
 };
 void decoder_prepare(cudaStream_t st, DecoderWork& w, const float* atoms, const float* proj);
 // Fused feature loss + decoder backward for one frame (pixel mode). Accumulates into d_proj,
@@ -92,6 +98,13 @@ void decoder_frame(cudaStream_t st, DecoderWork& w, const float* query, const in
                    int64_t npx, const float* feats, int64_t n_set, int64_t n_sup, const float* atoms,
                    const float* proj, float temperature, float lambda_cos, float lambda_l2, float scale,
                    bool want_grad, float* d_query, float* d_proj, float* d_atoms, double* partials);
+void decoder_target_norms(cudaStream_t st, const float* feats, int64_t n_set, int df, float* nv);
+// tcgen05 / TMEM path (bf16 operands, fp32 accumulation) for K in {128, 256}, d_s = 32, n_set <= 64.
+bool decoder_tc_supported(int64_t k, int ds, int64_t n_set);
+void decoder_frame_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_t* assignment,
+                      int64_t npx, const float* feats, int64_t n_set, int64_t n_sup, const float* atoms,
+                      const float* proj, float temperature, float lambda_cos, float lambda_l2, float scale,
+                      bool want_grad, float* d_query, float* d_proj, float* d_atoms, double* partials);
 void reconstruct(cudaStream_t st, const float* q, int64_t n, int ds, const float* atoms, const float* proj,
                  int64_t k, int df, float temperature, float* out, float* attention, float* scratch_qw);
 void reconstruct_backward(cudaStream_t st, const float* q, const float* att, int64_t n, int ds,
@@ -110,6 +123,8 @@ struct AdamBlock {
 void adam_flat(cudaStream_t st, float* param, const float* grad, float* m, float* v, const AdamBlock* blocks,
                int nblocks, int64_t* steps, int64_t* skipped, const float* corr1, const float* corr2,
                int32_t table_len, int32_t* flags, const int64_t* overflow);
+
+int umma_selftest(cudaStream_t st, const float* A, const float* B, float* C, int N, int K, int a_mn, int b_mn);
 
 void set_launch_counter(int64_t* c);
 void count_launch(int n = 1);

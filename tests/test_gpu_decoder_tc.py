@@ -1,0 +1,59 @@
+"""tcgen05 (bf16, TMEM) decoder against the fp32 decoder path (itself pinned to the oracle in
+test_gpu_parity.py) on configs 1 and 2 shapes. bf16 bars (BASELINE north_star): loss terms
+within 2e-3 relative, decoder gradients norm-wise within 1e-2, cosine >= 0.999."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2602_12314_b200 import api, synthetic  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return api.Context(0)
+
+
+def gpu_render(ctx):
+    def fn(m, q, t, intr):
+        out = api.render(ctx, api.GaussianMap.from_numpy(m), api.make_pose(q, t),
+                         api.make_intrinsics(intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height))
+        return out.color.cpu().numpy(), out.depth.cpu().numpy(), out.alpha.cpu().numpy()
+    return fn
+
+
+def run(ctx, w, precision):
+    cfg = api.default_config(**w.lambdas)
+    cfg.decoder_precision = precision
+    intr = api.make_intrinsics(w.intr.fx, w.intr.fy, w.intr.cx, w.intr.cy, w.intr.width, w.intr.height)
+    s = api.Session(ctx, cfg, w.map.n, w.map.features.shape[1], w.atoms.shape[0], w.atoms.shape[1], intr)
+    s.set_map(w.map)
+    s.set_dictionary(w.atoms, w.anchor, w.proj)
+    s.set_frames(w.frames)
+    s.set_batch(len(w.frames))
+    loss = s.objective(want_grad=True)
+    return loss, s.grad_buffer().cpu().numpy().copy(), s
+
+
+def cosine(a, b):
+    return float(np.dot(a, b) / (np.linalg.norm(a) * np.linalg.norm(b) + 1e-30))
+
+
+@pytest.mark.parametrize("cfg_id,scale", [(1, 0.5), (2, 0.25)])
+def test_tc_decoder_matches_fp32(ctx, cfg_id, scale):
+    w = synthetic.make_workload(cfg_id, gpu_render(ctx), scale=scale)
+    l32, g32, s32 = run(ctx, w, 0)
+    ltc, gtc, stc = run(ctx, w, 1)
+    for k in ("l_cos", "l_l2", "total"):
+        assert ltc[k] == pytest.approx(l32[k], rel=2e-3, abs=1e-5), (k, ltc[k], l32[k])
+    n, ds = w.map.n, w.map.features.shape[1]
+    K, D = w.atoms.shape
+    offs = np.cumsum([0, 3 * n, 4 * n, 3 * n, 3 * n, n, ds * n, ds * D, K * D])
+    names = ["positions", "rotations", "colors", "log_scales", "opacity", "features", "d_proj", "d_atoms"]
+    for i, name in enumerate(names):
+        a, b = gtc[offs[i]:offs[i + 1]], g32[offs[i]:offs[i + 1]]
+        rel = np.linalg.norm(a - b) / (np.linalg.norm(b) + 1e-30)
+        assert cosine(a, b) >= 0.999 and rel <= 2e-2, (name, rel, cosine(a, b))
