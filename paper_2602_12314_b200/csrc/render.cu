@@ -197,19 +197,46 @@ __global__ void __launch_bounds__(1024) scan_tiles_kernel(const int32_t* __restr
   }
 }
 
-// K3: scatter (depth_bits << 32 | source) keys into their tile buckets.
+// K3: scatter (depth_bits << 32 | source) keys into their tile buckets. Each block first
+// counts its pairs per tile in shared memory, reserves one contiguous range per (block, tile)
+// with a single global atomic, then fills it (slot order inside a bucket is irrelevant: the
+// per-tile sort below makes the list canonical).
+constexpr int kScatterPerThread = 8;
 __global__ void __launch_bounds__(256) scatter_kernel(const SplatRec* __restrict__ rec, int64_t n, int tiles_x,
-                                                      int32_t* cursor, uint64_t* __restrict__ keys,
+                                                      int ntiles, int32_t* cursor, uint64_t* __restrict__ keys,
                                                       int64_t pair_cap) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+  extern __shared__ int32_t s_cnt[];
+  int32_t* s_base = s_cnt + ntiles;
+  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s_cnt[t] = 0;
+  __syncthreads();
+  const int64_t b0 = (int64_t)blockIdx.x * blockDim.x * kScatterPerThread;
+#pragma unroll 1
+  for (int r = 0; r < kScatterPerThread; ++r) {
+    const int64_t i = b0 + (int64_t)r * blockDim.x + threadIdx.x;
+    if (i >= n) break;
     const int4 bb = reinterpret_cast<const int4*>(rec + i)[2];
     if (bb.x > bb.y) continue;
-    const float depth = rec[i].depth;
-    const uint64_t key = ((uint64_t)__float_as_uint(depth) << 32) | (uint32_t)i;
-    const int tx0 = bb.x / kTile, tx1 = bb.y / kTile, ty0 = bb.z / kTile, ty1 = bb.w / kTile;
-    for (int ty = ty0; ty <= ty1; ++ty)
-      for (int tx = tx0; tx <= tx1; ++tx) {
-        const int pos = atomicAdd(&cursor[ty * tiles_x + tx], 1);
+    for (int ty = bb.z / kTile; ty <= bb.w / kTile; ++ty)
+      for (int tx = bb.x / kTile; tx <= bb.y / kTile; ++tx) atomicAdd(&s_cnt[ty * tiles_x + tx], 1);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
+    const int c = s_cnt[t];
+    if (c) s_base[t] = atomicAdd(&cursor[t], c);
+    s_cnt[t] = 0;
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int r = 0; r < kScatterPerThread; ++r) {
+    const int64_t i = b0 + (int64_t)r * blockDim.x + threadIdx.x;
+    if (i >= n) break;
+    const int4 bb = reinterpret_cast<const int4*>(rec + i)[2];
+    if (bb.x > bb.y) continue;
+    const uint64_t key = ((uint64_t)__float_as_uint(rec[i].depth) << 32) | (uint32_t)i;
+    for (int ty = bb.z / kTile; ty <= bb.w / kTile; ++ty)
+      for (int tx = bb.x / kTile; tx <= bb.y / kTile; ++tx) {
+        const int t = ty * tiles_x + tx;
+        const int64_t pos = (int64_t)s_base[t] + atomicAdd(&s_cnt[t], 1);
         if (pos < pair_cap) keys[pos] = key;
       }
   }
@@ -414,27 +441,57 @@ struct RasterBwdArgs {
   float* g_feat;   // N x ds
 };
 
-constexpr int kBwdBatch = 64;
+constexpr int kBwdBatch = 16;  // splats per batch (one MMA M tile)
 
-// K8: reverse sweep of render_backward (render.cpp:315-353). Transmittance before each
-// blended splat is recovered by division from the forward's final T; per-splat
-// gradients are reduced warp-wise, then across the CTA in shared memory, then added
-// with one global atomic per (tile, splat, value).
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+  hi = to_tf32(x);
+  lo = to_tf32(x - __uint_as_float(hi));
+}
+// D += A * B, m16n8k8, tf32 inputs, fp32 accumulate (legacy warp MMA, used for small in-kernel reductions)
+__device__ __forceinline__ void mma_tf32(float* d, const uint32_t* a, const uint32_t* b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+// K8: reverse sweep of render_backward (render.cpp:315-353), one CTA per 16x16 tile, one
+// thread per pixel. Transmittance before each blended splat is recovered by division from
+// the forward's final T. Per batch of 16 splats each thread records, per (pixel, splat),
+//   w = alpha' T (blend weight), drho = -alpha' dalpha / 2, dg = dalpha alpha'/alpha.
+// The per-splat sums over the tile's pixels are then tensor-core reductions (3xTF32 split,
+// ~fp32 accurate):  [dcolor, dz, dfeat] = W^T U  (U = per-pixel upstream [uc, uz, uq]),
+// and the drho moments  sum drho * [1, x, y, x^2, xy, y^2]  (+ sum dg), from which
+// dmean and dA (render.cpp:345-352) follow per splat in closed form.
 template <int DSP>
-__global__ void __launch_bounds__(kTilePixels) raster_bwd_kernel(RasterBwdArgs a) {
-  constexpr int NV = 10 + DSP;
+__global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArgs a) {
+  constexpr int NU = ((4 + DSP) + 7) / 8 * 8;  // U columns: uc0..2, uz, uq[DSP], pad
+  constexpr int NT = NU / 8;                   // n-tiles of the W^T U product
+  constexpr int UP = NU + (NU % 32 == 0 ? 4 : (NU % 16 == 0 ? 4 : 0));  // bank-spread pitch
+  constexpr int WP = 36;                       // per-warp [splat][pixel] pitch (floats)
+  constexpr int NACC = NU + 8 + 8;             // per-splat accumulators: W^T U | drho moments | dg
+  extern __shared__ __align__(16) float s_dyn[];
+  float* s_u = s_dyn;                                          // [256][UP] per-pixel upstream rows
+  float* s_wbase = s_dyn + kTilePixels * UP;                   // [8 warps][3][16 * WP]: W, drho, dg
+  __shared__ __align__(16) float s_f[kBwdBatch * NU];        // splat rows [c0 c1 c2 z f...]
   __shared__ SplatRec s_rec[kBwdBatch];
-  __shared__ float s_col[kBwdBatch * 3];
-  __shared__ float s_feat[kBwdBatch * DSP];
   __shared__ uint32_t s_src[kBwdBatch];
-  __shared__ float s_acc[kBwdBatch * NV];
+  __shared__ float s_acc[kBwdBatch * NACC];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tile = blockIdx.x;
-  const int px = (tile % a.tiles_x) * kTile + (threadIdx.x % kTile);
-  const int py = (tile / a.tiles_x) * kTile + (threadIdx.x / kTile);
+  const int tx0 = (tile % a.tiles_x) * kTile, ty0 = (tile / a.tiles_x) * kTile;
+  const int px = tx0 + (tid % kTile), py = ty0 + (tid / kTile);
   const bool inside = px < a.width && py < a.height;
   const int start = a.offset[tile];
   const int tend = start + a.tile_max_last[tile];
+  if (tend <= start) return;
   const size_t p = inside ? (size_t)py * a.width + px : 0;
+  // per-pixel upstream row U[p] = [uc0, uc1, uc2, uz, uq...] (zero outside the image)
   float uc0 = 0.f, uc1 = 0.f, uc2 = 0.f, uz = 0.f;
   float uq[DSP];
 #pragma unroll
@@ -455,33 +512,81 @@ __global__ void __launch_bounds__(kTilePixels) raster_bwd_kernel(RasterBwdArgs a
     last = a.px_last[p];
     T = a.px_T[p];
   }
+  {
+    float* ur = s_u + tid * UP;
+    ur[0] = uc0;
+    ur[1] = uc1;
+    ur[2] = uc2;
+    ur[3] = uz;
+#pragma unroll
+    for (int c = 0; c < DSP; ++c) ur[4 + c] = uq[c];
+#pragma unroll
+    for (int c = 4 + DSP; c < NU; ++c) ur[c] = 0.f;
+  }
+  // MMA lane coordinates
+  const int g = lane >> 2, cq = lane & 3;
+  // B fragments of the pixel moment matrix X[p][q] = [1, x', y', x'^2, x'y', y'^2, 0, 0] for the
+  // warp's 32 pixels (k-steps of 8 pixels); x', y' are tile-centred (exact in tf32).
+  uint32_t xb[4][2];
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int pl = 32 * warp + 8 * ks + cq + 4 * hh;  // tile-linear pixel of this B element (row k)
+      const float xx = (float)(pl % kTile) - 7.5f, yy = (float)(pl / kTile) - 7.5f;
+      float v = 0.f;
+      switch (g) {  // column n = g
+        case 0: v = 1.f; break;
+        case 1: v = xx; break;
+        case 2: v = yy; break;
+        case 3: v = xx * xx; break;
+        case 4: v = xx * yy; break;
+        case 5: v = yy * yy; break;
+        default: v = 0.f;
+      }
+      xb[ks][hh] = __float_as_uint(v);
+    }
   const float fx = (float)px, fy = (float)py;
-  const int lane = threadIdx.x & 31;
   float s_after = 0.f;
+  float* sw_w = s_wbase + (warp * 3 + 0) * kBwdBatch * WP;
+  float* sw_r = s_wbase + (warp * 3 + 1) * kBwdBatch * WP;
+  float* sw_g = s_wbase + (warp * 3 + 2) * kBwdBatch * WP;
   for (int hi = tend; hi > start; hi -= kBwdBatch) {
     const int lo = max(start, hi - kBwdBatch);
     const int cnt = hi - lo;
     __syncthreads();
-    if (threadIdx.x < cnt) {
-      const uint32_t src = (uint32_t)a.keys[lo + threadIdx.x];
-      s_src[threadIdx.x] = src;
-      s_rec[threadIdx.x] = a.rec[src];
-      s_col[threadIdx.x * 3 + 0] = a.colors[3 * (size_t)src + 0];
-      s_col[threadIdx.x * 3 + 1] = a.colors[3 * (size_t)src + 1];
-      s_col[threadIdx.x * 3 + 2] = a.colors[3 * (size_t)src + 2];
-      const float* f = a.feats + (size_t)src * a.ds;
-#pragma unroll
-      for (int c = 0; c < DSP; ++c) s_feat[threadIdx.x * DSP + c] = c < a.ds ? f[c] : 0.f;
+    if (tid < kBwdBatch) {
+      if (tid < cnt) {
+        const uint32_t src = (uint32_t)a.keys[lo + tid];
+        s_src[tid] = src;
+        s_rec[tid] = a.rec[src];
+      } else {
+        s_src[tid] = 0xffffffffu;
+        s_rec[tid] = SplatRec{0, 0, 0, 1.f, 0, 0, 0, 0, 1, 0, 1, 0};
+      }
     }
-    for (int e = threadIdx.x; e < cnt * NV; e += blockDim.x) s_acc[e] = 0.f;
+    for (int e = tid; e < kBwdBatch * NU; e += blockDim.x) {
+      const int j = e / NU, c = e % NU;
+      float v = 0.f;
+      if (j < cnt) {
+        const size_t src = (uint32_t)a.keys[lo + j];
+        if (c < 3)
+          v = a.colors[3 * src + c];
+        else if (c == 3)
+          v = a.rec[src].depth;
+        else if (c - 4 < a.ds)
+          v = a.feats[src * a.ds + (c - 4)];
+      }
+      s_f[e] = v;
+    }
+    for (int e = tid; e < kBwdBatch * NACC; e += blockDim.x) s_acc[e] = 0.f;
     __syncthreads();
-    for (int j = cnt - 1; j >= 0; --j) {
+    // ---- per-pixel reverse sweep over the batch
+    for (int j = kBwdBatch - 1; j >= 0; --j) {
       const SplatRec& s = s_rec[j];
       const int idx = lo - start + j;
-      const bool contrib = inside && idx < last && px >= s.x0 && px <= s.x1 && py >= s.y0 && py <= s.y1;
-      float v[NV];
-#pragma unroll
-      for (int c = 0; c < NV; ++c) v[c] = 0.f;
+      const bool contrib = j < cnt && inside && idx < last && px >= s.x0 && px <= s.x1 && py >= s.y0 && py <= s.y1;
+      float w = 0.f, drho = 0.f, dg = 0.f;
       if (contrib) {
         const float dx = fs(fx, s.mean_x);
         const float dy = fs(fy, s.mean_y);
@@ -489,55 +594,111 @@ __global__ void __launch_bounds__(kTilePixels) raster_bwd_kernel(RasterBwdArgs a
         float al = fm(s.alpha, exp_exact(fm(-0.5f, rho)));
         const bool clamped = al > kAlphaMax;
         if (clamped) al = kAlphaMax;
-        const float one_m = fs(1.f, al);
-        const float Tb = fd(T, one_m);
-        const float w = al * Tb;
-        float value = uc0 * s_col[j * 3] + uc1 * s_col[j * 3 + 1] + uc2 * s_col[j * 3 + 2];
-        value += uz * s.depth;
+        const float r = 1.f / fs(1.f, al);
+        const float Tb = T * r;
+        w = al * Tb;
+        const float* fr = s_f + j * NU;
+        float value = uc0 * fr[0] + uc1 * fr[1] + uc2 * fr[2] + uz * fr[3];
 #pragma unroll
-        for (int c = 0; c < DSP; ++c) value += uq[c] * s_feat[j * DSP + c];
-        v[7] = w * uc0;
-        v[8] = w * uc1;
-        v[9] = w * uc2;
-        v[5] = w * uz;
-#pragma unroll
-        for (int c = 0; c < DSP; ++c) v[10 + c] = w * uq[c];
-        const float d_alpha = Tb * value - s_after / one_m;
-        s_after += w * value;
+        for (int c = 0; c < DSP; ++c) value = fmaf(uq[c], fr[4 + c], value);
+        const float d_alpha = Tb * value - s_after * r;
+        s_after = fmaf(w, value, s_after);
         if (!clamped) {
-          const float g = al / s.alpha;
-          v[6] = d_alpha * g;
-          const float d_rho = -0.5f * al * d_alpha;
-          const float ad_x = s.a00 * dx + s.a01 * dy;
-          const float ad_y = s.a10 * dx + s.a11 * dy;
-          v[0] = d_rho * -2.f * ad_x;
-          v[1] = d_rho * -2.f * ad_y;
-          v[2] = d_rho * dx * dx;
-          v[3] = d_rho * dx * dy;
-          v[4] = d_rho * dy * dy;
+          dg = d_alpha * (al / s.alpha);
+          drho = -0.5f * al * d_alpha;
         }
         T = Tb;
       }
-      if (__any_sync(0xffffffffu, contrib)) {
+      sw_w[j * WP + lane] = w;
+      sw_r[j * WP + lane] = drho;
+      sw_g[j * WP + lane] = dg;
+    }
+    __syncwarp();
+    // ---- tensor-core reductions over the warp's 32 pixels
+    float dwu[NT][4];
+    float dmo[2][4];
 #pragma unroll
-        for (int c = 0; c < NV; ++c) {
-          const float r = warp_sum(v[c]);
-          if (lane == 0 && r != 0.f) atomicAdd(&s_acc[j * NV + c], r);
-        }
+    for (int nt = 0; nt < NT; ++nt) dwu[nt][0] = dwu[nt][1] = dwu[nt][2] = dwu[nt][3] = 0.f;
+    dmo[0][0] = dmo[0][1] = dmo[0][2] = dmo[0][3] = dmo[1][0] = dmo[1][1] = dmo[1][2] = dmo[1][3] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      // A = W^T (rows: splats j, cols: pixels) ; split into tf32 hi/lo
+      uint32_t ah[4], al_[4];
+      split_tf32(sw_w[g * WP + 8 * ks + cq], ah[0], al_[0]);
+      split_tf32(sw_w[(g + 8) * WP + 8 * ks + cq], ah[1], al_[1]);
+      split_tf32(sw_w[g * WP + 8 * ks + cq + 4], ah[2], al_[2]);
+      split_tf32(sw_w[(g + 8) * WP + 8 * ks + cq + 4], ah[3], al_[3]);
+      const int prow = 32 * warp + 8 * ks + cq;  // pixel (k index) of b0; b1 is +4
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        uint32_t bh[2], bl[2];
+        split_tf32(s_u[prow * UP + 8 * nt + g], bh[0], bl[0]);
+        split_tf32(s_u[(prow + 4) * UP + 8 * nt + g], bh[1], bl[1]);
+        mma_tf32(dwu[nt], ah, bh);
+        mma_tf32(dwu[nt], ah, bl);
+        mma_tf32(dwu[nt], al_, bh);
+      }
+      // A = [drho ; dg]^T (2 m-tiles), B = X (exact)
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const float* src = mt ? sw_g : sw_r;
+        uint32_t rh[4], rl[4];
+        split_tf32(src[g * WP + 8 * ks + cq], rh[0], rl[0]);
+        split_tf32(src[(g + 8) * WP + 8 * ks + cq], rh[1], rl[1]);
+        split_tf32(src[g * WP + 8 * ks + cq + 4], rh[2], rl[2]);
+        split_tf32(src[(g + 8) * WP + 8 * ks + cq + 4], rh[3], rl[3]);
+        mma_tf32(dmo[mt], rh, xb[ks]);
+        mma_tf32(dmo[mt], rl, xb[ks]);
       }
     }
+    // ---- cross-warp sum into the CTA accumulator (rows = splats)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      atomicAdd(&s_acc[g * NACC + 8 * nt + 2 * cq], dwu[nt][0]);
+      atomicAdd(&s_acc[g * NACC + 8 * nt + 2 * cq + 1], dwu[nt][1]);
+      atomicAdd(&s_acc[(g + 8) * NACC + 8 * nt + 2 * cq], dwu[nt][2]);
+      atomicAdd(&s_acc[(g + 8) * NACC + 8 * nt + 2 * cq + 1], dwu[nt][3]);
+    }
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int base = NU + 8 * mt;
+      atomicAdd(&s_acc[g * NACC + base + 2 * cq], dmo[mt][0]);
+      atomicAdd(&s_acc[g * NACC + base + 2 * cq + 1], dmo[mt][1]);
+      atomicAdd(&s_acc[(g + 8) * NACC + base + 2 * cq], dmo[mt][2]);
+      atomicAdd(&s_acc[(g + 8) * NACC + base + 2 * cq + 1], dmo[mt][3]);
+    }
     __syncthreads();
-    for (int e = threadIdx.x; e < cnt * NV; e += blockDim.x) {
-      const float val = s_acc[e];
-      if (val == 0.f) continue;
-      const int j = e / NV, c = e % NV;
+    // ---- per-splat closed forms + global accumulation
+    for (int e = tid; e < cnt * 16; e += blockDim.x) {
+      const int j = e >> 4, k = e & 15;
+      const float* ac = s_acc + j * NACC;
       const size_t src = s_src[j];
-      if (c < 7)
-        atomicAdd(&a.geo_acc[src * 8 + c], val);
-      else if (c < 10)
-        atomicAdd(&a.g_col[src * 3 + (c - 7)], val);
-      else if (c - 10 < a.ds)
-        atomicAdd(&a.g_feat[src * a.ds + (c - 10)], val);
+      if (k < 7) {
+        // moments M0..M5 (k-th column of the drho rows) -> dmean, dA, dz, dg
+        const SplatRec& s = s_rec[j];
+        const float up = s.mean_x - ((float)tx0 + 7.5f), vp = s.mean_y - ((float)ty0 + 7.5f);
+        const float* M = ac + NU;
+        const float sdx = M[1] - up * M[0], sdy = M[2] - vp * M[0];
+        float val = 0.f;
+        switch (k) {
+          case 0: val = -2.f * (s.a00 * sdx + s.a01 * sdy); break;
+          case 1: val = -2.f * (s.a10 * sdx + s.a11 * sdy); break;
+          case 2: val = M[3] - 2.f * up * M[1] + up * up * M[0]; break;
+          case 3: val = M[4] - vp * M[1] - up * M[2] + up * vp * M[0]; break;
+          case 4: val = M[5] - 2.f * vp * M[2] + vp * vp * M[0]; break;
+          case 5: val = ac[3]; break;           // dz = sum w uz
+          case 6: val = ac[NU + 8]; break;      // dg = sum dg (row block 2, column 0)
+        }
+        if (val != 0.f) atomicAdd(&a.geo_acc[src * 8 + k], val);
+      } else if (k < 10) {
+        const float val = ac[k - 7];
+        if (val != 0.f) atomicAdd(&a.g_col[src * 3 + (k - 7)], val);
+      }
+    }
+    for (int e = tid; e < cnt * a.ds; e += blockDim.x) {
+      const int j = e / a.ds, c = e % a.ds;
+      const float val = s_acc[j * NACC + 4 + c];
+      if (val != 0.f) atomicAdd(&a.g_feat[(size_t)s_src[j] * a.ds + c], val);
     }
   }
 }
@@ -671,7 +832,15 @@ void launch_fwd(cudaStream_t st, int ntiles, const RasterArgs& a) {
 }
 template <int DSP>
 void launch_bwd(cudaStream_t st, int ntiles, const RasterBwdArgs& a) {
-  raster_bwd_kernel<DSP><<<ntiles, kTilePixels, 0, st>>>(a);
+  constexpr int NU = ((4 + DSP) + 7) / 8 * 8;
+  constexpr int UP = NU + (NU % 32 == 0 ? 4 : (NU % 16 == 0 ? 4 : 0));
+  const size_t smem = sizeof(float) * ((size_t)kTilePixels * UP + 8 * 3 * kBwdBatch * 36);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(raster_bwd_kernel<DSP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  raster_bwd_kernel<DSP><<<ntiles, kTilePixels, smem, st>>>(a);
 }
 
 int pad_ds(int ds) {
@@ -726,7 +895,15 @@ void render_forward(cudaStream_t st, const MapPtrs& map, const float rot_cw[9], 
   count_launch();
   if (count_only) return;
   if (map.n > 0) {
-    scatter_kernel<<<grid1 * 2, 256, 0, st>>>(w.rec, map.n, w.tiles_x, w.tile_cursor, w.keys, w.pair_cap);
+    const size_t sc_smem = sizeof(int32_t) * 2 * ntiles;
+    static bool sc_attr = false;
+    if (!sc_attr) {
+      cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 4 * kHistMax);
+      sc_attr = true;
+    }
+    const unsigned sc_grid = (unsigned)((map.n + 256 * kScatterPerThread - 1) / (256 * kScatterPerThread));
+    scatter_kernel<<<sc_grid, 256, sc_smem, st>>>(w.rec, map.n, w.tiles_x, ntiles, w.tile_cursor, w.keys,
+                                                 w.pair_cap);
     count_launch();
   }
   static bool attr_set = false;
