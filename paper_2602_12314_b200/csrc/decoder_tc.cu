@@ -87,10 +87,22 @@ struct Dec1Args {
   int want_grad;
 };
 
+// Unpack 8 bf16 (one 16-byte core-matrix row chunk) to fp32.
+__device__ __forceinline__ void ld_row8(const uint8_t* tile, int r, int c0, uint32_t col_stride, float* v) {
+  const uint4 u = *reinterpret_cast<const uint4*>(tile + tc::core_off(r, c0, 128u, col_stride));
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    v[2 * i] = __uint_as_float(w[i] << 16);
+    v[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+}
+
 template <int K, int DS>
 __global__ void __launch_bounds__(256, 1) dec1_kernel(Dec1Args a) {
-  constexpr int kTmemCols = 2 * K <= 256 ? 256 : 512;
   constexpr int MH = K / 128;  // M halves of R^T
+  constexpr int kColDQ = K, kColR = K + DS;
+  constexpr int kTmemCols = (K + DS + MH * DS) <= 256 ? 256 : 512;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sQ = smem;                              // 128 x DS
   uint8_t* sKd = sQ + kRows * DS * 2;              // K x DS
@@ -105,8 +117,8 @@ __global__ void __launch_bounds__(256, 1) dec1_kernel(Dec1Args a) {
   const int g = warp & 3, h = warp >> 2;  // TMEM lane group, column half
   const int row = 32 * g + lane;
   constexpr int HC = K / 2;               // columns per half
+  constexpr uint32_t kCS = 16u * kRows;   // column-group stride of 128-row tiles
 
-  // resident operands: Kd (K x DS) and M (K x K)
   load_tile_bf16(sKd, a.kd, K, DS, K, tid, 256);
   load_tile_bf16(sM, a.mm, K, K, K, tid, 256);
   if (tid == 0) {
@@ -127,11 +139,8 @@ __global__ void __launch_bounds__(256, 1) dec1_kernel(Dec1Args a) {
   const uint32_t idesc4 = tc::make_idesc_bf16(128, DS, 1, 1);
   const uint32_t aQ = tc::smem_u32(sQ), aKd = tc::smem_u32(sKd), aP = tc::smem_u32(sP), aM = tc::smem_u32(sM);
   const float cl = kLog2e * a.inv_temp;
-
-  float racc[MH * DS];  // R^T rows (k = row, row + 128) for warps 4..7
-#pragma unroll
-  for (int i = 0; i < MH * DS; ++i) racc[i] = 0.f;
   double cos_acc = 0.0, l2_acc = 0.0, zflag = 0.0;
+  bool first = true;
 
   const int64_t ntiles = (a.npx + kRows - 1) / kRows;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -152,7 +161,7 @@ __global__ void __launch_bounds__(256, 1) dec1_kernel(Dec1Args a) {
     tc::mbar_wait(&bar[0], ph[0]);
     ph[0] ^= 1;
     tc::tc_fence_after();
-    // ---- softmax: row max over both halves
+    // ---- softmax: row max over both halves, then e = exp(S - max) (bf16) and the row sum
     float mx = -INFINITY;
 #pragma unroll
     for (int c = 0; c < HC; c += 32) {
@@ -171,57 +180,62 @@ __global__ void __launch_bounds__(256, 1) dec1_kernel(Dec1Args a) {
       float v[32];
       tc::tmem_ld32(tl + h * HC + c, v);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        v[i] = ex2(fmaf(v[i], cl, -mxl));
-        sum += v[i];
-      }
+      for (int i = 0; i < 32; ++i) v[i] = ex2(fmaf(v[i], cl, -mxl));
 #pragma unroll
-      for (int i = 0; i < 32; i += 8) st_row8(sP, row, h * HC + c + i, 16u * kRows, v + i);
+      for (int i = 0; i < 32; i += 8) st_row8(sP, row, h * HC + c + i, kCS, v + i);
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {  // sum the bf16-rounded e that the MMA consumes
+        float r[8];
+        ld_row8(sP, row, h * HC + c + i, kCS, r);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sum += r[j];
+      }
     }
     s_red[(1 * 2 + h) * 128 + row] = sum;
     tc::fence_async_smem();
     tc::tc_fence_before();
     __syncthreads();
     const float inv_sum = 1.f / (s_red[2 * 128 + row] + s_red[3 * 128 + row]);
-    // ---- MMA2: t = e M -> TMEM[K, 2K)
+    // ---- MMA2: t = e M -> TMEM[0, K) (S is dead)
     if (tid == 0) {
       tc::tc_fence_after();
 #pragma unroll 4
       for (int ks = 0; ks < K / 16; ++ks)
-        tc::mma_bf16(tmem + K, tc::make_sdesc(aP + ks * 2 * 2048, 2048, 128),
-                     tc::make_sdesc(aM + ks * 2 * (16 * K), 16 * K, 128), tc::make_idesc_bf16(128, K, 0, 0), ks > 0);
+        tc::mma_bf16(tmem, tc::make_sdesc(aP + ks * 2 * 2048, 2048, 128),
+                     tc::make_sdesc(aM + ks * 2 * (16 * K), 16 * K, 128), idesc1, ks > 0);
       tc::mma_commit(&bar[1]);
     }
     tc::mbar_wait(&bar[1], ph[1]);
     ph[1] ^= 1;
     tc::tc_fence_after();
-    // ---- per-row statistics: nu^2 = P.t, dot = P.G[a]
+    // ---- per-row statistics: nu^2 = P.t, dot = P.G[a]   (P = e / sum, t = (e M) / sum)
     const int64_t grow = r0 + row;
     const int32_t asg = row < valid ? a.assign[grow] : -1;
     const float* grow_ptr = a.gt + (int64_t)(asg < 0 ? 0 : asg) * K;
     float nu2 = 0.f, dot = 0.f;
 #pragma unroll
     for (int c = 0; c < HC; c += 32) {
-      float s[32], t[32];
-      tc::tmem_ld32(tl + h * HC + c, s);
-      tc::tmem_ld32(tl + K + h * HC + c, t);
+      float t[32];
+      tc::tmem_ld32(tl + h * HC + c, t);
 #pragma unroll
-      for (int i = 0; i < 32; i += 4) {
-        const float4 gg = __ldg(reinterpret_cast<const float4*>(grow_ptr + h * HC + c + i));
-        const float gv[4] = {gg.x, gg.y, gg.z, gg.w};
+      for (int i = 0; i < 32; i += 8) {
+        float e[8];
+        ld_row8(sP, row, h * HC + c + i, kCS, e);
+        const float4 g0 = __ldg(reinterpret_cast<const float4*>(grow_ptr + h * HC + c + i));
+        const float4 g1 = __ldg(reinterpret_cast<const float4*>(grow_ptr + h * HC + c + i + 4));
+        const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float p = ex2(fmaf(s[i + j], cl, -mxl)) * inv_sum;
-          nu2 = fmaf(p, t[i + j] * inv_sum, nu2);
-          dot = fmaf(p, gv[j], dot);
+        for (int j = 0; j < 8; ++j) {
+          nu2 = fmaf(e[j], t[i + j], nu2);
+          dot = fmaf(e[j], gv[j], dot);
         }
       }
     }
     s_red[(2 * 2 + h) * 128 + row] = nu2;
     s_red[(3 * 2 + h) * 128 + row] = dot;
     __syncthreads();
-    nu2 = s_red[4 * 128 + row] + s_red[5 * 128 + row];
-    dot = s_red[6 * 128 + row] + s_red[7 * 128 + row];
+    nu2 = (s_red[4 * 128 + row] + s_red[5 * 128 + row]) * inv_sum * inv_sum;
+    dot = (s_red[6 * 128 + row] + s_red[7 * 128 + row]) * inv_sum;
     float al = 0.f, be = 0.f, cc = 0.f;
     if (asg >= 0) {
       const float eps = 1e-8f;
@@ -243,74 +257,74 @@ __global__ void __launch_bounds__(256, 1) dec1_kernel(Dec1Args a) {
       continue;
     }
     // ---- dS = P (al t + be g - c) / tau  (bf16, overwrites e in sP)
+    const float ps = inv_sum * a.inv_temp;  // P = e * inv_sum
+    const float al_t = al * inv_sum;        // al * t = al * inv_sum * (e M)
 #pragma unroll
     for (int c = 0; c < HC; c += 32) {
-      float s[32], t[32];
-      tc::tmem_ld32(tl + h * HC + c, s);
-      tc::tmem_ld32(tl + K + h * HC + c, t);
+      float t[32];
+      tc::tmem_ld32(tl + h * HC + c, t);
 #pragma unroll
-      for (int i = 0; i < 32; i += 4) {
-        const float4 gg = __ldg(reinterpret_cast<const float4*>(grow_ptr + h * HC + c + i));
-        const float gv[4] = {gg.x, gg.y, gg.z, gg.w};
+      for (int i = 0; i < 32; i += 8) {
+        float e[8];
+        ld_row8(sP, row, h * HC + c + i, kCS, e);
+        const float4 g0 = __ldg(reinterpret_cast<const float4*>(grow_ptr + h * HC + c + i));
+        const float4 g1 = __ldg(reinterpret_cast<const float4*>(grow_ptr + h * HC + c + i + 4));
+        const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float p = ex2(fmaf(s[i + j], cl, -mxl)) * inv_sum;
-          s[i + j] = p * (al * (t[i + j] * inv_sum) + be * gv[j] - cc) * a.inv_temp;
-        }
+        for (int j = 0; j < 8; ++j) e[j] = e[j] * ps * fmaf(al_t, t[i + j], fmaf(be, gv[j], -cc));
+        st_row8(sP, row, h * HC + c + i, kCS, e);
       }
-#pragma unroll
-      for (int i = 0; i < 32; i += 8) st_row8(sP, row, h * HC + c + i, 16u * kRows, s + i);
     }
     tc::fence_async_smem();
     tc::tc_fence_before();
     __syncthreads();
-    // ---- MMA3: dQ = dS Kd -> TMEM[0, DS);  MMA4: R^T = dS^T Q -> TMEM[DS + DS*mh, ...)
+    // ---- MMA3: dQ = dS Kd -> TMEM[K, K+DS);  MMA4: R^T += dS^T Q -> TMEM[K+DS + DS*mh, ...)
     if (tid == 0) {
       tc::tc_fence_after();
 #pragma unroll 4
       for (int ks = 0; ks < K / 16; ++ks)
-        tc::mma_bf16(tmem, tc::make_sdesc(aP + ks * 2 * 2048, 2048, 128),
+        tc::mma_bf16(tmem + kColDQ, tc::make_sdesc(aP + ks * 2 * 2048, 2048, 128),
                      tc::make_sdesc(aKd + ks * 2 * 128, 128, 16 * K), idesc3, ks > 0);
 #pragma unroll
       for (int mh = 0; mh < MH; ++mh)
 #pragma unroll
         for (int ks = 0; ks < kRows / 16; ++ks)
-          tc::mma_bf16(tmem + DS + DS * mh, tc::make_sdesc(aP + mh * 16 * 2048 + ks * 2 * 128, 128, 2048),
-                       tc::make_sdesc(aQ + ks * 2 * 128, 128, 2048), idesc4, ks > 0);
+          tc::mma_bf16(tmem + kColR + DS * mh, tc::make_sdesc(aP + mh * 16 * 2048 + ks * 2 * 128, 128, 2048),
+                       tc::make_sdesc(aQ + ks * 2 * 128, 128, 2048), idesc4, (!first) || ks > 0);
       tc::mma_commit(&bar[2]);
     }
+    first = false;
     tc::mbar_wait(&bar[2], ph[2]);
     ph[2] ^= 1;
     tc::tc_fence_after();
     if (h == 0) {
       float v[DS];
 #pragma unroll
-      for (int c = 0; c < DS; c += 16) tc::tmem_ld16(tl + c, v + c);  // warp-aligned: all lanes load
+      for (int c = 0; c < DS; c += 16) tc::tmem_ld16(tl + kColDQ + c, v + c);  // warp-aligned: all lanes load
       if (row < valid) {
         float4* dst = reinterpret_cast<float4*>(a.d_query + grow * DS);
 #pragma unroll
         for (int c = 0; c < DS; c += 4) dst[c / 4] = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
       }
-    } else {
-#pragma unroll
-      for (int mh = 0; mh < MH; ++mh) {
-        float v[DS];
-#pragma unroll
-        for (int c = 0; c < DS; c += 16) tc::tmem_ld16(tl + DS + DS * mh + c, v + c);
-#pragma unroll
-        for (int c = 0; c < DS; ++c) racc[mh * DS + c] += v[c];
-      }
     }
     tc::tc_fence_before();
     __syncthreads();
   }
-  // ---- flush per-CTA partials
+  // ---- flush per-CTA partials: R^T rows k = 32g + lane (+128 mh)
   if (h == 1) {
 #pragma unroll
     for (int mh = 0; mh < MH; ++mh) {
+      float v[DS];
+      if (first) {
+#pragma unroll
+        for (int c = 0; c < DS; ++c) v[c] = 0.f;
+      } else {
+#pragma unroll
+        for (int c = 0; c < DS; c += 16) tc::tmem_ld16(tl + kColR + DS * mh + c, v + c);
+      }
       float* dst = a.r_part + ((size_t)blockIdx.x * K + mh * 128 + row) * DS;
 #pragma unroll
-      for (int c = 0; c < DS; ++c) dst[c] = racc[mh * DS + c];
+      for (int c = 0; c < DS; ++c) dst[c] = v[c];
     }
   }
   cos_acc = warp_sum_d(cos_acc);
@@ -346,10 +360,11 @@ struct Dec2Args {
 };
 
 template <int K, int DS>
-__global__ void __launch_bounds__(128, 1) dec2_kernel(Dec2Args a) {
+__global__ void __launch_bounds__(256, 1) dec2_kernel(Dec2Args a) {
   constexpr int MH = K / 128, NH = K / 2, NB = 64;
   constexpr int kColA = 128, kColB = 128 + MH * NH;
   constexpr int kTmemCols = kColB + MH * NB <= 256 ? 256 : 512;
+  constexpr uint32_t kCS = 16u * kRows;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sQ = smem;                    // 128 x DS
   uint8_t* sKd = sQ + kRows * DS * 2;    // K x DS
@@ -358,9 +373,11 @@ __global__ void __launch_bounds__(128, 1) dec2_kernel(Dec2Args a) {
   uint8_t* sOh = sAP + kRows * NH * 2;   // 128 x NB
   __shared__ uint64_t bar[2];
   __shared__ uint32_t s_taddr;
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = warp & 3, h = warp >> 2;
+  const int row = 32 * g + lane;
   const int role = blockIdx.x & 1, group = blockIdx.x >> 1, ngroups = gridDim.x >> 1;
-  load_tile_bf16(sKd, a.kd, K, DS, K, tid, 128);
+  load_tile_bf16(sKd, a.kd, K, DS, K, tid, 256);
   if (tid == 0) {
     tc::mbar_init(&bar[0], 1);
     tc::mbar_init(&bar[1], 1);
@@ -372,7 +389,7 @@ __global__ void __launch_bounds__(128, 1) dec2_kernel(Dec2Args a) {
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = s_taddr;
-  const uint32_t tl = tmem + ((uint32_t)(32 * warp) << 16);
+  const uint32_t tl = tmem + ((uint32_t)(32 * g) << 16);
   uint32_t ph[2] = {0, 0};
   const uint32_t aQ = tc::smem_u32(sQ), aKd = tc::smem_u32(sKd), aP = tc::smem_u32(sP), aAP = tc::smem_u32(sAP),
                  aOh = tc::smem_u32(sOh);
@@ -382,8 +399,7 @@ __global__ void __launch_bounds__(128, 1) dec2_kernel(Dec2Args a) {
   for (int64_t tile = group; tile < ntiles; tile += ngroups) {
     const int64_t r0 = tile * kRows;
     const int valid = (int)(a.npx - r0 < kRows ? a.npx - r0 : kRows);
-    load_tile_bf16(sQ, a.query + r0 * DS, kRows, DS, valid, tid, 128);
-    const int row = tid;
+    load_tile_bf16(sQ, a.query + r0 * DS, kRows, DS, valid, tid, 256);
     float4 st = make_float4(0.f, 0.f, 0.f, 0.f);
     int32_t asg = -1;
     if (row < valid) {
@@ -408,30 +424,31 @@ __global__ void __launch_bounds__(128, 1) dec2_kernel(Dec2Args a) {
       ph[0] ^= 1;
       tc::tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < 128; c += 32) {
+      for (int c = 0; c < 64; c += 32) {
+        const int cc = h * 64 + c;
         float v[32], w[32];
-        tc::tmem_ld32(tl + c, v);
+        tc::tmem_ld32(tl + cc, v);
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           v[i] = row < valid ? ex2(fmaf(v[i], cl, -mxl)) * inv_sum : 0.f;
           w[i] = al * v[i];
         }
-        const int k0 = ch * 128 + c;
+        const int k0 = ch * 128 + cc;
 #pragma unroll
-        for (int i = 0; i < 32; i += 8) st_row8(sP, row, k0 + i, 16u * kRows, v + i);
+        for (int i = 0; i < 32; i += 8) st_row8(sP, row, k0 + i, kCS, v + i);
         if (k0 >= role * NH && k0 < (role + 1) * NH) {
 #pragma unroll
-          for (int i = 0; i < 32; i += 8) st_row8(sAP, row, k0 - role * NH + i, 16u * kRows, w + i);
+          for (int i = 0; i < 32; i += 8) st_row8(sAP, row, k0 - role * NH + i, kCS, w + i);
         }
       }
     }
     if (role == 0) {
 #pragma unroll
-      for (int c = 0; c < NB; c += 8) {
+      for (int c = h * 32; c < h * 32 + 32; c += 8) {
         float v[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = (asg == c + i) ? be : 0.f;
-        st_row8(sOh, row, c, 16u * kRows, v);
+        st_row8(sOh, row, c, kCS, v);
       }
     }
     tc::fence_async_smem();
@@ -461,10 +478,9 @@ __global__ void __launch_bounds__(128, 1) dec2_kernel(Dec2Args a) {
     first = false;
   }
   // drain: lane `row` of half mh holds A[mh*128 + row][role*NH + c], Bm[mh*128 + row][c]
-  const int row = tid;
   for (int mh = 0; mh < MH; ++mh) {
     float* dst = a.a_part + (((size_t)group * 2 + role) * K + mh * 128 + row) * NH;
-    for (int c = 0; c < NH; c += 16) {
+    for (int c = h * (NH / 2); c < (h + 1) * (NH / 2); c += 16) {
       float v[16];
       if (first) {
         for (int i = 0; i < 16; ++i) v[i] = 0.f;
@@ -475,7 +491,7 @@ __global__ void __launch_bounds__(128, 1) dec2_kernel(Dec2Args a) {
     }
     if (role == 0) {
       float* db = a.bm_part + ((size_t)group * K + mh * 128 + row) * NB;
-      for (int c = 0; c < NB; c += 16) {
+      for (int c = h * (NB / 2); c < (h + 1) * (NB / 2); c += 16) {
         float v[16];
         if (first) {
           for (int i = 0; i < 16; ++i) v[i] = 0.f;
@@ -563,7 +579,7 @@ void launch_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_
     cudaFuncSetAttribute(dec2_kernel<K, DS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
     attr2 = true;
   }
-  dec2_kernel<K, DS><<<g2, 128, sm2, st>>>(d2);
+  dec2_kernel<K, DS><<<g2, 256, sm2, st>>>(d2);
   count_launch();
   const int64_t tot = (int64_t)K * K + n_set * K + (int64_t)K * DS + 3;
   dec_reduce_kernel<<<(unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 8), 256, 0, st>>>(
