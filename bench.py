@@ -230,11 +230,11 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
     ctx = api.Context(local_rank)
     w = synthetic.make_workload(args.config, gpu_render_fn(ctx))
+    from paper_2602_12314_b200.sharding import rank_plan
+
     nf = len(w.frames)
-    if nf % world:
-        raise SystemExit(f"{nf} keyframes do not split over {world} ranks")
-    per = nf // world
-    mine = w.frames[rank * per:(rank + 1) * per]
+    plan = rank_plan(nf, world, rank)
+    mine = [w.frames[i] for i in plan["frames"]]
     cfg = api.default_config(**w.lambdas)
     # BASELINE: config 0 is all fp32; configs 1-4 decode in bf16 with fp32 accumulation (tcgen05)
     cfg.decoder_precision = 0 if args.config == 0 else 1
@@ -250,7 +250,7 @@ def main():
                                for a in (f.rgb, f.depth, f.assignment, f.features)])
         pinned.append(pf)
     s.set_frames(pinned)
-    s.set_batch(nf, add_trust=(rank == 0), slot_offset=rank * per)
+    s.set_batch(plan["global_batch"], add_trust=plan["add_trust"], slot_offset=plan["slot_offset"])
     grads = s.grad_buffer()
     parts = s.loss_buffer()
 

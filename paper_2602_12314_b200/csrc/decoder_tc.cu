@@ -162,34 +162,31 @@ __global__ void __launch_bounds__(256, 1) dec1_kernel(Dec1Args a) {
     ph[0] ^= 1;
     tc::tc_fence_after();
     // ---- softmax: row max over both halves, then e = exp(S - max) (bf16) and the row sum
+    float sv[HC];  // this thread's half-row of S
+#pragma unroll
+    for (int c = 0; c < HC; c += 32) tc::tmem_ld32_nw(tl + h * HC + c, sv + c);
+    tc::tmem_wait_ld();
+#pragma unroll
+    for (int c = 0; c < HC; c += 32) tc::tmem_reg_fence32(sv + c);
     float mx = -INFINITY;
 #pragma unroll
-    for (int c = 0; c < HC; c += 32) {
-      float v[32];
-      tc::tmem_ld32(tl + h * HC + c, v);
-#pragma unroll
-      for (int i = 0; i < 32; ++i) mx = fmaxf(mx, v[i]);
-    }
+    for (int i = 0; i < HC; ++i) mx = fmaxf(mx, sv[i]);
     s_red[(0 * 2 + h) * 128 + row] = mx;
     __syncthreads();
     mx = fmaxf(s_red[row], s_red[128 + row]);
     const float mxl = mx * cl;
     float sum = 0.f;
 #pragma unroll
-    for (int c = 0; c < HC; c += 32) {
-      float v[32];
-      tc::tmem_ld32(tl + h * HC + c, v);
+    for (int c = 0; c < HC; c += 8) {
+      uint4 u;
+      u.x = tc::pack_bf16(ex2(fmaf(sv[c + 0], cl, -mxl)), ex2(fmaf(sv[c + 1], cl, -mxl)));
+      u.y = tc::pack_bf16(ex2(fmaf(sv[c + 2], cl, -mxl)), ex2(fmaf(sv[c + 3], cl, -mxl)));
+      u.z = tc::pack_bf16(ex2(fmaf(sv[c + 4], cl, -mxl)), ex2(fmaf(sv[c + 5], cl, -mxl)));
+      u.w = tc::pack_bf16(ex2(fmaf(sv[c + 6], cl, -mxl)), ex2(fmaf(sv[c + 7], cl, -mxl)));
+      *reinterpret_cast<uint4*>(sP + tc::core_off(row, h * HC + c, 128u, kCS)) = u;
+      const uint32_t w4[4] = {u.x, u.y, u.z, u.w};  // sum the bf16-rounded e the MMA consumes
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = ex2(fmaf(v[i], cl, -mxl));
-#pragma unroll
-      for (int i = 0; i < 32; i += 8) st_row8(sP, row, h * HC + c + i, kCS, v + i);
-#pragma unroll
-      for (int i = 0; i < 32; i += 8) {  // sum the bf16-rounded e that the MMA consumes
-        float r[8];
-        ld_row8(sP, row, h * HC + c + i, kCS, r);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) sum += r[j];
-      }
+      for (int j = 0; j < 4; ++j) sum += __uint_as_float(w4[j] << 16) + __uint_as_float(w4[j] & 0xffff0000u);
     }
     s_red[(1 * 2 + h) * 128 + row] = sum;
     tc::fence_async_smem();
@@ -213,20 +210,25 @@ __global__ void __launch_bounds__(256, 1) dec1_kernel(Dec1Args a) {
     const int32_t asg = row < valid ? a.assign[grow] : -1;
     const float* grow_ptr = a.gt + (int64_t)(asg < 0 ? 0 : asg) * K;
     float nu2 = 0.f, dot = 0.f;
+    float tv[HC];
 #pragma unroll
-    for (int c = 0; c < HC; c += 32) {
-      float t[32];
-      tc::tmem_ld32(tl + h * HC + c, t);
+    for (int c = 0; c < HC; c += 32) tc::tmem_ld32_nw(tl + h * HC + c, tv + c);
+    {
+      float4 gq[HC / 4];
 #pragma unroll
-      for (int i = 0; i < 32; i += 8) {
+      for (int i = 0; i < HC / 4; ++i) gq[i] = __ldg(reinterpret_cast<const float4*>(grow_ptr + h * HC) + i);
+      tc::tmem_wait_ld();
+#pragma unroll
+      for (int c = 0; c < HC; c += 32) tc::tmem_reg_fence32(tv + c);
+#pragma unroll
+      for (int c = 0; c < HC; c += 8) {
         float e[8];
-        ld_row8(sP, row, h * HC + c + i, kCS, e);
-        const float4 g0 = __ldg(reinterpret_cast<const float4*>(grow_ptr + h * HC + c + i));
-        const float4 g1 = __ldg(reinterpret_cast<const float4*>(grow_ptr + h * HC + c + i + 4));
-        const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+        ld_row8(sP, row, h * HC + c, kCS, e);
+        const float gv[8] = {gq[c / 4].x, gq[c / 4].y, gq[c / 4].z, gq[c / 4].w,
+                             gq[c / 4 + 1].x, gq[c / 4 + 1].y, gq[c / 4 + 1].z, gq[c / 4 + 1].w};
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          nu2 = fmaf(e[j], t[i + j], nu2);
+          nu2 = fmaf(e[j], tv[c + j], nu2);
           dot = fmaf(e[j], gv[j], dot);
         }
       }
@@ -260,20 +262,15 @@ __global__ void __launch_bounds__(256, 1) dec1_kernel(Dec1Args a) {
     const float ps = inv_sum * a.inv_temp;  // P = e * inv_sum
     const float al_t = al * inv_sum;        // al * t = al * inv_sum * (e M)
 #pragma unroll
-    for (int c = 0; c < HC; c += 32) {
-      float t[32];
-      tc::tmem_ld32(tl + h * HC + c, t);
+    for (int c = 0; c < HC; c += 8) {
+      float e[8];
+      ld_row8(sP, row, h * HC + c, kCS, e);
+      const float4 g0 = __ldg(reinterpret_cast<const float4*>(grow_ptr + h * HC + c));
+      const float4 g1 = __ldg(reinterpret_cast<const float4*>(grow_ptr + h * HC + c + 4));
+      const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
 #pragma unroll
-      for (int i = 0; i < 32; i += 8) {
-        float e[8];
-        ld_row8(sP, row, h * HC + c + i, kCS, e);
-        const float4 g0 = __ldg(reinterpret_cast<const float4*>(grow_ptr + h * HC + c + i));
-        const float4 g1 = __ldg(reinterpret_cast<const float4*>(grow_ptr + h * HC + c + i + 4));
-        const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-#pragma unroll
-        for (int j = 0; j < 8; ++j) e[j] = e[j] * ps * fmaf(al_t, t[i + j], fmaf(be, gv[j], -cc));
-        st_row8(sP, row, h * HC + c + i, kCS, e);
-      }
+      for (int j = 0; j < 8; ++j) e[j] = e[j] * ps * fmaf(al_t, tv[c + j], fmaf(be, gv[j], -cc));
+      st_row8(sP, row, h * HC + c, kCS, e);
     }
     tc::fence_async_smem();
     tc::tc_fence_before();
