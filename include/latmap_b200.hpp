@@ -1,0 +1,152 @@
+// latmap_b200.hpp — C++ host layer over the C-ABI (latmap_b200.h), mirroring the reference
+// operator API of proj/include/latmap/** (names, argument meaning, error behaviour):
+//   latmap_b200::render / render_backward        <- latmap::render / render_backward (splat/render.hpp:103-119)
+//   latmap_b200::reconstruct / reconstruct_backward / trust_region_penalty
+//                                                <- dict/dictionary.hpp:63-77
+//   latmap_b200::Session::total_objective / step  <- total_objective (obj/objective.hpp:49-54) +
+//                                                   MapOptimizer::step_map/step_dict (pipe/pipeline.hpp:52-69)
+// Status codes map back to the reference's exceptions: LATMAP_ERR_INVALID_ARGUMENT ->
+// std::invalid_argument, LATMAP_ERR_STALE_CACHE -> std::runtime_error, anything else ->
+// latmap_b200::device_error. Device buffers are caller-owned raw pointers (any allocator).
+#pragma once
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "latmap_b200.h"
+
+namespace latmap_b200 {
+
+struct device_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void check(latmap_status s, const latmap_ctx* ctx) {
+  if (s == LATMAP_OK) return;
+  const std::string msg = latmap_ctx_last_error(ctx);
+  if (s == LATMAP_ERR_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  if (s == LATMAP_ERR_STALE_CACHE) throw std::runtime_error(msg);
+  throw device_error(msg.empty() ? "latmap_b200: device error" : msg);
+}
+
+// One context per host thread, bound to a device and a CUDA stream (cudaStream_t as void*).
+class Context {
+ public:
+  explicit Context(int device = 0, void* stream = nullptr) { check(latmap_ctx_create(device, stream, &h_), nullptr); }
+  ~Context() {
+    if (h_) latmap_ctx_destroy(h_);
+  }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+  latmap_ctx* get() const { return h_; }
+  void synchronize() { check(latmap_ctx_synchronize(h_), h_); }
+
+ private:
+  latmap_ctx* h_ = nullptr;
+};
+
+// RenderOutputT's cache half (splats + fingerprint); the images are caller-owned device buffers.
+class RenderCache {
+ public:
+  explicit RenderCache(Context& ctx) : ctx_(&ctx) { check(latmap_render_cache_create(ctx.get(), &h_), ctx.get()); }
+  ~RenderCache() {
+    if (h_) latmap_render_cache_destroy(h_);
+  }
+  RenderCache(const RenderCache&) = delete;
+  RenderCache& operator=(const RenderCache&) = delete;
+  latmap_render_cache* get() const { return h_; }
+  // RenderOutput::splats in source order (host copy).
+  std::vector<latmap_projected_splat> splats() const {
+    int64_t n = 0;
+    check(latmap_render_cache_splats(ctx_->get(), h_, nullptr, 0, &n), ctx_->get());
+    std::vector<latmap_projected_splat> out((size_t)n);
+    check(latmap_render_cache_splats(ctx_->get(), h_, out.data(), n, &n), ctx_->get());
+    return out;
+  }
+
+ private:
+  Context* ctx_;
+  latmap_render_cache* h_ = nullptr;
+};
+
+struct RenderImages {  // device pointers: color HxWx3, depth HxW, query HxWxds, alpha HxW
+  float *color, *depth, *query, *alpha;
+};
+
+// render (splat/render.hpp:103-105)
+inline void render(Context& ctx, const latmap_map& map, const latmap_pose& pose, const latmap_intrinsics& intr,
+                   RenderCache& cache, const RenderImages& out) {
+  check(latmap_render(ctx.get(), &map, &pose, &intr, cache.get(), out.color, out.depth, out.query, out.alpha),
+        ctx.get());
+}
+
+// render_backward (splat/render.hpp:116-119); gradients are accumulated into `grads`.
+inline void render_backward(Context& ctx, const latmap_map& map, const latmap_pose& pose,
+                            const latmap_intrinsics& intr, const RenderCache& cache, const float* d_color,
+                            const float* d_depth, const float* d_query, latmap_map& grads) {
+  check(latmap_render_backward(ctx.get(), &map, &pose, &intr, cache.get(), d_color, d_depth, d_query, &grads),
+        ctx.get());
+}
+
+// reconstruct (dict/dictionary.hpp:63-65)
+inline void reconstruct(Context& ctx, const float* queries, int64_t n, int32_t query_dim, const float* atoms,
+                        const float* proj, int64_t k, int32_t embed_dim, float temperature, float* out,
+                        float* attention = nullptr) {
+  check(latmap_reconstruct(ctx.get(), queries, n, query_dim, atoms, proj, k, embed_dim, temperature, out, attention),
+        ctx.get());
+}
+
+// trust_region_penalty (dict/dictionary.hpp:75-77)
+inline float trust_region_penalty(Context& ctx, const float* atoms, const float* anchor, int64_t k, int32_t df,
+                                  float delta, float* d_atoms = nullptr) {
+  float v = 0.f;
+  check(latmap_trust_region_penalty(ctx.get(), atoms, anchor, k, df, delta, d_atoms, &v), ctx.get());
+  return v;
+}
+
+// Device-resident GaussianMap + DictionaryState + MapOptimizer; one step() is one Stage-I
+// iteration (pipeline.cpp:236-246).
+class Session {
+ public:
+  Session(Context& ctx, const latmap_config& cfg, int64_t n, int32_t query_dim, int64_t k, int32_t embed_dim,
+          const latmap_intrinsics& intr)
+      : ctx_(&ctx) {
+    check(latmap_session_create(ctx.get(), &cfg, n, query_dim, k, embed_dim, &intr, &h_), ctx.get());
+  }
+  ~Session() {
+    if (h_) latmap_session_destroy(h_);
+  }
+  Session(const Session&) = delete;
+  Session& operator=(const Session&) = delete;
+  void set_map(const float* pos, const float* rot, const float* col, const float* lsc, const float* opa,
+               const float* feat) {
+    check(latmap_session_set_map(h_, pos, rot, col, lsc, opa, feat), ctx_->get());
+  }
+  void set_dictionary(const float* atoms, const float* anchor, const float* proj) {
+    check(latmap_session_set_dictionary(h_, atoms, anchor, proj), ctx_->get());
+  }
+  void set_frames(const std::vector<latmap_frame>& frames) {
+    check(latmap_session_set_frames(h_, (int32_t)frames.size(), frames.data()), ctx_->get());
+  }
+  // total_objective with gradients (objective.cpp:67-194)
+  latmap_loss_breakdown total_objective() {
+    latmap_loss_breakdown out{};
+    check(latmap_session_objective(h_, 1, &out), ctx_->get());
+    return out;
+  }
+  // MapOptimizer::step_map + step_dict (pipeline.cpp:75-95)
+  void apply() { check(latmap_session_apply(h_), ctx_->get()); }
+  latmap_loss_breakdown step() {
+    latmap_loss_breakdown out{};
+    check(latmap_session_step(h_, &out), ctx_->get());
+    return out;
+  }
+  latmap_session* get() const { return h_; }
+
+ private:
+  Context* ctx_;
+  latmap_session* h_ = nullptr;
+};
+
+}  // namespace latmap_b200
