@@ -105,6 +105,10 @@ latmap_status latmap_ctx_create(int32_t device, void* cuda_stream, latmap_ctx** 
 latmap_status latmap_ctx_destroy(latmap_ctx* ctx);
 latmap_status latmap_ctx_set_stream(latmap_ctx* ctx, void* cuda_stream);
 latmap_status latmap_ctx_synchronize(latmap_ctx* ctx);
+/* Parity mode for the forward blend: 1 = colour/depth/query accumulated with separately rounded
+ * products and sums in the reference's order (bit-exact images); 0 (default) = FMA accumulation
+ * (images within 1e-6 relative). alpha', clamp and termination decisions are exact in both. */
+latmap_status latmap_ctx_set_exact_blend(latmap_ctx* ctx, int32_t exact);
 const char* latmap_ctx_last_error(const latmap_ctx* ctx);
 /* Kernels launched by this context since creation (evidence for the bench). */
 int64_t latmap_ctx_launch_count(const latmap_ctx* ctx);

@@ -90,6 +90,9 @@ class Context:
     def sync(self):
         check(self.h, lib().latmap_ctx_synchronize(self.h))
 
+    def set_exact_blend(self, exact=True):
+        check(self.h, lib().latmap_ctx_set_exact_blend(self.h, int(bool(exact))))
+
     def launches(self):
         return lib().latmap_ctx_launch_count(self.h)
 

@@ -26,14 +26,27 @@ __device__ __forceinline__ int find_block(const Blocks& B, int64_t e) {
   return -1;
 }
 
-// Pass 1: per-block all-finite check (adam.hpp:65-68).
+// Pass 1: per-block all-finite check (adam.hpp:65-68), 16-byte loads.
 __global__ void adam_check_kernel(const float* __restrict__ grad, Blocks B, int64_t total, int32_t* flags) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t n4 = total / 4;
+  const float4* g4 = reinterpret_cast<const float4*>(grad);
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n4; q += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = g4[q];
+    if (!(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w))) {
+      const float vv[4] = {v.x, v.y, v.z, v.w};
+      for (int i = 0; i < 4; ++i)
+        if (!isfinite(vv[i])) {
+          const int b = find_block(B, 4 * q + i);
+          if (b >= 0) flags[b] = 1;
+        }
+    }
+  }
+  for (int64_t e = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x)
     if (!isfinite(grad[e])) {
       const int b = find_block(B, e);
       if (b >= 0) flags[b] = 1;
     }
-  }
 }
 
 __device__ __forceinline__ float adam_elem(float& p, float g, float& m, float& v, float lr, float c1, float c2) {
@@ -86,13 +99,39 @@ __global__ void adam_update_kernel(float* __restrict__ param, const float* __res
     }
     return;
   }
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < blk.count; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = blk.offset + i;
-    float p = param[e], mm = m[e], vv = v[e];
-    adam_elem(p, grad[e], mm, vv, blk.lr, c1, c2);
-    param[e] = p;
-    m[e] = mm;
-    v[e] = vv;
+  // 16-byte vectors over the 4-aligned interior of the block, scalar head/tail
+  const int64_t e0 = blk.offset, e1 = blk.offset + blk.count;
+  const int64_t a0 = (e0 + 3) / 4 * 4, a1 = e1 / 4 * 4;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+  if (a0 < a1) {
+    for (int64_t q = a0 / 4 + tid; q < a1 / 4; q += nth) {
+      float4 p = reinterpret_cast<float4*>(param)[q];
+      const float4 g = reinterpret_cast<const float4*>(grad)[q];
+      float4 mm = reinterpret_cast<float4*>(m)[q];
+      float4 vv = reinterpret_cast<float4*>(v)[q];
+      adam_elem(p.x, g.x, mm.x, vv.x, blk.lr, c1, c2);
+      adam_elem(p.y, g.y, mm.y, vv.y, blk.lr, c1, c2);
+      adam_elem(p.z, g.z, mm.z, vv.z, blk.lr, c1, c2);
+      adam_elem(p.w, g.w, mm.w, vv.w, blk.lr, c1, c2);
+      reinterpret_cast<float4*>(param)[q] = p;
+      reinterpret_cast<float4*>(m)[q] = mm;
+      reinterpret_cast<float4*>(v)[q] = vv;
+    }
+  }
+  auto scalar = [&](int64_t lo, int64_t hi) {
+    for (int64_t e = lo + tid; e < hi; e += nth) {
+      float p = param[e], mm = m[e], vv = v[e];
+      adam_elem(p, grad[e], mm, vv, blk.lr, c1, c2);
+      param[e] = p;
+      m[e] = mm;
+      v[e] = vv;
+    }
+  };
+  if (a0 < a1) {
+    scalar(e0, a0);
+    scalar(a1, e1);
+  } else {
+    scalar(e0, e1);
   }
 }
 

@@ -136,6 +136,7 @@ struct latmap_ctx {
   cudaStream_t stream = nullptr;
   std::string err;
   int64_t launches0 = 0;
+  bool exact_blend = false;  // parity mode: separately rounded accumulation in the forward blend
 };
 
 struct latmap_render_cache {
@@ -234,6 +235,12 @@ latmap_status latmap_ctx_set_stream(latmap_ctx* ctx, void* stream) {
   return LATMAP_OK;
 }
 
+latmap_status latmap_ctx_set_exact_blend(latmap_ctx* ctx, int32_t exact) {
+  if (!ctx) return LATMAP_ERR_INVALID_ARGUMENT;
+  ctx->exact_blend = exact != 0;
+  return LATMAP_OK;
+}
+
 latmap_status latmap_ctx_synchronize(latmap_ctx* ctx) {
   if (!ctx) return LATMAP_ERR_INVALID_ARGUMENT;
   CTX_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
@@ -316,7 +323,8 @@ latmap_status latmap_render(latmap_ctx* ctx, const latmap_map* map, const latmap
   CTX_CHECK(ctx, cudaMemcpyAsync(counters, b.w.counters, sizeof(counters), cudaMemcpyDeviceToHost, st));
   CTX_CHECK(ctx, cudaStreamSynchronize(st));
   if (counters[0] > b.w.pair_cap) CTX_CHECK(ctx, b.ensure(map->n, intr->width, intr->height, counters[0]));
-  render_forward(st, mp, rcw, pose->translation, in, b.w, color, depth, query, alpha, true, false);
+  render_forward(st, mp, rcw, pose->translation, in, b.w, color, depth, query, alpha, true, false, true,
+                 ctx->exact_blend);
   latmap_status s = post_launch(ctx);
   if (s != LATMAP_OK) return s;
   cache->valid = true;
@@ -712,7 +720,7 @@ latmap_status session_objective(latmap_session* s, bool want_grad) {
                    false, false, false);
     s->end();
     s->begin(1);
-    render_blend(st, map, in, rb.w, s->color[b], s->depth[b], s->query[b], s->alpha[b]);
+    render_blend(st, map, in, rb.w, s->color[b], s->depth[b], s->query[b], s->alpha[b], ctx->exact_blend);
     s->end();
     s->begin(2);
     image_losses(st, s->color[b], s->depth[b], s->alpha[b], f.rgb, f.depth, h, w, c.lambda_i1, c.lambda_i2,

@@ -284,7 +284,14 @@ void sgemm(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, f
   }
   const int64_t gx = (N + BN - 1) / BN, gy = (M + BM - 1) / BM;
   if (split < 1) split = 1;
-  // choose split so that each chunk still has >= 256 reduction steps
+  // small output grids with long reductions: split K across CTAs (atomics into C); C is
+  // pre-zeroed for beta == 0, accumulated into for beta == 1.
+  if (split == 1 && gx * gy < 148 && K >= 256 && (beta == 0.f || beta == 1.f)) {
+    const int64_t want = (296 + gx * gy - 1) / (gx * gy);
+    split = (int)std::max<int64_t>(1, std::min<int64_t>(want, K / 128));
+    if (split > 1 && beta == 0.f)
+      for (int64_t i = 0; i < M; ++i) cudaMemsetAsync(C + i * ldc, 0, sizeof(float) * N, st);
+  }
   const int64_t kchunk = ((K + split - 1) / split + BK - 1) / BK * BK;
   const int gz = (int)((K + kchunk - 1) / kchunk);
   const bool atomic = gz > 1 || split > 1;

@@ -39,10 +39,11 @@ struct RenderWork {
 // Renderer: project (K1) -> scan (K2) -> scatter (K3) -> per-tile sort -> blend (K4).
 void render_forward(cudaStream_t st, const MapPtrs& map, const float rot_cw[9], const float origin[3],
                     const Intr& intr, RenderWork& w, float* color, float* depth, float* query,
-                    float* alpha, bool zero_outputs, bool count_only = false, bool blend = true);
+                    float* alpha, bool zero_outputs, bool count_only = false, bool blend = true,
+                    bool exact = false);
 // K4 only (after render_forward(..., blend=false)).
 void render_blend(cudaStream_t st, const MapPtrs& map, const Intr& intr, RenderWork& w, float* color, float* depth,
-                  float* query, float* alpha);
+                  float* query, float* alpha, bool exact = false);
 void project_single(cudaStream_t st, const float* d_in11, const float rot_cw[9], const float origin[3],
                     const Intr& intr, float* d_out8);
 // Backward: blend replay + reverse sweep (K8) -> projection backward (K9). Accumulates.

@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(1024) scan_tiles_kernel(const int32_t* __restr
 // counts its pairs per tile in shared memory, reserves one contiguous range per (block, tile)
 // with a single global atomic, then fills it (slot order inside a bucket is irrelevant: the
 // per-tile sort below makes the list canonical).
-constexpr int kScatterPerThread = 8;
+constexpr int kScatterPerThread = 2;
 __global__ void __launch_bounds__(256) scatter_kernel(const SplatRec* __restrict__ rec, int64_t n, int tiles_x,
                                                       int ntiles, int32_t* cursor, uint64_t* __restrict__ keys,
                                                       int64_t pair_cap) {
@@ -341,8 +341,11 @@ struct RasterArgs {
   const int64_t* counters;
 };
 
-// K4: forward blend, one CTA per 16x16 tile, one thread per pixel.
-template <int DSP>
+// K4: forward blend, one CTA per 16x16 tile, one thread per pixel. alpha', the clamp, the
+// transmittance and the termination test always use the reference's float op sequence
+// (bit-exact decisions); EXACT additionally accumulates colour/depth/alpha/query with
+// separately rounded products and sums (bit-exact images), otherwise with FMA.
+template <int DSP, bool EXACT>
 __global__ void __launch_bounds__(kTilePixels) raster_fwd_kernel(RasterArgs a) {
   constexpr int kFwdBatch = DSP >= 64 ? 128 : 256;
   __shared__ SplatRec s_rec[kFwdBatch];
@@ -388,13 +391,22 @@ __global__ void __launch_bounds__(kTilePixels) raster_fwd_kernel(RasterArgs a) {
         float al = fm(s.alpha, exp_exact(fm(-0.5f, rho)));
         if (al > kAlphaMax) al = kAlphaMax;
         const float w = fm(al, T);
-        acc_c0 = fa(acc_c0, fm(w, s_col[j * 3 + 0]));
-        acc_c1 = fa(acc_c1, fm(w, s_col[j * 3 + 1]));
-        acc_c2 = fa(acc_c2, fm(w, s_col[j * 3 + 2]));
-        acc_d = fa(acc_d, fm(w, s.depth));
-        acc_a = fa(acc_a, w);
+        if (EXACT) {
+          acc_c0 = fa(acc_c0, fm(w, s_col[j * 3 + 0]));
+          acc_c1 = fa(acc_c1, fm(w, s_col[j * 3 + 1]));
+          acc_c2 = fa(acc_c2, fm(w, s_col[j * 3 + 2]));
+          acc_d = fa(acc_d, fm(w, s.depth));
 #pragma unroll
-        for (int c = 0; c < DSP; ++c) acc_q[c] = fa(acc_q[c], fm(w, s_feat[j * DSP + c]));
+          for (int c = 0; c < DSP; ++c) acc_q[c] = fa(acc_q[c], fm(w, s_feat[j * DSP + c]));
+        } else {
+          acc_c0 = fmaf(w, s_col[j * 3 + 0], acc_c0);
+          acc_c1 = fmaf(w, s_col[j * 3 + 1], acc_c1);
+          acc_c2 = fmaf(w, s_col[j * 3 + 2], acc_c2);
+          acc_d = fmaf(w, s.depth, acc_d);
+#pragma unroll
+          for (int c = 0; c < DSP; ++c) acc_q[c] = fmaf(w, s_feat[j * DSP + c], acc_q[c]);
+        }
+        acc_a = fa(acc_a, w);
         T = fm(T, fs(1.f, al));
         if (T < kTransmitStop) {
           done = true;
@@ -827,8 +839,11 @@ __global__ void project_single_kernel(const float* in, Cam cam, float* out) {
 }
 
 template <int DSP>
-void launch_fwd(cudaStream_t st, int ntiles, const RasterArgs& a) {
-  raster_fwd_kernel<DSP><<<ntiles, kTilePixels, 0, st>>>(a);
+void launch_fwd(cudaStream_t st, int ntiles, const RasterArgs& a, bool exact) {
+  if (exact)
+    raster_fwd_kernel<DSP, true><<<ntiles, kTilePixels, 0, st>>>(a);
+  else
+    raster_fwd_kernel<DSP, false><<<ntiles, kTilePixels, 0, st>>>(a);
 }
 template <int DSP>
 void launch_bwd(cudaStream_t st, int ntiles, const RasterBwdArgs& a) {
@@ -867,7 +882,7 @@ void project_single(cudaStream_t st, const float* d_in11, const float rot_cw[9],
 
 void render_forward(cudaStream_t st, const MapPtrs& map, const float rot_cw[9], const float origin[3],
                     const Intr& intr, RenderWork& w, float* color, float* depth, float* query, float* alpha,
-                    bool zero_outputs, bool count_only, bool blend) {
+                    bool zero_outputs, bool count_only, bool blend, bool exact) {
   Cam cam;
   for (int i = 0; i < 9; ++i) cam.r[i] = rot_cw[i];
   for (int i = 0; i < 3; ++i) cam.o[i] = origin[i];
@@ -914,20 +929,20 @@ void render_forward(cudaStream_t st, const MapPtrs& map, const float rot_cw[9], 
   tile_sort_kernel<<<ntiles, 512, kSortCap * 8, st>>>(w.tile_offset, w.keys, w.keys_tmp, w.pair_cap, w.counters);
   count_launch();
   if (!blend) return;
-  render_blend(st, map, intr, w, color, depth, query, alpha);
+  render_blend(st, map, intr, w, color, depth, query, alpha, exact);
 }
 
 void render_blend(cudaStream_t st, const MapPtrs& map, const Intr& intr, RenderWork& w, float* color, float* depth,
-                  float* query, float* alpha) {
+                  float* query, float* alpha, bool exact) {
   const int ntiles = w.tiles_x * w.tiles_y;
   RasterArgs a{w.rec, map.col, map.feat, map.ds, w.tile_offset, w.keys, w.tiles_x, intr.width, intr.height,
                color, depth, query, alpha, w.px_last, w.px_T, w.tile_max_last, w.counters};
   switch (pad_ds(map.ds)) {
-    case 4: launch_fwd<4>(st, ntiles, a); break;
-    case 8: launch_fwd<8>(st, ntiles, a); break;
-    case 16: launch_fwd<16>(st, ntiles, a); break;
-    case 32: launch_fwd<32>(st, ntiles, a); break;
-    case 64: launch_fwd<64>(st, ntiles, a); break;
+    case 4: launch_fwd<4>(st, ntiles, a, exact); break;
+    case 8: launch_fwd<8>(st, ntiles, a, exact); break;
+    case 16: launch_fwd<16>(st, ntiles, a, exact); break;
+    case 32: launch_fwd<32>(st, ntiles, a, exact); break;
+    case 64: launch_fwd<64>(st, ntiles, a, exact); break;
     default: break;
   }
   count_launch();
