@@ -99,28 +99,31 @@ __device__ __forceinline__ void ld_row8(const uint8_t* tile, int r, int c0, uint
 }
 
 template <int K, int DS>
-__global__ void __launch_bounds__(256, 1) dec1_kernel(Dec1Args a) {
+__global__ void __launch_bounds__(512, 1) dec1_kernel(Dec1Args a) {
+  constexpr int NT = 512;      // 16 warps: 4 TMEM lane groups x 4 column quarters
   constexpr int MH = K / 128;  // M halves of R^T
   constexpr int kColDQ = K, kColR = K + DS;
   constexpr int kTmemCols = (K + DS + MH * DS) <= 256 ? 256 : 512;
+  constexpr int QC = K / 4;               // columns per quarter
+  constexpr uint32_t kCS = 16u * kRows;   // column-group stride of 128-row tiles
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sQ = smem;                              // 128 x DS
   uint8_t* sKd = sQ + kRows * DS * 2;              // K x DS
   uint8_t* sP = sKd + K * DS * 2;                  // 128 x K  (e, then dS)
   uint8_t* sM = sP + kRows * K * 2;                // K x K
-  float* s_red = reinterpret_cast<float*>(sM + K * K * 2);  // [8][128]: max, sum, nu2, dot (x2 halves)
+  float* s_red = reinterpret_cast<float*>(sM + K * K * 2);  // [4 quantities][4 quarters][128]
   __shared__ uint64_t bar[3];
   __shared__ uint32_t s_taddr;
-  __shared__ double s_loss[8][3];
+  __shared__ double s_loss[16][3];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = warp & 3, h = warp >> 2;  // TMEM lane group, column half
+  const int g = warp & 3, qt = warp >> 2;  // TMEM lane group, column quarter
   const int row = 32 * g + lane;
-  constexpr int HC = K / 2;               // columns per half
-  constexpr uint32_t kCS = 16u * kRows;   // column-group stride of 128-row tiles
+  const int c0 = qt * QC;
+  auto red = [&](int q, int quarter) -> float& { return s_red[(q * 4 + quarter) * 128 + row]; };
 
-  load_tile_bf16(sKd, a.kd, K, DS, K, tid, 256);
-  load_tile_bf16(sM, a.mm, K, K, K, tid, 256);
+  load_tile_bf16(sKd, a.kd, K, DS, K, tid, NT);
+  load_tile_bf16(sM, a.mm, K, K, K, tid, NT);
   if (tid == 0) {
     for (int i = 0; i < 3; ++i) tc::mbar_init(&bar[i], 1);
     tc::fence_mbar_init();
@@ -142,11 +145,35 @@ __global__ void __launch_bounds__(256, 1) dec1_kernel(Dec1Args a) {
   double cos_acc = 0.0, l2_acc = 0.0, zflag = 0.0;
   bool first = true;
 
+  // Q tile prefetch: each thread owns 8 consecutive values (one 16-byte core row chunk)
+  constexpr int QCH = kRows * DS / 8;  // 8-value chunks per tile
+  static_assert(QCH <= NT, "one Q chunk per thread");
+  const int qr = tid / (DS / 8), qc = (tid % (DS / 8)) * 8;
+  float4 qpre[2];
+  auto q_fetch = [&](int64_t r0, int valid) {
+    if (tid < QCH && qr < valid) {
+      const float4* src = reinterpret_cast<const float4*>(a.query + (r0 + qr) * DS + qc);
+      qpre[0] = src[0];
+      qpre[1] = src[1];
+    } else {
+      qpre[0] = qpre[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  auto q_store = [&]() {
+    if (tid < QCH) {
+      const float v[8] = {qpre[0].x, qpre[0].y, qpre[0].z, qpre[0].w, qpre[1].x, qpre[1].y, qpre[1].z, qpre[1].w};
+      st_row8(sQ, qr, qc, kCS, v);
+    }
+  };
   const int64_t ntiles = (a.npx + kRows - 1) / kRows;
+  if ((int64_t)blockIdx.x < ntiles) {
+    const int64_t r0 = (int64_t)blockIdx.x * kRows;
+    q_fetch(r0, (int)(a.npx - r0 < kRows ? a.npx - r0 : kRows));
+  }
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t r0 = tile * kRows;
     const int valid = (int)(a.npx - r0 < kRows ? a.npx - r0 : kRows);
-    load_tile_bf16(sQ, a.query + r0 * DS, kRows, DS, valid, tid, 256);
+    q_store();
     tc::fence_async_smem();
     __syncthreads();
     // ---- MMA1: S = Q Kd^T  -> TMEM[0, K)
@@ -158,41 +185,45 @@ __global__ void __launch_bounds__(256, 1) dec1_kernel(Dec1Args a) {
                      tc::make_sdesc(aKd + ks * 2 * (16 * K), 16 * K, 128), idesc1, ks > 0);
       tc::mma_commit(&bar[0]);
     }
+    // row data for this tile (overlaps MMA1)
+    const int64_t grow = r0 + row;
+    const int32_t asg = row < valid ? a.assign[grow] : -1;
+    const float* grow_ptr = a.gt + (int64_t)(asg < 0 ? 0 : asg) * K + c0;
     tc::mbar_wait(&bar[0], ph[0]);
     ph[0] ^= 1;
     tc::tc_fence_after();
-    // ---- softmax: row max over both halves, then e = exp(S - max) (bf16) and the row sum
-    float sv[HC];  // this thread's half-row of S
+    // ---- softmax: row max, then e = exp(S - max) (bf16) and the row sum
+    float sv[QC];
 #pragma unroll
-    for (int c = 0; c < HC; c += 32) tc::tmem_ld32_nw(tl + h * HC + c, sv + c);
+    for (int c = 0; c < QC; c += 32) tc::tmem_ld32_nw(tl + c0 + c, sv + c);
     tc::tmem_wait_ld();
 #pragma unroll
-    for (int c = 0; c < HC; c += 32) tc::tmem_reg_fence32(sv + c);
+    for (int c = 0; c < QC; c += 32) tc::tmem_reg_fence32(sv + c);
     float mx = -INFINITY;
 #pragma unroll
-    for (int i = 0; i < HC; ++i) mx = fmaxf(mx, sv[i]);
-    s_red[(0 * 2 + h) * 128 + row] = mx;
+    for (int i = 0; i < QC; ++i) mx = fmaxf(mx, sv[i]);
+    red(0, qt) = mx;
     __syncthreads();
-    mx = fmaxf(s_red[row], s_red[128 + row]);
+    mx = fmaxf(fmaxf(red(0, 0), red(0, 1)), fmaxf(red(0, 2), red(0, 3)));
     const float mxl = mx * cl;
     float sum = 0.f;
 #pragma unroll
-    for (int c = 0; c < HC; c += 8) {
+    for (int c = 0; c < QC; c += 8) {
       uint4 u;
       u.x = tc::pack_bf16(ex2(fmaf(sv[c + 0], cl, -mxl)), ex2(fmaf(sv[c + 1], cl, -mxl)));
       u.y = tc::pack_bf16(ex2(fmaf(sv[c + 2], cl, -mxl)), ex2(fmaf(sv[c + 3], cl, -mxl)));
       u.z = tc::pack_bf16(ex2(fmaf(sv[c + 4], cl, -mxl)), ex2(fmaf(sv[c + 5], cl, -mxl)));
       u.w = tc::pack_bf16(ex2(fmaf(sv[c + 6], cl, -mxl)), ex2(fmaf(sv[c + 7], cl, -mxl)));
-      *reinterpret_cast<uint4*>(sP + tc::core_off(row, h * HC + c, 128u, kCS)) = u;
+      *reinterpret_cast<uint4*>(sP + tc::core_off(row, c0 + c, 128u, kCS)) = u;
       const uint32_t w4[4] = {u.x, u.y, u.z, u.w};  // sum the bf16-rounded e the MMA consumes
 #pragma unroll
       for (int j = 0; j < 4; ++j) sum += __uint_as_float(w4[j] << 16) + __uint_as_float(w4[j] & 0xffff0000u);
     }
-    s_red[(1 * 2 + h) * 128 + row] = sum;
+    red(1, qt) = sum;
     tc::fence_async_smem();
     tc::tc_fence_before();
     __syncthreads();
-    const float inv_sum = 1.f / (s_red[2 * 128 + row] + s_red[3 * 128 + row]);
+    const float inv_sum = 1.f / ((red(1, 0) + red(1, 1)) + (red(1, 2) + red(1, 3)));
     // ---- MMA2: t = e M -> TMEM[0, K) (S is dead)
     if (tid == 0) {
       tc::tc_fence_after();
@@ -202,48 +233,44 @@ __global__ void __launch_bounds__(256, 1) dec1_kernel(Dec1Args a) {
                      tc::make_sdesc(aM + ks * 2 * (16 * K), 16 * K, 128), idesc1, ks > 0);
       tc::mma_commit(&bar[1]);
     }
+    // warm L1 with the target-score row slice (overlaps MMA2)
+    if (lane == 0 || asg != __shfl_sync(0xffffffffu, asg, lane - 1))
+      for (int i = 0; i < QC; i += 32) asm volatile("prefetch.global.L1 [%0];" ::"l"(grow_ptr + i));
     tc::mbar_wait(&bar[1], ph[1]);
     ph[1] ^= 1;
     tc::tc_fence_after();
     // ---- per-row statistics: nu^2 = P.t, dot = P.G[a]   (P = e / sum, t = (e M) / sum)
-    const int64_t grow = r0 + row;
-    const int32_t asg = row < valid ? a.assign[grow] : -1;
-    const float* grow_ptr = a.gt + (int64_t)(asg < 0 ? 0 : asg) * K;
+    float tv[QC];
+#pragma unroll
+    for (int c = 0; c < QC; c += 32) tc::tmem_ld32_nw(tl + c0 + c, tv + c);
+    tc::tmem_wait_ld();
+#pragma unroll
+    for (int c = 0; c < QC; c += 32) tc::tmem_reg_fence32(tv + c);
     float nu2 = 0.f, dot = 0.f;
-    float tv[HC];
 #pragma unroll
-    for (int c = 0; c < HC; c += 32) tc::tmem_ld32_nw(tl + h * HC + c, tv + c);
-    {
-      float4 gq[HC / 4];
+    for (int c = 0; c < QC; c += 8) {
+      float e[8];
+      ld_row8(sP, row, c0 + c, kCS, e);
+      const float4 g0 = __ldg(reinterpret_cast<const float4*>(grow_ptr + c));
+      const float4 g1 = __ldg(reinterpret_cast<const float4*>(grow_ptr + c + 4));
+      const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
 #pragma unroll
-      for (int i = 0; i < HC / 4; ++i) gq[i] = __ldg(reinterpret_cast<const float4*>(grow_ptr + h * HC) + i);
-      tc::tmem_wait_ld();
-#pragma unroll
-      for (int c = 0; c < HC; c += 32) tc::tmem_reg_fence32(tv + c);
-#pragma unroll
-      for (int c = 0; c < HC; c += 8) {
-        float e[8];
-        ld_row8(sP, row, h * HC + c, kCS, e);
-        const float gv[8] = {gq[c / 4].x, gq[c / 4].y, gq[c / 4].z, gq[c / 4].w,
-                             gq[c / 4 + 1].x, gq[c / 4 + 1].y, gq[c / 4 + 1].z, gq[c / 4 + 1].w};
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          nu2 = fmaf(e[j], tv[c + j], nu2);
-          dot = fmaf(e[j], gv[j], dot);
-        }
+      for (int j = 0; j < 8; ++j) {
+        nu2 = fmaf(e[j], tv[c + j], nu2);
+        dot = fmaf(e[j], gv[j], dot);
       }
     }
-    s_red[(2 * 2 + h) * 128 + row] = nu2;
-    s_red[(3 * 2 + h) * 128 + row] = dot;
+    red(2, qt) = nu2;
+    red(3, qt) = dot;
     __syncthreads();
-    nu2 = (s_red[4 * 128 + row] + s_red[5 * 128 + row]) * inv_sum * inv_sum;
-    dot = (s_red[6 * 128 + row] + s_red[7 * 128 + row]) * inv_sum;
+    nu2 = ((red(2, 0) + red(2, 1)) + (red(2, 2) + red(2, 3))) * inv_sum * inv_sum;
+    dot = ((red(3, 0) + red(3, 1)) + (red(3, 2) + red(3, 3))) * inv_sum;
     float al = 0.f, be = 0.f, cc = 0.f;
     if (asg >= 0) {
       const float eps = 1e-8f;
       const float nu = sqrtf(fmaxf(nu2, 0.f)), vn = a.nv[asg];
       const float nug = fmaxf(nu, eps), nvg = fmaxf(vn, eps);
-      if (h == 0) {
+      if (qt == 0) {
         if (nu < eps || vn < eps) zflag = 1.0;
         cos_acc += 1.0 - (double)(dot / (nug * nvg));
         l2_acc += (double)nu2 - 2.0 * (double)dot + (double)vn * (double)vn;
@@ -252,7 +279,12 @@ __global__ void __launch_bounds__(256, 1) dec1_kernel(Dec1Args a) {
       be = a.scale * (-a.lambda_cos / (nug * nvg) * a.inv_nsup - 2.f * a.lambda_l2 * a.inv_nsup);
       cc = al * nu2 + be * dot;
     }
-    if (h == 0 && row < valid) a.row_stats[grow] = make_float4(mx, inv_sum, al, be);
+    if (qt == 0 && row < valid) a.row_stats[grow] = make_float4(mx, inv_sum, al, be);
+    // next tile's Q (consumed after this tile's MMA4 has read sQ)
+    if (tile + gridDim.x < ntiles) {
+      const int64_t nr0 = (tile + gridDim.x) * kRows;
+      q_fetch(nr0, (int)(a.npx - nr0 < kRows ? a.npx - nr0 : kRows));
+    }
     if (!a.want_grad) {
       tc::tc_fence_before();
       __syncthreads();
@@ -262,15 +294,15 @@ __global__ void __launch_bounds__(256, 1) dec1_kernel(Dec1Args a) {
     const float ps = inv_sum * a.inv_temp;  // P = e * inv_sum
     const float al_t = al * inv_sum;        // al * t = al * inv_sum * (e M)
 #pragma unroll
-    for (int c = 0; c < HC; c += 8) {
+    for (int c = 0; c < QC; c += 8) {
       float e[8];
-      ld_row8(sP, row, h * HC + c, kCS, e);
-      const float4 g0 = __ldg(reinterpret_cast<const float4*>(grow_ptr + h * HC + c));
-      const float4 g1 = __ldg(reinterpret_cast<const float4*>(grow_ptr + h * HC + c + 4));
+      ld_row8(sP, row, c0 + c, kCS, e);
+      const float4 g0 = __ldg(reinterpret_cast<const float4*>(grow_ptr + c));
+      const float4 g1 = __ldg(reinterpret_cast<const float4*>(grow_ptr + c + 4));
       const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
 #pragma unroll
       for (int j = 0; j < 8; ++j) e[j] = e[j] * ps * fmaf(al_t, tv[c + j], fmaf(be, gv[j], -cc));
-      st_row8(sP, row, h * HC + c, kCS, e);
+      st_row8(sP, row, c0 + c, kCS, e);
     }
     tc::fence_async_smem();
     tc::tc_fence_before();
@@ -294,7 +326,7 @@ __global__ void __launch_bounds__(256, 1) dec1_kernel(Dec1Args a) {
     tc::mbar_wait(&bar[2], ph[2]);
     ph[2] ^= 1;
     tc::tc_fence_after();
-    if (h == 0) {
+    if (qt == 0) {
       float v[DS];
 #pragma unroll
       for (int c = 0; c < DS; c += 16) tc::tmem_ld16(tl + kColDQ + c, v + c);  // warp-aligned: all lanes load
@@ -308,7 +340,7 @@ __global__ void __launch_bounds__(256, 1) dec1_kernel(Dec1Args a) {
     __syncthreads();
   }
   // ---- flush per-CTA partials: R^T rows k = 32g + lane (+128 mh)
-  if (h == 1) {
+  if (qt == 1) {
 #pragma unroll
     for (int mh = 0; mh < MH; ++mh) {
       float v[DS];
@@ -335,11 +367,11 @@ __global__ void __launch_bounds__(256, 1) dec1_kernel(Dec1Args a) {
   tc::tc_fence_before();
   __syncthreads();
   if (tid == 0) {
-    double c0 = 0, c1 = 0, c2 = 0;
-    for (int w = 0; w < 8; ++w) c0 += s_loss[w][0], c1 += s_loss[w][1], c2 += s_loss[w][2];
-    a.loss_part[blockIdx.x * 4 + 0] = c0;
-    a.loss_part[blockIdx.x * 4 + 1] = c1;
-    a.loss_part[blockIdx.x * 4 + 2] = c2;
+    double c0s = 0, c1s = 0, c2s = 0;
+    for (int w = 0; w < 16; ++w) c0s += s_loss[w][0], c1s += s_loss[w][1], c2s += s_loss[w][2];
+    a.loss_part[blockIdx.x * 4 + 0] = c0s;
+    a.loss_part[blockIdx.x * 4 + 1] = c1s;
+    a.loss_part[blockIdx.x * 4 + 2] = c2s;
   }
   if (warp == 0) tc::tmem_free<kTmemCols>(tmem);
 }
@@ -357,7 +389,7 @@ struct Dec2Args {
 };
 
 template <int K, int DS>
-__global__ void __launch_bounds__(256, 1) dec2_kernel(Dec2Args a) {
+__global__ void __launch_bounds__(512, 1) dec2_kernel(Dec2Args a) {
   constexpr int MH = K / 128, NH = K / 2, NB = 64;
   constexpr int kColA = 128, kColB = 128 + MH * NH;
   constexpr int kTmemCols = kColB + MH * NB <= 256 ? 256 : 512;
@@ -371,10 +403,10 @@ __global__ void __launch_bounds__(256, 1) dec2_kernel(Dec2Args a) {
   __shared__ uint64_t bar[2];
   __shared__ uint32_t s_taddr;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = warp & 3, h = warp >> 2;
+  const int g = warp & 3, h = warp >> 2;  // h: column quarter (0..3)
   const int row = 32 * g + lane;
   const int role = blockIdx.x & 1, group = blockIdx.x >> 1, ngroups = gridDim.x >> 1;
-  load_tile_bf16(sKd, a.kd, K, DS, K, tid, 256);
+  load_tile_bf16(sKd, a.kd, K, DS, K, tid, 512);
   if (tid == 0) {
     tc::mbar_init(&bar[0], 1);
     tc::mbar_init(&bar[1], 1);
@@ -396,7 +428,7 @@ __global__ void __launch_bounds__(256, 1) dec2_kernel(Dec2Args a) {
   for (int64_t tile = group; tile < ntiles; tile += ngroups) {
     const int64_t r0 = tile * kRows;
     const int valid = (int)(a.npx - r0 < kRows ? a.npx - r0 : kRows);
-    load_tile_bf16(sQ, a.query + r0 * DS, kRows, DS, valid, tid, 256);
+    load_tile_bf16(sQ, a.query + r0 * DS, kRows, DS, valid, tid, 512);
     float4 st = make_float4(0.f, 0.f, 0.f, 0.f);
     int32_t asg = -1;
     if (row < valid) {
@@ -421,8 +453,8 @@ __global__ void __launch_bounds__(256, 1) dec2_kernel(Dec2Args a) {
       ph[0] ^= 1;
       tc::tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < 64; c += 32) {
-        const int cc = h * 64 + c;
+      for (int c = 0; c < 32; c += 32) {
+        const int cc = h * 32 + c;
         float v[32], w[32];
         tc::tmem_ld32(tl + cc, v);
 #pragma unroll
@@ -441,7 +473,7 @@ __global__ void __launch_bounds__(256, 1) dec2_kernel(Dec2Args a) {
     }
     if (role == 0) {
 #pragma unroll
-      for (int c = h * 32; c < h * 32 + 32; c += 8) {
+      for (int c = h * 16; c < h * 16 + 16; c += 8) {
         float v[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = (asg == c + i) ? be : 0.f;
@@ -477,7 +509,7 @@ __global__ void __launch_bounds__(256, 1) dec2_kernel(Dec2Args a) {
   // drain: lane `row` of half mh holds A[mh*128 + row][role*NH + c], Bm[mh*128 + row][c]
   for (int mh = 0; mh < MH; ++mh) {
     float* dst = a.a_part + (((size_t)group * 2 + role) * K + mh * 128 + row) * NH;
-    for (int c = h * (NH / 2); c < (h + 1) * (NH / 2); c += 16) {
+    for (int c = h * (NH / 4); c < (h + 1) * (NH / 4); c += 16) {
       float v[16];
       if (first) {
         for (int i = 0; i < 16; ++i) v[i] = 0.f;
@@ -488,7 +520,7 @@ __global__ void __launch_bounds__(256, 1) dec2_kernel(Dec2Args a) {
     }
     if (role == 0) {
       float* db = a.bm_part + ((size_t)group * K + mh * 128 + row) * NB;
-      for (int c = h * (NB / 2); c < (h + 1) * (NB / 2); c += 16) {
+      for (int c = h * (NB / 4); c < (h + 1) * (NB / 4); c += 16) {
         float v[16];
         if (first) {
           for (int i = 0; i < 16; ++i) v[i] = 0.f;
@@ -553,13 +585,13 @@ void launch_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_
               n_sup > 0 ? 1.f / (float)n_sup : 0.f, scale, d_query, reinterpret_cast<float4*>(w.row_stats),
               w.r_part, w.loss_part, want_grad ? 1 : 0};
   const size_t sm1 = (size_t)kRows * DS * 2 + (size_t)K * DS * 2 + (size_t)kRows * K * 2 + (size_t)K * K * 2 +
-                     8 * 128 * 4;
+                     16 * 128 * 4;
   static bool attr1 = false;
   if (!attr1) {
     cudaFuncSetAttribute(dec1_kernel<K, DS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
     attr1 = true;
   }
-  dec1_kernel<K, DS><<<g1, 256, sm1, st>>>(d1);
+  dec1_kernel<K, DS><<<g1, 512, sm1, st>>>(d1);
   count_launch();
   if (!want_grad) {
     dec_reduce_kernel<<<1, 32, 0, st>>>(nullptr, nullptr, nullptr, w.loss_part, K, DS, 0, g1, 0, nullptr, nullptr,
@@ -576,7 +608,7 @@ void launch_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_
     cudaFuncSetAttribute(dec2_kernel<K, DS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
     attr2 = true;
   }
-  dec2_kernel<K, DS><<<g2, 256, sm2, st>>>(d2);
+  dec2_kernel<K, DS><<<g2, 512, sm2, st>>>(d2);
   count_launch();
   const int64_t tot = (int64_t)K * K + n_set * K + (int64_t)K * DS + 3;
   dec_reduce_kernel<<<(unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 8), 256, 0, st>>>(
