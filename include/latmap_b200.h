@@ -110,6 +110,8 @@ latmap_status latmap_ctx_synchronize(latmap_ctx* ctx);
  * (images within 1e-6 relative). alpha', clamp and termination decisions are exact in both. */
 latmap_status latmap_ctx_set_exact_blend(latmap_ctx* ctx, int32_t exact);
 const char* latmap_ctx_last_error(const latmap_ctx* ctx);
+/* The cudaStream_t the context's calls are ordered on (as void*). */
+void* latmap_ctx_stream(const latmap_ctx* ctx);
 /* Kernels launched by this context since creation (evidence for the bench). */
 int64_t latmap_ctx_launch_count(const latmap_ctx* ctx);
 void latmap_default_config(latmap_config* cfg);
@@ -228,6 +230,44 @@ latmap_status latmap_session_profile(latmap_session* s, int32_t enable);
 latmap_status latmap_session_phase_times(latmap_session* s, double* ms, int64_t* counts);
 /* Counters of the last objective: visible splats and tile pairs per frame (for roofline bytes). */
 latmap_status latmap_session_stats(latmap_session* s, int64_t* visible, int64_t* pairs);
+
+/* ---------------------------------------------------------------- voxel-hash store (config 3) */
+/* voxel_of (voxel_hash.cpp:9-16: double division + floor) and hash_voxel (voxel_hash.cpp:18-23:
+ * wrapping u32 multiply / xor, u64 modulo); host functions, bit-exact. */
+void latmap_voxel_of(const float p[3], float voxel_size, int32_t key[3]);
+int64_t latmap_hash_voxel(const int32_t key[3], int64_t capacity);
+
+/* VoxelHashStore (store/voxel_hash.hpp:25-73): fixed-capacity open-addressing table (linear
+ * probing, limit 8, one record per voxel) over an append-only record pool held in pinned,
+ * device-mapped host memory (the host-resident global map). Records are flat rows of
+ * 14 + query_dim floats: position 3, rotation 4, color 3, log_scale 3, opacity 1, features. */
+typedef struct latmap_store latmap_store;
+latmap_status latmap_store_create(latmap_ctx* ctx, int64_t capacity, int32_t query_dim, latmap_store** out);
+latmap_status latmap_store_destroy(latmap_store* s);
+int64_t latmap_store_size(const latmap_store* s);
+/* inserted, updated, rejected_duplicate, rejected_overflow, probe_steps (VoxelHashStore::Stats) */
+void latmap_store_stats(const latmap_store* s, int64_t out[5]);
+const char* latmap_store_last_error(const latmap_store* s);
+int64_t latmap_store_insert(latmap_store* s, const int32_t key[3], const float* rec); /* -1 = rejected */
+int32_t latmap_store_update(latmap_store* s, const int32_t key[3], const float* rec);
+int64_t latmap_store_find(latmap_store* s, const int32_t key[3]);
+latmap_status latmap_store_get_records(const latmap_store* s, int64_t first, int64_t count, float* out,
+                                       int32_t* keys_out);
+/* insert_global (voxel_hash.cpp:101-115): keys + home slots on the device, probe in row order. */
+latmap_status latmap_store_insert_global(latmap_store* s, const float* recs, int64_t n, float voxel_size,
+                                         int64_t* inserted);
+/* fetch_local (active_set.cpp:7-36): ascending record indices within `radius` (device radius scan +
+ * ordered compaction); optional gather of the records into device memory (d_records, AoS). */
+latmap_status latmap_store_fetch_local(latmap_store* s, const float center[3], float radius, int64_t* origin,
+                                       int64_t cap, int64_t* count, float* d_records);
+/* sync (active_set.cpp:38-128): writeback (dirty tracked rows scattered into the pinned pool in place,
+ * newborns inserted in row order), prune by radius, fetch the remaining in-radius records; output =
+ * kept rows (original order) ++ fetched records (ascending), gathered into d_out (device AoS).
+ * stats: written_back, newborn_inserted, newborn_rejected, pruned, fetched. */
+latmap_status latmap_store_sync(latmap_store* s, const float* d_active, const int64_t* origin, const uint8_t* dirty,
+                                int64_t n, const float center[3], float radius, float voxel_size, float* d_out,
+                                int64_t* out_origin, int64_t cap, uint8_t* kept_mask, int64_t stats[5],
+                                int64_t* out_count);
 
 /* ---------------------------------------------------------------- self-test */
 /* One-tile tcgen05 GEMM, C[128 x n] = A[128 x k] * B[n x k]^T (device fp32 in/out, bf16 staging),

@@ -128,6 +128,13 @@ def _declare(L):
         "latmap_session_stats": [P, P, P],
         "latmap_session_profile": [P, C.c_int32],
         "latmap_selftest_umma": [P, P, P, P, C.c_int32, C.c_int32, C.c_int32, C.c_int32],
+        "latmap_store_create": [P, C.c_int64, C.c_int32, C.POINTER(P)],
+        "latmap_store_destroy": [P],
+        "latmap_store_get_records": [P, C.c_int64, C.c_int64, P, P],
+        "latmap_store_insert_global": [P, P, C.c_int64, C.c_float, C.POINTER(C.c_int64)],
+        "latmap_store_fetch_local": [P, P, C.c_float, P, C.c_int64, C.POINTER(C.c_int64), P],
+        "latmap_store_sync": [P, P, P, P, C.c_int64, P, C.c_float, C.c_float, P, P, C.c_int64, P, P,
+                              C.POINTER(C.c_int64)],
         "latmap_session_phase_times": [P, P, P],
     }
     for name, args in sig.items():
@@ -140,6 +147,24 @@ def _declare(L):
     L.latmap_ctx_launch_count.restype = C.c_int64
     L.latmap_default_config.argtypes = [C.POINTER(Config)]
     L.latmap_default_config.restype = None
+    L.latmap_ctx_stream.argtypes = [P]
+    L.latmap_ctx_stream.restype = P
+    L.latmap_voxel_of.argtypes = [P, C.c_float, P]
+    L.latmap_voxel_of.restype = None
+    L.latmap_hash_voxel.argtypes = [P, C.c_int64]
+    L.latmap_hash_voxel.restype = C.c_int64
+    L.latmap_store_size.argtypes = [P]
+    L.latmap_store_size.restype = C.c_int64
+    L.latmap_store_stats.argtypes = [P, P]
+    L.latmap_store_stats.restype = None
+    L.latmap_store_last_error.argtypes = [P]
+    L.latmap_store_last_error.restype = C.c_char_p
+    L.latmap_store_insert.argtypes = [P, P, P]
+    L.latmap_store_insert.restype = C.c_int64
+    L.latmap_store_update.argtypes = [P, P, P]
+    L.latmap_store_update.restype = C.c_int32
+    L.latmap_store_find.argtypes = [P, P]
+    L.latmap_store_find.restype = C.c_int64
 
 
 EXPORTED = ["latmap_ctx_create", "latmap_ctx_destroy", "latmap_ctx_set_stream", "latmap_ctx_synchronize",
@@ -153,7 +178,11 @@ EXPORTED = ["latmap_ctx_create", "latmap_ctx_destroy", "latmap_ctx_set_stream", 
             "latmap_session_set_batch", "latmap_session_set_slot_offset", "latmap_session_objective",
             "latmap_session_apply", "latmap_session_step", "latmap_session_grad_buffer", "latmap_session_loss_buffer",
             "latmap_session_read_loss", "latmap_session_frame_images", "latmap_session_stats",
-            "latmap_session_profile", "latmap_session_phase_times", "latmap_selftest_umma"]
+            "latmap_session_profile", "latmap_session_phase_times", "latmap_selftest_umma", "latmap_ctx_stream",
+            "latmap_voxel_of", "latmap_hash_voxel", "latmap_store_create", "latmap_store_destroy", "latmap_store_size",
+            "latmap_store_stats", "latmap_store_last_error", "latmap_store_insert", "latmap_store_update",
+            "latmap_store_find", "latmap_store_get_records", "latmap_store_insert_global", "latmap_store_fetch_local",
+            "latmap_store_sync"]
 
 
 def check(ctx_handle, status):

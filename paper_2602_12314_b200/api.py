@@ -381,3 +381,112 @@ def _device_view(ptr, count, dtype, device):
     typestr = "<f4" if dtype == torch.float32 else "<f8"
     with torch.cuda.device(device):
         return torch.as_tensor(_CudaArrayView(ptr, count, typestr), device=f"cuda:{device}")
+
+
+# ----------------------------------------------------------------------------- voxel-hash store
+def voxel_of(p, voxel_size):
+    """voxel_of (voxel_hash.cpp:9-16), host."""
+    pa = np.ascontiguousarray(p, np.float32)
+    k = np.zeros(3, np.int32)
+    lib().latmap_voxel_of(pa.ctypes.data_as(C.c_void_p), float(voxel_size), k.ctypes.data_as(C.c_void_p))
+    return tuple(int(v) for v in k)
+
+
+def hash_voxel(key, capacity):
+    """hash_voxel (voxel_hash.cpp:18-23), host."""
+    k = np.ascontiguousarray(key, np.int32)
+    return lib().latmap_hash_voxel(k.ctypes.data_as(C.c_void_p), int(capacity))
+
+
+class Store:
+    """VoxelHashStore with a pinned, device-mapped record pool (store/voxel_hash.hpp:25-73)."""
+
+    def __init__(self, ctx, capacity, query_dim):
+        self.ctx, self.ds, self.rs = ctx, query_dim, 14 + query_dim
+        h = C.c_void_p()
+        check(ctx.h, lib().latmap_store_create(ctx.h, int(capacity), int(query_dim), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().latmap_store_destroy(self.h)
+            self.h = None
+
+    def _check(self, st):
+        if st != _capi.OK:
+            msg = (lib().latmap_store_last_error(self.h) or b"").decode()
+            if st == _capi.EINVAL:
+                raise _capi.InvalidArgument(msg)
+            raise _capi.LatmapError(msg)
+
+    def size(self):
+        return lib().latmap_store_size(self.h)
+
+    def stats(self):
+        o = np.zeros(5, np.int64)
+        lib().latmap_store_stats(self.h, o.ctypes.data_as(C.c_void_p))
+        return dict(zip(("inserted", "updated", "rejected_duplicate", "rejected_overflow", "probe_steps"), o.tolist()))
+
+    def insert(self, key, rec):
+        k = np.ascontiguousarray(key, np.int32)
+        r = np.ascontiguousarray(rec, np.float32)
+        return lib().latmap_store_insert(self.h, k.ctypes.data_as(C.c_void_p), r.ctypes.data_as(C.c_void_p))
+
+    def update(self, key, rec):
+        k = np.ascontiguousarray(key, np.int32)
+        r = np.ascontiguousarray(rec, np.float32)
+        return bool(lib().latmap_store_update(self.h, k.ctypes.data_as(C.c_void_p), r.ctypes.data_as(C.c_void_p)))
+
+    def find(self, key):
+        k = np.ascontiguousarray(key, np.int32)
+        return lib().latmap_store_find(self.h, k.ctypes.data_as(C.c_void_p))
+
+    def records(self):
+        n = self.size()
+        out = np.zeros((n, self.rs), np.float32)
+        keys = np.zeros((n, 3), np.int32)
+        if n:
+            self._check(lib().latmap_store_get_records(self.h, 0, n, out.ctypes.data_as(C.c_void_p),
+                                                       keys.ctypes.data_as(C.c_void_p)))
+        return out, keys
+
+    def insert_global(self, recs, voxel_size):
+        r = np.ascontiguousarray(recs, np.float32).reshape(-1, self.rs)
+        ins = C.c_int64(0)
+        self._check(lib().latmap_store_insert_global(self.h, r.ctypes.data_as(C.c_void_p), r.shape[0],
+                                                     float(voxel_size), C.byref(ins)))
+        return ins.value
+
+    def fetch_local(self, center, radius, gather=False):
+        c = np.ascontiguousarray(center, np.float32)
+        cnt = C.c_int64(0)
+        cap = self.size() + 1
+        org = np.zeros(cap, np.int64)
+        d = torch.empty((cap, self.rs), device=f"cuda:{self.ctx.device}") if gather else None
+        self._check(lib().latmap_store_fetch_local(self.h, c.ctypes.data_as(C.c_void_p), float(radius),
+                                                   org.ctypes.data_as(C.c_void_p), cap, C.byref(cnt),
+                                                   C.c_void_p(d.data_ptr()) if gather else None))
+        n = cnt.value
+        return (org[:n].copy(), d[:n]) if gather else org[:n].copy()
+
+    def sync(self, d_active, origin, dirty, center, radius, voxel_size):
+        """d_active: torch CUDA (n, 14+ds) records; returns (d_out, out_origin, kept_mask, stats)."""
+        n = 0 if d_active is None else d_active.shape[0]
+        org = np.ascontiguousarray(origin, np.int64)
+        dty = np.ascontiguousarray(dirty, np.uint8)
+        c = np.ascontiguousarray(center, np.float32)
+        cap = self.size() + n + 1
+        d_out = torch.empty((cap, self.rs), device=f"cuda:{self.ctx.device}")
+        oo = np.zeros(cap, np.int64)
+        kept = np.zeros(max(n, 1), np.uint8)
+        st = np.zeros(5, np.int64)
+        cnt = C.c_int64(0)
+        dptr = C.c_void_p(d_active.data_ptr()) if n else None
+        self._check(lib().latmap_store_sync(self.h, dptr, org.ctypes.data_as(C.c_void_p), dty.ctypes.data_as(C.c_void_p),
+                                            n, c.ctypes.data_as(C.c_void_p), float(radius), float(voxel_size),
+                                            C.c_void_p(d_out.data_ptr()), oo.ctypes.data_as(C.c_void_p), cap,
+                                            kept.ctypes.data_as(C.c_void_p), st.ctypes.data_as(C.c_void_p),
+                                            C.byref(cnt)))
+        w = cnt.value
+        stats = dict(zip(("written_back", "newborn_inserted", "newborn_rejected", "pruned", "fetched"), st.tolist()))
+        return d_out[:w], oo[:w].copy(), kept[:n].astype(bool), stats

@@ -249,6 +249,8 @@ latmap_status latmap_ctx_synchronize(latmap_ctx* ctx) {
 
 const char* latmap_ctx_last_error(const latmap_ctx* ctx) { return ctx ? ctx->err.c_str() : t_err.c_str(); }
 
+void* latmap_ctx_stream(const latmap_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
 int64_t latmap_ctx_launch_count(const latmap_ctx* ctx) { return g_launches.load() - (ctx ? ctx->launches0 : 0); }
 
 // ------------------------------------------------------------------------------- renderer

@@ -234,7 +234,8 @@ __global__ void __launch_bounds__(512, 1) dec1_kernel(Dec1Args a) {
       tc::mma_commit(&bar[1]);
     }
     // warm L1 with the target-score row slice (overlaps MMA2)
-    if (lane == 0 || asg != __shfl_sync(0xffffffffu, asg, lane - 1))
+    const int32_t asg_prev = __shfl_up_sync(0xffffffffu, asg, 1);  // all lanes take part
+    if (lane == 0 || asg != asg_prev)
       for (int i = 0; i < QC; i += 32) asm volatile("prefetch.global.L1 [%0];" ::"l"(grow_ptr + i));
     tc::mbar_wait(&bar[1], ph[1]);
     ph[1] ^= 1;

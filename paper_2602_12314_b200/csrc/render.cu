@@ -600,13 +600,15 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
       const bool contrib = j < cnt && inside && idx < last && px >= s.x0 && px <= s.x1 && py >= s.y0 && py <= s.y1;
       float w = 0.f, drho = 0.f, dg = 0.f;
       if (contrib) {
-        const float dx = fs(fx, s.mean_x);
-        const float dy = fs(fy, s.mean_y);
-        const float rho = fa(fa(fm(fm(s.a00, dx), dx), fm(fm(fm(2.f, s.a01), dx), dy)), fm(fm(s.a11, dy), dy));
-        float al = fm(s.alpha, exp_exact(fm(-0.5f, rho)));
+        // replay of the forward blend; the set of blended (pixel, splat) pairs comes from the
+        // forward (px_last), so alpha' only needs gradient accuracy here (fast exp / rcp).
+        const float dx = fx - s.mean_x;
+        const float dy = fy - s.mean_y;
+        const float rho = fmaf(s.a00 * dx, dx, fmaf(2.f * s.a01 * dx, dy, s.a11 * dy * dy));
+        float al = s.alpha * __expf(-0.5f * rho);
         const bool clamped = al > kAlphaMax;
         if (clamped) al = kAlphaMax;
-        const float r = 1.f / fs(1.f, al);
+        const float r = __frcp_rn(1.f - al);
         const float Tb = T * r;
         w = al * Tb;
         const float* fr = s_f + j * NU;
@@ -616,7 +618,7 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
         const float d_alpha = Tb * value - s_after * r;
         s_after = fmaf(w, value, s_after);
         if (!clamped) {
-          dg = d_alpha * (al / s.alpha);
+          dg = d_alpha * __fdividef(al, s.alpha);
           drho = -0.5f * al * d_alpha;
         }
         T = Tb;

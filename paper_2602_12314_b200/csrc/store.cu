@@ -1,0 +1,594 @@
+// store.cu — voxel-hash global map store and the active-set gather / scatter (K11).
+//
+// Reference: voxel_of / hash_voxel / VoxelHashStore / insert_global (proj/src/voxel_hash.cpp:9-115)
+// and fetch_local / sync (proj/src/active_set.cpp:7-128).
+//
+// The global record pool lives in pinned, device-mapped host memory (the host-resident
+// global map); a device mirror of the record positions serves the radius scans. The hash
+// table stays on the host and is probed sequentially (insertion order defines record indices
+// and duplicate / overflow rejections, voxel_hash.cpp:35-71), with voxel keys and hashes for a
+// batch computed on the device (double-precision floor, wrapping u32 multiply / xor, u64 mod).
+// fetch_local / the fetch step of sync are a device radius test (the reference's float op
+// order, no FMA) over the whole pool mirror with an order-preserving compaction, and the
+// gather reads the selected records from mapped host memory straight into device buffers;
+// the writeback scatter writes device records back into the pinned pool.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/latmap_b200.h"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace lm {
+
+namespace {
+
+constexpr int kProbeLimit = 8;
+
+__host__ __device__ inline void voxel_of(const float* p, float vs, int32_t* k) {
+  k[0] = (int32_t)floor((double)p[0] / (double)vs);
+  k[1] = (int32_t)floor((double)p[1] / (double)vs);
+  k[2] = (int32_t)floor((double)p[2] / (double)vs);
+}
+__host__ __device__ inline int64_t hash_voxel(const int32_t* k, int64_t cap) {
+  const uint32_t h = ((uint32_t)k[0] * 73856093u) ^ ((uint32_t)k[1] * 19349663u) ^ ((uint32_t)k[2] * 83492791u);
+  return (int64_t)((uint64_t)h % (uint64_t)cap);
+}
+
+// K11a: keys and home slots of a batch of records (AoS, rs floats each, position first).
+__global__ void keys_kernel(const float* __restrict__ recs, int64_t n, int rs, float vs, int64_t cap,
+                            int32_t* __restrict__ keys, int64_t* __restrict__ home) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t k[3];
+    voxel_of(recs + i * rs, vs, k);
+    keys[3 * i] = k[0];
+    keys[3 * i + 1] = k[1];
+    keys[3 * i + 2] = k[2];
+    home[i] = hash_voxel(k, cap);
+  }
+}
+
+// Radius test in the reference's float order: dx*dx + dy*dy + dz*dz <= r2 (active_set.cpp:16-19).
+__device__ __forceinline__ bool in_radius(const float* p, float cx, float cy, float cz, float r2) {
+  const float dx = fs(p[0], cx), dy = fs(p[1], cy), dz = fs(p[2], cz);
+  return fa(fa(fm(dx, dx), fm(dy, dy)), fm(dz, dz)) <= r2;
+}
+
+// K11b: per-block counts of in-radius, not-present pool records.
+constexpr int kScanBlock = 1024;
+__global__ void __launch_bounds__(kScanBlock) radius_count_kernel(const float* __restrict__ pos, int64_t n, float cx,
+                                                                   float cy, float cz, float r2,
+                                                                   const uint8_t* __restrict__ present,
+                                                                   int32_t* __restrict__ block_counts) {
+  const int64_t i = blockIdx.x * (int64_t)kScanBlock + threadIdx.x;
+  const bool hit = i < n && (!present || !present[i]) && in_radius(pos + 3 * i, cx, cy, cz, r2);
+  const int c = __syncthreads_count(hit);
+  if (threadIdx.x == 0) block_counts[blockIdx.x] = c;
+}
+
+// K11c: exclusive scan of the block counts (one block, loops over chunks).
+__global__ void __launch_bounds__(1024) block_scan_kernel(int32_t* counts, int64_t nblocks, int64_t* total) {
+  __shared__ int64_t s[1024];
+  int64_t carry = 0;
+  for (int64_t base = 0; base < nblocks; base += 1024) {
+    const int64_t i = base + threadIdx.x;
+    const int64_t v = i < nblocks ? counts[i] : 0;
+    s[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+      const int64_t t = threadIdx.x >= (unsigned)o ? s[threadIdx.x - o] : 0;
+      __syncthreads();
+      s[threadIdx.x] += t;
+      __syncthreads();
+    }
+    if (i < nblocks) counts[i] = (int32_t)(carry + s[threadIdx.x] - v);
+    const int64_t blk = s[1023];
+    __syncthreads();
+    carry += blk;
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+// K11d: order-preserving compaction of the hits (ascending record index).
+__global__ void __launch_bounds__(kScanBlock) radius_emit_kernel(const float* __restrict__ pos, int64_t n, float cx,
+                                                                  float cy, float cz, float r2,
+                                                                  const uint8_t* __restrict__ present,
+                                                                  const int32_t* __restrict__ block_offsets,
+                                                                  int64_t* __restrict__ out) {
+  __shared__ int32_t s_warp[kScanBlock / 32];
+  const int64_t i = blockIdx.x * (int64_t)kScanBlock + threadIdx.x;
+  const bool hit = i < n && (!present || !present[i]) && in_radius(pos + 3 * i, cx, cy, cz, r2);
+  const unsigned m = __ballot_sync(0xffffffffu, hit);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) s_warp[w] = __popc(m);
+  __syncthreads();
+  if (w == 0) {
+    int v = s_warp[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += t;
+    }
+    s_warp[lane] = v - s_warp[lane];  // exclusive
+  }
+  __syncthreads();
+  if (hit) out[block_offsets[blockIdx.x] + s_warp[w] + __popc(m & ((1u << lane) - 1u))] = i;
+}
+
+// K11e: gather records (mapped host pool -> device AoS) and scatter (device AoS -> mapped pool).
+__global__ void gather_kernel(const float* __restrict__ pool, const int64_t* __restrict__ idx, int64_t n, int rs,
+                              float* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * rs; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / rs, c = e % rs;
+    out[e] = pool[idx[r] * rs + c];
+  }
+}
+__global__ void scatter_rec_kernel(float* __restrict__ pool, float* __restrict__ pos_mirror,
+                                   const int64_t* __restrict__ idx, int64_t n, int rs, const float* __restrict__ in) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * rs; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / rs, c = e % rs;
+    const float v = in[e];
+    pool[idx[r] * rs + c] = v;
+    if (c < 3) pos_mirror[idx[r] * 3 + c] = v;
+  }
+}
+// prune test for the active entries + present flags of the kept records
+__global__ void prune_kernel(const float* __restrict__ recs, const int64_t* __restrict__ resolved, int64_t n, int rs,
+                             float cx, float cy, float cz, float r2, uint8_t* __restrict__ kept,
+                             uint8_t* __restrict__ present) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rr = resolved[i];
+    const bool k = rr >= 0 && in_radius(recs + i * rs, cx, cy, cz, r2);
+    kept[i] = k;
+    if (k) present[rr] = 1;
+  }
+}
+__global__ void copy_rows_kernel(const float* __restrict__ in, const int64_t* __restrict__ rows, int64_t n, int rs,
+                                 float* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * rs; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / rs, c = e % rs;
+    out[e] = in[rows[r] * rs + c];
+  }
+}
+
+inline unsigned grid_of(int64_t n, int per = 256) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + per - 1) / per, 148 * 16));
+}
+
+}  // namespace
+
+}  // namespace lm
+
+using namespace lm;
+
+struct latmap_store {
+  latmap_ctx* ctx = nullptr;
+  cudaStream_t st = nullptr;
+  int64_t capacity = 0;
+  int32_t ds = 0, rs = 0;
+  struct Slot {
+    int64_t record = -1;
+    int32_t key[3] = {0, 0, 0};
+  };
+  std::vector<Slot> slots;
+  float* pool = nullptr;  // pinned + mapped host memory, pool_cap x rs
+  float* pool_dev = nullptr;  // device alias of `pool`
+  int64_t pool_cap = 0, size = 0;
+  std::vector<int32_t> keys;  // 3 per record
+  int64_t stats[5] = {0, 0, 0, 0, 0};
+  float* d_pos = nullptr;  // device mirror of record positions
+  int64_t d_pos_cap = 0;
+  // scratch
+  std::string err;
+};
+
+namespace {
+
+latmap_status sfail(latmap_store* s, latmap_status code, const std::string& msg) {
+  if (s) s->err = msg;
+  return code;
+}
+#define S_CHECK(s, expr)                                                              \
+  do {                                                                                \
+    cudaError_t _e = (expr);                                                          \
+    if (_e != cudaSuccess) return sfail(s, LATMAP_ERR_CUDA, cudaGetErrorString(_e));  \
+  } while (0)
+
+latmap_status ensure_pool(latmap_store* s, int64_t need) {
+  if (need <= s->pool_cap) return LATMAP_OK;
+  int64_t cap = std::max<int64_t>(need, std::max<int64_t>(1024, s->pool_cap * 2));
+  float* np = nullptr;
+  S_CHECK(s, cudaHostAlloc(&np, sizeof(float) * cap * s->rs, cudaHostAllocMapped));
+  if (s->pool) {
+    std::memcpy(np, s->pool, sizeof(float) * s->size * s->rs);
+    cudaFreeHost(s->pool);
+  }
+  s->pool = np;
+  S_CHECK(s, cudaHostGetDevicePointer(&s->pool_dev, np, 0));
+  s->pool_cap = cap;
+  float* nd = nullptr;
+  S_CHECK(s, cudaMalloc(&nd, sizeof(float) * cap * 3));
+  if (s->d_pos) {
+    S_CHECK(s, cudaMemcpyAsync(nd, s->d_pos, sizeof(float) * s->size * 3, cudaMemcpyDeviceToDevice, s->st));
+    S_CHECK(s, cudaStreamSynchronize(s->st));
+    cudaFree(s->d_pos);
+  }
+  s->d_pos = nd;
+  s->d_pos_cap = cap;
+  return LATMAP_OK;
+}
+
+// VoxelHashStore::probe (voxel_hash.cpp:35-50) with a precomputed home slot.
+int64_t probe(latmap_store* s, const int32_t* key, int64_t home, bool for_insert, int64_t* free_slot) {
+  if (free_slot) *free_slot = -1;
+  const int limit = (int)std::min<int64_t>(kProbeLimit, s->capacity);
+  for (int i = 0; i < limit; ++i) {
+    const int64_t sl = (home + i) % s->capacity;
+    const latmap_store::Slot& slot = s->slots[sl];
+    ++s->stats[4];
+    if (slot.record < 0) {
+      if (for_insert && free_slot && *free_slot < 0) *free_slot = sl;
+      return -1;
+    }
+    if (slot.key[0] == key[0] && slot.key[1] == key[1] && slot.key[2] == key[2]) return sl;
+  }
+  return -1;
+}
+
+// VoxelHashStore::insert (voxel_hash.cpp:52-71); record written into the pinned pool.
+int64_t insert_one(latmap_store* s, const int32_t* key, int64_t home, const float* rec, bool rec_on_device,
+                   float* d_stage) {
+  int64_t free_slot = -1;
+  if (probe(s, key, home, true, &free_slot) >= 0) {
+    ++s->stats[2];
+    return -1;
+  }
+  if (free_slot < 0) {
+    ++s->stats[3];
+    return -1;
+  }
+  if (ensure_pool(s, s->size + 1) != LATMAP_OK) return -2;
+  const int64_t r = s->size++;
+  if (!rec_on_device) std::memcpy(s->pool + r * s->rs, rec, sizeof(float) * s->rs);
+  (void)d_stage;
+  s->keys.insert(s->keys.end(), key, key + 3);
+  s->slots[free_slot].record = r;
+  std::memcpy(s->slots[free_slot].key, key, 12);
+  ++s->stats[0];
+  return r;
+}
+
+}  // namespace
+
+extern "C" {
+
+void latmap_voxel_of(const float p[3], float voxel_size, int32_t key[3]) { lm::voxel_of(p, voxel_size, key); }
+
+int64_t latmap_hash_voxel(const int32_t key[3], int64_t capacity) {
+  return capacity > 0 ? lm::hash_voxel(key, capacity) : -1;
+}
+
+latmap_status latmap_store_create(latmap_ctx* ctx, int64_t capacity, int32_t query_dim, latmap_store** out) {
+  if (!ctx || !out || capacity <= 0 || query_dim < 1) return LATMAP_ERR_INVALID_ARGUMENT;
+  auto* s = new latmap_store();
+  s->ctx = ctx;
+  s->st = (cudaStream_t)latmap_ctx_stream(ctx);
+  s->capacity = capacity;
+  s->ds = query_dim;
+  s->rs = 14 + query_dim;
+  s->slots.resize((size_t)capacity);
+  *out = s;
+  return LATMAP_OK;
+}
+
+latmap_status latmap_store_destroy(latmap_store* s) {
+  if (!s) return LATMAP_ERR_INVALID_ARGUMENT;
+  cudaDeviceSynchronize();
+  if (s->pool) cudaFreeHost(s->pool);
+  if (s->d_pos) cudaFree(s->d_pos);
+  delete s;
+  return LATMAP_OK;
+}
+
+int64_t latmap_store_size(const latmap_store* s) { return s ? s->size : -1; }
+
+void latmap_store_stats(const latmap_store* s, int64_t out[5]) {
+  if (s && out) std::memcpy(out, s->stats, sizeof(s->stats));
+}
+
+const char* latmap_store_last_error(const latmap_store* s) { return s ? s->err.c_str() : ""; }
+
+int64_t latmap_store_insert(latmap_store* s, const int32_t key[3], const float* rec) {
+  if (!s || !rec) return -1;
+  const int64_t r = insert_one(s, key, lm::hash_voxel(key, s->capacity), rec, false, nullptr);
+  if (r >= 0) {
+    cudaMemcpyAsync(s->d_pos + r * 3, rec, 12, cudaMemcpyHostToDevice, s->st);
+    cudaStreamSynchronize(s->st);
+  }
+  return r;
+}
+
+int32_t latmap_store_update(latmap_store* s, const int32_t key[3], const float* rec) {
+  if (!s || !rec) return 0;
+  const int64_t hit = probe(s, key, lm::hash_voxel(key, s->capacity), false, nullptr);
+  if (hit < 0) return 0;
+  const int64_t r = s->slots[hit].record;
+  std::memcpy(s->pool + r * s->rs, rec, sizeof(float) * s->rs);
+  cudaMemcpyAsync(s->d_pos + r * 3, rec, 12, cudaMemcpyHostToDevice, s->st);
+  cudaStreamSynchronize(s->st);
+  ++s->stats[1];
+  return 1;
+}
+
+int64_t latmap_store_find(latmap_store* s, const int32_t key[3]) {
+  if (!s) return -1;
+  const int64_t hit = probe(s, key, lm::hash_voxel(key, s->capacity), false, nullptr);
+  return hit < 0 ? -1 : s->slots[hit].record;
+}
+
+latmap_status latmap_store_get_records(const latmap_store* s, int64_t first, int64_t count, float* out,
+                                       int32_t* keys_out) {
+  if (!s || first < 0 || first + count > s->size) return LATMAP_ERR_INVALID_ARGUMENT;
+  cudaStreamSynchronize(s->st);
+  if (out) std::memcpy(out, s->pool + first * s->rs, sizeof(float) * count * s->rs);
+  if (keys_out) std::memcpy(keys_out, s->keys.data() + first * 3, sizeof(int32_t) * count * 3);
+  return LATMAP_OK;
+}
+
+// insert_global (voxel_hash.cpp:101-115): keys / home slots on the device, sequential probe on
+// the host in record order (identical record indices and rejections).
+latmap_status latmap_store_insert_global(latmap_store* s, const float* recs, int64_t n, float voxel_size,
+                                         int64_t* inserted) {
+  if (!s || (n > 0 && !recs)) return LATMAP_ERR_INVALID_ARGUMENT;
+  if (!(voxel_size > 0.f)) return sfail(s, LATMAP_ERR_INVALID_ARGUMENT, "voxel_of: voxel_size must be > 0");
+  if (inserted) *inserted = 0;
+  if (n == 0) return LATMAP_OK;
+  float* d_recs = nullptr;
+  int32_t* d_keys = nullptr;
+  int64_t* d_home = nullptr;
+  S_CHECK(s, cudaMallocAsync(&d_recs, sizeof(float) * n * s->rs, s->st));
+  S_CHECK(s, cudaMallocAsync(&d_keys, sizeof(int32_t) * n * 3, s->st));
+  S_CHECK(s, cudaMallocAsync(&d_home, sizeof(int64_t) * n, s->st));
+  S_CHECK(s, cudaMemcpyAsync(d_recs, recs, sizeof(float) * n * s->rs, cudaMemcpyHostToDevice, s->st));
+  keys_kernel<<<grid_of(n), 256, 0, s->st>>>(d_recs, n, s->rs, voxel_size, s->capacity, d_keys, d_home);
+  count_launch();
+  std::vector<int32_t> keys((size_t)n * 3);
+  std::vector<int64_t> home((size_t)n);
+  S_CHECK(s, cudaMemcpyAsync(keys.data(), d_keys, sizeof(int32_t) * n * 3, cudaMemcpyDeviceToHost, s->st));
+  S_CHECK(s, cudaMemcpyAsync(home.data(), d_home, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s->st));
+  S_CHECK(s, cudaStreamSynchronize(s->st));
+  if (ensure_pool(s, s->size + n) != LATMAP_OK) return LATMAP_ERR_OUT_OF_MEMORY;
+  const int64_t first = s->size;
+  int64_t ins = 0;
+  for (int64_t i = 0; i < n; ++i) ins += insert_one(s, &keys[3 * i], home[i], recs + i * s->rs, false, nullptr) >= 0;
+  // position mirror for the new records
+  std::vector<float> pos((size_t)(s->size - first) * 3);
+  for (int64_t r = first; r < s->size; ++r) std::memcpy(&pos[(r - first) * 3], s->pool + r * s->rs, 12);
+  if (!pos.empty())
+    S_CHECK(s, cudaMemcpyAsync(s->d_pos + first * 3, pos.data(), sizeof(float) * pos.size(), cudaMemcpyHostToDevice,
+                               s->st));
+  S_CHECK(s, cudaFreeAsync(d_recs, s->st));
+  S_CHECK(s, cudaFreeAsync(d_keys, s->st));
+  S_CHECK(s, cudaFreeAsync(d_home, s->st));
+  S_CHECK(s, cudaStreamSynchronize(s->st));
+  if (inserted) *inserted = ins;
+  return LATMAP_OK;
+}
+
+// fetch_local (active_set.cpp:7-36): ascending record indices of the records within `radius`,
+// optional gather of their records into a device AoS buffer (records x (14 + ds) floats).
+latmap_status latmap_store_fetch_local(latmap_store* s, const float center[3], float radius, int64_t* origin,
+                                       int64_t cap, int64_t* count, float* d_records) {
+  if (!s || !count) return LATMAP_ERR_INVALID_ARGUMENT;
+  if (!(radius > 0.f)) return sfail(s, LATMAP_ERR_INVALID_ARGUMENT, "fetch_local: radius must be > 0");
+  *count = 0;
+  if (s->size == 0) return LATMAP_OK;
+  const float r2 = radius * radius;
+  const int64_t nb = (s->size + kScanBlock - 1) / kScanBlock;
+  int32_t* d_cnt = nullptr;
+  int64_t* d_total = nullptr;
+  int64_t* d_idx = nullptr;
+  S_CHECK(s, cudaMallocAsync(&d_cnt, sizeof(int32_t) * nb, s->st));
+  S_CHECK(s, cudaMallocAsync(&d_total, sizeof(int64_t), s->st));
+  S_CHECK(s, cudaMallocAsync(&d_idx, sizeof(int64_t) * s->size, s->st));
+  radius_count_kernel<<<(unsigned)nb, kScanBlock, 0, s->st>>>(s->d_pos, s->size, center[0], center[1], center[2], r2,
+                                                               nullptr, d_cnt);
+  block_scan_kernel<<<1, 1024, 0, s->st>>>(d_cnt, nb, d_total);
+  radius_emit_kernel<<<(unsigned)nb, kScanBlock, 0, s->st>>>(s->d_pos, s->size, center[0], center[1], center[2], r2,
+                                                              nullptr, d_cnt, d_idx);
+  count_launch(3);
+  int64_t total = 0;
+  S_CHECK(s, cudaMemcpyAsync(&total, d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, s->st));
+  S_CHECK(s, cudaStreamSynchronize(s->st));
+  *count = total;
+  latmap_status ret = LATMAP_OK;
+  if (origin) {
+    if (total > cap) {
+      ret = sfail(s, LATMAP_ERR_INVALID_ARGUMENT, "fetch_local: output capacity too small");
+    } else if (total > 0) {
+      S_CHECK(s, cudaMemcpyAsync(origin, d_idx, sizeof(int64_t) * total, cudaMemcpyDeviceToHost, s->st));
+    }
+  }
+  if (d_records && total > 0 && ret == LATMAP_OK) {
+    gather_kernel<<<grid_of(total * s->rs), 256, 0, s->st>>>(s->pool_dev, d_idx, total, s->rs, d_records);
+    count_launch();
+  }
+  S_CHECK(s, cudaFreeAsync(d_cnt, s->st));
+  S_CHECK(s, cudaFreeAsync(d_total, s->st));
+  S_CHECK(s, cudaFreeAsync(d_idx, s->st));
+  S_CHECK(s, cudaStreamSynchronize(s->st));
+  return ret;
+}
+
+// sync (active_set.cpp:38-128). Active records live on the device (AoS, n x (14 + ds));
+// origin / dirty / kept_mask / out_origin are host arrays; out_records is a device buffer.
+// stats: written_back, newborn_inserted, newborn_rejected, pruned, fetched.
+latmap_status latmap_store_sync(latmap_store* s, const float* d_active, const int64_t* origin, const uint8_t* dirty,
+                                int64_t n, const float center[3], float radius, float voxel_size, float* d_out,
+                                int64_t* out_origin, int64_t cap, uint8_t* kept_mask, int64_t stats_out[5],
+                                int64_t* out_count) {
+  if (!s || !center || !out_count || (n > 0 && (!d_active || !origin || !dirty))) return LATMAP_ERR_INVALID_ARGUMENT;
+  if (!(voxel_size > 0.f)) return sfail(s, LATMAP_ERR_INVALID_ARGUMENT, "voxel_of: voxel_size must be > 0");
+  const int rs = s->rs;
+  int64_t st5[5] = {0, 0, 0, 0, 0};
+  std::vector<int64_t> resolved((size_t)std::max<int64_t>(n, 1), -1);
+  // ---- step 1: writeback. Dirty tracked entries overwrite their record in place (origin voxel
+  // retained); newborns insert under the voxel of their optimised position, in row order.
+  std::vector<int64_t> wb_rows, wb_idx, nb_rows;
+  for (int64_t i = 0; i < n; ++i) {
+    if (origin[i] >= 0) {
+      resolved[i] = origin[i];
+      if (dirty[i]) {
+        wb_rows.push_back(i);
+        wb_idx.push_back(origin[i]);
+      }
+    } else {
+      nb_rows.push_back(i);
+    }
+  }
+  int64_t *d_rows = nullptr, *d_idx2 = nullptr;
+  const int64_t nwb = (int64_t)wb_rows.size();
+  if (nwb > 0) {
+    float* d_tmp = nullptr;
+    S_CHECK(s, cudaMallocAsync(&d_rows, sizeof(int64_t) * nwb, s->st));
+    S_CHECK(s, cudaMallocAsync(&d_idx2, sizeof(int64_t) * nwb, s->st));
+    S_CHECK(s, cudaMallocAsync(&d_tmp, sizeof(float) * nwb * rs, s->st));
+    S_CHECK(s, cudaMemcpyAsync(d_rows, wb_rows.data(), sizeof(int64_t) * nwb, cudaMemcpyHostToDevice, s->st));
+    S_CHECK(s, cudaMemcpyAsync(d_idx2, wb_idx.data(), sizeof(int64_t) * nwb, cudaMemcpyHostToDevice, s->st));
+    copy_rows_kernel<<<grid_of(nwb * rs), 256, 0, s->st>>>(d_active, d_rows, nwb, rs, d_tmp);
+    scatter_rec_kernel<<<grid_of(nwb * rs), 256, 0, s->st>>>(s->pool_dev, s->d_pos, d_idx2, nwb, rs, d_tmp);
+    count_launch(2);
+    S_CHECK(s, cudaFreeAsync(d_tmp, s->st));
+    S_CHECK(s, cudaFreeAsync(d_rows, s->st));
+    S_CHECK(s, cudaFreeAsync(d_idx2, s->st));
+    st5[0] = nwb;
+  }
+  const int64_t nnb = (int64_t)nb_rows.size();
+  if (nnb > 0) {
+    float* d_nb = nullptr;
+    int32_t* d_keys = nullptr;
+    int64_t* d_home = nullptr;
+    S_CHECK(s, cudaMallocAsync(&d_rows, sizeof(int64_t) * nnb, s->st));
+    S_CHECK(s, cudaMallocAsync(&d_nb, sizeof(float) * nnb * rs, s->st));
+    S_CHECK(s, cudaMallocAsync(&d_keys, sizeof(int32_t) * nnb * 3, s->st));
+    S_CHECK(s, cudaMallocAsync(&d_home, sizeof(int64_t) * nnb, s->st));
+    S_CHECK(s, cudaMemcpyAsync(d_rows, nb_rows.data(), sizeof(int64_t) * nnb, cudaMemcpyHostToDevice, s->st));
+    copy_rows_kernel<<<grid_of(nnb * rs), 256, 0, s->st>>>(d_active, d_rows, nnb, rs, d_nb);
+    keys_kernel<<<grid_of(nnb), 256, 0, s->st>>>(d_nb, nnb, rs, voxel_size, s->capacity, d_keys, d_home);
+    count_launch(2);
+    std::vector<float> nb((size_t)nnb * rs);
+    std::vector<int32_t> keys((size_t)nnb * 3);
+    std::vector<int64_t> home((size_t)nnb);
+    S_CHECK(s, cudaMemcpyAsync(nb.data(), d_nb, sizeof(float) * nnb * rs, cudaMemcpyDeviceToHost, s->st));
+    S_CHECK(s, cudaMemcpyAsync(keys.data(), d_keys, sizeof(int32_t) * nnb * 3, cudaMemcpyDeviceToHost, s->st));
+    S_CHECK(s, cudaMemcpyAsync(home.data(), d_home, sizeof(int64_t) * nnb, cudaMemcpyDeviceToHost, s->st));
+    S_CHECK(s, cudaStreamSynchronize(s->st));  // also orders the writeback scatter before host pool reads
+    if (ensure_pool(s, s->size + nnb) != LATMAP_OK) return LATMAP_ERR_OUT_OF_MEMORY;
+    const int64_t first = s->size;
+    for (int64_t j = 0; j < nnb; ++j) {
+      const int64_t r = insert_one(s, &keys[3 * j], home[j], &nb[j * rs], false, nullptr);
+      if (r >= 0) {
+        resolved[nb_rows[j]] = r;
+        ++st5[1];
+      } else {
+        ++st5[2];
+      }
+    }
+    std::vector<float> pos((size_t)(s->size - first) * 3);
+    for (int64_t r = first; r < s->size; ++r) std::memcpy(&pos[(r - first) * 3], s->pool + r * rs, 12);
+    if (!pos.empty())
+      S_CHECK(s, cudaMemcpyAsync(s->d_pos + first * 3, pos.data(), sizeof(float) * pos.size(), cudaMemcpyHostToDevice,
+                                 s->st));
+    S_CHECK(s, cudaFreeAsync(d_nb, s->st));
+    S_CHECK(s, cudaFreeAsync(d_keys, s->st));
+    S_CHECK(s, cudaFreeAsync(d_home, s->st));
+    S_CHECK(s, cudaFreeAsync(d_rows, s->st));
+  }
+  // ---- step 2: prune in-radius tracked entries, mark their records present
+  const float r2 = radius * radius;
+  uint8_t* d_present = nullptr;
+  uint8_t* d_kept = nullptr;
+  int64_t* d_res = nullptr;
+  S_CHECK(s, cudaMallocAsync(&d_present, std::max<int64_t>(s->size, 1), s->st));
+  S_CHECK(s, cudaMemsetAsync(d_present, 0, std::max<int64_t>(s->size, 1), s->st));
+  std::vector<uint8_t> kept((size_t)std::max<int64_t>(n, 1), 0);
+  if (n > 0) {
+    S_CHECK(s, cudaMallocAsync(&d_kept, n, s->st));
+    S_CHECK(s, cudaMallocAsync(&d_res, sizeof(int64_t) * n, s->st));
+    S_CHECK(s, cudaMemcpyAsync(d_res, resolved.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, s->st));
+    prune_kernel<<<grid_of(n), 256, 0, s->st>>>(d_active, d_res, n, rs, center[0], center[1], center[2], r2, d_kept,
+                                                d_present);
+    count_launch();
+    S_CHECK(s, cudaMemcpyAsync(kept.data(), d_kept, n, cudaMemcpyDeviceToHost, s->st));
+  }
+  // ---- step 3: fetch not-present in-radius records in ascending index order
+  const int64_t nb = std::max<int64_t>(1, (s->size + kScanBlock - 1) / kScanBlock);
+  int32_t* d_cnt = nullptr;
+  int64_t* d_total = nullptr;
+  int64_t* d_fetch = nullptr;
+  S_CHECK(s, cudaMallocAsync(&d_cnt, sizeof(int32_t) * nb, s->st));
+  S_CHECK(s, cudaMallocAsync(&d_total, sizeof(int64_t), s->st));
+  S_CHECK(s, cudaMallocAsync(&d_fetch, sizeof(int64_t) * std::max<int64_t>(s->size, 1), s->st));
+  int64_t fetched = 0;
+  if (s->size > 0) {
+    radius_count_kernel<<<(unsigned)nb, kScanBlock, 0, s->st>>>(s->d_pos, s->size, center[0], center[1], center[2],
+                                                                 r2, d_present, d_cnt);
+    block_scan_kernel<<<1, 1024, 0, s->st>>>(d_cnt, nb, d_total);
+    radius_emit_kernel<<<(unsigned)nb, kScanBlock, 0, s->st>>>(s->d_pos, s->size, center[0], center[1], center[2],
+                                                                r2, d_present, d_cnt, d_fetch);
+    count_launch(3);
+    S_CHECK(s, cudaMemcpyAsync(&fetched, d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, s->st));
+  }
+  S_CHECK(s, cudaStreamSynchronize(s->st));
+  std::vector<int64_t> keep_rows;
+  for (int64_t i = 0; i < n; ++i) {
+    if (resolved[i] < 0) continue;  // rejected newborn drops out
+    if (kept[i])
+      keep_rows.push_back(i);
+    else
+      ++st5[3];
+  }
+  st5[4] = fetched;
+  const int64_t total = (int64_t)keep_rows.size() + fetched;
+  *out_count = total;
+  if (kept_mask)
+    for (int64_t i = 0; i < n; ++i) kept_mask[i] = kept[i];
+  if (stats_out) std::memcpy(stats_out, st5, sizeof(st5));
+  latmap_status ret = LATMAP_OK;
+  if (total > cap) {
+    ret = sfail(s, LATMAP_ERR_INVALID_ARGUMENT, "sync: output capacity too small");
+  } else {
+    // ---- assemble: kept (original order) ++ fetched (ascending)
+    const int64_t nk = (int64_t)keep_rows.size();
+    if (nk > 0) {
+      int64_t* d_k = nullptr;
+      S_CHECK(s, cudaMallocAsync(&d_k, sizeof(int64_t) * nk, s->st));
+      S_CHECK(s, cudaMemcpyAsync(d_k, keep_rows.data(), sizeof(int64_t) * nk, cudaMemcpyHostToDevice, s->st));
+      copy_rows_kernel<<<grid_of(nk * rs), 256, 0, s->st>>>(d_active, d_k, nk, rs, d_out);
+      count_launch();
+      S_CHECK(s, cudaFreeAsync(d_k, s->st));
+      if (out_origin)
+        for (int64_t j = 0; j < nk; ++j) out_origin[j] = resolved[keep_rows[j]];
+    }
+    if (fetched > 0) {
+      gather_kernel<<<grid_of(fetched * rs), 256, 0, s->st>>>(s->pool_dev, d_fetch, fetched, rs, d_out + nk * rs);
+      count_launch();
+      if (out_origin)
+        S_CHECK(s, cudaMemcpyAsync(out_origin + nk, d_fetch, sizeof(int64_t) * fetched, cudaMemcpyDeviceToHost,
+                                   s->st));
+    }
+  }
+  S_CHECK(s, cudaFreeAsync(d_present, s->st));
+  if (d_kept) S_CHECK(s, cudaFreeAsync(d_kept, s->st));
+  if (d_res) S_CHECK(s, cudaFreeAsync(d_res, s->st));
+  S_CHECK(s, cudaFreeAsync(d_cnt, s->st));
+  S_CHECK(s, cudaFreeAsync(d_total, s->st));
+  S_CHECK(s, cudaFreeAsync(d_fetch, s->st));
+  S_CHECK(s, cudaStreamSynchronize(s->st));
+  return ret;
+}
+
+}  // extern "C"

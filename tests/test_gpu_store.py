@@ -1,0 +1,111 @@
+"""Device voxel-hash store (K11) against the oracle store: record indices, rejections, keys,
+fetch_local lists and sync outputs must be bit-exact (BASELINE: hash lookups bit-exact)."""
+import numpy as np
+import pytest
+
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2602_12314_b200 import api  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return api.Context(0)
+
+
+def recs(rng, n, extent=2.0, ds=4):
+    r = np.zeros((n, 14 + ds), np.float32)
+    r[:, 0:3] = rng.uniform(-extent, extent, (n, 3))
+    q = rng.standard_normal((n, 4))
+    r[:, 3:7] = q / np.linalg.norm(q, axis=1, keepdims=True)
+    r[:, 7:] = rng.standard_normal((n, 7 + ds))
+    return r
+
+
+def test_insert_find_records_match(ctx):
+    rng = np.random.default_rng(1)
+    r = recs(rng, 20000)
+    r[5000:6000, :3] = r[:1000, :3] + 1e-4  # duplicate voxels
+    for cap in (1 << 16, 20011):
+        s, o = api.Store(ctx, cap, 4), oracle.Store(cap, 4)
+        assert s.insert_global(r, 0.01) == o.insert_global(r, 0.01)
+        assert s.size() == o.size()
+        assert s.stats() == o.stats()
+        got, keys = s.records()
+        assert np.array_equal(got.view(np.uint32), o.records().view(np.uint32))
+        assert all(tuple(keys[i]) == o.record_key(i) for i in range(0, s.size(), 97))
+        for p in r[::53, :3]:
+            k = oracle.voxel_of(p, 0.01)
+            assert s.find(k) == o.find(k)
+
+
+def test_overflow_chain(ctx):  # test_store.cpp:106-124
+    cap = 64
+    target = oracle.hash_voxel((0, 0, 0), cap)
+    chain, ix = [], 0
+    while len(chain) <= 8:
+        if oracle.hash_voxel((ix, 0, 0), cap) == target:
+            chain.append((ix, 0, 0))
+        ix += 1
+    s = api.Store(ctx, cap, 4)
+    rec = np.zeros(18, np.float32)
+    for k in chain[:-1]:
+        assert s.insert(k, rec) >= 0
+    assert s.insert(chain[-1], rec) == -1
+    assert s.stats()["rejected_overflow"] == 1
+
+
+def test_fetch_local_matches(ctx):
+    rng = np.random.default_rng(2)
+    r = recs(rng, 30000)
+    s, o = api.Store(ctx, 1 << 17, 4), oracle.Store(1 << 17, 4)
+    s.insert_global(r, 0.01)
+    o.insert_global(r, 0.01)
+    pool = o.records()
+    for t in range(60):
+        c = rng.uniform(-2, 2, 3).astype(np.float32)
+        rad = np.float32(rng.uniform(0.05, 2.5))
+        idx, d = s.fetch_local(c, rad, gather=True)
+        ref = o.fetch_local(c, rad)
+        assert np.array_equal(idx, ref)
+        assert np.array_equal(d.cpu().numpy().view(np.uint32), pool[ref].view(np.uint32))
+    assert len(s.fetch_local((0, 0, 0), 1e-3)) >= 0
+    with pytest.raises(ValueError):
+        s.fetch_local((0, 0, 0), 0.0)
+
+
+def test_sync_sequence_matches(ctx):
+    rng = np.random.default_rng(3)
+    s, o = api.Store(ctx, 1 << 16, 4), oracle.Store(1 << 16, 4)
+    base = recs(rng, 3000)
+    s.insert_global(base, 0.05)
+    o.insert_global(base, 0.05)
+    center = np.zeros(3, np.float32)
+    org = o.fetch_local(center, 1.0)
+    act = o.records()[org]
+    dirty = np.zeros(len(org), np.uint8)
+    for step in range(6):
+        # optimisation moves some tracked entries (possibly across voxels), adds newborns
+        act = act.copy()
+        moved = rng.random(len(act)) < 0.3
+        act[moved, :3] += rng.normal(0, 0.05, (moved.sum(), 3)).astype(np.float32)
+        act[moved, 7:] += 0.1
+        dirty = moved.astype(np.uint8)
+        born = recs(rng, 50, extent=1.5)
+        born[:10, :3] = act[:10, :3]  # some land in occupied voxels -> rejected
+        act = np.concatenate([act, born])
+        org = np.concatenate([org, -np.ones(50, np.int64)])
+        dirty = np.concatenate([dirty, np.ones(50, np.uint8)])
+        center = (center + rng.normal(0, 0.3, 3)).astype(np.float32)
+        d_out, g_org, g_kept, g_st = s.sync(torch.as_tensor(act, device="cuda"), org, dirty, center, 1.0, 0.05)
+        r_out, r_org, r_kept, r_st = o.sync(act, org, dirty, center, 1.0, 0.05)
+        assert g_st == r_st, (step, g_st, r_st)
+        assert np.array_equal(g_org, r_org) and np.array_equal(g_kept, r_kept)
+        assert np.array_equal(d_out.cpu().numpy().view(np.uint32), r_out.view(np.uint32))
+        assert np.array_equal(s.records()[0].view(np.uint32), o.records().view(np.uint32))
+        act, org = r_out, r_org
