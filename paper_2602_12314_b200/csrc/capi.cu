@@ -866,7 +866,8 @@ latmap_status latmap_session_create(latmap_ctx* ctx, const latmap_config* cfg, i
            ok(cudaMalloc(&d.r_part, sizeof(float) * 148 * k * ds)) &&
            ok(cudaMalloc(&d.a_part, sizeof(float) * 74 * 2 * k * (k / 2 + 1))) &&
            ok(cudaMalloc(&d.bm_part, sizeof(float) * 74 * k * 64)) &&
-           ok(cudaMalloc(&d.loss_part, sizeof(double) * 148 * 4));
+           ok(cudaMalloc(&d.loss_part, sizeof(double) * 148 * 4)) &&
+           ok(cudaMalloc(&d.e_tiles, (size_t)((npx + 127) / 128) * 128 * k * 2));
   }
   if (!good) {
     t_err = "latmap_session_create: out of device memory";
@@ -897,7 +898,8 @@ latmap_status latmap_session_destroy(latmap_session* s) {
                   (void*)s->d_loss, (void*)s->dec.buf1, (void*)s->dec.buf2, (void*)s->dec.alpha_r, (void*)s->dec.beta_r,
                   (void*)s->dec.kd, (void*)s->dec.mm, (void*)s->dec.gt, (void*)s->dec.nv, (void*)s->dec.r,
                   (void*)s->dec.a, (void*)s->dec.bm, (void*)s->dec.row_stats, (void*)s->dec.r_part,
-                  (void*)s->dec.a_part, (void*)s->dec.bm_part, (void*)s->dec.loss_part})
+                  (void*)s->dec.a_part, (void*)s->dec.bm_part, (void*)s->dec.loss_part,
+                  (void*)s->dec.e_tiles})
     if (p) cudaFree(p);
   for (auto& r : s->rw) r.release();
   for (auto* p : s->color) cudaFree(p);

@@ -72,6 +72,7 @@ __device__ __forceinline__ void load_tile_bf16(uint8_t* tile, const float* __res
 }
 
 struct Dec1Args {
+  uint8_t* e_tiles;         // ntiles x (128 x K bf16) in the smem core-matrix layout (for DEC2)
   const float* query;       // npx x DS (fp32, raster order)
   const int32_t* assign;    // npx
   const float* kd;          // K x DS fp32 (D W^T)
@@ -224,9 +225,10 @@ __global__ void __launch_bounds__(512, 1) dec1_kernel(Dec1Args a) {
     tc::tc_fence_before();
     __syncthreads();
     const float inv_sum = 1.f / ((red(1, 0) + red(1, 1)) + (red(1, 2) + red(1, 3)));
-    // ---- MMA2: t = e M -> TMEM[0, K) (S is dead)
+    // ---- MMA2: t = e M -> TMEM[0, K) (S is dead); e also streams to HBM for DEC2
     if (tid == 0) {
       tc::tc_fence_after();
+      if (a.want_grad) tc::bulk_s2g(a.e_tiles + (size_t)tile * kRows * K * 2, sP, kRows * K * 2);
 #pragma unroll 4
       for (int ks = 0; ks < K / 16; ++ks)
         tc::mma_bf16(tmem, tc::make_sdesc(aP + ks * 2 * 2048, 2048, 128),
@@ -291,7 +293,9 @@ __global__ void __launch_bounds__(512, 1) dec1_kernel(Dec1Args a) {
       __syncthreads();
       continue;
     }
-    // ---- dS = P (al t + be g - c) / tau  (bf16, overwrites e in sP)
+    // ---- dS = P (al t + be g - c) / tau  (bf16, overwrites e in sP once its copy-out is read)
+    if (tid == 0) tc::bulk_wait_read();
+    __syncthreads();
     const float ps = inv_sum * a.inv_temp;  // P = e * inv_sum
     const float al_t = al * inv_sum;        // al * t = al * inv_sum * (e M)
 #pragma unroll
@@ -368,6 +372,7 @@ __global__ void __launch_bounds__(512, 1) dec1_kernel(Dec1Args a) {
   tc::tc_fence_before();
   __syncthreads();
   if (tid == 0) {
+    tc::bulk_wait_all();
     double c0s = 0, c1s = 0, c2s = 0;
     for (int w = 0; w < 16; ++w) c0s += s_loss[w][0], c1s += s_loss[w][1], c2s += s_loss[w][2];
     a.loss_part[blockIdx.x * 4 + 0] = c0s;
@@ -378,106 +383,93 @@ __global__ void __launch_bounds__(512, 1) dec1_kernel(Dec1Args a) {
 }
 
 struct Dec2Args {
-  const float* query;
+  const uint8_t* e_tiles;    // from DEC1: per tile 128 x K bf16 e = exp(S - max), core-matrix layout
   const int32_t* assign;
-  const float* kd;
-  const float4* row_stats;
+  const float4* row_stats;   // (max, 1/sum, alpha, beta)
   int64_t npx;
-  float inv_temp;
-  int n_set;
   float* a_part;   // (gridDim/2) x 2 roles x K x (K/2)
   float* bm_part;  // (gridDim/2) x K x 64  (role 0 only)
 };
 
-template <int K, int DS>
-__global__ void __launch_bounds__(512, 1) dec2_kernel(Dec2Args a) {
+// DEC2: A[:, role half] = e^T diag(alpha / sum^2) e and (role 0) Bm = e^T Ohb with
+// Ohb[r][s] = beta_r / sum_r [a_r == s], streaming the e tiles DEC1 exported (TMA bulk loads,
+// double-buffered) -- no recomputation of S or exp.
+template <int K>
+__global__ void __launch_bounds__(256, 1) dec2_kernel(Dec2Args a) {
   constexpr int MH = K / 128, NH = K / 2, NB = 64;
-  constexpr int kColA = 128, kColB = 128 + MH * NH;
+  constexpr int kColA = 0, kColB = MH * NH;
   constexpr int kTmemCols = kColB + MH * NB <= 256 ? 256 : 512;
   constexpr uint32_t kCS = 16u * kRows;
+  constexpr uint32_t kTileBytes = kRows * K * 2;
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sQ = smem;                    // 128 x DS
-  uint8_t* sKd = sQ + kRows * DS * 2;    // K x DS
-  uint8_t* sP = sKd + K * DS * 2;        // 128 x K
-  uint8_t* sAP = sP + kRows * K * 2;     // 128 x NH
-  uint8_t* sOh = sAP + kRows * NH * 2;   // 128 x NB
-  __shared__ uint64_t bar[2];
+  uint8_t* sE[2] = {smem, smem + kTileBytes};      // 2 x (128 x K)
+  uint8_t* sAP = smem + 2 * kTileBytes;            // 128 x NH
+  uint8_t* sOh = sAP + kRows * NH * 2;             // 128 x NB
+  __shared__ uint64_t bar_ld[2], bar_mma;
   __shared__ uint32_t s_taddr;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = warp & 3, h = warp >> 2;  // h: column quarter (0..3)
+  const int g = warp & 3, h = warp >> 2;  // TMEM lane group, column half (of the role's NH)
   const int row = 32 * g + lane;
   const int role = blockIdx.x & 1, group = blockIdx.x >> 1, ngroups = gridDim.x >> 1;
-  load_tile_bf16(sKd, a.kd, K, DS, K, tid, 512);
   if (tid == 0) {
-    tc::mbar_init(&bar[0], 1);
-    tc::mbar_init(&bar[1], 1);
+    tc::mbar_init(&bar_ld[0], 1);
+    tc::mbar_init(&bar_ld[1], 1);
+    tc::mbar_init(&bar_mma, 1);
     tc::fence_mbar_init();
   }
   if (warp == 0) tc::tmem_alloc<kTmemCols>(&s_taddr);
-  tc::fence_async_smem();
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = s_taddr;
   const uint32_t tl = tmem + ((uint32_t)(32 * g) << 16);
-  uint32_t ph[2] = {0, 0};
-  const uint32_t aQ = tc::smem_u32(sQ), aKd = tc::smem_u32(sKd), aP = tc::smem_u32(sP), aAP = tc::smem_u32(sAP),
-                 aOh = tc::smem_u32(sOh);
-  const float cl = kLog2e * a.inv_temp;
+  uint32_t ph_ld[2] = {0, 0}, ph_mma = 0;
+  const uint32_t aAP = tc::smem_u32(sAP), aOh = tc::smem_u32(sOh);
   const int64_t ntiles = (a.npx + kRows - 1) / kRows;
-  bool first = true;
-  for (int64_t tile = group; tile < ntiles; tile += ngroups) {
+  int it = 0;
+  if (tid == 0 && group < ntiles) {
+    tc::mbar_expect_tx(&bar_ld[0], kTileBytes);
+    tc::bulk_g2s(sE[0], a.e_tiles + (size_t)group * kTileBytes, kTileBytes, &bar_ld[0]);
+  }
+  for (int64_t tile = group; tile < ntiles; tile += ngroups, ++it) {
+    const int buf = it & 1;
     const int64_t r0 = tile * kRows;
     const int valid = (int)(a.npx - r0 < kRows ? a.npx - r0 : kRows);
-    load_tile_bf16(sQ, a.query + r0 * DS, kRows, DS, valid, tid, 512);
     float4 st = make_float4(0.f, 0.f, 0.f, 0.f);
     int32_t asg = -1;
     if (row < valid) {
       st = a.row_stats[r0 + row];
       asg = a.assign[r0 + row];
     }
-    const float mxl = st.x * cl, inv_sum = st.y, al = st.z, be = st.w;
-    for (int ch = 0; ch < MH; ++ch) {
-      tc::fence_async_smem();
-      tc::tc_fence_before();
-      __syncthreads();
-      if (tid == 0) {
-        tc::tc_fence_after();
+    const float wa = st.z * st.y * st.y;  // alpha / sum^2
+    const float wb = st.w * st.y;         // beta / sum
+    // previous MMA done -> its operands (sAP, sOh, sE[buf^1]) are free
+    if (it > 0) {
+      tc::mbar_wait(&bar_mma, ph_mma);
+      ph_mma ^= 1;
+    }
+    if (tid == 0 && tile + ngroups < ntiles) {
+      tc::mbar_expect_tx(&bar_ld[buf ^ 1], kTileBytes);
+      tc::bulk_g2s(sE[buf ^ 1], a.e_tiles + (size_t)(tile + ngroups) * kTileBytes, kTileBytes, &bar_ld[buf ^ 1]);
+    }
+    tc::mbar_wait(&bar_ld[buf], ph_ld[buf]);
+    ph_ld[buf] ^= 1;
+    // B operands: (alpha / sum^2) e[:, role half] and the beta / sum one-hot
+    const uint8_t* E = sE[buf];
 #pragma unroll
-        for (int ks = 0; ks < DS / 16; ++ks)
-          tc::mma_bf16(tmem, tc::make_sdesc(aQ + ks * 2 * 2048, 2048, 128),
-                       tc::make_sdesc(aKd + ch * 2048 + ks * 2 * (16 * K), 16 * K, 128),
-                       tc::make_idesc_bf16(128, 128, 0, 0), ks > 0);
-        tc::mma_commit(&bar[0]);
-      }
-      tc::mbar_wait(&bar[0], ph[0]);
-      ph[0] ^= 1;
-      tc::tc_fence_after();
+    for (int c = h * (NH / 2); c < (h + 1) * (NH / 2); c += 8) {
+      float v[8];
+      ld_row8(E, row, role * NH + c, kCS, v);
 #pragma unroll
-      for (int c = 0; c < 32; c += 32) {
-        const int cc = h * 32 + c;
-        float v[32], w[32];
-        tc::tmem_ld32(tl + cc, v);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          v[i] = row < valid ? ex2(fmaf(v[i], cl, -mxl)) * inv_sum : 0.f;
-          w[i] = al * v[i];
-        }
-        const int k0 = ch * 128 + cc;
-#pragma unroll
-        for (int i = 0; i < 32; i += 8) st_row8(sP, row, k0 + i, kCS, v + i);
-        if (k0 >= role * NH && k0 < (role + 1) * NH) {
-#pragma unroll
-          for (int i = 0; i < 32; i += 8) st_row8(sAP, row, k0 - role * NH + i, kCS, w + i);
-        }
-      }
+      for (int j = 0; j < 8; ++j) v[j] = row < valid ? v[j] * wa : 0.f;
+      st_row8(sAP, row, c, kCS, v);
     }
     if (role == 0) {
 #pragma unroll
-      for (int c = h * 16; c < h * 16 + 16; c += 8) {
+      for (int c = h * (NB / 2); c < (h + 1) * (NB / 2); c += 8) {
         float v[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = (asg == c + i) ? be : 0.f;
+        for (int j = 0; j < 8; ++j) v[j] = (asg == c + j) ? wb : 0.f;
         st_row8(sOh, row, c, kCS, v);
       }
     }
@@ -486,33 +478,34 @@ __global__ void __launch_bounds__(512, 1) dec2_kernel(Dec2Args a) {
     __syncthreads();
     if (tid == 0) {
       tc::tc_fence_after();
+      const uint32_t aE = tc::smem_u32(E);
       for (int mh = 0; mh < MH; ++mh) {
 #pragma unroll
         for (int ks = 0; ks < kRows / 16; ++ks)
-          tc::mma_bf16(tmem + kColA + mh * NH, tc::make_sdesc(aP + mh * 16 * 2048 + ks * 2 * 128, 128, 2048),
+          tc::mma_bf16(tmem + kColA + mh * NH, tc::make_sdesc(aE + mh * 16 * 2048 + ks * 2 * 128, 128, 2048),
                        tc::make_sdesc(aAP + ks * 2 * 128, 128, 2048), tc::make_idesc_bf16(128, NH, 1, 1),
-                       (!first) || ks > 0);
+                       it > 0 || ks > 0);
         if (role == 0) {
 #pragma unroll
           for (int ks = 0; ks < kRows / 16; ++ks)
-            tc::mma_bf16(tmem + kColB + mh * NB, tc::make_sdesc(aP + mh * 16 * 2048 + ks * 2 * 128, 128, 2048),
+            tc::mma_bf16(tmem + kColB + mh * NB, tc::make_sdesc(aE + mh * 16 * 2048 + ks * 2 * 128, 128, 2048),
                          tc::make_sdesc(aOh + ks * 2 * 128, 128, 2048), tc::make_idesc_bf16(128, NB, 1, 1),
-                         (!first) || ks > 0);
+                         it > 0 || ks > 0);
         }
       }
-      tc::mma_commit(&bar[1]);
+      tc::mma_commit(&bar_mma);
     }
-    tc::mbar_wait(&bar[1], ph[1]);
-    ph[1] ^= 1;
+  }
+  if (it > 0) {
+    tc::mbar_wait(&bar_mma, ph_mma);
     tc::tc_fence_after();
-    first = false;
   }
   // drain: lane `row` of half mh holds A[mh*128 + row][role*NH + c], Bm[mh*128 + row][c]
   for (int mh = 0; mh < MH; ++mh) {
     float* dst = a.a_part + (((size_t)group * 2 + role) * K + mh * 128 + row) * NH;
-    for (int c = h * (NH / 4); c < (h + 1) * (NH / 4); c += 16) {
+    for (int c = h * (NH / 2); c < (h + 1) * (NH / 2); c += 16) {
       float v[16];
-      if (first) {
+      if (it == 0) {
         for (int i = 0; i < 16; ++i) v[i] = 0.f;
       } else {
         tc::tmem_ld16(tl + kColA + mh * NH + c, v);
@@ -521,9 +514,9 @@ __global__ void __launch_bounds__(512, 1) dec2_kernel(Dec2Args a) {
     }
     if (role == 0) {
       float* db = a.bm_part + ((size_t)group * K + mh * 128 + row) * NB;
-      for (int c = h * (NB / 4); c < (h + 1) * (NB / 4); c += 16) {
+      for (int c = h * (NB / 2); c < (h + 1) * (NB / 2); c += 16) {
         float v[16];
-        if (first) {
+        if (it == 0) {
           for (int i = 0; i < 16; ++i) v[i] = 0.f;
         } else {
           tc::tmem_ld16(tl + kColB + mh * NB + c, v);
@@ -582,7 +575,7 @@ void launch_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_
                float scale, bool want_grad, float* d_query, double* partials) {
   const int g1 = 148;
   const int g2 = 148;  // 74 groups x 2 roles
-  Dec1Args d1{query, assignment, w.kd, w.mm, w.gt, w.nv, npx, 1.f / temperature, lambda_cos, lambda_l2,
+  Dec1Args d1{w.e_tiles, query, assignment, w.kd, w.mm, w.gt, w.nv, npx, 1.f / temperature, lambda_cos, lambda_l2,
               n_sup > 0 ? 1.f / (float)n_sup : 0.f, scale, d_query, reinterpret_cast<float4*>(w.row_stats),
               w.r_part, w.loss_part, want_grad ? 1 : 0};
   const size_t sm1 = (size_t)kRows * DS * 2 + (size_t)K * DS * 2 + (size_t)kRows * K * 2 + (size_t)K * K * 2 +
@@ -600,16 +593,14 @@ void launch_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_
     count_launch();
     return;
   }
-  Dec2Args d2{query, assignment, w.kd, reinterpret_cast<const float4*>(w.row_stats), npx, 1.f / temperature,
-              (int)n_set, w.a_part, w.bm_part};
-  const size_t sm2 = (size_t)kRows * DS * 2 + (size_t)K * DS * 2 + (size_t)kRows * K * 2 + (size_t)kRows * (K / 2) * 2 +
-                     (size_t)kRows * 64 * 2;
+  Dec2Args d2{w.e_tiles, assignment, reinterpret_cast<const float4*>(w.row_stats), npx, w.a_part, w.bm_part};
+  const size_t sm2 = 2 * (size_t)kRows * K * 2 + (size_t)kRows * (K / 2) * 2 + (size_t)kRows * 64 * 2;
   static bool attr2 = false;
   if (!attr2) {
-    cudaFuncSetAttribute(dec2_kernel<K, DS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+    cudaFuncSetAttribute(dec2_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
     attr2 = true;
   }
-  dec2_kernel<K, DS><<<g2, 512, sm2, st>>>(d2);
+  dec2_kernel<K><<<g2, 256, sm2, st>>>(d2);
   count_launch();
   const int64_t tot = (int64_t)K * K + n_set * K + (int64_t)K * DS + 3;
   dec_reduce_kernel<<<(unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 8), 256, 0, st>>>(

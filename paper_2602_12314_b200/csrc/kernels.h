@@ -91,6 +91,7 @@ struct DecoderWork {
   float* a_part = nullptr;     // 74 x 2 x K x K/2
   float* bm_part = nullptr;    // 74 x K x 64
   double* loss_part = nullptr; // 148 x 4
+  uint8_t* e_tiles = nullptr;  // ceil(npx/128) x 128 x K bf16 (DEC1 -> DEC2)
 };
 void decoder_prepare(cudaStream_t st, DecoderWork& w, const float* atoms, const float* proj);
 // Fused feature loss + decoder backward for one frame (pixel mode). Accumulates into d_proj,
