@@ -472,6 +472,184 @@ __device__ __forceinline__ void mma_tf32(float* d, const uint32_t* a, const uint
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
 }
 
+// K4 (fast mode, ds >= 8): same per-pixel decisions and colour/depth/alpha accumulation as
+// raster_fwd_kernel<DSP, false>; the query channels, which dominate the per-(pixel, splat) work,
+// are accumulated on the tensor cores instead: per warp and 16-splat sub-batch the blend weights
+// W (32 pixels x 16 splats, from the scalar pass) multiply the splats' features F (16 x DSP),
+// Q += W F as 3xTF32 m16n8k8 MMAs (~fp32 accurate, different summation order than the scalar loop).
+template <int DSP>
+__global__ void __launch_bounds__(kTilePixels, 2) raster_fwd_mma_kernel(RasterArgs a) {
+  constexpr int FB = 128;           // splats per shared-memory batch
+  constexpr int FP = DSP + 8;       // feature pitch: B-fragment loads hit distinct banks
+  constexpr int WP = 40;            // per-warp [splat][pixel] weight pitch
+  constexpr int NQ = DSP / 8;       // n-tiles (8 channels each)
+  extern __shared__ __align__(16) float s_dyn[];
+  float* s_fh = s_dyn;                      // [FB][FP] tf32 hi
+  float* s_fl = s_fh + FB * FP;             // [FB][FP] tf32 lo
+  float* s_w = s_fl + FB * FP;              // [8 warps][16][WP]
+  __shared__ SplatRec s_rec[FB];
+  __shared__ float s_col[FB * 3];
+  __shared__ uint32_t s_src[FB];
+  __shared__ int32_t s_max;
+  if (a.counters[2]) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, cq = lane & 3;
+  const int tile = blockIdx.x;
+  const int tx0 = (tile % a.tiles_x) * kTile, ty0 = (tile / a.tiles_x) * kTile;
+  const int px = tx0 + (tid % kTile), py = ty0 + (tid / kTile);
+  const bool inside = px < a.width && py < a.height;
+  const int start = a.offset[tile], end = a.offset[tile + 1];
+  if (tid == 0) s_max = 0;
+  float T = 1.f, acc_c0 = 0.f, acc_c1 = 0.f, acc_c2 = 0.f, acc_d = 0.f, acc_a = 0.f;
+  float q[2][NQ][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NQ; ++nt) q[mt][nt][0] = q[mt][nt][1] = q[mt][nt][2] = q[mt][nt][3] = 0.f;
+  bool done = !inside;
+  int last = end - start;
+  const float fx = (float)px, fy = (float)py;
+  float* sw = s_w + warp * 16 * WP;
+  for (int base = start; base < end; base += FB) {
+    if (__syncthreads_and(done)) break;
+    const int cnt = min(FB, end - base);
+    if (tid < cnt) {
+      const uint32_t src = (uint32_t)a.keys[base + tid];
+      s_src[tid] = src;
+      s_rec[tid] = a.rec[src];
+      s_col[tid * 3 + 0] = a.colors[3 * (size_t)src + 0];
+      s_col[tid * 3 + 1] = a.colors[3 * (size_t)src + 1];
+      s_col[tid * 3 + 2] = a.colors[3 * (size_t)src + 2];
+    }
+    __syncthreads();
+    for (int e = tid; e < cnt * DSP; e += kTilePixels) {
+      const int j = e / DSP, c = e % DSP;
+      const float v = c < a.ds ? a.feats[(size_t)s_src[j] * a.ds + c] : 0.f;
+      uint32_t hi, lo;
+      split_tf32(v, hi, lo);
+      s_fh[j * FP + c] = __uint_as_float(hi);
+      s_fl[j * FP + c] = __uint_as_float(lo);
+    }
+    if (cnt < FB)  // zero the tail of the last sub-batch so padded splats contribute nothing
+      for (int e = cnt * DSP + tid; e < ((cnt + 15) & ~15) * DSP; e += kTilePixels) {
+        const int j = e / DSP, c = e % DSP;
+        s_fh[j * FP + c] = 0.f;
+        s_fl[j * FP + c] = 0.f;
+      }
+    __syncthreads();
+    for (int sb = 0; sb < cnt; sb += 16) {
+      if (__all_sync(0xffffffffu, done)) break;
+#pragma unroll
+      for (int j4 = 0; j4 < 16; j4 += 4) {
+        // alpha' of four splats evaluated independently (ILP over the exact exp), then the
+        // transmittance chain in order
+        float alv[4];
+        bool ok[4];
+        bool any = false;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = sb + j4 + u;
+          const SplatRec& s = s_rec[j];
+          ok[u] = !done && j < cnt && px >= s.x0 && px <= s.x1 && py >= s.y0 && py <= s.y1;
+          any |= ok[u];
+        }
+        if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const SplatRec& s = s_rec[sb + j4 + u];
+            const float dx = fs(fx, s.mean_x);
+            const float dy = fs(fy, s.mean_y);
+            const float rho =
+                fa(fa(fm(fm(s.a00, dx), dx), fm(fm(fm(2.f, s.a01), dx), dy)), fm(fm(s.a11, dy), dy));
+            float al = fm(s.alpha, exp_exact(fm(-0.5f, rho)));
+            alv[u] = al > kAlphaMax ? kAlphaMax : al;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = sb + j4 + u;
+          float w = 0.f;
+          if (ok[u] && !done) {
+            const float al = alv[u];
+            w = fm(al, T);
+            acc_c0 = fmaf(w, s_col[j * 3 + 0], acc_c0);
+            acc_c1 = fmaf(w, s_col[j * 3 + 1], acc_c1);
+            acc_c2 = fmaf(w, s_col[j * 3 + 2], acc_c2);
+            acc_d = fmaf(w, s_rec[j].depth, acc_d);
+            acc_a = fa(acc_a, w);
+            T = fm(T, fs(1.f, al));
+            if (T < kTransmitStop) {
+              done = true;
+              last = base - start + j + 1;
+            }
+          }
+          sw[(j4 + u) * WP + lane] = w;
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        uint32_t ah[2][4], alo[2][4];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const int r = 16 * mt + g;
+          split_tf32(sw[(8 * ks + cq) * WP + r], ah[mt][0], alo[mt][0]);
+          split_tf32(sw[(8 * ks + cq) * WP + r + 8], ah[mt][1], alo[mt][1]);
+          split_tf32(sw[(8 * ks + cq + 4) * WP + r], ah[mt][2], alo[mt][2]);
+          split_tf32(sw[(8 * ks + cq + 4) * WP + r + 8], ah[mt][3], alo[mt][3]);
+        }
+        const int j0 = sb + 8 * ks + cq;
+#pragma unroll
+        for (int nt = 0; nt < NQ; ++nt) {
+          uint32_t bh[2], bl[2];
+          bh[0] = __float_as_uint(s_fh[j0 * FP + 8 * nt + g]);
+          bh[1] = __float_as_uint(s_fh[(j0 + 4) * FP + 8 * nt + g]);
+          bl[0] = __float_as_uint(s_fl[j0 * FP + 8 * nt + g]);
+          bl[1] = __float_as_uint(s_fl[(j0 + 4) * FP + 8 * nt + g]);
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            mma_tf32(q[mt][nt], alo[mt], bh);
+            mma_tf32(q[mt][nt], ah[mt], bl);
+            mma_tf32(q[mt][nt], ah[mt], bh);
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+  if (inside) {
+    const size_t p = (size_t)py * a.width + px;
+    a.color[3 * p + 0] = acc_c0;
+    a.color[3 * p + 1] = acc_c1;
+    a.color[3 * p + 2] = acc_c2;
+    a.depth[p] = acc_d;
+    a.alpha[p] = acc_a;
+    a.px_last[p] = last;
+    a.px_T[p] = T;
+  }
+  // query from the accumulator fragments: rows = the warp's pixels, columns = channels
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int pl = 32 * warp + 16 * mt + g + 8 * hh;
+      const int qx = tx0 + (pl % kTile), qy = ty0 + (pl / kTile);
+      if (qx < a.width && qy < a.height) {
+        float* qo = a.query + ((size_t)qy * a.width + qx) * a.ds;
+#pragma unroll
+        for (int nt = 0; nt < NQ; ++nt) {
+          const int c = 8 * nt + 2 * cq;
+          if (c < a.ds) qo[c] = q[mt][nt][2 * hh];
+          if (c + 1 < a.ds) qo[c + 1] = q[mt][nt][2 * hh + 1];
+        }
+      }
+    }
+  __syncthreads();
+  if (inside) atomicMax(&s_max, last);
+  __syncthreads();
+  if (tid == 0) a.tile_max_last[tile] = s_max;
+}
+
 // K8: reverse sweep of render_backward (render.cpp:315-353), one CTA per 16x16 tile, one
 // thread per pixel. Transmittance before each blended splat is recovered by division from
 // the forward's final T. Per batch of 16 splats each thread records, per (pixel, splat),
@@ -484,13 +662,20 @@ template <int DSP>
 __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArgs a) {
   constexpr int NU = ((4 + DSP) + 7) / 8 * 8;  // U columns: uc0..2, uz, uq[DSP], pad
   constexpr int NT = NU / 8;                   // n-tiles of the W^T U product
-  constexpr int UP = NU + (NU % 32 == 0 ? 4 : (NU % 16 == 0 ? 4 : 0));  // bank-spread pitch
+  // U row pitch = 8 mod 16 plus a column XOR swizzle on row bit 2: both the row-fragment
+  // (value MMA) and the column-fragment (W^T U MMA) loads are bank-conflict free
+  constexpr int UP = NU % 16 == 8 ? NU : NU + 8;
   constexpr int WP = 36;                       // per-warp [splat][pixel] pitch (floats)
   constexpr int NACC = NU + 8 + 8;             // per-splat accumulators: W^T U | drho moments | dg
+  constexpr int NUP = NU + 4;                  // splat-row pitch (B-fragment loads hit distinct banks)
+  constexpr int PP = (NACC + 23) / 32 * 32 + 8;  // per-warp partial pitch (= 8 mod 32)
+  static_assert(16 * PP <= 3 * kBwdBatch * WP, "warp partials must fit the warp's staging area");
+  auto uidx = [](int p, int c) { return p * UP + (c ^ (((p >> 2) & 1) << 2)); };
   extern __shared__ __align__(16) float s_dyn[];
   float* s_u = s_dyn;                                          // [256][UP] per-pixel upstream rows
   float* s_wbase = s_dyn + kTilePixels * UP;                   // [8 warps][3][16 * WP]: W, drho, dg
-  __shared__ __align__(16) float s_f[kBwdBatch * NU];        // splat rows [c0 c1 c2 z f...]
+  __shared__ __align__(16) float s_fh[kBwdBatch * NUP];      // splat rows [c0 c1 c2 z f...], tf32 hi
+  __shared__ __align__(16) float s_fl[kBwdBatch * NUP];      //   ... and tf32 lo
   __shared__ SplatRec s_rec[kBwdBatch];
   __shared__ uint32_t s_src[kBwdBatch];
   __shared__ float s_acc[kBwdBatch * NACC];
@@ -525,15 +710,14 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
     T = a.px_T[p];
   }
   {
-    float* ur = s_u + tid * UP;
-    ur[0] = uc0;
-    ur[1] = uc1;
-    ur[2] = uc2;
-    ur[3] = uz;
+    s_u[uidx(tid, 0)] = uc0;
+    s_u[uidx(tid, 1)] = uc1;
+    s_u[uidx(tid, 2)] = uc2;
+    s_u[uidx(tid, 3)] = uz;
 #pragma unroll
-    for (int c = 0; c < DSP; ++c) ur[4 + c] = uq[c];
+    for (int c = 0; c < DSP; ++c) s_u[uidx(tid, 4 + c)] = uq[c];
 #pragma unroll
-    for (int c = 4 + DSP; c < NU; ++c) ur[c] = 0.f;
+    for (int c = 4 + DSP; c < NU; ++c) s_u[uidx(tid, c)] = 0.f;
   }
   // MMA lane coordinates
   const int g = lane >> 2, cq = lane & 3;
@@ -589,43 +773,108 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
         else if (c - 4 < a.ds)
           v = a.feats[src * a.ds + (c - 4)];
       }
-      s_f[e] = v;
+      uint32_t hi, lo;
+      split_tf32(v, hi, lo);
+      s_fh[j * NUP + c] = __uint_as_float(hi);
+      s_fl[j * NUP + c] = __uint_as_float(lo);
     }
-    for (int e = tid; e < kBwdBatch * NACC; e += blockDim.x) s_acc[e] = 0.f;
     __syncthreads();
-    // ---- per-pixel reverse sweep over the batch
-    for (int j = kBwdBatch - 1; j >= 0; --j) {
-      const SplatRec& s = s_rec[j];
-      const int idx = lo - start + j;
-      const bool contrib = j < cnt && inside && idx < last && px >= s.x0 && px <= s.x1 && py >= s.y0 && py <= s.y1;
-      float w = 0.f, drho = 0.f, dg = 0.f;
-      if (contrib) {
-        // replay of the forward blend; the set of blended (pixel, splat) pairs comes from the
-        // forward (px_last), so alpha' only needs gradient accuracy here (fast exp / rcp).
-        const float dx = fx - s.mean_x;
-        const float dy = fy - s.mean_y;
-        const float rho = fmaf(s.a00 * dx, dx, fmaf(2.f * s.a01 * dx, dy, s.a11 * dy * dy));
-        float al = s.alpha * __expf(-0.5f * rho);
-        const bool clamped = al > kAlphaMax;
-        if (clamped) al = kAlphaMax;
-        const float r = __frcp_rn(1.f - al);
-        const float Tb = T * r;
-        w = al * Tb;
-        const float* fr = s_f + j * NU;
-        float value = uc0 * fr[0] + uc1 * fr[1] + uc2 * fr[2] + uz * fr[3];
+    // ---- value[p][j] = U[p] . [c_j, z_j, f_j] for the warp's 32 pixels x 16 splats on the tensor
+    // cores (3xTF32), staged through sw_g as [splat][pixel] (each thread then reads its own
+    // pixel's column and overwrites that slot with dg)
+    {
+      float va[2][2][4];
 #pragma unroll
-        for (int c = 0; c < DSP; ++c) value = fmaf(uq[c], fr[4 + c], value);
-        const float d_alpha = Tb * value - s_after * r;
-        s_after = fmaf(w, value, s_after);
-        if (!clamped) {
-          dg = d_alpha * __fdividef(al, s.alpha);
-          drho = -0.5f * al * d_alpha;
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) va[mt][nt][0] = va[mt][nt][1] = va[mt][nt][2] = va[mt][nt][3] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < NU / 8; ++ks) {
+        uint32_t uh[2][4], ul[2][4];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const int pr = 32 * warp + 16 * mt + g;
+          split_tf32(s_u[uidx(pr, 8 * ks + cq)], uh[mt][0], ul[mt][0]);
+          split_tf32(s_u[uidx(pr + 8, 8 * ks + cq)], uh[mt][1], ul[mt][1]);
+          split_tf32(s_u[uidx(pr, 8 * ks + cq + 4)], uh[mt][2], ul[mt][2]);
+          split_tf32(s_u[uidx(pr + 8, 8 * ks + cq + 4)], uh[mt][3], ul[mt][3]);
         }
-        T = Tb;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          const int fo = (8 * nt + g) * NUP + 8 * ks + cq;
+          const uint32_t bh[2] = {__float_as_uint(s_fh[fo]), __float_as_uint(s_fh[fo + 4])};
+          const uint32_t bl[2] = {__float_as_uint(s_fl[fo]), __float_as_uint(s_fl[fo + 4])};
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            mma_tf32(va[mt][nt], ul[mt], bh);
+            mma_tf32(va[mt][nt], uh[mt], bl);
+            mma_tf32(va[mt][nt], uh[mt], bh);
+          }
+        }
       }
-      sw_w[j * WP + lane] = w;
-      sw_r[j * WP + lane] = drho;
-      sw_g[j * WP + lane] = dg;
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          float* d = sw_g + (8 * nt + 2 * cq) * WP + 16 * mt + g;
+          d[0] = va[mt][nt][0];
+          d[WP] = va[mt][nt][1];
+          d[8] = va[mt][nt][2];
+          d[WP + 8] = va[mt][nt][3];
+        }
+      __syncwarp();
+    }
+    // ---- per-pixel reverse sweep over the batch. alpha' of four splats is evaluated
+    // independently (ILP), then the transmittance recovery / d_alpha chain runs serially.
+    // The set of blended (pixel, splat) pairs comes from the forward (px_last), so alpha' only
+    // needs gradient accuracy here (fast exp / rcp).
+#pragma unroll
+    for (int j4 = kBwdBatch - 4; j4 >= 0; j4 -= 4) {
+      float alv[4], ex[4], rv[4];
+      bool ok[4], unc[4];
+      bool any = false;
+#pragma unroll
+      for (int u = 3; u >= 0; --u) {
+        const int j = j4 + u;
+        const SplatRec& s = s_rec[j];
+        ok[u] = j < cnt && inside && lo - start + j < last && px >= s.x0 && px <= s.x1 && py >= s.y0 && py <= s.y1;
+        any |= ok[u];
+      }
+      if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+        for (int u = 3; u >= 0; --u) {
+          const SplatRec& s = s_rec[j4 + u];
+          const float dx = fx - s.mean_x;
+          const float dy = fy - s.mean_y;
+          const float rho = fmaf(s.a00 * dx, dx, fmaf(2.f * s.a01 * dx, dy, s.a11 * dy * dy));
+          ex[u] = __expf(-0.5f * rho);
+          float al = s.alpha * ex[u];
+          unc[u] = !(al > kAlphaMax);
+          if (!unc[u]) al = kAlphaMax;
+          alv[u] = al;
+          rv[u] = __frcp_rn(1.f - al);
+        }
+      }
+#pragma unroll
+      for (int u = 3; u >= 0; --u) {
+        const int j = j4 + u;
+        float w = 0.f, drho = 0.f, dg = 0.f;
+        if (ok[u]) {
+          const float Tb = T * rv[u];
+          w = alv[u] * Tb;
+          const float value = sw_g[j * WP + lane];
+          const float d_alpha = Tb * value - s_after * rv[u];
+          s_after = fmaf(w, value, s_after);
+          if (unc[u]) {
+            dg = d_alpha * ex[u];
+            drho = -0.5f * alv[u] * d_alpha;
+          }
+          T = Tb;
+        }
+        sw_w[j * WP + lane] = w;
+        sw_r[j * WP + lane] = drho;
+        sw_g[j * WP + lane] = dg;
+      }
     }
     __syncwarp();
     // ---- tensor-core reductions over the warp's 32 pixels
@@ -646,8 +895,8 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         uint32_t bh[2], bl[2];
-        split_tf32(s_u[prow * UP + 8 * nt + g], bh[0], bl[0]);
-        split_tf32(s_u[(prow + 4) * UP + 8 * nt + g], bh[1], bl[1]);
+        split_tf32(s_u[uidx(prow, 8 * nt + g)], bh[0], bl[0]);
+        split_tf32(s_u[uidx(prow + 4, 8 * nt + g)], bh[1], bl[1]);
         mma_tf32(dwu[nt], ah, bh);
         mma_tf32(dwu[nt], ah, bl);
         mma_tf32(dwu[nt], al_, bh);
@@ -665,21 +914,27 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
         mma_tf32(dmo[mt], rl, xb[ks]);
       }
     }
-    // ---- cross-warp sum into the CTA accumulator (rows = splats)
+    // ---- warp partials (rows = splats) into the warp's own staging area, then a cross-warp sum
+    __syncwarp();
+    float* part = sw_w;
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
-      atomicAdd(&s_acc[g * NACC + 8 * nt + 2 * cq], dwu[nt][0]);
-      atomicAdd(&s_acc[g * NACC + 8 * nt + 2 * cq + 1], dwu[nt][1]);
-      atomicAdd(&s_acc[(g + 8) * NACC + 8 * nt + 2 * cq], dwu[nt][2]);
-      atomicAdd(&s_acc[(g + 8) * NACC + 8 * nt + 2 * cq + 1], dwu[nt][3]);
+      *reinterpret_cast<float2*>(part + g * PP + 8 * nt + 2 * cq) = make_float2(dwu[nt][0], dwu[nt][1]);
+      *reinterpret_cast<float2*>(part + (g + 8) * PP + 8 * nt + 2 * cq) = make_float2(dwu[nt][2], dwu[nt][3]);
     }
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
       const int base = NU + 8 * mt;
-      atomicAdd(&s_acc[g * NACC + base + 2 * cq], dmo[mt][0]);
-      atomicAdd(&s_acc[g * NACC + base + 2 * cq + 1], dmo[mt][1]);
-      atomicAdd(&s_acc[(g + 8) * NACC + base + 2 * cq], dmo[mt][2]);
-      atomicAdd(&s_acc[(g + 8) * NACC + base + 2 * cq + 1], dmo[mt][3]);
+      *reinterpret_cast<float2*>(part + g * PP + base + 2 * cq) = make_float2(dmo[mt][0], dmo[mt][1]);
+      *reinterpret_cast<float2*>(part + (g + 8) * PP + base + 2 * cq) = make_float2(dmo[mt][2], dmo[mt][3]);
+    }
+    __syncthreads();
+    for (int e = tid; e < kBwdBatch * NACC; e += blockDim.x) {
+      const int j = e / NACC, c = e % NACC;
+      float v = 0.f;
+#pragma unroll
+      for (int w8 = 0; w8 < 8; ++w8) v += s_wbase[w8 * 3 * kBwdBatch * WP + j * PP + c];
+      s_acc[e] = v;
     }
     __syncthreads();
     // ---- per-splat closed forms + global accumulation
@@ -842,15 +1097,24 @@ __global__ void project_single_kernel(const float* in, Cam cam, float* out) {
 
 template <int DSP>
 void launch_fwd(cudaStream_t st, int ntiles, const RasterArgs& a, bool exact) {
-  if (exact)
+  if (exact) {
     raster_fwd_kernel<DSP, true><<<ntiles, kTilePixels, 0, st>>>(a);
-  else
+  } else if constexpr (DSP >= 8) {
+    const size_t smem = sizeof(float) * (2 * 128 * (DSP + 8) + 8 * 16 * 40);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(raster_fwd_mma_kernel<DSP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    raster_fwd_mma_kernel<DSP><<<ntiles, kTilePixels, smem, st>>>(a);
+  } else {
     raster_fwd_kernel<DSP, false><<<ntiles, kTilePixels, 0, st>>>(a);
+  }
 }
 template <int DSP>
 void launch_bwd(cudaStream_t st, int ntiles, const RasterBwdArgs& a) {
   constexpr int NU = ((4 + DSP) + 7) / 8 * 8;
-  constexpr int UP = NU + (NU % 32 == 0 ? 4 : (NU % 16 == 0 ? 4 : 0));
+  constexpr int UP = NU % 16 == 8 ? NU : NU + 8;
   const size_t smem = sizeof(float) * ((size_t)kTilePixels * UP + 8 * 3 * kBwdBatch * 36);
   static bool attr = false;
   if (!attr) {
