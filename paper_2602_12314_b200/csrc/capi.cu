@@ -85,10 +85,19 @@ struct RenderBufs {
     w.tiles_x = (width + kTile - 1) / kTile;
     w.tiles_y = (height + kTile - 1) / kTile;
     const size_t nt = (size_t)w.tiles_x * w.tiles_y;
-    if ((e = dgrow(w.rec, c_rec, (size_t)std::max<int64_t>(n, 1)))) return e;
-    size_t c1 = c_tiles, c2 = c_tiles, c3 = c_tiles, c4 = c_tiles;
+    const size_t n1 = (size_t)std::max<int64_t>(n, 1);
+    if (n1 > c_rec) {
+      size_t a = 0, b = 0;
+      if (w.rec) cudaFree(w.rec), w.rec = nullptr;
+      if (w.dkey) cudaFree(w.dkey), w.dkey = nullptr;
+      if ((e = dgrow(w.rec, a, n1))) return e;
+      if ((e = dgrow(w.dkey, b, n1))) return e;
+      c_rec = n1;
+    }
+    size_t c1 = c_tiles, c2 = c_tiles, c3 = c_tiles, c4 = c_tiles, c5 = c_tiles;
     if (nt + 1 > c_tiles) {
-      c1 = c2 = c3 = c4 = 0;
+      c1 = c2 = c3 = c4 = c5 = 0;
+      if ((e = dgrow(w.tile_order, c5, nt + 1))) return e;
       if ((e = dgrow(w.tile_count, c1, nt + 1))) return e;
       if ((e = dgrow(w.tile_offset, c2, nt + 1))) return e;
       if ((e = dgrow(w.tile_cursor, c3, nt + 1))) return e;
@@ -99,9 +108,9 @@ struct RenderBufs {
       size_t a = 0, b = 0;
       if (w.keys) cudaFree(w.keys), w.keys = nullptr;
       if (w.keys_tmp) cudaFree(w.keys_tmp), w.keys_tmp = nullptr;
-      if ((e = dgrow(w.keys, a, (size_t)std::max<int64_t>(pairs, 1)))) return e;
-      if ((e = dgrow(w.keys_tmp, b, (size_t)std::max<int64_t>(pairs, 1)))) return e;
       c_keys = (size_t)std::max<int64_t>(pairs, 1);
+      if ((e = dgrow(w.keys, a, c_keys))) return e;
+      if ((e = dgrow(w.keys_tmp, b, c_keys))) return e;
     }
     w.pair_cap = (int64_t)c_keys;
     size_t px = (size_t)width * height;
@@ -114,16 +123,18 @@ struct RenderBufs {
       c_px = px;
     }
     if ((e = dgrow(w.counters, c_cnt, 4))) return e;
-    if ((e = dgrow(geo_acc, c_geo, (size_t)std::max<int64_t>(n, 1) * 8))) return e;
+    if ((e = dgrow(geo_acc, c_geo, n1 * 8))) return e;
     w.n_cap = n;
     return cudaSuccess;
   }
   void release() {
     for (void* p : {(void*)w.rec, (void*)w.tile_count, (void*)w.tile_offset, (void*)w.tile_cursor, (void*)w.keys,
-                    (void*)w.keys_tmp, (void*)w.px_last, (void*)w.px_T, (void*)w.counters, (void*)w.tile_max_last,
-                    (void*)geo_acc})
+                    (void*)w.keys_tmp, (void*)w.dkey, (void*)w.px_last, (void*)w.px_T, (void*)w.counters,
+                    (void*)w.tile_max_last, (void*)w.tile_order, (void*)geo_acc})
       if (p) cudaFree(p);
     w = RenderWork{};
+    geo_acc = nullptr;
+    c_rec = c_tiles = c_keys = c_px = c_cnt = c_geo = 0;
   }
 };
 

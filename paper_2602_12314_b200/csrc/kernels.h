@@ -29,10 +29,12 @@ struct RenderWork {
   int32_t* tile_cursor = nullptr;   // ntiles
   uint64_t* keys = nullptr;         // pair_cap, (depth_bits << 32 | source), sorted per tile
   uint64_t* keys_tmp = nullptr;     // pair_cap, merge scratch for oversized tiles
+  uint32_t* dkey = nullptr;         // n_cap: float bits of camera z (0xffffffff = culled)
   int32_t* px_last = nullptr;       // H*W: tile-list entries consumed by the pixel
   float* px_T = nullptr;            // H*W: transmittance after the last blended splat
   int64_t* counters = nullptr;      // [0] pairs, [1] visible, [2] overflow, [3] big tiles
   int32_t* tile_max_last = nullptr; // ntiles: max px_last over the tile
+  int32_t* tile_order = nullptr;    // ntiles: blend dispatch order (longest lists first)
   int64_t* step_overflow = nullptr;  // optional session-level overflow flag
 };
 

@@ -124,10 +124,12 @@ __device__ __forceinline__ bool project_exact(const float* __restrict__ p, const
 }
 
 constexpr int kHistMax = 12288;  // tiles counted in shared memory (48 KB)
+constexpr uint32_t kCulledKey = 0xffffffffu;  // depth key of a culled Gaussian (z bits < 0x7f800000)
 
 // K1: project every Gaussian, write its record, count tile pairs.
 __global__ void __launch_bounds__(256) project_kernel(MapPtrs map, Cam cam, SplatRec* __restrict__ rec,
-                                                      int32_t* __restrict__ tile_count, int64_t* counters) {
+                                                      uint32_t* __restrict__ dkey, int32_t* __restrict__ tile_count,
+                                                      int64_t* counters) {
   extern __shared__ int32_t s_hist[];
   const int ntiles = cam.tiles_x * cam.tiles_y;
   const bool use_smem = ntiles <= kHistMax;
@@ -152,6 +154,7 @@ __global__ void __launch_bounds__(256) project_kernel(MapPtrs map, Cam cam, Spla
             atomicAdd(&tile_count[t], 1);
         }
     }
+    dkey[i] = ok ? __float_as_uint(r.depth) : kCulledKey;
     reinterpret_cast<float4*>(rec + i)[0] = make_float4(r.mean_x, r.mean_y, r.depth, r.alpha);
     reinterpret_cast<float4*>(rec + i)[1] = make_float4(r.a00, r.a01, r.a10, r.a11);
     reinterpret_cast<int4*>(rec + i)[2] = make_int4(r.x0, r.x1, r.y0, r.y1);
@@ -164,10 +167,14 @@ __global__ void __launch_bounds__(256) project_kernel(MapPtrs map, Cam cam, Spla
       if (s_hist[t]) atomicAdd(&tile_count[t], s_hist[t]);
 }
 
-// K2: exclusive scan of per-tile counts (one block).
+constexpr int kOrderBuckets = 512;
+__device__ __forceinline__ int order_bucket(int c) { return kOrderBuckets - 1 - min(kOrderBuckets - 1, c >> 3); }
+
+// K2: exclusive scan of per-tile counts (one block) + the longest-first tile dispatch order.
 __global__ void __launch_bounds__(1024) scan_tiles_kernel(const int32_t* __restrict__ count, int32_t* offset,
                                                           int32_t* cursor, int ntiles, int64_t* counters,
-                                                          int64_t pair_cap, int64_t* step_overflow) {
+                                                          int64_t pair_cap, int64_t* step_overflow,
+                                                          int32_t* order) {
   __shared__ int64_t s_part[1024];
   const int per = (ntiles + blockDim.x - 1) / blockDim.x;
   const int b = threadIdx.x * per;
@@ -189,6 +196,25 @@ __global__ void __launch_bounds__(1024) scan_tiles_kernel(const int32_t* __restr
       cursor[b + i] = (int32_t)run;
       run += count[b + i];
     }
+  // Dispatch order for the blend kernels: tiles by descending list length (coarse buckets of
+  // 8 splats), so the longest tiles start first and the last wave is made of short tiles.
+  if (order) {
+    __shared__ int32_t s_bk[kOrderBuckets];
+    for (int i = threadIdx.x; i < kOrderBuckets; i += blockDim.x) s_bk[i] = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) atomicAdd(&s_bk[order_bucket(count[t])], 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int run2 = 0;
+      for (int i = 0; i < kOrderBuckets; ++i) {
+        const int c = s_bk[i];
+        s_bk[i] = run2;
+        run2 += c;
+      }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) order[atomicAdd(&s_bk[order_bucket(count[t])], 1)] = t;
+  }
   if (threadIdx.x == blockDim.x - 1) {
     offset[ntiles] = (int32_t)s_part[threadIdx.x];
     counters[0] = s_part[threadIdx.x];
@@ -200,9 +226,13 @@ __global__ void __launch_bounds__(1024) scan_tiles_kernel(const int32_t* __restr
 // K3: scatter (depth_bits << 32 | source) keys into their tile buckets. Each block first
 // counts its pairs per tile in shared memory, reserves one contiguous range per (block, tile)
 // with a single global atomic, then fills it (slot order inside a bucket is irrelevant: the
-// per-tile sort below makes the list canonical).
-constexpr int kScatterPerThread = 2;
-__global__ void __launch_bounds__(256) scatter_kernel(const SplatRec* __restrict__ rec, int64_t n, int tiles_x,
+// per-tile sort below makes the list canonical). 2048 Gaussians per block keep the number of
+// global reservations (blocks x touched tiles) low; culled Gaussians are skipped via the
+// projection's depth keys without touching their records.
+constexpr int kScatterPerThread = 4;
+constexpr int kScatterThreads = 512;
+__global__ void __launch_bounds__(kScatterThreads, 2) scatter_kernel(const SplatRec* __restrict__ rec,
+                                                      const uint32_t* __restrict__ dkey, int64_t n, int tiles_x,
                                                       int ntiles, int32_t* cursor, uint64_t* __restrict__ keys,
                                                       int64_t pair_cap) {
   extern __shared__ int32_t s_cnt[];
@@ -210,14 +240,22 @@ __global__ void __launch_bounds__(256) scatter_kernel(const SplatRec* __restrict
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s_cnt[t] = 0;
   __syncthreads();
   const int64_t b0 = (int64_t)blockIdx.x * blockDim.x * kScatterPerThread;
-#pragma unroll 1
+  uint32_t dk[kScatterPerThread];
+  int4 bb[kScatterPerThread];
+#pragma unroll
   for (int r = 0; r < kScatterPerThread; ++r) {
     const int64_t i = b0 + (int64_t)r * blockDim.x + threadIdx.x;
-    if (i >= n) break;
-    const int4 bb = reinterpret_cast<const int4*>(rec + i)[2];
-    if (bb.x > bb.y) continue;
-    for (int ty = bb.z / kTile; ty <= bb.w / kTile; ++ty)
-      for (int tx = bb.x / kTile; tx <= bb.y / kTile; ++tx) atomicAdd(&s_cnt[ty * tiles_x + tx], 1);
+    dk[r] = i < n ? dkey[i] : kCulledKey;
+    bb[r] = make_int4(1, 0, 1, 0);
+  }
+#pragma unroll
+  for (int r = 0; r < kScatterPerThread; ++r)
+    if (dk[r] != kCulledKey) bb[r] = reinterpret_cast<const int4*>(rec + b0 + (int64_t)r * blockDim.x + threadIdx.x)[2];
+#pragma unroll
+  for (int r = 0; r < kScatterPerThread; ++r) {
+    if (dk[r] == kCulledKey) continue;
+    for (int ty = bb[r].z / kTile; ty <= bb[r].w / kTile; ++ty)
+      for (int tx = bb[r].x / kTile; tx <= bb[r].y / kTile; ++tx) atomicAdd(&s_cnt[ty * tiles_x + tx], 1);
   }
   __syncthreads();
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
@@ -226,15 +264,12 @@ __global__ void __launch_bounds__(256) scatter_kernel(const SplatRec* __restrict
     s_cnt[t] = 0;
   }
   __syncthreads();
-#pragma unroll 1
+#pragma unroll
   for (int r = 0; r < kScatterPerThread; ++r) {
-    const int64_t i = b0 + (int64_t)r * blockDim.x + threadIdx.x;
-    if (i >= n) break;
-    const int4 bb = reinterpret_cast<const int4*>(rec + i)[2];
-    if (bb.x > bb.y) continue;
-    const uint64_t key = ((uint64_t)__float_as_uint(rec[i].depth) << 32) | (uint32_t)i;
-    for (int ty = bb.z / kTile; ty <= bb.w / kTile; ++ty)
-      for (int tx = bb.x / kTile; tx <= bb.y / kTile; ++tx) {
+    if (dk[r] == kCulledKey) continue;
+    const uint64_t key = ((uint64_t)dk[r] << 32) | (uint32_t)(b0 + (int64_t)r * blockDim.x + threadIdx.x);
+    for (int ty = bb[r].z / kTile; ty <= bb[r].w / kTile; ++ty)
+      for (int tx = bb[r].x / kTile; tx <= bb[r].y / kTile; ++tx) {
         const int t = ty * tiles_x + tx;
         const int64_t pos = (int64_t)s_base[t] + atomicAdd(&s_cnt[t], 1);
         if (pos < pair_cap) keys[pos] = key;
@@ -242,54 +277,205 @@ __global__ void __launch_bounds__(256) scatter_kernel(const SplatRec* __restrict
   }
 }
 
-constexpr int kSortCap = 8192;  // keys sorted in shared memory per tile (64 KB)
+// K3b: per-tile bitonic sort of the (depth, source) keys -> canonical order. Keys are unique,
+// so the result is deterministic whatever order K3's atomics produced. 512 threads hold KPT
+// consecutive keys each (blocked layout): compare-exchange partners at distance j < KPT are in
+// the same thread's registers, j < 32 KPT in the same warp (shuffles), larger j go through
+// shared memory (10 of the 66 stages at P = 2048).
+constexpr int kSortThreads = 512;
+constexpr int kSortCap = 8192;  // keys sorted in one pass (16 per thread, 64 KB of shared memory)
 
-__device__ void bitonic_smem(uint64_t* s, int P) {
-  for (int k = 2; k <= P; k <<= 1)
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const bool asc = (i & k) == 0;
-          const uint64_t a = s[i], b = s[ixj];
-          if ((a > b) == asc) {
-            s[i] = b;
-            s[ixj] = a;
-          }
-        }
+template <int KPT, int J>
+__device__ __forceinline__ void bitonic_reg_stage(uint64_t (&v)[KPT], int tid, int k) {
+#pragma unroll
+  for (int e = 0; e < KPT; ++e)
+    if ((e & J) == 0) {
+      const bool asc = (((tid * KPT + e) & k) == 0);
+      const uint64_t a = v[e], b = v[e | J];
+      if ((a > b) == asc) {
+        v[e] = b;
+        v[e | J] = a;
       }
-      __syncthreads();
     }
 }
 
-// K3b: per-tile sort of the keys -> canonical (depth, source) order. Keys are unique,
-// so the result is deterministic whatever order K3's atomics produced.
-__global__ void __launch_bounds__(512) tile_sort_kernel(const int32_t* __restrict__ offset, uint64_t* keys,
-                                                        uint64_t* tmp, int64_t pair_cap, const int64_t* counters) {
+template <int KPT>
+__device__ void bitonic_block(uint64_t (&v)[KPT], uint64_t* s, int P) {
+  const int tid = threadIdx.x;
+  for (int k = 2; k <= P; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j < KPT) {
+        if (j == 1) bitonic_reg_stage<KPT, 1>(v, tid, k);
+        if constexpr (KPT > 2) if (j == 2) bitonic_reg_stage<KPT, 2>(v, tid, k);
+        if constexpr (KPT > 4) if (j == 4) bitonic_reg_stage<KPT, 4>(v, tid, k);
+        if constexpr (KPT > 8) if (j == 8) bitonic_reg_stage<KPT, 8>(v, tid, k);
+      } else if (j < 32 * KPT) {
+        const int lm = j / KPT;
+        const bool lower = (tid & lm) == 0;
+#pragma unroll
+        for (int e = 0; e < KPT; ++e) {
+          const uint64_t o = __shfl_xor_sync(0xffffffffu, v[e], lm);
+          const bool asc = (((tid * KPT + e) & k) == 0);
+          v[e] = (lower == asc) ? (v[e] < o ? v[e] : o) : (v[e] < o ? o : v[e]);
+        }
+      } else {
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < KPT; ++e) s[tid * KPT + e] = v[e];
+        __syncthreads();
+        const bool lower = ((tid * KPT) & j) == 0;
+#pragma unroll
+        for (int e = 0; e < KPT; ++e) {
+          const int i = tid * KPT + e;
+          const uint64_t o = s[i ^ j];
+          const bool asc = ((i & k) == 0);
+          v[e] = (lower == asc) ? (v[e] < o ? v[e] : o) : (v[e] < o ? o : v[e]);
+        }
+      }
+    }
+}
+
+template <int KPT>
+__device__ void sort_chunk(uint64_t* g, int n, uint64_t* s) {
+  constexpr int P = KPT * kSortThreads;
+  uint64_t v[KPT];
+#pragma unroll
+  for (int e = 0; e < KPT; ++e) {
+    const int i = threadIdx.x * KPT + e;
+    v[e] = i < n ? g[i] : ~0ull;
+  }
+  bitonic_block<KPT>(v, s, P);
+#pragma unroll
+  for (int e = 0; e < KPT; ++e) {
+    const int i = threadIdx.x * KPT + e;
+    if (i < n) g[i] = v[e];
+  }
+}
+
+__device__ void sort_chunk_any(uint64_t* g, int n, uint64_t* s) {
+  if (n <= 512) sort_chunk<1>(g, n, s);
+  else if (n <= 1024) sort_chunk<2>(g, n, s);
+  else if (n <= 2048) sort_chunk<4>(g, n, s);
+  else if (n <= 4096) sort_chunk<8>(g, n, s);
+  else sort_chunk<16>(g, n, s);
+}
+
+// Per-tile stable LSD radix sort on the depth half of the keys (4 passes of 8 bits) in shared
+// memory, then the rare runs of equal depth are put in source order (the key's low half). The
+// 512 threads form 16 warps; warp w owns elements [w*32*EPT, (w+1)*32*EPT) in EPT rounds of 32,
+// and an element's rank among equal digits before it is (round peers below it, __match_any)
+// + (warp's running count) + (exclusive scan over (digit, warp) in digit-major order).
+constexpr int kRadixCap = 4096;  // tile lists up to this length take the radix path (EPT <= 8)
+constexpr size_t kTileSortSmem = 2 * kRadixCap * 8 + 16 * 257 * 4;  // >= kSortCap * 8
+
+__device__ void tile_radix_sort(uint64_t* __restrict__ g, int n, uint64_t* s_a, uint64_t* s_b, uint32_t* s_h) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ept = (n + kSortThreads - 1) / kSortThreads;
+  for (int i = tid; i < n; i += kSortThreads) s_a[i] = g[i];
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t* s_w = s_h;  // [16 warps][257] (padded: conflict-free column walks)
+#pragma unroll 1
+  for (int pass = 0; pass < 4; ++pass) {
+    const int shift = 32 + 8 * pass;
+    for (int i = tid; i < 257 * 16; i += kSortThreads) s_w[i] = 0u;
+    __syncthreads();
+    uint64_t k[8];
+    uint32_t loc[8];
+    int d[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      if (r >= ept) break;
+      const int i = (warp * ept + r) * 32 + lane;
+      k[r] = i < n ? s_a[i] : 0ull;
+      d[r] = i < n ? (int)((k[r] >> shift) & 255u) : 256;
+      const uint32_t peers = __match_any_sync(0xffffffffu, d[r]);
+      const bool ok = d[r] < 256;
+      loc[r] = __popc(peers & lt) + (ok ? s_w[warp * 257 + (ok ? d[r] : 0)] : 0u);
+      __syncwarp();
+      if (ok && (peers & lt) == 0u) s_w[warp * 257 + d[r]] += __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    {  // exclusive scan over (digit, warp) in digit-major order: entry e = tid * 8 + j
+      uint32_t v[8], sum = 0;
+      const int dd = tid >> 1, w0 = (tid & 1) * 8;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        v[j] = s_w[(w0 + j) * 257 + dd];
+        sum += v[j];
+      }
+      uint32_t incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      __shared__ uint32_t s_ws[16];
+      if (lane == 31) s_ws[warp] = incl;
+      __syncthreads();
+      uint32_t wb = lane < 16 && lane < warp ? s_ws[lane] : 0u;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) wb += __shfl_xor_sync(0xffffffffu, wb, o);
+      uint32_t run = wb + incl - sum;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        s_w[(w0 + j) * 257 + dd] = run;
+        run += v[j];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      if (r >= ept) break;
+      if (d[r] < 256) s_b[s_w[warp * 257 + d[r]] + loc[r]] = k[r];
+    }
+    __syncthreads();
+    uint64_t* sw = s_a;
+    s_a = s_b;
+    s_b = sw;
+  }
+  // equal depths (rare): order each run by source
+  for (int i = tid; i < n; i += kSortThreads) {
+    const uint32_t di = (uint32_t)(s_a[i] >> 32);
+    const bool start = i == 0 || (uint32_t)(s_a[i - 1] >> 32) != di;
+    if (start && i + 1 < n && (uint32_t)(s_a[i + 1] >> 32) == di) {
+      int e = i + 1;
+      while (e < n && (uint32_t)(s_a[e] >> 32) == di) ++e;
+      for (int a = i + 1; a < e; ++a) {  // insertion sort of [i, e) by the full key
+        const uint64_t x = s_a[a];
+        int b = a - 1;
+        while (b >= i && s_a[b] > x) {
+          s_a[b + 1] = s_a[b];
+          --b;
+        }
+        s_a[b + 1] = x;
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += kSortThreads) g[i] = s_a[i];
+}
+
+__global__ void __launch_bounds__(kSortThreads, 2) tile_sort_kernel(const int32_t* __restrict__ offset, uint64_t* keys,
+                                                                 uint64_t* tmp, int64_t pair_cap,
+                                                                 const int64_t* counters) {
   extern __shared__ uint64_t s_keys[];
   if (counters[2]) return;  // overflowed: step is discarded and re-run by the host
   const int t = blockIdx.x;
   const int start = offset[t], n = offset[t + 1] - start;
   if (n <= 1) return;
   uint64_t* g = keys + start;
-  if (n <= kSortCap) {
-    int P = 1;
-    while (P < n) P <<= 1;
-    for (int i = threadIdx.x; i < P; i += blockDim.x) s_keys[i] = i < n ? g[i] : ~0ull;
-    __syncthreads();
-    bitonic_smem(s_keys, P);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) g[i] = s_keys[i];
+  if (n <= kRadixCap) {
+    tile_radix_sort(g, n, s_keys, s_keys + kRadixCap, reinterpret_cast<uint32_t*>(s_keys + 2 * kRadixCap));
     return;
   }
-  // Oversized tile: sort kSortCap chunks in smem, then merge runs pairwise in global memory.
+  if (n <= kSortCap) {
+    sort_chunk_any(g, n, s_keys);
+    return;
+  }
+  // Oversized tile: sort kSortCap chunks, then merge runs pairwise in global memory.
   for (int c0 = 0; c0 < n; c0 += kSortCap) {
-    const int cn = min(kSortCap, n - c0);
-    int P = 1;
-    while (P < cn) P <<= 1;
-    for (int i = threadIdx.x; i < P; i += blockDim.x) s_keys[i] = i < cn ? g[c0 + i] : ~0ull;
-    __syncthreads();
-    bitonic_smem(s_keys, P);
-    for (int i = threadIdx.x; i < cn; i += blockDim.x) g[c0 + i] = s_keys[i];
+    sort_chunk<16>(g + c0, min(kSortCap, n - c0), s_keys);
     __syncthreads();
   }
   uint64_t* src = g;
@@ -332,13 +518,14 @@ struct RasterArgs {
   const float* feats;
   int32_t ds;
   const int32_t* offset;
-  const uint64_t* keys;
+  const uint64_t* keys;  // per-tile lists: (depth bits << 32 | source)
   int32_t tiles_x, width, height;
   float *color, *depth, *query, *alpha;
   int32_t* px_last;
   float* px_T;
   int32_t* tile_max_last;
   const int64_t* counters;
+  const int32_t* order;  // dispatch order (longest tile lists first)
 };
 
 // K4: forward blend, one CTA per 16x16 tile, one thread per pixel. alpha', the clamp, the
@@ -353,7 +540,7 @@ __global__ void __launch_bounds__(kTilePixels) raster_fwd_kernel(RasterArgs a) {
   __shared__ float s_feat[kFwdBatch * DSP];
   __shared__ int32_t s_max;
   if (a.counters[2]) return;
-  const int tile = blockIdx.x;
+  const int tile = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
   const int px = (tile % a.tiles_x) * kTile + (threadIdx.x % kTile);
   const int py = (tile / a.tiles_x) * kTile + (threadIdx.x / kTile);
   const bool inside = px < a.width && py < a.height;
@@ -442,7 +629,7 @@ struct RasterBwdArgs {
   const float* feats;
   int32_t ds;
   const int32_t* offset;
-  const uint64_t* keys;
+  const uint64_t* keys;  // per-tile lists: (depth bits << 32 | source)
   int32_t tiles_x, width, height;
   const int32_t* px_last;
   const float* px_T;
@@ -451,6 +638,7 @@ struct RasterBwdArgs {
   float* geo_acc;  // N x 8: dmean_u, dmean_v, dA00, dA01, dA11, dz, dg
   float* g_col;    // N x 3
   float* g_feat;   // N x ds
+  const int32_t* order;
 };
 
 constexpr int kBwdBatch = 16;  // splats per batch (one MMA M tile)
@@ -460,9 +648,12 @@ __device__ __forceinline__ uint32_t to_tf32(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return r;
 }
+// 3xTF32 operand split by truncation: hi keeps the top 10 mantissa bits, lo = x - hi (exact
+// in fp32) truncated likewise; |x - hi - lo| < 2^-20 |x|. Three integer/fp ops instead of the
+// six of two cvt.rna.tf32 conversions (which lower to FSETP + IADD + LOP3 each on sm_100a).
 __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
-  hi = to_tf32(x);
-  lo = to_tf32(x - __uint_as_float(hi));
+  hi = __float_as_uint(x) & 0xffffe000u;
+  lo = __float_as_uint(x - __uint_as_float(hi)) & 0xffffe000u;
 }
 // D += A * B, m16n8k8, tf32 inputs, fp32 accumulate (legacy warp MMA, used for small in-kernel reductions)
 __device__ __forceinline__ void mma_tf32(float* d, const uint32_t* a, const uint32_t* b) {
@@ -494,7 +685,7 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_fwd_mma_kernel(RasterAr
   if (a.counters[2]) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, cq = lane & 3;
-  const int tile = blockIdx.x;
+  const int tile = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
   const int tx0 = (tile % a.tiles_x) * kTile, ty0 = (tile / a.tiles_x) * kTile;
   const int px = tx0 + (tid % kTile), py = ty0 + (tid / kTile);
   const bool inside = px < a.width && py < a.height;
@@ -680,7 +871,7 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
   __shared__ uint32_t s_src[kBwdBatch];
   __shared__ float s_acc[kBwdBatch * NACC];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int tile = blockIdx.x;
+  const int tile = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
   const int tx0 = (tile % a.tiles_x) * kTile, ty0 = (tile / a.tiles_x) * kTile;
   const int px = tx0 + (tid % kTile), py = ty0 + (tid / kTile);
   const bool inside = px < a.width && py < a.height;
@@ -1168,11 +1359,11 @@ void render_forward(cudaStream_t st, const MapPtrs& map, const float rot_cw[9], 
   const int grid1 = 148 * 2;
   const size_t hist_smem = ntiles <= kHistMax ? sizeof(int32_t) * ntiles : 0;
   if (map.n > 0) {
-    project_kernel<<<grid1, 256, hist_smem, st>>>(map, cam, w.rec, w.tile_count, w.counters);
+    project_kernel<<<grid1, 256, hist_smem, st>>>(map, cam, w.rec, w.dkey, w.tile_count, w.counters);
     count_launch();
   }
   scan_tiles_kernel<<<1, 1024, 0, st>>>(w.tile_count, w.tile_offset, w.tile_cursor, ntiles, w.counters, w.pair_cap,
-                                        w.step_overflow);
+                                        w.step_overflow, w.tile_order);
   count_launch();
   if (count_only) return;
   if (map.n > 0) {
@@ -1182,17 +1373,19 @@ void render_forward(cudaStream_t st, const MapPtrs& map, const float rot_cw[9], 
       cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 4 * kHistMax);
       sc_attr = true;
     }
-    const unsigned sc_grid = (unsigned)((map.n + 256 * kScatterPerThread - 1) / (256 * kScatterPerThread));
-    scatter_kernel<<<sc_grid, 256, sc_smem, st>>>(w.rec, map.n, w.tiles_x, ntiles, w.tile_cursor, w.keys,
+    const unsigned sc_grid =
+        (unsigned)((map.n + kScatterThreads * kScatterPerThread - 1) / (kScatterThreads * kScatterPerThread));
+    scatter_kernel<<<sc_grid, kScatterThreads, sc_smem, st>>>(w.rec, w.dkey, map.n, w.tiles_x, ntiles, w.tile_cursor, w.keys,
                                                  w.pair_cap);
     count_launch();
   }
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(tile_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortCap * 8);
+    cudaFuncSetAttribute(tile_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSortSmem);
     attr_set = true;
   }
-  tile_sort_kernel<<<ntiles, 512, kSortCap * 8, st>>>(w.tile_offset, w.keys, w.keys_tmp, w.pair_cap, w.counters);
+  tile_sort_kernel<<<ntiles, kSortThreads, kTileSortSmem, st>>>(w.tile_offset, w.keys, w.keys_tmp, w.pair_cap,
+                                                              w.counters);
   count_launch();
   if (!blend) return;
   render_blend(st, map, intr, w, color, depth, query, alpha, exact);
@@ -1202,7 +1395,7 @@ void render_blend(cudaStream_t st, const MapPtrs& map, const Intr& intr, RenderW
                   float* query, float* alpha, bool exact) {
   const int ntiles = w.tiles_x * w.tiles_y;
   RasterArgs a{w.rec, map.col, map.feat, map.ds, w.tile_offset, w.keys, w.tiles_x, intr.width, intr.height,
-               color, depth, query, alpha, w.px_last, w.px_T, w.tile_max_last, w.counters};
+               color, depth, query, alpha, w.px_last, w.px_T, w.tile_max_last, w.counters, w.tile_order};
   switch (pad_ds(map.ds)) {
     case 4: launch_fwd<4>(st, ntiles, a, exact); break;
     case 8: launch_fwd<8>(st, ntiles, a, exact); break;
@@ -1220,7 +1413,8 @@ void render_backward(cudaStream_t st, const MapPtrs& map, const float rot_cw[9],
                      bool project) {
   const int ntiles = w.tiles_x * w.tiles_y;
   RasterBwdArgs a{w.rec, map.col, map.feat, map.ds, w.tile_offset, w.keys, w.tiles_x, intr.width, intr.height,
-                  w.px_last, w.px_T, w.tile_max_last, d_color, d_depth, d_query, geo_acc, grads.col, grads.feat};
+                  w.px_last, w.px_T, w.tile_max_last, d_color, d_depth, d_query, geo_acc, grads.col, grads.feat,
+                  w.tile_order};
   switch (pad_ds(map.ds)) {
     case 4: launch_bwd<4>(st, ntiles, a); break;
     case 8: launch_bwd<8>(st, ntiles, a); break;
