@@ -849,6 +849,9 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_fwd_mma_kernel(RasterAr
 // ~fp32 accurate):  [dcolor, dz, dfeat] = W^T U  (U = per-pixel upstream [uc, uz, uq]),
 // and the drho moments  sum drho * [1, x, y, x^2, xy, y^2]  (+ sum dg), from which
 // dmean and dA (render.cpp:345-352) follow per splat in closed form.
+// Batches are staged with cp.async one batch ahead (record, colour, features of 16 splats,
+// issued by 16 lanes of warp 0), and a warp whose 16x2 pixel strip meets none of the batch's
+// bboxes, or whose pixels all stopped before the batch, skips the batch entirely.
 template <int DSP>
 __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArgs a) {
   constexpr int NU = ((4 + DSP) + 7) / 8 * 8;  // U columns: uc0..2, uz, uq[DSP], pad
@@ -860,6 +863,8 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
   constexpr int NACC = NU + 8 + 8;             // per-splat accumulators: W^T U | drho moments | dg
   constexpr int NUP = NU + 4;                  // splat-row pitch (B-fragment loads hit distinct banks)
   constexpr int PP = (NACC + 23) / 32 * 32 + 8;  // per-warp partial pitch (= 8 mod 32)
+  // raw staging row (floats): [SplatRec 12 | colour 3 | source bits | features DSP (padded to 4)]
+  constexpr int RP = 16 + (DSP + 3) / 4 * 4;
   static_assert(16 * PP <= 3 * kBwdBatch * WP, "warp partials must fit the warp's staging area");
   auto uidx = [](int p, int c) { return p * UP + (c ^ (((p >> 2) & 1) << 2)); };
   extern __shared__ __align__(16) float s_dyn[];
@@ -867,9 +872,10 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
   float* s_wbase = s_dyn + kTilePixels * UP;                   // [8 warps][3][16 * WP]: W, drho, dg
   __shared__ __align__(16) float s_fh[kBwdBatch * NUP];      // splat rows [c0 c1 c2 z f...], tf32 hi
   __shared__ __align__(16) float s_fl[kBwdBatch * NUP];      //   ... and tf32 lo
-  __shared__ SplatRec s_rec[kBwdBatch];
-  __shared__ uint32_t s_src[kBwdBatch];
+  __shared__ __align__(16) float s_raw[2][kBwdBatch * RP];   // cp.async staging, double-buffered
+  __shared__ __align__(16) float4 s_sp[kBwdBatch][3];        // {mx,my,q00,q01} {q11,alpha} {bbox}
   __shared__ float s_acc[kBwdBatch * NACC];
+  __shared__ int32_t s_wact[8];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tile = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
   const int tx0 = (tile % a.tiles_x) * kTile, ty0 = (tile / a.tiles_x) * kTile;
@@ -878,29 +884,54 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
   const int start = a.offset[tile];
   const int tend = start + a.tile_max_last[tile];
   if (tend <= start) return;
+  const bool vec_feat = (a.ds & 3) == 0;
+  // warp 0, lanes 0..15: stage splat `lane` of the batch [lo, lo + cnt) into raw buffer `buf`
+  auto stage = [&](int buf, int lo, int cnt, uint32_t src) {
+    float* row = s_raw[buf] + lane * RP;
+    if (lane < cnt) {
+      const float4* rg = reinterpret_cast<const float4*>(a.rec + src);
+      cp_async16(row, rg);
+      cp_async16(row + 4, rg + 1);
+      cp_async16(row + 8, rg + 2);
+      cp_async4(row + 12, a.colors + 3 * (size_t)src);
+      cp_async4(row + 13, a.colors + 3 * (size_t)src + 1);
+      cp_async4(row + 14, a.colors + 3 * (size_t)src + 2);
+      row[15] = __uint_as_float(src);
+      const float* f = a.feats + (size_t)src * a.ds;
+      if (vec_feat) {
+        for (int c = 0; c < a.ds; c += 4) cp_async16(row + 16 + c, f + c);
+      } else {
+        for (int c = 0; c < a.ds; ++c) cp_async4(row + 16 + c, f + c);
+      }
+      for (int c = a.ds; c < RP - 16; ++c) row[16 + c] = 0.f;
+    } else {
+      for (int c = 0; c < RP; ++c) row[c] = 0.f;
+      reinterpret_cast<int32_t*>(row)[8] = 1;  // empty bbox (x0 > x1)
+    }
+  };
   const size_t p = inside ? (size_t)py * a.width + px : 0;
   // per-pixel upstream row U[p] = [uc0, uc1, uc2, uz, uq...] (zero outside the image)
-  float uc0 = 0.f, uc1 = 0.f, uc2 = 0.f, uz = 0.f;
-  float uq[DSP];
-#pragma unroll
-  for (int c = 0; c < DSP; ++c) uq[c] = 0.f;
   int last = 0;
   float T = 1.f;
-  if (inside) {
-    if (a.d_color) {
-      uc0 = a.d_color[3 * p];
-      uc1 = a.d_color[3 * p + 1];
-      uc2 = a.d_color[3 * p + 2];
-    }
-    if (a.d_depth) uz = a.d_depth[p];
-    if (a.d_query) {
-#pragma unroll
-      for (int c = 0; c < DSP; ++c) uq[c] = c < a.ds ? a.d_query[p * a.ds + c] : 0.f;
-    }
-    last = a.px_last[p];
-    T = a.px_T[p];
-  }
   {
+    float uc0 = 0.f, uc1 = 0.f, uc2 = 0.f, uz = 0.f;
+    float uq[DSP];
+#pragma unroll
+    for (int c = 0; c < DSP; ++c) uq[c] = 0.f;
+    if (inside) {
+      if (a.d_color) {
+        uc0 = a.d_color[3 * p];
+        uc1 = a.d_color[3 * p + 1];
+        uc2 = a.d_color[3 * p + 2];
+      }
+      if (a.d_depth) uz = a.d_depth[p];
+      if (a.d_query) {
+#pragma unroll
+        for (int c = 0; c < DSP; ++c) uq[c] = c < a.ds ? a.d_query[p * a.ds + c] : 0.f;
+      }
+      last = a.px_last[p];
+      T = a.px_T[p];
+    }
     s_u[uidx(tid, 0)] = uc0;
     s_u[uidx(tid, 1)] = uc1;
     s_u[uidx(tid, 2)] = uc2;
@@ -910,6 +941,8 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
 #pragma unroll
     for (int c = 4 + DSP; c < NU; ++c) s_u[uidx(tid, c)] = 0.f;
   }
+  const int warp_last = __reduce_max_sync(0xffffffffu, last);
+  const int sy0 = ty0 + 2 * warp;  // this warp's pixel strip: rows sy0, sy0 + 1; columns tx0 .. tx0 + 15
   // MMA lane coordinates
   const int g = lane >> 2, cq = lane & 3;
   // B fragments of the pixel moment matrix X[p][q] = [1, x', y', x'^2, x'y', y'^2, 0, 0] for the
@@ -938,211 +971,250 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
   float* sw_w = s_wbase + (warp * 3 + 0) * kBwdBatch * WP;
   float* sw_r = s_wbase + (warp * 3 + 1) * kBwdBatch * WP;
   float* sw_g = s_wbase + (warp * 3 + 2) * kBwdBatch * WP;
-  for (int hi = tend; hi > start; hi -= kBwdBatch) {
+  constexpr float kNegHalfLog2e = -0.72134752044448170f;  // -0.5 * log2(e)
+  // prologue: stage batch 0, fetch the sources of batch 1
+  uint32_t nsrc = 0;
+  {
+    const int lo0 = max(start, tend - kBwdBatch);
+    if (warp == 0 && lane < kBwdBatch) {
+      const int cnt0 = tend - lo0;
+      stage(0, lo0, cnt0, lane < cnt0 ? (uint32_t)a.keys[lo0 + lane] : 0u);
+      cp_async_commit();
+      const int lo1 = max(start, lo0 - kBwdBatch);
+      if (lane < lo0 - lo1) nsrc = (uint32_t)a.keys[lo1 + lane];
+    }
+  }
+  int it = 0;
+  for (int hi = tend; hi > start; hi -= kBwdBatch, ++it) {
     const int lo = max(start, hi - kBwdBatch);
     const int cnt = hi - lo;
+    const int cur = it & 1;
+    const float* raw = s_raw[cur];
+    cp_async_wait_all();
     __syncthreads();
-    if (tid < kBwdBatch) {
-      if (tid < cnt) {
-        const uint32_t src = (uint32_t)a.keys[lo + tid];
-        s_src[tid] = src;
-        s_rec[tid] = a.rec[src];
-      } else {
-        s_src[tid] = 0xffffffffu;
-        s_rec[tid] = SplatRec{0, 0, 0, 1.f, 0, 0, 0, 0, 1, 0, 1, 0};
-      }
-    }
+    // ---- split the staged batch into tf32 hi/lo splat rows and the prescaled per-splat terms
     for (int e = tid; e < kBwdBatch * NU; e += blockDim.x) {
       const int j = e / NU, c = e % NU;
-      float v = 0.f;
-      if (j < cnt) {
-        const size_t src = (uint32_t)a.keys[lo + j];
-        if (c < 3)
-          v = a.colors[3 * src + c];
-        else if (c == 3)
-          v = a.rec[src].depth;
-        else if (c - 4 < a.ds)
-          v = a.feats[src * a.ds + (c - 4)];
+      const float* row = raw + j * RP;
+      const float v = c < 3 ? row[12 + c] : (c == 3 ? row[2] : (c - 4 < DSP ? row[16 + c - 4] : 0.f));
+      uint32_t h, l;
+      split_tf32(v, h, l);
+      s_fh[j * NUP + c] = __uint_as_float(h);
+      s_fl[j * NUP + c] = __uint_as_float(l);
+    }
+    if (tid < kBwdBatch) {
+      const float* row = raw + tid * RP;
+      s_sp[tid][0] = make_float4(row[0], row[1], kNegHalfLog2e * row[4], kNegHalfLog2e * (2.f * row[5]));
+      s_sp[tid][1] = make_float4(kNegHalfLog2e * row[7], row[3], 0.f, 0.f);
+      s_sp[tid][2] = *reinterpret_cast<const float4*>(row + 8);
+    }
+    // ---- prefetch the next batch into the other buffer (free: last read before the barrier)
+    if (warp == 0 && lane < kBwdBatch) {
+      const int nhi = lo, nlo = max(start, lo - kBwdBatch);
+      if (nhi > start) {
+        stage(cur ^ 1, nlo, nhi - nlo, nsrc);
+        cp_async_commit();
+        const int nnlo = max(start, nlo - kBwdBatch);
+        nsrc = lane < nlo - nnlo ? (uint32_t)a.keys[nnlo + lane] : 0u;
       }
-      uint32_t hi, lo;
-      split_tf32(v, hi, lo);
-      s_fh[j * NUP + c] = __uint_as_float(hi);
-      s_fl[j * NUP + c] = __uint_as_float(lo);
     }
     __syncthreads();
-    // ---- value[p][j] = U[p] . [c_j, z_j, f_j] for the warp's 32 pixels x 16 splats on the tensor
-    // cores (3xTF32), staged through sw_g as [splat][pixel] (each thread then reads its own
-    // pixel's column and overwrites that slot with dg)
-    {
-      float va[2][2][4];
+    // ---- warp activity: some pixel of the strip still blends at this batch and some bbox meets it
+    bool act = (lo - start) < warp_last;
+    if (act) {
+      bool meets = false;
+      if (lane < cnt) {
+        const int4 bb = f4_as_i4(s_sp[lane][2]);
+        meets = bb.x <= tx0 + kTile - 1 && bb.y >= tx0 && bb.z <= sy0 + 1 && bb.w >= sy0;
+      }
+      act = __any_sync(0xffffffffu, meets);
+    }
+    if (lane == 0) s_wact[warp] = act ? 1 : 0;
+    if (act) {
+      // ---- value[p][j] = U[p] . [c_j, z_j, f_j] for the warp's 32 pixels x 16 splats on the tensor
+      // cores (3xTF32), staged through sw_g as [splat][pixel] (each thread then reads its own
+      // pixel's column and overwrites that slot with dg)
+      {
+        float va[2][2][4];
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
+        for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) va[mt][nt][0] = va[mt][nt][1] = va[mt][nt][2] = va[mt][nt][3] = 0.f;
+          for (int nt = 0; nt < 2; ++nt) va[mt][nt][0] = va[mt][nt][1] = va[mt][nt][2] = va[mt][nt][3] = 0.f;
 #pragma unroll
-      for (int ks = 0; ks < NU / 8; ++ks) {
-        uint32_t uh[2][4], ul[2][4];
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          const int pr = 32 * warp + 16 * mt + g;
-          split_tf32(s_u[uidx(pr, 8 * ks + cq)], uh[mt][0], ul[mt][0]);
-          split_tf32(s_u[uidx(pr + 8, 8 * ks + cq)], uh[mt][1], ul[mt][1]);
-          split_tf32(s_u[uidx(pr, 8 * ks + cq + 4)], uh[mt][2], ul[mt][2]);
-          split_tf32(s_u[uidx(pr + 8, 8 * ks + cq + 4)], uh[mt][3], ul[mt][3]);
-        }
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          const int fo = (8 * nt + g) * NUP + 8 * ks + cq;
-          const uint32_t bh[2] = {__float_as_uint(s_fh[fo]), __float_as_uint(s_fh[fo + 4])};
-          const uint32_t bl[2] = {__float_as_uint(s_fl[fo]), __float_as_uint(s_fl[fo + 4])};
+        for (int ks = 0; ks < NU / 8; ++ks) {
+          uint32_t uh[2][4], ul[2][4];
 #pragma unroll
           for (int mt = 0; mt < 2; ++mt) {
-            mma_tf32(va[mt][nt], ul[mt], bh);
-            mma_tf32(va[mt][nt], uh[mt], bl);
-            mma_tf32(va[mt][nt], uh[mt], bh);
+            const int pr = 32 * warp + 16 * mt + g;
+            split_tf32(s_u[uidx(pr, 8 * ks + cq)], uh[mt][0], ul[mt][0]);
+            split_tf32(s_u[uidx(pr + 8, 8 * ks + cq)], uh[mt][1], ul[mt][1]);
+            split_tf32(s_u[uidx(pr, 8 * ks + cq + 4)], uh[mt][2], ul[mt][2]);
+            split_tf32(s_u[uidx(pr + 8, 8 * ks + cq + 4)], uh[mt][3], ul[mt][3]);
+          }
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            const int fo = (8 * nt + g) * NUP + 8 * ks + cq;
+            const uint32_t bh[2] = {__float_as_uint(s_fh[fo]), __float_as_uint(s_fh[fo + 4])};
+            const uint32_t bl[2] = {__float_as_uint(s_fl[fo]), __float_as_uint(s_fl[fo + 4])};
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+              mma_tf32(va[mt][nt], ul[mt], bh);
+              mma_tf32(va[mt][nt], uh[mt], bl);
+              mma_tf32(va[mt][nt], uh[mt], bh);
+            }
           }
         }
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            float* d = sw_g + (8 * nt + 2 * cq) * WP + 16 * mt + g;
+            d[0] = va[mt][nt][0];
+            d[WP] = va[mt][nt][1];
+            d[8] = va[mt][nt][2];
+            d[WP + 8] = va[mt][nt][3];
+          }
+        __syncwarp();
       }
+      // ---- per-pixel reverse sweep over the batch. alpha' of four splats is evaluated
+      // independently (ILP), then the transmittance recovery / d_alpha chain runs serially.
+      // The set of blended (pixel, splat) pairs comes from the forward (px_last), so alpha' only
+      // needs gradient accuracy here (SFU exp2 / reciprocal).
+      const int rel = lo - start;
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          float* d = sw_g + (8 * nt + 2 * cq) * WP + 16 * mt + g;
-          d[0] = va[mt][nt][0];
-          d[WP] = va[mt][nt][1];
-          d[8] = va[mt][nt][2];
-          d[WP + 8] = va[mt][nt][3];
-        }
-      __syncwarp();
-    }
-    // ---- per-pixel reverse sweep over the batch. alpha' of four splats is evaluated
-    // independently (ILP), then the transmittance recovery / d_alpha chain runs serially.
-    // The set of blended (pixel, splat) pairs comes from the forward (px_last), so alpha' only
-    // needs gradient accuracy here (fast exp / rcp).
-#pragma unroll
-    for (int j4 = kBwdBatch - 4; j4 >= 0; j4 -= 4) {
-      float alv[4], ex[4], rv[4];
-      bool ok[4], unc[4];
-      bool any = false;
-#pragma unroll
-      for (int u = 3; u >= 0; --u) {
-        const int j = j4 + u;
-        const SplatRec& s = s_rec[j];
-        ok[u] = j < cnt && inside && lo - start + j < last && px >= s.x0 && px <= s.x1 && py >= s.y0 && py <= s.y1;
-        any |= ok[u];
-      }
-      if (__any_sync(0xffffffffu, any)) {
+      for (int j4 = kBwdBatch - 4; j4 >= 0; j4 -= 4) {
+        float alv[4], ex[4], rv[4];
+        bool ok[4], unc[4];
+        bool any = false;
 #pragma unroll
         for (int u = 3; u >= 0; --u) {
-          const SplatRec& s = s_rec[j4 + u];
-          const float dx = fx - s.mean_x;
-          const float dy = fy - s.mean_y;
-          const float rho = fmaf(s.a00 * dx, dx, fmaf(2.f * s.a01 * dx, dy, s.a11 * dy * dy));
-          ex[u] = __expf(-0.5f * rho);
-          float al = s.alpha * ex[u];
-          unc[u] = !(al > kAlphaMax);
-          if (!unc[u]) al = kAlphaMax;
-          alv[u] = al;
-          rv[u] = __frcp_rn(1.f - al);
+          const int j = j4 + u;
+          const int4 bb = f4_as_i4(s_sp[j][2]);
+          ok[u] = j < cnt && rel + j < last && (unsigned)(px - bb.x) <= (unsigned)(bb.y - bb.x) &&
+                  (unsigned)(py - bb.z) <= (unsigned)(bb.w - bb.z);
+          any |= ok[u];
         }
-      }
+        if (__any_sync(0xffffffffu, any)) {
 #pragma unroll
-      for (int u = 3; u >= 0; --u) {
-        const int j = j4 + u;
-        float w = 0.f, drho = 0.f, dg = 0.f;
-        if (ok[u]) {
-          const float Tb = T * rv[u];
-          w = alv[u] * Tb;
-          const float value = sw_g[j * WP + lane];
-          const float d_alpha = Tb * value - s_after * rv[u];
-          s_after = fmaf(w, value, s_after);
-          if (unc[u]) {
-            dg = d_alpha * ex[u];
-            drho = -0.5f * alv[u] * d_alpha;
+          for (int u = 3; u >= 0; --u) {
+            const float4 s0 = s_sp[j4 + u][0];
+            const float4 s1 = s_sp[j4 + u][1];
+            const float dx = fx - s0.x;
+            const float dy = fy - s0.y;
+            const float pw = fmaf(dx, fmaf(s0.z, dx, s0.w * dy), s1.x * dy * dy);
+            ex[u] = ex2_approx(pw);
+            float al = s1.y * ex[u];
+            unc[u] = !(al > kAlphaMax);
+            if (!unc[u]) al = kAlphaMax;
+            alv[u] = al;
+            rv[u] = rcp_approx(1.f - al);
           }
-          T = Tb;
         }
-        sw_w[j * WP + lane] = w;
-        sw_r[j * WP + lane] = drho;
-        sw_g[j * WP + lane] = dg;
+#pragma unroll
+        for (int u = 3; u >= 0; --u) {
+          const int j = j4 + u;
+          float w = 0.f, drho = 0.f, dg = 0.f;
+          if (ok[u]) {
+            const float Tb = T * rv[u];
+            w = alv[u] * Tb;
+            const float value = sw_g[j * WP + lane];
+            const float d_alpha = Tb * value - s_after * rv[u];
+            s_after = fmaf(w, value, s_after);
+            if (unc[u]) {
+              dg = d_alpha * ex[u];
+              drho = -0.5f * alv[u] * d_alpha;
+            }
+            T = Tb;
+          }
+          sw_w[j * WP + lane] = w;
+          sw_r[j * WP + lane] = drho;
+          sw_g[j * WP + lane] = dg;
+        }
       }
-    }
-    __syncwarp();
-    // ---- tensor-core reductions over the warp's 32 pixels
-    float dwu[NT][4];
-    float dmo[2][4];
+      __syncwarp();
+      // ---- tensor-core reductions over the warp's 32 pixels
+      float dwu[NT][4];
+      float dmo[2][4];
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) dwu[nt][0] = dwu[nt][1] = dwu[nt][2] = dwu[nt][3] = 0.f;
-    dmo[0][0] = dmo[0][1] = dmo[0][2] = dmo[0][3] = dmo[1][0] = dmo[1][1] = dmo[1][2] = dmo[1][3] = 0.f;
+      for (int nt = 0; nt < NT; ++nt) dwu[nt][0] = dwu[nt][1] = dwu[nt][2] = dwu[nt][3] = 0.f;
+      dmo[0][0] = dmo[0][1] = dmo[0][2] = dmo[0][3] = dmo[1][0] = dmo[1][1] = dmo[1][2] = dmo[1][3] = 0.f;
 #pragma unroll
-    for (int ks = 0; ks < 4; ++ks) {
-      // A = W^T (rows: splats j, cols: pixels) ; split into tf32 hi/lo
-      uint32_t ah[4], al_[4];
-      split_tf32(sw_w[g * WP + 8 * ks + cq], ah[0], al_[0]);
-      split_tf32(sw_w[(g + 8) * WP + 8 * ks + cq], ah[1], al_[1]);
-      split_tf32(sw_w[g * WP + 8 * ks + cq + 4], ah[2], al_[2]);
-      split_tf32(sw_w[(g + 8) * WP + 8 * ks + cq + 4], ah[3], al_[3]);
-      const int prow = 32 * warp + 8 * ks + cq;  // pixel (k index) of b0; b1 is +4
+      for (int ks = 0; ks < 4; ++ks) {
+        // A = W^T (rows: splats j, cols: pixels) ; split into tf32 hi/lo
+        uint32_t ah[4], al_[4];
+        split_tf32(sw_w[g * WP + 8 * ks + cq], ah[0], al_[0]);
+        split_tf32(sw_w[(g + 8) * WP + 8 * ks + cq], ah[1], al_[1]);
+        split_tf32(sw_w[g * WP + 8 * ks + cq + 4], ah[2], al_[2]);
+        split_tf32(sw_w[(g + 8) * WP + 8 * ks + cq + 4], ah[3], al_[3]);
+        const int prow = 32 * warp + 8 * ks + cq;  // pixel (k index) of b0; b1 is +4
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          uint32_t bh[2], bl[2];
+          split_tf32(s_u[uidx(prow, 8 * nt + g)], bh[0], bl[0]);
+          split_tf32(s_u[uidx(prow + 4, 8 * nt + g)], bh[1], bl[1]);
+          mma_tf32(dwu[nt], ah, bh);
+          mma_tf32(dwu[nt], ah, bl);
+          mma_tf32(dwu[nt], al_, bh);
+        }
+        // A = [drho ; dg]^T (2 m-tiles), B = X (exact)
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const float* src = mt ? sw_g : sw_r;
+          uint32_t rh[4], rl[4];
+          split_tf32(src[g * WP + 8 * ks + cq], rh[0], rl[0]);
+          split_tf32(src[(g + 8) * WP + 8 * ks + cq], rh[1], rl[1]);
+          split_tf32(src[g * WP + 8 * ks + cq + 4], rh[2], rl[2]);
+          split_tf32(src[(g + 8) * WP + 8 * ks + cq + 4], rh[3], rl[3]);
+          mma_tf32(dmo[mt], rh, xb[ks]);
+          mma_tf32(dmo[mt], rl, xb[ks]);
+        }
+      }
+      // ---- warp partials (rows = splats) into the warp's own staging area
+      __syncwarp();
+      float* part = sw_w;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        uint32_t bh[2], bl[2];
-        split_tf32(s_u[uidx(prow, 8 * nt + g)], bh[0], bl[0]);
-        split_tf32(s_u[uidx(prow + 4, 8 * nt + g)], bh[1], bl[1]);
-        mma_tf32(dwu[nt], ah, bh);
-        mma_tf32(dwu[nt], ah, bl);
-        mma_tf32(dwu[nt], al_, bh);
+        *reinterpret_cast<float2*>(part + g * PP + 8 * nt + 2 * cq) = make_float2(dwu[nt][0], dwu[nt][1]);
+        *reinterpret_cast<float2*>(part + (g + 8) * PP + 8 * nt + 2 * cq) = make_float2(dwu[nt][2], dwu[nt][3]);
       }
-      // A = [drho ; dg]^T (2 m-tiles), B = X (exact)
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
-        const float* src = mt ? sw_g : sw_r;
-        uint32_t rh[4], rl[4];
-        split_tf32(src[g * WP + 8 * ks + cq], rh[0], rl[0]);
-        split_tf32(src[(g + 8) * WP + 8 * ks + cq], rh[1], rl[1]);
-        split_tf32(src[g * WP + 8 * ks + cq + 4], rh[2], rl[2]);
-        split_tf32(src[(g + 8) * WP + 8 * ks + cq + 4], rh[3], rl[3]);
-        mma_tf32(dmo[mt], rh, xb[ks]);
-        mma_tf32(dmo[mt], rl, xb[ks]);
+        const int base = NU + 8 * mt;
+        *reinterpret_cast<float2*>(part + g * PP + base + 2 * cq) = make_float2(dmo[mt][0], dmo[mt][1]);
+        *reinterpret_cast<float2*>(part + (g + 8) * PP + base + 2 * cq) = make_float2(dmo[mt][2], dmo[mt][3]);
       }
     }
-    // ---- warp partials (rows = splats) into the warp's own staging area, then a cross-warp sum
-    __syncwarp();
-    float* part = sw_w;
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      *reinterpret_cast<float2*>(part + g * PP + 8 * nt + 2 * cq) = make_float2(dwu[nt][0], dwu[nt][1]);
-      *reinterpret_cast<float2*>(part + (g + 8) * PP + 8 * nt + 2 * cq) = make_float2(dwu[nt][2], dwu[nt][3]);
-    }
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt) {
-      const int base = NU + 8 * mt;
-      *reinterpret_cast<float2*>(part + g * PP + base + 2 * cq) = make_float2(dmo[mt][0], dmo[mt][1]);
-      *reinterpret_cast<float2*>(part + (g + 8) * PP + base + 2 * cq) = make_float2(dmo[mt][2], dmo[mt][3]);
-    }
     __syncthreads();
-    for (int e = tid; e < kBwdBatch * NACC; e += blockDim.x) {
-      const int j = e / NACC, c = e % NACC;
-      float v = 0.f;
+    // ---- cross-warp sum over the active warps
+    {
+      int wm = 0;
 #pragma unroll
-      for (int w8 = 0; w8 < 8; ++w8) v += s_wbase[w8 * 3 * kBwdBatch * WP + j * PP + c];
-      s_acc[e] = v;
+      for (int w8 = 0; w8 < 8; ++w8) wm |= s_wact[w8] << w8;
+      for (int e = tid; e < kBwdBatch * NACC; e += blockDim.x) {
+        const int j = e / NACC, c = e % NACC;
+        float v = 0.f;
+#pragma unroll
+        for (int w8 = 0; w8 < 8; ++w8)
+          if (wm & (1 << w8)) v += s_wbase[w8 * 3 * kBwdBatch * WP + j * PP + c];
+        s_acc[e] = v;
+      }
     }
     __syncthreads();
     // ---- per-splat closed forms + global accumulation
     for (int e = tid; e < cnt * 16; e += blockDim.x) {
       const int j = e >> 4, k = e & 15;
       const float* ac = s_acc + j * NACC;
-      const size_t src = s_src[j];
+      const float* row = raw + j * RP;
+      const size_t src = __float_as_uint(row[15]);
       if (k < 7) {
         // moments M0..M5 (k-th column of the drho rows) -> dmean, dA, dz, dg
-        const SplatRec& s = s_rec[j];
-        const float up = s.mean_x - ((float)tx0 + 7.5f), vp = s.mean_y - ((float)ty0 + 7.5f);
+        const float up = row[0] - ((float)tx0 + 7.5f), vp = row[1] - ((float)ty0 + 7.5f);
         const float* M = ac + NU;
         const float sdx = M[1] - up * M[0], sdy = M[2] - vp * M[0];
         float val = 0.f;
         switch (k) {
-          case 0: val = -2.f * (s.a00 * sdx + s.a01 * sdy); break;
-          case 1: val = -2.f * (s.a10 * sdx + s.a11 * sdy); break;
+          case 0: val = -2.f * (row[4] * sdx + row[5] * sdy); break;
+          case 1: val = -2.f * (row[6] * sdx + row[7] * sdy); break;
           case 2: val = M[3] - 2.f * up * M[1] + up * up * M[0]; break;
           case 3: val = M[4] - vp * M[1] - up * M[2] + up * vp * M[0]; break;
           case 4: val = M[5] - 2.f * vp * M[2] + vp * vp * M[0]; break;
@@ -1158,7 +1230,7 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
     for (int e = tid; e < cnt * a.ds; e += blockDim.x) {
       const int j = e / a.ds, c = e % a.ds;
       const float val = s_acc[j * NACC + 4 + c];
-      if (val != 0.f) atomicAdd(&a.g_feat[(size_t)s_src[j] * a.ds + c], val);
+      if (val != 0.f) atomicAdd(&a.g_feat[(size_t)__float_as_uint(raw[j * RP + 15]) * a.ds + c], val);
     }
   }
 }
