@@ -765,6 +765,7 @@ latmap_status session_objective(latmap_session* s, bool want_grad) {
       s->end();
     }
   }
+  if (want_grad) decoder_finish_tc(st, s->dec, atoms, proj, g_proj, g_atoms);
   // trust term enters once (objective.cpp:247-256)
   if (s->add_trust) {
     double* tslot = s->partials + (size_t)s->part_frames * kPart;
@@ -878,7 +879,8 @@ latmap_status latmap_session_create(latmap_ctx* ctx, const latmap_config* cfg, i
            ok(cudaMalloc(&d.a_part, sizeof(float) * 74 * 2 * k * (k / 2 + 1))) &&
            ok(cudaMalloc(&d.bm_part, sizeof(float) * 74 * k * 64)) &&
            ok(cudaMalloc(&d.loss_part, sizeof(double) * 148 * 4)) &&
-           ok(cudaMalloc(&d.e_tiles, (size_t)((npx + 127) / 128) * 128 * k * 2));
+           ok(cudaMalloc(&d.e_tiles, (size_t)((npx + 127) / 128) * 128 * k * 2)) &&
+           ok(cudaMalloc(&d.a_acc, sizeof(float) * k * k)) && ok(cudaMalloc(&d.r_acc, sizeof(float) * ds * k));
   }
   if (!good) {
     t_err = "latmap_session_create: out of device memory";
@@ -910,7 +912,7 @@ latmap_status latmap_session_destroy(latmap_session* s) {
                   (void*)s->dec.kd, (void*)s->dec.mm, (void*)s->dec.gt, (void*)s->dec.nv, (void*)s->dec.r,
                   (void*)s->dec.a, (void*)s->dec.bm, (void*)s->dec.row_stats, (void*)s->dec.r_part,
                   (void*)s->dec.a_part, (void*)s->dec.bm_part, (void*)s->dec.loss_part,
-                  (void*)s->dec.e_tiles})
+                  (void*)s->dec.e_tiles, (void*)s->dec.a_acc, (void*)s->dec.r_acc})
     if (p) cudaFree(p);
   for (auto& r : s->rw) r.release();
   for (auto* p : s->color) cudaFree(p);

@@ -11,13 +11,14 @@
 //   dQ = dS Kd,  R^T = dS^T Q,  A = P^T diag(alpha) P,  Bm = P^T Ohb (Ohb[r][s] = beta_r [a_r == s])
 //   d_atoms += A D + Bm E + R^T W,   d_proj += R D.
 //
-// DEC1 (persistent, 1 CTA / SM, 256 threads): per 128-pixel tile
-//   MMA1 S -> TMEM[0,K); softmax epilogue writes bf16 e = exp(S - max) to smem;
-//   MMA2 t = e M -> TMEM[K,2K); loss / alpha / beta epilogue; dS (bf16) overwrites e;
-//   MMA3 dQ = dS Kd -> TMEM[0,DS); MMA4 R^T = dS^T Q -> TMEM[DS, DS + DS*K/128);
-//   dQ rows go to HBM, R^T is accumulated in registers across tiles.
-// DEC2 (persistent, 128 threads, two roles = two column halves of A): recomputes P in
-//   128-column chunks from the stored row max / 1/sum and accumulates A[:, half] and Bm in TMEM.
+// DEC1 (persistent, 1 CTA / SM, 512 threads): per 128-pixel tile
+//   MMA1 S -> TMEM[0,K); softmax epilogue writes bf16 e = exp(S - max) to smem (and streams it
+//   to HBM for DEC2); MMA2 t = e M -> TMEM[0,K); loss / alpha / beta epilogue; dS (bf16)
+//   overwrites e; MMA3 dQ = dS Kd -> TMEM[K,K+DS); MMA4 R^T += dS^T Q -> TMEM[K+DS, ...)
+//   (accumulated across the CTA's tiles); dQ rows go to HBM.
+// DEC2 (persistent, warp-specialised, two roles = two column halves of A): streams DEC1's e
+//   tiles back with TMA, scales them by the row statistics and accumulates A[:, half] and Bm
+//   in TMEM.
 // Shared-memory operand tiles use the no-swizzle core-matrix layout of tc_common.cuh with
 // row-group stride 128 B and column-group stride 16 * rows B, so one tile serves as a K-major
 // operand (rows = M|N) and, transposed, as an MN-major operand (rows = K).
@@ -392,29 +393,38 @@ struct Dec2Args {
 };
 
 // DEC2: A[:, role half] = e^T diag(alpha / sum^2) e and (role 0) Bm = e^T Ohb with
-// Ohb[r][s] = beta_r / sum_r [a_r == s], streaming the e tiles DEC1 exported (TMA bulk loads,
-// double-buffered) -- no recomputation of S or exp.
+// Ohb[r][s] = beta_r / sum_r [a_r == s], streaming the e tiles DEC1 exported -- no
+// recomputation of S or exp. Warp-specialised: warp 8 (one elected lane) issues the TMA bulk
+// loads of the e tiles and the MMAs; warps 0-7 build the scaled B operands. The e tiles and the
+// B operands are double-buffered, so the build of tile i overlaps the MMAs of tile i-1, and the
+// load of tile i+1 overlaps both.
+//   bar_ld[b]    : e tile landed in sE[b]            (TMA complete_tx)
+//   bar_built[b] : 8 builder warps filled sAP/sOh[b]  (8 arrivals)
+//   bar_mma[b]   : MMAs reading sE/sAP/sOh[b] done    (tcgen05.commit)
+// A load into sE[b] is issued only after the MMAs of the tile that last used b completed, so a
+// builder that sees bar_ld[b] may also overwrite sAP/sOh[b].
 template <int K>
-__global__ void __launch_bounds__(256, 1) dec2_kernel(Dec2Args a) {
+__global__ void __launch_bounds__(288, 1) dec2_kernel(Dec2Args a) {
   constexpr int MH = K / 128, NH = K / 2, NB = 64;
   constexpr int kColA = 0, kColB = MH * NH;
   constexpr int kTmemCols = kColB + MH * NB <= 256 ? 256 : 512;
   constexpr uint32_t kCS = 16u * kRows;
   constexpr uint32_t kTileBytes = kRows * K * 2;
+  constexpr uint32_t kAPBytes = kRows * NH * 2, kOhBytes = kRows * NB * 2;
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sE[2] = {smem, smem + kTileBytes};      // 2 x (128 x K)
-  uint8_t* sAP = smem + 2 * kTileBytes;            // 128 x NH
-  uint8_t* sOh = sAP + kRows * NH * 2;             // 128 x NB
-  __shared__ uint64_t bar_ld[2], bar_mma;
+  uint8_t* sE0 = smem;                       // 2 x (128 x K)
+  uint8_t* sAP0 = smem + 2 * kTileBytes;     // 2 x (128 x NH)
+  uint8_t* sOh0 = sAP0 + 2 * kAPBytes;       // 2 x (128 x NB)
+  __shared__ uint64_t bar_ld[2], bar_built[2], bar_mma[2];
   __shared__ uint32_t s_taddr;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = warp & 3, h = warp >> 2;  // TMEM lane group, column half (of the role's NH)
-  const int row = 32 * g + lane;
   const int role = blockIdx.x & 1, group = blockIdx.x >> 1, ngroups = gridDim.x >> 1;
   if (tid == 0) {
-    tc::mbar_init(&bar_ld[0], 1);
-    tc::mbar_init(&bar_ld[1], 1);
-    tc::mbar_init(&bar_mma, 1);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&bar_ld[i], 1);
+      tc::mbar_init(&bar_built[i], 8);
+      tc::mbar_init(&bar_mma[i], 1);
+    }
     tc::fence_mbar_init();
   }
   if (warp == 0) tc::tmem_alloc<kTmemCols>(&s_taddr);
@@ -422,106 +432,119 @@ __global__ void __launch_bounds__(256, 1) dec2_kernel(Dec2Args a) {
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = s_taddr;
-  const uint32_t tl = tmem + ((uint32_t)(32 * g) << 16);
-  uint32_t ph_ld[2] = {0, 0}, ph_mma = 0;
-  const uint32_t aAP = tc::smem_u32(sAP), aOh = tc::smem_u32(sOh);
   const int64_t ntiles = (a.npx + kRows - 1) / kRows;
-  int it = 0;
-  if (tid == 0 && group < ntiles) {
-    tc::mbar_expect_tx(&bar_ld[0], kTileBytes);
-    tc::bulk_g2s(sE[0], a.e_tiles + (size_t)group * kTileBytes, kTileBytes, &bar_ld[0]);
-  }
-  for (int64_t tile = group; tile < ntiles; tile += ngroups, ++it) {
-    const int buf = it & 1;
-    const int64_t r0 = tile * kRows;
-    const int valid = (int)(a.npx - r0 < kRows ? a.npx - r0 : kRows);
-    float4 st = make_float4(0.f, 0.f, 0.f, 0.f);
-    int32_t asg = -1;
-    if (row < valid) {
-      st = a.row_stats[r0 + row];
-      asg = a.assign[r0 + row];
-    }
-    const float wa = st.z * st.y * st.y;  // alpha / sum^2
-    const float wb = st.w * st.y;         // beta / sum
-    // previous MMA done -> its operands (sAP, sOh, sE[buf^1]) are free
-    if (it > 0) {
-      tc::mbar_wait(&bar_mma, ph_mma);
-      ph_mma ^= 1;
-    }
-    if (tid == 0 && tile + ngroups < ntiles) {
-      tc::mbar_expect_tx(&bar_ld[buf ^ 1], kTileBytes);
-      tc::bulk_g2s(sE[buf ^ 1], a.e_tiles + (size_t)(tile + ngroups) * kTileBytes, kTileBytes, &bar_ld[buf ^ 1]);
-    }
-    tc::mbar_wait(&bar_ld[buf], ph_ld[buf]);
-    ph_ld[buf] ^= 1;
-    // B operands: (alpha / sum^2) e[:, role half] and the beta / sum one-hot
-    const uint8_t* E = sE[buf];
-#pragma unroll
-    for (int c = h * (NH / 2); c < (h + 1) * (NH / 2); c += 8) {
-      float v[8];
-      ld_row8(E, row, role * NH + c, kCS, v);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = row < valid ? v[j] * wa : 0.f;
-      st_row8(sAP, row, c, kCS, v);
-    }
-    if (role == 0) {
-#pragma unroll
-      for (int c = h * (NB / 2); c < (h + 1) * (NB / 2); c += 8) {
-        float v[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = (asg == c + j) ? wb : 0.f;
-        st_row8(sOh, row, c, kCS, v);
+  const int nmine = group < ntiles ? (int)((ntiles - 1 - group) / ngroups + 1) : 0;
+  if (warp == 8) {
+    // ---------------- producer: TMA loads + MMA issue (one lane)
+    if (lane == 0 && nmine > 0) {
+      const uint32_t aAP0 = tc::smem_u32(sAP0), aOh0 = tc::smem_u32(sOh0), aE0 = tc::smem_u32(sE0);
+      for (int i = 0; i < 2 && i < nmine; ++i) {
+        tc::mbar_expect_tx(&bar_ld[i], kTileBytes);
+        tc::bulk_g2s(sE0 + i * kTileBytes, a.e_tiles + (size_t)(group + (int64_t)i * ngroups) * kTileBytes,
+                     kTileBytes, &bar_ld[i]);
       }
-    }
-    tc::fence_async_smem();
-    tc::tc_fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      tc::tc_fence_after();
-      const uint32_t aE = tc::smem_u32(E);
-      for (int mh = 0; mh < MH; ++mh) {
-#pragma unroll
-        for (int ks = 0; ks < kRows / 16; ++ks)
-          tc::mma_bf16(tmem + kColA + mh * NH, tc::make_sdesc(aE + mh * 16 * 2048 + ks * 2 * 128, 128, 2048),
-                       tc::make_sdesc(aAP + ks * 2 * 128, 128, 2048), tc::make_idesc_bf16(128, NH, 1, 1),
-                       it > 0 || ks > 0);
-        if (role == 0) {
+      for (int it = 0; it < nmine; ++it) {
+        const int buf = it & 1;
+        tc::mbar_wait(&bar_built[buf], (it >> 1) & 1);
+        tc::tc_fence_after();
+        const uint32_t aE = aE0 + buf * kTileBytes, aAP = aAP0 + buf * kAPBytes, aOh = aOh0 + buf * kOhBytes;
+        for (int mh = 0; mh < MH; ++mh) {
 #pragma unroll
           for (int ks = 0; ks < kRows / 16; ++ks)
-            tc::mma_bf16(tmem + kColB + mh * NB, tc::make_sdesc(aE + mh * 16 * 2048 + ks * 2 * 128, 128, 2048),
-                         tc::make_sdesc(aOh + ks * 2 * 128, 128, 2048), tc::make_idesc_bf16(128, NB, 1, 1),
+            tc::mma_bf16(tmem + kColA + mh * NH, tc::make_sdesc(aE + mh * 16 * 2048 + ks * 2 * 128, 128, 2048),
+                         tc::make_sdesc(aAP + ks * 2 * 128, 128, 2048), tc::make_idesc_bf16(128, NH, 1, 1),
                          it > 0 || ks > 0);
+          if (role == 0) {
+#pragma unroll
+            for (int ks = 0; ks < kRows / 16; ++ks)
+              tc::mma_bf16(tmem + kColB + mh * NB, tc::make_sdesc(aE + mh * 16 * 2048 + ks * 2 * 128, 128, 2048),
+                           tc::make_sdesc(aOh + ks * 2 * 128, 128, 2048), tc::make_idesc_bf16(128, NB, 1, 1),
+                           it > 0 || ks > 0);
+          }
+        }
+        tc::mma_commit(&bar_mma[buf]);
+        // refill the other buffer with tile it+1 once the MMAs of tile it-1 (its last user) are done
+        if (it >= 1 && it + 1 < nmine) {
+          tc::mbar_wait(&bar_mma[buf ^ 1], ((it - 1) >> 1) & 1);
+          tc::mbar_expect_tx(&bar_ld[buf ^ 1], kTileBytes);
+          tc::bulk_g2s(sE0 + (buf ^ 1) * kTileBytes,
+                       a.e_tiles + (size_t)(group + (int64_t)(it + 1) * ngroups) * kTileBytes, kTileBytes,
+                       &bar_ld[buf ^ 1]);
         }
       }
-      tc::mma_commit(&bar_mma);
     }
-  }
-  if (it > 0) {
-    tc::mbar_wait(&bar_mma, ph_mma);
-    tc::tc_fence_after();
-  }
-  // drain: lane `row` of half mh holds A[mh*128 + row][role*NH + c], Bm[mh*128 + row][c]
-  for (int mh = 0; mh < MH; ++mh) {
-    float* dst = a.a_part + (((size_t)group * 2 + role) * K + mh * 128 + row) * NH;
-    for (int c = h * (NH / 2); c < (h + 1) * (NH / 2); c += 16) {
-      float v[16];
-      if (it == 0) {
-        for (int i = 0; i < 16; ++i) v[i] = 0.f;
-      } else {
-        tc::tmem_ld16(tl + kColA + mh * NH + c, v);
+  } else {
+    // ---------------- builders: B operands (alpha / sum^2) e[:, role half] and the beta / sum one-hot
+    const int g = warp & 3, h = warp >> 2;  // TMEM lane group, column half (of the role's NH)
+    const int row = 32 * g + lane;
+    for (int it = 0; it < nmine; ++it) {
+      const int buf = it & 1;
+      const int64_t tile = group + (int64_t)it * ngroups;
+      const int64_t r0 = tile * kRows;
+      const int valid = (int)(a.npx - r0 < kRows ? a.npx - r0 : kRows);
+      float4 st = make_float4(0.f, 0.f, 0.f, 0.f);
+      int32_t asg = -1;
+      if (row < valid) {
+        st = a.row_stats[r0 + row];
+        asg = a.assign[r0 + row];
       }
-      for (int i = 0; i < 16; ++i) dst[c + i] = v[i];
+      const float wa = st.z * st.y * st.y;  // alpha / sum^2
+      const float wb = st.w * st.y;         // beta / sum
+      tc::mbar_wait(&bar_ld[buf], (it >> 1) & 1);
+      const uint8_t* E = sE0 + buf * kTileBytes;
+      uint8_t* AP = sAP0 + buf * kAPBytes;
+#pragma unroll
+      for (int c = h * (NH / 2); c < (h + 1) * (NH / 2); c += 8) {
+        float v[8];
+        ld_row8(E, row, role * NH + c, kCS, v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = row < valid ? v[j] * wa : 0.f;
+        st_row8(AP, row, c, kCS, v);
+      }
+      if (role == 0) {
+        uint8_t* Oh = sOh0 + buf * kOhBytes;
+#pragma unroll
+        for (int c = h * (NB / 2); c < (h + 1) * (NB / 2); c += 8) {
+          float v[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = (asg == c + j) ? wb : 0.f;
+          st_row8(Oh, row, c, kCS, v);
+        }
+      }
+      tc::fence_async_smem();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&bar_built[buf]);
     }
-    if (role == 0) {
-      float* db = a.bm_part + ((size_t)group * K + mh * 128 + row) * NB;
-      for (int c = h * (NB / 2); c < (h + 1) * (NB / 2); c += 16) {
+    // all MMAs complete once the last tile's commit arrives
+    if (nmine > 0) {
+      tc::mbar_wait(&bar_mma[(nmine - 1) & 1], ((nmine - 1) >> 1) & 1);
+      tc::tc_fence_after();
+    }
+    // drain: lane `row` of half mh holds A[mh*128 + row][role*NH + c], Bm[mh*128 + row][c]
+    for (int mh = 0; mh < MH; ++mh) {
+      float* dst = a.a_part + (((size_t)group * 2 + role) * K + mh * 128 + row) * NH;
+      for (int c = h * (NH / 2); c < (h + 1) * (NH / 2); c += 16) {
         float v[16];
-        if (it == 0) {
+        if (nmine == 0) {
           for (int i = 0; i < 16; ++i) v[i] = 0.f;
         } else {
-          tc::tmem_ld16(tl + kColB + mh * NB + c, v);
+          tc::tmem_ld16(tmem + ((uint32_t)(32 * g) << 16) + kColA + mh * NH + c, v);
         }
-        for (int i = 0; i < 16; ++i) db[c + i] = v[i];
+        for (int i = 0; i < 16; i += 4)
+          *reinterpret_cast<float4*>(dst + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      }
+      if (role == 0) {
+        float* db = a.bm_part + ((size_t)group * K + mh * 128 + row) * NB;
+        for (int c = h * (NB / 2); c < (h + 1) * (NB / 2); c += 16) {
+          float v[16];
+          if (nmine == 0) {
+            for (int i = 0; i < 16; ++i) v[i] = 0.f;
+          } else {
+            tc::tmem_ld16(tmem + ((uint32_t)(32 * g) << 16) + kColB + mh * NB + c, v);
+          }
+          for (int i = 0; i < 16; i += 4)
+            *reinterpret_cast<float4*>(db + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        }
       }
     }
   }
@@ -530,8 +553,22 @@ __global__ void __launch_bounds__(256, 1) dec2_kernel(Dec2Args a) {
   if (warp == 0) tc::tmem_free<kTmemCols>(tmem);
 }
 
-// Sum the per-CTA partials: A (K x K) from (groups x 2 roles x K x K/2), Bm^T (n_set x K) from
-// (groups x K x 64), R^T (K x DS) -> R (DS x K), loss partials -> frame partial slots.
+// Sum the per-CTA partials: A (K x K) from (groups x 2 roles x K x K/2) and R^T (K x DS) -> R
+// (DS x K) are ADDED to the step accumulators (decoder_finish_tc applies them once per step),
+// Bm^T (n_set x K) from (groups x K x 64) is written for this frame, loss partials -> the frame's
+// partial slots. Partial sums run over 8 independent accumulators so the loads overlap.
+template <class F>
+__device__ __forceinline__ float sum_strided(int n, F at) {
+  float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  int gi = 0;
+  for (; gi + 8 <= n; gi += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s[u] += at(gi + u);
+  }
+  for (; gi < n; ++gi) s[0] += at(gi);
+  return ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+}
+
 __global__ void dec_reduce_kernel(const float* a_part, const float* bm_part, const float* r_part,
                                   const double* loss_part, int K, int DS, int n_set, int groups1, int groups2,
                                   float* A, float* bmt, float* R, double* partials) {
@@ -542,21 +579,18 @@ __global__ void dec_reduce_kernel(const float* a_part, const float* bm_part, con
     if (e < total_a) {
       const int i = (int)(e / K), j = (int)(e % K);
       const int role = j / NH, jj = j % NH;
-      float s = 0.f;
-      for (int gi = 0; gi < groups2; ++gi) s += a_part[(((size_t)gi * 2 + role) * K + i) * NH + jj];
-      A[e] = s;
-    } else if (e < total_a + total_b) {
+      const size_t stride = (size_t)2 * K * NH, off = ((size_t)role * K + i) * NH + jj;
+      A[e] += sum_strided(groups2, [&](int gi) { return a_part[gi * stride + off]; });
+    } else if (e < total_a + total_b) {  // thread order follows the partials' layout (coalesced reads)
       const int64_t f = e - total_a;
-      const int sidx = (int)(f / K), k = (int)(f % K);
-      float s = 0.f;
-      for (int gi = 0; gi < groups2; ++gi) s += bm_part[((size_t)gi * K + k) * 64 + sidx];
-      bmt[f] = s;
+      const int k = (int)(f / n_set), sidx = (int)(f % n_set);
+      const size_t stride = (size_t)K * 64, off = (size_t)k * 64 + sidx;
+      bmt[(size_t)sidx * K + k] = sum_strided(groups2, [&](int gi) { return bm_part[gi * stride + off]; });
     } else if (e < total_a + total_b + total_r) {
       const int64_t f = e - total_a - total_b;
-      const int s_ = (int)(f / K), k = (int)(f % K);
-      float s = 0.f;
-      for (int gi = 0; gi < groups1; ++gi) s += r_part[((size_t)gi * K + k) * DS + s_];
-      R[f] = s;
+      const int k = (int)(f / DS), s_ = (int)(f % DS);
+      const size_t stride = (size_t)K * DS, off = (size_t)k * DS + s_;
+      R[(size_t)s_ * K + k] += sum_strided(groups1, [&](int gi) { return r_part[gi * stride + off]; });
     } else {
       const int which = (int)(e - total_a - total_b - total_r);
       double s = 0.0;
@@ -594,17 +628,17 @@ void launch_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_
     return;
   }
   Dec2Args d2{w.e_tiles, assignment, reinterpret_cast<const float4*>(w.row_stats), npx, w.a_part, w.bm_part};
-  const size_t sm2 = 2 * (size_t)kRows * K * 2 + (size_t)kRows * (K / 2) * 2 + (size_t)kRows * 64 * 2;
+  const size_t sm2 = 2 * ((size_t)kRows * K * 2 + (size_t)kRows * (K / 2) * 2 + (size_t)kRows * 64 * 2);
   static bool attr2 = false;
   if (!attr2) {
     cudaFuncSetAttribute(dec2_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
     attr2 = true;
   }
-  dec2_kernel<K><<<g2, 256, sm2, st>>>(d2);
+  dec2_kernel<K><<<g2, 288, sm2, st>>>(d2);
   count_launch();
   const int64_t tot = (int64_t)K * K + n_set * K + (int64_t)K * DS + 3;
   dec_reduce_kernel<<<(unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 8), 256, 0, st>>>(
-      w.a_part, w.bm_part, w.r_part, w.loss_part, K, DS, (int)n_set, g1, g2 / 2, w.a, w.bm, w.r, partials);
+      w.a_part, w.bm_part, w.r_part, w.loss_part, K, DS, (int)n_set, g1, g2 / 2, w.a_acc, w.bm, w.r_acc, partials);
   count_launch();
 }
 
@@ -635,11 +669,24 @@ void decoder_frame_tc(cudaStream_t st, DecoderWork& w, const float* query, const
     launch_tc<128, 32>(st, w, query, assignment, npx, feats, n_set, n_sup, temperature, lambda_cos, lambda_l2, scale,
                        want_grad, d_query, partials);
   if (!want_grad) return;
-  // d_atoms += A D + Bm E + R^T W ;  d_proj += R D   (R stored ds x K)
-  sgemm(st, false, false, k, df, k, 1.f, w.a, k, atoms, df, 1.f, d_atoms, df);
+  // d_atoms += Bm E for this frame's embedding table; A and R accumulate over the step's frames
+  // and enter once in decoder_finish_tc (they multiply the same D, W in every frame)
   sgemm(st, true, false, k, df, n_set, 1.f, w.bm, k, feats, df, 1.f, d_atoms, df);
-  sgemm(st, true, false, k, df, ds, 1.f, w.r, k, proj, df, 1.f, d_atoms, df);
-  sgemm(st, false, false, ds, df, k, 1.f, w.r, k, atoms, df, 1.f, d_proj, df);
+  w.tc_pending = true;
+  (void)d_proj;
+  (void)proj;
+}
+
+void decoder_finish_tc(cudaStream_t st, DecoderWork& w, const float* atoms, const float* proj, float* d_proj,
+                       float* d_atoms) {
+  if (!w.tc_pending) return;
+  const int64_t k = w.k;
+  const int ds = w.ds, df = w.df;
+  // d_atoms += A D + R^T W ;  d_proj += R D   (R stored ds x K)
+  sgemm(st, false, false, k, df, k, 1.f, w.a_acc, k, atoms, df, 1.f, d_atoms, df);
+  sgemm(st, true, false, k, df, ds, 1.f, w.r_acc, k, proj, df, 1.f, d_atoms, df);
+  sgemm(st, false, false, ds, df, k, 1.f, w.r_acc, k, atoms, df, 1.f, d_proj, df);
+  w.tc_pending = false;
 }
 
 }  // namespace lm

@@ -94,6 +94,9 @@ struct DecoderWork {
   float* bm_part = nullptr;    // 74 x K x 64
   double* loss_part = nullptr; // 148 x 4
   uint8_t* e_tiles = nullptr;  // ceil(npx/128) x 128 x K bf16 (DEC1 -> DEC2)
+  float* a_acc = nullptr;      // K x K: sum over the step's frames of P^T diag(alpha) P
+  float* r_acc = nullptr;      // ds x K: sum over the step's frames of Q^T dS
+  bool tc_pending = false;     // a_acc / r_acc hold contributions not yet applied
 };
 void decoder_prepare(cudaStream_t st, DecoderWork& w, const float* atoms, const float* proj);
 // Fused feature loss + decoder backward for one frame (pixel mode). Accumulates into d_proj,
@@ -109,6 +112,9 @@ void decoder_frame_tc(cudaStream_t st, DecoderWork& w, const float* query, const
                       int64_t npx, const float* feats, int64_t n_set, int64_t n_sup, const float* atoms,
                       const float* proj, float temperature, float lambda_cos, float lambda_l2, float scale,
                       bool want_grad, float* d_query, float* d_proj, float* d_atoms, double* partials);
+// Applies the step-accumulated A and R of the tcgen05 frames: d_atoms += A D + R^T W, d_proj += R D.
+void decoder_finish_tc(cudaStream_t st, DecoderWork& w, const float* atoms, const float* proj, float* d_proj,
+                       float* d_atoms);
 void reconstruct(cudaStream_t st, const float* q, int64_t n, int ds, const float* atoms, const float* proj,
                  int64_t k, int df, float temperature, float* out, float* attention, float* scratch_qw);
 void reconstruct_backward(cudaStream_t st, const float* q, const float* att, int64_t n, int ds,
