@@ -674,13 +674,14 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_fwd_mma_kernel(RasterAr
   constexpr int FP = DSP + 8;       // feature pitch: B-fragment loads hit distinct banks
   constexpr int WP = 40;            // per-warp [splat][pixel] weight pitch
   constexpr int NQ = DSP / 8;       // n-tiles (8 channels each)
+  constexpr int RP = 16 + (DSP + 3) / 4 * 4;  // raw staging row: [SplatRec 12 | colour 3 | - | features]
   extern __shared__ __align__(16) float s_dyn[];
   float* s_fh = s_dyn;                      // [FB][FP] tf32 hi
   float* s_fl = s_fh + FB * FP;             // [FB][FP] tf32 lo
   float* s_w = s_fl + FB * FP;              // [8 warps][16][WP]
-  __shared__ SplatRec s_rec[FB];
+  float* s_raw = s_w + 8 * 16 * WP;         // [FB][RP] cp.async staging of the next batch
+  __shared__ float4 s_sp[FB][3];            // {mean_x, mean_y, a00, 2 a01} {a11, alpha, depth, -} {bbox}
   __shared__ float s_col[FB * 3];
-  __shared__ uint32_t s_src[FB];
   __shared__ int32_t s_max;
   if (a.counters[2]) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -691,6 +692,30 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_fwd_mma_kernel(RasterAr
   const bool inside = px < a.width && py < a.height;
   const int start = a.offset[tile], end = a.offset[tile + 1];
   if (tid == 0) s_max = 0;
+  const bool vec_feat = (a.ds & 3) == 0;
+  // thread t < FB stages splat t of a batch: record, colour and features into s_raw (cp.async)
+  auto stage = [&](uint32_t src) {
+    float* row = s_raw + tid * RP;
+    const float4* rg = reinterpret_cast<const float4*>(a.rec + src);
+    cp_async16(row, rg);
+    cp_async16(row + 4, rg + 1);
+    cp_async16(row + 8, rg + 2);
+    cp_async4(row + 12, a.colors + 3 * (size_t)src);
+    cp_async4(row + 13, a.colors + 3 * (size_t)src + 1);
+    cp_async4(row + 14, a.colors + 3 * (size_t)src + 2);
+    const float* f = a.feats + (size_t)src * a.ds;
+    if (vec_feat) {
+      for (int c = 0; c < a.ds; c += 4) cp_async16(row + 16 + c, f + c);
+    } else {
+      for (int c = 0; c < a.ds; ++c) cp_async4(row + 16 + c, f + c);
+    }
+  };
+  uint32_t nsrc = 0;
+  if (tid < FB) {
+    if (start + tid < end) stage((uint32_t)a.keys[start + tid]);
+    cp_async_commit();
+    if (start + FB + tid < end) nsrc = (uint32_t)a.keys[start + FB + tid];
+  }
   float T = 1.f, acc_c0 = 0.f, acc_c1 = 0.f, acc_c2 = 0.f, acc_d = 0.f, acc_a = 0.f;
   float q[2][NQ][4];
 #pragma unroll
@@ -702,20 +727,13 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_fwd_mma_kernel(RasterAr
   const float fx = (float)px, fy = (float)py;
   float* sw = s_w + warp * 16 * WP;
   for (int base = start; base < end; base += FB) {
+    cp_async_wait_all();
     if (__syncthreads_and(done)) break;
     const int cnt = min(FB, end - base);
-    if (tid < cnt) {
-      const uint32_t src = (uint32_t)a.keys[base + tid];
-      s_src[tid] = src;
-      s_rec[tid] = a.rec[src];
-      s_col[tid * 3 + 0] = a.colors[3 * (size_t)src + 0];
-      s_col[tid * 3 + 1] = a.colors[3 * (size_t)src + 1];
-      s_col[tid * 3 + 2] = a.colors[3 * (size_t)src + 2];
-    }
-    __syncthreads();
+    // ---- unpack the staged batch: tf32 hi/lo feature rows, record terms, colours
     for (int e = tid; e < cnt * DSP; e += kTilePixels) {
       const int j = e / DSP, c = e % DSP;
-      const float v = c < a.ds ? a.feats[(size_t)s_src[j] * a.ds + c] : 0.f;
+      const float v = c < a.ds ? s_raw[j * RP + 16 + c] : 0.f;
       uint32_t hi, lo;
       split_tf32(v, hi, lo);
       s_fh[j * FP + c] = __uint_as_float(hi);
@@ -727,7 +745,24 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_fwd_mma_kernel(RasterAr
         s_fh[j * FP + c] = 0.f;
         s_fl[j * FP + c] = 0.f;
       }
+    if (tid < cnt) {
+      const float* row = s_raw + tid * RP;
+      const float4 r0 = *reinterpret_cast<const float4*>(row);      // mean_x, mean_y, depth, alpha
+      const float4 r1 = *reinterpret_cast<const float4*>(row + 4);  // a00, a01, a10, a11
+      s_sp[tid][0] = make_float4(r0.x, r0.y, r1.x, fm(2.f, r1.y));  // 2 a01: exact
+      s_sp[tid][1] = make_float4(r1.w, r0.w, r0.z, 0.f);
+      s_sp[tid][2] = *reinterpret_cast<const float4*>(row + 8);
+      s_col[tid * 3 + 0] = row[12];
+      s_col[tid * 3 + 1] = row[13];
+      s_col[tid * 3 + 2] = row[14];
+    }
     __syncthreads();
+    // ---- prefetch the next batch into the (now free) staging rows
+    if (tid < FB && base + FB < end) {
+      if (base + FB + tid < end) stage(nsrc);
+      cp_async_commit();
+      nsrc = base + 2 * FB + tid < end ? (uint32_t)a.keys[base + 2 * FB + tid] : 0u;
+    }
     for (int sb = 0; sb < cnt; sb += 16) {
       if (__all_sync(0xffffffffu, done)) break;
 #pragma unroll
@@ -740,19 +775,20 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_fwd_mma_kernel(RasterAr
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int j = sb + j4 + u;
-          const SplatRec& s = s_rec[j];
-          ok[u] = !done && j < cnt && px >= s.x0 && px <= s.x1 && py >= s.y0 && py <= s.y1;
+          const int4 bb = f4_as_i4(s_sp[j][2]);
+          ok[u] = !done && j < cnt && (unsigned)(px - bb.x) <= (unsigned)(bb.y - bb.x) &&
+                  (unsigned)(py - bb.z) <= (unsigned)(bb.w - bb.z);
           any |= ok[u];
         }
         if (__any_sync(0xffffffffu, any)) {
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const SplatRec& s = s_rec[sb + j4 + u];
-            const float dx = fs(fx, s.mean_x);
-            const float dy = fs(fy, s.mean_y);
-            const float rho =
-                fa(fa(fm(fm(s.a00, dx), dx), fm(fm(fm(2.f, s.a01), dx), dy)), fm(fm(s.a11, dy), dy));
-            float al = fm(s.alpha, exp_exact(fm(-0.5f, rho)));
+            const float4 s0 = s_sp[sb + j4 + u][0];
+            const float4 s1 = s_sp[sb + j4 + u][1];
+            const float dx = fs(fx, s0.x);
+            const float dy = fs(fy, s0.y);
+            const float rho = fa(fa(fm(fm(s0.z, dx), dx), fm(fm(s0.w, dx), dy)), fm(fm(s1.x, dy), dy));
+            float al = fm(s1.y, exp_exact(fm(-0.5f, rho)));
             alv[u] = al > kAlphaMax ? kAlphaMax : al;
           }
         }
@@ -766,7 +802,7 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_fwd_mma_kernel(RasterAr
             acc_c0 = fmaf(w, s_col[j * 3 + 0], acc_c0);
             acc_c1 = fmaf(w, s_col[j * 3 + 1], acc_c1);
             acc_c2 = fmaf(w, s_col[j * 3 + 2], acc_c2);
-            acc_d = fmaf(w, s_rec[j].depth, acc_d);
+            acc_d = fmaf(w, s_sp[j][1].z, acc_d);
             acc_a = fa(acc_a, w);
             T = fm(T, fs(1.f, al));
             if (T < kTransmitStop) {
@@ -808,6 +844,7 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_fwd_mma_kernel(RasterAr
       __syncwarp();
     }
   }
+  cp_async_wait_all();
   if (inside) {
     const size_t p = (size_t)py * a.width + px;
     a.color[3 * p + 0] = acc_c0;
@@ -1363,7 +1400,7 @@ void launch_fwd(cudaStream_t st, int ntiles, const RasterArgs& a, bool exact) {
   if (exact) {
     raster_fwd_kernel<DSP, true><<<ntiles, kTilePixels, 0, st>>>(a);
   } else if constexpr (DSP >= 8) {
-    const size_t smem = sizeof(float) * (2 * 128 * (DSP + 8) + 8 * 16 * 40);
+    const size_t smem = sizeof(float) * (2 * 128 * (DSP + 8) + 8 * 16 * 40 + 128 * (16 + (DSP + 3) / 4 * 4));
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(raster_fwd_mma_kernel<DSP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
