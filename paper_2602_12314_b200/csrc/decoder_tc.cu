@@ -553,52 +553,88 @@ __global__ void __launch_bounds__(288, 1) dec2_kernel(Dec2Args a) {
   if (warp == 0) tc::tmem_free<kTmemCols>(tmem);
 }
 
-// Sum the per-CTA partials: A (K x K) from (groups x 2 roles x K x K/2) and R^T (K x DS) -> R
-// (DS x K) are ADDED to the step accumulators (decoder_finish_tc applies them once per step),
-// Bm^T (n_set x K) from (groups x K x 64) is written for this frame, loss partials -> the frame's
-// partial slots. Partial sums run over 8 independent accumulators so the loads overlap.
-template <class F>
-__device__ __forceinline__ float sum_strided(int n, F at) {
-  float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  int gi = 0;
-  for (; gi + 8 <= n; gi += 8) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u) s[u] += at(gi + u);
-  }
-  for (; gi < n; ++gi) s[0] += at(gi);
-  return ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
-}
-
-__global__ void dec_reduce_kernel(const float* a_part, const float* bm_part, const float* r_part,
-                                  const double* loss_part, int K, int DS, int n_set, int groups1, int groups2,
-                                  float* A, float* bmt, float* R, double* partials) {
-  const int64_t total_a = (int64_t)K * K, total_b = (int64_t)n_set * K, total_r = (int64_t)K * DS;
+// Sum the per-CTA partials into the step accumulators: A (K x K) from (groups x 2 roles x K x
+// K/2), R^T (K x DS) -> R (DS x K), and this frame's Bm^T (n_set x K, zeroed beforehand) from
+// (groups x K x 64). Each thread owns 4 consecutive partial entries (float4 loads) and a
+// 1/kRedSplit share of the groups; the shares meet in global atomics (distinct addresses).
+// Block (0, 0) also folds the loss partials into the frame's slots.
+constexpr int kRedSplit = 4;
+__global__ void __launch_bounds__(256) dec_reduce_kernel(const float* __restrict__ a_part,
+                                                         const float* __restrict__ bm_part,
+                                                         const float* __restrict__ r_part,
+                                                         const double* loss_part, int K, int DS, int n_set,
+                                                         int groups1, int groups2, float* A, float* bmt, float* R,
+                                                         double* partials) {
   const int NH = K / 2;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total_a + total_b + total_r + 3;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    if (e < total_a) {
-      const int i = (int)(e / K), j = (int)(e % K);
-      const int role = j / NH, jj = j % NH;
-      const size_t stride = (size_t)2 * K * NH, off = ((size_t)role * K + i) * NH + jj;
-      A[e] += sum_strided(groups2, [&](int gi) { return a_part[gi * stride + off]; });
-    } else if (e < total_a + total_b) {  // thread order follows the partials' layout (coalesced reads)
-      const int64_t f = e - total_a;
-      const int k = (int)(f / n_set), sidx = (int)(f % n_set);
-      const size_t stride = (size_t)K * 64, off = (size_t)k * 64 + sidx;
-      bmt[(size_t)sidx * K + k] = sum_strided(groups2, [&](int gi) { return bm_part[gi * stride + off]; });
-    } else if (e < total_a + total_b + total_r) {
-      const int64_t f = e - total_a - total_b;
-      const int k = (int)(f / DS), s_ = (int)(f % DS);
-      const size_t stride = (size_t)K * DS, off = (size_t)k * DS + s_;
-      R[(size_t)s_ * K + k] += sum_strided(groups1, [&](int gi) { return r_part[gi * stride + off]; });
+  const int64_t qa = (int64_t)K * K / 4, qb = (int64_t)K * 64 / 4, qr = (int64_t)K * DS / 4;
+  const int split = blockIdx.y;
+  if (blockIdx.x == 0 && split == 0 && threadIdx.x < 3) {
+    const int which = threadIdx.x;
+    double s = 0.0;
+    for (int gi = 0; gi < groups1; ++gi) s += loss_part[gi * 4 + which];
+    if (which == 2)
+      partials[6] = fmax(partials[6], s > 0.0 ? 1.0 : 0.0);
+    else
+      partials[4 + which] += s;
+  }
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < qa + qb + qr;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const float4* src;
+    size_t stride;  // in float4
+    int ng;
+    if (q < qa) {  // partial layout [g][role][i][jj], 4 consecutive jj
+      const int64_t e = q * 4;
+      const int role = (int)(e / ((int64_t)K * NH)), rem = (int)(e % ((int64_t)K * NH));
+      src = reinterpret_cast<const float4*>(a_part) + (((size_t)role * K * NH) + rem) / 4;
+      stride = (size_t)2 * K * NH / 4;
+      ng = groups2;
+    } else if (q < qa + qb) {  // [g][k][64]
+      src = reinterpret_cast<const float4*>(bm_part) + (q - qa);
+      stride = (size_t)K * 64 / 4;
+      ng = groups2;
+    } else {  // [g][k][DS]
+      src = reinterpret_cast<const float4*>(r_part) + (q - qa - qb);
+      stride = (size_t)K * DS / 4;
+      ng = groups1;
+    }
+    const int per = (ng + kRedSplit - 1) / kRedSplit, g0 = split * per, g1 = min(ng, g0 + per);
+    float4 acc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    int gi = g0;
+    for (; gi + 4 <= g1; gi += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float4 v = __ldg(src + (size_t)(gi + u) * stride);
+        acc[u].x += v.x; acc[u].y += v.y; acc[u].z += v.z; acc[u].w += v.w;
+      }
+    }
+    for (; gi < g1; ++gi) {
+      const float4 v = __ldg(src + (size_t)gi * stride);
+      acc[0].x += v.x; acc[0].y += v.y; acc[0].z += v.z; acc[0].w += v.w;
+    }
+    const float4 t = make_float4((acc[0].x + acc[1].x) + (acc[2].x + acc[3].x),
+                                 (acc[0].y + acc[1].y) + (acc[2].y + acc[3].y),
+                                 (acc[0].z + acc[1].z) + (acc[2].z + acc[3].z),
+                                 (acc[0].w + acc[1].w) + (acc[2].w + acc[3].w));
+    const float tv[4] = {t.x, t.y, t.z, t.w};
+    if (q < qa) {
+      const int64_t e = q * 4;
+      const int role = (int)(e / ((int64_t)K * NH)), rem = (int)(e % ((int64_t)K * NH));
+      const int i = rem / NH, jj = rem % NH;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) atomicAdd(&A[(size_t)i * K + role * NH + jj + u], tv[u]);
+    } else if (q < qa + qb) {
+      const int64_t e = (q - qa) * 4;
+      const int k = (int)(e / 64), s0 = (int)(e % 64);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (s0 + u < n_set) atomicAdd(&bmt[(size_t)(s0 + u) * K + k], tv[u]);
     } else {
-      const int which = (int)(e - total_a - total_b - total_r);
-      double s = 0.0;
-      for (int gi = 0; gi < groups1; ++gi) s += loss_part[gi * 4 + which];
-      if (which == 2)
-        partials[6] = fmax(partials[6], s > 0.0 ? 1.0 : 0.0);
-      else
-        partials[4 + which] += s;
+      const int64_t e = (q - qa - qb) * 4;
+      const int k = (int)(e / DS), s0 = (int)(e % DS);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) atomicAdd(&R[(size_t)(s0 + u) * K + k], tv[u]);
     }
   }
 }
@@ -622,8 +658,8 @@ void launch_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_
   dec1_kernel<K, DS><<<g1, 512, sm1, st>>>(d1);
   count_launch();
   if (!want_grad) {
-    dec_reduce_kernel<<<1, 32, 0, st>>>(nullptr, nullptr, nullptr, w.loss_part, K, DS, 0, g1, 0, nullptr, nullptr,
-                                        nullptr, partials);
+    dec_reduce_kernel<<<dim3(1, 1), 32, 0, st>>>(nullptr, nullptr, nullptr, w.loss_part, 0, 0, 0, g1, 0, nullptr,
+                                                 nullptr, nullptr, partials);
     count_launch();
     return;
   }
@@ -636,8 +672,9 @@ void launch_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_
   }
   dec2_kernel<K><<<g2, 288, sm2, st>>>(d2);
   count_launch();
-  const int64_t tot = (int64_t)K * K + n_set * K + (int64_t)K * DS + 3;
-  dec_reduce_kernel<<<(unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 8), 256, 0, st>>>(
+  cudaMemsetAsync(w.bm, 0, sizeof(float) * n_set * K, st);
+  const int64_t quads = ((int64_t)K * K + (int64_t)K * 64 + (int64_t)K * DS) / 4;
+  dec_reduce_kernel<<<dim3((unsigned)((quads + 255) / 256), kRedSplit), 256, 0, st>>>(
       w.a_part, w.bm_part, w.r_part, w.loss_part, K, DS, (int)n_set, g1, g2 / 2, w.a_acc, w.bm, w.r_acc, partials);
   count_launch();
 }
