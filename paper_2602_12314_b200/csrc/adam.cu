@@ -59,79 +59,105 @@ __device__ __forceinline__ float adam_elem(float& p, float g, float& m, float& v
 }
 
 // Pass 2: update (adam.hpp:69-78); quaternion blocks renormalise rows (pipeline.cpp:78-84).
-__global__ void adam_update_kernel(float* __restrict__ param, const float* __restrict__ grad, float* __restrict__ m,
-                                   float* __restrict__ v, Blocks B, const int64_t* steps, const float* corr1,
-                                   const float* corr2, int32_t table_len, const int32_t* flags,
-                                   const int64_t* overflow) {
-  if (overflow && *overflow) return;
-  const int bi = blockIdx.y;
-  const AdamBlock blk = B.b[bi];
-  if (blk.kind < 0) return;
-  const bool skip = flags[bi] != 0;  // skipped block: parameters untouched (rotations still renormalised)
-  if (skip && blk.kind != 1) return;
-  const int64_t t = steps[bi] + 1;
-  const float c1 = t <= table_len ? corr1[t - 1] : 1.f;
-  const float c2 = t <= table_len ? corr2[t - 1] : 1.f;
-  if (blk.kind == 1) {
-    const int64_t nq = blk.count / 4;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nq; i += (int64_t)gridDim.x * blockDim.x) {
-      const int64_t e = blk.offset + 4 * i;
-      float q[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        float p = param[e + c];
-        if (!skip) {
-          float mm = m[e + c], vv = v[e + c];
-          adam_elem(p, grad[e + c], mm, vv, blk.lr, c1, c2);
-          m[e + c] = mm;
-          v[e + c] = vv;
-        }
-        q[c] = p;
-      }
-      const float n = __fsqrt_rn(fa(fa(fa(fm(q[0], q[0]), fm(q[1], q[1])), fm(q[2], q[2])), fm(q[3], q[3])));
-      if (n > 1e-12f) {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) param[e + c] = fd(q[c], n);
-      } else {
-        param[e] = 1.f;
-        param[e + 1] = param[e + 2] = param[e + 3] = 0.f;
-      }
-    }
-    return;
+// Every CTA walks every block in turn (grid-stride inside each block), so each block is
+// streamed by the whole GPU; rows / 4-aligned interiors use 16-byte vectors.
+__device__ __forceinline__ void quat_row(float4& p, const float4& g, float4& mm, float4& vv, bool skip, float lr,
+                                         float c1, float c2) {
+  if (!skip) {
+    adam_elem(p.x, g.x, mm.x, vv.x, lr, c1, c2);
+    adam_elem(p.y, g.y, mm.y, vv.y, lr, c1, c2);
+    adam_elem(p.z, g.z, mm.z, vv.z, lr, c1, c2);
+    adam_elem(p.w, g.w, mm.w, vv.w, lr, c1, c2);
   }
-  // 16-byte vectors over the 4-aligned interior of the block, scalar head/tail
-  const int64_t e0 = blk.offset, e1 = blk.offset + blk.count;
-  const int64_t a0 = (e0 + 3) / 4 * 4, a1 = e1 / 4 * 4;
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
-  if (a0 < a1) {
-    for (int64_t q = a0 / 4 + tid; q < a1 / 4; q += nth) {
-      float4 p = reinterpret_cast<float4*>(param)[q];
-      const float4 g = reinterpret_cast<const float4*>(grad)[q];
-      float4 mm = reinterpret_cast<float4*>(m)[q];
-      float4 vv = reinterpret_cast<float4*>(v)[q];
-      adam_elem(p.x, g.x, mm.x, vv.x, blk.lr, c1, c2);
-      adam_elem(p.y, g.y, mm.y, vv.y, blk.lr, c1, c2);
-      adam_elem(p.z, g.z, mm.z, vv.z, blk.lr, c1, c2);
-      adam_elem(p.w, g.w, mm.w, vv.w, blk.lr, c1, c2);
-      reinterpret_cast<float4*>(param)[q] = p;
-      reinterpret_cast<float4*>(m)[q] = mm;
-      reinterpret_cast<float4*>(v)[q] = vv;
-    }
-  }
-  auto scalar = [&](int64_t lo, int64_t hi) {
-    for (int64_t e = lo + tid; e < hi; e += nth) {
-      float p = param[e], mm = m[e], vv = v[e];
-      adam_elem(p, grad[e], mm, vv, blk.lr, c1, c2);
-      param[e] = p;
-      m[e] = mm;
-      v[e] = vv;
-    }
-  };
-  if (a0 < a1) {
-    scalar(e0, a0);
-    scalar(a1, e1);
+  const float n = __fsqrt_rn(fa(fa(fa(fm(p.x, p.x), fm(p.y, p.y)), fm(p.z, p.z)), fm(p.w, p.w)));
+  if (n > 1e-12f) {
+    p = make_float4(fd(p.x, n), fd(p.y, n), fd(p.z, n), fd(p.w, n));
   } else {
-    scalar(e0, e1);
+    p = make_float4(1.f, 0.f, 0.f, 0.f);
+  }
+}
+
+__global__ void __launch_bounds__(256) adam_update_kernel(float* __restrict__ param, const float* __restrict__ grad,
+                                                          float* __restrict__ m, float* __restrict__ v, Blocks B,
+                                                          const int64_t* steps, const float* corr1,
+                                                          const float* corr2, int32_t table_len, const int32_t* flags,
+                                                          const int64_t* overflow) {
+  if (overflow && *overflow) return;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+  for (int bi = 0; bi < B.n; ++bi) {
+    const AdamBlock blk = B.b[bi];
+    if (blk.kind < 0) continue;
+    const bool skip = flags[bi] != 0;  // skipped block: parameters untouched (rotations still renormalised)
+    if (skip && blk.kind != 1) continue;
+    const int64_t t = steps[bi] + 1;
+    const float c1 = t <= table_len ? corr1[t - 1] : 1.f;
+    const float c2 = t <= table_len ? corr2[t - 1] : 1.f;
+    const int64_t e0 = blk.offset, e1 = blk.offset + blk.count;
+    if (blk.kind == 1) {
+      const int64_t nq = blk.count / 4;
+      if ((e0 & 3) == 0) {
+        float4* p4 = reinterpret_cast<float4*>(param + e0);
+        const float4* g4 = reinterpret_cast<const float4*>(grad + e0);
+        float4* m4 = reinterpret_cast<float4*>(m + e0);
+        float4* v4 = reinterpret_cast<float4*>(v + e0);
+        for (int64_t i = tid; i < nq; i += nth) {
+          float4 p = p4[i], mm = m4[i], vv = v4[i];
+          quat_row(p, g4[i], mm, vv, skip, blk.lr, c1, c2);
+          p4[i] = p;
+          if (!skip) {
+            m4[i] = mm;
+            v4[i] = vv;
+          }
+        }
+      } else {
+        for (int64_t i = tid; i < nq; i += nth) {
+          const int64_t e = e0 + 4 * i;
+          float4 p = make_float4(param[e], param[e + 1], param[e + 2], param[e + 3]);
+          float4 mm = make_float4(m[e], m[e + 1], m[e + 2], m[e + 3]);
+          float4 vv = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+          const float4 g = make_float4(grad[e], grad[e + 1], grad[e + 2], grad[e + 3]);
+          quat_row(p, g, mm, vv, skip, blk.lr, c1, c2);
+          param[e] = p.x, param[e + 1] = p.y, param[e + 2] = p.z, param[e + 3] = p.w;
+          if (!skip) {
+            m[e] = mm.x, m[e + 1] = mm.y, m[e + 2] = mm.z, m[e + 3] = mm.w;
+            v[e] = vv.x, v[e + 1] = vv.y, v[e + 2] = vv.z, v[e + 3] = vv.w;
+          }
+        }
+      }
+      continue;
+    }
+    // 16-byte vectors over the 4-aligned interior of the block, scalar head/tail
+    const int64_t a0 = (e0 + 3) / 4 * 4, a1 = e1 / 4 * 4;
+    if (a0 < a1) {
+      for (int64_t q = a0 / 4 + tid; q < a1 / 4; q += nth) {
+        float4 p = reinterpret_cast<float4*>(param)[q];
+        const float4 g = reinterpret_cast<const float4*>(grad)[q];
+        float4 mm = reinterpret_cast<float4*>(m)[q];
+        float4 vv = reinterpret_cast<float4*>(v)[q];
+        adam_elem(p.x, g.x, mm.x, vv.x, blk.lr, c1, c2);
+        adam_elem(p.y, g.y, mm.y, vv.y, blk.lr, c1, c2);
+        adam_elem(p.z, g.z, mm.z, vv.z, blk.lr, c1, c2);
+        adam_elem(p.w, g.w, mm.w, vv.w, blk.lr, c1, c2);
+        reinterpret_cast<float4*>(param)[q] = p;
+        reinterpret_cast<float4*>(m)[q] = mm;
+        reinterpret_cast<float4*>(v)[q] = vv;
+      }
+    }
+    auto scalar = [&](int64_t lo, int64_t hi) {
+      for (int64_t e = lo + tid; e < hi; e += nth) {
+        float p = param[e], mm = m[e], vv = v[e];
+        adam_elem(p, grad[e], mm, vv, blk.lr, c1, c2);
+        param[e] = p;
+        m[e] = mm;
+        v[e] = vv;
+      }
+    };
+    if (a0 < a1) {
+      scalar(e0, a0);
+      scalar(a1, e1);
+    } else {
+      scalar(e0, e1);
+    }
   }
 }
 
@@ -161,8 +187,8 @@ void adam_flat(cudaStream_t st, float* param, const float* grad, float* m, float
     total = std::max(total, blocks[i].offset + blocks[i].count);
   }
   adam_check_kernel<<<148 * 4, 256, 0, st>>>(grad, B, total, flags);
-  adam_update_kernel<<<dim3(148 * 2, nblocks), 256, 0, st>>>(param, grad, m, v, B, steps, corr1, corr2, table_len,
-                                                              flags, overflow);
+  adam_update_kernel<<<148 * 8, 256, 0, st>>>(param, grad, m, v, B, steps, corr1, corr2, table_len, flags,
+                                               overflow);
   adam_finish_kernel<<<1, 32, 0, st>>>(B, steps, skipped, flags, overflow);
   count_launch(3);
 }
