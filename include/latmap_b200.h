@@ -214,6 +214,24 @@ latmap_status latmap_session_objective(latmap_session* s, int32_t want_grad, lat
 latmap_status latmap_session_apply(latmap_session* s);
 /* objective + apply; `out` may be NULL. */
 latmap_status latmap_session_step(latmap_session* s, latmap_loss_breakdown* out);
+/* total_objective with ObjectiveOptions (objective.hpp:33-43): map_grads = 0 skips the image-loss
+ * gradients and render_backward; use_cached_renders = 1 reuses the session's per-frame renders
+ * when the map has not changed since they were produced (cached_renders / render_sink). */
+latmap_status latmap_session_objective_ex(latmap_session* s, int32_t want_grad, int32_t map_grads,
+                                          int32_t use_cached_renders, latmap_loss_breakdown* out);
+/* One Stage-II iteration (pipeline.cpp:250-259): objective with map_grads = false on cached
+ * renders, then MapOptimizer::step_dict (proj, and atoms when dict_learn). */
+latmap_status latmap_session_step_dict(latmap_session* s, latmap_loss_breakdown* out);
+/* The active-map row set changes (ActiveSet after sync / append_newborns, active_set.hpp:10-26):
+ * export writes the map as device AoS rows [position 3 | rotation 4 | color 3 | log_scale 3 |
+ * opacity 1 | features query_dim] (the store's record layout); import replaces the map with
+ * n_new such rows, carrying the Adam moments of the old rows with kept[i] != 0 (in order) to the
+ * first n_kept new rows and zeroing the rest (MapOptimizer::keep_map_rows, pipeline.cpp:97-104;
+ * AdamState::ensure, adam.hpp:18-29). kept = NULL keeps every old row (pure append). */
+latmap_status latmap_session_export_rows(latmap_session* s, float* d_rows);
+latmap_status latmap_session_import_rows(latmap_session* s, const float* d_rows, int64_t n_new, const uint8_t* kept,
+                                         int64_t n_kept);
+int64_t latmap_session_size(const latmap_session* s);
 /* Flat device buffers: [positions|rotations|colors|log_scales|opacity|features|proj|atoms]
  * gradient layout (for the multi-GPU all-reduce) and the loss-partials vector. */
 latmap_status latmap_session_grad_buffer(latmap_session* s, float** grads, int64_t* count);

@@ -142,6 +142,37 @@ class Session {
     check(latmap_session_step(h_, &out), ctx_->get());
     return out;
   }
+  // total_objective with ObjectiveOptions::map_grads / cached_renders (objective.hpp:33-43)
+  latmap_loss_breakdown total_objective(bool map_grads, bool use_cached_renders) {
+    latmap_loss_breakdown out{};
+    check(latmap_session_objective_ex(h_, 1, map_grads ? 1 : 0, use_cached_renders ? 1 : 0, &out), ctx_->get());
+    return out;
+  }
+  // Stage II iteration: cached renders + MapOptimizer::step_dict (pipeline.cpp:250-259)
+  latmap_loss_breakdown step_dict() {
+    latmap_loss_breakdown out{};
+    check(latmap_session_step_dict(h_, &out), ctx_->get());
+    return out;
+  }
+  // Stage I x stage1 then Stage II x stage2 of process_keyframe_inner (pipeline.cpp:236-259);
+  // returns the last LossBreakdown (KeyframeLog::loss).
+  latmap_loss_breakdown optimize_keyframe(int stage1, int stage2) {
+    latmap_loss_breakdown out{};
+    bool have = false;
+    for (int it = 0; it < stage1; ++it) out = step(), have = true;
+    for (int it = 0; it < stage2; ++it) out = step_dict(), have = true;
+    if (!have) check(latmap_session_objective_ex(h_, 0, 0, 0, &out), ctx_->get());
+    return out;
+  }
+  // active-set row changes (keep_map_rows + append); rows are device AoS [n][14 + query_dim]
+  void export_rows(float* d_rows) { check(latmap_session_export_rows(h_, d_rows), ctx_->get()); }
+  void import_rows(const float* d_rows, int64_t n_new, const std::vector<uint8_t>* kept) {
+    int64_t nk = 0;
+    if (kept)
+      for (uint8_t k : *kept) nk += k != 0;
+    check(latmap_session_import_rows(h_, d_rows, n_new, kept ? kept->data() : nullptr, nk), ctx_->get());
+  }
+  int64_t size() const { return latmap_session_size(h_); }
   latmap_session* get() const { return h_; }
 
  private:

@@ -121,6 +121,10 @@ def _declare(L):
         "latmap_session_objective": [P, C.c_int32, C.POINTER(LossBreakdown)],
         "latmap_session_apply": [P],
         "latmap_session_step": [P, C.POINTER(LossBreakdown)],
+        "latmap_session_objective_ex": [P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(LossBreakdown)],
+        "latmap_session_step_dict": [P, C.POINTER(LossBreakdown)],
+        "latmap_session_export_rows": [P, P],
+        "latmap_session_import_rows": [P, P, C.c_int64, P, C.c_int64],
         "latmap_session_grad_buffer": [P, C.POINTER(P), C.POINTER(C.c_int64)],
         "latmap_session_loss_buffer": [P, C.POINTER(P), C.POINTER(C.c_int64)],
         "latmap_session_read_loss": [P, C.POINTER(LossBreakdown)],
@@ -165,6 +169,8 @@ def _declare(L):
     L.latmap_store_update.restype = C.c_int32
     L.latmap_store_find.argtypes = [P, P]
     L.latmap_store_find.restype = C.c_int64
+    L.latmap_session_size.argtypes = [P]
+    L.latmap_session_size.restype = C.c_int64
 
 
 EXPORTED = ["latmap_ctx_create", "latmap_ctx_destroy", "latmap_ctx_set_stream", "latmap_ctx_synchronize",
@@ -176,7 +182,9 @@ EXPORTED = ["latmap_ctx_create", "latmap_ctx_destroy", "latmap_ctx_set_stream", 
             "latmap_session_create", "latmap_session_destroy", "latmap_session_set_map", "latmap_session_get_map",
             "latmap_session_set_dictionary", "latmap_session_get_dictionary", "latmap_session_set_frames",
             "latmap_session_set_batch", "latmap_session_set_slot_offset", "latmap_session_objective",
-            "latmap_session_apply", "latmap_session_step", "latmap_session_grad_buffer", "latmap_session_loss_buffer",
+            "latmap_session_apply", "latmap_session_step", "latmap_session_objective_ex", "latmap_session_step_dict",
+            "latmap_session_export_rows", "latmap_session_import_rows", "latmap_session_size",
+            "latmap_session_grad_buffer", "latmap_session_loss_buffer",
             "latmap_session_read_loss", "latmap_session_frame_images", "latmap_session_stats",
             "latmap_session_profile", "latmap_session_phase_times", "latmap_selftest_umma", "latmap_ctx_stream",
             "latmap_voxel_of", "latmap_hash_voxel", "latmap_store_create", "latmap_store_destroy", "latmap_store_size",

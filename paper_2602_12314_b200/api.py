@@ -329,6 +329,38 @@ class Session:
         check(self.ctx.h, lib().latmap_session_step(self.h, C.byref(out) if read else None))
         return out.as_dict() if read else None
 
+    def objective_ex(self, want_grad=True, map_grads=True, use_cached_renders=False, read=True):
+        """total_objective with ObjectiveOptions (objective.hpp:33-43)."""
+        out = LossBreakdown()
+        check(self.ctx.h, lib().latmap_session_objective_ex(self.h, int(want_grad), int(map_grads),
+                                                            int(use_cached_renders), C.byref(out) if read else None))
+        return out.as_dict() if read else None
+
+    def step_dict(self, read=True):
+        """One Stage-II iteration (pipeline.cpp:250-259): cached renders, dictionary-only Adam."""
+        out = LossBreakdown()
+        check(self.ctx.h, lib().latmap_session_step_dict(self.h, C.byref(out) if read else None))
+        return out.as_dict() if read else None
+
+    ROW = 14  # + query_dim: position 3 | rotation 4 | color 3 | log_scale 3 | opacity 1 | features
+
+    def export_rows(self, out=None):
+        """The map as device AoS rows (the store's record layout), a torch tensor [n, 14 + ds]."""
+        if out is None:
+            out = torch.empty((self.n, self.ROW + self.ds), dtype=torch.float32, device=f"cuda:{self.ctx.device}")
+        check(self.ctx.h, lib().latmap_session_export_rows(self.h, C.c_void_p(out.data_ptr())))
+        return out
+
+    def import_rows(self, rows, kept=None):
+        """Replace the map with device AoS ``rows``; Adam moments of old rows with kept[i] carry over
+        to the first sum(kept) rows (MapOptimizer::keep_map_rows), the rest start at zero."""
+        n_new = int(rows.shape[0])
+        km = None if kept is None else np.ascontiguousarray(kept, np.uint8)
+        n_kept = int(km.sum()) if km is not None else self.n
+        check(self.ctx.h, lib().latmap_session_import_rows(self.h, C.c_void_p(rows.data_ptr()) if n_new else None,
+                                                           n_new, self._np_ptr(km), n_kept))
+        self.n = n_new
+
     def read_loss(self):
         out = LossBreakdown()
         check(self.ctx.h, lib().latmap_session_read_loss(self.h, C.byref(out)))

@@ -583,6 +583,8 @@ struct latmap_session {
   double* partials = nullptr;
   int32_t part_frames = 0;
   latmap_loss_breakdown* d_loss = nullptr;
+  // the per-frame images hold renders of the current map (ObjectiveOptions::cached_renders)
+  bool renders_valid = false;
   // phase timing with CUDA events on the session stream (bench.py roofline evidence)
   struct Span {
     int phase;
@@ -682,7 +684,11 @@ latmap_status session_alloc_frames(latmap_session* s, int nf) {
   return LATMAP_OK;
 }
 
-latmap_status session_objective(latmap_session* s, bool want_grad) {
+// One total_objective over the session's keyframes (objective.cpp:67-194). map_grads = false
+// skips the image-loss gradients and the render backward (ObjectiveOptions::map_grads);
+// use_cache skips the render when the per-frame images still hold renders of the current map
+// (ObjectiveOptions::cached_renders, Stage II of pipeline.cpp:250-259).
+latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grads = true, bool use_cache = false) {
   latmap_ctx* ctx = s->ctx;
   cudaStream_t st = ctx->stream;
   const latmap_config& c = s->cfg;
@@ -728,16 +734,20 @@ latmap_status session_objective(latmap_session* s, bool want_grad) {
     RenderBufs& rb = s->rw[b];
     rb.w.step_overflow = s->overflow;
     double* part = s->partials + (size_t)(s->slot_offset + b) * kPart;
-    s->begin(0);
-    render_forward(st, map, f.rcw, f.pose.translation, in, rb.w, s->color[b], s->depth[b], s->query[b], s->alpha[b],
-                   false, false, false);
-    s->end();
-    s->begin(1);
-    render_blend(st, map, in, rb.w, s->color[b], s->depth[b], s->query[b], s->alpha[b], ctx->exact_blend);
-    s->end();
+    const bool cached = use_cache && s->renders_valid;
+    if (!cached) {
+      s->begin(0);
+      render_forward(st, map, f.rcw, f.pose.translation, in, rb.w, s->color[b], s->depth[b], s->query[b],
+                     s->alpha[b], false, false, false);
+      s->end();
+      s->begin(1);
+      render_blend(st, map, in, rb.w, s->color[b], s->depth[b], s->query[b], s->alpha[b], ctx->exact_blend);
+      s->end();
+    }
+    const bool map_grad = want_grad && map_grads;
     s->begin(2);
     image_losses(st, s->color[b], s->depth[b], s->alpha[b], f.rgb, f.depth, h, w, c.lambda_i1, c.lambda_i2,
-                 c.lambda_rgb * inv_b, c.lambda_depth * inv_b, want_grad, s->d_color, s->d_depth, part,
+                 c.lambda_rgb * inv_b, c.lambda_depth * inv_b, map_grad, s->d_color, s->d_depth, part,
                  s->ssim_scratch);
     s->end();
     set_double_kernel<<<1, 1, 0, st>>>(part + 7, (double)f.n_sup);
@@ -754,7 +764,7 @@ latmap_status session_objective(latmap_session* s, bool want_grad) {
                       c.lambda_cos, c.lambda_l2, c.lambda_feat * inv_b, want_grad, s->d_query, g_proj, g_atoms, part);
       s->end();
     }
-    if (want_grad) {
+    if (map_grad) {
       CTX_CHECK(ctx, cudaMemsetAsync(rb.geo_acc, 0, sizeof(float) * 8 * s->n, st));
       s->begin(4);
       render_backward(st, map, f.rcw, f.rwc, f.pose.translation, in, rb.w, s->d_color, s->d_depth,
@@ -765,6 +775,7 @@ latmap_status session_objective(latmap_session* s, bool want_grad) {
       s->end();
     }
   }
+  s->renders_valid = true;
   if (want_grad) decoder_finish_tc(st, s->dec, atoms, proj, g_proj, g_atoms);
   // trust term enters once (objective.cpp:247-256)
   if (s->add_trust) {
@@ -798,7 +809,8 @@ latmap_status session_assemble(latmap_session* s, latmap_loss_breakdown* out) {
   return post_launch(ctx);
 }
 
-void session_adam(latmap_session* s) {
+// MapOptimizer::step_map + step_dict (pipeline.cpp:75-95); dict_only = step_dict alone (Stage II).
+void session_adam(latmap_session* s, bool dict_only = false) {
   const latmap_config& c = s->cfg;
   s->begin(6);
   AdamBlock blocks[8] = {
@@ -811,6 +823,10 @@ void session_adam(latmap_session* s) {
       {s->off[6], s->off[7] - s->off[6], c.lr_proj, 0},                       // pipeline.cpp:93
       {s->off[7], s->off[8] - s->off[7], c.lr_dict, c.dict_learn ? 0 : -1},  // pipeline.cpp:94
   };
+  if (dict_only)
+    for (int i = 0; i < 6; ++i) blocks[i].kind = -1;
+  else
+    s->renders_valid = false;  // the map moves
   adam_flat(s->ctx->stream, s->params, s->grads, s->m, s->v, blocks, 8, s->steps, s->skipped, s->corr1, s->corr2,
             kCorrLen, s->flags, s->overflow);
   s->end();
@@ -933,6 +949,7 @@ latmap_status latmap_session_set_map(latmap_session* s, const float* pos, const 
                                      const float* lsc, const float* opa, const float* feat) {
   if (!s) return LATMAP_ERR_INVALID_ARGUMENT;
   latmap_ctx* ctx = s->ctx;
+  s->renders_valid = false;
   const float* src[6] = {pos, rot, col, lsc, opa, feat};
   for (int i = 0; i < 6; ++i)
     if (s->off[i + 1] > s->off[i])
@@ -1003,15 +1020,18 @@ latmap_status latmap_session_set_frames(latmap_session* s, int32_t nf, const lat
     CTX_CHECK(ctx, cudaMemcpyAsync(f.assign, in.assignment, sizeof(int32_t) * npx, cudaMemcpyHostToDevice, ctx->stream));
     if (nfeat) CTX_CHECK(ctx, cudaMemcpyAsync(f.feats, in.features, sizeof(float) * nfeat, cudaMemcpyHostToDevice, ctx->stream));
     int64_t nsup = 0;
-    for (size_t p = 0; p < npx; ++p) {
+    int32_t amax = -1;
+    for (size_t p = 0; p < npx; ++p) {  // branch-free: vectorises
       const int32_t a = in.assignment[p];
-      if (a >= in.n_set) return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "gather_supervision: assignment out of range");
       nsup += a >= 0;
+      amax = a > amax ? a : amax;
     }
+    if (amax >= in.n_set) return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "gather_supervision: assignment out of range");
     f.n_sup = nsup;
     f.n_set = in.n_set;
   }
   s->nframes = nf;
+  s->renders_valid = false;  // poses may differ
   // per-frame decoder buffers sized by the largest embedding table
   int64_t max_set = 1;
   for (int b = 0; b < nf; ++b) max_set = std::max(max_set, s->frames[b].n_set);
@@ -1069,6 +1089,158 @@ latmap_status latmap_session_step(latmap_session* s, latmap_loss_breakdown* out)
   }
   return fail(s->ctx, LATMAP_ERR_CUDA, "tile-pair buffer overflow persisted");
 }
+
+latmap_status latmap_session_objective_ex(latmap_session* s, int32_t want_grad, int32_t map_grads,
+                                          int32_t use_cached_renders, latmap_loss_breakdown* out) {
+  if (!s || s->nframes < 1) return LATMAP_ERR_INVALID_ARGUMENT;
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    latmap_status st = session_objective(s, want_grad != 0, map_grads != 0, use_cached_renders != 0);
+    if (st != LATMAP_OK) return st;
+    if (!out) return LATMAP_OK;
+    CTX_CHECK(s->ctx, cudaStreamSynchronize(s->ctx->stream));
+    if (!session_fix_overflow(s)) return session_assemble(s, out);
+    s->renders_valid = false;
+  }
+  return fail(s->ctx, LATMAP_ERR_CUDA, "tile-pair buffer overflow persisted");
+}
+
+latmap_status latmap_session_step_dict(latmap_session* s, latmap_loss_breakdown* out) {
+  if (!s || s->nframes < 1) return LATMAP_ERR_INVALID_ARGUMENT;
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    latmap_status st = session_objective(s, true, false, true);
+    if (st != LATMAP_OK) return st;
+    session_adam(s, true);  // no-op on device when a tile buffer overflowed
+    if (!out) return post_launch(s->ctx);
+    st = session_assemble(s, out);
+    if (st != LATMAP_OK) return st;
+    if (!session_fix_overflow(s)) return LATMAP_OK;
+    s->renders_valid = false;
+  }
+  return fail(s->ctx, LATMAP_ERR_CUDA, "tile-pair buffer overflow persisted");
+}
+
+// ------------------------------------------------------------------ map row-set changes
+// AoS row = [position 3 | rotation 4 | color 3 | log_scale 3 | opacity 1 | features ds] (the
+// store's record layout, voxel_hash.hpp:61-72).
+namespace {
+struct MapOff {
+  int64_t o[6];
+};
+__global__ void soa_to_aos_kernel(const float* __restrict__ p, MapOff mo, int64_t n, int ds, float* __restrict__ rows) {
+  const int rs = 14 + ds;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * rs; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / rs;
+    const int c = (int)(e % rs);
+    float v;
+    if (c < 3) v = p[mo.o[0] + 3 * i + c];
+    else if (c < 7) v = p[mo.o[1] + 4 * i + c - 3];
+    else if (c < 10) v = p[mo.o[2] + 3 * i + c - 7];
+    else if (c < 13) v = p[mo.o[3] + 3 * i + c - 10];
+    else if (c == 13) v = p[mo.o[4] + i];
+    else v = p[mo.o[5] + (int64_t)ds * i + c - 14];
+    rows[e] = v;
+  }
+}
+__global__ void aos_to_soa_kernel(const float* __restrict__ rows, MapOff mo, int64_t n, int ds, float* __restrict__ p) {
+  const int rs = 14 + ds;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * rs; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / rs;
+    const int c = (int)(e % rs);
+    const float v = rows[e];
+    if (c < 3) p[mo.o[0] + 3 * i + c] = v;
+    else if (c < 7) p[mo.o[1] + 4 * i + c - 3] = v;
+    else if (c < 10) p[mo.o[2] + 3 * i + c - 7] = v;
+    else if (c < 13) p[mo.o[3] + 3 * i + c - 10] = v;
+    else if (c == 13) p[mo.o[4] + i] = v;
+    else p[mo.o[5] + (int64_t)ds * i + c - 14] = v;
+  }
+}
+// moments of the map blocks: new row r < n_kept <- old row idx[r]; rows >= n_kept <- 0
+__global__ void gather_moments_kernel(const float* __restrict__ src, MapOff so, float* __restrict__ dst, MapOff d_o,
+                                      const int64_t* __restrict__ idx, int64_t n_kept, int64_t n_new, int ds) {
+  const int w[6] = {3, 4, 3, 3, 1, ds};
+  for (int b = 0; b < 6; ++b) {
+    const int wb = w[b];
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_new * wb;
+         e += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t r = e / wb;
+      const int c = (int)(e % wb);
+      dst[d_o.o[b] + e] = r < n_kept ? src[so.o[b] + idx[r] * wb + c] : 0.f;
+    }
+  }
+}
+unsigned grid_cap(int64_t n) { return (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16); }
+}  // namespace
+
+latmap_status latmap_session_export_rows(latmap_session* s, float* d_rows) {
+  if (!s || (!d_rows && s->n > 0)) return LATMAP_ERR_INVALID_ARGUMENT;
+  MapOff mo;
+  for (int i = 0; i < 6; ++i) mo.o[i] = s->off[i];
+  if (s->n > 0) {
+    soa_to_aos_kernel<<<grid_cap(s->n * (14 + s->ds)), 256, 0, s->ctx->stream>>>(s->params, mo, s->n, s->ds, d_rows);
+    count_launch();
+  }
+  return post_launch(s->ctx);
+}
+
+latmap_status latmap_session_import_rows(latmap_session* s, const float* d_rows, int64_t n_new, const uint8_t* kept,
+                                         int64_t n_kept) {
+  if (!s || n_new < 0 || (n_new > 0 && !d_rows)) return LATMAP_ERR_INVALID_ARGUMENT;
+  latmap_ctx* ctx = s->ctx;
+  cudaStream_t st = ctx->stream;
+  // rows of the old map whose Adam moments carry over, in order (MapOptimizer::keep_map_rows)
+  std::vector<int64_t> idx;
+  if (kept) {
+    for (int64_t i = 0; i < s->n; ++i)
+      if (kept[i]) idx.push_back(i);
+  } else {
+    for (int64_t i = 0; i < s->n; ++i) idx.push_back(i);
+  }
+  if ((kept && (int64_t)idx.size() != n_kept) || (int64_t)idx.size() > n_new)
+    return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "import_rows: kept rows do not match the new row count");
+  n_kept = (int64_t)idx.size();
+  const int ds = s->ds;
+  const int64_t sizes[8] = {3 * n_new, 4 * n_new, 3 * n_new, 3 * n_new, n_new, (int64_t)ds * n_new,
+                            (int64_t)ds * s->df, s->k * s->df};
+  int64_t off[9];
+  off[0] = 0;
+  for (int i = 0; i < 8; ++i) off[i + 1] = off[i] + sizes[i];
+  const int64_t total = off[8];
+  float *np = nullptr, *ng = nullptr, *nm = nullptr, *nv = nullptr;
+  int64_t* d_idx = nullptr;
+  CTX_CHECK(ctx, cudaMalloc(&np, sizeof(float) * std::max<int64_t>(total, 1)));
+  CTX_CHECK(ctx, cudaMalloc(&ng, sizeof(float) * std::max<int64_t>(total, 1)));
+  CTX_CHECK(ctx, cudaMalloc(&nm, sizeof(float) * std::max<int64_t>(total, 1)));
+  CTX_CHECK(ctx, cudaMalloc(&nv, sizeof(float) * std::max<int64_t>(total, 1)));
+  CTX_CHECK(ctx, cudaMalloc(&d_idx, sizeof(int64_t) * std::max<size_t>(idx.size(), 1)));
+  if (!idx.empty())
+    CTX_CHECK(ctx, cudaMemcpyAsync(d_idx, idx.data(), sizeof(int64_t) * idx.size(), cudaMemcpyHostToDevice, st));
+  MapOff so, d_o;
+  for (int i = 0; i < 6; ++i) so.o[i] = s->off[i], d_o.o[i] = off[i];
+  if (n_new > 0) {
+    aos_to_soa_kernel<<<grid_cap(n_new * (14 + ds)), 256, 0, st>>>(d_rows, d_o, n_new, ds, np);
+    gather_moments_kernel<<<grid_cap(n_new * ds), 256, 0, st>>>(s->m, so, nm, d_o, d_idx, n_kept, n_new, ds);
+    gather_moments_kernel<<<grid_cap(n_new * ds), 256, 0, st>>>(s->v, so, nv, d_o, d_idx, n_kept, n_new, ds);
+    count_launch(3);
+  }
+  // dictionary blocks and their moments carry over unchanged
+  const size_t dict = (size_t)(s->total - s->off[6]);
+  CTX_CHECK(ctx, cudaMemcpyAsync(np + off[6], s->params + s->off[6], sizeof(float) * dict, cudaMemcpyDeviceToDevice, st));
+  CTX_CHECK(ctx, cudaMemcpyAsync(nm + off[6], s->m + s->off[6], sizeof(float) * dict, cudaMemcpyDeviceToDevice, st));
+  CTX_CHECK(ctx, cudaMemcpyAsync(nv + off[6], s->v + s->off[6], sizeof(float) * dict, cudaMemcpyDeviceToDevice, st));
+  CTX_CHECK(ctx, cudaMemsetAsync(ng, 0, sizeof(float) * std::max<int64_t>(total, 1), st));
+  CTX_CHECK(ctx, cudaStreamSynchronize(st));
+  cudaFree(s->params), cudaFree(s->grads), cudaFree(s->m), cudaFree(s->v), cudaFree(d_idx);
+  s->params = np, s->grads = ng, s->m = nm, s->v = nv;
+  s->n = n_new;
+  for (int i = 0; i < 9; ++i) s->off[i] = off[i];
+  s->total = total;
+  for (auto& r : s->rw) r.release();  // re-sized for the new N on the next objective
+  s->renders_valid = false;
+  return LATMAP_OK;
+}
+
+int64_t latmap_session_size(const latmap_session* s) { return s ? s->n : -1; }
 
 latmap_status latmap_session_grad_buffer(latmap_session* s, float** grads, int64_t* count) {
   if (!s || !grads || !count) return LATMAP_ERR_INVALID_ARGUMENT;
