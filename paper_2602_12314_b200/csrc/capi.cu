@@ -563,13 +563,16 @@ struct FrameDev {
 constexpr int kPart = 8;  // per-frame loss partial slots (see losses.cu / decoder.cu)
 }  // namespace
 
+// session parameter blocks start on 16-byte boundaries (vector loads / cp.async of rows)
+static inline int64_t pad4(int64_t x) { return (x + 3) & ~int64_t(3); }
+
 struct latmap_session {
   latmap_ctx* ctx = nullptr;
   latmap_config cfg{};
   int64_t n = 0, k = 0;
   int32_t ds = 0, df = 0;
   latmap_intrinsics intr{};
-  int64_t total = 0, off[9] = {};
+  int64_t total = 0, off[9] = {}, len[8] = {};  // block offsets (16-byte aligned) and true lengths
   float *params = nullptr, *grads = nullptr, *m = nullptr, *v = nullptr, *anchor = nullptr;
   int64_t *steps = nullptr, *skipped = nullptr, *overflow = nullptr;
   int32_t* flags = nullptr;
@@ -814,14 +817,14 @@ void session_adam(latmap_session* s, bool dict_only = false) {
   const latmap_config& c = s->cfg;
   s->begin(6);
   AdamBlock blocks[8] = {
-      {s->off[0], s->off[1] - s->off[0], c.lr_position * c.scene_extent, 0},  // pipeline.cpp:76
-      {s->off[1], s->off[2] - s->off[1], c.lr_rotation, 1},
-      {s->off[2], s->off[3] - s->off[2], c.lr_color, 0},
-      {s->off[3], s->off[4] - s->off[3], c.lr_log_scale, 0},
-      {s->off[4], s->off[5] - s->off[4], c.lr_opacity, 0},
-      {s->off[5], s->off[6] - s->off[5], c.lr_feature, 0},
-      {s->off[6], s->off[7] - s->off[6], c.lr_proj, 0},                       // pipeline.cpp:93
-      {s->off[7], s->off[8] - s->off[7], c.lr_dict, c.dict_learn ? 0 : -1},  // pipeline.cpp:94
+      {s->off[0], s->len[0], c.lr_position * c.scene_extent, 0},  // pipeline.cpp:76
+      {s->off[1], s->len[1], c.lr_rotation, 1},
+      {s->off[2], s->len[2], c.lr_color, 0},
+      {s->off[3], s->len[3], c.lr_log_scale, 0},
+      {s->off[4], s->len[4], c.lr_opacity, 0},
+      {s->off[5], s->len[5], c.lr_feature, 0},
+      {s->off[6], s->len[6], c.lr_proj, 0},                       // pipeline.cpp:93
+      {s->off[7], s->len[7], c.lr_dict, c.dict_learn ? 0 : -1},  // pipeline.cpp:94
   };
   if (dict_only)
     for (int i = 0; i < 6; ++i) blocks[i].kind = -1;
@@ -866,7 +869,8 @@ latmap_status latmap_session_create(latmap_ctx* ctx, const latmap_config* cfg, i
   s->intr = *intr;
   const int64_t sizes[8] = {3 * n, 4 * n, 3 * n, 3 * n, n, (int64_t)ds * n, (int64_t)ds * df, k * df};
   s->off[0] = 0;
-  for (int i = 0; i < 8; ++i) s->off[i + 1] = s->off[i] + sizes[i];
+  for (int i = 0; i < 8; ++i) s->off[i + 1] = pad4(s->off[i] + sizes[i]);  // 16-byte aligned blocks
+  for (int i = 0; i < 8; ++i) s->len[i] = sizes[i];
   s->total = s->off[8];
   const size_t npx = (size_t)intr->width * intr->height;
   auto ok = [&](cudaError_t e) { return e == cudaSuccess; };
@@ -952,8 +956,8 @@ latmap_status latmap_session_set_map(latmap_session* s, const float* pos, const 
   s->renders_valid = false;
   const float* src[6] = {pos, rot, col, lsc, opa, feat};
   for (int i = 0; i < 6; ++i)
-    if (s->off[i + 1] > s->off[i])
-      CTX_CHECK(ctx, cudaMemcpyAsync(s->params + s->off[i], src[i], sizeof(float) * (s->off[i + 1] - s->off[i]),
+    if (s->len[i] > 0)
+      CTX_CHECK(ctx, cudaMemcpyAsync(s->params + s->off[i], src[i], sizeof(float) * s->len[i],
                                      cudaMemcpyHostToDevice, ctx->stream));
   return LATMAP_OK;
 }
@@ -964,8 +968,8 @@ latmap_status latmap_session_get_map(latmap_session* s, float* pos, float* rot, 
   latmap_ctx* ctx = s->ctx;
   float* dst[6] = {pos, rot, col, lsc, opa, feat};
   for (int i = 0; i < 6; ++i)
-    if (dst[i] && s->off[i + 1] > s->off[i])
-      CTX_CHECK(ctx, cudaMemcpyAsync(dst[i], s->params + s->off[i], sizeof(float) * (s->off[i + 1] - s->off[i]),
+    if (dst[i] && s->len[i] > 0)
+      CTX_CHECK(ctx, cudaMemcpyAsync(dst[i], s->params + s->off[i], sizeof(float) * s->len[i],
                                      cudaMemcpyDeviceToHost, ctx->stream));
   CTX_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
   return LATMAP_OK;
@@ -1204,7 +1208,7 @@ latmap_status latmap_session_import_rows(latmap_session* s, const float* d_rows,
                             (int64_t)ds * s->df, s->k * s->df};
   int64_t off[9];
   off[0] = 0;
-  for (int i = 0; i < 8; ++i) off[i + 1] = off[i] + sizes[i];
+  for (int i = 0; i < 8; ++i) off[i + 1] = pad4(off[i] + sizes[i]);
   const int64_t total = off[8];
   float *np = nullptr, *ng = nullptr, *nm = nullptr, *nv = nullptr;
   int64_t* d_idx = nullptr;
@@ -1234,6 +1238,7 @@ latmap_status latmap_session_import_rows(latmap_session* s, const float* d_rows,
   s->params = np, s->grads = ng, s->m = nm, s->v = nv;
   s->n = n_new;
   for (int i = 0; i < 9; ++i) s->off[i] = off[i];
+  for (int i = 0; i < 8; ++i) s->len[i] = sizes[i];
   s->total = total;
   for (auto& r : s->rw) r.release();  // re-sized for the new N on the next objective
   s->renders_valid = false;

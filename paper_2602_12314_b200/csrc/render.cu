@@ -692,7 +692,7 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_fwd_mma_kernel(RasterAr
   const bool inside = px < a.width && py < a.height;
   const int start = a.offset[tile], end = a.offset[tile + 1];
   if (tid == 0) s_max = 0;
-  const bool vec_feat = (a.ds & 3) == 0;
+  const bool vec_feat = (a.ds & 3) == 0 && (reinterpret_cast<uintptr_t>(a.feats) & 15) == 0;
   // thread t < FB stages splat t of a batch: record, colour and features into s_raw (cp.async)
   auto stage = [&](uint32_t src) {
     float* row = s_raw + tid * RP;
@@ -921,7 +921,7 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
   const int start = a.offset[tile];
   const int tend = start + a.tile_max_last[tile];
   if (tend <= start) return;
-  const bool vec_feat = (a.ds & 3) == 0;
+  const bool vec_feat = (a.ds & 3) == 0 && (reinterpret_cast<uintptr_t>(a.feats) & 15) == 0;
   // warp 0, lanes 0..15: stage splat `lane` of the batch [lo, lo + cnt) into raw buffer `buf`
   auto stage = [&](int buf, int lo, int cnt, uint32_t src) {
     float* row = s_raw[buf] + lane * RP;

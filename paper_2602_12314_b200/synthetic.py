@@ -104,8 +104,16 @@ def random_map(rng, n, lo, hi, ds, dtype=np.float32):
     return HostMap(*[np.ascontiguousarray(a, dtype) for a in (pos, q, col, lsc, opa, feat)])
 
 
-def voronoi_assignment(rng, w, h, n_seeds):
+def voronoi_assignment(rng, w, h, n_seeds, device=None):
     seeds = rng.random((n_seeds, 2)) * np.array([w, h])
+    if device is not None:  # same float64 distances and first-minimum ties, evaluated with torch
+        import torch
+
+        ys, xs = torch.meshgrid(torch.arange(h, dtype=torch.float64, device=device),
+                                torch.arange(w, dtype=torch.float64, device=device), indexing="ij")
+        sd = torch.as_tensor(seeds, device=device)
+        d = (xs.reshape(-1, 1) - sd[None, :, 0]) ** 2 + (ys.reshape(-1, 1) - sd[None, :, 1]) ** 2
+        return torch.argmin(d, dim=1).to(torch.int32).cpu().numpy()
     ys, xs = np.mgrid[0:h, 0:w]
     px = np.stack([xs.ravel(), ys.ravel()], 1).astype(np.float64)
     best = np.zeros(px.shape[0], np.int32)
@@ -178,3 +186,108 @@ def make_workload(cfg_id, render_fn, scale=1.0):
     iters = {0: 1, 1: 100, 2: 1, 4: 20}[cfg_id]
     return Workload(cfg_id, intr, m, atoms, atoms.copy(), proj, temperature, frames, lambdas, iters,
                     NAMES[cfg_id] + ("" if scale == 1.0 else f"-scale{scale}"))
+
+
+# ----------------------------------------------------------------------------- config 3
+@dataclass
+class Streaming:
+    """Config 3 (BASELINE.json configs[3]): a host-resident global map
+    of voxel-hashed records streamed through the GPU active set along a camera trajectory."""
+    intr: Intr
+    records: np.ndarray      # n_global x (14 + d_s) AoS, the store's record layout
+    atoms: np.ndarray
+    proj: np.ndarray
+    temperature: float
+    poses: list              # (quat, trans) per frame
+    assignments: list        # per frame H x W int32 (Voronoi cells)
+    features: list           # per frame n_seeds x d_f
+    voxel_size: float = 0.01
+    radius: float = 6.0
+    capacity: int = 1 << 24
+    iters_per_frame: int = 10
+    lambdas: dict = field(default_factory=dict)
+    name: str = ""
+
+
+def look_quat(d):
+    """Camera-to-world rotation (w, x, y, z) of a camera looking along the horizontal unit vector d
+    with image-down = world -z (camera axes: x right, y down, z forward; synthetic.cpp:145)."""
+    z = np.array([d[0], d[1], 0.0])
+    z /= np.linalg.norm(z)
+    y = np.array([0.0, 0.0, -1.0])
+    x = np.cross(y, z)
+    R = np.stack([x, y, z], 1)  # columns = camera axes in world coordinates
+    tr = R[0, 0] + R[1, 1] + R[2, 2]
+    if tr > 0:
+        s = math.sqrt(tr + 1.0) * 2
+        q = (0.25 * s, (R[2, 1] - R[1, 2]) / s, (R[0, 2] - R[2, 0]) / s, (R[1, 0] - R[0, 1]) / s)
+    elif R[0, 0] > R[1, 1] and R[0, 0] > R[2, 2]:
+        s = math.sqrt(1.0 + R[0, 0] - R[1, 1] - R[2, 2]) * 2
+        q = ((R[2, 1] - R[1, 2]) / s, 0.25 * s, (R[0, 1] + R[1, 0]) / s, (R[0, 2] + R[2, 0]) / s)
+    elif R[1, 1] > R[2, 2]:
+        s = math.sqrt(1.0 + R[1, 1] - R[0, 0] - R[2, 2]) * 2
+        q = ((R[0, 2] - R[2, 0]) / s, (R[0, 1] + R[1, 0]) / s, 0.25 * s, (R[1, 2] + R[2, 1]) / s)
+    else:
+        s = math.sqrt(1.0 + R[2, 2] - R[0, 0] - R[1, 1]) * 2
+        q = ((R[1, 0] - R[0, 1]) / s, (R[0, 2] + R[2, 0]) / s, (R[1, 2] + R[2, 1]) / s, 0.25 * s)
+    return tuple(float(v) for v in q)
+
+
+def spline_path(rng, nframes, step, lo, hi, margin=8.0, height=4.5):
+    """Seeded Catmull-Rom spline through random control points inside the volume, sampled every
+    `step` metres of arc length; returns positions and horizontal tangents."""
+    lo, hi = np.asarray(lo, np.float64), np.asarray(hi, np.float64)
+    cps = lo[:2] + margin + rng.random((8, 2)) * (hi[:2] - lo[:2] - 2 * margin)
+    pts = []
+    for i in range(1, len(cps) - 2):
+        p0, p1, p2, p3 = cps[i - 1], cps[i], cps[i + 1], cps[i + 2]
+        for t in np.linspace(0, 1, 400, endpoint=False):
+            t2, t3 = t * t, t * t * t
+            pts.append(0.5 * (2 * p1 + (-p0 + p2) * t + (2 * p0 - 5 * p1 + 4 * p2 - p3) * t2 +
+                              (-p0 + 3 * p1 - 3 * p2 + p3) * t3))
+    pts = np.asarray(pts)
+    seg = np.linalg.norm(np.diff(pts, axis=0), axis=1)
+    arc = np.concatenate([[0.0], np.cumsum(seg)])
+    s = np.arange(nframes) * step
+    out_p, out_d = [], []
+    for si in s:
+        j = min(np.searchsorted(arc, si), len(pts) - 2)
+        d = pts[j + 1] - pts[j]
+        out_p.append(np.array([pts[j][0], pts[j][1], height]))
+        out_d.append(d / np.linalg.norm(d))
+    return out_p, out_d
+
+
+def make_streaming(n_global=5_000_000, nframes=100, scale=1.0, seeds=48, mix=3, device=None):
+    """Config 3: 1200x680 (fx = fy = 600, principal point at the centre: SURVEY Appendix B.5),
+    100 frames 0.05 m apart on a seeded spline through a 60 x 60 x 9 m volume, n_global records
+    uniform in it, record voxel 0.01 m with a 2^24-slot table (Appendix B.6), active radius 6 m,
+    d_s = 32, K = 256, D = 1024, 10 iterations per frame. ``scale`` < 1 shrinks the image and
+    the record count (tests)."""
+    W, H, fx = 1200, 680, 600.0
+    if scale != 1.0:
+        W, H, fx = max(32, int(W * scale)), max(32, int(H * scale)), fx * scale
+        n_global = max(1000, int(n_global * scale * scale))
+    ds, K, df = 32, 256, 1024
+    rng = np.random.default_rng(seed_for(3))
+    intr = Intr(fx, fx, W / 2, H / 2, W, H)
+    lo, hi = (0.0, 0.0, 0.0), (60.0, 60.0, 9.0)
+    m = random_map(rng, n_global, lo, hi, ds)
+    recs = np.concatenate([m.positions, m.rotations, m.colors, m.log_scales, m.opacity_logits[:, None],
+                           m.features], axis=1).astype(np.float32)
+    del m
+    atoms = rng.standard_normal((K, df))
+    atoms /= np.linalg.norm(atoms, axis=1, keepdims=True)
+    atoms = atoms.astype(np.float32)
+    proj = rng.standard_normal((ds, df)).astype(np.float32)
+    temperature = float(np.float32(math.sqrt(ds)))
+    pos, dirs = spline_path(rng, nframes, 0.05, lo, hi)
+    poses = [(look_quat(d), tuple(float(v) for v in p)) for p, d in zip(pos, dirs)]
+    assigns, feats = [], []
+    for _ in range(nframes):
+        assigns.append(voronoi_assignment(rng, W, H, seeds, device).reshape(H, W))
+        feats.append(cell_embeddings(rng, atoms, seeds, mix))
+    lambdas = dict(lambda_l2=0.0, lambda_i2=0.0, lambda_trust=0.1, softmax_temp=temperature)
+    return Streaming(intr, np.ascontiguousarray(recs), atoms, proj, temperature, poses, assigns, feats,
+                     lambdas=lambdas, name=f"cfg3-{nframes}f-{W}x{H}-G{n_global}-d32-K256-D1024"
+                     + ("" if scale == 1.0 else f"-scale{scale}"))

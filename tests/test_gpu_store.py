@@ -109,3 +109,45 @@ def test_sync_sequence_matches(ctx):
         assert np.array_equal(d_out.cpu().numpy().view(np.uint32), r_out.view(np.uint32))
         assert np.array_equal(s.records()[0].view(np.uint32), o.records().view(np.uint32))
         act, org = r_out, r_org
+
+
+def test_streaming_session_loop_matches_oracle_store(ctx):
+    """Config-3 loop at reduced scale: per frame store sync of the session's optimised active
+    set -> row import -> Stage-I steps. The active set (row order, origins, kept masks) must match
+    the oracle store's sync run on the same rows bit for bit, and the steps must stay finite.
+    An odd active count exercises the session's block alignment."""
+    from paper_2602_12314_b200 import synthetic
+
+    st = synthetic.make_streaming(n_global=1_000_000, nframes=3, scale=0.2, device="cuda")  # 40k records
+    intr = api.make_intrinsics(st.intr.fx, st.intr.fy, st.intr.cx, st.intr.cy, st.intr.width, st.intr.height)
+    store = api.Store(ctx, st.capacity, 32)
+    ostore = oracle.Store(st.capacity, 32)
+    store.insert_global(st.records, st.voxel_size)
+    ostore.insert_global(st.records, st.voxel_size)
+    cfg = api.default_config(**st.lambdas)
+    cfg.decoder_precision = 1
+    s = api.Session(ctx, cfg, 0, 32, 256, 1024, intr)
+    s.set_dictionary(st.atoms, st.atoms, st.proj)
+    origin = np.zeros(0, np.int64)
+    ncount = []
+    for f, (q, t) in enumerate(st.poses):
+        rows = s.export_rows() if s.n else None
+        host_rows = rows.cpu().numpy() if rows is not None else np.zeros((0, 46), np.float32)
+        dirty = np.ones(len(origin), np.uint8)
+        d_out, org, kept, stats = store.sync(rows, origin, dirty, np.asarray(t, np.float32), st.radius, st.voxel_size)
+        o_out, o_org, o_kept, o_stats = ostore.sync(host_rows, origin, dirty, np.asarray(t, np.float32), st.radius,
+                                                     st.voxel_size)
+        assert np.array_equal(org, o_org) and np.array_equal(kept, np.asarray(o_kept, bool))
+        assert np.array_equal(d_out.cpu().numpy(), o_out)
+        s.import_rows(d_out.contiguous(), kept=kept if len(origin) else None)
+        origin = org
+        ncount.append(s.n)
+        h, w = st.intr.height, st.intr.width
+        rgb = np.full((h, w, 3), 0.5, np.float32)
+        dep = np.full((h, w), 3.0, np.float32)
+        s.set_frames([synthetic.Frame(q, t, rgb, dep, st.assignments[f], st.features[f])])
+        s.set_batch(1)
+        for _ in range(2):
+            loss = s.step(read=True)
+        assert np.isfinite(loss["total"])
+    assert min(ncount) > 0
