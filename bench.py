@@ -82,6 +82,21 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def ncu_traffic():
+    """Per-launch DRAM bytes of each phase's kernels from the committed ncu --set full capture
+    (profiles/ncu_traffic.json, written by tools/ncu_traffic.py), or {} when absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            k = json.load(f)["kernels"]
+    except Exception:
+        return {}
+    out = {}
+    for v in k.values():
+        if v.get("phase"):
+            out[v["phase"]] = out.get(v["phase"], 0.0) + v["bytes_per_launch"]
+    return out
+
+
 # ----------------------------------------------------------------------------- workload
 def gpu_render_fn(ctx):
     import torch
@@ -435,6 +450,7 @@ def main():
     for ph in per_launch:
         per_launch[ph]["share"] = phases[ph][0] / total_ph
     rb = raster_bytes(n, float(np.mean(vis)), float(np.mean(pairs)), H, W, ds)
+    traffic = ncu_traffic()
     roof = None
     if per_launch:
         dom = max(per_launch, key=lambda p: phases[p][0])
@@ -443,13 +459,13 @@ def main():
             fl = decoder_flops_executed(H * W, K, ds) + 2.0 * H * W * K * (ds + 64)  # + DEC2 S recompute, Bm
             roof = {"kernel": "decoder (fused feature loss + backward, factored algebra)", "bound": "tensor",
                     "achieved": fl / t_launch / 1e12, "peak": bf16_sus, "unit": "TFLOP/s",
-                    "frac": fl / t_launch / 1e12 / bf16_sus, "traffic": None,
+                    "frac": fl / t_launch / 1e12 / bf16_sus, "traffic": traffic.get("decoder"),
                     "algorithmic_per_launch": fl, "peak_source": f"{src} bf16 sustained",
                     "algorithmic_equiv_tflops": decoder_flops_algorithmic(H * W, K, ds, D) / t_launch / 1e12}
         elif dom in rb:
             by = rb[dom]
             roof = {"kernel": dom, "bound": "hbm", "achieved": by / t_launch / 1e9, "peak": hbm, "unit": "GB/s",
-                    "frac": by / t_launch / 1e9 / hbm, "traffic": None, "algorithmic_per_launch": by,
+                    "frac": by / t_launch / 1e9 / hbm, "traffic": traffic.get(dom), "algorithmic_per_launch": by,
                     "peak_source": f"{src} HBM copy"}
         else:
             roof = {"kernel": dom, "bound": "hbm", "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None,
