@@ -29,7 +29,7 @@ def main():
             for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                 b += float(d[k]) * scale[dict(zip(h, units))[k]]
             tu = dict(zip(h, units))["gpu__time_duration.sum"]
-            us = float(d["gpu__time_duration.sum"]) * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}[tu]
+            us = float(d["gpu__time_duration.sum"]) * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}[tu]
             per_kernel.setdefault(name, []).append((b, us))
     res = {"source": reps, "kernels": {}}
     for name, v in per_kernel.items():
