@@ -952,9 +952,6 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
   float T = 1.f;
   {
     float uc0 = 0.f, uc1 = 0.f, uc2 = 0.f, uz = 0.f;
-    float uq[DSP];
-#pragma unroll
-    for (int c = 0; c < DSP; ++c) uq[c] = 0.f;
     if (inside) {
       if (a.d_color) {
         uc0 = a.d_color[3 * p];
@@ -962,10 +959,6 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
         uc2 = a.d_color[3 * p + 2];
       }
       if (a.d_depth) uz = a.d_depth[p];
-      if (a.d_query) {
-#pragma unroll
-        for (int c = 0; c < DSP; ++c) uq[c] = c < a.ds ? a.d_query[p * a.ds + c] : 0.f;
-      }
       last = a.px_last[p];
       T = a.px_T[p];
     }
@@ -974,9 +967,28 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
     s_u[uidx(tid, 2)] = uc2;
     s_u[uidx(tid, 3)] = uz;
 #pragma unroll
-    for (int c = 0; c < DSP; ++c) s_u[uidx(tid, 4 + c)] = uq[c];
-#pragma unroll
     for (int c = 4 + DSP; c < NU; ++c) s_u[uidx(tid, c)] = 0.f;
+    // query gradients: the tile's 16 pixel rows are contiguous runs of 16 * ds floats, read
+    // cooperatively (coalesced 16-byte loads when ds % 4 == 0)
+    const bool vq = a.d_query && (a.ds & 3) == 0 && (reinterpret_cast<uintptr_t>(a.d_query) & 15) == 0;
+    if (vq) {
+      const int q4 = a.ds / 4;
+      for (int i = tid; i < kTilePixels * (DSP / 4); i += kTilePixels) {
+        const int pl = i / (DSP / 4), c4 = i % (DSP / 4);
+        const int qx = tx0 + (pl % kTile), qy = ty0 + (pl / kTile);
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (c4 < q4 && qx < a.width && qy < a.height)
+          v = reinterpret_cast<const float4*>(a.d_query)[((size_t)qy * a.width + qx) * q4 + c4];
+        s_u[uidx(pl, 4 + 4 * c4)] = v.x;
+        s_u[uidx(pl, 5 + 4 * c4)] = v.y;
+        s_u[uidx(pl, 6 + 4 * c4)] = v.z;
+        s_u[uidx(pl, 7 + 4 * c4)] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < DSP; ++c)
+        s_u[uidx(tid, 4 + c)] = (inside && a.d_query && c < a.ds) ? a.d_query[p * a.ds + c] : 0.f;
+    }
   }
   const int warp_last = __reduce_max_sync(0xffffffffu, last);
   const int sy0 = ty0 + 2 * warp;  // this warp's pixel strip: rows sy0, sy0 + 1; columns tx0 .. tx0 + 15
@@ -1222,52 +1234,67 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
       }
     }
     __syncthreads();
-    // ---- cross-warp sum over the active warps
+    // ---- cross-warp sum over the active warps (fixed entries per thread)
     {
       int wm = 0;
 #pragma unroll
       for (int w8 = 0; w8 < 8; ++w8) wm |= s_wact[w8] << w8;
-      for (int e = tid; e < kBwdBatch * NACC; e += blockDim.x) {
-        const int j = e / NACC, c = e % NACC;
-        float v = 0.f;
 #pragma unroll
-        for (int w8 = 0; w8 < 8; ++w8)
-          if (wm & (1 << w8)) v += s_wbase[w8 * 3 * kBwdBatch * WP + j * PP + c];
-        s_acc[e] = v;
+      for (int k = 0; k < (kBwdBatch * NACC + kTilePixels - 1) / kTilePixels; ++k) {
+        const int e = tid + k * kTilePixels;
+        if (e < kBwdBatch * NACC) {
+          const int j = e / NACC, c = e % NACC;
+          float v = 0.f;
+#pragma unroll
+          for (int w8 = 0; w8 < 8; ++w8)
+            if (wm & (1 << w8)) v += s_wbase[w8 * 3 * kBwdBatch * WP + j * PP + c];
+          s_acc[e] = v;
+        }
       }
     }
     __syncthreads();
-    // ---- per-splat closed forms + global accumulation
-    for (int e = tid; e < cnt * 16; e += blockDim.x) {
-      const int j = e >> 4, k = e & 15;
-      const float* ac = s_acc + j * NACC;
-      const float* row = raw + j * RP;
-      const size_t src = __float_as_uint(row[15]);
-      if (k < 7) {
-        // moments M0..M5 (k-th column of the drho rows) -> dmean, dA, dz, dg
-        const float up = row[0] - ((float)tx0 + 7.5f), vp = row[1] - ((float)ty0 + 7.5f);
-        const float* M = ac + NU;
-        const float sdx = M[1] - up * M[0], sdy = M[2] - vp * M[0];
-        float val = 0.f;
-        switch (k) {
-          case 0: val = -2.f * (row[4] * sdx + row[5] * sdy); break;
-          case 1: val = -2.f * (row[6] * sdx + row[7] * sdy); break;
-          case 2: val = M[3] - 2.f * up * M[1] + up * up * M[0]; break;
-          case 3: val = M[4] - vp * M[1] - up * M[2] + up * vp * M[0]; break;
-          case 4: val = M[5] - 2.f * vp * M[2] + vp * vp * M[0]; break;
-          case 5: val = ac[3]; break;           // dz = sum w uz
-          case 6: val = ac[NU + 8]; break;      // dg = sum dg (row block 2, column 0)
+    // ---- per-splat closed forms + global accumulation: per splat 2 x float4 geometry
+    // (dmean, dA, dz, dg), 3 colour and ds/4 x float4 feature reductions (vector REDs)
+    {
+      constexpr int SL = 5 + DSP / 4;  // slots per splat
+      const bool vf = (a.ds & 3) == 0 && (reinterpret_cast<uintptr_t>(a.g_feat) & 15) == 0;
+      for (int e = tid; e < cnt * SL; e += blockDim.x) {
+        const int j = e / SL, k = e % SL;
+        const float* ac = s_acc + j * NACC;
+        const float* row = raw + j * RP;
+        const size_t src = __float_as_uint(row[15]);
+        if (k < 2) {
+          // moments M0..M5 of the drho rows -> dmean_u, dmean_v, dA00, dA01 | dA11, dz, dg
+          const float up = row[0] - ((float)tx0 + 7.5f), vp = row[1] - ((float)ty0 + 7.5f);
+          const float* M = ac + NU;
+          float4 v;
+          if (k == 0) {
+            const float sdx = M[1] - up * M[0], sdy = M[2] - vp * M[0];
+            v = make_float4(-2.f * (row[4] * sdx + row[5] * sdy), -2.f * (row[6] * sdx + row[7] * sdy),
+                            M[3] - 2.f * up * M[1] + up * up * M[0], M[4] - vp * M[1] - up * M[2] + up * vp * M[0]);
+          } else {
+            v = make_float4(M[5] - 2.f * vp * M[2] + vp * vp * M[0], ac[3], ac[NU + 8], 0.f);
+          }
+          if (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f)
+            atomicAdd(reinterpret_cast<float4*>(a.geo_acc + src * 8) + k, v);
+        } else if (k < 5) {
+          const float val = ac[k - 2];
+          if (val != 0.f) atomicAdd(&a.g_col[src * 3 + (k - 2)], val);
+        } else {
+          const int c0 = 4 * (k - 5);
+          if (c0 < a.ds) {
+            const float4 v = make_float4(ac[4 + c0], ac[5 + c0], ac[6 + c0], ac[7 + c0]);
+            if (vf) {
+              if (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f)
+                atomicAdd(reinterpret_cast<float4*>(a.g_feat + src * a.ds + c0), v);
+            } else {
+              const float vv[4] = {v.x, v.y, v.z, v.w};
+              for (int c = 0; c < 4 && c0 + c < a.ds; ++c)
+                if (vv[c] != 0.f) atomicAdd(&a.g_feat[src * a.ds + c0 + c], vv[c]);
+            }
+          }
         }
-        if (val != 0.f) atomicAdd(&a.geo_acc[src * 8 + k], val);
-      } else if (k < 10) {
-        const float val = ac[k - 7];
-        if (val != 0.f) atomicAdd(&a.g_col[src * 3 + (k - 7)], val);
       }
-    }
-    for (int e = tid; e < cnt * a.ds; e += blockDim.x) {
-      const int j = e / a.ds, c = e % a.ds;
-      const float val = s_acc[j * NACC + 4 + c];
-      if (val != 0.f) atomicAdd(&a.g_feat[(size_t)__float_as_uint(raw[j * RP + 15]) * a.ds + c], val);
     }
   }
 }

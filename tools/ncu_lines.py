@@ -14,6 +14,7 @@ def main():
     ap.add_argument("rep")
     ap.add_argument("kernel")
     ap.add_argument("--top", type=int, default=40)
+    ap.add_argument("--regions", default="", help="name:first-last,... line ranges of the kernel's file to total")
     a = ap.parse_args()
     txt = subprocess.run(["ncu", "-i", a.rep, "--page", "source", "--csv", "--print-source", "cuda,sass",
                           "-k", "regex:" + a.kernel], capture_output=True, text=True).stdout
@@ -39,6 +40,14 @@ def main():
     print(f"# {a.kernel}: {te:.3e} warp instructions, {ts:.0f} stall samples")
     for e, s, loc, src in sorted(out, key=lambda x: -x[1])[: a.top]:
         print(f"{100 * e / te:5.1f}% inst {100 * s / ts:5.1f}% stall  {loc:>16s}  {src}")
+    if a.regions:
+        print("# regions")
+        for spec in a.regions.split(","):
+            name, rng = spec.split(":")
+            lo, hi = (int(x) for x in rng.split("-"))
+            e = sum(x[0] for x in out if lo <= int(x[2].split(":")[-1]) <= hi)
+            st = sum(x[1] for x in out if lo <= int(x[2].split(":")[-1]) <= hi)
+            print(f"{100 * e / te:5.1f}% inst {100 * st / ts:5.1f}% stall  {name} ({lo}-{hi})")
 
 
 if __name__ == "__main__":
