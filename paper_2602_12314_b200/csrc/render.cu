@@ -512,6 +512,12 @@ __global__ void __launch_bounds__(kSortThreads, 2) tile_sort_kernel(const int32_
     for (int i = threadIdx.x; i < n; i += blockDim.x) g[i] = src[i];
 }
 
+// Pixel `pl` (0..255) of a 16x16 tile in the blend kernels: warp w = pl / 32 covers an 8x4 pixel
+// block (w & 1: left/right half, w / 2: 4-row band), lane i = pl % 32 pixel (i % 8, i / 8) of it.
+// Square-ish warp footprints meet fewer splat bboxes than 16x2 strips and waste fewer lanes.
+__device__ __forceinline__ int tile_dx(int pl) { return ((pl >> 5) & 1) * 8 + (pl & 7); }
+__device__ __forceinline__ int tile_dy(int pl) { return (pl >> 6) * 4 + ((pl >> 3) & 3); }
+
 struct RasterArgs {
   const SplatRec* rec;
   const float* colors;
@@ -688,7 +694,7 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_fwd_mma_kernel(RasterAr
   const int g = lane >> 2, cq = lane & 3;
   const int tile = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
   const int tx0 = (tile % a.tiles_x) * kTile, ty0 = (tile / a.tiles_x) * kTile;
-  const int px = tx0 + (tid % kTile), py = ty0 + (tid / kTile);
+  const int px = tx0 + tile_dx(tid), py = ty0 + tile_dy(tid);
   const bool inside = px < a.width && py < a.height;
   const int start = a.offset[tile], end = a.offset[tile + 1];
   if (tid == 0) s_max = 0;
@@ -861,7 +867,7 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_fwd_mma_kernel(RasterAr
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh) {
       const int pl = 32 * warp + 16 * mt + g + 8 * hh;
-      const int qx = tx0 + (pl % kTile), qy = ty0 + (pl / kTile);
+      const int qx = tx0 + tile_dx(pl), qy = ty0 + tile_dy(pl);
       if (qx < a.width && qy < a.height) {
         float* qo = a.query + ((size_t)qy * a.width + qx) * a.ds;
 #pragma unroll
@@ -887,7 +893,7 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_fwd_mma_kernel(RasterAr
 // and the drho moments  sum drho * [1, x, y, x^2, xy, y^2]  (+ sum dg), from which
 // dmean and dA (render.cpp:345-352) follow per splat in closed form.
 // Batches are staged with cp.async one batch ahead (record, colour, features of 16 splats,
-// issued by 16 lanes of warp 0), and a warp whose 16x2 pixel strip meets none of the batch's
+// issued by 16 lanes of warp 0), and a warp whose 8x4 pixel block meets none of the batch's
 // bboxes, or whose pixels all stopped before the batch, skips the batch entirely.
 template <int DSP>
 __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArgs a) {
@@ -916,7 +922,7 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tile = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
   const int tx0 = (tile % a.tiles_x) * kTile, ty0 = (tile / a.tiles_x) * kTile;
-  const int px = tx0 + (tid % kTile), py = ty0 + (tid / kTile);
+  const int px = tx0 + tile_dx(tid), py = ty0 + tile_dy(tid);
   const bool inside = px < a.width && py < a.height;
   const int start = a.offset[tile];
   const int tend = start + a.tile_max_last[tile];
@@ -975,7 +981,7 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
       const int q4 = a.ds / 4;
       for (int i = tid; i < kTilePixels * (DSP / 4); i += kTilePixels) {
         const int pl = i / (DSP / 4), c4 = i % (DSP / 4);
-        const int qx = tx0 + (pl % kTile), qy = ty0 + (pl / kTile);
+        const int qx = tx0 + tile_dx(pl), qy = ty0 + tile_dy(pl);
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
         if (c4 < q4 && qx < a.width && qy < a.height)
           v = reinterpret_cast<const float4*>(a.d_query)[((size_t)qy * a.width + qx) * q4 + c4];
@@ -991,7 +997,8 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
     }
   }
   const int warp_last = __reduce_max_sync(0xffffffffu, last);
-  const int sy0 = ty0 + 2 * warp;  // this warp's pixel strip: rows sy0, sy0 + 1; columns tx0 .. tx0 + 15
+  // this warp's pixel block: columns bx0 .. bx0 + 7, rows by0 .. by0 + 3
+  const int bx0 = tx0 + (warp & 1) * 8, by0 = ty0 + (warp >> 1) * 4;
   // MMA lane coordinates
   const int g = lane >> 2, cq = lane & 3;
   // B fragments of the pixel moment matrix X[p][q] = [1, x', y', x'^2, x'y', y'^2, 0, 0] for the
@@ -1002,7 +1009,7 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh) {
       const int pl = 32 * warp + 8 * ks + cq + 4 * hh;  // tile-linear pixel of this B element (row k)
-      const float xx = (float)(pl % kTile) - 7.5f, yy = (float)(pl / kTile) - 7.5f;
+      const float xx = (float)tile_dx(pl) - 7.5f, yy = (float)tile_dy(pl) - 7.5f;
       float v = 0.f;
       switch (g) {  // column n = g
         case 0: v = 1.f; break;
@@ -1068,13 +1075,13 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
       }
     }
     __syncthreads();
-    // ---- warp activity: some pixel of the strip still blends at this batch and some bbox meets it
+    // ---- warp activity: some pixel of the block still blends at this batch and some bbox meets it
     bool act = (lo - start) < warp_last;
     if (act) {
       bool meets = false;
       if (lane < cnt) {
         const int4 bb = f4_as_i4(s_sp[lane][2]);
-        meets = bb.x <= tx0 + kTile - 1 && bb.y >= tx0 && bb.z <= sy0 + 1 && bb.w >= sy0;
+        meets = bb.x <= bx0 + 7 && bb.y >= bx0 && bb.z <= by0 + 3 && bb.w >= by0;
       }
       act = __any_sync(0xffffffffu, meets);
     }
