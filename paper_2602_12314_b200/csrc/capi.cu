@@ -557,6 +557,11 @@ struct FrameDev {
   float* feats = nullptr;
   size_t c_px = 0, c_feat = 0;
   int64_t n_set = 0, n_sup = 0;
+  // segment mode (objective.cpp:37-64): assignment rows present in the frame, ascending
+  int32_t* seg_rows = nullptr;    // n_sup: assignment row of each supervision row
+  int32_t* seg_of = nullptr;      // n_set: supervision row of an assignment row (-1 = absent)
+  float* seg_inv = nullptr;       // n_sup: 1 / pixels of the segment
+  size_t c_seg = 0;
   latmap_pose pose{};
   float rcw[9], rwc[9];
 };
@@ -582,6 +587,8 @@ struct latmap_session {
   std::vector<RenderBufs> rw;
   std::vector<float*> color, depth, query, alpha;
   float *d_color = nullptr, *d_depth = nullptr, *d_query = nullptr, *ssim_scratch = nullptr;
+  float *seg_q = nullptr, *seg_dq = nullptr;  // segment mode: pooled rows and their gradients
+  int64_t seg_cap = 0;
   DecoderWork dec;
   double* partials = nullptr;
   int32_t part_frames = 0;
@@ -687,6 +694,39 @@ latmap_status session_alloc_frames(latmap_session* s, int nf) {
   return LATMAP_OK;
 }
 
+// ---- segment supervision (objective.cpp:37-64, 147-157): mean rendered query per present
+// assignment row, and the per-pixel share of the row gradient
+__global__ void seg_pool_kernel(const float* __restrict__ query, const int32_t* __restrict__ assign, int64_t npx,
+                                int ds, const int32_t* __restrict__ seg_of, float* __restrict__ qsum) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < npx * ds;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = e / ds;
+    const int a = assign[p];
+    if (a < 0) continue;
+    atomicAdd(&qsum[(size_t)seg_of[a] * ds + (e % ds)], query[e]);
+  }
+}
+__global__ void seg_mean_kernel(float* q, const float* __restrict__ inv, int64_t rows, int ds) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rows * ds;
+       e += (int64_t)gridDim.x * blockDim.x)
+    q[e] *= inv[e / ds];
+}
+__global__ void seg_scatter_kernel(const float* __restrict__ dq, const int32_t* __restrict__ assign, int64_t npx,
+                                   int ds, const int32_t* __restrict__ seg_of, const float* __restrict__ inv,
+                                   float* __restrict__ d_query) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < npx * ds;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = e / ds;
+    const int a = assign[p];
+    float v = 0.f;
+    if (a >= 0) {
+      const int r = seg_of[a];
+      v = dq[(size_t)r * ds + (e % ds)] * inv[r];
+    }
+    d_query[e] = v;
+  }
+}
+
 // One total_objective over the session's keyframes (objective.cpp:67-194). map_grads = false
 // skips the image-loss gradients and the render backward (ObjectiveOptions::map_grads);
 // use_cache skips the render when the per-frame images still hold renders of the current map
@@ -756,7 +796,24 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
     set_double_kernel<<<1, 1, 0, st>>>(part + 7, (double)f.n_sup);
     count_launch();
     const bool have_sup = f.n_sup > 0;
-    if (have_sup) {
+    if (have_sup && c.segment_mode) {
+      // pooled rows: Q_r = mean of the rendered queries over segment r; the decoder runs on the
+      // n_sup rows (targets = features[seg_rows[r]]), then d_query[p] = dQ_r / |segment r|
+      s->begin(3);
+      const unsigned gq = (unsigned)std::min<int64_t>((npx * s->ds + 255) / 256, 148 * 16);
+      CTX_CHECK(ctx, cudaMemsetAsync(s->seg_q, 0, sizeof(float) * f.n_sup * s->ds, st));
+      seg_pool_kernel<<<gq, 256, 0, st>>>(s->query[b], f.assign, npx, s->ds, f.seg_of, s->seg_q);
+      seg_mean_kernel<<<(unsigned)((f.n_sup * s->ds + 255) / 256), 256, 0, st>>>(s->seg_q, f.seg_inv, f.n_sup, s->ds);
+      count_launch(2);
+      decoder_frame(st, s->dec, s->seg_q, f.seg_rows, f.n_sup, f.feats, f.n_set, f.n_sup, atoms, proj,
+                    c.softmax_temp, c.lambda_cos, c.lambda_l2, c.lambda_feat * inv_b, want_grad, s->seg_dq, g_proj,
+                    g_atoms, part);
+      if (want_grad) {
+        seg_scatter_kernel<<<gq, 256, 0, st>>>(s->seg_dq, f.assign, npx, s->ds, f.seg_of, f.seg_inv, s->d_query);
+        count_launch();
+      }
+      s->end();
+    } else if (have_sup) {
       s->begin(3);
       if (c.decoder_precision == 1 && decoder_tc_supported(s->k, s->ds, f.n_set))
         decoder_frame_tc(st, s->dec, s->query[b], f.assign, npx, f.feats, f.n_set, f.n_sup, atoms, proj,
@@ -857,7 +914,6 @@ latmap_status latmap_session_create(latmap_ctx* ctx, const latmap_config* cfg, i
   if (!ctx || !cfg || !intr || !out || n < 0 || ds < 1 || k < 1 || df < 1) return LATMAP_ERR_INVALID_ARGUMENT;
   if (!intr_valid(*intr)) return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "render: invalid intrinsics");
   if (ds > 64) return fail(ctx, LATMAP_ERR_UNSUPPORTED, "query_dim must be <= 64");
-  if (cfg->segment_mode) return fail(ctx, LATMAP_ERR_UNSUPPORTED, "segment supervision is not on the device path yet");
   if (!(cfg->softmax_temp > 0.f)) return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "reconstruct: temperature must be > 0");
   auto* s = new latmap_session();
   s->ctx = ctx;
@@ -939,7 +995,9 @@ latmap_status latmap_session_destroy(latmap_session* s) {
   for (auto* p : s->depth) cudaFree(p);
   for (auto* p : s->query) cudaFree(p);
   for (auto* p : s->alpha) cudaFree(p);
+  if (s->seg_q) cudaFree(s->seg_q), cudaFree(s->seg_dq);
   for (auto& f : s->frames) {
+    if (f.seg_rows) cudaFree(f.seg_rows), cudaFree(f.seg_of), cudaFree(f.seg_inv);
     if (f.rgb) cudaFree(f.rgb);
     if (f.depth) cudaFree(f.depth);
     if (f.assign) cudaFree(f.assign);
@@ -1031,6 +1089,40 @@ latmap_status latmap_session_set_frames(latmap_session* s, int32_t nf, const lat
       amax = a > amax ? a : amax;
     }
     if (amax >= in.n_set) return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "gather_supervision: assignment out of range");
+    if (s->cfg.segment_mode) {
+      // present assignment rows in ascending order (objective.cpp:39-64)
+      std::vector<int64_t> cnt((size_t)std::max<int64_t>(in.n_set, 1), 0);
+      for (size_t p = 0; p < npx; ++p)
+        if (in.assignment[p] >= 0) ++cnt[(size_t)in.assignment[p]];
+      std::vector<int32_t> rows, of((size_t)std::max<int64_t>(in.n_set, 1), -1);
+      std::vector<float> inv;
+      for (int64_t a = 0; a < in.n_set; ++a)
+        if (cnt[(size_t)a] > 0) {
+          of[(size_t)a] = (int32_t)rows.size();
+          rows.push_back((int32_t)a);
+          inv.push_back(1.f / (float)cnt[(size_t)a]);
+        }
+      const size_t need = (size_t)std::max<int64_t>(in.n_set, 1);
+      if (need > f.c_seg) {
+        if (f.seg_rows) cudaFree(f.seg_rows), cudaFree(f.seg_of), cudaFree(f.seg_inv);
+        CTX_CHECK(ctx, cudaMalloc(&f.seg_rows, sizeof(int32_t) * need));
+        CTX_CHECK(ctx, cudaMalloc(&f.seg_of, sizeof(int32_t) * need));
+        CTX_CHECK(ctx, cudaMalloc(&f.seg_inv, sizeof(float) * need));
+        f.c_seg = need;
+      }
+      if (!rows.empty()) {
+        CTX_CHECK(ctx, cudaMemcpy(f.seg_rows, rows.data(), sizeof(int32_t) * rows.size(), cudaMemcpyHostToDevice));
+        CTX_CHECK(ctx, cudaMemcpy(f.seg_inv, inv.data(), sizeof(float) * inv.size(), cudaMemcpyHostToDevice));
+      }
+      CTX_CHECK(ctx, cudaMemcpy(f.seg_of, of.data(), sizeof(int32_t) * need, cudaMemcpyHostToDevice));
+      nsup = (int64_t)rows.size();
+      if ((int64_t)need > s->seg_cap) {
+        if (s->seg_q) cudaFree(s->seg_q), cudaFree(s->seg_dq);
+        CTX_CHECK(ctx, cudaMalloc(&s->seg_q, sizeof(float) * need * s->ds));
+        CTX_CHECK(ctx, cudaMalloc(&s->seg_dq, sizeof(float) * need * s->ds));
+        s->seg_cap = (int64_t)need;
+      }
+    }
     f.n_sup = nsup;
     f.n_set = in.n_set;
   }

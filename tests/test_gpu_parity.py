@@ -442,3 +442,28 @@ def test_export_import_rows_keep_and_append(ctx, cfg0):
     _moved_like("positions", after["positions"], nm.positions, g2.positions, 1e-4, 2)
     _moved_like("features", after["features"], nm.features, g2.features, 2.5e-3, 2)
     _moved_like("colors", after["colors"], nm.colors, g2.colors, 2.5e-3, 2)
+
+
+def test_session_segment_supervision_config0(ctx, cfg0):
+    """feature_supervision = "segment" (objective.cpp:37-64, 147-157): queries pooled per present
+    assignment row, the row gradient shared equally by the segment's pixels."""
+    w = cfg0
+    s = make_session(ctx, w, segment_mode=1, decoder_precision=0)
+    loss = s.objective(want_grad=True)
+    d = oracle.Dictionary(w.atoms.copy(), w.anchor.copy(), w.proj.copy(), np.float32(w.temperature))
+    cfg = oracle_cfg(w)
+    cfg.segment_mode = True
+    ref, (g, dp, da) = oracle.total_objective(to_oracle_map(w.map), d, oracle_frames(w), oi(w.intr), cfg,
+                                              threads=THREADS)
+    assert loss["supervised_rows"] == ref["supervised_rows"] == len(np.unique(w.frames[0].assignment[
+        w.frames[0].assignment >= 0]))
+    for key in ("l_rgb", "l_depth", "l_cos", "l_l2", "l_trust", "total"):
+        assert loss[key] == pytest.approx(ref[key], rel=2e-4, abs=1e-6), key
+    gb = s.grad_buffer().cpu().numpy()
+    n, ds = w.map.n, w.map.features.shape[1]
+    offs = np.cumsum([0, 3 * n, 4 * n, 3 * n, 3 * n, n, ds * n, ds * w.proj.shape[1], w.atoms.size])
+    blocks = [g.positions, g.rotations, g.colors, g.log_scales, g.opacity_logits, g.features]
+    for i, (name, ref_b) in enumerate(zip(oracle.FIELDS, blocks)):
+        assert_close_floor(gb[offs[i]:offs[i + 1]], ref_b.reshape(-1), 1e-3, name)
+    for name, got, r in (("d_proj", gb[offs[6]:offs[7]], dp), ("d_atoms", gb[offs[7]:offs[8]], da)):
+        assert_close_floor(got, r.reshape(-1), 1e-3, name)
