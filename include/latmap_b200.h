@@ -214,6 +214,9 @@ latmap_status latmap_session_objective(latmap_session* s, int32_t want_grad, lat
 latmap_status latmap_session_apply(latmap_session* s);
 /* objective + apply; `out` may be NULL. */
 latmap_status latmap_session_step(latmap_session* s, latmap_loss_breakdown* out);
+/* Steps are captured once into a CUDA graph and replayed while frames, batch settings and the
+ * row set are unchanged (default on; off while phase profiling). */
+latmap_status latmap_session_set_graphs(latmap_session* s, int32_t enable);
 /* total_objective with ObjectiveOptions (objective.hpp:33-43): map_grads = 0 skips the image-loss
  * gradients and render_backward; use_cached_renders = 1 reuses the session's per-frame renders
  * when the map has not changed since they were produced (cached_renders / render_sink). */

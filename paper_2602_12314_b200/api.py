@@ -336,6 +336,10 @@ class Session:
                                                             int(use_cached_renders), C.byref(out) if read else None))
         return out.as_dict() if read else None
 
+    def set_graphs(self, enable=True):
+        """Replay captured CUDA graphs of the Stage-I step (default on)."""
+        check(self.ctx.h, lib().latmap_session_set_graphs(self.h, int(bool(enable))))
+
     def step_dict(self, read=True):
         """One Stage-II iteration (pipeline.cpp:250-259): cached renders, dictionary-only Adam."""
         out = LossBreakdown()

@@ -5,6 +5,7 @@
 
 #include <atomic>
 #include <cmath>
+#include <array>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -595,6 +596,17 @@ struct latmap_session {
   latmap_loss_breakdown* d_loss = nullptr;
   // the per-frame images hold renders of the current map (ObjectiveOptions::cached_renders)
   bool renders_valid = false;
+  // CUDA graph of one Stage-I step (objective + Adam), replayed while the launch sequence and its
+  // arguments (frame poses, buffer pointers, sizes) are unchanged
+  cudaGraphExec_t step_graph = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  int64_t graph_launches = 0;
+  bool graph_exact = false;
+  bool use_graph = true;
+  void drop_graph() {
+    if (step_graph) cudaGraphExecDestroy(step_graph);
+    step_graph = nullptr;
+  }
   // phase timing with CUDA events on the session stream (bench.py roofline evidence)
   struct Span {
     int phase;
@@ -897,6 +909,7 @@ bool session_fix_overflow(latmap_session* s) {
   int64_t of = 0;
   cudaMemcpy(&of, s->overflow, sizeof(of), cudaMemcpyDeviceToHost);
   if (!of) return false;
+  s->drop_graph();  // buffers move
   for (int b = 0; b < s->nframes; ++b) {
     int64_t cnt[4];
     cudaMemcpy(cnt, s->rw[b].w.counters, sizeof(cnt), cudaMemcpyDeviceToHost);
@@ -981,6 +994,8 @@ latmap_status latmap_session_create(latmap_ctx* ctx, const latmap_config* cfg, i
 latmap_status latmap_session_destroy(latmap_session* s) {
   if (!s) return LATMAP_ERR_INVALID_ARGUMENT;
   cudaStreamSynchronize(s->ctx->stream);
+  s->drop_graph();
+  if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
   for (void* p : {(void*)s->params, (void*)s->grads, (void*)s->m, (void*)s->v, (void*)s->anchor, (void*)s->steps,
                   (void*)s->skipped, (void*)s->overflow, (void*)s->flags, (void*)s->corr1, (void*)s->corr2,
                   (void*)s->d_color, (void*)s->d_depth, (void*)s->d_query, (void*)s->ssim_scratch, (void*)s->partials,
@@ -1056,9 +1071,20 @@ latmap_status latmap_session_get_dictionary(latmap_session* s, float* atoms, flo
 latmap_status latmap_session_set_frames(latmap_session* s, int32_t nf, const latmap_frame* frames) {
   if (!s || nf < 1 || !frames) return fail(s ? s->ctx : nullptr, LATMAP_ERR_INVALID_ARGUMENT, "total_objective: empty batch");
   latmap_ctx* ctx = s->ctx;
+  // the captured step graph bakes in frame poses (camera constants are kernel arguments),
+  // buffer pointers and per-frame sizes: any change drops it
+  bool same = s->nframes == nf && (int)s->frames.size() >= nf;
+  std::vector<std::array<void*, 4>> ptrs0;
+  for (int b = 0; same && b < nf; ++b) {
+    const FrameDev& f = s->frames[b];
+    same = std::memcmp(&f.pose, &frames[b].pose, sizeof(latmap_pose)) == 0 && f.n_set == frames[b].n_set;
+    ptrs0.push_back({(void*)f.rgb, (void*)f.depth, (void*)f.assign, (void*)f.feats});
+  }
   latmap_status st = session_alloc_frames(s, nf);
   if (st != LATMAP_OK) return st;
   const size_t npx = (size_t)s->intr.width * s->intr.height;
+  std::vector<int64_t> nsup0;
+  for (int b = 0; same && b < nf; ++b) nsup0.push_back(s->frames[b].n_sup);
   for (int b = 0; b < nf; ++b) {
     const latmap_frame& in = frames[b];
     FrameDev& f = s->frames[b];
@@ -1128,6 +1154,12 @@ latmap_status latmap_session_set_frames(latmap_session* s, int32_t nf, const lat
   }
   s->nframes = nf;
   s->renders_valid = false;  // poses may differ
+  for (int b = 0; same && b < nf; ++b) {
+    const FrameDev& f = s->frames[b];
+    same = ptrs0[b] == std::array<void*, 4>{(void*)f.rgb, (void*)f.depth, (void*)f.assign, (void*)f.feats} &&
+           nsup0[b] == f.n_sup;
+  }
+  if (!same) s->drop_graph();
   // per-frame decoder buffers sized by the largest embedding table
   int64_t max_set = 1;
   for (int b = 0; b < nf; ++b) max_set = std::max(max_set, s->frames[b].n_set);
@@ -1143,6 +1175,7 @@ latmap_status latmap_session_set_frames(latmap_session* s, int32_t nf, const lat
 
 latmap_status latmap_session_set_batch(latmap_session* s, int32_t global_batch, int32_t add_trust) {
   if (!s || global_batch < 0) return LATMAP_ERR_INVALID_ARGUMENT;
+  if (s->global_batch != global_batch || s->add_trust != add_trust) s->drop_graph();
   s->global_batch = global_batch;
   s->add_trust = add_trust;
   return session_alloc_frames(s, std::max(1, s->nframes));
@@ -1150,6 +1183,7 @@ latmap_status latmap_session_set_batch(latmap_session* s, int32_t global_batch, 
 
 latmap_status latmap_session_set_slot_offset(latmap_session* s, int32_t offset) {
   if (!s || offset < 0) return LATMAP_ERR_INVALID_ARGUMENT;
+  if (s->slot_offset != offset) s->drop_graph();
   s->slot_offset = offset;
   return LATMAP_OK;
 }
@@ -1172,12 +1206,74 @@ latmap_status latmap_session_apply(latmap_session* s) {
   return post_launch(s->ctx);
 }
 
+// Capture (objective + Adam) into s->step_graph. Requires sized tile buffers (a prior step).
+static latmap_status session_capture_step(latmap_session* s) {
+  latmap_ctx* ctx = s->ctx;
+  s->drop_graph();
+  // capture on a private non-blocking stream (the context's stream may be the legacy default
+  // stream, which cannot be captured); the graph is then launched on the context's stream
+  if (!s->cap_stream) CTX_CHECK(ctx, cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking));
+  cudaStream_t saved = ctx->stream;
+  // order the capture after everything already queued on the context stream
+  CTX_CHECK(ctx, cudaStreamSynchronize(saved));
+  ctx->stream = s->cap_stream;
+  cudaGraph_t g = nullptr;
+  const int64_t l0 = g_launches.load();
+  cudaError_t e = cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) {
+    ctx->stream = saved;
+    CTX_CHECK(ctx, e);
+  }
+  latmap_status rs = session_objective(s, true);
+  if (rs == LATMAP_OK) session_adam(s);
+  e = cudaStreamEndCapture(s->cap_stream, &g);
+  ctx->stream = saved;
+  const int64_t captured = g_launches.load() - l0;
+  g_launches.fetch_sub(captured);  // captured, not executed
+  if (rs != LATMAP_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rs;
+  }
+  CTX_CHECK(ctx, e);
+  e = cudaGraphInstantiate(&s->step_graph, g, 0);
+  cudaGraphDestroy(g);
+  CTX_CHECK(ctx, e);
+  s->graph_launches = captured;
+  s->graph_exact = ctx->exact_blend;
+  return LATMAP_OK;
+}
+
+static bool session_sized(const latmap_session* s) {
+  for (int b = 0; b < s->nframes; ++b)
+    if (s->rw[b].w.pair_cap <= 1) return false;
+  return true;
+}
+
+latmap_status latmap_session_set_graphs(latmap_session* s, int32_t enable) {
+  if (!s) return LATMAP_ERR_INVALID_ARGUMENT;
+  s->use_graph = enable != 0;
+  if (!s->use_graph) s->drop_graph();
+  return LATMAP_OK;
+}
+
 latmap_status latmap_session_step(latmap_session* s, latmap_loss_breakdown* out) {
   if (!s || s->nframes < 1) return LATMAP_ERR_INVALID_ARGUMENT;
   for (int attempt = 0; attempt < 3; ++attempt) {
-    latmap_status st = session_objective(s, true);
-    if (st != LATMAP_OK) return st;
-    session_adam(s);  // no-op on device when a tile buffer overflowed
+    latmap_status st = LATMAP_OK;
+    if (s->use_graph && !s->prof && session_sized(s)) {
+      if (s->step_graph && s->graph_exact != s->ctx->exact_blend) s->drop_graph();
+      if (!s->step_graph) {
+        st = session_capture_step(s);
+        if (st != LATMAP_OK) return st;
+      }
+      CTX_CHECK(s->ctx, cudaGraphLaunch(s->step_graph, s->ctx->stream));
+      count_launch((int)s->graph_launches);
+      s->renders_valid = false;
+    } else {
+      st = session_objective(s, true);
+      if (st != LATMAP_OK) return st;
+      session_adam(s);  // no-op on device when a tile buffer overflowed
+    }
     if (!out) return post_launch(s->ctx);
     st = session_assemble(s, out);
     if (st != LATMAP_OK) return st;
@@ -1334,6 +1430,7 @@ latmap_status latmap_session_import_rows(latmap_session* s, const float* d_rows,
   s->total = total;
   for (auto& r : s->rw) r.release();  // re-sized for the new N on the next objective
   s->renders_valid = false;
+  s->drop_graph();
   return LATMAP_OK;
 }
 

@@ -467,3 +467,26 @@ def test_session_segment_supervision_config0(ctx, cfg0):
         assert_close_floor(gb[offs[i]:offs[i + 1]], ref_b.reshape(-1), 1e-3, name)
     for name, got, r in (("d_proj", gb[offs[6]:offs[7]], dp), ("d_atoms", gb[offs[7]:offs[8]], da)):
         assert_close_floor(got, r.reshape(-1), 1e-3, name)
+
+
+def test_graph_replay_matches_direct_steps(ctx, cfg0):
+    """Steps replayed from the captured CUDA graph equal directly launched steps (up to the
+    run-to-run rounding of the atomic gradient sums), and a pose change re-captures."""
+    w = cfg0
+    a = make_session(ctx, w)
+    b = make_session(ctx, w)
+    b.set_graphs(False)
+    for _ in range(3):
+        la = a.step(read=True)
+        lb = b.step(read=True)
+    assert la["total"] == pytest.approx(lb["total"], rel=1e-5)
+    ma, mb = a.get_map(), b.get_map()
+    for f in oracle.FIELDS:
+        assert np.allclose(ma[f], mb[f], rtol=1e-5, atol=1e-6), f
+    # move the camera: the graph must not replay the old pose
+    fr = w.frames[0]
+    moved = synthetic.Frame(synthetic.yaw_quat(0.05), (0.02, 0.0, 0.0), fr.rgb, fr.depth, fr.assignment, fr.features)
+    a.set_frames([moved])
+    b.set_frames([moved])
+    la, lb = a.step(read=True), b.step(read=True)
+    assert la["total"] == pytest.approx(lb["total"], rel=1e-5)
