@@ -274,12 +274,25 @@ inline int grid_for(int64_t n, int per_block, int cap = 148 * 32) {
 
 }  // namespace
 
+// zero an M x N block of a row-major matrix with leading dimension ldc (one launch)
+__global__ void zero_block_kernel(float* C, int64_t M, int64_t N, int64_t ldc) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < M * N; e += (int64_t)gridDim.x * blockDim.x)
+    C[(e / N) * ldc + e % N] = 0.f;
+}
+static void zero_block(cudaStream_t st, float* C, int64_t M, int64_t N, int64_t ldc) {
+  if (ldc == N) {
+    cudaMemsetAsync(C, 0, sizeof(float) * M * N, st);
+  } else {
+    zero_block_kernel<<<(unsigned)std::min<int64_t>((M * N + 255) / 256, 1184), 256, 0, st>>>(C, M, N, ldc);
+    count_launch();
+  }
+}
+
 void sgemm(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, float alpha, const float* A,
            int64_t lda, const float* B, int64_t ldb, float beta, float* C, int64_t ldc, int split) {
   if (M <= 0 || N <= 0) return;
   if (K <= 0) {
-    if (split <= 1 && beta == 0.f)
-      for (int64_t i = 0; i < M; ++i) cudaMemsetAsync(C + i * ldc, 0, sizeof(float) * N, st);
+    if (split <= 1 && beta == 0.f) zero_block(st, C, M, N, ldc);
     return;
   }
   const int64_t gx = (N + BN - 1) / BN, gy = (M + BM - 1) / BM;
@@ -289,8 +302,7 @@ void sgemm(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, f
   if (split == 1 && gx * gy < 148 && K >= 256 && (beta == 0.f || beta == 1.f)) {
     const int64_t want = (296 + gx * gy - 1) / (gx * gy);
     split = (int)std::max<int64_t>(1, std::min<int64_t>(want, K / 128));
-    if (split > 1 && beta == 0.f)
-      for (int64_t i = 0; i < M; ++i) cudaMemsetAsync(C + i * ldc, 0, sizeof(float) * N, st);
+    if (split > 1 && beta == 0.f) zero_block(st, C, M, N, ldc);
   }
   const int64_t kchunk = ((K + split - 1) / split + BK - 1) / BK * BK;
   const int gz = (int)((K + kchunk - 1) / kchunk);

@@ -160,6 +160,69 @@ __global__ void __launch_bounds__(256) ssim_v_kernel(const float* __restrict__ h
   block_add_double(acc, sum_out);
 }
 
+// SSIM value only (no gradient requested): both separable passes fused per 32x8 output tile
+// with a 5-pixel reflect-101 halo in shared memory, the same per-pixel float expressions as
+// ssim_h_kernel + ssim_v_kernel (so the same values), one pass over the two images.
+constexpr int kSTX = 32, kSTY = 8, kSHX = kSTX + 2 * kRad, kSHY = kSTY + 2 * kRad;
+__global__ void __launch_bounds__(256) ssim_fused_kernel(const float* __restrict__ a, const float* __restrict__ b,
+                                                         int h, int w, int ch, SsimKernel K, double* sum_out) {
+  __shared__ float s_a[kSHY][kSHX], s_b[kSHY][kSHX];
+  __shared__ float s_h[5][kSHY][kSTX];
+  const float c1 = 0.01f * 0.01f, c2 = 0.03f * 0.03f;
+  const int x0 = blockIdx.x * kSTX, y0 = blockIdx.y * kSTY;
+  const int tid = threadIdx.x;
+  double acc = 0.0;
+  for (int c = 0; c < ch; ++c) {
+    for (int i = tid; i < kSHY * kSHX; i += blockDim.x) {
+      const int yy = i / kSHX, xx = i % kSHX;
+      const int gy = refl(min(y0 - kRad + yy, h - 1 + kRad), h), gx = refl(min(x0 - kRad + xx, w - 1 + kRad), w);
+      const int64_t q = ((int64_t)gy * w + gx) * ch + c;
+      s_a[yy][xx] = a[q];
+      s_b[yy][xx] = b[q];
+    }
+    __syncthreads();
+    for (int i = tid; i < kSHY * kSTX; i += blockDim.x) {
+      const int yy = i / kSTX, xx = i % kSTX;
+      float s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0;
+#pragma unroll
+      for (int k = -kRad; k <= kRad; ++k) {
+        const float av = s_a[yy][xx + kRad + k], bv = s_b[yy][xx + kRad + k], kw = K.k[k + kRad];
+        s0 += kw * av;
+        s1 += kw * bv;
+        s2 += kw * (av * av);
+        s3 += kw * (bv * bv);
+        s4 += kw * (av * bv);
+      }
+      s_h[0][yy][xx] = s0;
+      s_h[1][yy][xx] = s1;
+      s_h[2][yy][xx] = s2;
+      s_h[3][yy][xx] = s3;
+      s_h[4][yy][xx] = s4;
+    }
+    __syncthreads();
+    {
+      const int yy = tid / kSTX, xx = tid % kSTX;
+      const int y = y0 + yy, x = x0 + xx;
+      if (y < h && x < w) {
+        float q[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+        for (int k = -kRad; k <= kRad; ++k) {
+          const float kw = K.k[k + kRad];
+#pragma unroll
+          for (int t = 0; t < 5; ++t) q[t] += kw * s_h[t][yy + kRad + k][xx];
+        }
+        const float mx = q[0], my = q[1];
+        const float sx2 = q[2] - mx * mx, sy2 = q[3] - my * my, sxy = q[4] - mx * my;
+        const float a1 = 2.f * mx * my + c1, a2 = 2.f * sxy + c2;
+        const float b1 = mx * mx + my * my + c1, b2 = sx2 + sy2 + c2;
+        acc += (double)((a1 * a2) / (b1 * b2));
+      }
+    }
+    __syncthreads();
+  }
+  block_add_double(acc, sum_out);
+}
+
 // Adjoint of one separable pass along an axis (filter_plane_adjoint, losses.cpp:57-75),
 // in gather form: out[i'] = sum over preimages i of refl with refl(i) == i'.
 __device__ __forceinline__ float adj_gather(const float* in, int64_t stride, int len, int ip, const SsimKernel& K) {
@@ -269,6 +332,12 @@ void ssim_run(cudaStream_t st, const float* a, const float* b, int h, int w, int
   const int64_t n = (int64_t)h * w;
   if (h < kWin || w < kWin) {
     ssim_global_kernel<<<1, 256, 0, st>>>(a, b, h, w, ch, d_a, out_scale, accumulate, sum_out);
+    count_launch();
+    return;
+  }
+  if (!d_a) {
+    ssim_fused_kernel<<<dim3((w + kSTX - 1) / kSTX, (h + kSTY - 1) / kSTY), kSTX * kSTY, 0, st>>>(a, b, h, w, ch, K,
+                                                                                              sum_out);
     count_launch();
     return;
   }
