@@ -124,7 +124,10 @@ struct RenderBufs {
       c_px = px;
     }
     if ((e = dgrow(w.counters, c_cnt, 4))) return e;
-    if ((e = dgrow(geo_acc, c_geo, n1 * 8))) return e;
+    if (n1 * 8 > c_geo || !geo_acc) {
+      if ((e = dgrow(geo_acc, c_geo, n1 * 8))) return e;
+      if ((e = cudaMemset(geo_acc, 0, sizeof(float) * n1 * 8))) return e;
+    }
     w.n_cap = n;
     return cudaSuccess;
   }
@@ -837,7 +840,7 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
       s->end();
     }
     if (map_grad) {
-      CTX_CHECK(ctx, cudaMemsetAsync(rb.geo_acc, 0, sizeof(float) * 8 * s->n, st));
+      // geo_acc is zero here: zeroed at allocation, and project_bwd re-zeroes every entry it reads
       s->begin(4);
       render_backward(st, map, f.rcw, f.rwc, f.pose.translation, in, rb.w, s->d_color, s->d_depth,
                       have_sup ? s->d_query : nullptr, rb.geo_acc, gmap, false);

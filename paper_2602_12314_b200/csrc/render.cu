@@ -645,6 +645,7 @@ struct RasterBwdArgs {
   float* g_col;    // N x 3
   float* g_feat;   // N x ds
   const int32_t* order;
+  const int64_t* counters;
 };
 
 constexpr int kBwdBatch = 16;  // splats per batch (one MMA M tile)
@@ -924,6 +925,7 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
   const int tx0 = (tile % a.tiles_x) * kTile, ty0 = (tile / a.tiles_x) * kTile;
   const int px = tx0 + tile_dx(tid), py = ty0 + tile_dy(tid);
   const bool inside = px < a.width && py < a.height;
+  if (a.counters[2]) return;  // tile lists overflowed: the step is discarded and re-run
   const int start = a.offset[tile];
   const int tend = start + a.tile_max_last[tile];
   if (tend <= start) return;
@@ -1319,18 +1321,30 @@ struct ProjBwdArgs {
 __global__ void __launch_bounds__(256) project_bwd_kernel(ProjBwdArgs a) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= a.map.n) return;
+  const float4* rv = reinterpret_cast<const float4*>(a.rec + i);
   const int4 bb = reinterpret_cast<const int4*>(a.rec + i)[2];
   if (bb.x > bb.y) return;
-  float* acc = a.geo_acc + 8 * i;
-  float ac[7];
-#pragma unroll
-  for (int c = 0; c < 7; ++c) {
-    ac[c] = acc[c];
-    acc[c] = 0.f;
-  }
-  const float* p = a.map.pos + 3 * i;
-  const float* q = a.map.rot + 4 * i;
-  const float* ls = a.map.lsc + 3 * i;
+  // 16-byte loads of the record, the accumulators (then re-zeroed for the next frame) and the
+  // quaternion; everything is issued before the math
+  const float4 r0 = rv[0], r1 = rv[1];
+  float4* acc4 = reinterpret_cast<float4*>(a.geo_acc + 8 * i);
+  const float4 g0 = acc4[0], g1 = acc4[1];
+  acc4[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+  acc4[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float ac[7] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z};
+  const float pv[3] = {a.map.pos[3 * i], a.map.pos[3 * i + 1], a.map.pos[3 * i + 2]};
+  const float4 q4 = (reinterpret_cast<uintptr_t>(a.map.rot) & 15) == 0
+                        ? reinterpret_cast<const float4*>(a.map.rot)[i]
+                        : make_float4(a.map.rot[4 * i], a.map.rot[4 * i + 1], a.map.rot[4 * i + 2], a.map.rot[4 * i + 3]);
+  const float lv[3] = {a.map.lsc[3 * i], a.map.lsc[3 * i + 1], a.map.lsc[3 * i + 2]};
+  const float* p = pv;
+  const float q[4] = {q4.x, q4.y, q4.z, q4.w};
+  const float* ls = lv;
+  // the gradient read-modify-writes: loads issued here, independent of the math below
+  const float go = a.grads.opa[i];
+  const float gl[3] = {a.grads.lsc[3 * i], a.grads.lsc[3 * i + 1], a.grads.lsc[3 * i + 2]};
+  const float gr[4] = {a.grads.rot[4 * i], a.grads.rot[4 * i + 1], a.grads.rot[4 * i + 2], a.grads.rot[4 * i + 3]};
+  const float gp[3] = {a.grads.pos[3 * i], a.grads.pos[3 * i + 1], a.grads.pos[3 * i + 2]};
   const float d0 = p[0] - a.o[0], d1 = p[1] - a.o[1], d2 = p[2] - a.o[2];
   float pc[3];
   for (int r = 0; r < 3; ++r) pc[r] = a.rcw[3 * r] * d0 + a.rcw[3 * r + 1] * d1 + a.rcw[3 * r + 2] * d2;
@@ -1352,11 +1366,9 @@ __global__ void __launch_bounds__(256) project_bwd_kernel(ProjBwdArgs a) {
   const float x = pc[0], y = pc[1], z = pc[2];
   const float fx = a.fx, fy = a.fy;
   const float J[6] = {fx / z, 0.f, -fx * x / (z * z), 0.f, fy / z, -fy * y / (z * z)};
-  const SplatRec s = a.rec[i];
-  const float A[4] = {s.a00, s.a01, s.a10, s.a11};
-  // cov_cam for d_jac; cov_inv from the forward record (identical values)
-  const float alpha = s.alpha;
-  a.grads.opa[i] += ac[6] * alpha * (1.f - alpha);
+  const float A[4] = {r1.x, r1.y, r1.z, r1.w};  // cov_inv from the forward record (identical values)
+  const float alpha = r0.w;
+  a.grads.opa[i] = go + ac[6] * alpha * (1.f - alpha);
   const float dA[4] = {ac[2], ac[3], ac[3], ac[4]};
   float t1[4], dc[4];
   for (int r = 0; r < 2; ++r)
@@ -1383,7 +1395,7 @@ __global__ void __launch_bounds__(256) project_bwd_kernel(ProjBwdArgs a) {
     for (int c = 0; c < 3; ++c)
       drg[3 * r + c] = (a.rcw[r] * dm_[c] + a.rcw[3 + r] * dm_[3 + c] + a.rcw[6 + r] * dm_[6 + c]) * sc[c];
   for (int c = 0; c < 3; ++c)
-    a.grads.lsc[3 * i + c] += (rcg[c] * dm_[c] + rcg[3 + c] * dm_[3 + c] + rcg[6 + c] * dm_[6 + c]) * sc[c];
+    a.grads.lsc[3 * i + c] = gl[c] + (rcg[c] * dm_[c] + rcg[3 + c] * dm_[3 + c] + rcg[6 + c] * dm_[6 + c]) * sc[c];
   const float dw[9] = {0.f, -qz, qy, qz, 0.f, -qx, -qy, qx, 0.f};
   const float dxm[9] = {0.f, qy, qz, qy, -2.f * qx, -qw, qz, qw, -2.f * qx};
   const float dym[9] = {-2.f * qy, qx, qw, qx, 0.f, qz, -qw, qz, -2.f * qy};
@@ -1398,7 +1410,7 @@ __global__ void __launch_bounds__(256) project_bwd_kernel(ProjBwdArgs a) {
   for (int r = 0; r < 4; ++r) dq[r] *= 2.f;
   const float qh[4] = {qw, qx, qy, qz};
   const float qd = qh[0] * dq[0] + qh[1] * dq[1] + qh[2] * dq[2] + qh[3] * dq[3];
-  for (int r = 0; r < 4; ++r) a.grads.rot[4 * i + r] += (dq[r] - qh[r] * qd) / qn;
+  for (int r = 0; r < 4; ++r) a.grads.rot[4 * i + r] = gr[r] + (dq[r] - qh[r] * qd) / qn;
   float dp[3] = {0.f, 0.f, 0.f};
   const float z2 = z * z, z3 = z2 * z;
   dp[0] += ac[0] * fx / z;
@@ -1409,7 +1421,8 @@ __global__ void __launch_bounds__(256) project_bwd_kernel(ProjBwdArgs a) {
   dp[1] += djac[5] * (-fy / z2);
   dp[2] += djac[0] * (-fx / z2) + djac[2] * (2.f * fx * x / z3) + djac[4] * (-fy / z2) + djac[5] * (2.f * fy * y / z3);
   dp[2] += ac[5];
-  for (int r = 0; r < 3; ++r) a.grads.pos[3 * i + r] += a.rwc[3 * r] * dp[0] + a.rwc[3 * r + 1] * dp[1] + a.rwc[3 * r + 2] * dp[2];
+  for (int r = 0; r < 3; ++r)
+    a.grads.pos[3 * i + r] = gp[r] + (a.rwc[3 * r] * dp[0] + a.rwc[3 * r + 1] * dp[1] + a.rwc[3 * r + 2] * dp[2]);
 }
 
 // project_gaussian (render.cpp:118-132): one Gaussian, returns cov2d (not its inverse).
@@ -1557,7 +1570,7 @@ void render_backward(cudaStream_t st, const MapPtrs& map, const float rot_cw[9],
   const int ntiles = w.tiles_x * w.tiles_y;
   RasterBwdArgs a{w.rec, map.col, map.feat, map.ds, w.tile_offset, w.keys, w.tiles_x, intr.width, intr.height,
                   w.px_last, w.px_T, w.tile_max_last, d_color, d_depth, d_query, geo_acc, grads.col, grads.feat,
-                  w.tile_order};
+                  w.tile_order, w.counters};
   switch (pad_ds(map.ds)) {
     case 4: launch_bwd<4>(st, ntiles, a); break;
     case 8: launch_bwd<8>(st, ntiles, a); break;
