@@ -235,6 +235,16 @@ latmap_status latmap_session_export_rows(latmap_session* s, float* d_rows);
 latmap_status latmap_session_import_rows(latmap_session* s, const float* d_rows, int64_t n_new, const uint8_t* kept,
                                          int64_t n_kept);
 int64_t latmap_session_size(const latmap_session* s);
+/* seed_gaussians (pipeline.cpp:39-73) for frame b against a render of the current map: the
+ * stride-2 pixels with observed depth > 0 whose rendered alpha < 0.5 or |rendered - observed
+ * depth| > 0.1, in raster order, written as AoS rows (features zero: the reference draws them
+ * from the pipeline's std::mt19937_64, see latmap_b200.hpp seed_gaussians) into d_rows (cap
+ * rows; d_rows = NULL only counts). */
+latmap_status latmap_session_seed_candidates(latmap_session* s, int32_t b, float* d_rows, int64_t cap,
+                                             int64_t* count);
+/* ActiveSet::append_newborns: append n_rows device AoS rows (features replaced by h_features,
+ * n_rows x query_dim host floats, when given) with zero Adam moments. */
+latmap_status latmap_session_append_rows(latmap_session* s, float* d_rows, int64_t n_rows, const float* h_features);
 /* Flat device buffers: [positions|rotations|colors|log_scales|opacity|features|proj|atoms]
  * gradient layout (for the multi-GPU all-reduce) and the loss-partials vector. */
 latmap_status latmap_session_grad_buffer(latmap_session* s, float** grads, int64_t* count);

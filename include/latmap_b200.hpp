@@ -9,6 +9,8 @@
 // std::invalid_argument, LATMAP_ERR_STALE_CACHE -> std::runtime_error, anything else ->
 // latmap_b200::device_error. Device buffers are caller-owned raw pointers (any allocator).
 #pragma once
+#include <algorithm>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -173,6 +175,20 @@ class Session {
     check(latmap_session_import_rows(h_, d_rows, n_new, kept ? kept->data() : nullptr, nk), ctx_->get());
   }
   int64_t size() const { return latmap_session_size(h_); }
+  // seed_gaussians + append_newborns (pipeline.cpp:39-73, 224-230): candidates on the device,
+  // features ~ N(0, 0.01) drawn here from the pipeline's generator in row order (as the reference
+  // does); d_scratch must hold the frame's stride-2 grid rows ((W/2) x (H/2) x (14 + query_dim)).
+  template <class Rng>
+  int64_t seed_gaussians(int32_t frame, int32_t query_dim, Rng& rng, float* d_scratch, int64_t scratch_rows) {
+    int64_t n = 0;
+    check(latmap_session_seed_candidates(h_, frame, d_scratch, scratch_rows, &n), ctx_->get());
+    n = std::min(n, scratch_rows);
+    std::normal_distribution<float> gauss(0.0f, 0.01f);
+    std::vector<float> feats((size_t)n * query_dim);
+    for (auto& v : feats) v = gauss(rng);
+    check(latmap_session_append_rows(h_, d_scratch, n, feats.data()), ctx_->get());
+    return n;
+  }
   latmap_session* get() const { return h_; }
 
  private:

@@ -124,6 +124,8 @@ def _declare(L):
         "latmap_session_objective_ex": [P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(LossBreakdown)],
         "latmap_session_step_dict": [P, C.POINTER(LossBreakdown)],
         "latmap_session_set_graphs": [P, C.c_int32],
+        "latmap_session_seed_candidates": [P, C.c_int32, P, C.c_int64, C.POINTER(C.c_int64)],
+        "latmap_session_append_rows": [P, P, C.c_int64, P],
         "latmap_session_export_rows": [P, P],
         "latmap_session_import_rows": [P, P, C.c_int64, P, C.c_int64],
         "latmap_session_grad_buffer": [P, C.POINTER(P), C.POINTER(C.c_int64)],
@@ -185,7 +187,7 @@ EXPORTED = ["latmap_ctx_create", "latmap_ctx_destroy", "latmap_ctx_set_stream", 
             "latmap_session_set_batch", "latmap_session_set_slot_offset", "latmap_session_objective",
             "latmap_session_apply", "latmap_session_step", "latmap_session_objective_ex", "latmap_session_step_dict",
             "latmap_session_export_rows", "latmap_session_import_rows", "latmap_session_size",
-            "latmap_session_set_graphs",
+            "latmap_session_set_graphs", "latmap_session_seed_candidates", "latmap_session_append_rows",
             "latmap_session_grad_buffer", "latmap_session_loss_buffer",
             "latmap_session_read_loss", "latmap_session_frame_images", "latmap_session_stats",
             "latmap_session_profile", "latmap_session_phase_times", "latmap_selftest_umma", "latmap_ctx_stream",

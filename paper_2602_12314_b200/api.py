@@ -365,6 +365,24 @@ class Session:
                                                            n_new, self._np_ptr(km), n_kept))
         self.n = n_new
 
+    def seed_candidates(self, frame=0):
+        """seed_gaussians (pipeline.cpp:39-73) rows for `frame` (features zero), device [n, 14 + ds]."""
+        w, h = self.intr.width, self.intr.height
+        cap = ((w + 1) // 2) * ((h + 1) // 2)
+        rows = torch.empty((cap, self.ROW + self.ds), dtype=torch.float32, device=f"cuda:{self.ctx.device}")
+        n = C.c_int64()
+        check(self.ctx.h, lib().latmap_session_seed_candidates(self.h, int(frame), C.c_void_p(rows.data_ptr()), cap,
+                                                               C.byref(n)))
+        return rows[:n.value]
+
+    def append_rows(self, rows, features=None):
+        """ActiveSet::append_newborns: append device AoS rows (features from host when given)."""
+        f = None if features is None else np.ascontiguousarray(features, np.float32)
+        r = rows.contiguous()
+        check(self.ctx.h, lib().latmap_session_append_rows(self.h, C.c_void_p(r.data_ptr()), int(r.shape[0]),
+                                                           self._np_ptr(f)))
+        self.n += int(r.shape[0])
+
     def read_loss(self):
         out = LossBreakdown()
         check(self.ctx.h, lib().latmap_session_read_loss(self.h, C.byref(out)))

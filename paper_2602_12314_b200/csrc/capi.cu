@@ -1439,6 +1439,128 @@ latmap_status latmap_session_import_rows(latmap_session* s, const float* d_rows,
 
 int64_t latmap_session_size(const latmap_session* s) { return s ? s->n : -1; }
 
+// ------------------------------------------------------------------ seeding (pipeline.cpp:39-73)
+namespace {
+constexpr int kSeedStride = 2;  // kStride
+struct SeedArgs {
+  const float *obs_depth, *alpha, *depth, *rgb;
+  int w, h, gw, gh;
+  float fx, fy, cx, cy, rwc[9], t[3];
+};
+__device__ __forceinline__ bool seed_cand(const SeedArgs& a, int i, int& x, int& y, float& z) {
+  y = (i / a.gw) * kSeedStride;
+  x = (i % a.gw) * kSeedStride;
+  const size_t p = (size_t)y * a.w + x;
+  z = a.obs_depth[p];
+  if (!(z > 0.f)) return false;
+  const float al = a.alpha[p], zr = a.depth[p];
+  return al < 0.5f || fabsf(fs(zr, z)) > 0.1f;  // kAlphaCovered, kDepthErr
+}
+__global__ void seed_count_kernel(SeedArgs a, int32_t* blk) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int x, y;
+  float z;
+  const bool c = i < a.gw * a.gh && seed_cand(a, i, x, y, z);
+  const int n = __syncthreads_count(c);
+  if (threadIdx.x == 0) blk[blockIdx.x] = n;
+}
+__global__ void seed_scan_kernel(int32_t* blk, int nb, int64_t* total) {
+  if (threadIdx.x == 0) {
+    int64_t run = 0;
+    for (int b = 0; b < nb; ++b) {
+      const int c = blk[b];
+      blk[b] = (int32_t)run;
+      run += c;
+    }
+    *total = run;
+  }
+}
+// rows in raster order of the stride-2 grid: [position | (1,0,0,0) | rgb | log(z/fx*2) x3 | 0 | 0...]
+__global__ void seed_write_kernel(SeedArgs a, const int32_t* blk, int ds, int64_t cap, float* rows) {
+  __shared__ int32_t s_w[32];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int x = 0, y = 0;
+  float z = 0.f;
+  const bool c = i < a.gw * a.gh && seed_cand(a, i, x, y, z);
+  const unsigned bal = __ballot_sync(0xffffffffu, c);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) s_w[wid] = __popc(bal);
+  __syncthreads();
+  int base = blk[blockIdx.x];
+  for (int w = 0; w < wid; ++w) base += s_w[w];
+  if (!c) return;
+  const int64_t r = base + __popc(bal & ((1u << lane) - 1u));
+  if (r >= cap) return;
+  float* o = rows + r * (14 + ds);
+  const float pc[3] = {fm(fd(fs((float)x, a.cx), a.fx), z), fm(fd(fs((float)y, a.cy), a.fy), z), z};
+  for (int k = 0; k < 3; ++k)
+    o[k] = fa(fa(fa(fm(a.rwc[3 * k], pc[0]), fm(a.rwc[3 * k + 1], pc[1])), fm(a.rwc[3 * k + 2], pc[2])), a.t[k]);
+  o[3] = 1.f, o[4] = 0.f, o[5] = 0.f, o[6] = 0.f;
+  const size_t p = (size_t)y * a.w + x;
+  o[7] = a.rgb[3 * p], o[8] = a.rgb[3 * p + 1], o[9] = a.rgb[3 * p + 2];
+  const float ls = __double2float_rn(log((double)fm(fd(z, a.fx), 2.f)));  // std::log(float), two-pixel footprint
+  o[10] = ls, o[11] = ls, o[12] = ls;
+  o[13] = 0.f;  // opacity logit 0 -> alpha 0.5
+  for (int k = 0; k < ds; ++k) o[14 + k] = 0.f;
+}
+}  // namespace
+
+latmap_status latmap_session_seed_candidates(latmap_session* s, int32_t b, float* d_rows, int64_t cap,
+                                             int64_t* count) {
+  if (!s || b < 0 || b >= s->nframes || !count) return LATMAP_ERR_INVALID_ARGUMENT;
+  latmap_ctx* ctx = s->ctx;
+  cudaStream_t st = ctx->stream;
+  const FrameDev& f = s->frames[b];
+  if (!s->renders_valid) {  // render(active map, kf.pose) right before seeding (pipeline.cpp:224-226)
+    latmap_status rs = latmap_session_objective_ex(s, 0, 0, 0, nullptr);
+    if (rs != LATMAP_OK) return rs;
+  }
+  SeedArgs a;
+  a.obs_depth = f.depth, a.alpha = s->alpha[b], a.depth = s->depth[b], a.rgb = f.rgb;
+  a.w = s->intr.width, a.h = s->intr.height;
+  a.gw = (a.w + kSeedStride - 1) / kSeedStride, a.gh = (a.h + kSeedStride - 1) / kSeedStride;
+  a.fx = s->intr.fx, a.fy = s->intr.fy, a.cx = s->intr.cx, a.cy = s->intr.cy;
+  for (int i = 0; i < 9; ++i) a.rwc[i] = f.rwc[i];
+  for (int i = 0; i < 3; ++i) a.t[i] = f.pose.translation[i];
+  const int nc = a.gw * a.gh, nb = (nc + 255) / 256;
+  int32_t* blk = nullptr;
+  int64_t* tot = nullptr;
+  CTX_CHECK(ctx, cudaMallocAsync(&blk, sizeof(int32_t) * std::max(nb, 1), st));
+  CTX_CHECK(ctx, cudaMallocAsync(&tot, sizeof(int64_t), st));
+  seed_count_kernel<<<nb, 256, 0, st>>>(a, blk);
+  seed_scan_kernel<<<1, 32, 0, st>>>(blk, nb, tot);
+  if (d_rows) seed_write_kernel<<<nb, 256, 0, st>>>(a, blk, s->ds, cap, d_rows);
+  count_launch(d_rows ? 3 : 2);
+  CTX_CHECK(ctx, cudaMemcpyAsync(count, tot, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CTX_CHECK(ctx, cudaFreeAsync(blk, st));
+  CTX_CHECK(ctx, cudaFreeAsync(tot, st));
+  CTX_CHECK(ctx, cudaStreamSynchronize(st));
+  return post_launch(ctx);
+}
+
+latmap_status latmap_session_append_rows(latmap_session* s, float* d_rows, int64_t n_rows, const float* h_features) {
+  if (!s || n_rows < 0 || (n_rows > 0 && !d_rows)) return LATMAP_ERR_INVALID_ARGUMENT;
+  latmap_ctx* ctx = s->ctx;
+  cudaStream_t st = ctx->stream;
+  const int rs = 14 + s->ds;
+  if (n_rows > 0 && h_features)
+    CTX_CHECK(ctx, cudaMemcpy2DAsync(d_rows + 14, sizeof(float) * rs, h_features, sizeof(float) * s->ds,
+                                     sizeof(float) * s->ds, (size_t)n_rows, cudaMemcpyHostToDevice, st));
+  // new map = current rows ++ appended rows; every current row keeps its moments
+  float* all = nullptr;
+  const int64_t n_old = s->n;
+  CTX_CHECK(ctx, cudaMalloc(&all, sizeof(float) * std::max<int64_t>((n_old + n_rows) * rs, 1)));
+  latmap_status r = latmap_session_export_rows(s, all);
+  if (r == LATMAP_OK && n_rows > 0)
+    r = cudaMemcpyAsync(all + n_old * rs, d_rows, sizeof(float) * n_rows * rs, cudaMemcpyDeviceToDevice, st) ==
+                cudaSuccess
+            ? LATMAP_OK
+            : LATMAP_ERR_CUDA;
+  if (r == LATMAP_OK) r = latmap_session_import_rows(s, all, n_old + n_rows, nullptr, n_old);
+  cudaFree(all);
+  return r;
+}
+
 latmap_status latmap_session_grad_buffer(latmap_session* s, float** grads, int64_t* count) {
   if (!s || !grads || !count) return LATMAP_ERR_INVALID_ARGUMENT;
   *grads = s->grads;

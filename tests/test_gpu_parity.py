@@ -490,3 +490,43 @@ def test_graph_replay_matches_direct_steps(ctx, cfg0):
     b.set_frames([moved])
     la, lb = a.step(read=True), b.step(read=True)
     assert la["total"] == pytest.approx(lb["total"], rel=1e-5)
+
+
+def test_seed_gaussians_candidates_and_append(ctx, cfg0):
+    """seed_gaussians (pipeline.cpp:39-73): stride-2 pixels with observed depth whose render leaves
+    them uncovered (alpha < 0.5) or misplaced (|depth error| > 0.1), in raster order, restated in
+    numpy float32 with the reference's op order; then append_newborns with zero moments."""
+    w = cfg0
+    s = make_session(ctx, w)
+    s.step(read=False)  # the map moved: seeding renders it again
+    rows = s.seed_candidates(0).cpu().numpy()
+    color, depth, _, alpha = [x.cpu().numpy() for x in s.frame_images(0)]
+    fr = w.frames[0]
+    f32 = np.float32
+    intr = w.intr
+    R = oracle.quat_to_rot(fr.pose_rot, np.float32)
+    t = np.asarray(fr.pose_trans, f32)
+    exp = []
+    for y in range(0, intr.height, 2):
+        for x in range(0, intr.width, 2):
+            z = fr.depth[y, x]
+            if not z > 0:
+                continue
+            if not (alpha[y, x] < f32(0.5) or abs(f32(depth[y, x] - z)) > f32(0.1)):
+                continue
+            pc = [f32(f32(f32(f32(x) - f32(intr.cx)) / f32(intr.fx)) * z),
+                  f32(f32(f32(f32(y) - f32(intr.cy)) / f32(intr.fy)) * z), z]
+            pos = [f32(f32(f32(R[k, 0] * pc[0]) + f32(R[k, 1] * pc[1])) + f32(R[k, 2] * pc[2])) + t[k]
+                   for k in range(3)]
+            ls = f32(np.log(np.float64(f32(f32(z / f32(intr.fx)) * f32(2.0)))))
+            exp.append(pos + [1, 0, 0, 0] + list(fr.rgb[y, x]) + [ls, ls, ls, 0] + [0] * w.map.features.shape[1])
+    exp = np.asarray(exp, f32)
+    assert rows.shape == exp.shape and rows.shape[0] > 0
+    assert np.array_equal(rows, exp)
+    n0 = s.n
+    feats = np.random.default_rng(3).normal(0, 0.01, (rows.shape[0], w.map.features.shape[1])).astype(f32)
+    s.append_rows(torch.from_numpy(rows).cuda(), feats)
+    assert s.n == n0 + rows.shape[0]
+    m = s.get_map()
+    assert np.array_equal(m["positions"][n0:], rows[:, :3]) and np.array_equal(m["features"][n0:], feats)
+    assert np.isfinite(s.step(read=True)["total"])
