@@ -77,7 +77,7 @@ def lib():
     if _lib is None:
         if not os.path.exists(LIB_PATH):
             raise ImportError(f"{LIB_PATH} not built: run __graft_entry__.build() (no CPU fallback exists)")
-        _lib = C.CDLL(LIB_PATH)
+        _lib = C.CDLL(os.environ.get("LATMAP_LIB", LIB_PATH))  # override: experiment builds only
         _declare(_lib)
     return _lib
 

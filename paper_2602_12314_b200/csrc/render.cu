@@ -1243,6 +1243,7 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
       }
     }
     __syncthreads();
+
     // ---- cross-warp sum over the active warps (fixed entries per thread)
     {
       int wm = 0;
