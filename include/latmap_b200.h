@@ -109,6 +109,12 @@ latmap_status latmap_ctx_synchronize(latmap_ctx* ctx);
  * products and sums in the reference's order (bit-exact images); 0 (default) = FMA accumulation
  * (images within 1e-6 relative). alpha', clamp and termination decisions are exact in both. */
 latmap_status latmap_ctx_set_exact_blend(latmap_ctx* ctx, int32_t exact);
+/* bf16 (tcgen05) decoder kernels: 0 = auto (fused on-chip DEC1/DEC2 when K in {128, 256},
+ * d_s = 32, n_set <= 64; else the staged DL1-DL5 path for K in {256..1024}, d_s in {32, 64},
+ * n_set <= 256; else fp32 SIMT), 1 = fused only, 2 = staged whenever it supports the shape.
+ * Replaces no reference interface (the reference has one fp32 CPU decoder,
+ * proj/src/dictionary.cpp:25-83); results agree within the bf16 tolerances either way. */
+latmap_status latmap_ctx_set_decoder_path(latmap_ctx* ctx, int32_t path);
 const char* latmap_ctx_last_error(const latmap_ctx* ctx);
 /* The cudaStream_t the context's calls are ordered on (as void*). */
 void* latmap_ctx_stream(const latmap_ctx* ctx);

@@ -152,6 +152,7 @@ struct latmap_ctx {
   std::string err;
   int64_t launches0 = 0;
   bool exact_blend = false;  // parity mode: separately rounded accumulation in the forward blend
+  int32_t decoder_path = 0;  // bf16 decoder: 0 auto, 1 fused on-chip (DEC1/DEC2), 2 staged (DL1-DL5)
 };
 
 struct latmap_render_cache {
@@ -253,6 +254,12 @@ latmap_status latmap_ctx_set_stream(latmap_ctx* ctx, void* stream) {
 latmap_status latmap_ctx_set_exact_blend(latmap_ctx* ctx, int32_t exact) {
   if (!ctx) return LATMAP_ERR_INVALID_ARGUMENT;
   ctx->exact_blend = exact != 0;
+  return LATMAP_OK;
+}
+
+latmap_status latmap_ctx_set_decoder_path(latmap_ctx* ctx, int32_t path) {
+  if (!ctx || path < 0 || path > 2) return LATMAP_ERR_INVALID_ARGUMENT;
+  ctx->decoder_path = path;
   return LATMAP_OK;
 }
 
@@ -605,6 +612,7 @@ struct latmap_session {
   cudaStream_t cap_stream = nullptr;
   int64_t graph_launches = 0;
   bool graph_exact = false;
+  int32_t graph_dec_path = 0;
   bool use_graph = true;
   void drop_graph() {
     if (step_graph) cudaGraphExecDestroy(step_graph);
@@ -787,6 +795,8 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
   }
   CTX_CHECK(ctx, cudaMemsetAsync(s->overflow, 0, sizeof(int64_t), st));
   decoder_prepare(st, s->dec, atoms, proj);
+  if (s->cfg.decoder_precision == 1 && (ctx->decoder_path == 2 || !decoder_tc_supported(s->k, s->ds, s->dec.nset_cap)))
+    decoder_dl_prepare(st, s->dec);  // M in the staged path's operand blocks
   for (int b = 0; b < nf; ++b) {
     FrameDev& f = s->frames[b];
     RenderBufs& rb = s->rw[b];
@@ -830,10 +840,15 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
       s->end();
     } else if (have_sup) {
       s->begin(3);
-      if (c.decoder_precision == 1 && decoder_tc_supported(s->k, s->ds, f.n_set))
+      const bool fused_ok = decoder_tc_supported(s->k, s->ds, f.n_set) && ctx->decoder_path != 2;
+      const bool staged_ok = s->dec.dl_mt && decoder_dl_supported(s->k, s->ds, f.n_set) && ctx->decoder_path != 1;
+      if (c.decoder_precision == 1 && fused_ok)
         decoder_frame_tc(st, s->dec, s->query[b], f.assign, npx, f.feats, f.n_set, f.n_sup, atoms, proj,
                          c.softmax_temp, c.lambda_cos, c.lambda_l2, c.lambda_feat * inv_b, want_grad, s->d_query,
                          g_proj, g_atoms, part);
+      else if (c.decoder_precision == 1 && staged_ok)
+        decoder_frame_dl(st, s->dec, s->query[b], f.assign, npx, f.feats, f.n_set, f.n_sup, atoms, c.softmax_temp,
+                         c.lambda_cos, c.lambda_l2, c.lambda_feat * inv_b, want_grad, s->d_query, g_atoms, part);
       else
         decoder_frame(st, s->dec, s->query[b], f.assign, npx, f.feats, f.n_set, f.n_sup, atoms, proj, c.softmax_temp,
                       c.lambda_cos, c.lambda_l2, c.lambda_feat * inv_b, want_grad, s->d_query, g_proj, g_atoms, part);
@@ -961,7 +976,8 @@ latmap_status latmap_session_create(latmap_ctx* ctx, const latmap_config* cfg, i
   d.k = k;
   d.ds = ds;
   d.df = df;
-  good = good && ok(cudaMalloc(&d.buf1, sizeof(float) * npx * k)) && ok(cudaMalloc(&d.buf2, sizeof(float) * npx * k)) &&
+  const size_t npx_t = (npx + 127) / 128 * 128;  // whole 128-row tiles (the staged path aliases buf1/buf2)
+  good = good && ok(cudaMalloc(&d.buf1, sizeof(float) * npx_t * k)) && ok(cudaMalloc(&d.buf2, sizeof(float) * npx_t * k)) &&
          ok(cudaMalloc(&d.alpha_r, sizeof(float) * npx)) && ok(cudaMalloc(&d.beta_r, sizeof(float) * npx)) &&
          ok(cudaMalloc(&d.kd, sizeof(float) * k * ds)) && ok(cudaMalloc(&d.mm, sizeof(float) * k * k)) &&
          ok(cudaMalloc(&d.r, sizeof(float) * ds * k)) && ok(cudaMalloc(&d.a, sizeof(float) * k * k));
@@ -973,6 +989,13 @@ latmap_status latmap_session_create(latmap_ctx* ctx, const latmap_config* cfg, i
            ok(cudaMalloc(&d.loss_part, sizeof(double) * 148 * 4)) &&
            ok(cudaMalloc(&d.e_tiles, (size_t)((npx + 127) / 128) * 128 * k * 2)) &&
            ok(cudaMalloc(&d.a_acc, sizeof(float) * k * k)) && ok(cudaMalloc(&d.r_acc, sizeof(float) * ds * k));
+    if (good && decoder_dl_supported(k, ds, 1)) {
+      d.dl_t = d.buf1;
+      d.dl_ae = reinterpret_cast<uint8_t*>(d.buf2);  // 128 x (K + NB) bf16 per tile <= 128 x K fp32
+      good = ok(cudaMalloc(&d.dl_mt, sizeof(uint16_t) * k * k)) &&
+             ok(cudaMalloc(&d.dl_nu, sizeof(float) * (k / 256) * npx_t)) &&
+             ok(cudaMalloc(&d.dl_part, sizeof(float) * decoder_dl_part_floats(k)));
+    }
   }
   if (!good) {
     t_err = "latmap_session_create: out of device memory";
@@ -1006,7 +1029,8 @@ latmap_status latmap_session_destroy(latmap_session* s) {
                   (void*)s->dec.kd, (void*)s->dec.mm, (void*)s->dec.gt, (void*)s->dec.nv, (void*)s->dec.r,
                   (void*)s->dec.a, (void*)s->dec.bm, (void*)s->dec.row_stats, (void*)s->dec.r_part,
                   (void*)s->dec.a_part, (void*)s->dec.bm_part, (void*)s->dec.loss_part,
-                  (void*)s->dec.e_tiles, (void*)s->dec.a_acc, (void*)s->dec.r_acc})
+                  (void*)s->dec.e_tiles, (void*)s->dec.a_acc, (void*)s->dec.r_acc, (void*)s->dec.dl_mt,
+                  (void*)s->dec.dl_nu, (void*)s->dec.dl_part})
     if (p) cudaFree(p);
   for (auto& r : s->rw) r.release();
   for (auto* p : s->color) cudaFree(p);
@@ -1243,6 +1267,7 @@ static latmap_status session_capture_step(latmap_session* s) {
   CTX_CHECK(ctx, e);
   s->graph_launches = captured;
   s->graph_exact = ctx->exact_blend;
+  s->graph_dec_path = ctx->decoder_path;
   return LATMAP_OK;
 }
 
@@ -1264,7 +1289,8 @@ latmap_status latmap_session_step(latmap_session* s, latmap_loss_breakdown* out)
   for (int attempt = 0; attempt < 3; ++attempt) {
     latmap_status st = LATMAP_OK;
     if (s->use_graph && !s->prof && session_sized(s)) {
-      if (s->step_graph && s->graph_exact != s->ctx->exact_blend) s->drop_graph();
+      if (s->step_graph && (s->graph_exact != s->ctx->exact_blend || s->graph_dec_path != s->ctx->decoder_path))
+        s->drop_graph();
       if (!s->step_graph) {
         st = session_capture_step(s);
         if (st != LATMAP_OK) return st;

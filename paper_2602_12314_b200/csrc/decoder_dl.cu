@@ -1,0 +1,792 @@
+// decoder_dl.cu — large-dictionary decoder on tcgen05 (bf16 operands, fp32 TMEM accumulators)
+// for K in {256, 512, 768, 1024}, d_s in {32, 64}, n_set <= 256 (BASELINE config 4: K = 1024,
+// d_s = 64, d_f = 1024, 128 target cells).
+//
+// Reference semantics: reconstruct (proj/src/dictionary.cpp:25-53), feature_loss
+// (proj/src/losses.cpp:257-294), reconstruct_backward (dictionary.cpp:55-83), assembled by
+// total_objective (proj/src/objective.cpp:100-185). Same factored algebra as decoder.cu and
+// decoder_tc.cu (S = Q Kd^T, P = softmax(S / tau), t = P M with M = D D^T, G = E D^T):
+//
+//   nu^2 = P.t,  dot = P.G[a],  dS = P * (alpha t + beta G[a] - (alpha nu^2 + beta dot)) / tau,
+//   dQ = dS Kd,  R^T = dS^T Q,  A = P^T diag(alpha) P,  Bm = P^T Ohb.
+//
+// The fused DEC1/DEC2 pair of decoder_tc.cu keeps a whole 128 x K row tile (and M) on chip; at
+// K = 1024 neither the S tile (1024 TMEM columns) nor M (2 MB) fits, so this path stages the
+// K-wide row quantities through HBM in the same core-matrix tile layout, every GEMM on tcgen05:
+//
+//   DL1 dl_softmax_kernel  S = Q Kd^T in 256-column TMEM chunks (double-buffered), two passes:
+//                          row max, then e = exp(S - max) -> bf16 e tiles + row sum + e.G[a].
+//   DL2 dl_t_kernel        T = e M (128 x 256 units, 4-stage TMA-bulk pipeline of e / M blocks,
+//                          double-buffered TMEM accumulator), epilogue stores T (fp32) and the
+//                          per-unit partial of e.T (-> nu^2).
+//   DL3 dl_back_kernel     two roles per row tile (key halves): per-row alpha/beta/loss, dS
+//                          (bf16, smem) -> dQ += dS Kd and R^T += dS^T Q on tcgen05; writes the
+//                          scaled B operand [alpha/sum^2 e | beta/sum onehot(a)] for DL4.
+//   DL4 dl_gram_kernel     [A | Bm] = e^T [alpha e | Ohb] over all row tiles (split in row
+//                          ranges), upper-triangle units of the symmetric A only.
+//   DL5 dl_reduce_kernel   deterministic sum of the per-CTA partials into the step accumulators.
+//
+// Tile layout in HBM and shared memory: the no-swizzle core-matrix layout of tc_common.cuh with
+// 128 rows per tile, row-group stride 128 B and column-group stride 2048 B, so a 64-column
+// block of a tile is 16 contiguous KB (one 1-D bulk copy) and the same bytes serve as a K-major
+// operand (e as A of T = e M) and as an MN-major operand (e^T in the gram).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "tc_common.cuh"
+
+namespace lm {
+
+namespace {
+
+constexpr int kRows = 128;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr uint32_t kCS = 2048;  // column-group stride of a 128-row tile
+
+// ------------------------------------------------------------------------------------------ DL1
+struct Dl1Args {
+  uint8_t* e_tiles;       // ntiles x (128 x K bf16)
+  const float* query;     // npx x DS
+  const int32_t* assign;  // npx
+  const float* kd;        // K x DS fp32
+  const float* gt;        // n_set x K fp32
+  int64_t npx;
+  int K;
+  float inv_temp;
+  float4* rs;             // npx: (max S, 1/sum, dot = P.G[a], 0)
+  float* d_query;         // zeroed here (DL3 accumulates the two key halves)
+  int zero_dq;
+};
+
+template <int DS>
+__global__ void __launch_bounds__(256, 1) dl_softmax_kernel(Dl1Args a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int K = a.K;
+  uint8_t* sKd = smem;               // K x DS (rows = K)
+  uint8_t* sQ = smem + K * DS * 2;   // 128 x DS
+  __shared__ uint64_t bar[2];
+  __shared__ uint32_t s_taddr;
+  __shared__ float s_red[3][2][kRows];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = warp & 3, h = warp >> 2;
+  const int row = 32 * g + lane;
+  tc::load_tile_bf16(sKd, a.kd, K, DS, K, tid, 256);
+  if (tid == 0) {
+    tc::mbar_init(&bar[0], 1);
+    tc::mbar_init(&bar[1], 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc<512>(&s_taddr);
+  tc::fence_async_smem();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = s_taddr;
+  const uint32_t tl = tmem + ((uint32_t)(32 * g) << 16);
+  uint32_t ph[2] = {0, 0};
+  const uint32_t idesc = tc::make_idesc_bf16(128, 256, 0, 0);
+  const uint32_t aQ = tc::smem_u32(sQ), aKd = tc::smem_u32(sKd);
+  const uint32_t kdCS = 16u * K;
+  const float cl = kLog2e * a.inv_temp;
+  const int nch = K / 256;
+  const int64_t ntiles = (a.npx + kRows - 1) / kRows;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * kRows;
+    const int valid = (int)(a.npx - r0 < kRows ? a.npx - r0 : kRows);
+    tc::load_tile_bf16(sQ, a.query + r0 * DS, kRows, DS, valid, tid, 256);
+    if (a.zero_dq) {
+      float4* dq = reinterpret_cast<float4*>(a.d_query + r0 * DS);
+      for (int i = tid; i < valid * DS / 4; i += 256) dq[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const int32_t asg = row < valid ? a.assign[r0 + row] : -1;
+    const float* gp = a.gt + (int64_t)(asg < 0 ? 0 : asg) * K;
+    uint8_t* et = a.e_tiles + (size_t)tile * kRows * K * 2;
+    tc::fence_async_smem();
+    tc::tc_fence_before();
+    __syncthreads();
+    auto issue = [&](int c, int buf) {
+      tc::tc_fence_after();
+#pragma unroll
+      for (int ks = 0; ks < DS / 16; ++ks)
+        tc::mma_bf16(tmem + buf * 256, tc::make_sdesc(aQ + ks * 2 * kCS, kCS, 128),
+                     tc::make_sdesc(aKd + c * 4096 + ks * 2 * kdCS, kdCS, 128), idesc, ks > 0);
+      tc::mma_commit(&bar[buf]);
+    };
+    if (tid == 0) issue(0, 0);
+    float mx = -INFINITY, ml = 0.f, sum = 0.f, dot = 0.f;
+    for (int j = 0; j < 2 * nch; ++j) {
+      const int buf = j & 1;
+      if (tid == 0 && j + 1 < 2 * nch) issue((j + 1) % nch, buf ^ 1);
+      tc::mbar_wait(&bar[buf], ph[buf]);
+      ph[buf] ^= 1;
+      tc::tc_fence_after();
+      const int cb = (j % nch) * 256 + h * 128;  // key index of this thread's first column
+      const uint32_t tcol = tl + buf * 256 + h * 128;
+      if (j < nch) {
+#pragma unroll 1
+        for (int i = 0; i < 128; i += 32) {
+          float v[32];
+          tc::tmem_ld32(tcol + i, v);
+#pragma unroll
+          for (int k = 0; k < 32; ++k) mx = fmaxf(mx, v[k]);
+        }
+      } else {
+#pragma unroll 1
+        for (int i = 0; i < 128; i += 32) {
+          float v[32];
+          tc::tmem_ld32(tcol + i, v);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int c = cb + i + 8 * q;
+            uint4 u;
+            u.x = tc::pack_bf16(tc::ex2(fmaf(v[8 * q + 0], cl, -ml)), tc::ex2(fmaf(v[8 * q + 1], cl, -ml)));
+            u.y = tc::pack_bf16(tc::ex2(fmaf(v[8 * q + 2], cl, -ml)), tc::ex2(fmaf(v[8 * q + 3], cl, -ml)));
+            u.z = tc::pack_bf16(tc::ex2(fmaf(v[8 * q + 4], cl, -ml)), tc::ex2(fmaf(v[8 * q + 5], cl, -ml)));
+            u.w = tc::pack_bf16(tc::ex2(fmaf(v[8 * q + 6], cl, -ml)), tc::ex2(fmaf(v[8 * q + 7], cl, -ml)));
+            *reinterpret_cast<uint4*>(et + tc::core_off(row, c, 128u, kCS)) = u;
+            const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+            float e[8];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              e[2 * k] = __uint_as_float(w4[k] << 16);
+              e[2 * k + 1] = __uint_as_float(w4[k] & 0xffff0000u);
+              sum += e[2 * k] + e[2 * k + 1];
+            }
+            if (asg >= 0) {
+              const float4 g0 = __ldg(reinterpret_cast<const float4*>(gp + c));
+              const float4 g1 = __ldg(reinterpret_cast<const float4*>(gp + c + 4));
+              dot = fmaf(e[0], g0.x, dot);
+              dot = fmaf(e[1], g0.y, dot);
+              dot = fmaf(e[2], g0.z, dot);
+              dot = fmaf(e[3], g0.w, dot);
+              dot = fmaf(e[4], g1.x, dot);
+              dot = fmaf(e[5], g1.y, dot);
+              dot = fmaf(e[6], g1.z, dot);
+              dot = fmaf(e[7], g1.w, dot);
+            }
+          }
+        }
+      }
+      tc::tc_fence_before();
+      if (j == nch - 1) {
+        s_red[0][h][row] = mx;
+        __syncthreads();
+        mx = fmaxf(s_red[0][0][row], s_red[0][1][row]);
+        ml = mx * cl;
+      } else {
+        __syncthreads();
+      }
+    }
+    s_red[1][h][row] = sum;
+    s_red[2][h][row] = dot;
+    __syncthreads();
+    if (h == 0 && row < valid) {
+      const float inv = 1.f / (s_red[1][0][row] + s_red[1][1][row]);
+      a.rs[r0 + row] = make_float4(mx, inv, (s_red[2][0][row] + s_red[2][1][row]) * inv, 0.f);
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free<512>(tmem);
+}
+
+// ------------------------------------------------------------------------------------------ DL2
+struct Dl2Args {
+  const uint8_t* e_tiles;  // ntiles x (128 x K bf16)
+  const uint8_t* mt;       // (K/256) x (K/64) blocks of 256 x 64 bf16 (rows = 256): M[n][k]
+  float* t_tiles;          // ntiles x [K/4][128][4] fp32: T = e M
+  float* nu_part;          // (K/256) x ntiles*128: sum over the unit's columns of e * T
+  int64_t npx;
+  int K;
+};
+
+constexpr int kT_Stages = 4;
+constexpr uint32_t kT_A = 16384, kT_B = 32768;
+
+__global__ void __launch_bounds__(192, 1) dl_t_kernel(Dl2Args a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t full[kT_Stages], empty[kT_Stages], accf[2], acce[2];
+  __shared__ uint32_t s_taddr;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int K = a.K, KB = K / 64, NC = K / 256;
+  const int64_t ntiles = (a.npx + kRows - 1) / kRows, units = ntiles * NC;
+  auto sA = [&](int s) { return smem + s * (kT_A + kT_B); };
+  auto sB = [&](int s) { return smem + s * (kT_A + kT_B) + kT_A; };
+  if (tid == 0) {
+    for (int i = 0; i < kT_Stages; ++i) {
+      tc::mbar_init(&full[i], 1);
+      tc::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&accf[i], 1);
+      tc::mbar_init(&acce[i], 128);
+    }
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc<512>(&s_taddr);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = s_taddr;
+  if (warp == 4) {
+    if (lane == 0) {  // producer: TMA bulk loads of the e block and the M block of each k-step
+      int st = 0;
+      uint32_t ph = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const int64_t t = u / NC;
+        const int nc = (int)(u % NC);
+        const uint8_t* ea = a.e_tiles + (size_t)t * kRows * K * 2;
+        const uint8_t* mb = a.mt + (size_t)nc * KB * kT_B;
+        for (int ks = 0; ks < KB; ++ks) {
+          tc::mbar_wait(&empty[st], ph ^ 1);
+          tc::mbar_expect_tx(&full[st], kT_A + kT_B);
+          tc::bulk_g2s(sA(st), ea + (size_t)ks * kT_A, kT_A, &full[st]);
+          tc::bulk_g2s(sB(st), mb + (size_t)ks * kT_B, kT_B, &full[st]);
+          if (++st == kT_Stages) st = 0, ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {  // MMA issuer
+      const uint32_t idesc = tc::make_idesc_bf16(128, 256, 0, 0);
+      int st = 0;
+      uint32_t ph = 0;
+      int i = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+        const int buf = i & 1;
+        tc::mbar_wait(&acce[buf], ((i >> 1) & 1) ^ 1);
+        tc::tc_fence_after();
+        for (int ks = 0; ks < KB; ++ks) {
+          tc::mbar_wait(&full[st], ph);
+          tc::tc_fence_after();
+          const uint32_t aa = tc::smem_u32(sA(st)), ab = tc::smem_u32(sB(st));
+#pragma unroll
+          for (int k16 = 0; k16 < 4; ++k16)
+            tc::mma_bf16(tmem + buf * 256, tc::make_sdesc(aa + k16 * 2 * kCS, kCS, 128),
+                         tc::make_sdesc(ab + k16 * 2 * 4096, 4096, 128), idesc, (ks | k16) != 0);
+          tc::mma_commit(&empty[st]);
+          if (++st == kT_Stages) st = 0, ph ^= 1;
+        }
+        tc::mma_commit(&accf[buf]);
+      }
+    }
+  } else {  // epilogue: warps 0-3, one pixel row per thread
+    const int row = 32 * warp + lane;
+    const int64_t ntr = ntiles * kRows;
+    int i = 0;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+      const int buf = i & 1;
+      const int64_t t = u / NC;
+      const int nc = (int)(u % NC);
+      const uint8_t* et = a.e_tiles + (size_t)t * kRows * K * 2;
+      float4* tt = reinterpret_cast<float4*>(a.t_tiles + (size_t)t * kRows * K);
+      tc::mbar_wait(&accf[buf], (i >> 1) & 1);
+      tc::tc_fence_after();
+      float nu = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < 256; c += 32) {
+        float v[32];
+        tc::tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + buf * 256 + c, v);
+        const int col = nc * 256 + c;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float e[8];
+          tc::ld_row8(et, row, col + 8 * q, kCS, e);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) nu = fmaf(e[k], v[8 * q + k], nu);
+        }
+#pragma unroll
+        for (int f = 0; f < 8; ++f)
+          tt[(size_t)(col / 4 + f) * kRows + row] = make_float4(v[4 * f], v[4 * f + 1], v[4 * f + 2], v[4 * f + 3]);
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&acce[buf]);
+      a.nu_part[(size_t)nc * ntr + t * kRows + row] = nu;
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free<512>(tmem);
+}
+
+// M (K x K fp32, symmetric) -> the B-operand blocks of dl_t_kernel.
+__global__ void dl_tile_m_kernel(const float* __restrict__ mm, int K, uint8_t* __restrict__ mt) {
+  const int KB = K / 64;
+  const int64_t chunks = (int64_t)K * K / 8;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < chunks; q += (int64_t)gridDim.x * blockDim.x) {
+    const int n = (int)(q / (K / 8)), k0 = (int)(q % (K / 8)) * 8;
+    const int nc = n / 256, nl = n % 256, ks = k0 / 64, kl = k0 % 64;
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = mm[(size_t)n * K + k0 + i];
+    tc::st_row8(mt + ((size_t)nc * KB + ks) * kT_B, nl, kl, 4096u, v);
+  }
+}
+
+// ------------------------------------------------------------------------------------------ DL3
+struct Dl3Args {
+  const uint8_t* e_tiles;
+  const float* t_tiles;
+  const float* nu_part;
+  const float4* rs;
+  const float* query;
+  const int32_t* assign;
+  const float* kd;
+  const float* gt;
+  const float* nv;
+  uint8_t* ae_tiles;   // ntiles x (128 x (K + NB) bf16): [alpha/sum^2 e | beta/sum onehot(a)]
+  float* d_query;      // npx x DS, zeroed by DL1; the two key halves add into it
+  float* r_part;       // gridDim x (K/2) x DS: per-CTA R^T of the role's key half
+  double* loss_part;   // gridDim x 4
+  int64_t npx;
+  int K, NB;
+  float inv_temp, lambda_cos, lambda_l2, inv_nsup, scale;
+  int want_grad;
+};
+
+template <int DS>
+__global__ void __launch_bounds__(256, 1) dl_back_kernel(Dl3Args a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int K = a.K, KH = K / 2, PB = KH / 128, NTOT = K + a.NB;
+  uint8_t* sKd = smem;                 // KH x DS (rows = KH): this role's key half of Kd
+  uint8_t* sQ = sKd + KH * DS * 2;     // 128 x DS
+  uint8_t* sD0 = sQ + kRows * DS * 2;  // 2 x (128 x 128): dS of one 128-key block
+  __shared__ uint64_t bar[2];
+  __shared__ uint32_t s_taddr;
+  __shared__ double s_loss[8][3];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = warp & 3, sub = warp >> 2;
+  const int row = 32 * g + lane;
+  const int role = blockIdx.x & 1, group = blockIdx.x >> 1, ngroups = gridDim.x >> 1;
+  if (a.want_grad) tc::load_tile_bf16(sKd, a.kd + (size_t)role * KH * DS, KH, DS, KH, tid, 256);
+  if (tid == 0) {
+    tc::mbar_init(&bar[0], 1);
+    tc::mbar_init(&bar[1], 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc<512>(&s_taddr);
+  tc::fence_async_smem();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = s_taddr;
+  const uint32_t tl = tmem + ((uint32_t)(32 * g) << 16);
+  const uint32_t aKd = tc::smem_u32(sKd), aQ = tc::smem_u32(sQ);
+  const uint32_t kdCS = 16u * KH;
+  const uint32_t idq = tc::make_idesc_bf16(128, DS, 0, 1), ir = tc::make_idesc_bf16(128, DS, 1, 1);
+  const int64_t ntiles = (a.npx + kRows - 1) / kRows, ntr = ntiles * kRows;
+  const int NC = K / 256;
+  int pc = 0;
+  bool first = true;
+  double cos_acc = 0.0, l2_acc = 0.0, zflag = 0.0;
+  for (int64_t tile = group; tile < ntiles; tile += ngroups) {
+    const int64_t r0 = tile * kRows;
+    const int valid = (int)(a.npx - r0 < kRows ? a.npx - r0 : kRows);
+    if (a.want_grad) tc::load_tile_bf16(sQ, a.query + r0 * DS, kRows, DS, valid, tid, 256);
+    // per-row loss quantities (objective.cpp:100-185 via the factored algebra)
+    const int32_t asg = row < valid ? a.assign[r0 + row] : -1;
+    const float4 st = row < valid ? a.rs[r0 + row] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float inv_sum = st.y, dot = st.z;
+    float nu2 = 0.f;
+    for (int nc = 0; nc < NC; ++nc) nu2 += a.nu_part[(size_t)nc * ntr + r0 + row];
+    nu2 *= inv_sum * inv_sum;
+    float al = 0.f, be = 0.f, cc = 0.f;
+    if (asg >= 0) {
+      const float eps = 1e-8f;
+      const float nu = sqrtf(fmaxf(nu2, 0.f)), vn = a.nv[asg];
+      const float nug = fmaxf(nu, eps), nvg = fmaxf(vn, eps);
+      if (role == 0 && sub == 0) {
+        if (nu < eps || vn < eps) zflag = 1.0;
+        cos_acc += 1.0 - (double)(dot / (nug * nvg));
+        l2_acc += (double)nu2 - 2.0 * (double)dot + (double)vn * (double)vn;
+      }
+      al = a.scale * (a.lambda_cos * dot / (nug * nug * nug * nvg) * a.inv_nsup + 2.f * a.lambda_l2 * a.inv_nsup);
+      be = a.scale * (-a.lambda_cos / (nug * nvg) * a.inv_nsup - 2.f * a.lambda_l2 * a.inv_nsup);
+      cc = al * nu2 + be * dot;
+    }
+    if (!a.want_grad) continue;
+    const float ps = inv_sum * a.inv_temp, al_t = al * inv_sum, wa = al * inv_sum * inv_sum, wb = be * inv_sum;
+    const float* gp = a.gt + (int64_t)(asg < 0 ? 0 : asg) * K;
+    const uint8_t* et = a.e_tiles + (size_t)tile * kRows * K * 2;
+    const float4* tt = reinterpret_cast<const float4*>(a.t_tiles + (size_t)tile * kRows * K);
+    uint8_t* aet = a.ae_tiles + (size_t)tile * kRows * NTOT * 2;
+    if (role == 0) {  // one-hot block of the gram's B operand: beta / sum at column a
+      for (int c8 = 8 * sub; c8 < a.NB; c8 += 16) {
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = (asg == c8 + j) ? wb : 0.f;
+        tc::st_row8(aet, row, K + c8, kCS, v);
+      }
+    }
+    for (int p = 0; p < PB; ++p, ++pc) {
+      const int buf = pc & 1, use = pc >> 1;
+      if (use >= 1) tc::mbar_wait(&bar[buf], (use - 1) & 1);  // MMAs that read sD[buf] are done
+      uint8_t* sD = sD0 + buf * 32768;
+      const int kb = role * KH + p * 128 + sub * 64;  // key of this thread's first column
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int c = kb + 8 * q;
+        float e[8];
+        tc::ld_row8(et, row, c, kCS, e);
+        const float4 t0 = tt[(size_t)(c / 4) * kRows + row], t1 = tt[(size_t)(c / 4 + 1) * kRows + row];
+        const float4 g0 = __ldg(reinterpret_cast<const float4*>(gp + c));
+        const float4 g1 = __ldg(reinterpret_cast<const float4*>(gp + c + 4));
+        const float tv[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+        const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+        float d[8], w8[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          d[j] = e[j] * ps * fmaf(al_t, tv[j], fmaf(be, gv[j], -cc));
+          w8[j] = e[j] * wa;
+        }
+        tc::st_row8(sD, row, sub * 64 + 8 * q, kCS, d);
+        tc::st_row8(aet, row, c, kCS, w8);
+      }
+      tc::fence_async_smem();
+      tc::tc_fence_before();
+      __syncthreads();
+      if (tid == 0) {
+        tc::tc_fence_after();
+        const uint32_t aD = tc::smem_u32(sD);
+        // dQ (+)= dS[:, block] Kd[block, :]
+#pragma unroll
+        for (int k16 = 0; k16 < 8; ++k16)
+          tc::mma_bf16(tmem, tc::make_sdesc(aD + k16 * 2 * kCS, kCS, 128),
+                       tc::make_sdesc(aKd + (p * 16 + 2 * k16) * 128, 128, kdCS), idq, (p | k16) != 0);
+        // R^T[block] += dS[:, block]^T Q
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+          tc::mma_bf16(tmem + DS + p * DS, tc::make_sdesc(aD + ks * 2 * 128, 128, kCS),
+                       tc::make_sdesc(aQ + ks * 2 * 128, 128, kCS), ir, (!first) || ks > 0);
+        tc::mma_commit(&bar[buf]);
+      }
+    }
+    first = false;
+    {
+      const int lp = pc - 1;
+      tc::mbar_wait(&bar[lp & 1], (lp >> 1) & 1);  // every MMA of this tile has completed
+      tc::tc_fence_after();
+    }
+    // dQ: this role's half of the key sum; exactly two adds onto the zeroed row (order-free)
+    {
+      float v[DS / 2];
+#pragma unroll
+      for (int c = 0; c < DS / 2; c += 16) tc::tmem_ld16(tl + sub * (DS / 2) + c, v + c);
+      if (row < valid) {
+        float* dst = a.d_query + (r0 + row) * DS + sub * (DS / 2);
+#pragma unroll
+        for (int c = 0; c < DS / 2; ++c) atomicAdd(dst + c, v[c]);
+      }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+  }
+  if (a.want_grad) {
+    // R^T partial of this CTA: accumulator lane = key within the 128-key block
+    for (int p = 0; p < PB; ++p) {
+      float* dst = a.r_part + ((size_t)blockIdx.x * KH + p * 128 + row) * DS + sub * (DS / 2);
+#pragma unroll
+      for (int c = 0; c < DS / 2; c += 16) {
+        float v[16];
+        if (first) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        } else {
+          tc::tmem_ld16(tl + DS + p * DS + sub * (DS / 2) + c, v);
+        }
+#pragma unroll
+        for (int i = 0; i < 16; i += 4)
+          *reinterpret_cast<float4*>(dst + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      }
+    }
+  }
+  cos_acc = warp_sum_d(cos_acc);
+  l2_acc = warp_sum_d(l2_acc);
+  zflag = warp_sum_d(zflag);
+  if (lane == 0) {
+    s_loss[warp][0] = cos_acc;
+    s_loss[warp][1] = l2_acc;
+    s_loss[warp][2] = zflag;
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (tid == 0) {
+    double c0s = 0, c1s = 0, c2s = 0;
+    for (int w = 0; w < 8; ++w) c0s += s_loss[w][0], c1s += s_loss[w][1], c2s += s_loss[w][2];
+    a.loss_part[blockIdx.x * 4 + 0] = c0s;
+    a.loss_part[blockIdx.x * 4 + 1] = c1s;
+    a.loss_part[blockIdx.x * 4 + 2] = c2s;
+  }
+  if (warp == 0) tc::tmem_free<512>(tmem);
+}
+
+// ------------------------------------------------------------------------------------------ DL4
+struct Dl4Args {
+  const uint8_t* e_tiles;   // ntiles x (128 x K)
+  const uint8_t* ae_tiles;  // ntiles x (128 x NTOT)
+  int nunits;
+  int64_t ntiles;
+  int K, NTOT;
+  float* part;              // splits x K x NTOT (only the units' blocks are written)
+};
+
+constexpr uint32_t kG_A = 32768, kG_B = 65536;
+
+__global__ void __launch_bounds__(192, 1) dl_gram_kernel(Dl4Args a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t full[2], empty[2], accf;
+  __shared__ uint32_t s_taddr;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int unit = blockIdx.x % a.nunits, split = blockIdx.x / a.nunits;
+  const int splits = gridDim.x / a.nunits;
+  // unit -> (M block mb of 128 keys, N chunk nc of 256 columns): per mb the chunks
+  // [mb / 2, nchunks) -- the upper-triangle blocks of A and every Bm chunk
+  const int nchunks = (a.NTOT + 255) / 256;
+  int mb = 0, rem = unit;
+  while (rem >= nchunks - mb / 2) rem -= nchunks - mb / 2, ++mb;
+  const int nc = mb / 2 + rem;
+  const int w = min(256, a.NTOT - nc * 256);
+  const int64_t t0 = split * a.ntiles / splits, t1 = (split + 1) * a.ntiles / splits;
+  auto sA = [&](int s) { return smem + s * (kG_A + kG_B); };
+  auto sB = [&](int s) { return smem + s * (kG_A + kG_B) + kG_A; };
+  if (tid == 0) {
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&full[i], 1);
+      tc::mbar_init(&empty[i], 1);
+    }
+    tc::mbar_init(&accf, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc<256>(&s_taddr);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = s_taddr;
+  const size_t etb = (size_t)kRows * a.K * 2, aetb = (size_t)kRows * a.NTOT * 2;
+  if (warp == 4) {
+    if (lane == 0) {
+      int st = 0;
+      uint32_t ph = 0;
+      for (int64_t t = t0; t < t1; ++t) {
+        tc::mbar_wait(&empty[st], ph ^ 1);
+        tc::mbar_expect_tx(&full[st], kG_A + (uint32_t)w * 256u);
+        tc::bulk_g2s(sA(st), a.e_tiles + t * etb + (size_t)mb * kG_A, kG_A, &full[st]);
+        tc::bulk_g2s(sB(st), a.ae_tiles + t * aetb + (size_t)nc * kG_B, (uint32_t)w * 256u, &full[st]);
+        if (++st == 2) st = 0, ph ^= 1;
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0 && t1 > t0) {
+      const uint32_t idesc = tc::make_idesc_bf16(128, w, 1, 1);
+      int st = 0;
+      uint32_t ph = 0;
+      for (int64_t t = t0; t < t1; ++t) {
+        tc::mbar_wait(&full[st], ph);
+        tc::tc_fence_after();
+        const uint32_t aa = tc::smem_u32(sA(st)), ab = tc::smem_u32(sB(st));
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+          tc::mma_bf16(tmem, tc::make_sdesc(aa + ks * 2 * 128, 128, kCS), tc::make_sdesc(ab + ks * 2 * 128, 128, kCS),
+                       idesc, (t > t0) || ks > 0);
+        tc::mma_commit(&empty[st]);
+        if (++st == 2) st = 0, ph ^= 1;
+      }
+      tc::mma_commit(&accf);
+    }
+  } else {
+    const int row = 32 * warp + lane;
+    if (t1 > t0) {
+      tc::mbar_wait(&accf, 0);
+      tc::tc_fence_after();
+    }
+    float* dst = a.part + ((size_t)split * a.K + mb * 128 + row) * a.NTOT + nc * 256;
+    for (int c = 0; c < w; c += 16) {
+      float v[16];
+      if (t1 > t0) {
+        tc::tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + c, v);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < 16; i += 4)
+        *reinterpret_cast<float4*>(dst + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free<256>(tmem);
+}
+
+// ------------------------------------------------------------------------------------------ DL5
+// A (K x K) += sum over splits of the gram partial at (min(i,j), max(i,j)) (A is symmetric; only
+// upper-triangle units were computed); Bm^T (n_set x K) = the partial's columns K..K+n_set;
+// R (DS x K) += sum over the DL3 CTAs of their R^T partials; loss partials folded once.
+__global__ void __launch_bounds__(256) dl_reduce_kernel(const float* __restrict__ part, int splits, int K, int NTOT,
+                                                        int n_set, const float* __restrict__ r_part, int r_groups,
+                                                        int DS, const double* __restrict__ loss_part, int loss_n,
+                                                        float* A, float* bmt, float* R, double* partials) {
+  if (blockIdx.x == 0 && threadIdx.x < 3) {
+    const int which = threadIdx.x;
+    double s = 0.0;
+    for (int i = 0; i < loss_n; ++i) s += loss_part[i * 4 + which];
+    if (which == 2)
+      partials[6] = fmax(partials[6], s > 0.0 ? 1.0 : 0.0);
+    else
+      partials[4 + which] += s;
+  }
+  const int KH = K / 2;
+  const int64_t na = (int64_t)K * K, nb = (int64_t)n_set * K, nr = (int64_t)DS * K;
+  const size_t pstride = (size_t)K * NTOT;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < na + nb + nr;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    if (q < na) {
+      const int i = (int)(q / K), j = (int)(q % K);
+      const size_t o = (size_t)min(i, j) * NTOT + max(i, j);
+      float s = 0.f;
+      for (int sp = 0; sp < splits; ++sp) s += part[sp * pstride + o];
+      A[q] += s;
+    } else if (q < na + nb) {
+      const int64_t e = q - na;
+      const int s_ = (int)(e / K), k = (int)(e % K);
+      const size_t o = (size_t)k * NTOT + K + s_;
+      float s = 0.f;
+      for (int sp = 0; sp < splits; ++sp) s += part[sp * pstride + o];
+      bmt[e] = s;
+    } else {
+      const int64_t e = q - na - nb;
+      const int d = (int)(e / K), k = (int)(e % K);
+      const int role = k / KH, kl = k % KH;
+      float s = 0.f;
+      for (int gi = 0; gi < r_groups; ++gi) s += r_part[((size_t)(2 * gi + role) * KH + kl) * DS + d];
+      R[e] += s;
+    }
+  }
+}
+
+constexpr int kBackGroups = 74;  // DL3 grid = 2 roles x 74 groups
+
+int nb_for(int64_t n_set) { return (int)std::max<int64_t>(16, (n_set + 15) / 16 * 16); }
+
+int dl_units(int K, int NTOT) {
+  const int nchunks = (NTOT + 255) / 256;
+  int n = 0;
+  for (int mb = 0; mb < K / 128; ++mb) n += nchunks - mb / 2;
+  return n;
+}
+
+template <typename F>
+void set_smem(F* f, size_t bytes) {
+  static size_t done = 0;  // per kernel instantiation
+  if (done < bytes) {
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    done = bytes;
+  }
+}
+
+template <int DS>
+void launch_dl(cudaStream_t st, DecoderWork& w, const float* query, const int32_t* assignment, int64_t npx,
+               int64_t n_set, int64_t n_sup, float temperature, float lambda_cos, float lambda_l2, float scale,
+               bool want_grad, float* d_query, double* partials) {
+  const int K = (int)w.k;
+  const int NB = nb_for(n_set), NTOT = K + NB;
+  const int64_t ntiles = (npx + kRows - 1) / kRows;
+  const float inv_temp = 1.f / temperature;
+  // DL1
+  {
+    Dl1Args d{w.e_tiles, query, assignment, w.kd, w.gt, npx, K, inv_temp, reinterpret_cast<float4*>(w.row_stats),
+              d_query, want_grad ? 1 : 0};
+    const size_t sm = (size_t)K * DS * 2 + (size_t)kRows * DS * 2;
+    set_smem(dl_softmax_kernel<DS>, sm);
+    dl_softmax_kernel<DS><<<148, 256, sm, st>>>(d);
+    count_launch();
+  }
+  // DL2
+  {
+    Dl2Args d{w.e_tiles, w.dl_mt, w.dl_t, w.dl_nu, npx, K};
+    const size_t sm = (size_t)kT_Stages * (kT_A + kT_B);
+    set_smem(dl_t_kernel, sm);
+    const int64_t units = ntiles * (K / 256);
+    dl_t_kernel<<<(unsigned)std::min<int64_t>(148, units), 192, sm, st>>>(d);
+    count_launch();
+  }
+  // DL3
+  {
+    Dl3Args d{w.e_tiles, w.dl_t, w.dl_nu, reinterpret_cast<const float4*>(w.row_stats), query, assignment, w.kd,
+              w.gt, w.nv, w.dl_ae, d_query, w.r_part, w.loss_part, npx, K, NB, inv_temp, lambda_cos, lambda_l2,
+              n_sup > 0 ? 1.f / (float)n_sup : 0.f, scale, want_grad ? 1 : 0};
+    const size_t sm = (size_t)(K / 2) * DS * 2 + (size_t)kRows * DS * 2 + 2 * 32768;
+    set_smem(dl_back_kernel<DS>, sm);
+    dl_back_kernel<DS><<<2 * kBackGroups, 256, sm, st>>>(d);
+    count_launch();
+  }
+  if (!want_grad) {
+    dl_reduce_kernel<<<1, 32, 0, st>>>(nullptr, 0, 0, 0, 0, nullptr, 0, 0, w.loss_part, 2 * kBackGroups,
+                                        nullptr, nullptr, nullptr, partials);
+    count_launch();
+    return;
+  }
+  // DL4: units = upper-triangle blocks of A + the Bm columns
+  const int nunits = dl_units(K, NTOT);
+  const int splits = std::max(1, std::min<int>(148 / nunits, (int)ntiles));
+  {
+    Dl4Args d{w.e_tiles, w.dl_ae, nunits, ntiles, K, NTOT, w.dl_part};
+    const size_t sm = 2 * (size_t)(kG_A + kG_B);
+    set_smem(dl_gram_kernel, sm);
+    dl_gram_kernel<<<nunits * splits, 192, sm, st>>>(d);
+    count_launch();
+  }
+  {
+    const int64_t total = (int64_t)K * K + n_set * K + (int64_t)DS * K;
+    dl_reduce_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, st>>>(
+        w.dl_part, splits, K, NTOT, (int)n_set, w.r_part, kBackGroups, DS, w.loss_part, 2 * kBackGroups, w.a_acc,
+        w.bm, w.r_acc, partials);
+    count_launch();
+  }
+}
+
+}  // namespace
+
+bool decoder_dl_supported(int64_t k, int ds, int64_t n_set) {
+  return k >= 256 && k <= 1024 && k % 256 == 0 && (ds == 32 || ds == 64) && n_set >= 1 && n_set <= 256;
+}
+
+size_t decoder_dl_part_floats(int64_t k) {
+  // gram partials: splits x K x (K + NB) with splits <= 148 / units and NB <= 256
+  const int kk = (int)k, least = dl_units(kk, kk + 16);
+  return (size_t)(148 / least) * (size_t)k * (size_t)(k + 256);
+}
+
+void decoder_dl_prepare(cudaStream_t st, DecoderWork& w) {
+  if (!w.dl_mt) return;
+  const int K = (int)w.k;
+  dl_tile_m_kernel<<<(unsigned)std::min<int64_t>(((int64_t)K * K / 8 + 255) / 256, 148 * 8), 256, 0, st>>>(
+      w.mm, K, w.dl_mt);
+  count_launch();
+}
+
+void decoder_frame_dl(cudaStream_t st, DecoderWork& w, const float* query, const int32_t* assignment, int64_t npx,
+                      const float* feats, int64_t n_set, int64_t n_sup, const float* atoms, float temperature,
+                      float lambda_cos, float lambda_l2, float scale, bool want_grad, float* d_query,
+                      float* d_atoms, double* partials) {
+  const int64_t k = w.k;
+  const int df = w.df;
+  sgemm(st, false, true, n_set, k, df, 1.f, feats, df, atoms, df, 0.f, w.gt, k);
+  decoder_target_norms(st, feats, n_set, df, w.nv);
+  if (w.ds == 64)
+    launch_dl<64>(st, w, query, assignment, npx, n_set, n_sup, temperature, lambda_cos, lambda_l2, scale, want_grad,
+                  d_query, partials);
+  else
+    launch_dl<32>(st, w, query, assignment, npx, n_set, n_sup, temperature, lambda_cos, lambda_l2, scale, want_grad,
+                  d_query, partials);
+  if (!want_grad) return;
+  sgemm(st, true, false, k, df, n_set, 1.f, w.bm, k, feats, df, 1.f, d_atoms, df);
+  w.tc_pending = true;
+}
+
+}  // namespace lm

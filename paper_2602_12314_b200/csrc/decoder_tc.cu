@@ -36,42 +36,6 @@ namespace {
 constexpr int kRows = 128;        // pixels per tile (UMMA M)
 constexpr float kLog2e = 1.4426950408889634f;
 
-__device__ __forceinline__ float ex2(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
-// Store 8 consecutive bf16 (cols c0..c0+7, c0 % 8 == 0) of row r into a core-matrix tile.
-__device__ __forceinline__ void st_row8(uint8_t* tile, int r, int c0, uint32_t col_stride, const float* v) {
-  uint4 u;
-  u.x = tc::pack_bf16(v[0], v[1]);
-  u.y = tc::pack_bf16(v[2], v[3]);
-  u.z = tc::pack_bf16(v[4], v[5]);
-  u.w = tc::pack_bf16(v[6], v[7]);
-  *reinterpret_cast<uint4*>(tile + tc::core_off(r, c0, 128u, col_stride)) = u;
-}
-
-// Load a row-major fp32 matrix [rows x cols] (cols % 8 == 0) into a bf16 core-matrix tile.
-__device__ __forceinline__ void load_tile_bf16(uint8_t* tile, const float* __restrict__ src, int rows, int cols,
-                                               int valid_rows, int tid, int nthr) {
-  const uint32_t cs = 16u * rows;
-  const int chunks = rows * (cols / 8);
-  for (int e = tid; e < chunks; e += nthr) {
-    const int r = e / (cols / 8), c0 = (e % (cols / 8)) * 8;
-    float v[8];
-    if (r < valid_rows) {
-      const float4 a = *reinterpret_cast<const float4*>(src + (size_t)r * cols + c0);
-      const float4 b = *reinterpret_cast<const float4*>(src + (size_t)r * cols + c0 + 4);
-      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-    } else {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = 0.f;
-    }
-    st_row8(tile, r, c0, cs, v);
-  }
-}
-
 struct Dec1Args {
   uint8_t* e_tiles;         // ntiles x (128 x K bf16) in the smem core-matrix layout (for DEC2)
   const float* query;       // npx x DS (fp32, raster order)
@@ -88,17 +52,6 @@ struct Dec1Args {
   double* loss_part;        // gridDim x 4
   int want_grad;
 };
-
-// Unpack 8 bf16 (one 16-byte core-matrix row chunk) to fp32.
-__device__ __forceinline__ void ld_row8(const uint8_t* tile, int r, int c0, uint32_t col_stride, float* v) {
-  const uint4 u = *reinterpret_cast<const uint4*>(tile + tc::core_off(r, c0, 128u, col_stride));
-  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    v[2 * i] = __uint_as_float(w[i] << 16);
-    v[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
-  }
-}
 
 template <int K, int DS>
 __global__ void __launch_bounds__(512, 1) dec1_kernel(Dec1Args a) {
@@ -124,8 +77,8 @@ __global__ void __launch_bounds__(512, 1) dec1_kernel(Dec1Args a) {
   const int c0 = qt * QC;
   auto red = [&](int q, int quarter) -> float& { return s_red[(q * 4 + quarter) * 128 + row]; };
 
-  load_tile_bf16(sKd, a.kd, K, DS, K, tid, NT);
-  load_tile_bf16(sM, a.mm, K, K, K, tid, NT);
+  tc::load_tile_bf16(sKd, a.kd, K, DS, K, tid, NT);
+  tc::load_tile_bf16(sM, a.mm, K, K, K, tid, NT);
   if (tid == 0) {
     for (int i = 0; i < 3; ++i) tc::mbar_init(&bar[i], 1);
     tc::fence_mbar_init();
@@ -164,7 +117,7 @@ __global__ void __launch_bounds__(512, 1) dec1_kernel(Dec1Args a) {
   auto q_store = [&]() {
     if (tid < QCH) {
       const float v[8] = {qpre[0].x, qpre[0].y, qpre[0].z, qpre[0].w, qpre[1].x, qpre[1].y, qpre[1].z, qpre[1].w};
-      st_row8(sQ, qr, qc, kCS, v);
+      tc::st_row8(sQ, qr, qc, kCS, v);
     }
   };
   const int64_t ntiles = (a.npx + kRows - 1) / kRows;
@@ -212,10 +165,10 @@ __global__ void __launch_bounds__(512, 1) dec1_kernel(Dec1Args a) {
 #pragma unroll
     for (int c = 0; c < QC; c += 8) {
       uint4 u;
-      u.x = tc::pack_bf16(ex2(fmaf(sv[c + 0], cl, -mxl)), ex2(fmaf(sv[c + 1], cl, -mxl)));
-      u.y = tc::pack_bf16(ex2(fmaf(sv[c + 2], cl, -mxl)), ex2(fmaf(sv[c + 3], cl, -mxl)));
-      u.z = tc::pack_bf16(ex2(fmaf(sv[c + 4], cl, -mxl)), ex2(fmaf(sv[c + 5], cl, -mxl)));
-      u.w = tc::pack_bf16(ex2(fmaf(sv[c + 6], cl, -mxl)), ex2(fmaf(sv[c + 7], cl, -mxl)));
+      u.x = tc::pack_bf16(tc::ex2(fmaf(sv[c + 0], cl, -mxl)), tc::ex2(fmaf(sv[c + 1], cl, -mxl)));
+      u.y = tc::pack_bf16(tc::ex2(fmaf(sv[c + 2], cl, -mxl)), tc::ex2(fmaf(sv[c + 3], cl, -mxl)));
+      u.z = tc::pack_bf16(tc::ex2(fmaf(sv[c + 4], cl, -mxl)), tc::ex2(fmaf(sv[c + 5], cl, -mxl)));
+      u.w = tc::pack_bf16(tc::ex2(fmaf(sv[c + 6], cl, -mxl)), tc::ex2(fmaf(sv[c + 7], cl, -mxl)));
       *reinterpret_cast<uint4*>(sP + tc::core_off(row, c0 + c, 128u, kCS)) = u;
       const uint32_t w4[4] = {u.x, u.y, u.z, u.w};  // sum the bf16-rounded e the MMA consumes
 #pragma unroll
@@ -254,7 +207,7 @@ __global__ void __launch_bounds__(512, 1) dec1_kernel(Dec1Args a) {
 #pragma unroll
     for (int c = 0; c < QC; c += 8) {
       float e[8];
-      ld_row8(sP, row, c0 + c, kCS, e);
+      tc::ld_row8(sP, row, c0 + c, kCS, e);
       const float4 g0 = __ldg(reinterpret_cast<const float4*>(grow_ptr + c));
       const float4 g1 = __ldg(reinterpret_cast<const float4*>(grow_ptr + c + 4));
       const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
@@ -302,13 +255,13 @@ __global__ void __launch_bounds__(512, 1) dec1_kernel(Dec1Args a) {
 #pragma unroll
     for (int c = 0; c < QC; c += 8) {
       float e[8];
-      ld_row8(sP, row, c0 + c, kCS, e);
+      tc::ld_row8(sP, row, c0 + c, kCS, e);
       const float4 g0 = __ldg(reinterpret_cast<const float4*>(grow_ptr + c));
       const float4 g1 = __ldg(reinterpret_cast<const float4*>(grow_ptr + c + 4));
       const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
 #pragma unroll
       for (int j = 0; j < 8; ++j) e[j] = e[j] * ps * fmaf(al_t, tv[c + j], fmaf(be, gv[j], -cc));
-      st_row8(sP, row, c0 + c, kCS, e);
+      tc::st_row8(sP, row, c0 + c, kCS, e);
     }
     tc::fence_async_smem();
     tc::tc_fence_before();
@@ -496,10 +449,10 @@ __global__ void __launch_bounds__(288, 1) dec2_kernel(Dec2Args a) {
 #pragma unroll
       for (int c = h * (NH / 2); c < (h + 1) * (NH / 2); c += 8) {
         float v[8];
-        ld_row8(E, row, role * NH + c, kCS, v);
+        tc::ld_row8(E, row, role * NH + c, kCS, v);
 #pragma unroll
         for (int j = 0; j < 8; ++j) v[j] = row < valid ? v[j] * wa : 0.f;
-        st_row8(AP, row, c, kCS, v);
+        tc::st_row8(AP, row, c, kCS, v);
       }
       if (role == 0) {
         uint8_t* Oh = sOh0 + buf * kOhBytes;
@@ -508,7 +461,7 @@ __global__ void __launch_bounds__(288, 1) dec2_kernel(Dec2Args a) {
           float v[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) v[j] = (asg == c + j) ? wb : 0.f;
-          st_row8(Oh, row, c, kCS, v);
+          tc::st_row8(Oh, row, c, kCS, v);
         }
       }
       tc::fence_async_smem();

@@ -97,6 +97,12 @@ struct DecoderWork {
   float* a_acc = nullptr;      // K x K: sum over the step's frames of P^T diag(alpha) P
   float* r_acc = nullptr;      // ds x K: sum over the step's frames of Q^T dS
   bool tc_pending = false;     // a_acc / r_acc hold contributions not yet applied
+  // staged large-K tcgen05 path scratch (decoder_dl.cu)
+  uint8_t* dl_mt = nullptr;    // K x K bf16: M in the B-operand blocks of the T GEMM
+  float* dl_t = nullptr;       // ntiles x 128 x K fp32: T = e M (aliases buf1)
+  uint8_t* dl_ae = nullptr;    // ntiles x 128 x (K + NB) bf16: gram B operand (aliases buf2)
+  float* dl_nu = nullptr;      // (K/256) x ntiles*128: partial e.T per 256-column unit
+  float* dl_part = nullptr;    // gram partials
 };
 void decoder_prepare(cudaStream_t st, DecoderWork& w, const float* atoms, const float* proj);
 // Fused feature loss + decoder backward for one frame (pixel mode). Accumulates into d_proj,
@@ -112,6 +118,15 @@ void decoder_frame_tc(cudaStream_t st, DecoderWork& w, const float* query, const
                       int64_t npx, const float* feats, int64_t n_set, int64_t n_sup, const float* atoms,
                       const float* proj, float temperature, float lambda_cos, float lambda_l2, float scale,
                       bool want_grad, float* d_query, float* d_proj, float* d_atoms, double* partials);
+// Staged tcgen05 path for large dictionaries (decoder_dl.cu): K in {256..1024} (multiple of 256),
+// d_s in {32, 64}, n_set <= 256. Same outputs and accumulators as decoder_frame_tc.
+bool decoder_dl_supported(int64_t k, int ds, int64_t n_set);
+size_t decoder_dl_part_floats(int64_t k);
+void decoder_dl_prepare(cudaStream_t st, DecoderWork& w);
+void decoder_frame_dl(cudaStream_t st, DecoderWork& w, const float* query, const int32_t* assignment,
+                      int64_t npx, const float* feats, int64_t n_set, int64_t n_sup, const float* atoms,
+                      float temperature, float lambda_cos, float lambda_l2, float scale, bool want_grad,
+                      float* d_query, float* d_atoms, double* partials);
 // Applies the step-accumulated A and R of the tcgen05 frames: d_atoms += A D + R^T W, d_proj += R D.
 void decoder_finish_tc(cudaStream_t st, DecoderWork& w, const float* atoms, const float* proj, float* d_proj,
                        float* d_atoms);

@@ -176,5 +176,54 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+
+// ---- bf16 core-matrix tile helpers (shared by the decoder kernels)
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Store 8 consecutive bf16 (cols c0..c0+7, c0 % 8 == 0) of row r into a core-matrix tile.
+__device__ __forceinline__ void st_row8(uint8_t* tile, int r, int c0, uint32_t col_stride, const float* v) {
+  uint4 u;
+  u.x = pack_bf16(v[0], v[1]);
+  u.y = pack_bf16(v[2], v[3]);
+  u.z = pack_bf16(v[4], v[5]);
+  u.w = pack_bf16(v[6], v[7]);
+  *reinterpret_cast<uint4*>(tile + core_off(r, c0, 128u, col_stride)) = u;
+}
+
+// Load a row-major fp32 matrix [rows x cols] (cols % 8 == 0) into a bf16 core-matrix tile.
+__device__ __forceinline__ void load_tile_bf16(uint8_t* tile, const float* __restrict__ src, int rows, int cols,
+                                               int valid_rows, int tid, int nthr) {
+  const uint32_t cs = 16u * rows;
+  const int chunks = rows * (cols / 8);
+  for (int e = tid; e < chunks; e += nthr) {
+    const int r = e / (cols / 8), c0 = (e % (cols / 8)) * 8;
+    float v[8];
+    if (r < valid_rows) {
+      const float4 a = *reinterpret_cast<const float4*>(src + (size_t)r * cols + c0);
+      const float4 b = *reinterpret_cast<const float4*>(src + (size_t)r * cols + c0 + 4);
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = 0.f;
+    }
+    st_row8(tile, r, c0, cs, v);
+  }
+}
+
+// Unpack 8 bf16 (one 16-byte core-matrix row chunk) to fp32.
+__device__ __forceinline__ void ld_row8(const uint8_t* tile, int r, int c0, uint32_t col_stride, float* v) {
+  const uint4 u = *reinterpret_cast<const uint4*>(tile + core_off(r, c0, 128u, col_stride));
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    v[2 * i] = __uint_as_float(w[i] << 16);
+    v[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+}
+
 }  // namespace tc
 }  // namespace lm
