@@ -19,6 +19,9 @@ namespace lm {
 static std::atomic<int64_t> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 void set_launch_counter(int64_t*) {}
+static std::atomic<const char*> g_sticky{nullptr};
+void set_sticky_error(const char* msg) { g_sticky.store(msg); }
+const char* take_sticky_error() { return g_sticky.exchange(nullptr); }
 
 static thread_local std::string t_err;
 latmap_status set_cuda_error(cudaError_t e, const char* what, const char* file, int line) {
@@ -181,6 +184,11 @@ static latmap_status fail(latmap_ctx* ctx, latmap_status s, const char* msg) {
 }
 
 static latmap_status post_launch(latmap_ctx* ctx) {
+  if (const char* m = take_sticky_error()) {
+    t_err = m;
+    ctx->err = t_err;
+    return LATMAP_ERR_CUDA;
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     latmap_status s = set_cuda_error(e, "kernel launch", __FILE__, __LINE__);

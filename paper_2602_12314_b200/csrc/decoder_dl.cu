@@ -17,20 +17,23 @@
 //   DL1 dl_softmax_kernel  S = Q Kd^T in 256-column TMEM chunks (double-buffered), two passes:
 //                          row max, then e = exp(S - max) -> bf16 e tiles + row sum + e.G[a].
 //   DL2 dl_t_kernel        T = e M (128 x 256 units, 4-stage TMA-bulk pipeline of e / M blocks,
-//                          double-buffered TMEM accumulator), epilogue stores T (fp32) and the
+//                          double-buffered TMEM accumulator), epilogue stores T (fp16) and the
 //                          per-unit partial of e.T (-> nu^2).
 //   DL3 dl_back_kernel     two roles per row tile (key halves): per-row alpha/beta/loss, dS
 //                          (bf16, smem) -> dQ += dS Kd and R^T += dS^T Q on tcgen05; writes the
 //                          scaled B operand [alpha/sum^2 e | beta/sum onehot(a)] for DL4.
 //   DL4 dl_gram_kernel     [A | Bm] = e^T [alpha e | Ohb] over all row tiles (split in row
-//                          ranges), upper-triangle units of the symmetric A only.
+//                          ranges), 256 x 256 upper-triangle units of the symmetric A only.
 //   DL5 dl_reduce_kernel   deterministic sum of the per-CTA partials into the step accumulators.
 //
 // Tile layout in HBM and shared memory: the no-swizzle core-matrix layout of tc_common.cuh with
 // 128 rows per tile, row-group stride 128 B and column-group stride 2048 B, so a 64-column
 // block of a tile is 16 contiguous KB (one 1-D bulk copy) and the same bytes serve as a K-major
 // operand (e as A of T = e M) and as an MN-major operand (e^T in the gram).
+#include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <stdint.h>
 
 #include <algorithm>
@@ -48,6 +51,20 @@ constexpr int kRows = 128;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr uint32_t kCS = 2048;  // column-group stride of a 128-row tile
 
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
+  __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ void unpack_h8(uint4 u, float* v) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+    v[2 * i] = f.x;
+    v[2 * i + 1] = f.y;
+  }
+}
+
 // ------------------------------------------------------------------------------------------ DL1
 struct Dl1Args {
   uint8_t* e_tiles;       // ntiles x (128 x K bf16)
@@ -64,18 +81,18 @@ struct Dl1Args {
 };
 
 template <int DS>
-__global__ void __launch_bounds__(256, 1) dl_softmax_kernel(Dl1Args a) {
+__global__ void __launch_bounds__(512, 1) dl_softmax_kernel(Dl1Args a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int K = a.K;
   uint8_t* sKd = smem;               // K x DS (rows = K)
   uint8_t* sQ = smem + K * DS * 2;   // 128 x DS
   __shared__ uint64_t bar[2];
   __shared__ uint32_t s_taddr;
-  __shared__ float s_red[3][2][kRows];
+  __shared__ float s_red[3][4][kRows];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = warp & 3, h = warp >> 2;
+  const int g = warp & 3, h = warp >> 2;  // TMEM lane group, 64-column quarter of a chunk
   const int row = 32 * g + lane;
-  tc::load_tile_bf16(sKd, a.kd, K, DS, K, tid, 256);
+  tc::load_tile_bf16(sKd, a.kd, K, DS, K, tid, 512);
   if (tid == 0) {
     tc::mbar_init(&bar[0], 1);
     tc::mbar_init(&bar[1], 1);
@@ -98,10 +115,10 @@ __global__ void __launch_bounds__(256, 1) dl_softmax_kernel(Dl1Args a) {
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t r0 = tile * kRows;
     const int valid = (int)(a.npx - r0 < kRows ? a.npx - r0 : kRows);
-    tc::load_tile_bf16(sQ, a.query + r0 * DS, kRows, DS, valid, tid, 256);
+    tc::load_tile_bf16(sQ, a.query + r0 * DS, kRows, DS, valid, tid, 512);
     if (a.zero_dq) {
       float4* dq = reinterpret_cast<float4*>(a.d_query + r0 * DS);
-      for (int i = tid; i < valid * DS / 4; i += 256) dq[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int i = tid; i < valid * DS / 4; i += 512) dq[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     const int32_t asg = row < valid ? a.assign[r0 + row] : -1;
     const float* gp = a.gt + (int64_t)(asg < 0 ? 0 : asg) * K;
@@ -125,11 +142,11 @@ __global__ void __launch_bounds__(256, 1) dl_softmax_kernel(Dl1Args a) {
       tc::mbar_wait(&bar[buf], ph[buf]);
       ph[buf] ^= 1;
       tc::tc_fence_after();
-      const int cb = (j % nch) * 256 + h * 128;  // key index of this thread's first column
-      const uint32_t tcol = tl + buf * 256 + h * 128;
+      const int cb = (j % nch) * 256 + h * 64;  // key index of this thread's first column
+      const uint32_t tcol = tl + buf * 256 + h * 64;
       if (j < nch) {
 #pragma unroll 1
-        for (int i = 0; i < 128; i += 32) {
+        for (int i = 0; i < 64; i += 32) {
           float v[32];
           tc::tmem_ld32(tcol + i, v);
 #pragma unroll
@@ -137,7 +154,7 @@ __global__ void __launch_bounds__(256, 1) dl_softmax_kernel(Dl1Args a) {
         }
       } else {
 #pragma unroll 1
-        for (int i = 0; i < 128; i += 32) {
+        for (int i = 0; i < 64; i += 32) {
           float v[32];
           tc::tmem_ld32(tcol + i, v);
 #pragma unroll
@@ -176,7 +193,7 @@ __global__ void __launch_bounds__(256, 1) dl_softmax_kernel(Dl1Args a) {
       if (j == nch - 1) {
         s_red[0][h][row] = mx;
         __syncthreads();
-        mx = fmaxf(s_red[0][0][row], s_red[0][1][row]);
+        mx = fmaxf(fmaxf(s_red[0][0][row], s_red[0][1][row]), fmaxf(s_red[0][2][row], s_red[0][3][row]));
         ml = mx * cl;
       } else {
         __syncthreads();
@@ -186,8 +203,9 @@ __global__ void __launch_bounds__(256, 1) dl_softmax_kernel(Dl1Args a) {
     s_red[2][h][row] = dot;
     __syncthreads();
     if (h == 0 && row < valid) {
-      const float inv = 1.f / (s_red[1][0][row] + s_red[1][1][row]);
-      a.rs[r0 + row] = make_float4(mx, inv, (s_red[2][0][row] + s_red[2][1][row]) * inv, 0.f);
+      const float inv = 1.f / ((s_red[1][0][row] + s_red[1][1][row]) + (s_red[1][2][row] + s_red[1][3][row]));
+      const float dsum = (s_red[2][0][row] + s_red[2][1][row]) + (s_red[2][2][row] + s_red[2][3][row]);
+      a.rs[r0 + row] = make_float4(mx, inv, dsum * inv, 0.f);
     }
   }
   tc::tc_fence_before();
@@ -199,7 +217,8 @@ __global__ void __launch_bounds__(256, 1) dl_softmax_kernel(Dl1Args a) {
 struct Dl2Args {
   const uint8_t* e_tiles;  // ntiles x (128 x K bf16)
   const uint8_t* mt;       // (K/256) x (K/64) blocks of 256 x 64 bf16 (rows = 256): M[n][k]
-  float* t_tiles;          // ntiles x [K/4][128][4] fp32: T = e M
+  uint4* t_tiles;          // ntiles x [K/8][128] x 8 fp16: T = e M (|T| <= sum e <= K; fp16 keeps
+                           // 11 bits, 4x finer than the bf16 e it multiplies)
   float* nu_part;          // (K/256) x ntiles*128: sum over the unit's columns of e * T
   int64_t npx;
   int K;
@@ -284,7 +303,7 @@ __global__ void __launch_bounds__(192, 1) dl_t_kernel(Dl2Args a) {
       const int64_t t = u / NC;
       const int nc = (int)(u % NC);
       const uint8_t* et = a.e_tiles + (size_t)t * kRows * K * 2;
-      float4* tt = reinterpret_cast<float4*>(a.t_tiles + (size_t)t * kRows * K);
+      uint4* tt = a.t_tiles + (size_t)t * kRows * (K / 8);
       tc::mbar_wait(&accf[buf], (i >> 1) & 1);
       tc::tc_fence_after();
       float nu = 0.f;
@@ -301,8 +320,10 @@ __global__ void __launch_bounds__(192, 1) dl_t_kernel(Dl2Args a) {
           for (int k = 0; k < 8; ++k) nu = fmaf(e[k], v[8 * q + k], nu);
         }
 #pragma unroll
-        for (int f = 0; f < 8; ++f)
-          tt[(size_t)(col / 4 + f) * kRows + row] = make_float4(v[4 * f], v[4 * f + 1], v[4 * f + 2], v[4 * f + 3]);
+        for (int f = 0; f < 4; ++f)
+          tt[(size_t)(col / 8 + f) * kRows + row] =
+              make_uint4(pack_h2(v[8 * f], v[8 * f + 1]), pack_h2(v[8 * f + 2], v[8 * f + 3]),
+                         pack_h2(v[8 * f + 4], v[8 * f + 5]), pack_h2(v[8 * f + 6], v[8 * f + 7]));
       }
       tc::tc_fence_before();
       tc::mbar_arrive(&acce[buf]);
@@ -331,7 +352,7 @@ __global__ void dl_tile_m_kernel(const float* __restrict__ mm, int K, uint8_t* _
 // ------------------------------------------------------------------------------------------ DL3
 struct Dl3Args {
   const uint8_t* e_tiles;
-  const float* t_tiles;
+  const uint4* t_tiles;
   const float* nu_part;
   const float4* rs;
   const float* query;
@@ -349,8 +370,16 @@ struct Dl3Args {
   int want_grad;
 };
 
+template <int N>
+__device__ __forceinline__ void tmem_ldq(uint32_t taddr, float* v) {
+  if constexpr (N == 8)
+    tc::tmem_ld8(taddr, v);
+  else
+    tc::tmem_ld16(taddr, v);
+}
+
 template <int DS>
-__global__ void __launch_bounds__(256, 1) dl_back_kernel(Dl3Args a) {
+__global__ void __launch_bounds__(512, 1) dl_back_kernel(Dl3Args a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int K = a.K, KH = K / 2, PB = KH / 128, NTOT = K + a.NB;
   uint8_t* sKd = smem;                 // KH x DS (rows = KH): this role's key half of Kd
@@ -358,12 +387,13 @@ __global__ void __launch_bounds__(256, 1) dl_back_kernel(Dl3Args a) {
   uint8_t* sD0 = sQ + kRows * DS * 2;  // 2 x (128 x 128): dS of one 128-key block
   __shared__ uint64_t bar[2];
   __shared__ uint32_t s_taddr;
-  __shared__ double s_loss[8][3];
+  __shared__ double s_loss[16][3];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = warp & 3, sub = warp >> 2;
+  const int g = warp & 3, sub = warp >> 2;  // TMEM lane group, 32-key quarter of a block
+  constexpr int DQ = DS / 4;                  // dQ / R^T columns per thread
   const int row = 32 * g + lane;
   const int role = blockIdx.x & 1, group = blockIdx.x >> 1, ngroups = gridDim.x >> 1;
-  if (a.want_grad) tc::load_tile_bf16(sKd, a.kd + (size_t)role * KH * DS, KH, DS, KH, tid, 256);
+  if (a.want_grad) tc::load_tile_bf16(sKd, a.kd + (size_t)role * KH * DS, KH, DS, KH, tid, 512);
   if (tid == 0) {
     tc::mbar_init(&bar[0], 1);
     tc::mbar_init(&bar[1], 1);
@@ -387,7 +417,7 @@ __global__ void __launch_bounds__(256, 1) dl_back_kernel(Dl3Args a) {
   for (int64_t tile = group; tile < ntiles; tile += ngroups) {
     const int64_t r0 = tile * kRows;
     const int valid = (int)(a.npx - r0 < kRows ? a.npx - r0 : kRows);
-    if (a.want_grad) tc::load_tile_bf16(sQ, a.query + r0 * DS, kRows, DS, valid, tid, 256);
+    if (a.want_grad) tc::load_tile_bf16(sQ, a.query + r0 * DS, kRows, DS, valid, tid, 512);
     // per-row loss quantities (objective.cpp:100-185 via the factored algebra)
     const int32_t asg = row < valid ? a.assign[r0 + row] : -1;
     const float4 st = row < valid ? a.rs[r0 + row] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -413,10 +443,10 @@ __global__ void __launch_bounds__(256, 1) dl_back_kernel(Dl3Args a) {
     const float ps = inv_sum * a.inv_temp, al_t = al * inv_sum, wa = al * inv_sum * inv_sum, wb = be * inv_sum;
     const float* gp = a.gt + (int64_t)(asg < 0 ? 0 : asg) * K;
     const uint8_t* et = a.e_tiles + (size_t)tile * kRows * K * 2;
-    const float4* tt = reinterpret_cast<const float4*>(a.t_tiles + (size_t)tile * kRows * K);
+    const uint4* tt = a.t_tiles + (size_t)tile * kRows * (K / 8);
     uint8_t* aet = a.ae_tiles + (size_t)tile * kRows * NTOT * 2;
     if (role == 0) {  // one-hot block of the gram's B operand: beta / sum at column a
-      for (int c8 = 8 * sub; c8 < a.NB; c8 += 16) {
+      for (int c8 = 8 * sub; c8 < a.NB; c8 += 32) {
         float v[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) v[j] = (asg == c8 + j) ? wb : 0.f;
@@ -427,16 +457,29 @@ __global__ void __launch_bounds__(256, 1) dl_back_kernel(Dl3Args a) {
       const int buf = pc & 1, use = pc >> 1;
       if (use >= 1) tc::mbar_wait(&bar[buf], (use - 1) & 1);  // MMAs that read sD[buf] are done
       uint8_t* sD = sD0 + buf * 32768;
-      const int kb = role * KH + p * 128 + sub * 64;  // key of this thread's first column
+      const int kb = role * KH + p * 128 + sub * 32;  // key of this thread's first column
+      // all loads of the block first (the ae stores below could otherwise alias them)
+      uint4 ev[4], th[4];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < 4; ++q) {
         const int c = kb + 8 * q;
+        ev[q] = *reinterpret_cast<const uint4*>(et + tc::core_off(row, c, 128u, kCS));
+        th[q] = tt[(size_t)(c / 8) * kRows + row];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = kb + 8 * q;
+        const uint32_t w4[4] = {ev[q].x, ev[q].y, ev[q].z, ev[q].w};
         float e[8];
-        tc::ld_row8(et, row, c, kCS, e);
-        const float4 t0 = tt[(size_t)(c / 4) * kRows + row], t1 = tt[(size_t)(c / 4 + 1) * kRows + row];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          e[2 * k] = __uint_as_float(w4[k] << 16);
+          e[2 * k + 1] = __uint_as_float(w4[k] & 0xffff0000u);
+        }
         const float4 g0 = __ldg(reinterpret_cast<const float4*>(gp + c));
         const float4 g1 = __ldg(reinterpret_cast<const float4*>(gp + c + 4));
-        const float tv[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+        float tv[8];
+        unpack_h8(th[q], tv);
         const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
         float d[8], w8[8];
 #pragma unroll
@@ -444,7 +487,7 @@ __global__ void __launch_bounds__(256, 1) dl_back_kernel(Dl3Args a) {
           d[j] = e[j] * ps * fmaf(al_t, tv[j], fmaf(be, gv[j], -cc));
           w8[j] = e[j] * wa;
         }
-        tc::st_row8(sD, row, sub * 64 + 8 * q, kCS, d);
+        tc::st_row8(sD, row, sub * 32 + 8 * q, kCS, d);
         tc::st_row8(aet, row, c, kCS, w8);
       }
       tc::fence_async_smem();
@@ -474,13 +517,12 @@ __global__ void __launch_bounds__(256, 1) dl_back_kernel(Dl3Args a) {
     }
     // dQ: this role's half of the key sum; exactly two adds onto the zeroed row (order-free)
     {
-      float v[DS / 2];
-#pragma unroll
-      for (int c = 0; c < DS / 2; c += 16) tc::tmem_ld16(tl + sub * (DS / 2) + c, v + c);
+      float v[DQ];
+      tmem_ldq<DQ>(tl + sub * DQ, v);
       if (row < valid) {
-        float* dst = a.d_query + (r0 + row) * DS + sub * (DS / 2);
+        float4* dst = reinterpret_cast<float4*>(a.d_query + (r0 + row) * DS + sub * DQ);
 #pragma unroll
-        for (int c = 0; c < DS / 2; ++c) atomicAdd(dst + c, v[c]);
+        for (int c = 0; c < DQ; c += 4) atomicAdd(dst + c / 4, make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]));
       }
     }
     tc::tc_fence_before();
@@ -489,20 +531,17 @@ __global__ void __launch_bounds__(256, 1) dl_back_kernel(Dl3Args a) {
   if (a.want_grad) {
     // R^T partial of this CTA: accumulator lane = key within the 128-key block
     for (int p = 0; p < PB; ++p) {
-      float* dst = a.r_part + ((size_t)blockIdx.x * KH + p * 128 + row) * DS + sub * (DS / 2);
+      float* dst = a.r_part + ((size_t)blockIdx.x * KH + p * 128 + row) * DS + sub * DQ;
+      float v[DQ];
+      if (first) {
 #pragma unroll
-      for (int c = 0; c < DS / 2; c += 16) {
-        float v[16];
-        if (first) {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = 0.f;
-        } else {
-          tc::tmem_ld16(tl + DS + p * DS + sub * (DS / 2) + c, v);
-        }
-#pragma unroll
-        for (int i = 0; i < 16; i += 4)
-          *reinterpret_cast<float4*>(dst + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        for (int i = 0; i < DQ; ++i) v[i] = 0.f;
+      } else {
+        tmem_ldq<DQ>(tl + DS + p * DS + sub * DQ, v);
       }
+#pragma unroll
+      for (int i = 0; i < DQ; i += 4)
+        *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
     }
   }
   cos_acc = warp_sum_d(cos_acc);
@@ -517,7 +556,7 @@ __global__ void __launch_bounds__(256, 1) dl_back_kernel(Dl3Args a) {
   __syncthreads();
   if (tid == 0) {
     double c0s = 0, c1s = 0, c2s = 0;
-    for (int w = 0; w < 8; ++w) c0s += s_loss[w][0], c1s += s_loss[w][1], c2s += s_loss[w][2];
+    for (int w = 0; w < 16; ++w) c0s += s_loss[w][0], c1s += s_loss[w][1], c2s += s_loss[w][2];
     a.loss_part[blockIdx.x * 4 + 0] = c0s;
     a.loss_part[blockIdx.x * 4 + 1] = c1s;
     a.loss_part[blockIdx.x * 4 + 2] = c2s;
@@ -529,55 +568,84 @@ __global__ void __launch_bounds__(256, 1) dl_back_kernel(Dl3Args a) {
 struct Dl4Args {
   const uint8_t* e_tiles;   // ntiles x (128 x K)
   const uint8_t* ae_tiles;  // ntiles x (128 x NTOT)
-  int nunits;
+  int nunits_a, splits_a, nunits_b, splits_b;
   int64_t ntiles;
   int K, NTOT;
-  float* part;              // splits x K x NTOT (only the units' blocks are written)
+  float* part;              // max(splits) x K x NTOT (only the units' blocks are written)
 };
 
-constexpr uint32_t kG_A = 32768, kG_B = 65536;
+// One stage = 64 pixel rows (half a tile) of the A operand (256 keys) and of the B operand (w
+// columns), copied as 1 KB column-group pieces into a 64-row core-matrix layout (column-group
+// stride 1024 B). Output tile 256 keys x w in two TMEM accumulators: 128 KB of operands per
+// 16.8 MFLOP, a third less L2 traffic per flop than 128-key units (the gram is L2-bound).
+constexpr int kG_Stages = 3;
+constexpr uint32_t kG_Half = 32768, kG_Stage = 2 * kG_Half, kG_CS = 1024;
 
-__global__ void __launch_bounds__(192, 1) dl_gram_kernel(Dl4Args a) {
+// One 4-D TMA box: 64 rows (two 512-byte row pieces) x `box_cg` column groups of one tile.
+__device__ __forceinline__ void tma_half(void* dst, const CUtensorMap* map, int piece, int cg, int64_t tile,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(tc::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(piece), "r"(cg), "r"((int)tile), "r"(tc::smem_u32(bar))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(192, 1) dl_gram_kernel(const __grid_constant__ CUtensorMap tm_e,
+                                                         const __grid_constant__ CUtensorMap tm_ae,
+                                                         const __grid_constant__ CUtensorMap tm_oh, Dl4Args a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t full[2], empty[2], accf;
+  __shared__ uint64_t full[kG_Stages], empty[kG_Stages], accf;
   __shared__ uint32_t s_taddr;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int unit = blockIdx.x % a.nunits, split = blockIdx.x / a.nunits;
-  const int splits = gridDim.x / a.nunits;
-  // unit -> (M block mb of 128 keys, N chunk nc of 256 columns): per mb the chunks
-  // [mb / 2, nchunks) -- the upper-triangle blocks of A and every Bm chunk
-  const int nchunks = (a.NTOT + 255) / 256;
-  int mb = 0, rem = unit;
-  while (rem >= nchunks - mb / 2) rem -= nchunks - mb / 2, ++mb;
-  const int nc = mb / 2 + rem;
+  // CTA -> (unit, row split). A units: M pair mp (keys [256 mp, +256)) x N chunk nc in
+  // [mp, K / 256) (upper triangle of the symmetric A); Bm units: every mp x the chunks >= K / 256.
+  // A units take splits_a row ranges, the narrower Bm units splits_b.
+  const int KC = a.K / 256, nchunks = (a.NTOT + 255) / 256, nbc = nchunks - KC;
+  int cta = blockIdx.x, splits, split, mp = 0, nc;
+  if (cta < a.nunits_a * a.splits_a) {
+    splits = a.splits_a;
+    split = cta / a.nunits_a;
+    int rem = cta % a.nunits_a;
+    while (rem >= KC - mp) rem -= KC - mp, ++mp;
+    nc = mp + rem;
+  } else {
+    cta -= a.nunits_a * a.splits_a;
+    splits = a.splits_b;
+    split = cta / a.nunits_b;
+    const int rem = cta % a.nunits_b;
+    mp = rem / nbc;
+    nc = KC + rem % nbc;
+  }
   const int w = min(256, a.NTOT - nc * 256);
   const int64_t t0 = split * a.ntiles / splits, t1 = (split + 1) * a.ntiles / splits;
-  auto sA = [&](int s) { return smem + s * (kG_A + kG_B); };
-  auto sB = [&](int s) { return smem + s * (kG_A + kG_B) + kG_A; };
   if (tid == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kG_Stages; ++i) {
       tc::mbar_init(&full[i], 1);
       tc::mbar_init(&empty[i], 1);
     }
     tc::mbar_init(&accf, 1);
     tc::fence_mbar_init();
   }
-  if (warp == 0) tc::tmem_alloc<256>(&s_taddr);
+  if (warp == 0) tc::tmem_alloc<512>(&s_taddr);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = s_taddr;
-  const size_t etb = (size_t)kRows * a.K * 2, aetb = (size_t)kRows * a.NTOT * 2;
   if (warp == 4) {
     if (lane == 0) {
       int st = 0;
       uint32_t ph = 0;
+      const CUtensorMap* mb = nc < KC ? &tm_ae : &tm_oh;
       for (int64_t t = t0; t < t1; ++t) {
-        tc::mbar_wait(&empty[st], ph ^ 1);
-        tc::mbar_expect_tx(&full[st], kG_A + (uint32_t)w * 256u);
-        tc::bulk_g2s(sA(st), a.e_tiles + t * etb + (size_t)mb * kG_A, kG_A, &full[st]);
-        tc::bulk_g2s(sB(st), a.ae_tiles + t * aetb + (size_t)nc * kG_B, (uint32_t)w * 256u, &full[st]);
-        if (++st == 2) st = 0, ph ^= 1;
+        for (int hh = 0; hh < 2; ++hh) {
+          uint8_t* dst = smem + st * kG_Stage;
+          tc::mbar_wait(&empty[st], ph ^ 1);
+          tc::mbar_expect_tx(&full[st], kG_Half + (uint32_t)w * 128u);
+          tma_half(dst, &tm_e, 2 * hh, 32 * mp, t, &full[st]);
+          tma_half(dst + kG_Half, mb, 2 * hh, 32 * nc, t, &full[st]);
+          if (++st == kG_Stages) st = 0, ph ^= 1;
+        }
       }
     }
   } else if (warp == 5) {
@@ -586,15 +654,19 @@ __global__ void __launch_bounds__(192, 1) dl_gram_kernel(Dl4Args a) {
       int st = 0;
       uint32_t ph = 0;
       for (int64_t t = t0; t < t1; ++t) {
-        tc::mbar_wait(&full[st], ph);
-        tc::tc_fence_after();
-        const uint32_t aa = tc::smem_u32(sA(st)), ab = tc::smem_u32(sB(st));
+        for (int hh = 0; hh < 2; ++hh) {
+          tc::mbar_wait(&full[st], ph);
+          tc::tc_fence_after();
+          const uint32_t as = tc::smem_u32(smem + st * kG_Stage), bs = as + kG_Half;
 #pragma unroll
-        for (int ks = 0; ks < 8; ++ks)
-          tc::mma_bf16(tmem, tc::make_sdesc(aa + ks * 2 * 128, 128, kCS), tc::make_sdesc(ab + ks * 2 * 128, 128, kCS),
-                       idesc, (t > t0) || ks > 0);
-        tc::mma_commit(&empty[st]);
-        if (++st == 2) st = 0, ph ^= 1;
+          for (int m2 = 0; m2 < 2; ++m2)
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks)
+              tc::mma_bf16(tmem + m2 * 256, tc::make_sdesc(as + m2 * 16 * kG_CS + ks * 2 * 128, 128, kG_CS),
+                           tc::make_sdesc(bs + ks * 2 * 128, 128, kG_CS), idesc, (t > t0) || hh > 0 || ks > 0);
+          tc::mma_commit(&empty[st]);
+          if (++st == kG_Stages) st = 0, ph ^= 1;
+        }
       }
       tc::mma_commit(&accf);
     }
@@ -604,30 +676,33 @@ __global__ void __launch_bounds__(192, 1) dl_gram_kernel(Dl4Args a) {
       tc::mbar_wait(&accf, 0);
       tc::tc_fence_after();
     }
-    float* dst = a.part + ((size_t)split * a.K + mb * 128 + row) * a.NTOT + nc * 256;
-    for (int c = 0; c < w; c += 16) {
-      float v[16];
-      if (t1 > t0) {
-        tc::tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + c, v);
-      } else {
+    for (int m2 = 0; m2 < 2; ++m2) {
+      float* dst = a.part + ((size_t)split * a.K + mp * 256 + m2 * 128 + row) * a.NTOT + nc * 256;
+      for (int c = 0; c < w; c += 16) {
+        float v[16];
+        if (t1 > t0) {
+          tc::tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + m2 * 256 + c, v);
+        } else {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = 0.f;
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < 16; i += 4)
+          *reinterpret_cast<float4*>(dst + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
       }
-#pragma unroll
-      for (int i = 0; i < 16; i += 4)
-        *reinterpret_cast<float4*>(dst + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
     }
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 0) tc::tmem_free<256>(tmem);
+  if (warp == 0) tc::tmem_free<512>(tmem);
 }
 
 // ------------------------------------------------------------------------------------------ DL5
 // A (K x K) += sum over splits of the gram partial at (min(i,j), max(i,j)) (A is symmetric; only
-// upper-triangle units were computed); Bm^T (n_set x K) = the partial's columns K..K+n_set;
+// upper-triangle units were computed: (min, max) always lies in one); Bm^T (n_set x K) = the partial's columns K..K+n_set;
 // R (DS x K) += sum over the DL3 CTAs of their R^T partials; loss partials folded once.
-__global__ void __launch_bounds__(256) dl_reduce_kernel(const float* __restrict__ part, int splits, int K, int NTOT,
+__global__ void __launch_bounds__(256) dl_reduce_kernel(const float* __restrict__ part, int splits_a, int splits_b,
+                                                        int K, int NTOT,
                                                         int n_set, const float* __restrict__ r_part, int r_groups,
                                                         int DS, const double* __restrict__ loss_part, int loss_n,
                                                         float* A, float* bmt, float* R, double* partials) {
@@ -649,14 +724,14 @@ __global__ void __launch_bounds__(256) dl_reduce_kernel(const float* __restrict_
       const int i = (int)(q / K), j = (int)(q % K);
       const size_t o = (size_t)min(i, j) * NTOT + max(i, j);
       float s = 0.f;
-      for (int sp = 0; sp < splits; ++sp) s += part[sp * pstride + o];
+      for (int sp = 0; sp < splits_a; ++sp) s += part[sp * pstride + o];
       A[q] += s;
     } else if (q < na + nb) {
       const int64_t e = q - na;
       const int s_ = (int)(e / K), k = (int)(e % K);
       const size_t o = (size_t)k * NTOT + K + s_;
       float s = 0.f;
-      for (int sp = 0; sp < splits; ++sp) s += part[sp * pstride + o];
+      for (int sp = 0; sp < splits_b; ++sp) s += part[sp * pstride + o];
       bmt[e] = s;
     } else {
       const int64_t e = q - na - nb;
@@ -673,11 +748,48 @@ constexpr int kBackGroups = 74;  // DL3 grid = 2 roles x 74 groups
 
 int nb_for(int64_t n_set) { return (int)std::max<int64_t>(16, (n_set + 15) / 16 * 16); }
 
-int dl_units(int K, int NTOT) {
-  const int nchunks = (NTOT + 255) / 256;
-  int n = 0;
-  for (int mb = 0; mb < K / 128; ++mb) n += nchunks - mb / 2;
-  return n;
+// Gram work split: na A units of 256 x 256 (upper triangle), nbu Bm units of 256 x (NB per
+// chunk), sa / sb row splits of each, sa * na + sb * nbu <= 148 CTAs of about equal MMA work.
+void dl_gram_plan(int K, int NB, int64_t ntiles, int& na, int& nbu, int& sa, int& sb) {
+  const int KC = K / 256, nbc = (NB + 255) / 256;
+  na = KC * (KC + 1) / 2;
+  nbu = KC * nbc;
+  const double wb = (double)std::min(NB, 256) / 256.0 * nbc;  // Bm work per unit, in A units
+  const double per = (na + nbu * wb) / 148.0;                  // work per CTA
+  sa = std::max(1, (int)(1.0 / per));
+  sb = std::max(1, (int)(wb / per));
+  while (na * sa + nbu * sb > 148 && (sa > 1 || sb > 1)) {
+    if (sa >= sb && sa > 1) --sa; else --sb;
+  }
+  sa = (int)std::min<int64_t>(sa, ntiles);
+  sb = (int)std::min<int64_t>(sb, ntiles);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&fn), cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+  }
+  return fn;
+}
+
+// A tile array [ntiles][ncg column groups][128 rows][8 bf16] viewed as the 4-D tensor
+// (256 elements = 32 rows x 8, 4 row pieces, ncg, ntiles); a box of (256, 2, box_cg, 1) is 64
+// rows x box_cg column groups, landing in shared memory as a 64-row core-matrix tile.
+bool half_tile_map(CUtensorMap* m, const void* base, int ncg, int64_t ntiles, int box_cg) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {256, 4, (cuuint64_t)ncg, (cuuint64_t)ntiles};
+  cuuint64_t strides[3] = {512, 2048, (cuuint64_t)ncg * 2048};
+  cuuint32_t box[4] = {256, 2, (cuuint32_t)box_cg, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <typename F>
@@ -703,12 +815,12 @@ void launch_dl(cudaStream_t st, DecoderWork& w, const float* query, const int32_
               d_query, want_grad ? 1 : 0};
     const size_t sm = (size_t)K * DS * 2 + (size_t)kRows * DS * 2;
     set_smem(dl_softmax_kernel<DS>, sm);
-    dl_softmax_kernel<DS><<<148, 256, sm, st>>>(d);
+    dl_softmax_kernel<DS><<<148, 512, sm, st>>>(d);
     count_launch();
   }
   // DL2
   {
-    Dl2Args d{w.e_tiles, w.dl_mt, w.dl_t, w.dl_nu, npx, K};
+    Dl2Args d{w.e_tiles, w.dl_mt, reinterpret_cast<uint4*>(w.dl_t), w.dl_nu, npx, K};
     const size_t sm = (size_t)kT_Stages * (kT_A + kT_B);
     set_smem(dl_t_kernel, sm);
     const int64_t units = ntiles * (K / 256);
@@ -717,34 +829,44 @@ void launch_dl(cudaStream_t st, DecoderWork& w, const float* query, const int32_
   }
   // DL3
   {
-    Dl3Args d{w.e_tiles, w.dl_t, w.dl_nu, reinterpret_cast<const float4*>(w.row_stats), query, assignment, w.kd,
+    Dl3Args d{w.e_tiles, reinterpret_cast<const uint4*>(w.dl_t), w.dl_nu, reinterpret_cast<const float4*>(w.row_stats), query, assignment, w.kd,
               w.gt, w.nv, w.dl_ae, d_query, w.r_part, w.loss_part, npx, K, NB, inv_temp, lambda_cos, lambda_l2,
               n_sup > 0 ? 1.f / (float)n_sup : 0.f, scale, want_grad ? 1 : 0};
     const size_t sm = (size_t)(K / 2) * DS * 2 + (size_t)kRows * DS * 2 + 2 * 32768;
     set_smem(dl_back_kernel<DS>, sm);
-    dl_back_kernel<DS><<<2 * kBackGroups, 256, sm, st>>>(d);
+    dl_back_kernel<DS><<<2 * kBackGroups, 512, sm, st>>>(d);
     count_launch();
   }
   if (!want_grad) {
-    dl_reduce_kernel<<<1, 32, 0, st>>>(nullptr, 0, 0, 0, 0, nullptr, 0, 0, w.loss_part, 2 * kBackGroups,
+    dl_reduce_kernel<<<1, 32, 0, st>>>(nullptr, 0, 0, 0, 0, 0, nullptr, 0, 0, w.loss_part, 2 * kBackGroups,
                                         nullptr, nullptr, nullptr, partials);
     count_launch();
     return;
   }
-  // DL4: units = upper-triangle blocks of A + the Bm columns
-  const int nunits = dl_units(K, NTOT);
-  const int splits = std::max(1, std::min<int>(148 / nunits, (int)ntiles));
+  // DL4: units = upper-triangle blocks of A (full 256-column chunks) + the Bm chunks (NB <= 256
+  // columns); row splits chosen so each CTA gets about 1/148 of the MMA work
+  int na, nbu, sa, sb;
+  dl_gram_plan(K, NB, ntiles, na, nbu, sa, sb);
   {
-    Dl4Args d{w.e_tiles, w.dl_ae, nunits, ntiles, K, NTOT, w.dl_part};
-    const size_t sm = 2 * (size_t)(kG_A + kG_B);
+    Dl4Args d{w.e_tiles, w.dl_ae, na, sa, nbu, sb, ntiles, K, NTOT, w.dl_part};
+    const size_t sm = (size_t)kG_Stages * kG_Stage;
     set_smem(dl_gram_kernel, sm);
-    dl_gram_kernel<<<nunits * splits, 192, sm, st>>>(d);
+    CUtensorMap tm_e, tm_ae, tm_oh;
+    const bool ok = half_tile_map(&tm_e, w.e_tiles, K / 8, ntiles, 32) &&
+                    half_tile_map(&tm_ae, w.dl_ae, NTOT / 8, ntiles, 32) &&
+                    half_tile_map(&tm_oh, w.dl_ae, NTOT / 8, ntiles, std::min(NB, 256) / 8);
+    if (!ok) {
+      cudaGetLastError();
+      set_sticky_error("decoder_dl: cuTensorMapEncodeTiled unavailable or rejected the gram operand maps");
+      return;
+    }
+    dl_gram_kernel<<<na * sa + nbu * sb, 192, sm, st>>>(tm_e, tm_ae, tm_oh, d);
     count_launch();
   }
   {
     const int64_t total = (int64_t)K * K + n_set * K + (int64_t)DS * K;
     dl_reduce_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, st>>>(
-        w.dl_part, splits, K, NTOT, (int)n_set, w.r_part, kBackGroups, DS, w.loss_part, 2 * kBackGroups, w.a_acc,
+        w.dl_part, sa, sb, K, NTOT, (int)n_set, w.r_part, kBackGroups, DS, w.loss_part, 2 * kBackGroups, w.a_acc,
         w.bm, w.r_acc, partials);
     count_launch();
   }
@@ -757,9 +879,14 @@ bool decoder_dl_supported(int64_t k, int ds, int64_t n_set) {
 }
 
 size_t decoder_dl_part_floats(int64_t k) {
-  // gram partials: splits x K x (K + NB) with splits <= 148 / units and NB <= 256
-  const int kk = (int)k, least = dl_units(kk, kk + 16);
-  return (size_t)(148 / least) * (size_t)k * (size_t)(k + 256);
+  // gram partials: max(splits) x K x (K + NB), NB <= 256
+  int smax = 1;
+  for (int nb = 16; nb <= 256; nb += 16) {
+    int na, nbu, sa, sb;
+    dl_gram_plan((int)k, nb, 1 << 30, na, nbu, sa, sb);
+    smax = std::max(smax, std::max(sa, sb));
+  }
+  return (size_t)smax * (size_t)k * (size_t)(k + 256);
 }
 
 void decoder_dl_prepare(cudaStream_t st, DecoderWork& w) {

@@ -99,7 +99,7 @@ struct DecoderWork {
   bool tc_pending = false;     // a_acc / r_acc hold contributions not yet applied
   // staged large-K tcgen05 path scratch (decoder_dl.cu)
   uint8_t* dl_mt = nullptr;    // K x K bf16: M in the B-operand blocks of the T GEMM
-  float* dl_t = nullptr;       // ntiles x 128 x K fp32: T = e M (aliases buf1)
+  float* dl_t = nullptr;       // ntiles x 128 x K fp16: T = e M (aliases buf1)
   uint8_t* dl_ae = nullptr;    // ntiles x 128 x (K + NB) bf16: gram B operand (aliases buf2)
   float* dl_nu = nullptr;      // (K/256) x ntiles*128: partial e.T per 256-column unit
   float* dl_part = nullptr;    // gram partials
@@ -152,6 +152,10 @@ void adam_flat(cudaStream_t st, float* param, const float* grad, float* m, float
 int umma_selftest(cudaStream_t st, const float* A, const float* B, float* C, int N, int K, int a_mn, int b_mn);
 
 void set_launch_counter(int64_t* c);
+// Host-side failure inside a launcher (no CUDA error to carry it): recorded here, reported and
+// cleared by the next post-launch check of the C-ABI.
+void set_sticky_error(const char* msg);
+const char* take_sticky_error();
 void count_launch(int n = 1);
 
 }  // namespace lm
