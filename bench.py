@@ -310,6 +310,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-phases", type=int, default=1)
+    ap.add_argument("--decoder-path", type=int, default=0,
+                    help="bf16 decoder kernels: 0 auto, 1 fused on-chip, 2 staged (experiments)")
     args = ap.parse_args()
 
     if args.config == 3 and args.impl == "ours":
@@ -352,6 +354,7 @@ def main():
 
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
     ctx = api.Context(local_rank)
+    ctx.set_decoder_path(args.decoder_path)
     w = synthetic.make_workload(args.config, gpu_render_fn(ctx))
     from paper_2602_12314_b200.sharding import rank_plan
 

@@ -991,7 +991,7 @@ latmap_status latmap_session_create(latmap_ctx* ctx, const latmap_config* cfg, i
          ok(cudaMalloc(&d.r, sizeof(float) * ds * k)) && ok(cudaMalloc(&d.a, sizeof(float) * k * k));
   if (good && cfg->decoder_precision == 1) {
     good = ok(cudaMalloc(&d.row_stats, sizeof(float) * 4 * npx)) &&
-           ok(cudaMalloc(&d.r_part, sizeof(float) * 148 * k * ds)) &&
+           ok(cudaMalloc(&d.r_part, sizeof(float) * 2 * 148 * k * ds)) &&
            ok(cudaMalloc(&d.a_part, sizeof(float) * 74 * 2 * k * (k / 2 + 1))) &&
            ok(cudaMalloc(&d.bm_part, sizeof(float) * 74 * k * 64)) &&
            ok(cudaMalloc(&d.loss_part, sizeof(double) * 148 * 4)) &&

@@ -220,6 +220,96 @@ __global__ void row_norms_kernel(const float* __restrict__ x, int64_t n, int d, 
   if (lane == 0) out[r] = sqrtf(s);
 }
 
+// Per-frame target scores and norms: G[s][k] = E[s] . D[k] (G = E D^T), nv[s] = |E[s]|.
+// CTA = 8 target rows x 32 keys (E rows staged in shared memory); each warp takes 4 keys at a
+// time with 4 x (df / 128) independent float4 loads of D in flight per lane. Requires df % 4 == 0.
+constexpr int kTsRows = 8, kTsKeys = 32;
+__global__ void __launch_bounds__(256) target_scores_kernel(const float* __restrict__ feats,
+                                                            const float* __restrict__ atoms, int64_t n_set, int k,
+                                                            int df, float* __restrict__ gt, float* __restrict__ nv) {
+  extern __shared__ __align__(16) float s_e[];  // kTsRows x df
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t s0 = (int64_t)blockIdx.x * kTsRows;
+  const int nr = (int)(n_set - s0 < kTsRows ? n_set - s0 : kTsRows);
+  const int k0 = blockIdx.y * kTsKeys;
+  for (int i = tid; i < kTsRows * df / 4; i += blockDim.x) {
+    const int r = i / (df / 4);
+    reinterpret_cast<float4*>(s_e)[i] =
+        r < nr ? __ldg(reinterpret_cast<const float4*>(feats + (s0 + r) * df) + i % (df / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __syncthreads();
+  if (blockIdx.y == 0 && warp < nr) {  // norms of the CTA's rows
+    float sq = 0.f;
+    for (int j = lane; j < df; j += 32) sq += s_e[warp * df + j] * s_e[warp * df + j];
+    sq = warp_sum(sq);
+    if (lane == 0) nv[s0 + warp] = sqrtf(sq);
+  }
+  const float4* e4 = reinterpret_cast<const float4*>(s_e);
+  for (int kq = k0 + 4 * warp; kq < min(k, k0 + kTsKeys); kq += 32) {
+    float acc[4][kTsRows];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int r = 0; r < kTsRows; ++r) acc[u][r] = 0.f;
+    for (int j = lane; j < df / 4; j += 32) {
+      float4 d[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        d[u] = kq + u < k ? __ldg(reinterpret_cast<const float4*>(atoms + (size_t)(kq + u) * df) + j)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int r = 0; r < kTsRows; ++r) {
+        const float4 e = e4[r * (df / 4) + j];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          acc[u][r] = fmaf(d[u].x, e.x, fmaf(d[u].y, e.y, fmaf(d[u].z, e.z, fmaf(d[u].w, e.w, acc[u][r]))));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int r = 0; r < kTsRows; ++r) {
+        const float v = warp_sum(acc[u][r]);
+        if (lane == 0 && r < nr && kq + u < k) gt[(s0 + r) * k + kq + u] = v;
+      }
+  }
+}
+
+// d_atoms[k][:] += sum_s Bm^T[s][k] E[s][:]  (the frame's Bm E term). CTA = 4 keys x 128
+// float4 columns; the E row load of each s is shared by the 4 keys. Requires df % 4 == 0.
+__global__ void __launch_bounds__(128) bm_embed_kernel(const float* __restrict__ bmt, const float* __restrict__ feats,
+                                                       int64_t n_set, int k, int df, float* __restrict__ d_atoms) {
+  const int k0 = blockIdx.x * 4;
+  const int c4 = blockIdx.y * blockDim.x + threadIdx.x;
+  if (c4 >= df / 4) return;
+  float4 acc[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+  for (int64_t sidx = 0; sidx < n_set; ++sidx) {
+    const float4 e = __ldg(reinterpret_cast<const float4*>(feats + sidx * df) + c4);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float b = k0 + u < k ? __ldg(bmt + sidx * k + k0 + u) : 0.f;
+      acc[u].x = fmaf(b, e.x, acc[u].x);
+      acc[u].y = fmaf(b, e.y, acc[u].y);
+      acc[u].z = fmaf(b, e.z, acc[u].z);
+      acc[u].w = fmaf(b, e.w, acc[u].w);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    if (k0 + u >= k) break;
+    float4* dst = reinterpret_cast<float4*>(d_atoms + (size_t)(k0 + u) * df) + c4;
+    float4 d = *dst;
+    d.x += acc[u].x;
+    d.y += acc[u].y;
+    d.z += acc[u].z;
+    d.w += acc[u].w;
+    *dst = d;
+  }
+}
+
 // softmax backward rows (dictionary.cpp:69-74): d = P * (d - rowdot(P, d)) / temperature
 __global__ void softmax_bwd_rows_kernel(const float* __restrict__ P, float* __restrict__ d, int64_t n, int k,
                                         float temperature) {
@@ -329,6 +419,7 @@ void decoder_prepare(cudaStream_t st, DecoderWork& w, const float* atoms, const 
   if (w.a_acc) cudaMemsetAsync(w.a_acc, 0, sizeof(float) * w.k * w.k, st);
   if (w.r_acc) cudaMemsetAsync(w.r_acc, 0, sizeof(float) * w.ds * w.k, st);
   w.tc_pending = false;
+  w.tc_frames = 0;
 }
 
 void decoder_frame(cudaStream_t st, DecoderWork& w, const float* query, const int32_t* assignment, int64_t npx,
@@ -339,9 +430,7 @@ void decoder_frame(cudaStream_t st, DecoderWork& w, const float* query, const in
   const int ds = w.ds, df = w.df;
   const float inv_temp = 1.f / temperature;
   // per-frame target scores G^T = E D^T (n_set x K) and target norms
-  sgemm(st, false, true, n_set, k, df, 1.f, feats, df, atoms, df, 0.f, w.gt, k);
-  row_norms_kernel<<<grid_for(n_set * 32, 256), 256, 0, st>>>(feats, n_set, df, w.nv);
-  count_launch();
+  decoder_targets(st, feats, n_set, atoms, k, df, w.gt, w.nv);
   // S = Q Kd^T / temperature ; P = softmax(S)
   sgemm(st, false, true, npx, k, ds, inv_temp, query, ds, w.kd, ds, 0.f, w.buf1, k);
   softmax_rows_kernel<<<grid_for(npx * 32, 256, 1 << 30), 256, 0, st>>>(w.buf1, npx, (int)k);
@@ -373,7 +462,7 @@ void decoder_frame(cudaStream_t st, DecoderWork& w, const float* query, const in
   sgemm(st, true, false, k, k, npx, 1.f, w.buf1, k, w.buf2, k, 0.f, w.a, k, split_for(k, k, npx));
   // d_atoms += A D + Bm E + R^T W ;  d_proj += R D
   sgemm(st, false, false, k, df, k, 1.f, w.a, k, atoms, df, 1.f, d_atoms, df);
-  sgemm(st, true, false, k, df, n_set, 1.f, w.bm, k, feats, df, 1.f, d_atoms, df);
+  decoder_bm_embed(st, w.bm, feats, n_set, k, df, d_atoms);
   sgemm(st, true, false, k, df, ds, 1.f, w.r, k, proj, df, 1.f, d_atoms, df);
   sgemm(st, false, false, ds, df, k, 1.f, w.r, k, atoms, df, 1.f, d_proj, df);
 }
@@ -381,6 +470,33 @@ void decoder_frame(cudaStream_t st, DecoderWork& w, const float* query, const in
 void decoder_target_norms(cudaStream_t st, const float* feats, int64_t n_set, int df, float* nv) {
   row_norms_kernel<<<grid_for(n_set * 32, 256), 256, 0, st>>>(feats, n_set, df, nv);
   count_launch();
+}
+
+void decoder_targets(cudaStream_t st, const float* feats, int64_t n_set, const float* atoms, int64_t k, int df,
+                     float* gt, float* nv) {
+  if (n_set <= 0) return;
+  if (df % 4 == 0 && (reinterpret_cast<uintptr_t>(feats) & 15) == 0 && (reinterpret_cast<uintptr_t>(atoms) & 15) == 0) {
+    const size_t sm = sizeof(float) * kTsRows * df;
+    if (sm > 48 * 1024) cudaFuncSetAttribute(target_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    dim3 grid((unsigned)((n_set + kTsRows - 1) / kTsRows), (unsigned)((k + kTsKeys - 1) / kTsKeys));
+    target_scores_kernel<<<grid, 256, sm, st>>>(feats, atoms, n_set, (int)k, df, gt, nv);
+    count_launch();
+  } else {
+    sgemm(st, false, true, n_set, k, df, 1.f, feats, df, atoms, df, 0.f, gt, k);
+    decoder_target_norms(st, feats, n_set, df, nv);
+  }
+}
+
+void decoder_bm_embed(cudaStream_t st, const float* bmt, const float* feats, int64_t n_set, int64_t k, int df,
+                      float* d_atoms) {
+  if (n_set <= 0) return;
+  if (df % 4 == 0 && (reinterpret_cast<uintptr_t>(feats) & 15) == 0 && (reinterpret_cast<uintptr_t>(d_atoms) & 15) == 0) {
+    dim3 grid((unsigned)((k + 3) / 4), (unsigned)((df / 4 + 127) / 128));
+    bm_embed_kernel<<<grid, 128, 0, st>>>(bmt, feats, n_set, (int)k, df, d_atoms);
+    count_launch();
+  } else {
+    sgemm(st, true, false, k, df, n_set, 1.f, bmt, k, feats, df, 1.f, d_atoms, df);
+  }
 }
 
 void reconstruct(cudaStream_t st, const float* q, int64_t n, int ds, const float* atoms, const float* proj, int64_t k,

@@ -830,7 +830,7 @@ void launch_dl(cudaStream_t st, DecoderWork& w, const float* query, const int32_
   // DL3
   {
     Dl3Args d{w.e_tiles, reinterpret_cast<const uint4*>(w.dl_t), w.dl_nu, reinterpret_cast<const float4*>(w.row_stats), query, assignment, w.kd,
-              w.gt, w.nv, w.dl_ae, d_query, w.r_part, w.loss_part, npx, K, NB, inv_temp, lambda_cos, lambda_l2,
+              w.gt, w.nv, w.dl_ae, d_query, w.r_part + 148 * (size_t)K * DS, w.loss_part, npx, K, NB, inv_temp, lambda_cos, lambda_l2,
               n_sup > 0 ? 1.f / (float)n_sup : 0.f, scale, want_grad ? 1 : 0};
     const size_t sm = (size_t)(K / 2) * DS * 2 + (size_t)kRows * DS * 2 + 2 * 32768;
     set_smem(dl_back_kernel<DS>, sm);
@@ -866,7 +866,7 @@ void launch_dl(cudaStream_t st, DecoderWork& w, const float* query, const int32_
   {
     const int64_t total = (int64_t)K * K + n_set * K + (int64_t)DS * K;
     dl_reduce_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, st>>>(
-        w.dl_part, sa, sb, K, NTOT, (int)n_set, w.r_part, kBackGroups, DS, w.loss_part, 2 * kBackGroups, w.a_acc,
+        w.dl_part, sa, sb, K, NTOT, (int)n_set, w.r_part + 148 * (size_t)K * DS, kBackGroups, DS, w.loss_part, 2 * kBackGroups, w.a_acc,
         w.bm, w.r_acc, partials);
     count_launch();
   }
@@ -903,8 +903,7 @@ void decoder_frame_dl(cudaStream_t st, DecoderWork& w, const float* query, const
                       float* d_atoms, double* partials) {
   const int64_t k = w.k;
   const int df = w.df;
-  sgemm(st, false, true, n_set, k, df, 1.f, feats, df, atoms, df, 0.f, w.gt, k);
-  decoder_target_norms(st, feats, n_set, df, w.nv);
+  decoder_targets(st, feats, n_set, atoms, k, df, w.gt, w.nv);
   if (w.ds == 64)
     launch_dl<64>(st, w, query, assignment, npx, n_set, n_sup, temperature, lambda_cos, lambda_l2, scale, want_grad,
                   d_query, partials);
@@ -912,7 +911,7 @@ void decoder_frame_dl(cudaStream_t st, DecoderWork& w, const float* query, const
     launch_dl<32>(st, w, query, assignment, npx, n_set, n_sup, temperature, lambda_cos, lambda_l2, scale, want_grad,
                   d_query, partials);
   if (!want_grad) return;
-  sgemm(st, true, false, k, df, n_set, 1.f, w.bm, k, feats, df, 1.f, d_atoms, df);
+  decoder_bm_embed(st, w.bm, feats, n_set, k, df, d_atoms);
   w.tc_pending = true;
 }
 

@@ -51,6 +51,7 @@ struct Dec1Args {
   float* r_part;            // gridDim x K x DS
   double* loss_part;        // gridDim x 4
   int want_grad;
+  int accum;                // add R^T into r_part (later frames of a step) instead of storing
 };
 
 template <int K, int DS>
@@ -310,9 +311,16 @@ __global__ void __launch_bounds__(512, 1) dec1_kernel(Dec1Args a) {
 #pragma unroll
         for (int c = 0; c < DS; c += 16) tc::tmem_ld16(tl + kColR + DS * mh + c, v + c);
       }
-      float* dst = a.r_part + ((size_t)blockIdx.x * K + mh * 128 + row) * DS;
+      float4* dst = reinterpret_cast<float4*>(a.r_part + ((size_t)blockIdx.x * K + mh * 128 + row) * DS);
 #pragma unroll
-      for (int c = 0; c < DS; ++c) dst[c] = v[c];
+      for (int c = 0; c < DS; c += 4) {
+        float4 o = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+        if (a.accum) {
+          const float4 p = dst[c / 4];
+          o.x += p.x, o.y += p.y, o.z += p.z, o.w += p.w;
+        }
+        dst[c / 4] = o;
+      }
     }
   }
   cos_acc = warp_sum_d(cos_acc);
@@ -341,8 +349,9 @@ struct Dec2Args {
   const int32_t* assign;
   const float4* row_stats;   // (max, 1/sum, alpha, beta)
   int64_t npx;
-  float* a_part;   // (gridDim/2) x 2 roles x K x (K/2)
+  float* a_part;   // (gridDim/2) x 2 roles x K x (K/2), summed over the step's frames
   float* bm_part;  // (gridDim/2) x K x 64  (role 0 only)
+  int accum;       // add A into a_part (later frames of a step) instead of storing
 };
 
 // DEC2: A[:, role half] = e^T diag(alpha / sum^2) e and (role 0) Bm = e^T Ohb with
@@ -483,8 +492,15 @@ __global__ void __launch_bounds__(288, 1) dec2_kernel(Dec2Args a) {
         } else {
           tc::tmem_ld16(tmem + ((uint32_t)(32 * g) << 16) + kColA + mh * NH + c, v);
         }
-        for (int i = 0; i < 16; i += 4)
-          *reinterpret_cast<float4*>(dst + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        for (int i = 0; i < 16; i += 4) {
+          float4* d4 = reinterpret_cast<float4*>(dst + c + i);
+          float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          if (a.accum) {
+            const float4 p = *d4;
+            o.x += p.x, o.y += p.y, o.z += p.z, o.w += p.w;
+          }
+          *d4 = o;
+        }
       }
       if (role == 0) {
         float* db = a.bm_part + ((size_t)group * K + mh * 128 + row) * NB;
@@ -506,9 +522,9 @@ __global__ void __launch_bounds__(288, 1) dec2_kernel(Dec2Args a) {
   if (warp == 0) tc::tmem_free<kTmemCols>(tmem);
 }
 
-// Sum the per-CTA partials into the step accumulators: A (K x K) from (groups x 2 roles x K x
-// K/2), R^T (K x DS) -> R (DS x K), and this frame's Bm^T (n_set x K, zeroed beforehand) from
-// (groups x K x 64). Each thread owns 4 consecutive partial entries (float4 loads) and a
+// Sum the per-CTA partials: this frame's Bm^T (n_set x K, zeroed beforehand) from (groups x K x
+// 64) after every frame (do_bm); once per step (do_ar) the step-summed partials of A (K x K)
+// from (groups x 2 roles x K x K/2) and R^T (K x DS) -> R (DS x K) into the accumulators. Each thread owns 4 consecutive partial entries (float4 loads) and a
 // 1/kRedSplit share of the groups; the shares meet in global atomics (distinct addresses).
 // Block (0, 0) also folds the loss partials into the frame's slots.
 constexpr int kRedSplit = 4;
@@ -517,11 +533,12 @@ __global__ void __launch_bounds__(256) dec_reduce_kernel(const float* __restrict
                                                          const float* __restrict__ r_part,
                                                          const double* loss_part, int K, int DS, int n_set,
                                                          int groups1, int groups2, float* A, float* bmt, float* R,
-                                                         double* partials) {
+                                                         double* partials, int do_ar, int do_bm) {
   const int NH = K / 2;
-  const int64_t qa = (int64_t)K * K / 4, qb = (int64_t)K * 64 / 4, qr = (int64_t)K * DS / 4;
+  const int64_t qa = do_ar ? (int64_t)K * K / 4 : 0, qb = do_bm ? (int64_t)K * 64 / 4 : 0,
+                qr = do_ar ? (int64_t)K * DS / 4 : 0;
   const int split = blockIdx.y;
-  if (blockIdx.x == 0 && split == 0 && threadIdx.x < 3) {
+  if (loss_part && blockIdx.x == 0 && split == 0 && threadIdx.x < 3) {
     const int which = threadIdx.x;
     double s = 0.0;
     for (int gi = 0; gi < groups1; ++gi) s += loss_part[gi * 4 + which];
@@ -592,15 +609,78 @@ __global__ void __launch_bounds__(256) dec_reduce_kernel(const float* __restrict
   }
 }
 
+// This frame's d_atoms += Bm E from DEC2's per-group Bm partials (groups x K x 64), without
+// materialising Bm^T. CTA = 2 keys, 256 threads: phase 1 sums the partials of each (key, set)
+// pair with two threads (half the groups each, 8 independent loads in flight); phase 2 forms
+// the two output rows with two threads per float4 column (half the sets each).
+__global__ void __launch_bounds__(256) bm_embed_fused_kernel(const float* __restrict__ bm_part, int groups, int K,
+                                                             const float* __restrict__ feats, int n_set, int df,
+                                                             float* __restrict__ d_atoms) {
+  __shared__ float s_half[2][128];
+  __shared__ float s_bm[2][64];
+  __shared__ float4 s_out[2][128];
+  const int tid = threadIdx.x, k0 = blockIdx.x * 2;
+  {
+    const int pair = tid & 127, hf = tid >> 7;  // (key, set) pair, half of the groups
+    const int kk = pair >> 6, sidx = pair & 63;
+    const float* src = bm_part + (size_t)(k0 + kk) * 64 + sidx;
+    const size_t gs = (size_t)K * 64;
+    const int g0 = hf ? groups / 2 : 0, g1 = hf ? groups : groups / 2;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    int g = g0;
+    for (; g + 8 <= g1; g += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[u] += __ldg(src + (size_t)(g + u) * gs);
+    }
+    for (; g < g1; ++g) acc[0] += __ldg(src + (size_t)g * gs);
+    s_half[hf][pair] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+  }
+  __syncthreads();
+  if (tid < 128) s_bm[tid >> 6][tid & 63] = s_half[0][tid] + s_half[1][tid];
+  __syncthreads();
+  const int hs = tid >> 7, s0 = hs ? n_set / 2 : 0, s1 = hs ? n_set : n_set / 2;
+  for (int cb = 0; cb < df / 4; cb += 128) {
+    const int c4 = cb + (tid & 127);
+    float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+    if (c4 < df / 4) {
+#pragma unroll 8
+      for (int sidx = s0; sidx < s1; ++sidx) {
+        const float4 e = __ldg(reinterpret_cast<const float4*>(feats + (size_t)sidx * df) + c4);
+        const float b0 = s_bm[0][sidx], b1 = s_bm[1][sidx];
+        a0.x = fmaf(b0, e.x, a0.x), a0.y = fmaf(b0, e.y, a0.y), a0.z = fmaf(b0, e.z, a0.z), a0.w = fmaf(b0, e.w, a0.w);
+        a1.x = fmaf(b1, e.x, a1.x), a1.y = fmaf(b1, e.y, a1.y), a1.z = fmaf(b1, e.z, a1.z), a1.w = fmaf(b1, e.w, a1.w);
+      }
+    }
+    if (hs == 1) {
+      s_out[0][tid & 127] = a0;
+      s_out[1][tid & 127] = a1;
+    }
+    __syncthreads();
+    if (hs == 0 && c4 < df / 4) {
+      const float4 p0 = s_out[0][tid], p1 = s_out[1][tid];
+      float4* d0 = reinterpret_cast<float4*>(d_atoms + (size_t)k0 * df) + c4;
+      float4* d1 = reinterpret_cast<float4*>(d_atoms + (size_t)(k0 + 1) * df) + c4;
+      float4 o = *d0;
+      o.x += a0.x + p0.x, o.y += a0.y + p0.y, o.z += a0.z + p0.z, o.w += a0.w + p0.w;
+      *d0 = o;
+      o = *d1;
+      o.x += a1.x + p1.x, o.y += a1.y + p1.y, o.z += a1.z + p1.z, o.w += a1.w + p1.w;
+      *d1 = o;
+    }
+    __syncthreads();
+  }
+}
+
 template <int K, int DS>
 void launch_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_t* assignment, int64_t npx,
                const float* feats, int64_t n_set, int64_t n_sup, float temperature, float lambda_cos, float lambda_l2,
                float scale, bool want_grad, float* d_query, double* partials) {
   const int g1 = 148;
   const int g2 = 148;  // 74 groups x 2 roles
+  const int accum = want_grad && w.tc_frames > 0 ? 1 : 0;
   Dec1Args d1{w.e_tiles, query, assignment, w.kd, w.mm, w.gt, w.nv, npx, 1.f / temperature, lambda_cos, lambda_l2,
               n_sup > 0 ? 1.f / (float)n_sup : 0.f, scale, d_query, reinterpret_cast<float4*>(w.row_stats),
-              w.r_part, w.loss_part, want_grad ? 1 : 0};
+              w.r_part, w.loss_part, want_grad ? 1 : 0, accum};
   const size_t sm1 = (size_t)kRows * DS * 2 + (size_t)K * DS * 2 + (size_t)kRows * K * 2 + (size_t)K * K * 2 +
                      16 * 128 * 4;
   static bool attr1 = false;
@@ -612,11 +692,11 @@ void launch_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_
   count_launch();
   if (!want_grad) {
     dec_reduce_kernel<<<dim3(1, 1), 32, 0, st>>>(nullptr, nullptr, nullptr, w.loss_part, 0, 0, 0, g1, 0, nullptr,
-                                                 nullptr, nullptr, partials);
+                                                 nullptr, nullptr, partials, 0, 0);
     count_launch();
     return;
   }
-  Dec2Args d2{w.e_tiles, assignment, reinterpret_cast<const float4*>(w.row_stats), npx, w.a_part, w.bm_part};
+  Dec2Args d2{w.e_tiles, assignment, reinterpret_cast<const float4*>(w.row_stats), npx, w.a_part, w.bm_part, accum};
   const size_t sm2 = 2 * ((size_t)kRows * K * 2 + (size_t)kRows * (K / 2) * 2 + (size_t)kRows * 64 * 2);
   static bool attr2 = false;
   if (!attr2) {
@@ -625,11 +705,11 @@ void launch_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_
   }
   dec2_kernel<K><<<g2, 288, sm2, st>>>(d2);
   count_launch();
-  cudaMemsetAsync(w.bm, 0, sizeof(float) * n_set * K, st);
-  const int64_t quads = ((int64_t)K * K + (int64_t)K * 64 + (int64_t)K * DS) / 4;
-  dec_reduce_kernel<<<dim3((unsigned)((quads + 255) / 256), kRedSplit), 256, 0, st>>>(
-      w.a_part, w.bm_part, w.r_part, w.loss_part, K, DS, (int)n_set, g1, g2 / 2, w.a_acc, w.bm, w.r_acc, partials);
+  // loss partials of this frame
+  dec_reduce_kernel<<<dim3(1, 1), 32, 0, st>>>(nullptr, nullptr, nullptr, w.loss_part, 0, 0, 0, g1, 0, nullptr,
+                                               nullptr, nullptr, partials, 0, 0);
   count_launch();
+  w.tc_frames += 1;
 }
 
 }  // namespace
@@ -650,8 +730,7 @@ void decoder_frame_tc(cudaStream_t st, DecoderWork& w, const float* query, const
   const int64_t k = w.k;
   const int ds = w.ds, df = w.df;
   // per-frame target scores G^T = E D^T and norms (tiny SIMT GEMMs)
-  sgemm(st, false, true, n_set, k, df, 1.f, feats, df, atoms, df, 0.f, w.gt, k);
-  decoder_target_norms(st, feats, n_set, df, w.nv);
+  decoder_targets(st, feats, n_set, atoms, k, df, w.gt, w.nv);
   if (k == 256)
     launch_tc<256, 32>(st, w, query, assignment, npx, feats, n_set, n_sup, temperature, lambda_cos, lambda_l2, scale,
                        want_grad, d_query, partials);
@@ -661,7 +740,17 @@ void decoder_frame_tc(cudaStream_t st, DecoderWork& w, const float* query, const
   if (!want_grad) return;
   // d_atoms += Bm E for this frame's embedding table; A and R accumulate over the step's frames
   // and enter once in decoder_finish_tc (they multiply the same D, W in every frame)
-  sgemm(st, true, false, k, df, n_set, 1.f, w.bm, k, feats, df, 1.f, d_atoms, df);
+  if (df % 4 == 0 && (reinterpret_cast<uintptr_t>(feats) & 15) == 0 && (reinterpret_cast<uintptr_t>(d_atoms) & 15) == 0) {
+    bm_embed_fused_kernel<<<(unsigned)(k / 2), 256, 0, st>>>(w.bm_part, 74, (int)k, feats, (int)n_set, df, d_atoms);
+    count_launch();
+  } else {
+    cudaMemsetAsync(w.bm, 0, sizeof(float) * n_set * k, st);
+    const int64_t quads = k * 64 / 4;
+    dec_reduce_kernel<<<dim3((unsigned)((quads + 255) / 256), kRedSplit), 256, 0, st>>>(
+        nullptr, w.bm_part, nullptr, nullptr, (int)k, ds, (int)n_set, 148, 74, nullptr, w.bm, nullptr, nullptr, 0, 1);
+    count_launch();
+    decoder_bm_embed(st, w.bm, feats, n_set, k, df, d_atoms);
+  }
   w.tc_pending = true;
   (void)d_proj;
   (void)proj;
@@ -672,6 +761,13 @@ void decoder_finish_tc(cudaStream_t st, DecoderWork& w, const float* atoms, cons
   if (!w.tc_pending) return;
   const int64_t k = w.k;
   const int ds = w.ds, df = w.df;
+  if (w.tc_frames > 0) {  // the fused frames' step-summed A and R partials
+    const int64_t quads = (k * k + k * ds) / 4;
+    dec_reduce_kernel<<<dim3((unsigned)((quads + 255) / 256), kRedSplit), 256, 0, st>>>(
+        w.a_part, nullptr, w.r_part, nullptr, (int)k, ds, 0, 148, 74, w.a_acc, nullptr, w.r_acc, nullptr, 1, 0);
+    count_launch();
+    w.tc_frames = 0;
+  }
   // d_atoms += A D + R^T W ;  d_proj += R D   (R stored ds x K)
   sgemm(st, false, false, k, df, k, 1.f, w.a_acc, k, atoms, df, 1.f, d_atoms, df);
   sgemm(st, true, false, k, df, ds, 1.f, w.r_acc, k, proj, df, 1.f, d_atoms, df);

@@ -89,7 +89,7 @@ struct DecoderWork {
   int64_t nset_cap = 0;
   // tcgen05 path scratch (decoder_tc.cu)
   float* row_stats = nullptr;  // npx x 4: max S, 1/sum, alpha, beta
-  float* r_part = nullptr;     // 148 x K x ds
+  float* r_part = nullptr;     // 2 x 148 x K x ds (fused path step sums, staged path per frame)
   float* a_part = nullptr;     // 74 x 2 x K x K/2
   float* bm_part = nullptr;    // 74 x K x 64
   double* loss_part = nullptr; // 148 x 4
@@ -97,6 +97,7 @@ struct DecoderWork {
   float* a_acc = nullptr;      // K x K: sum over the step's frames of P^T diag(alpha) P
   float* r_acc = nullptr;      // ds x K: sum over the step's frames of Q^T dS
   bool tc_pending = false;     // a_acc / r_acc hold contributions not yet applied
+  int tc_frames = 0;           // fused-path frames whose A / R partials are summed in a_part / r_part
   // staged large-K tcgen05 path scratch (decoder_dl.cu)
   uint8_t* dl_mt = nullptr;    // K x K bf16: M in the B-operand blocks of the T GEMM
   float* dl_t = nullptr;       // ntiles x 128 x K fp16: T = e M (aliases buf1)
@@ -112,6 +113,12 @@ void decoder_frame(cudaStream_t st, DecoderWork& w, const float* query, const in
                    const float* proj, float temperature, float lambda_cos, float lambda_l2, float scale,
                    bool want_grad, float* d_query, float* d_proj, float* d_atoms, double* partials);
 void decoder_target_norms(cudaStream_t st, const float* feats, int64_t n_set, int df, float* nv);
+// G = E D^T (n_set x K) and |E| rows in one launch (falls back to sgemm + norms for df % 4 != 0).
+void decoder_targets(cudaStream_t st, const float* feats, int64_t n_set, const float* atoms, int64_t k, int df,
+                     float* gt, float* nv);
+// d_atoms += Bm E with Bm^T stored n_set x K.
+void decoder_bm_embed(cudaStream_t st, const float* bmt, const float* feats, int64_t n_set, int64_t k, int df,
+                      float* d_atoms);
 // tcgen05 / TMEM path (bf16 operands, fp32 accumulation) for K in {128, 256}, d_s = 32, n_set <= 64.
 bool decoder_tc_supported(int64_t k, int ds, int64_t n_set);
 void decoder_frame_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_t* assignment,
