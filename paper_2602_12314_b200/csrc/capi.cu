@@ -8,6 +8,7 @@
 #include <array>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/latmap_b200.h"
@@ -156,6 +157,7 @@ struct latmap_ctx {
   int64_t launches0 = 0;
   bool exact_blend = false;  // parity mode: separately rounded accumulation in the forward blend
   int32_t decoder_path = 0;  // bf16 decoder: 0 auto, 1 fused on-chip (DEC1/DEC2), 2 staged (DL1-DL5)
+  cudaStream_t copy_stream = nullptr;  // keyframe uploads (overlap the step's render of earlier frames)
 };
 
 struct latmap_render_cache {
@@ -249,6 +251,10 @@ latmap_status latmap_ctx_create(int32_t device, void* stream, latmap_ctx** out) 
 latmap_status latmap_ctx_destroy(latmap_ctx* ctx) {
   if (!ctx) return LATMAP_ERR_INVALID_ARGUMENT;
   cudaStreamSynchronize(ctx->stream);
+  if (ctx->copy_stream) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+  }
   delete ctx;
   return LATMAP_OK;
 }
@@ -618,6 +624,11 @@ struct latmap_session {
   // arguments (frame poses, buffer pointers, sizes) are unchanged
   cudaGraphExec_t step_graph = nullptr;
   cudaStream_t cap_stream = nullptr;
+  // set_frames uploads on ctx->copy_stream; up_ev[b] marks frame b's data resident. Every use of
+  // frame data waits on it (an external event node when captured), so the render of frame 0 and
+  // the uploads of later frames overlap.
+  std::vector<cudaEvent_t> up_ev;
+  cudaEvent_t ev_ready = nullptr;
   int64_t graph_launches = 0;
   bool graph_exact = false;
   int32_t graph_dec_path = 0;
@@ -758,6 +769,15 @@ __global__ void seg_scatter_kernel(const float* __restrict__ dq, const int32_t* 
   }
 }
 
+// Order `st` after frame b's upload (set_frames). Under stream capture the wait becomes an
+// external event node, so replays wait on the latest upload.
+static void wait_frame(const latmap_session* s, int b, cudaStream_t st) {
+  if (b >= (int)s->up_ev.size()) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  cudaStreamWaitEvent(st, s->up_ev[b], cs == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0);
+}
+
 // One total_objective over the session's keyframes (objective.cpp:67-194). map_grads = false
 // skips the image-loss gradients and the render backward (ObjectiveOptions::map_grads);
 // use_cache skips the render when the per-frame images still hold renders of the current map
@@ -822,6 +842,7 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
     }
     const bool map_grad = want_grad && map_grads;
     s->begin(2);
+    wait_frame(s, b, st);
     image_losses(st, s->color[b], s->depth[b], s->alpha[b], f.rgb, f.depth, h, w, c.lambda_i1, c.lambda_i2,
                  c.lambda_rgb * inv_b, c.lambda_depth * inv_b, map_grad, s->d_color, s->d_depth, part,
                  s->ssim_scratch);
@@ -1030,6 +1051,9 @@ latmap_status latmap_session_destroy(latmap_session* s) {
   cudaStreamSynchronize(s->ctx->stream);
   s->drop_graph();
   if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
+  if (s->ctx->copy_stream) cudaStreamSynchronize(s->ctx->copy_stream);
+  for (cudaEvent_t e : s->up_ev) cudaEventDestroy(e);
+  if (s->ev_ready) cudaEventDestroy(s->ev_ready);
   for (void* p : {(void*)s->params, (void*)s->grads, (void*)s->m, (void*)s->v, (void*)s->anchor, (void*)s->steps,
                   (void*)s->skipped, (void*)s->overflow, (void*)s->flags, (void*)s->corr1, (void*)s->corr2,
                   (void*)s->d_color, (void*)s->d_depth, (void*)s->d_query, (void*)s->ssim_scratch, (void*)s->partials,
@@ -1118,6 +1142,39 @@ latmap_status latmap_session_set_frames(latmap_session* s, int32_t nf, const lat
   latmap_status st = session_alloc_frames(s, nf);
   if (st != LATMAP_OK) return st;
   const size_t npx = (size_t)s->intr.width * s->intr.height;
+  if (!ctx->copy_stream) CTX_CHECK(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  if (!s->ev_ready) CTX_CHECK(ctx, cudaEventCreateWithFlags(&s->ev_ready, cudaEventDisableTiming));
+  while ((int)s->up_ev.size() < nf) {
+    cudaEvent_t e;
+    CTX_CHECK(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    s->up_ev.push_back(e);
+  }
+  // uploads start after the work already queued on the context stream (it may still read them)
+  CTX_CHECK(ctx, cudaEventRecord(s->ev_ready, ctx->stream));
+  CTX_CHECK(ctx, cudaStreamWaitEvent(ctx->copy_stream, s->ev_ready, 0));
+  // supervised-pixel counts and the assignment range check, one host thread per frame
+  std::vector<int64_t> scan_nsup(nf, 0);
+  std::vector<int32_t> scan_amax(nf, -1);
+  {
+    auto scan = [&](int b) {
+      const int32_t* asg = frames[b].assignment;
+      int64_t ns = 0;
+      int32_t am = -1;
+      for (size_t p = 0; p < npx; ++p) {  // branch-free: vectorises
+        const int32_t a = asg[p];
+        ns += a >= 0;
+        am = a > am ? a : am;
+      }
+      scan_nsup[b] = ns;
+      scan_amax[b] = am;
+    };
+    std::vector<std::thread> pool;
+    for (int b = 1; b < nf && npx >= (1u << 16); ++b) pool.emplace_back(scan, b);
+    scan(0);
+    if (pool.empty())
+      for (int b = 1; b < nf; ++b) scan(b);
+    for (auto& t : pool) t.join();
+  }
   std::vector<int64_t> nsup0;
   for (int b = 0; same && b < nf; ++b) nsup0.push_back(s->frames[b].n_sup);
   for (int b = 0; b < nf; ++b) {
@@ -1138,17 +1195,14 @@ latmap_status latmap_session_set_frames(latmap_session* s, int32_t nf, const lat
       CTX_CHECK(ctx, cudaMalloc(&f.feats, sizeof(float) * std::max<size_t>(nfeat, 1)));
       f.c_feat = nfeat;
     }
-    CTX_CHECK(ctx, cudaMemcpyAsync(f.rgb, in.rgb, sizeof(float) * npx * 3, cudaMemcpyHostToDevice, ctx->stream));
-    CTX_CHECK(ctx, cudaMemcpyAsync(f.depth, in.depth, sizeof(float) * npx, cudaMemcpyHostToDevice, ctx->stream));
-    CTX_CHECK(ctx, cudaMemcpyAsync(f.assign, in.assignment, sizeof(int32_t) * npx, cudaMemcpyHostToDevice, ctx->stream));
-    if (nfeat) CTX_CHECK(ctx, cudaMemcpyAsync(f.feats, in.features, sizeof(float) * nfeat, cudaMemcpyHostToDevice, ctx->stream));
-    int64_t nsup = 0;
-    int32_t amax = -1;
-    for (size_t p = 0; p < npx; ++p) {  // branch-free: vectorises
-      const int32_t a = in.assignment[p];
-      nsup += a >= 0;
-      amax = a > amax ? a : amax;
-    }
+    cudaStream_t cs = ctx->copy_stream;
+    CTX_CHECK(ctx, cudaMemcpyAsync(f.rgb, in.rgb, sizeof(float) * npx * 3, cudaMemcpyHostToDevice, cs));
+    CTX_CHECK(ctx, cudaMemcpyAsync(f.depth, in.depth, sizeof(float) * npx, cudaMemcpyHostToDevice, cs));
+    CTX_CHECK(ctx, cudaMemcpyAsync(f.assign, in.assignment, sizeof(int32_t) * npx, cudaMemcpyHostToDevice, cs));
+    if (nfeat) CTX_CHECK(ctx, cudaMemcpyAsync(f.feats, in.features, sizeof(float) * nfeat, cudaMemcpyHostToDevice, cs));
+    CTX_CHECK(ctx, cudaEventRecord(s->up_ev[b], cs));
+    int64_t nsup = scan_nsup[b];
+    const int32_t amax = scan_amax[b];
     if (amax >= in.n_set) return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "gather_supervision: assignment out of range");
     if (s->cfg.segment_mode) {
       // present assignment rows in ascending order (objective.cpp:39-64)
@@ -1549,6 +1603,7 @@ latmap_status latmap_session_seed_candidates(latmap_session* s, int32_t b, float
     latmap_status rs = latmap_session_objective_ex(s, 0, 0, 0, nullptr);
     if (rs != LATMAP_OK) return rs;
   }
+  wait_frame(s, b, st);
   SeedArgs a;
   a.obs_depth = f.depth, a.alpha = s->alpha[b], a.depth = s->depth[b], a.rgb = f.rgb;
   a.w = s->intr.width, a.h = s->intr.height;
