@@ -306,6 +306,28 @@ latmap_status latmap_store_sync(latmap_store* s, const float* d_active, const in
                                 int64_t* out_origin, int64_t cap, uint8_t* kept_mask, int64_t stats[5],
                                 int64_t* out_count);
 
+/* ---------------------------------------------------------------- streaming k-means */
+/* std::uniform_real_distribution<double>(0, 1) drawn from the caller's generator (the pipeline's
+ * std::mt19937_64, pipeline.cpp:203): k-means++ consumes exactly the draws the reference does. */
+typedef double (*latmap_uniform_fn)(void* user);
+/* weighted_kmeans (stream_kmeans.hpp:18-21, stream_kmeans.cpp:94-157): host points n x dim,
+ * weights n, optional warm-start rows (n_warm x dim); writes centers (k x dim), per-centre mass
+ * (k) and the Lloyd iteration count. Nearest-centre scores, argmin, k-means++ distances and the
+ * centre sums run on the device; the generator draws and orderings on the host. */
+latmap_status latmap_weighted_kmeans(latmap_ctx* ctx, const float* points, const float* weights, int64_t n,
+                                     int32_t dim, int64_t k, latmap_uniform_fn uniform, void* user,
+                                     const float* warm, int64_t n_warm, int32_t max_iters, float* centers,
+                                     float* center_weights, int32_t* iterations);
+/* Dictionary maintenance of process_keyframe_inner for dict_init = "kmeans" (pipeline.cpp:201-205):
+ * stream_kmeans_update (stream_kmeans.hpp:27-33) of the session's atoms / anchor / atom weights
+ * with the keyframe's (host, n x embed_dim) embedding rows, then MapOptimizer::reset_atom_moments
+ * (pipeline.hpp:62-64: the atoms' Adam moments and step count). */
+latmap_status latmap_session_stream_kmeans(latmap_session* s, const float* batch, int64_t n, float decay,
+                                           latmap_uniform_fn uniform, void* user);
+/* DictionaryState::weights (dictionary.hpp:15), K floats; zero after session creation (init). */
+latmap_status latmap_session_get_dict_weights(const latmap_session* s, float* out);
+latmap_status latmap_session_set_dict_weights(latmap_session* s, const float* w);
+
 /* ---------------------------------------------------------------- self-test */
 /* One-tile tcgen05 GEMM, C[128 x n] = A[128 x k] * B[n x k]^T (device fp32 in/out, bf16 staging),
  * with A / B staged K-major (0) or MN-major (1); pins the UMMA descriptor conventions. */

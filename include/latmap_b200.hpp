@@ -48,6 +48,38 @@ class Context {
   latmap_ctx* h_ = nullptr;
 };
 
+// std::uniform_real_distribution<double>(0, 1) over the caller's generator, as a C callback
+// (k-means++ draws exactly what stream_kmeans.cpp:58-71 draws from the pipeline's rng).
+template <class Rng>
+double uniform01_trampoline(void* user) {
+  std::uniform_real_distribution<double> uni(0.0, 1.0);
+  return uni(*static_cast<Rng*>(user));
+}
+
+// weighted_kmeans (stream_kmeans.hpp:18-21) on the device; points row-major n x dim.
+struct WeightedKmeansResult {
+  std::vector<float> centers;  // k x dim
+  std::vector<float> weights;  // k
+  int iterations = 0;
+};
+template <class Rng>
+WeightedKmeansResult weighted_kmeans(Context& ctx, const std::vector<float>& points, const std::vector<float>& weights,
+                                     int64_t dim, int64_t k, Rng& rng, const std::vector<float>* warm = nullptr,
+                                     int max_iters = 10) {
+  const int64_t n = dim > 0 ? (int64_t)points.size() / dim : 0;
+  if ((int64_t)weights.size() != n) throw std::invalid_argument("weighted_kmeans: weight count");
+  WeightedKmeansResult r;
+  r.centers.assign((size_t)(std::max<int64_t>(k, 0) * dim), 0.f);
+  r.weights.assign((size_t)std::max<int64_t>(k, 0), 0.f);
+  int32_t it = 0;
+  check(latmap_weighted_kmeans(ctx.get(), points.data(), weights.data(), n, (int32_t)dim, k, &uniform01_trampoline<Rng>,
+                               &rng, warm ? warm->data() : nullptr, warm ? (int64_t)warm->size() / dim : 0, max_iters,
+                               r.centers.data(), r.weights.data(), &it),
+        ctx.get());
+  r.iterations = it;
+  return r;
+}
+
 // RenderOutputT's cache half (splats + fingerprint); the images are caller-owned device buffers.
 class RenderCache {
  public:
@@ -113,7 +145,7 @@ class Session {
  public:
   Session(Context& ctx, const latmap_config& cfg, int64_t n, int32_t query_dim, int64_t k, int32_t embed_dim,
           const latmap_intrinsics& intr)
-      : ctx_(&ctx) {
+      : ctx_(&ctx), k_(k) {
     check(latmap_session_create(ctx.get(), &cfg, n, query_dim, k, embed_dim, &intr, &h_), ctx.get());
   }
   ~Session() {
@@ -189,10 +221,23 @@ class Session {
     check(latmap_session_append_rows(h_, d_scratch, n, feats.data()), ctx_->get());
     return n;
   }
+  // Dictionary maintenance for dict_init = "kmeans" (pipeline.cpp:201-205): stream_kmeans_update
+  // with the keyframe's embedding rows (host, n x embed_dim) and the pipeline's generator, then
+  // reset_atom_moments.
+  template <class Rng>
+  void stream_kmeans(const float* batch, int64_t n, Rng& rng, float decay = 1.0f) {
+    check(latmap_session_stream_kmeans(h_, batch, n, decay, &uniform01_trampoline<Rng>, &rng), ctx_->get());
+  }
+  std::vector<float> dict_weights() const {
+    std::vector<float> w((size_t)k_);
+    check(latmap_session_get_dict_weights(h_, w.data()), ctx_->get());
+    return w;
+  }
   latmap_session* get() const { return h_; }
 
  private:
   Context* ctx_;
+  int64_t k_ = 0;
   latmap_session* h_ = nullptr;
 };
 

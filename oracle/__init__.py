@@ -157,6 +157,20 @@ def _declare(L):
     L.lm_store_get_record.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_float)]
     L.lm_store_set_record.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_float)]
     L.lm_store_record_key.argtypes = [C.c_void_p, C.c_int64]
+    UNI = C.CFUNCTYPE(C.c_double, C.c_void_p)
+    for dt in (np.float32, np.float64):
+        sfx, ct = _SUF[dt], _CT[dt]
+        P = C.POINTER(ct)
+        f = getattr(L, "lm_weighted_kmeans" + sfx)
+        f.argtypes = [P, P, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, P, C.c_int64, C.c_int, P, P,
+                      C.POINTER(C.c_int)]
+        f = getattr(L, "lm_stream_kmeans_update" + sfx)
+        f.argtypes = [P, C.c_int64, C.c_int64, P, P, P, C.c_int64, C.c_void_p, C.c_void_p, ct]
+    L.lm_mt64_seed.argtypes = [C.c_void_p, C.c_uint64]
+    L.lm_mt64_next.argtypes = [C.c_void_p]
+    L.lm_mt64_next.restype = C.c_uint64
+    L.lm_mt64_uniform01.argtypes = [C.c_void_p]
+    L.lm_mt64_uniform01.restype = C.c_double
     L.lm_store_record_key.restype = VoxelKey
     L.lm_store_stats.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
     L.lm_insert_global.argtypes = [C.c_void_p, C.POINTER(C.c_float), C.c_int64, C.c_float]
@@ -618,3 +632,55 @@ def records_to_map(r, ds):
     return GaussianMap(np.ascontiguousarray(r[:, 0:3]), np.ascontiguousarray(r[:, 3:7]),
                        np.ascontiguousarray(r[:, 7:10]), np.ascontiguousarray(r[:, 10:13]),
                        np.ascontiguousarray(r[:, 13]), np.ascontiguousarray(r[:, 14:14 + ds]))
+
+
+# --------------------------------------------------------------------------- streaming k-means
+class MT64(C.Structure):
+    """std::mt19937_64 state (lm_mt64); ``uniform01`` is the C function pointer drawing
+    std::uniform_real_distribution<double>(0, 1) from it (what k-means++ consumes)."""
+    _fields_ = [("mt", C.c_uint64 * 312), ("idx", C.c_int32)]
+
+    def __init__(self, seed=5489):
+        super().__init__()
+        lib().lm_mt64_seed(C.byref(self), seed)
+
+    def next(self):
+        return int(lib().lm_mt64_next(C.byref(self)))
+
+    def uniform01(self):
+        return float(lib().lm_mt64_uniform01(C.byref(self)))
+
+    @staticmethod
+    def uniform01_fn():
+        """Address of lm_mt64_uniform01 (a C callback double(void*))."""
+        return C.cast(lib().lm_mt64_uniform01, C.c_void_p).value
+
+
+def weighted_kmeans(points, weights, k, rng: MT64, warm=None, max_iters=10):
+    """weighted_kmeans (stream_kmeans.cpp:94-157) -> (centers k x dim, weights k, iterations)."""
+    dt = points.dtype.type
+    pts = np.ascontiguousarray(points)
+    w = np.ascontiguousarray(weights, dtype=dt)
+    n, dim = pts.shape
+    cen = np.zeros((k, dim), dt)
+    cw = np.zeros(k, dt)
+    it = C.c_int(0)
+    wm = None if warm is None else np.ascontiguousarray(warm, dtype=dt)
+    rc = getattr(lib(), "lm_weighted_kmeans" + _SUF[dt])(
+        _p(pts), _p(w), n, dim, k, MT64.uniform01_fn(), C.cast(C.byref(rng), C.c_void_p), _p(wm),
+        0 if wm is None else wm.shape[0], max_iters, _p(cen), _p(cw), C.byref(it))
+    if rc != 0:
+        raise ValueError("weighted_kmeans: k must be >= 1")
+    return cen, cw, it.value
+
+
+def stream_kmeans_update(batch, atoms, anchor, weights, rng: MT64, decay=1.0):
+    """stream_kmeans_update (stream_kmeans.cpp:159-196); updates atoms / anchor / weights in place."""
+    dt = atoms.dtype.type
+    b = np.ascontiguousarray(batch, dtype=dt)
+    n = b.shape[0]
+    if n and b.shape[1] != atoms.shape[1]:
+        raise ValueError("stream_kmeans_update: embedding dimension mismatch")
+    getattr(lib(), "lm_stream_kmeans_update" + _SUF[dt])(
+        _p(b), n, atoms.shape[1], _p(atoms), _p(anchor), _p(weights), atoms.shape[0], MT64.uniform01_fn(),
+        C.cast(C.byref(rng), C.c_void_p), _CT[dt](decay))

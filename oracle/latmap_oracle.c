@@ -1199,7 +1199,239 @@ void S(lm_renorm_quats)(T* rot, int64_t n) {
   }
 }
 
+
+/* ------------------------------------------------------------------ streaming k-means */
+
+/* assign_nearest, stream_kmeans.cpp:11-36: score = P C^T (ascending inner index),
+ * d = |c|^2 - 2 score, ties to the lower center index. */
+static void S(km_assign)(const T* P, int64_t n, int64_t dim, const T* C, int64_t k, int64_t* asg) {
+  if (k == 0) {
+    for (int64_t r = 0; r < n; ++r) asg[r] = 0;
+    return;
+  }
+  T* c2 = (T*)malloc(sizeof(T) * (size_t)k);
+  for (int64_t j = 0; j < k; ++j) {
+    T s = 0;
+    for (int64_t d = 0; d < dim; ++d) s += C[j * dim + d] * C[j * dim + d];
+    c2[j] = s;
+  }
+  for (int64_t r = 0; r < n; ++r) {
+    T best = 0;
+    int64_t bj = 0;
+    for (int64_t j = 0; j < k; ++j) {
+      T sc = 0;
+      for (int64_t d = 0; d < dim; ++d) sc += P[r * dim + d] * C[j * dim + d];
+      const T dd = c2[j] - (T)2 * sc;
+      if (j == 0 || dd < best) {
+        best = dd;
+        bj = j;
+      }
+    }
+    asg[r] = bj;
+  }
+  free(c2);
+}
+
+/* update_min_dist, stream_kmeans.cpp:38-45 */
+static void S(km_update_min)(const T* P, int64_t n, int64_t dim, const T* c, T* min_d2) {
+  for (int64_t i = 0; i < n; ++i) {
+    T d = 0;
+    for (int64_t e = 0; e < dim; ++e) {
+      const T t = P[i * dim + e] - c[e];
+      d += t * t;
+    }
+    if (d < min_d2[i]) min_d2[i] = d;
+  }
+}
+
+/* kmeanspp_fill, stream_kmeans.cpp:48-90: weighted k-means++ continuation of rows [filled, k). */
+static void S(km_pp_fill)(const T* P, const T* W, int64_t n, int64_t dim, T* centers, int64_t k,
+                          int64_t filled, double (*uni)(void*), void* rng) {
+  T* min_d2 = (T*)malloc(sizeof(T) * (size_t)n);
+  uint8_t* used = (uint8_t*)calloc((size_t)n, 1);
+  for (int64_t i = 0; i < n; ++i) min_d2[i] = LM_DOUBLE ? (T)1.7976931348623157e308 : (T)3.40282346638528859812e+38F;
+  for (int64_t j = 0; j < filled; ++j) S(km_update_min)(P, n, dim, centers + j * dim, min_d2);
+  for (int64_t j = filled; j < k; ++j) {
+    double total = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      double p = (double)W[i];
+      if (j > 0 || filled > 0) p *= (double)min_d2[i];
+      total += p;
+    }
+    int64_t pick = -1;
+    if (total > 0) {
+      const double target = uni(rng) * total;
+      double run = 0;
+      for (int64_t i = 0; i < n; ++i) {
+        double p = (double)W[i];
+        if (j > 0 || filled > 0) p *= (double)min_d2[i];
+        run += p;
+        if (run >= target) {
+          pick = i;
+          break;
+        }
+      }
+      if (pick < 0) pick = n - 1;
+    } else {
+      for (int64_t i = 0; i < n; ++i)
+        if (!used[i]) {
+          pick = i;
+          break;
+        }
+      if (pick < 0) pick = (j - filled) % n;
+    }
+    used[pick] = 1;
+    memcpy(centers + j * dim, P + pick * dim, sizeof(T) * (size_t)dim);
+    S(km_update_min)(P, n, dim, centers + j * dim, min_d2);
+  }
+  free(min_d2);
+  free(used);
+}
+
+/* weighted_kmeans, stream_kmeans.cpp:94-157 */
+int S(lm_weighted_kmeans)(const T* P, const T* W, int64_t n, int64_t dim, int64_t k, double (*uni)(void*),
+                          void* rng, const T* warm, int64_t n_warm, int max_iters, T* centers, T* cw,
+                          int* iterations) {
+  if (k < 1) return -1;
+  memset(centers, 0, sizeof(T) * (size_t)(k * dim));
+  for (int64_t j = 0; j < k; ++j) cw[j] = 0;
+  *iterations = 0;
+  if (n == 0) return 0;
+  int64_t filled = 0;
+  if (warm) {
+    filled = k < n_warm ? k : n_warm;
+    memcpy(centers, warm, sizeof(T) * (size_t)(filled * dim));
+  }
+  S(km_pp_fill)(P, W, n, dim, centers, k, filled, uni, rng);
+  int64_t* asg = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+  int64_t* prev = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+  uint8_t* claimed = (uint8_t*)calloc((size_t)n, 1);
+  T* mass = (T*)malloc(sizeof(T) * (size_t)k);
+  T* sums = (T*)malloc(sizeof(T) * (size_t)(k * dim));
+  for (int it = 0; it < max_iters; ++it) {
+    S(km_assign)(P, n, dim, centers, k, asg);
+    for (int64_t j = 0; j < k; ++j) mass[j] = 0;
+    memset(sums, 0, sizeof(T) * (size_t)(k * dim));
+    for (int64_t i = 0; i < n; ++i) {
+      mass[asg[i]] += W[i];
+      for (int64_t e = 0; e < dim; ++e) sums[asg[i] * dim + e] += W[i] * P[i * dim + e];
+    }
+    int reseeded = 0;
+    for (int64_t j = 0; j < k; ++j) {
+      if (mass[j] > (T)0) {
+        for (int64_t e = 0; e < dim; ++e) centers[j * dim + e] = sums[j * dim + e] / mass[j];
+      } else {
+        int64_t pick = -1;
+        T best = (T)-1;
+        for (int64_t i = 0; i < n; ++i)
+          if (!claimed[i] && W[i] > best) {
+            best = W[i];
+            pick = i;
+          }
+        if (pick >= 0) {
+          claimed[pick] = 1;
+          memcpy(centers + j * dim, P + pick * dim, sizeof(T) * (size_t)dim);
+          reseeded = 1;
+        }
+      }
+    }
+    *iterations = it + 1;
+    if (!reseeded && it > 0 && memcmp(asg, prev, sizeof(int64_t) * (size_t)n) == 0) break;
+    memcpy(prev, asg, sizeof(int64_t) * (size_t)n);
+  }
+  S(km_assign)(P, n, dim, centers, k, asg);
+  for (int64_t j = 0; j < k; ++j) cw[j] = 0;
+  for (int64_t i = 0; i < n; ++i) cw[asg[i]] += W[i];
+  free(asg);
+  free(prev);
+  free(claimed);
+  free(mass);
+  free(sums);
+  return 0;
+}
+
+/* stream_kmeans_update, stream_kmeans.cpp:159-196 (state = atoms / anchor / weights, K rows). */
+int S(lm_stream_kmeans_update)(const T* batch, int64_t n, int64_t dim, T* atoms, T* anchor, T* weights, int64_t k,
+                               double (*uni)(void*), void* rng, T decay) {
+  if (n == 0) return 0;
+  const int64_t m = n < k ? n : k;
+  T* unit = (T*)malloc(sizeof(T) * (size_t)n);
+  for (int64_t i = 0; i < n; ++i) unit[i] = (T)1;
+  T* lc = (T*)malloc(sizeof(T) * (size_t)(m * dim));
+  T* lw = (T*)malloc(sizeof(T) * (size_t)m);
+  int iters = 0;
+  S(lm_weighted_kmeans)(batch, unit, n, dim, m, uni, rng, NULL, 0, 10, lc, lw, &iters);
+  int64_t old_count = 0;
+  for (int64_t j = 0; j < k; ++j)
+    if (weights[j] > (T)0) ++old_count;
+  T* pooled = (T*)malloc(sizeof(T) * (size_t)((m + old_count) * dim));
+  T* pw = (T*)malloc(sizeof(T) * (size_t)(m + old_count));
+  T* warm = (T*)malloc(sizeof(T) * (size_t)((old_count > 0 ? old_count : 1) * dim));
+  memcpy(pooled, lc, sizeof(T) * (size_t)(m * dim));
+  memcpy(pw, lw, sizeof(T) * (size_t)m);
+  int64_t at = 0;
+  for (int64_t j = 0; j < k; ++j) {
+    if (weights[j] > (T)0) {
+      memcpy(pooled + (m + at) * dim, atoms + j * dim, sizeof(T) * (size_t)dim);
+      pw[m + at] = weights[j] * decay;
+      memcpy(warm + at * dim, atoms + j * dim, sizeof(T) * (size_t)dim);
+      ++at;
+    }
+  }
+  S(lm_weighted_kmeans)(pooled, pw, m + old_count, dim, k, uni, rng, old_count > 0 ? warm : NULL, old_count, 10,
+                        atoms, weights, &iters);
+  memcpy(anchor, atoms, sizeof(T) * (size_t)(k * dim));
+  free(unit);
+  free(lc);
+  free(lw);
+  free(pooled);
+  free(pw);
+  free(warm);
+  return 0;
+}
+
 #else /* LM_ONCE: voxel hash store, voxel_hash.cpp / active_set.cpp */
+
+/* ------------------------------------------------------------------ std::mt19937_64 */
+/* The 64-bit Mersenne Twister with the C++ standard's parameters ([rand.predef]:
+ * w=64 n=312 m=156 r=31 a=0xb5026f5aa96619e9 u=29 d=0x5555555555555555 s=17
+ * b=0x71d67fffeda60000 t=37 c=0xfff7eee000000000 l=43 f=6364136223846793005). */
+void lm_mt64_seed(lm_mt64* r, uint64_t seed) {
+  r->mt[0] = seed;
+  for (int i = 1; i < 312; ++i) r->mt[i] = 6364136223846793005ULL * (r->mt[i - 1] ^ (r->mt[i - 1] >> 62)) + (uint64_t)i;
+  r->idx = 312;
+}
+
+uint64_t lm_mt64_next(lm_mt64* r) {
+  if (r->idx >= 312) {
+    const uint64_t lower = (1ULL << 31) - 1, upper = ~lower;
+    for (int i = 0; i < 312; ++i) {
+      const uint64_t x = (r->mt[i] & upper) | (r->mt[(i + 1) % 312] & lower);
+      uint64_t xa = x >> 1;
+      if (x & 1ULL) xa ^= 0xb5026f5aa96619e9ULL;
+      r->mt[i] = r->mt[(i + 156) % 312] ^ xa;
+    }
+    r->idx = 0;
+  }
+  uint64_t y = r->mt[r->idx++];
+  y ^= (y >> 29) & 0x5555555555555555ULL;
+  y ^= (y << 17) & 0x71d67fffeda60000ULL;
+  y ^= (y << 37) & 0xfff7eee000000000ULL;
+  y ^= y >> 43;
+  return y;
+}
+
+/* std::uniform_real_distribution<double>(0, 1) over mt19937_64 with libstdc++'s
+ * generate_canonical<double, 53>: one draw (53 <= 64 bits), (double)x / 2^64, values that
+ * round to 1 clamp to nextafter(1, 0); then a + (b - a) * u with a = 0, b = 1. */
+double lm_mt64_uniform01(void* rp) {
+  const double sum = (double)lm_mt64_next((lm_mt64*)rp);
+  double ret = sum / 18446744073709551616.0;
+  if (ret >= 1.0) ret = nextafter(1.0, 0.0);
+  return ret * (1.0 - 0.0) + 0.0;
+}
+
+
 
 #define PROBE_LIMIT 8
 

@@ -114,10 +114,30 @@ typedef struct {
                             lm_map##S* map_grads, T* d_proj, T* d_atoms, lm_loss##S* out);      \
   int lm_adam_step##S(T* param, const T* grad, T* m, T* v, int64_t count, int64_t* step,        \
                       int64_t* skipped, T lr);                                                  \
-  void lm_renorm_quats##S(T* rot, int64_t n);
+  void lm_renorm_quats##S(T* rot, int64_t n);                                                   \
+  /* weighted_kmeans / stream_kmeans_update (stream_kmeans.cpp:94-196); uni draws */            \
+  /* std::uniform_real_distribution<double>(0, 1) from the caller's generator */                \
+  int lm_weighted_kmeans##S(const T* points, const T* weights, int64_t n, int64_t dim,          \
+                            int64_t k, double (*uni)(void*), void* rng, const T* warm,          \
+                            int64_t n_warm, int max_iters, T* centers, T* cweights,             \
+                            int* iterations);                                                   \
+  int lm_stream_kmeans_update##S(const T* batch, int64_t n, int64_t dim, T* atoms, T* anchor,   \
+                                 T* weights, int64_t k, double (*uni)(void*), void* rng,        \
+                                 T decay);
 
 LM_DECLARE(float, _f32)
 LM_DECLARE(double, _f64)
+
+/* ---- std::mt19937_64 and std::uniform_real_distribution<double>(0, 1) (libstdc++
+ * generate_canonical), the generator the reference pipeline threads through k-means++
+ * (stream_kmeans.cpp:58) and seeding (pipeline.cpp:46) ---- */
+typedef struct {
+  uint64_t mt[312];
+  int32_t idx;
+} lm_mt64;
+void lm_mt64_seed(lm_mt64* r, uint64_t seed);
+uint64_t lm_mt64_next(lm_mt64* r);
+double lm_mt64_uniform01(void* r);
 
 /* ---- voxel hash store (float only, voxel_hash.hpp / active_set.hpp) ---- */
 lm_voxel_key lm_voxel_of(const float p[3], float voxel_size);

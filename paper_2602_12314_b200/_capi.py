@@ -136,6 +136,11 @@ def _declare(L):
         "latmap_session_stats": [P, P, P],
         "latmap_session_profile": [P, C.c_int32],
         "latmap_selftest_umma": [P, P, P, P, C.c_int32, C.c_int32, C.c_int32, C.c_int32],
+        "latmap_weighted_kmeans": [P, P, P, C.c_int64, C.c_int32, C.c_int64, P, P, P, C.c_int64, C.c_int32, P, P,
+                                   C.POINTER(C.c_int32)],
+        "latmap_session_stream_kmeans": [P, P, C.c_int64, C.c_float, P, P],
+        "latmap_session_get_dict_weights": [P, P],
+        "latmap_session_set_dict_weights": [P, P],
         "latmap_store_create": [P, C.c_int64, C.c_int32, C.POINTER(P)],
         "latmap_store_destroy": [P],
         "latmap_store_get_records": [P, C.c_int64, C.c_int64, P, P],
@@ -195,7 +200,8 @@ EXPORTED = ["latmap_ctx_create", "latmap_ctx_destroy", "latmap_ctx_set_stream", 
             "latmap_voxel_of", "latmap_hash_voxel", "latmap_store_create", "latmap_store_destroy", "latmap_store_size",
             "latmap_store_stats", "latmap_store_last_error", "latmap_store_insert", "latmap_store_update",
             "latmap_store_find", "latmap_store_get_records", "latmap_store_insert_global", "latmap_store_fetch_local",
-            "latmap_store_sync"]
+            "latmap_store_sync", "latmap_weighted_kmeans", "latmap_session_stream_kmeans",
+            "latmap_session_get_dict_weights", "latmap_session_set_dict_weights"]
 
 
 def check(ctx_handle, status):

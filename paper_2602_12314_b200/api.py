@@ -70,6 +70,18 @@ def make_intrinsics(fx, fy, cx, cy, width, height):
     return Intrinsics(fx, fy, cx, cy, width, height)
 
 
+_UNIFORM = C.CFUNCTYPE(C.c_double, C.c_void_p)
+
+
+def _uniform_arg(uniform):
+    """(fn, user, keepalive) for a latmap_uniform_fn argument."""
+    if callable(uniform):
+        cb = _UNIFORM(lambda _user: float(uniform()))
+        return C.cast(cb, C.c_void_p), None, cb
+    fn, user = uniform
+    return C.c_void_p(fn), C.c_void_p(user), None
+
+
 class Context:
     """A latmap_ctx bound to one device and torch's current stream."""
 
@@ -96,6 +108,26 @@ class Context:
     def set_decoder_path(self, path):
         """bf16 decoder kernels: 0 auto, 1 fused on-chip (DEC1/DEC2), 2 staged (DL1-DL5)."""
         check(self.h, lib().latmap_ctx_set_decoder_path(self.h, int(path)))
+
+    def weighted_kmeans(self, points, weights, k, uniform, warm=None, max_iters=10):
+        """weighted_kmeans (stream_kmeans.cpp:94-157) on the device -> (centers, weights, iterations).
+
+        ``uniform`` supplies std::uniform_real_distribution<double>(0, 1) draws of the caller's
+        generator: a Python callable, or a (C function pointer, user pointer) pair."""
+        pts = np.ascontiguousarray(points, np.float32)
+        w = np.ascontiguousarray(weights, np.float32)
+        n, dim = pts.shape
+        cen = np.zeros((k, dim), np.float32)
+        cw = np.zeros(k, np.float32)
+        it = C.c_int32(0)
+        wm = None if warm is None else np.ascontiguousarray(warm, np.float32)
+        fn, user, keep = _uniform_arg(uniform)
+        check(self.h, lib().latmap_weighted_kmeans(
+            self.h, pts.ctypes.data_as(C.c_void_p), w.ctypes.data_as(C.c_void_p), n, dim, int(k), fn, user,
+            None if wm is None else wm.ctypes.data_as(C.c_void_p), 0 if wm is None else wm.shape[0], int(max_iters),
+            cen.ctypes.data_as(C.c_void_p), cw.ctypes.data_as(C.c_void_p), C.byref(it)))
+        del keep
+        return cen, cw, it.value
 
     def launches(self):
         return lib().latmap_ctx_launch_count(self.h)
@@ -291,6 +323,27 @@ class Session:
         arrs = [None if a is None else np.ascontiguousarray(a, np.float32) for a in (atoms, anchor, proj)]
         check(self.ctx.h, lib().latmap_session_set_dictionary(self.h, *[self._np_ptr(a) for a in arrs]))
         self.ctx.sync()
+
+    def stream_kmeans(self, batch, uniform, decay=1.0):
+        """Dictionary maintenance (pipeline.cpp:201-205): stream_kmeans_update of the atoms /
+        anchor / atom weights with the keyframe embeddings (host n x embed_dim), then the atoms'
+        Adam moments reset. ``uniform`` as in Context.weighted_kmeans."""
+        b = np.ascontiguousarray(batch, np.float32)
+        if b.shape[0] and b.shape[1] != self.df:
+            raise _capi.InvalidArgument("stream_kmeans_update: embedding dimension mismatch")
+        fn, user, keep = _uniform_arg(uniform)
+        check(self.ctx.h, lib().latmap_session_stream_kmeans(self.h, b.ctypes.data_as(C.c_void_p), b.shape[0],
+                                                             float(decay), fn, user))
+        del keep
+
+    def dict_weights(self):
+        out = np.zeros(self.k, np.float32)
+        check(self.ctx.h, lib().latmap_session_get_dict_weights(self.h, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def set_dict_weights(self, w):
+        w = np.ascontiguousarray(w, np.float32)
+        check(self.ctx.h, lib().latmap_session_set_dict_weights(self.h, w.ctypes.data_as(C.c_void_p)))
 
     def get_dictionary(self):
         atoms = np.zeros((self.k, self.df), np.float32)

@@ -629,6 +629,7 @@ struct latmap_session {
   // the uploads of later frames overlap.
   std::vector<cudaEvent_t> up_ev;
   cudaEvent_t ev_ready = nullptr;
+  std::vector<float> dict_w;  // DictionaryState::weights (host; k-means maintenance only)
   int64_t graph_launches = 0;
   bool graph_exact = false;
   int32_t graph_dec_path = 0;
@@ -1032,6 +1033,7 @@ latmap_status latmap_session_create(latmap_ctx* ctx, const latmap_config* cfg, i
     delete s;  // leaks partial allocations on failure; acceptable for an OOM path
     return LATMAP_ERR_OUT_OF_MEMORY;
   }
+  s->dict_w.assign((size_t)k, 0.f);
   cudaMemset(s->m, 0, sizeof(float) * s->total);
   cudaMemset(s->v, 0, sizeof(float) * s->total);
   cudaMemset(s->grads, 0, sizeof(float) * s->total);
@@ -1676,6 +1678,71 @@ latmap_status latmap_session_frame_images(latmap_session* s, int32_t b, float** 
   if (depth) *depth = s->depth[b];
   if (query) *query = s->query[b];
   if (alpha) *alpha = s->alpha[b];
+  return LATMAP_OK;
+}
+
+latmap_status latmap_weighted_kmeans(latmap_ctx* ctx, const float* points, const float* weights, int64_t n,
+                                     int32_t dim, int64_t k, latmap_uniform_fn uniform, void* user,
+                                     const float* warm, int64_t n_warm, int32_t max_iters, float* centers,
+                                     float* center_weights, int32_t* iterations) {
+  if (!ctx || n < 0 || dim < 1 || !centers || !center_weights || !iterations || (n > 0 && (!points || !weights)) ||
+      (warm && n_warm < 0) || max_iters < 0)
+    return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "weighted_kmeans: invalid arguments");
+  if (k < 1) return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "weighted_kmeans: k must be >= 1");
+  if (!uniform) return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "weighted_kmeans: no generator");
+  cudaStream_t st = ctx->stream;
+  const int64_t nw = warm ? std::min<int64_t>(n_warm, k) : 0;
+  float *dp = nullptr, *dc = nullptr, *dw = nullptr;
+  CTX_CHECK(ctx, cudaMallocAsync(&dp, sizeof(float) * std::max<int64_t>(n, 1) * dim, st));
+  CTX_CHECK(ctx, cudaMallocAsync(&dc, sizeof(float) * k * dim, st));
+  if (nw > 0) CTX_CHECK(ctx, cudaMallocAsync(&dw, sizeof(float) * nw * dim, st));
+  if (n > 0) CTX_CHECK(ctx, cudaMemcpyAsync(dp, points, sizeof(float) * n * dim, cudaMemcpyHostToDevice, st));
+  if (nw > 0) CTX_CHECK(ctx, cudaMemcpyAsync(dw, warm, sizeof(float) * nw * dim, cudaMemcpyHostToDevice, st));
+  int it = 0;
+  cudaError_t e = kmeans_weighted(st, dp, weights, n, dim, k, uniform, user, nw > 0 ? dw : nullptr, nw, max_iters, dc,
+                                  center_weights, &it);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(centers, dc, sizeof(float) * k * dim, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFreeAsync(dp, st);
+  cudaFreeAsync(dc, st);
+  if (dw) cudaFreeAsync(dw, st);
+  CTX_CHECK(ctx, e);
+  *iterations = it;
+  return post_launch(ctx);
+}
+
+latmap_status latmap_session_stream_kmeans(latmap_session* s, const float* batch, int64_t n, float decay,
+                                           latmap_uniform_fn uniform, void* user) {
+  if (!s || n < 0 || (n > 0 && !batch)) return LATMAP_ERR_INVALID_ARGUMENT;
+  latmap_ctx* ctx = s->ctx;
+  if (!uniform) return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "stream_kmeans_update: no generator");
+  if (n == 0) return LATMAP_OK;  // empty batch: no-op (the pipeline skips maintenance too)
+  cudaStream_t st = ctx->stream;
+  float* db = nullptr;
+  CTX_CHECK(ctx, cudaMallocAsync(&db, sizeof(float) * n * s->df, st));
+  CTX_CHECK(ctx, cudaMemcpyAsync(db, batch, sizeof(float) * n * s->df, cudaMemcpyHostToDevice, st));
+  float* atoms = s->params + s->off[7];
+  cudaError_t e = kmeans_stream_update(st, db, n, s->df, atoms, s->anchor, s->dict_w.data(), s->k, uniform, user, decay);
+  cudaFreeAsync(db, st);
+  CTX_CHECK(ctx, e);
+  // MapOptimizer::reset_atom_moments: AdamState::reset of the atoms block (m = v = 0, step = 0)
+  CTX_CHECK(ctx, cudaMemsetAsync(s->m + s->off[7], 0, sizeof(float) * s->len[7], st));
+  CTX_CHECK(ctx, cudaMemsetAsync(s->v + s->off[7], 0, sizeof(float) * s->len[7], st));
+  CTX_CHECK(ctx, cudaMemsetAsync(s->steps + 7, 0, sizeof(int64_t), st));
+  return post_launch(ctx);
+}
+
+latmap_status latmap_session_get_dict_weights(const latmap_session* s, float* out) {
+  if (!s || !out) return LATMAP_ERR_INVALID_ARGUMENT;
+  std::memcpy(out, s->dict_w.data(), sizeof(float) * s->dict_w.size());
+  return LATMAP_OK;
+}
+
+latmap_status latmap_session_set_dict_weights(latmap_session* s, const float* w) {
+  if (!s || !w) return LATMAP_ERR_INVALID_ARGUMENT;
+  for (size_t j = 0; j < s->dict_w.size(); ++j)
+    if (!(w[j] >= 0.f)) return fail(s->ctx, LATMAP_ERR_INVALID_ARGUMENT, "dictionary weights must be >= 0");
+  std::memcpy(s->dict_w.data(), w, sizeof(float) * s->dict_w.size());
   return LATMAP_OK;
 }
 

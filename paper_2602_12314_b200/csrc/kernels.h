@@ -156,6 +156,13 @@ void adam_flat(cudaStream_t st, float* param, const float* grad, float* m, float
                int nblocks, int64_t* steps, int64_t* skipped, const float* corr1, const float* corr2,
                int32_t table_len, int32_t* flags, const int64_t* overflow);
 
+// Streaming k-means (kmeans.cu): device points / centres / atoms, host weights.
+cudaError_t kmeans_weighted(cudaStream_t st, const float* P, const float* W, int64_t n, int dim, int64_t k,
+                            double (*uni)(void*), void* user, const float* warm, int64_t n_warm, int max_iters,
+                            float* C, float* cw, int* iterations);
+cudaError_t kmeans_stream_update(cudaStream_t st, const float* batch, int64_t n, int dim, float* atoms, float* anchor,
+                                 float* weights, int64_t K, double (*uni)(void*), void* user, float decay);
+
 int umma_selftest(cudaStream_t st, const float* A, const float* B, float* C, int N, int K, int a_mn, int b_mn);
 
 void set_launch_counter(int64_t* c);
