@@ -20,6 +20,15 @@ int main() {
   try { latmap_b200::check(LATMAP_ERR_INVALID_ARGUMENT, nullptr); return 3; } catch (const std::invalid_argument&) {}
   try { latmap_b200::check(LATMAP_ERR_STALE_CACHE, nullptr); return 4; } catch (const std::runtime_error&) {}
   try { latmap_b200::Context ctx(0); std::puts("has-gpu"); } catch (const latmap_b200::device_error&) { std::puts("no-gpu"); }
+  // template instantiations of the k-means entry points (std::mt19937_64 through the callback)
+  std::mt19937_64 rng(12);
+  if (latmap_b200::uniform01_trampoline<std::mt19937_64>(&rng) != 0.18722118704556479) return 5;
+  if (cfg.lambda_feat < 0) {
+    latmap_b200::Context ctx(0);
+    std::vector<float> pts(8, 0.f), w(4, 1.f);
+    auto r = latmap_b200::weighted_kmeans(ctx, pts, w, 2, 2, rng);
+    (void)r;
+  }
   return 0;
 }
 '''
