@@ -56,6 +56,27 @@ double uniform01_trampoline(void* user) {
   return uni(*static_cast<Rng*>(user));
 }
 
+// sample_history (pipeline.cpp:19-37): up to `count` of the n history keyframes, uniform without
+// replacement by a partial Fisher-Yates over indices, drawing from the pipeline's generator
+// exactly as the reference does (one uniform_int_distribution<size_t>(k, n - 1) per slot).
+template <class Rng>
+std::vector<size_t> sample_history(size_t n, int count, Rng& rng) {
+  std::vector<size_t> out;
+  if (n == 0 || count <= 0) return out;
+  if (n <= size_t(count)) {
+    for (size_t i = 0; i < n; ++i) out.push_back(i);
+    return out;
+  }
+  std::vector<size_t> idx(n);
+  for (size_t i = 0; i < n; ++i) idx[i] = i;
+  for (int k = 0; k < count; ++k) {
+    std::uniform_int_distribution<size_t> pick(size_t(k), n - 1);
+    std::swap(idx[size_t(k)], idx[pick(rng)]);
+    out.push_back(idx[size_t(k)]);
+  }
+  return out;
+}
+
 // weighted_kmeans (stream_kmeans.hpp:18-21) on the device; points row-major n x dim.
 struct WeightedKmeansResult {
   std::vector<float> centers;  // k x dim

@@ -23,6 +23,18 @@ int main() {
   // template instantiations of the k-means entry points (std::mt19937_64 through the callback)
   std::mt19937_64 rng(12);
   if (latmap_b200::uniform01_trampoline<std::mt19937_64>(&rng) != 0.18722118704556479) return 5;
+  {
+    std::mt19937_64 a(7), b(7);
+    auto got = latmap_b200::sample_history(10, 4, a);
+    std::vector<size_t> idx(10);
+    for (size_t i = 0; i < 10; ++i) idx[i] = i;
+    for (int k = 0; k < 4; ++k) {  // the reference's loop (pipeline.cpp:29-34)
+      std::uniform_int_distribution<size_t> pick(size_t(k), 9);
+      std::swap(idx[size_t(k)], idx[pick(b)]);
+      if (got[size_t(k)] != idx[size_t(k)]) return 6;
+    }
+    if (latmap_b200::sample_history(3, 5, a).size() != 3 || !latmap_b200::sample_history(0, 5, a).empty()) return 7;
+  }
   if (cfg.lambda_feat < 0) {
     latmap_b200::Context ctx(0);
     std::vector<float> pts(8, 0.f), w(4, 1.f);

@@ -36,3 +36,18 @@ for _ in range(20):
     t3 = time.perf_counter()
     T["set_frames"].append(t1 - t0), T["step_launch"].append(t2 - t1), T["read"].append(t3 - t2), T["total"].append(t3 - t0)
 print({k: round(1e3 * float(np.median(v)), 3) for k, v in T.items()})
+
+# split set_frames: Python argument marshalling vs the C call
+import ctypes as C
+from paper_2602_12314_b200._capi import Frame, lib, check
+cf = (Frame * len(pinned))()
+for i, f in enumerate(pinned):
+    cf[i] = Frame(api.make_pose(f.pose_rot, f.pose_trans), s._np_ptr(f.rgb), s._np_ptr(f.depth),
+                  s._np_ptr(f.assignment), s._np_ptr(f.features), f.features.shape[0])
+tc = []
+for _ in range(20):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    check(ctx.h, lib().latmap_session_set_frames(s.h, len(pinned), cf))
+    tc.append(time.perf_counter() - t0)
+print({"c_set_frames_ms": round(1e3 * float(np.median(tc)), 3)})
