@@ -581,7 +581,8 @@ struct FrameDev {
   int32_t* assign = nullptr;
   float* feats = nullptr;
   size_t c_px = 0, c_feat = 0;
-  int64_t n_set = 0, n_sup = 0;
+  int64_t n_set = 0, n_sup = 0;    // n_sup: host value in segment mode only (pixel mode: stat[0])
+  int64_t* stat = nullptr;          // device [supervised count, out-of-range count] (set_frames)
   // segment mode (objective.cpp:37-64): assignment rows present in the frame, ascending
   int32_t* seg_rows = nullptr;    // n_sup: assignment row of each supervision row
   int32_t* seg_of = nullptr;      // n_set: supervision row of an assignment row (-1 = absent)
@@ -673,6 +674,29 @@ struct latmap_session {
 namespace {
 
 __global__ void set_double_kernel(double* p, double v) { *p = v; }
+__global__ void copy_count_kernel(double* p, const int64_t* v) { *p = (double)*v; }
+
+// gather_supervision's pixel-mode scan (objective.cpp:16-35) on the uploaded assignment: counts
+// the supervised pixels (a >= 0) and the out-of-range ones (a >= n_set), which it rewrites to -1
+// so no later kernel indexes past the embedding table; the error is reported with the loss read.
+__global__ void assign_scan_kernel(int32_t* __restrict__ asg, int64_t npx, int64_t n_set, int64_t* stat) {
+  int64_t nsup = 0, bad = 0;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npx; p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t a = asg[p];
+    if (a >= n_set) {
+      asg[p] = -1;
+      ++bad;
+    } else if (a >= 0) {
+      ++nsup;
+    }
+  }
+  nsup = warp_sum_i64(nsup);
+  bad = warp_sum_i64(bad);
+  if ((threadIdx.x & 31) == 0 && (nsup | bad)) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(stat), (unsigned long long)nsup);
+    atomicAdd(reinterpret_cast<unsigned long long*>(stat + 1), (unsigned long long)bad);
+  }
+}
 
 struct LossWeights {
   float lambda_rgb, lambda_i1, lambda_i2, lambda_depth, lambda_feat, lambda_cos, lambda_l2, lambda_trust;
@@ -848,9 +872,12 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
                  c.lambda_rgb * inv_b, c.lambda_depth * inv_b, map_grad, s->d_color, s->d_depth, part,
                  s->ssim_scratch);
     s->end();
-    set_double_kernel<<<1, 1, 0, st>>>(part + 7, (double)f.n_sup);
+    if (c.segment_mode)
+      set_double_kernel<<<1, 1, 0, st>>>(part + 7, (double)f.n_sup);
+    else
+      copy_count_kernel<<<1, 1, 0, st>>>(part + 7, f.stat);  // supervised pixels, counted on the device
     count_launch();
-    const bool have_sup = f.n_sup > 0;
+    const bool have_sup = c.segment_mode ? f.n_sup > 0 : f.n_set > 0;
     if (have_sup && c.segment_mode) {
       // pooled rows: Q_r = mean of the rendered queries over segment r; the decoder runs on the
       // n_sup rows (targets = features[seg_rows[r]]), then d_query[p] = dQ_r / |segment r|
@@ -860,7 +887,7 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
       seg_pool_kernel<<<gq, 256, 0, st>>>(s->query[b], f.assign, npx, s->ds, f.seg_of, s->seg_q);
       seg_mean_kernel<<<(unsigned)((f.n_sup * s->ds + 255) / 256), 256, 0, st>>>(s->seg_q, f.seg_inv, f.n_sup, s->ds);
       count_launch(2);
-      decoder_frame(st, s->dec, s->seg_q, f.seg_rows, f.n_sup, f.feats, f.n_set, f.n_sup, atoms, proj,
+      decoder_frame(st, s->dec, s->seg_q, f.seg_rows, f.n_sup, f.feats, f.n_set, f.stat, atoms, proj,
                     c.softmax_temp, c.lambda_cos, c.lambda_l2, c.lambda_feat * inv_b, want_grad, s->seg_dq, g_proj,
                     g_atoms, part);
       if (want_grad) {
@@ -873,14 +900,14 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
       const bool fused_ok = decoder_tc_supported(s->k, s->ds, f.n_set) && ctx->decoder_path != 2;
       const bool staged_ok = s->dec.dl_mt && decoder_dl_supported(s->k, s->ds, f.n_set) && ctx->decoder_path != 1;
       if (c.decoder_precision == 1 && fused_ok)
-        decoder_frame_tc(st, s->dec, s->query[b], f.assign, npx, f.feats, f.n_set, f.n_sup, atoms, proj,
+        decoder_frame_tc(st, s->dec, s->query[b], f.assign, npx, f.feats, f.n_set, f.stat, atoms, proj,
                          c.softmax_temp, c.lambda_cos, c.lambda_l2, c.lambda_feat * inv_b, want_grad, s->d_query,
                          g_proj, g_atoms, part);
       else if (c.decoder_precision == 1 && staged_ok)
-        decoder_frame_dl(st, s->dec, s->query[b], f.assign, npx, f.feats, f.n_set, f.n_sup, atoms, c.softmax_temp,
+        decoder_frame_dl(st, s->dec, s->query[b], f.assign, npx, f.feats, f.n_set, f.stat, atoms, c.softmax_temp,
                          c.lambda_cos, c.lambda_l2, c.lambda_feat * inv_b, want_grad, s->d_query, g_atoms, part);
       else
-        decoder_frame(st, s->dec, s->query[b], f.assign, npx, f.feats, f.n_set, f.n_sup, atoms, proj, c.softmax_temp,
+        decoder_frame(st, s->dec, s->query[b], f.assign, npx, f.feats, f.n_set, f.stat, atoms, proj, c.softmax_temp,
                       c.lambda_cos, c.lambda_l2, c.lambda_feat * inv_b, want_grad, s->d_query, g_proj, g_atoms, part);
       s->end();
     }
@@ -924,7 +951,14 @@ latmap_status session_assemble(latmap_session* s, latmap_loss_breakdown* out) {
   count_launch();
   if (out) {
     CTX_CHECK(ctx, cudaMemcpyAsync(out, s->d_loss, sizeof(*out), cudaMemcpyDeviceToHost, st));
+    std::vector<int64_t> stat((size_t)2 * s->nframes, 0);
+    for (int b = 0; b < s->nframes; ++b)
+      if (s->frames[b].stat)
+        CTX_CHECK(ctx, cudaMemcpyAsync(stat.data() + 2 * b, s->frames[b].stat, 2 * sizeof(int64_t),
+                                       cudaMemcpyDeviceToHost, st));
     CTX_CHECK(ctx, cudaStreamSynchronize(st));
+    for (int b = 0; b < s->nframes; ++b)
+      if (stat[2 * b + 1] > 0) return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "gather_supervision: assignment out of range");
   }
   return post_launch(ctx);
 }
@@ -1078,6 +1112,7 @@ latmap_status latmap_session_destroy(latmap_session* s) {
     if (f.depth) cudaFree(f.depth);
     if (f.assign) cudaFree(f.assign);
     if (f.feats) cudaFree(f.feats);
+    if (f.stat) cudaFree(f.stat);
   }
   delete s;
   return LATMAP_OK;
@@ -1144,6 +1179,8 @@ latmap_status latmap_session_set_frames(latmap_session* s, int32_t nf, const lat
   latmap_status st = session_alloc_frames(s, nf);
   if (st != LATMAP_OK) return st;
   const size_t npx = (size_t)s->intr.width * s->intr.height;
+  std::vector<int64_t> nsup0;
+  for (int b = 0; same && b < nf; ++b) nsup0.push_back(s->frames[b].n_sup);
   if (!ctx->copy_stream) CTX_CHECK(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
   if (!s->ev_ready) CTX_CHECK(ctx, cudaEventCreateWithFlags(&s->ev_ready, cudaEventDisableTiming));
   while ((int)s->up_ev.size() < nf) {
@@ -1154,31 +1191,6 @@ latmap_status latmap_session_set_frames(latmap_session* s, int32_t nf, const lat
   // uploads start after the work already queued on the context stream (it may still read them)
   CTX_CHECK(ctx, cudaEventRecord(s->ev_ready, ctx->stream));
   CTX_CHECK(ctx, cudaStreamWaitEvent(ctx->copy_stream, s->ev_ready, 0));
-  // supervised-pixel counts and the assignment range check, one host thread per frame
-  std::vector<int64_t> scan_nsup(nf, 0);
-  std::vector<int32_t> scan_amax(nf, -1);
-  {
-    auto scan = [&](int b) {
-      const int32_t* asg = frames[b].assignment;
-      int64_t ns = 0;
-      int32_t am = -1;
-      for (size_t p = 0; p < npx; ++p) {  // branch-free: vectorises
-        const int32_t a = asg[p];
-        ns += a >= 0;
-        am = a > am ? a : am;
-      }
-      scan_nsup[b] = ns;
-      scan_amax[b] = am;
-    };
-    std::vector<std::thread> pool;
-    for (int b = 1; b < nf && npx >= (1u << 16); ++b) pool.emplace_back(scan, b);
-    scan(0);
-    if (pool.empty())
-      for (int b = 1; b < nf; ++b) scan(b);
-    for (auto& t : pool) t.join();
-  }
-  std::vector<int64_t> nsup0;
-  for (int b = 0; same && b < nf; ++b) nsup0.push_back(s->frames[b].n_sup);
   for (int b = 0; b < nf; ++b) {
     const latmap_frame& in = frames[b];
     FrameDev& f = s->frames[b];
@@ -1202,11 +1214,21 @@ latmap_status latmap_session_set_frames(latmap_session* s, int32_t nf, const lat
     CTX_CHECK(ctx, cudaMemcpyAsync(f.depth, in.depth, sizeof(float) * npx, cudaMemcpyHostToDevice, cs));
     CTX_CHECK(ctx, cudaMemcpyAsync(f.assign, in.assignment, sizeof(int32_t) * npx, cudaMemcpyHostToDevice, cs));
     if (nfeat) CTX_CHECK(ctx, cudaMemcpyAsync(f.feats, in.features, sizeof(float) * nfeat, cudaMemcpyHostToDevice, cs));
+    if (!f.stat) CTX_CHECK(ctx, cudaMalloc(&f.stat, 2 * sizeof(int64_t)));
+    int64_t nsup = 0;
+    if (!s->cfg.segment_mode) {
+      // supervised-pixel count and range check on the device, behind the upload (reported by the
+      // objective call that reads the loss, as gather_supervision throws inside total_objective)
+      CTX_CHECK(ctx, cudaMemsetAsync(f.stat, 0, 2 * sizeof(int64_t), cs));
+      assign_scan_kernel<<<(unsigned)std::min<size_t>((npx + 1023) / 1024, 148 * 4), 256, 0, cs>>>(f.assign, (int64_t)npx,
+                                                                                                 in.n_set, f.stat);
+      count_launch();
+    }
     CTX_CHECK(ctx, cudaEventRecord(s->up_ev[b], cs));
-    int64_t nsup = scan_nsup[b];
-    const int32_t amax = scan_amax[b];
-    if (amax >= in.n_set) return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "gather_supervision: assignment out of range");
     if (s->cfg.segment_mode) {
+      int32_t amax = -1;
+      for (size_t p = 0; p < npx; ++p) amax = std::max(amax, in.assignment[p]);
+      if (amax >= in.n_set) return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "gather_supervision: assignment out of range");
       // present assignment rows in ascending order (objective.cpp:39-64)
       std::vector<int64_t> cnt((size_t)std::max<int64_t>(in.n_set, 1), 0);
       for (size_t p = 0; p < npx; ++p)
@@ -1239,6 +1261,10 @@ latmap_status latmap_session_set_frames(latmap_session* s, int32_t nf, const lat
         CTX_CHECK(ctx, cudaMalloc(&s->seg_dq, sizeof(float) * need * s->ds));
         s->seg_cap = (int64_t)need;
       }
+    }
+    if (s->cfg.segment_mode) {
+      const int64_t h[2] = {nsup, 0};  // supervision rows = present segments
+      CTX_CHECK(ctx, cudaMemcpy(f.stat, h, sizeof(h), cudaMemcpyHostToDevice));
     }
     f.n_sup = nsup;
     f.n_set = in.n_set;

@@ -117,8 +117,9 @@ __global__ void softmax_rows_kernel(float* __restrict__ x, int64_t n, int k) {
 __global__ void decoder_rows_kernel(const float* __restrict__ P, float* __restrict__ T, int64_t n, int k,
                                     const int32_t* __restrict__ assign, const float* __restrict__ gt,
                                     const float* __restrict__ nv, float inv_temp, float lambda_cos, float lambda_l2,
-                                    float inv_nsup, float scale, float* __restrict__ alpha_r,
+                                    const int64_t* __restrict__ nsup, float scale, float* __restrict__ alpha_r,
                                     float* __restrict__ beta_r, double* partials) {
+  const float inv_nsup = *nsup > 0 ? 1.f / (float)*nsup : 0.f;
   const int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   double cos_acc = 0.0, l2_acc = 0.0, zflag = 0.0;
@@ -423,7 +424,7 @@ void decoder_prepare(cudaStream_t st, DecoderWork& w, const float* atoms, const 
 }
 
 void decoder_frame(cudaStream_t st, DecoderWork& w, const float* query, const int32_t* assignment, int64_t npx,
-                   const float* feats, int64_t n_set, int64_t n_sup, const float* atoms, const float* proj,
+                   const float* feats, int64_t n_set, const int64_t* nsup, const float* atoms, const float* proj,
                    float temperature, float lambda_cos, float lambda_l2, float scale, bool want_grad, float* d_query,
                    float* d_proj, float* d_atoms, double* partials) {
   const int64_t k = w.k;
@@ -439,7 +440,7 @@ void decoder_frame(cudaStream_t st, DecoderWork& w, const float* query, const in
   sgemm(st, false, false, npx, k, k, 1.f, w.buf1, k, w.mm, k, 0.f, w.buf2, k);
   decoder_rows_kernel<<<grid_for(npx * 32, 256, 1 << 30), 256, 0, st>>>(
       w.buf1, w.buf2, npx, (int)k, assignment, w.gt, w.nv, inv_temp, lambda_cos, lambda_l2,
-      n_sup > 0 ? 1.f / (float)n_sup : 0.f, scale, w.alpha_r, w.beta_r, partials);
+      nsup, scale, w.alpha_r, w.beta_r, partials);
   count_launch();
   if (!want_grad) return;
   // d_query = dS Kd   (n x ds)

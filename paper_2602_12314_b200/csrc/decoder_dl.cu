@@ -366,7 +366,8 @@ struct Dl3Args {
   double* loss_part;   // gridDim x 4
   int64_t npx;
   int K, NB;
-  float inv_temp, lambda_cos, lambda_l2, inv_nsup, scale;
+  float inv_temp, lambda_cos, lambda_l2, scale;
+  const int64_t* nsup;  // supervised rows (device)
   int want_grad;
 };
 
@@ -411,6 +412,7 @@ __global__ void __launch_bounds__(512, 1) dl_back_kernel(Dl3Args a) {
   const uint32_t idq = tc::make_idesc_bf16(128, DS, 0, 1), ir = tc::make_idesc_bf16(128, DS, 1, 1);
   const int64_t ntiles = (a.npx + kRows - 1) / kRows, ntr = ntiles * kRows;
   const int NC = K / 256;
+  const float inv_nsup = *a.nsup > 0 ? 1.f / (float)*a.nsup : 0.f;
   int pc = 0;
   bool first = true;
   double cos_acc = 0.0, l2_acc = 0.0, zflag = 0.0;
@@ -435,8 +437,8 @@ __global__ void __launch_bounds__(512, 1) dl_back_kernel(Dl3Args a) {
         cos_acc += 1.0 - (double)(dot / (nug * nvg));
         l2_acc += (double)nu2 - 2.0 * (double)dot + (double)vn * (double)vn;
       }
-      al = a.scale * (a.lambda_cos * dot / (nug * nug * nug * nvg) * a.inv_nsup + 2.f * a.lambda_l2 * a.inv_nsup);
-      be = a.scale * (-a.lambda_cos / (nug * nvg) * a.inv_nsup - 2.f * a.lambda_l2 * a.inv_nsup);
+      al = a.scale * (a.lambda_cos * dot / (nug * nug * nug * nvg) * inv_nsup + 2.f * a.lambda_l2 * inv_nsup);
+      be = a.scale * (-a.lambda_cos / (nug * nvg) * inv_nsup - 2.f * a.lambda_l2 * inv_nsup);
       cc = al * nu2 + be * dot;
     }
     if (!a.want_grad) continue;
@@ -803,7 +805,7 @@ void set_smem(F* f, size_t bytes) {
 
 template <int DS>
 void launch_dl(cudaStream_t st, DecoderWork& w, const float* query, const int32_t* assignment, int64_t npx,
-               int64_t n_set, int64_t n_sup, float temperature, float lambda_cos, float lambda_l2, float scale,
+               int64_t n_set, const int64_t* nsup, float temperature, float lambda_cos, float lambda_l2, float scale,
                bool want_grad, float* d_query, double* partials) {
   const int K = (int)w.k;
   const int NB = nb_for(n_set), NTOT = K + NB;
@@ -831,7 +833,7 @@ void launch_dl(cudaStream_t st, DecoderWork& w, const float* query, const int32_
   {
     Dl3Args d{w.e_tiles, reinterpret_cast<const uint4*>(w.dl_t), w.dl_nu, reinterpret_cast<const float4*>(w.row_stats), query, assignment, w.kd,
               w.gt, w.nv, w.dl_ae, d_query, w.r_part + 148 * (size_t)K * DS, w.loss_part, npx, K, NB, inv_temp, lambda_cos, lambda_l2,
-              n_sup > 0 ? 1.f / (float)n_sup : 0.f, scale, want_grad ? 1 : 0};
+              scale, nsup, want_grad ? 1 : 0};
     const size_t sm = (size_t)(K / 2) * DS * 2 + (size_t)kRows * DS * 2 + 2 * 32768;
     set_smem(dl_back_kernel<DS>, sm);
     dl_back_kernel<DS><<<2 * kBackGroups, 512, sm, st>>>(d);
@@ -898,17 +900,17 @@ void decoder_dl_prepare(cudaStream_t st, DecoderWork& w) {
 }
 
 void decoder_frame_dl(cudaStream_t st, DecoderWork& w, const float* query, const int32_t* assignment, int64_t npx,
-                      const float* feats, int64_t n_set, int64_t n_sup, const float* atoms, float temperature,
+                      const float* feats, int64_t n_set, const int64_t* nsup, const float* atoms, float temperature,
                       float lambda_cos, float lambda_l2, float scale, bool want_grad, float* d_query,
                       float* d_atoms, double* partials) {
   const int64_t k = w.k;
   const int df = w.df;
   decoder_targets(st, feats, n_set, atoms, k, df, w.gt, w.nv);
   if (w.ds == 64)
-    launch_dl<64>(st, w, query, assignment, npx, n_set, n_sup, temperature, lambda_cos, lambda_l2, scale, want_grad,
+    launch_dl<64>(st, w, query, assignment, npx, n_set, nsup, temperature, lambda_cos, lambda_l2, scale, want_grad,
                   d_query, partials);
   else
-    launch_dl<32>(st, w, query, assignment, npx, n_set, n_sup, temperature, lambda_cos, lambda_l2, scale, want_grad,
+    launch_dl<32>(st, w, query, assignment, npx, n_set, nsup, temperature, lambda_cos, lambda_l2, scale, want_grad,
                   d_query, partials);
   if (!want_grad) return;
   decoder_bm_embed(st, w.bm, feats, n_set, k, df, d_atoms);

@@ -45,7 +45,8 @@ struct Dec1Args {
   const float* gt;          // n_set x K fp32 (E D^T)
   const float* nv;          // n_set (target row norms)
   int64_t npx;
-  float inv_temp, lambda_cos, lambda_l2, inv_nsup, scale;
+  float inv_temp, lambda_cos, lambda_l2, scale;
+  const int64_t* nsup;      // supervised rows (device)
   float* d_query;           // npx x DS
   float4* row_stats;        // npx: (max S, 1/sum, alpha, beta)
   float* r_part;            // gridDim x K x DS
@@ -98,6 +99,7 @@ __global__ void __launch_bounds__(512, 1) dec1_kernel(Dec1Args a) {
   const uint32_t idesc4 = tc::make_idesc_bf16(128, DS, 1, 1);
   const uint32_t aQ = tc::smem_u32(sQ), aKd = tc::smem_u32(sKd), aP = tc::smem_u32(sP), aM = tc::smem_u32(sM);
   const float cl = kLog2e * a.inv_temp;
+  const float inv_nsup = *a.nsup > 0 ? 1.f / (float)*a.nsup : 0.f;
   double cos_acc = 0.0, l2_acc = 0.0, zflag = 0.0;
   bool first = true;
 
@@ -233,8 +235,8 @@ __global__ void __launch_bounds__(512, 1) dec1_kernel(Dec1Args a) {
         cos_acc += 1.0 - (double)(dot / (nug * nvg));
         l2_acc += (double)nu2 - 2.0 * (double)dot + (double)vn * (double)vn;
       }
-      al = a.scale * (a.lambda_cos * dot / (nug * nug * nug * nvg) * a.inv_nsup + 2.f * a.lambda_l2 * a.inv_nsup);
-      be = a.scale * (-a.lambda_cos / (nug * nvg) * a.inv_nsup - 2.f * a.lambda_l2 * a.inv_nsup);
+      al = a.scale * (a.lambda_cos * dot / (nug * nug * nug * nvg) * inv_nsup + 2.f * a.lambda_l2 * inv_nsup);
+      be = a.scale * (-a.lambda_cos / (nug * nvg) * inv_nsup - 2.f * a.lambda_l2 * inv_nsup);
       cc = al * nu2 + be * dot;
     }
     if (qt == 0 && row < valid) a.row_stats[grow] = make_float4(mx, inv_sum, al, be);
@@ -673,13 +675,13 @@ __global__ void __launch_bounds__(256) bm_embed_fused_kernel(const float* __rest
 
 template <int K, int DS>
 void launch_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_t* assignment, int64_t npx,
-               const float* feats, int64_t n_set, int64_t n_sup, float temperature, float lambda_cos, float lambda_l2,
+               const float* feats, int64_t n_set, const int64_t* nsup, float temperature, float lambda_cos, float lambda_l2,
                float scale, bool want_grad, float* d_query, double* partials) {
   const int g1 = 148;
   const int g2 = 148;  // 74 groups x 2 roles
   const int accum = want_grad && w.tc_frames > 0 ? 1 : 0;
   Dec1Args d1{w.e_tiles, query, assignment, w.kd, w.mm, w.gt, w.nv, npx, 1.f / temperature, lambda_cos, lambda_l2,
-              n_sup > 0 ? 1.f / (float)n_sup : 0.f, scale, d_query, reinterpret_cast<float4*>(w.row_stats),
+              scale, nsup, d_query, reinterpret_cast<float4*>(w.row_stats),
               w.r_part, w.loss_part, want_grad ? 1 : 0, accum};
   const size_t sm1 = (size_t)kRows * DS * 2 + (size_t)K * DS * 2 + (size_t)kRows * K * 2 + (size_t)K * K * 2 +
                      16 * 128 * 4;
@@ -724,7 +726,7 @@ size_t decoder_tc_scratch_floats(int64_t k, int ds, int64_t npx) {
 }
 
 void decoder_frame_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_t* assignment, int64_t npx,
-                      const float* feats, int64_t n_set, int64_t n_sup, const float* atoms, const float* proj,
+                      const float* feats, int64_t n_set, const int64_t* nsup, const float* atoms, const float* proj,
                       float temperature, float lambda_cos, float lambda_l2, float scale, bool want_grad, float* d_query,
                       float* d_proj, float* d_atoms, double* partials) {
   const int64_t k = w.k;
@@ -732,10 +734,10 @@ void decoder_frame_tc(cudaStream_t st, DecoderWork& w, const float* query, const
   // per-frame target scores G^T = E D^T and norms (tiny SIMT GEMMs)
   decoder_targets(st, feats, n_set, atoms, k, df, w.gt, w.nv);
   if (k == 256)
-    launch_tc<256, 32>(st, w, query, assignment, npx, feats, n_set, n_sup, temperature, lambda_cos, lambda_l2, scale,
+    launch_tc<256, 32>(st, w, query, assignment, npx, feats, n_set, nsup, temperature, lambda_cos, lambda_l2, scale,
                        want_grad, d_query, partials);
   else
-    launch_tc<128, 32>(st, w, query, assignment, npx, feats, n_set, n_sup, temperature, lambda_cos, lambda_l2, scale,
+    launch_tc<128, 32>(st, w, query, assignment, npx, feats, n_set, nsup, temperature, lambda_cos, lambda_l2, scale,
                        want_grad, d_query, partials);
   if (!want_grad) return;
   // d_atoms += Bm E for this frame's embedding table; A and R accumulate over the step's frames

@@ -108,8 +108,9 @@ struct DecoderWork {
 void decoder_prepare(cudaStream_t st, DecoderWork& w, const float* atoms, const float* proj);
 // Fused feature loss + decoder backward for one frame (pixel mode). Accumulates into d_proj,
 // d_atoms (scaled by lambda_feat * inv_b) and writes d_query (HxWxds, scaled likewise).
+// nsup: device int64, the supervised-row count (inv_nsup = 1 / nsup, 0 without supervision).
 void decoder_frame(cudaStream_t st, DecoderWork& w, const float* query, const int32_t* assignment,
-                   int64_t npx, const float* feats, int64_t n_set, int64_t n_sup, const float* atoms,
+                   int64_t npx, const float* feats, int64_t n_set, const int64_t* nsup, const float* atoms,
                    const float* proj, float temperature, float lambda_cos, float lambda_l2, float scale,
                    bool want_grad, float* d_query, float* d_proj, float* d_atoms, double* partials);
 void decoder_target_norms(cudaStream_t st, const float* feats, int64_t n_set, int df, float* nv);
@@ -122,7 +123,7 @@ void decoder_bm_embed(cudaStream_t st, const float* bmt, const float* feats, int
 // tcgen05 / TMEM path (bf16 operands, fp32 accumulation) for K in {128, 256}, d_s = 32, n_set <= 64.
 bool decoder_tc_supported(int64_t k, int ds, int64_t n_set);
 void decoder_frame_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_t* assignment,
-                      int64_t npx, const float* feats, int64_t n_set, int64_t n_sup, const float* atoms,
+                      int64_t npx, const float* feats, int64_t n_set, const int64_t* nsup, const float* atoms,
                       const float* proj, float temperature, float lambda_cos, float lambda_l2, float scale,
                       bool want_grad, float* d_query, float* d_proj, float* d_atoms, double* partials);
 // Staged tcgen05 path for large dictionaries (decoder_dl.cu): K in {256..1024} (multiple of 256),
@@ -131,7 +132,7 @@ bool decoder_dl_supported(int64_t k, int ds, int64_t n_set);
 size_t decoder_dl_part_floats(int64_t k);
 void decoder_dl_prepare(cudaStream_t st, DecoderWork& w);
 void decoder_frame_dl(cudaStream_t st, DecoderWork& w, const float* query, const int32_t* assignment,
-                      int64_t npx, const float* feats, int64_t n_set, int64_t n_sup, const float* atoms,
+                      int64_t npx, const float* feats, int64_t n_set, const int64_t* nsup, const float* atoms,
                       float temperature, float lambda_cos, float lambda_l2, float scale, bool want_grad,
                       float* d_query, float* d_atoms, double* partials);
 // Applies the step-accumulated A and R of the tcgen05 frames: d_atoms += A D + R^T W, d_proj += R D.

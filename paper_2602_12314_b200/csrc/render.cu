@@ -228,16 +228,24 @@ __global__ void __launch_bounds__(1024) scan_tiles_kernel(const int32_t* __restr
 // with a single global atomic, then fills it (slot order inside a bucket is irrelevant: the
 // per-tile sort below makes the list canonical). 2048 Gaussians per block keep the number of
 // global reservations (blocks x touched tiles) low; culled Gaussians are skipped via the
-// projection's depth keys without touching their records.
+// projection's depth keys without touching their records. Footprints of up to kBigFootprint
+// tiles are walked by their own thread; larger ones (Gaussians close to the camera: hundreds to
+// thousands of tiles) are queued and walked by whole warps, a lane per tile, so one near splat
+// does not serialise its block.
 constexpr int kScatterPerThread = 4;
 constexpr int kScatterThreads = 512;
+constexpr int kBigFootprint = 24;  // tiles
 __global__ void __launch_bounds__(kScatterThreads, 2) scatter_kernel(const SplatRec* __restrict__ rec,
                                                       const uint32_t* __restrict__ dkey, int64_t n, int tiles_x,
                                                       int ntiles, int32_t* cursor, uint64_t* __restrict__ keys,
                                                       int64_t pair_cap) {
   extern __shared__ int32_t s_cnt[];
   int32_t* s_base = s_cnt + ntiles;
+  __shared__ int32_t s_big[kScatterThreads * kScatterPerThread];
+  __shared__ int32_t s_nbig;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s_cnt[t] = 0;
+  if (threadIdx.x == 0) s_nbig = 0;
   __syncthreads();
   const int64_t b0 = (int64_t)blockIdx.x * blockDim.x * kScatterPerThread;
   uint32_t dk[kScatterPerThread];
@@ -251,11 +259,26 @@ __global__ void __launch_bounds__(kScatterThreads, 2) scatter_kernel(const Splat
 #pragma unroll
   for (int r = 0; r < kScatterPerThread; ++r)
     if (dk[r] != kCulledKey) bb[r] = reinterpret_cast<const int4*>(rec + b0 + (int64_t)r * blockDim.x + threadIdx.x)[2];
+  bool big[kScatterPerThread];
 #pragma unroll
   for (int r = 0; r < kScatterPerThread; ++r) {
+    big[r] = false;
     if (dk[r] == kCulledKey) continue;
-    for (int ty = bb[r].z / kTile; ty <= bb[r].w / kTile; ++ty)
-      for (int tx = bb[r].x / kTile; tx <= bb[r].y / kTile; ++tx) atomicAdd(&s_cnt[ty * tiles_x + tx], 1);
+    const int tx0 = bb[r].x / kTile, tx1 = bb[r].y / kTile, ty0 = bb[r].z / kTile, ty1 = bb[r].w / kTile;
+    if ((tx1 - tx0 + 1) * (ty1 - ty0 + 1) > kBigFootprint) {
+      big[r] = true;
+      s_big[atomicAdd(&s_nbig, 1)] = r * blockDim.x + threadIdx.x;
+      continue;
+    }
+    for (int ty = ty0; ty <= ty1; ++ty)
+      for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(&s_cnt[ty * tiles_x + tx], 1);
+  }
+  __syncthreads();
+  const int nbig = s_nbig;
+  for (int e = warp; e < nbig; e += nwarps) {
+    const int4 q = reinterpret_cast<const int4*>(rec + b0 + s_big[e])[2];
+    const int tx0 = q.x / kTile, ty0 = q.z / kTile, w = q.y / kTile - tx0 + 1, nt = w * (q.w / kTile - ty0 + 1);
+    for (int t = lane; t < nt; t += 32) atomicAdd(&s_cnt[(ty0 + t / w) * tiles_x + tx0 + t % w], 1);
   }
   __syncthreads();
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
@@ -266,7 +289,7 @@ __global__ void __launch_bounds__(kScatterThreads, 2) scatter_kernel(const Splat
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < kScatterPerThread; ++r) {
-    if (dk[r] == kCulledKey) continue;
+    if (dk[r] == kCulledKey || big[r]) continue;
     const uint64_t key = ((uint64_t)dk[r] << 32) | (uint32_t)(b0 + (int64_t)r * blockDim.x + threadIdx.x);
     for (int ty = bb[r].z / kTile; ty <= bb[r].w / kTile; ++ty)
       for (int tx = bb[r].x / kTile; tx <= bb[r].y / kTile; ++tx) {
@@ -274,6 +297,17 @@ __global__ void __launch_bounds__(kScatterThreads, 2) scatter_kernel(const Splat
         const int64_t pos = (int64_t)s_base[t] + atomicAdd(&s_cnt[t], 1);
         if (pos < pair_cap) keys[pos] = key;
       }
+  }
+  for (int e = warp; e < nbig; e += nwarps) {
+    const int64_t src = b0 + s_big[e];
+    const int4 q = reinterpret_cast<const int4*>(rec + src)[2];
+    const uint64_t key = ((uint64_t)dkey[src] << 32) | (uint32_t)src;
+    const int tx0 = q.x / kTile, ty0 = q.z / kTile, w = q.y / kTile - tx0 + 1, nt = w * (q.w / kTile - ty0 + 1);
+    for (int t = lane; t < nt; t += 32) {
+      const int tile = (ty0 + t / w) * tiles_x + tx0 + t % w;
+      const int64_t pos = (int64_t)s_base[tile] + atomicAdd(&s_cnt[tile], 1);
+      if (pos < pair_cap) keys[pos] = key;
+    }
   }
 }
 

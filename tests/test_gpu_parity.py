@@ -18,6 +18,7 @@ pytestmark = pytest.mark.gpu
 
 from paper_2602_12314_b200 import api  # noqa: E402
 from paper_2602_12314_b200 import synthetic  # noqa: E402
+from paper_2602_12314_b200 import _capi  # noqa: E402
 from paper_2602_12314_b200._capi import StaleCache  # noqa: E402
 
 THREADS = 8
@@ -530,3 +531,21 @@ def test_seed_gaussians_candidates_and_append(ctx, cfg0):
     m = s.get_map()
     assert np.array_equal(m["positions"][n0:], rows[:, :3]) and np.array_equal(m["features"][n0:], feats)
     assert np.isfinite(s.step(read=True)["total"])
+
+
+def test_assignment_out_of_range_is_reported(ctx, cfg0):
+    """gather_supervision (objective.cpp:16-35) rejects an assignment >= n_set. The pixel-mode scan
+    runs on the device behind the keyframe upload, so the objective call that reads the loss
+    raises (the reference throws from inside total_objective); a valid batch afterwards works."""
+    import copy
+    w = cfg0
+    bad = copy.deepcopy(w.frames[0])
+    bad.assignment = bad.assignment.copy()
+    bad.assignment.reshape(-1)[17] = bad.features.shape[0]  # == n_set: out of range
+    s = make_session(ctx, w)
+    s.set_frames([bad])
+    with pytest.raises(_capi.InvalidArgument, match="assignment out of range"):
+        s.objective(want_grad=True)
+    s.set_frames(w.frames)
+    loss = s.objective(want_grad=True)
+    assert np.isfinite(loss["total"]) and loss["supervised_rows"] == int((w.frames[0].assignment >= 0).sum())
