@@ -1357,29 +1357,36 @@ __global__ void __launch_bounds__(256) project_bwd_kernel(ProjBwdArgs a) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= a.map.n) return;
   const float4* rv = reinterpret_cast<const float4*>(a.rec + i);
+  // every load is issued before the culled test (one memory round trip instead of two; a culled
+  // Gaussian's extra bytes cost less than the serialised latency): 16-byte loads of the record,
+  // the accumulators (re-zeroed below for the next frame), the quaternion
   const int4 bb = reinterpret_cast<const int4*>(a.rec + i)[2];
-  if (bb.x > bb.y) return;
-  // 16-byte loads of the record, the accumulators (then re-zeroed for the next frame) and the
-  // quaternion; everything is issued before the math
-  const float4 r0 = rv[0], r1 = rv[1];
+  const float4 r0 = ld_early4(rv), r1 = ld_early4(rv + 1);
   float4* acc4 = reinterpret_cast<float4*>(a.geo_acc + 8 * i);
-  const float4 g0 = acc4[0], g1 = acc4[1];
-  acc4[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-  acc4[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 g0 = ld_early4(acc4), g1 = ld_early4(acc4 + 1);
   const float ac[7] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z};
-  const float pv[3] = {a.map.pos[3 * i], a.map.pos[3 * i + 1], a.map.pos[3 * i + 2]};
+  const float pv[3] = {ld_early(a.map.pos + 3 * i), ld_early(a.map.pos + 3 * i + 1), ld_early(a.map.pos + 3 * i + 2)};
   const float4 q4 = (reinterpret_cast<uintptr_t>(a.map.rot) & 15) == 0
-                        ? reinterpret_cast<const float4*>(a.map.rot)[i]
+                        ? ld_early4(reinterpret_cast<const float4*>(a.map.rot) + i)
                         : make_float4(a.map.rot[4 * i], a.map.rot[4 * i + 1], a.map.rot[4 * i + 2], a.map.rot[4 * i + 3]);
-  const float lv[3] = {a.map.lsc[3 * i], a.map.lsc[3 * i + 1], a.map.lsc[3 * i + 2]};
+  const float lv[3] = {ld_early(a.map.lsc + 3 * i), ld_early(a.map.lsc + 3 * i + 1), ld_early(a.map.lsc + 3 * i + 2)};
   const float* p = pv;
   const float q[4] = {q4.x, q4.y, q4.z, q4.w};
   const float* ls = lv;
   // the gradient read-modify-writes: loads issued here, independent of the math below
-  const float go = a.grads.opa[i];
-  const float gl[3] = {a.grads.lsc[3 * i], a.grads.lsc[3 * i + 1], a.grads.lsc[3 * i + 2]};
-  const float gr[4] = {a.grads.rot[4 * i], a.grads.rot[4 * i + 1], a.grads.rot[4 * i + 2], a.grads.rot[4 * i + 3]};
-  const float gp[3] = {a.grads.pos[3 * i], a.grads.pos[3 * i + 1], a.grads.pos[3 * i + 2]};
+  const float go = ld_early(a.grads.opa + i);
+  const float gl[3] = {ld_early(a.grads.lsc + 3 * i), ld_early(a.grads.lsc + 3 * i + 1), ld_early(a.grads.lsc + 3 * i + 2)};
+  const float gr[4] = {ld_early(a.grads.rot + 4 * i), ld_early(a.grads.rot + 4 * i + 1), ld_early(a.grads.rot + 4 * i + 2),
+                       ld_early(a.grads.rot + 4 * i + 3)};
+  const float gp[3] = {ld_early(a.grads.pos + 3 * i), ld_early(a.grads.pos + 3 * i + 1), ld_early(a.grads.pos + 3 * i + 2)};
+  // culled (empty bbox): no accumulation happened, nothing is written. The test only guards the
+  // stores, so the loads above are all in flight together (an early exit lets the compiler sink
+  // them behind it: two serialised round trips)
+  const bool vis = bb.x <= bb.y;
+  if (vis) {
+    acc4[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    acc4[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   const float d0 = p[0] - a.o[0], d1 = p[1] - a.o[1], d2 = p[2] - a.o[2];
   float pc[3];
   for (int r = 0; r < 3; ++r) pc[r] = a.rcw[3 * r] * d0 + a.rcw[3 * r + 1] * d1 + a.rcw[3 * r + 2] * d2;
@@ -1403,7 +1410,7 @@ __global__ void __launch_bounds__(256) project_bwd_kernel(ProjBwdArgs a) {
   const float J[6] = {fx / z, 0.f, -fx * x / (z * z), 0.f, fy / z, -fy * y / (z * z)};
   const float A[4] = {r1.x, r1.y, r1.z, r1.w};  // cov_inv from the forward record (identical values)
   const float alpha = r0.w;
-  a.grads.opa[i] = go + ac[6] * alpha * (1.f - alpha);
+  if (vis) a.grads.opa[i] = go + ac[6] * alpha * (1.f - alpha);
   const float dA[4] = {ac[2], ac[3], ac[3], ac[4]};
   float t1[4], dc[4];
   for (int r = 0; r < 2; ++r)
@@ -1429,8 +1436,9 @@ __global__ void __launch_bounds__(256) project_bwd_kernel(ProjBwdArgs a) {
   for (int r = 0; r < 3; ++r)
     for (int c = 0; c < 3; ++c)
       drg[3 * r + c] = (a.rcw[r] * dm_[c] + a.rcw[3 + r] * dm_[3 + c] + a.rcw[6 + r] * dm_[6 + c]) * sc[c];
-  for (int c = 0; c < 3; ++c)
-    a.grads.lsc[3 * i + c] = gl[c] + (rcg[c] * dm_[c] + rcg[3 + c] * dm_[3 + c] + rcg[6 + c] * dm_[6 + c]) * sc[c];
+  if (vis)
+    for (int c = 0; c < 3; ++c)
+      a.grads.lsc[3 * i + c] = gl[c] + (rcg[c] * dm_[c] + rcg[3 + c] * dm_[3 + c] + rcg[6 + c] * dm_[6 + c]) * sc[c];
   const float dw[9] = {0.f, -qz, qy, qz, 0.f, -qx, -qy, qx, 0.f};
   const float dxm[9] = {0.f, qy, qz, qy, -2.f * qx, -qw, qz, qw, -2.f * qx};
   const float dym[9] = {-2.f * qy, qx, qw, qx, 0.f, qz, -qw, qz, -2.f * qy};
@@ -1445,7 +1453,8 @@ __global__ void __launch_bounds__(256) project_bwd_kernel(ProjBwdArgs a) {
   for (int r = 0; r < 4; ++r) dq[r] *= 2.f;
   const float qh[4] = {qw, qx, qy, qz};
   const float qd = qh[0] * dq[0] + qh[1] * dq[1] + qh[2] * dq[2] + qh[3] * dq[3];
-  for (int r = 0; r < 4; ++r) a.grads.rot[4 * i + r] = gr[r] + (dq[r] - qh[r] * qd) / qn;
+  if (vis)
+    for (int r = 0; r < 4; ++r) a.grads.rot[4 * i + r] = gr[r] + (dq[r] - qh[r] * qd) / qn;
   float dp[3] = {0.f, 0.f, 0.f};
   const float z2 = z * z, z3 = z2 * z;
   dp[0] += ac[0] * fx / z;
@@ -1456,8 +1465,9 @@ __global__ void __launch_bounds__(256) project_bwd_kernel(ProjBwdArgs a) {
   dp[1] += djac[5] * (-fy / z2);
   dp[2] += djac[0] * (-fx / z2) + djac[2] * (2.f * fx * x / z3) + djac[4] * (-fy / z2) + djac[5] * (2.f * fy * y / z3);
   dp[2] += ac[5];
-  for (int r = 0; r < 3; ++r)
-    a.grads.pos[3 * i + r] = gp[r] + (a.rwc[3 * r] * dp[0] + a.rwc[3 * r + 1] * dp[1] + a.rwc[3 * r + 2] * dp[2]);
+  if (vis)
+    for (int r = 0; r < 3; ++r)
+      a.grads.pos[3 * i + r] = gp[r] + (a.rwc[3 * r] * dp[0] + a.rwc[3 * r + 1] * dp[1] + a.rwc[3 * r + 2] * dp[2]);
 }
 
 // project_gaussian (render.cpp:118-132): one Gaussian, returns cov2d (not its inverse).
