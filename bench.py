@@ -247,7 +247,7 @@ def run_streaming(args, hbm_peak):
     s = api.Session(ctx, cfg, 0, 32, st.atoms.shape[0], st.atoms.shape[1], intr)
     s.set_dictionary(st.atoms, st.atoms, st.proj)
     origin = np.zeros(0, np.int64)
-    stats_all, active = [], []
+    stats_all, active, vis_all, pairs_all = [], [], [], []
 
     def one_frame(f):
         nonlocal origin
@@ -276,6 +276,9 @@ def run_streaming(args, hbm_peak):
     for f in range(args.warmup, nfr):
         stats_all.append(one_frame(f))
         active.append(s.n)
+        vis_f, pairs_f = s.stats(1)
+        vis_all.append(float(vis_f[0]))
+        pairs_all.append(float(pairs_f[0]))
     ev1.record(stream)
     torch.cuda.synchronize()
     wall = (time.perf_counter() - tw) * 1000.0
@@ -294,6 +297,7 @@ def run_streaming(args, hbm_peak):
                        "query_dim": 32, "dict_K": 256, "embed_D": 1024, "parallelism": "single GPU",
                        "step": "one step = one frame: store sync + 10 Stage-I iterations"},
             "frames_per_s": 1000.0 * args.steps / ms, "active_mean": float(np.mean(active)),
+            "visible_per_frame": float(np.mean(vis_all)), "tile_pairs_per_frame": float(np.mean(pairs_all)),
             "records_moved_per_frame": moved / max(1, args.steps),
             "sync_stats_last": stats_all[-1] if stats_all else None, "gpu_launches": int(ctx.launches() - launches0),
             "clocks": clocks, "loss_last": last["total"], "setup_s": gen_s}

@@ -587,8 +587,12 @@ class Store:
         dty = np.ascontiguousarray(dirty, np.uint8)
         c = np.ascontiguousarray(center, np.float32)
         cap = self.size() + n + 1
-        d_out = torch.empty((cap, self.rs), device=f"cuda:{self.ctx.device}")
-        oo = np.zeros(cap, np.int64)
+        # output buffers sized for the worst case (every stored record in radius) are kept across
+        # calls: a fresh ~1 GB device buffer and a zero-filled origin array per frame cost tens of ms
+        if getattr(self, "_dout", None) is None or self._dout.shape[0] < cap:
+            self._dout = torch.empty((cap + cap // 8, self.rs), device=f"cuda:{self.ctx.device}")
+            self._oo = np.empty(cap + cap // 8, np.int64)
+        d_out, oo = self._dout, self._oo
         kept = np.zeros(max(n, 1), np.uint8)
         st = np.zeros(5, np.int64)
         cnt = C.c_int64(0)
@@ -600,4 +604,4 @@ class Store:
                                             C.byref(cnt)))
         w = cnt.value
         stats = dict(zip(("written_back", "newborn_inserted", "newborn_rejected", "pruned", "fetched"), st.tolist()))
-        return d_out[:w], oo[:w].copy(), kept[:n].astype(bool), stats
+        return d_out[:w].clone(), oo[:w].copy(), kept[:n].astype(bool), stats

@@ -95,8 +95,11 @@ struct RenderBufs {
       size_t a = 0, b = 0;
       if (w.rec) cudaFree(w.rec), w.rec = nullptr;
       if (w.dkey) cudaFree(w.dkey), w.dkey = nullptr;
+      if (w.big) cudaFree(w.big), w.big = nullptr;
+      size_t c = 0;
       if ((e = dgrow(w.rec, a, n1))) return e;
       if ((e = dgrow(w.dkey, b, n1))) return e;
+      if ((e = dgrow(w.big, c, n1))) return e;
       c_rec = n1;
     }
     size_t c1 = c_tiles, c2 = c_tiles, c3 = c_tiles, c4 = c_tiles, c5 = c_tiles;
@@ -127,7 +130,7 @@ struct RenderBufs {
       if ((e = dgrow(w.px_T, b, px))) return e;
       c_px = px;
     }
-    if ((e = dgrow(w.counters, c_cnt, 4))) return e;
+    if ((e = dgrow(w.counters, c_cnt, 8))) return e;
     if (n1 * 8 > c_geo || !geo_acc) {
       if ((e = dgrow(geo_acc, c_geo, n1 * 8))) return e;
       if ((e = cudaMemset(geo_acc, 0, sizeof(float) * n1 * 8))) return e;
@@ -137,7 +140,7 @@ struct RenderBufs {
   }
   void release() {
     for (void* p : {(void*)w.rec, (void*)w.tile_count, (void*)w.tile_offset, (void*)w.tile_cursor, (void*)w.keys,
-                    (void*)w.keys_tmp, (void*)w.dkey, (void*)w.px_last, (void*)w.px_T, (void*)w.counters,
+                    (void*)w.keys_tmp, (void*)w.dkey, (void*)w.px_last, (void*)w.px_T, (void*)w.counters, (void*)w.big,
                     (void*)w.tile_max_last, (void*)w.tile_order, (void*)geo_acc})
       if (p) cudaFree(p);
     w = RenderWork{};
@@ -240,6 +243,13 @@ latmap_status latmap_ctx_create(int32_t device, void* stream, latmap_ctx** out) 
   if (device < 0 || device >= count) return LATMAP_ERR_INVALID_ARGUMENT;
   e = cudaSetDevice(device);
   if (e != cudaSuccess) return set_cuda_error(e, "cudaSetDevice", __FILE__, __LINE__);
+  // stream-ordered allocations (store sync, k-means, row import scratch) stay cached in the
+  // device's default pool instead of returning to the driver at every synchronisation
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
   latmap_ctx* c = new latmap_ctx();
   c->device = device;
   c->stream = (cudaStream_t)stream;
@@ -605,6 +615,9 @@ struct latmap_session {
   latmap_intrinsics intr{};
   int64_t total = 0, off[9] = {}, len[8] = {};  // block offsets (16-byte aligned) and true lengths
   float *params = nullptr, *grads = nullptr, *m = nullptr, *v = nullptr, *anchor = nullptr;
+  // import_rows builds the next map into a spare set and swaps (no per-frame malloc / free)
+  float *sp_params = nullptr, *sp_grads = nullptr, *sp_m = nullptr, *sp_v = nullptr;
+  int64_t cur_cap = 0, sp_cap = 0;  // floats per buffer of the current / spare set
   int64_t *steps = nullptr, *skipped = nullptr, *overflow = nullptr;
   int32_t* flags = nullptr;
   float *corr1 = nullptr, *corr2 = nullptr;
@@ -1068,6 +1081,7 @@ latmap_status latmap_session_create(latmap_ctx* ctx, const latmap_config* cfg, i
     return LATMAP_ERR_OUT_OF_MEMORY;
   }
   s->dict_w.assign((size_t)k, 0.f);
+  s->cur_cap = std::max<int64_t>(s->total, 1);
   cudaMemset(s->m, 0, sizeof(float) * s->total);
   cudaMemset(s->v, 0, sizeof(float) * s->total);
   cudaMemset(s->grads, 0, sizeof(float) * s->total);
@@ -1090,6 +1104,8 @@ latmap_status latmap_session_destroy(latmap_session* s) {
   if (s->ctx->copy_stream) cudaStreamSynchronize(s->ctx->copy_stream);
   for (cudaEvent_t e : s->up_ev) cudaEventDestroy(e);
   if (s->ev_ready) cudaEventDestroy(s->ev_ready);
+  for (void* p : {(void*)s->sp_params, (void*)s->sp_grads, (void*)s->sp_m, (void*)s->sp_v})
+    if (p) cudaFree(p);
   for (void* p : {(void*)s->params, (void*)s->grads, (void*)s->m, (void*)s->v, (void*)s->anchor, (void*)s->steps,
                   (void*)s->skipped, (void*)s->overflow, (void*)s->flags, (void*)s->corr1, (void*)s->corr2,
                   (void*)s->d_color, (void*)s->d_depth, (void*)s->d_query, (void*)s->ssim_scratch, (void*)s->partials,
@@ -1517,13 +1533,21 @@ latmap_status latmap_session_import_rows(latmap_session* s, const float* d_rows,
   off[0] = 0;
   for (int i = 0; i < 8; ++i) off[i + 1] = pad4(off[i] + sizes[i]);
   const int64_t total = off[8];
-  float *np = nullptr, *ng = nullptr, *nm = nullptr, *nv = nullptr;
+  if (s->sp_cap < total) {  // grow the spare set with headroom (the active set drifts frame to frame)
+    for (float* p : {s->sp_params, s->sp_grads, s->sp_m, s->sp_v})
+      if (p) cudaFree(p);
+    s->sp_params = s->sp_grads = s->sp_m = s->sp_v = nullptr;
+    s->sp_cap = 0;
+    const int64_t cap = std::max<int64_t>(total + total / 4, 1);
+    CTX_CHECK(ctx, cudaMalloc(&s->sp_params, sizeof(float) * cap));
+    CTX_CHECK(ctx, cudaMalloc(&s->sp_grads, sizeof(float) * cap));
+    CTX_CHECK(ctx, cudaMalloc(&s->sp_m, sizeof(float) * cap));
+    CTX_CHECK(ctx, cudaMalloc(&s->sp_v, sizeof(float) * cap));
+    s->sp_cap = cap;
+  }
+  float *np = s->sp_params, *ng = s->sp_grads, *nm = s->sp_m, *nv = s->sp_v;
   int64_t* d_idx = nullptr;
-  CTX_CHECK(ctx, cudaMalloc(&np, sizeof(float) * std::max<int64_t>(total, 1)));
-  CTX_CHECK(ctx, cudaMalloc(&ng, sizeof(float) * std::max<int64_t>(total, 1)));
-  CTX_CHECK(ctx, cudaMalloc(&nm, sizeof(float) * std::max<int64_t>(total, 1)));
-  CTX_CHECK(ctx, cudaMalloc(&nv, sizeof(float) * std::max<int64_t>(total, 1)));
-  CTX_CHECK(ctx, cudaMalloc(&d_idx, sizeof(int64_t) * std::max<size_t>(idx.size(), 1)));
+  CTX_CHECK(ctx, cudaMallocAsync(&d_idx, sizeof(int64_t) * std::max<size_t>(idx.size(), 1), st));
   if (!idx.empty())
     CTX_CHECK(ctx, cudaMemcpyAsync(d_idx, idx.data(), sizeof(int64_t) * idx.size(), cudaMemcpyHostToDevice, st));
   MapOff so, d_o;
@@ -1540,14 +1564,19 @@ latmap_status latmap_session_import_rows(latmap_session* s, const float* d_rows,
   CTX_CHECK(ctx, cudaMemcpyAsync(nm + off[6], s->m + s->off[6], sizeof(float) * dict, cudaMemcpyDeviceToDevice, st));
   CTX_CHECK(ctx, cudaMemcpyAsync(nv + off[6], s->v + s->off[6], sizeof(float) * dict, cudaMemcpyDeviceToDevice, st));
   CTX_CHECK(ctx, cudaMemsetAsync(ng, 0, sizeof(float) * std::max<int64_t>(total, 1), st));
-  CTX_CHECK(ctx, cudaStreamSynchronize(st));
-  cudaFree(s->params), cudaFree(s->grads), cudaFree(s->m), cudaFree(s->v), cudaFree(d_idx);
-  s->params = np, s->grads = ng, s->m = nm, s->v = nv;
+  CTX_CHECK(ctx, cudaFreeAsync(d_idx, st));
+  // swap: the old set (stream-ordered behind the copies above) becomes the next spare
+  std::swap(s->params, s->sp_params), std::swap(s->grads, s->sp_grads), std::swap(s->m, s->sp_m),
+      std::swap(s->v, s->sp_v), std::swap(s->cur_cap, s->sp_cap);
   s->n = n_new;
   for (int i = 0; i < 9; ++i) s->off[i] = off[i];
   for (int i = 0; i < 8; ++i) s->len[i] = sizes[i];
   s->total = total;
-  for (auto& r : s->rw) r.release();  // re-sized for the new N on the next objective
+  // per-Gaussian render buffers grow to the new N; tile-pair capacity is kept (an overflow
+  // re-runs the step with larger lists), so no sizing pass is needed per frame. geo_acc stays
+  // all-zero between backward passes (project_bwd re-zeroes what it reads).
+  for (auto& r : s->rw)
+    if (r.w.pair_cap > 1) CTX_CHECK(ctx, r.ensure(n_new, s->intr.width, s->intr.height, r.w.pair_cap));
   s->renders_valid = false;
   s->drop_graph();
   return LATMAP_OK;

@@ -32,7 +32,8 @@ struct RenderWork {
   uint32_t* dkey = nullptr;         // n_cap: float bits of camera z (0xffffffff = culled)
   int32_t* px_last = nullptr;       // H*W: tile-list entries consumed by the pixel
   float* px_T = nullptr;            // H*W: transmittance after the last blended splat
-  int64_t* counters = nullptr;      // [0] pairs, [1] visible, [2] overflow, [3] big tiles
+  int64_t* counters = nullptr;      // [0] pairs, [1] visible, [2] overflow, [3] big tiles, [4] big footprints
+  int32_t* big = nullptr;           // n_cap: Gaussians whose footprint K3 defers to K3c
   int32_t* tile_max_last = nullptr; // ntiles: max px_last over the tile
   int32_t* tile_order = nullptr;    // ntiles: blend dispatch order (longest lists first)
   int64_t* step_overflow = nullptr;  // optional session-level overflow flag

@@ -228,24 +228,19 @@ __global__ void __launch_bounds__(1024) scan_tiles_kernel(const int32_t* __restr
 // with a single global atomic, then fills it (slot order inside a bucket is irrelevant: the
 // per-tile sort below makes the list canonical). 2048 Gaussians per block keep the number of
 // global reservations (blocks x touched tiles) low; culled Gaussians are skipped via the
-// projection's depth keys without touching their records. Footprints of up to kBigFootprint
-// tiles are walked by their own thread; larger ones (Gaussians close to the camera: hundreds to
-// thousands of tiles) are queued and walked by whole warps, a lane per tile, so one near splat
-// does not serialise its block.
+// projection's depth keys without touching their records. Footprints above kBigFootprint tiles
+// (Gaussians close to the camera: hundreds to thousands of tiles, config 3) are not walked
+// here: they are appended to a global list that K3c spreads over every warp of the GPU.
 constexpr int kScatterPerThread = 4;
 constexpr int kScatterThreads = 512;
 constexpr int kBigFootprint = 24;  // tiles
 __global__ void __launch_bounds__(kScatterThreads, 2) scatter_kernel(const SplatRec* __restrict__ rec,
                                                       const uint32_t* __restrict__ dkey, int64_t n, int tiles_x,
                                                       int ntiles, int32_t* cursor, uint64_t* __restrict__ keys,
-                                                      int64_t pair_cap) {
+                                                      int64_t pair_cap, int32_t* __restrict__ big, int64_t* counters) {
   extern __shared__ int32_t s_cnt[];
   int32_t* s_base = s_cnt + ntiles;
-  __shared__ int32_t s_big[kScatterThreads * kScatterPerThread];
-  __shared__ int32_t s_nbig;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s_cnt[t] = 0;
-  if (threadIdx.x == 0) s_nbig = 0;
   __syncthreads();
   const int64_t b0 = (int64_t)blockIdx.x * blockDim.x * kScatterPerThread;
   uint32_t dk[kScatterPerThread];
@@ -259,26 +254,18 @@ __global__ void __launch_bounds__(kScatterThreads, 2) scatter_kernel(const Splat
 #pragma unroll
   for (int r = 0; r < kScatterPerThread; ++r)
     if (dk[r] != kCulledKey) bb[r] = reinterpret_cast<const int4*>(rec + b0 + (int64_t)r * blockDim.x + threadIdx.x)[2];
-  bool big[kScatterPerThread];
 #pragma unroll
   for (int r = 0; r < kScatterPerThread; ++r) {
-    big[r] = false;
     if (dk[r] == kCulledKey) continue;
     const int tx0 = bb[r].x / kTile, tx1 = bb[r].y / kTile, ty0 = bb[r].z / kTile, ty1 = bb[r].w / kTile;
     if ((tx1 - tx0 + 1) * (ty1 - ty0 + 1) > kBigFootprint) {
-      big[r] = true;
-      s_big[atomicAdd(&s_nbig, 1)] = r * blockDim.x + threadIdx.x;
+      big[atomicAdd(reinterpret_cast<unsigned long long*>(counters + 4), 1ull)] =
+          (int32_t)(b0 + (int64_t)r * blockDim.x + threadIdx.x);
+      dk[r] = kCulledKey;  // emitted by K3c
       continue;
     }
     for (int ty = ty0; ty <= ty1; ++ty)
       for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(&s_cnt[ty * tiles_x + tx], 1);
-  }
-  __syncthreads();
-  const int nbig = s_nbig;
-  for (int e = warp; e < nbig; e += nwarps) {
-    const int4 q = reinterpret_cast<const int4*>(rec + b0 + s_big[e])[2];
-    const int tx0 = q.x / kTile, ty0 = q.z / kTile, w = q.y / kTile - tx0 + 1, nt = w * (q.w / kTile - ty0 + 1);
-    for (int t = lane; t < nt; t += 32) atomicAdd(&s_cnt[(ty0 + t / w) * tiles_x + tx0 + t % w], 1);
   }
   __syncthreads();
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
@@ -289,7 +276,7 @@ __global__ void __launch_bounds__(kScatterThreads, 2) scatter_kernel(const Splat
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < kScatterPerThread; ++r) {
-    if (dk[r] == kCulledKey || big[r]) continue;
+    if (dk[r] == kCulledKey) continue;
     const uint64_t key = ((uint64_t)dk[r] << 32) | (uint32_t)(b0 + (int64_t)r * blockDim.x + threadIdx.x);
     for (int ty = bb[r].z / kTile; ty <= bb[r].w / kTile; ++ty)
       for (int tx = bb[r].x / kTile; tx <= bb[r].y / kTile; ++tx) {
@@ -298,14 +285,27 @@ __global__ void __launch_bounds__(kScatterThreads, 2) scatter_kernel(const Splat
         if (pos < pair_cap) keys[pos] = key;
       }
   }
-  for (int e = warp; e < nbig; e += nwarps) {
-    const int64_t src = b0 + s_big[e];
+}
+
+// K3c: the large footprints K3 deferred, one warp per Gaussian (grid-stride over the global
+// list), a lane per tile; each pair takes its slot with one global atomic on the tile cursor
+// (slot order is again irrelevant).
+__global__ void __launch_bounds__(256) scatter_big_kernel(const SplatRec* __restrict__ rec,
+                                                          const uint32_t* __restrict__ dkey,
+                                                          const int32_t* __restrict__ big, const int64_t* counters,
+                                                          int tiles_x, int32_t* cursor, uint64_t* __restrict__ keys,
+                                                          int64_t pair_cap) {
+  const int64_t nbig = counters[4];
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t e = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); e < nbig; e += nw) {
+    const int32_t src = big[e];
     const int4 q = reinterpret_cast<const int4*>(rec + src)[2];
     const uint64_t key = ((uint64_t)dkey[src] << 32) | (uint32_t)src;
     const int tx0 = q.x / kTile, ty0 = q.z / kTile, w = q.y / kTile - tx0 + 1, nt = w * (q.w / kTile - ty0 + 1);
     for (int t = lane; t < nt; t += 32) {
       const int tile = (ty0 + t / w) * tiles_x + tx0 + t % w;
-      const int64_t pos = (int64_t)s_base[tile] + atomicAdd(&s_cnt[tile], 1);
+      const int64_t pos = atomicAdd(&cursor[tile], 1);
       if (pos < pair_cap) keys[pos] = key;
     }
   }
@@ -1550,7 +1550,7 @@ void render_forward(cudaStream_t st, const MapPtrs& map, const float rot_cw[9], 
   const int ntiles = w.tiles_x * w.tiles_y;
   const size_t npx = (size_t)intr.width * intr.height;
   cudaMemsetAsync(w.tile_count, 0, sizeof(int32_t) * ntiles, st);
-  cudaMemsetAsync(w.counters, 0, sizeof(int64_t) * 4, st);
+  cudaMemsetAsync(w.counters, 0, sizeof(int64_t) * 8, st);
   if (zero_outputs) {
     cudaMemsetAsync(color, 0, sizeof(float) * npx * 3, st);
     cudaMemsetAsync(depth, 0, sizeof(float) * npx, st);
@@ -1577,8 +1577,10 @@ void render_forward(cudaStream_t st, const MapPtrs& map, const float rot_cw[9], 
     const unsigned sc_grid =
         (unsigned)((map.n + kScatterThreads * kScatterPerThread - 1) / (kScatterThreads * kScatterPerThread));
     scatter_kernel<<<sc_grid, kScatterThreads, sc_smem, st>>>(w.rec, w.dkey, map.n, w.tiles_x, ntiles, w.tile_cursor, w.keys,
-                                                 w.pair_cap);
-    count_launch();
+                                                 w.pair_cap, w.big, w.counters);
+    scatter_big_kernel<<<148 * 4, 256, 0, st>>>(w.rec, w.dkey, w.big, w.counters, w.tiles_x, w.tile_cursor, w.keys,
+                                                w.pair_cap);
+    count_launch(2);
   }
   static bool attr_set = false;
   if (!attr_set) {

