@@ -643,6 +643,11 @@ struct latmap_session {
   // the uploads of later frames overlap.
   std::vector<cudaEvent_t> up_ev;
   cudaEvent_t ev_ready = nullptr;
+  // renders of every frame run ahead on rstream (they only read the map); frame b's losses,
+  // decoder and backward on the context stream wait on rend_ev[b]
+  cudaStream_t rstream = nullptr;
+  cudaEvent_t rend_start = nullptr;
+  std::vector<cudaEvent_t> rend_ev;
   std::vector<float> dict_w;  // DictionaryState::weights (host; k-means maintenance only)
   int64_t graph_launches = 0;
   bool graph_exact = false;
@@ -863,13 +868,39 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
   decoder_prepare(st, s->dec, atoms, proj);
   if (s->cfg.decoder_precision == 1 && (ctx->decoder_path == 2 || !decoder_tc_supported(s->k, s->ds, s->dec.nset_cap)))
     decoder_dl_prepare(st, s->dec);  // M in the staged path's operand blocks
+  const bool cached_all = use_cache && s->renders_valid;
+  // side-stream renders: off while phases are profiled (per-phase events need one stream)
+  const bool ahead = !cached_all && !s->prof && nf > 1;
+  if (ahead) {
+    if (!s->rstream) CTX_CHECK(ctx, cudaStreamCreateWithFlags(&s->rstream, cudaStreamNonBlocking));
+    if (!s->rend_start) CTX_CHECK(ctx, cudaEventCreateWithFlags(&s->rend_start, cudaEventDisableTiming));
+    while ((int)s->rend_ev.size() < nf) {
+      cudaEvent_t e;
+      CTX_CHECK(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      s->rend_ev.push_back(e);
+    }
+    // after the memsets / previous step's update above; joined back frame by frame below
+    CTX_CHECK(ctx, cudaEventRecord(s->rend_start, st));
+    CTX_CHECK(ctx, cudaStreamWaitEvent(s->rstream, s->rend_start, 0));
+    for (int b = 0; b < nf; ++b) {
+      FrameDev& f = s->frames[b];
+      RenderBufs& rb = s->rw[b];
+      rb.w.step_overflow = s->overflow;
+      render_forward(s->rstream, map, f.rcw, f.pose.translation, in, rb.w, s->color[b], s->depth[b], s->query[b],
+                     s->alpha[b], false, false, false);
+      render_blend(s->rstream, map, in, rb.w, s->color[b], s->depth[b], s->query[b], s->alpha[b], ctx->exact_blend);
+      CTX_CHECK(ctx, cudaEventRecord(s->rend_ev[b], s->rstream));
+    }
+  }
   for (int b = 0; b < nf; ++b) {
     FrameDev& f = s->frames[b];
     RenderBufs& rb = s->rw[b];
     rb.w.step_overflow = s->overflow;
     double* part = s->partials + (size_t)(s->slot_offset + b) * kPart;
     const bool cached = use_cache && s->renders_valid;
-    if (!cached) {
+    if (ahead) {
+      CTX_CHECK(ctx, cudaStreamWaitEvent(st, s->rend_ev[b], 0));
+    } else if (!cached) {
       s->begin(0);
       render_forward(st, map, f.rcw, f.pose.translation, in, rb.w, s->color[b], s->depth[b], s->query[b],
                      s->alpha[b], false, false, false);
@@ -1101,6 +1132,9 @@ latmap_status latmap_session_destroy(latmap_session* s) {
   cudaStreamSynchronize(s->ctx->stream);
   s->drop_graph();
   if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
+  if (s->rstream) cudaStreamSynchronize(s->rstream), cudaStreamDestroy(s->rstream);
+  if (s->rend_start) cudaEventDestroy(s->rend_start);
+  for (cudaEvent_t e : s->rend_ev) cudaEventDestroy(e);
   if (s->ctx->copy_stream) cudaStreamSynchronize(s->ctx->copy_stream);
   for (cudaEvent_t e : s->up_ev) cudaEventDestroy(e);
   if (s->ev_ready) cudaEventDestroy(s->ev_ready);
