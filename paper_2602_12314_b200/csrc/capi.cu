@@ -648,6 +648,12 @@ struct latmap_session {
   cudaStream_t rstream = nullptr;
   cudaEvent_t rend_start = nullptr;
   std::vector<cudaEvent_t> rend_ev;
+  // frame b's render backward runs on bstream behind its losses + decoder (evD[b]) while frame
+  // b+1's losses + decoder proceed on the context stream; the upstream-gradient images
+  // alternate between two slots (slot 1 below), reused once frame b-2's backward is done (evB)
+  cudaStream_t bstream = nullptr;
+  std::vector<cudaEvent_t> evD, evB;
+  float *d_color2 = nullptr, *d_depth2 = nullptr, *d_query2 = nullptr;
   std::vector<float> dict_w;  // DictionaryState::weights (host; k-means maintenance only)
   int64_t graph_launches = 0;
   bool graph_exact = false;
@@ -892,12 +898,33 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
       CTX_CHECK(ctx, cudaEventRecord(s->rend_ev[b], s->rstream));
     }
   }
+  const bool pipe = ahead && want_grad && map_grads;
+  if (pipe) {
+    if (!s->bstream) CTX_CHECK(ctx, cudaStreamCreateWithFlags(&s->bstream, cudaStreamNonBlocking));
+    while ((int)s->evD.size() < nf) {
+      cudaEvent_t e1, e2;
+      CTX_CHECK(ctx, cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+      CTX_CHECK(ctx, cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+      s->evD.push_back(e1);
+      s->evB.push_back(e2);
+    }
+    if (!s->d_color2) {
+      CTX_CHECK(ctx, cudaMalloc(&s->d_color2, sizeof(float) * npx * 3));
+      CTX_CHECK(ctx, cudaMalloc(&s->d_depth2, sizeof(float) * npx));
+      CTX_CHECK(ctx, cudaMalloc(&s->d_query2, sizeof(float) * npx * s->ds));
+    }
+  }
   for (int b = 0; b < nf; ++b) {
     FrameDev& f = s->frames[b];
     RenderBufs& rb = s->rw[b];
     rb.w.step_overflow = s->overflow;
     double* part = s->partials + (size_t)(s->slot_offset + b) * kPart;
     const bool cached = use_cache && s->renders_valid;
+    const bool slot1 = pipe && (b & 1);
+    float* d_col = slot1 ? s->d_color2 : s->d_color;
+    float* d_dep = slot1 ? s->d_depth2 : s->d_depth;
+    float* d_qry = slot1 ? s->d_query2 : s->d_query;
+    if (pipe && b >= 2) CTX_CHECK(ctx, cudaStreamWaitEvent(st, s->evB[b - 2], 0));  // slot free again
     if (ahead) {
       CTX_CHECK(ctx, cudaStreamWaitEvent(st, s->rend_ev[b], 0));
     } else if (!cached) {
@@ -913,7 +940,7 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
     s->begin(2);
     wait_frame(s, b, st);
     image_losses(st, s->color[b], s->depth[b], s->alpha[b], f.rgb, f.depth, h, w, c.lambda_i1, c.lambda_i2,
-                 c.lambda_rgb * inv_b, c.lambda_depth * inv_b, map_grad, s->d_color, s->d_depth, part,
+                 c.lambda_rgb * inv_b, c.lambda_depth * inv_b, map_grad, d_col, d_dep, part,
                  s->ssim_scratch);
     s->end();
     if (c.segment_mode)
@@ -935,7 +962,7 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
                     c.softmax_temp, c.lambda_cos, c.lambda_l2, c.lambda_feat * inv_b, want_grad, s->seg_dq, g_proj,
                     g_atoms, part);
       if (want_grad) {
-        seg_scatter_kernel<<<gq, 256, 0, st>>>(s->seg_dq, f.assign, npx, s->ds, f.seg_of, f.seg_inv, s->d_query);
+        seg_scatter_kernel<<<gq, 256, 0, st>>>(s->seg_dq, f.assign, npx, s->ds, f.seg_of, f.seg_inv, d_qry);
         count_launch();
       }
       s->end();
@@ -945,27 +972,35 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
       const bool staged_ok = s->dec.dl_mt && decoder_dl_supported(s->k, s->ds, f.n_set) && ctx->decoder_path != 1;
       if (c.decoder_precision == 1 && fused_ok)
         decoder_frame_tc(st, s->dec, s->query[b], f.assign, npx, f.feats, f.n_set, f.stat, atoms, proj,
-                         c.softmax_temp, c.lambda_cos, c.lambda_l2, c.lambda_feat * inv_b, want_grad, s->d_query,
+                         c.softmax_temp, c.lambda_cos, c.lambda_l2, c.lambda_feat * inv_b, want_grad, d_qry,
                          g_proj, g_atoms, part);
       else if (c.decoder_precision == 1 && staged_ok)
         decoder_frame_dl(st, s->dec, s->query[b], f.assign, npx, f.feats, f.n_set, f.stat, atoms, c.softmax_temp,
-                         c.lambda_cos, c.lambda_l2, c.lambda_feat * inv_b, want_grad, s->d_query, g_atoms, part);
+                         c.lambda_cos, c.lambda_l2, c.lambda_feat * inv_b, want_grad, d_qry, g_atoms, part);
       else
         decoder_frame(st, s->dec, s->query[b], f.assign, npx, f.feats, f.n_set, f.stat, atoms, proj, c.softmax_temp,
-                      c.lambda_cos, c.lambda_l2, c.lambda_feat * inv_b, want_grad, s->d_query, g_proj, g_atoms, part);
+                      c.lambda_cos, c.lambda_l2, c.lambda_feat * inv_b, want_grad, d_qry, g_proj, g_atoms, part);
       s->end();
     }
     if (map_grad) {
       // geo_acc is zero here: zeroed at allocation, and project_bwd re-zeroes every entry it reads
+      cudaStream_t bs = st;
+      if (pipe) {
+        CTX_CHECK(ctx, cudaEventRecord(s->evD[b], st));
+        CTX_CHECK(ctx, cudaStreamWaitEvent(s->bstream, s->evD[b], 0));
+        bs = s->bstream;
+      }
       s->begin(4);
-      render_backward(st, map, f.rcw, f.rwc, f.pose.translation, in, rb.w, s->d_color, s->d_depth,
-                      have_sup ? s->d_query : nullptr, rb.geo_acc, gmap, false);
+      render_backward(bs, map, f.rcw, f.rwc, f.pose.translation, in, rb.w, d_col, d_dep, have_sup ? d_qry : nullptr,
+                      rb.geo_acc, gmap, false);
       s->end();
       s->begin(5);
-      render_project_backward(st, map, f.rcw, f.rwc, f.pose.translation, in, rb.w, rb.geo_acc, gmap);
+      render_project_backward(bs, map, f.rcw, f.rwc, f.pose.translation, in, rb.w, rb.geo_acc, gmap);
       s->end();
+      if (pipe) CTX_CHECK(ctx, cudaEventRecord(s->evB[b], s->bstream));
     }
   }
+  if (pipe) CTX_CHECK(ctx, cudaStreamWaitEvent(st, s->evB[nf - 1], 0));  // join: every backward done
   s->renders_valid = true;
   if (want_grad) decoder_finish_tc(st, s->dec, atoms, proj, g_proj, g_atoms);
   // trust term enters once (objective.cpp:247-256)
@@ -1135,6 +1170,11 @@ latmap_status latmap_session_destroy(latmap_session* s) {
   if (s->rstream) cudaStreamSynchronize(s->rstream), cudaStreamDestroy(s->rstream);
   if (s->rend_start) cudaEventDestroy(s->rend_start);
   for (cudaEvent_t e : s->rend_ev) cudaEventDestroy(e);
+  if (s->bstream) cudaStreamSynchronize(s->bstream), cudaStreamDestroy(s->bstream);
+  for (cudaEvent_t e : s->evD) cudaEventDestroy(e);
+  for (cudaEvent_t e : s->evB) cudaEventDestroy(e);
+  for (float* p : {s->d_color2, s->d_depth2, s->d_query2})
+    if (p) cudaFree(p);
   if (s->ctx->copy_stream) cudaStreamSynchronize(s->ctx->copy_stream);
   for (cudaEvent_t e : s->up_ev) cudaEventDestroy(e);
   if (s->ev_ready) cudaEventDestroy(s->ev_ready);
