@@ -224,14 +224,14 @@ cudaError_t kmeans_weighted(cudaStream_t st, const float* P, const float* W, int
   *iterations = 0;
   if (n == 0) return cudaStreamSynchronize(st);
   KmBufs b(st);
-  cudaMallocAsync(&b.w, sizeof(float) * n, st);
-  cudaMallocAsync(&b.c2, sizeof(float) * k, st);
-  cudaMallocAsync(&b.S, sizeof(float) * n * k, st);
-  cudaMallocAsync(&b.mind2, sizeof(float) * n, st);
-  cudaMallocAsync(&b.mass, sizeof(float) * k, st);
-  cudaMallocAsync(&b.asg, sizeof(int32_t) * n, st);
-  cudaMallocAsync(&b.order, sizeof(int32_t) * n, st);
-  cudaMallocAsync(&b.seg, sizeof(int32_t) * (k + 1), st);
+  for (cudaError_t e : {cudaMallocAsync(&b.w, sizeof(float) * n, st), cudaMallocAsync(&b.c2, sizeof(float) * k, st),
+                        cudaMallocAsync(&b.S, sizeof(float) * n * k, st),
+                        cudaMallocAsync(&b.mind2, sizeof(float) * n, st),
+                        cudaMallocAsync(&b.mass, sizeof(float) * k, st),
+                        cudaMallocAsync(&b.asg, sizeof(int32_t) * n, st),
+                        cudaMallocAsync(&b.order, sizeof(int32_t) * n, st),
+                        cudaMallocAsync(&b.seg, sizeof(int32_t) * (k + 1), st)})
+    if (e != cudaSuccess) return e;
   cudaMemcpyAsync(b.w, W, sizeof(float) * n, cudaMemcpyHostToDevice, st);
   // warm start fills the first rows (stream_kmeans.cpp:107-111)
   int64_t filled = 0;
@@ -301,7 +301,7 @@ cudaError_t kmeans_weighted(cudaStream_t st, const float* P, const float* W, int
       }
       const int64_t nr = (int64_t)rows.size();
       int32_t* d_rows = nullptr;
-      cudaMallocAsync(&d_rows, sizeof(int32_t) * nr, st);
+      if (cudaError_t e = cudaMallocAsync(&d_rows, sizeof(int32_t) * nr, st)) return e;
       cudaMemcpyAsync(d_rows, rows.data(), sizeof(int32_t) * nr, cudaMemcpyHostToDevice, st);
       km_gather_kernel<<<blocks_for(nr * dim, 256), 256, 0, st>>>(P, d_rows, nr, dim, C + (k - nr) * dim);
       count_launch();
@@ -371,7 +371,7 @@ cudaError_t kmeans_stream_update(cudaStream_t st, const float* batch, int64_t n,
   const int64_t m = std::min(n, K);
   std::vector<float> unit((size_t)n, 1.f), lw((size_t)m);
   float *lc = nullptr, *pooled = nullptr, *warm = nullptr;
-  cudaMallocAsync(&lc, sizeof(float) * m * dim, st);
+  if (cudaError_t e0 = cudaMallocAsync(&lc, sizeof(float) * m * dim, st)) return e0;
   int iters = 0;
   cudaError_t e = kmeans_weighted(st, batch, unit.data(), n, dim, m, uni, user, nullptr, 0, 10, lc, lw.data(), &iters);
   if (e != cudaSuccess) return e;
@@ -379,8 +379,8 @@ cudaError_t kmeans_stream_update(cudaStream_t st, const float* batch, int64_t n,
   int64_t old_count = 0;
   for (int64_t j = 0; j < K; ++j)
     if (weights[j] > 0.f) ++old_count;
-  cudaMallocAsync(&pooled, sizeof(float) * (m + old_count) * dim, st);
-  cudaMallocAsync(&warm, sizeof(float) * std::max<int64_t>(old_count, 1) * dim, st);
+  if (cudaError_t e1 = cudaMallocAsync(&pooled, sizeof(float) * (m + old_count) * dim, st)) return e1;
+  if (cudaError_t e2 = cudaMallocAsync(&warm, sizeof(float) * std::max<int64_t>(old_count, 1) * dim, st)) return e2;
   std::vector<float> pw((size_t)(m + old_count));
   cudaMemcpyAsync(pooled, lc, sizeof(float) * m * dim, cudaMemcpyDeviceToDevice, st);
   for (int64_t j = 0; j < m; ++j) pw[(size_t)j] = lw[(size_t)j];
@@ -392,7 +392,7 @@ cudaError_t kmeans_stream_update(cudaStream_t st, const float* batch, int64_t n,
   }
   if (old_count > 0) {
     int32_t* d_live = nullptr;
-    cudaMallocAsync(&d_live, sizeof(int32_t) * old_count, st);
+    if (cudaError_t e3 = cudaMallocAsync(&d_live, sizeof(int32_t) * old_count, st)) return e3;
     cudaMemcpyAsync(d_live, live.data(), sizeof(int32_t) * old_count, cudaMemcpyHostToDevice, st);
     km_gather_kernel<<<blocks_for(old_count * dim, 256), 256, 0, st>>>(atoms, d_live, old_count, dim, warm);
     cudaMemcpyAsync(pooled + m * dim, warm, sizeof(float) * old_count * dim, cudaMemcpyDeviceToDevice, st);
