@@ -77,7 +77,7 @@ __device__ __forceinline__ void quat_row(float4& p, const float4& g, float4& mm,
   }
 }
 
-__global__ void __launch_bounds__(256) adam_update_kernel(float* __restrict__ param, const float* __restrict__ grad,
+__global__ void __launch_bounds__(256, 5) adam_update_kernel(float* __restrict__ param, const float* __restrict__ grad,
                                                           float* __restrict__ m, float* __restrict__ v, Blocks B,
                                                           const int64_t* steps, const float* corr1,
                                                           const float* corr2, int32_t table_len, const int32_t* flags,
@@ -187,7 +187,7 @@ void adam_flat(cudaStream_t st, float* param, const float* grad, float* m, float
     total = std::max(total, blocks[i].offset + blocks[i].count);
   }
   adam_check_kernel<<<148 * 4, 256, 0, st>>>(grad, B, total, flags);
-  adam_update_kernel<<<148 * 8, 256, 0, st>>>(param, grad, m, v, B, steps, corr1, corr2, table_len, flags,
+  adam_update_kernel<<<148 * 5, 256, 0, st>>>(param, grad, m, v, B, steps, corr1, corr2, table_len, flags,
                                                overflow);
   adam_finish_kernel<<<1, 32, 0, st>>>(B, steps, skipped, flags, overflow);
   count_launch(3);
