@@ -73,3 +73,32 @@ def test_staged_decoder_loss_only(ctx, cfg_id, scale, path):
     ln, _, _ = run(ctx, w, 1, path, want_grad=False)
     for k in ("l_cos", "l_l2", "total"):
         assert ln[k] == pytest.approx(lg[k], rel=1e-6, abs=1e-7), (k, ln[k], lg[k])
+
+
+def test_multiframe_stream_pipeline_matches_single_stream(ctx):
+    """The step's three-stream pipeline (renders ahead on one stream, frame b's backward overlapping
+    frame b+1's losses + decoder on another, two upstream-gradient slots) against the same objective
+    issued on one stream (phase profiling disables the pipeline): identical losses, gradients equal up
+    to the run-to-run rounding of the atomic sums."""
+    w = synthetic.make_workload(2, gpu_render(ctx), scale=0.25)  # 8 keyframes
+
+    def objective(pipelined):
+        cfg = api.default_config(**w.lambdas)
+        cfg.decoder_precision = 1
+        intr = api.make_intrinsics(w.intr.fx, w.intr.fy, w.intr.cx, w.intr.cy, w.intr.width, w.intr.height)
+        s = api.Session(ctx, cfg, w.map.n, w.map.features.shape[1], w.atoms.shape[0], w.atoms.shape[1], intr)
+        s.set_map(w.map)
+        s.set_dictionary(w.atoms, w.anchor, w.proj)
+        s.set_frames(w.frames)
+        s.set_batch(len(w.frames))
+        s.objective(want_grad=True)  # sizes the tile lists
+        s.profile(not pipelined)
+        loss = s.objective(want_grad=True)
+        return loss, s.grad_buffer().cpu().numpy().copy()
+
+    l1, g1 = objective(False)
+    l3, g3 = objective(True)
+    for k in ("l_rgb", "l_ssim", "l_depth", "l_cos", "l_l2", "total"):
+        assert l3[k] == pytest.approx(l1[k], rel=1e-6, abs=1e-9), (k, l3[k], l1[k])
+    rel = np.linalg.norm(g3 - g1) / np.linalg.norm(g1)
+    assert rel < 1e-5 and cosine(g3, g1) > 0.999999, rel
