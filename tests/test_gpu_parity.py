@@ -556,3 +556,28 @@ def test_assignment_out_of_range_is_reported(ctx, cfg0):
     s.set_frames(w.frames)
     loss = s.objective(want_grad=True)
     assert np.isfinite(loss["total"]) and loss["supervised_rows"] == int((w.frames[0].assignment >= 0).sum())
+
+
+def test_tile_list_overflow_is_recovered(ctx, cfg0):
+    """Tile-pair buffers are sized by the first step; a map whose splats grow far larger overflows
+    them inside the captured (multi-stream) step. The step must detect it, discard the partial
+    step (Adam skipped), grow the lists and re-run: same loss and map as a fresh session."""
+    import copy
+    w = cfg0
+    big = copy.deepcopy(w.map)
+    big.log_scales = (big.log_scales + 1.5).astype(np.float32)  # ~4.5x larger footprints
+    a = make_session(ctx, w)
+    a.step(read=True)  # sizes the buffers for the small splats
+    a.set_map(big)
+    a.set_dictionary(w.atoms, w.anchor, w.proj)  # undo the first step's dictionary update
+    la = a.objective(want_grad=True)
+    b = make_session(ctx, w)
+    b.set_map(big)
+    lb = b.objective(want_grad=True)
+    for k in ("l_rgb", "l_depth", "l_cos", "total"):
+        assert la[k] == pytest.approx(lb[k], rel=1e-5), (k, la[k], lb[k])
+    ga, gb = a.grad_buffer().cpu().numpy(), b.grad_buffer().cpu().numpy()
+    assert np.linalg.norm(ga - gb) <= 1e-4 * np.linalg.norm(gb)
+    la2 = a.step(read=True)  # and through the captured step
+    lb2 = b.step(read=True)
+    assert la2["total"] == pytest.approx(lb2["total"], rel=1e-5)
