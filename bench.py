@@ -332,7 +332,10 @@ def main():
               "image": f"{synthetic.SPECS[args.config][0]}x{synthetic.SPECS[args.config][1]}",
               "parallelism": f"keyframe-sharded x{world}" if world > 1 else "single GPU",
               "l2": "working set > L2 (126 MB) every step; no explicit flush",
-              "launch": "each Stage-I step replayed as one captured CUDA graph (N=1)"}
+              "launch": "each Stage-I step replayed as one captured CUDA graph (N=1)",
+              "streams": "renders of all keyframes ahead on a render stream; frame b's render backward on a "
+                         "backward stream overlapping frame b+1's losses + decoder; joined inside the graph",
+              "phases_note": "per-phase times are measured single-stream (phase profiling disables the overlap)"}
 
     if args.impl == "reference":
         if rank != 0:
