@@ -328,6 +328,31 @@ latmap_status latmap_session_stream_kmeans(latmap_session* s, const float* batch
 latmap_status latmap_session_get_dict_weights(const latmap_session* s, float* out);
 latmap_status latmap_session_set_dict_weights(latmap_session* s, const float* w);
 
+/* ---------------------------------------------------------------- evaluation (device rows in) */
+/* gather_supervision, pixel mode (objective.cpp:16-35): rows of the pixels with assignment >= 0
+ * in ascending pixel order -> q_out (n x ds), t_out (n x df; each row normalised when `normalize`,
+ * as evaluate_map does, evaluate.cpp:38-42), pixel_of_row (n). Pass q_out = NULL to count only;
+ * *n_rows is always set; LATMAP_ERR_INVALID_ARGUMENT if n > cap. */
+latmap_status latmap_gather_supervision(latmap_ctx* ctx, const float* query, int32_t ds, const int32_t* assignment,
+                                        int64_t npx, const float* features, int32_t df, int32_t normalize,
+                                        float* q_out, float* t_out, int64_t* pixel_of_row, int64_t cap,
+                                        int64_t* n_rows);
+/* metric_cos (metrics.hpp:12-13) over n rows of width d; flagged as in the reference. */
+latmap_status latmap_metric_cos(latmap_ctx* ctx, const float* reconstructed, const float* target, int64_t n,
+                                int32_t d, double* value, int32_t* flagged);
+/* metric_miou (metrics.hpp:15-26): intersection / union per class (host, c entries each). */
+latmap_status latmap_metric_miou(latmap_ctx* ctx, const float* embeddings, const int32_t* labels, int64_t n,
+                                 int32_t d, const float* prototypes, int32_t c, int64_t* intersection,
+                                 int64_t* union_, double* miou);
+/* metric_psnr (metrics.hpp:28-33) over n values. */
+latmap_status latmap_metric_psnr(latmap_ctx* ctx, const float* rendered, const float* observed, int64_t n,
+                                 double* db, int32_t* exact);
+/* query_map (evaluate.hpp:37-40): cosine of every Gaussian's reconstructed embedding with one
+ * embedding (device, df) -> scores (device, n). */
+latmap_status latmap_query_map(latmap_ctx* ctx, const float* features, int64_t n, int32_t ds, const float* atoms,
+                               const float* proj, int64_t k, int32_t df, float temperature, const float* embedding,
+                               float* scores);
+
 /* ---------------------------------------------------------------- self-test */
 /* One-tile tcgen05 GEMM, C[128 x n] = A[128 x k] * B[n x k]^T (device fp32 in/out, bf16 staging),
  * with A / B staged K-major (0) or MN-major (1); pins the UMMA descriptor conventions. */

@@ -171,6 +171,15 @@ def _declare(L):
     L.lm_mt64_next.restype = C.c_uint64
     L.lm_mt64_uniform01.argtypes = [C.c_void_p]
     L.lm_mt64_uniform01.restype = C.c_double
+    PF, PI = C.POINTER(C.c_float), C.POINTER(C.c_int32)
+    L.lm_metric_cos.argtypes = [PF, PF, C.c_int64, C.c_int64, PI]
+    L.lm_metric_cos.restype = C.c_double
+    L.lm_metric_miou.argtypes = [PF, PI, C.c_int64, C.c_int64, PF, C.c_int64, C.POINTER(C.c_int64),
+                                 C.POINTER(C.c_int64)]
+    L.lm_metric_miou.restype = C.c_double
+    L.lm_metric_psnr.argtypes = [PF, PF, C.c_int64, PI]
+    L.lm_metric_psnr.restype = C.c_double
+    L.lm_query_scores.argtypes = [PF, C.c_int64, C.c_int64, PF, PF]
     L.lm_store_record_key.restype = VoxelKey
     L.lm_store_stats.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
     L.lm_insert_global.argtypes = [C.c_void_p, C.POINTER(C.c_float), C.c_int64, C.c_float]
@@ -684,3 +693,50 @@ def stream_kmeans_update(batch, atoms, anchor, weights, rng: MT64, decay=1.0):
     getattr(lib(), "lm_stream_kmeans_update" + _SUF[dt])(
         _p(b), n, atoms.shape[1], _p(atoms), _p(anchor), _p(weights), atoms.shape[0], MT64.uniform01_fn(),
         C.cast(C.byref(rng), C.c_void_p), _CT[dt](decay))
+
+
+# --------------------------------------------------------------------------- evaluation metrics
+def metric_cos(rec, tgt):
+    """metric_cos (metrics.cpp:8-24) -> (value, flagged)."""
+    r = np.ascontiguousarray(rec, np.float32)
+    t = np.ascontiguousarray(tgt, np.float32)
+    if r.shape != t.shape:
+        raise ValueError("metric_cos: shape mismatch")
+    fl = C.c_int32(0)
+    v = lib().lm_metric_cos(_p(r), _p(t), r.shape[0], r.shape[1] if r.ndim > 1 else 0, C.byref(fl))
+    return float(v), bool(fl.value)
+
+
+def metric_miou(emb, labels, protos):
+    """metric_miou (metrics.cpp:26-73) -> (miou, intersection, union)."""
+    e = np.ascontiguousarray(emb, np.float32)
+    lab = np.ascontiguousarray(labels, np.int32)
+    p = np.ascontiguousarray(protos, np.float32)
+    c = p.shape[0]
+    inter = np.zeros(c, np.int64)
+    uni = np.zeros(c, np.int64)
+    v = lib().lm_metric_miou(_p(e), lab.ctypes.data_as(C.POINTER(C.c_int32)), e.shape[0], e.shape[1], _p(p), c,
+                             inter.ctypes.data_as(C.POINTER(C.c_int64)), uni.ctypes.data_as(C.POINTER(C.c_int64)))
+    if v < 0:
+        raise ValueError("metric_miou: label id out of range")
+    return float(v), inter, uni
+
+
+def metric_psnr(a, b):
+    """metric_psnr (metrics.cpp:75-89) -> (dB, exact)."""
+    x = np.ascontiguousarray(a, np.float32).reshape(-1)
+    y = np.ascontiguousarray(b, np.float32).reshape(-1)
+    if x.shape != y.shape:
+        raise ValueError("metric_psnr: shape mismatch")
+    ex = C.c_int32(0)
+    v = lib().lm_metric_psnr(_p(x), _p(y), x.shape[0], C.byref(ex))
+    return float(v), bool(ex.value)
+
+
+def query_scores(rec, embedding):
+    """query_map (evaluate.cpp:74-88) scores of reconstructed rows against one embedding."""
+    r = np.ascontiguousarray(rec, np.float32)
+    e = np.ascontiguousarray(embedding, np.float32)
+    out = np.zeros(r.shape[0], np.float32)
+    lib().lm_query_scores(_p(r), r.shape[0], r.shape[1], _p(e), _p(out))
+    return out

@@ -1392,6 +1392,105 @@ int S(lm_stream_kmeans_update)(const T* batch, int64_t n, int64_t dim, T* atoms,
 
 #else /* LM_ONCE: voxel hash store, voxel_hash.cpp / active_set.cpp */
 
+/* ------------------------------------------------------------------ evaluation metrics */
+static float lmo_dot(const float* a, const float* b, int64_t d) {
+  float s = 0.f;
+  for (int64_t i = 0; i < d; ++i) s += a[i] * b[i];
+  return s;
+}
+
+/* metric_cos, metrics.cpp:8-24: float row norms / dot (Eigen on float rows), double mean. */
+double lm_metric_cos(const float* rec, const float* tgt, int64_t n, int64_t d, int32_t* flagged) {
+  if (flagged) *flagged = 0;
+  if (n == 0) return 0.0;
+  double sum = 0.0;
+  for (int64_t r = 0; r < n; ++r) {
+    double nu = (double)sqrtf(lmo_dot(rec + r * d, rec + r * d, d));
+    double nv = (double)sqrtf(lmo_dot(tgt + r * d, tgt + r * d, d));
+    if ((nu < 1e-8 || nv < 1e-8) && flagged) *flagged = 1;
+    nu = nu > 1e-8 ? nu : 1e-8;
+    nv = nv > 1e-8 ? nv : 1e-8;
+    sum += 1.0 - (double)lmo_dot(rec + r * d, tgt + r * d, d) / (nu * nv);
+  }
+  return sum / (double)n;
+}
+
+/* metric_miou, metrics.cpp:26-73: softmax over prototype scores (float; exp correctly rounded),
+ * prediction = first maximum of the probabilities; classes absent from both are excluded. */
+double lm_metric_miou(const float* emb, const int32_t* labels, int64_t n, int64_t d, const float* protos, int64_t c,
+                      int64_t* inter, int64_t* uni) {
+  for (int64_t k = 0; k < c; ++k) inter[k] = uni[k] = 0;
+  float* sc = (float*)malloc(sizeof(float) * (size_t)(c > 0 ? c : 1));
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t gt = labels[i];
+    if (gt < 0) continue;
+    if (gt >= c) {
+      free(sc);
+      return -1.0;
+    }
+    float m = 0.f;
+    for (int64_t k = 0; k < c; ++k) {
+      sc[k] = lmo_dot(protos + k * d, emb + i * d, d);
+      if (k == 0 || sc[k] > m) m = sc[k];
+    }
+    float s = 0.f;
+    for (int64_t k = 0; k < c; ++k) {
+      sc[k] = (float)exp((double)(sc[k] - m));
+      s += sc[k];
+    }
+    int64_t pred = 0;
+    float best = 0.f;
+    for (int64_t k = 0; k < c; ++k) {
+      const float p = sc[k] / s;
+      if (k == 0 || p > best) best = p, pred = k;
+    }
+    if (pred == gt) {
+      ++inter[gt];
+      ++uni[gt];
+    } else {
+      ++uni[gt];
+      ++uni[pred];
+    }
+  }
+  free(sc);
+  double sum = 0.0;
+  int64_t inc = 0;
+  for (int64_t k = 0; k < c; ++k) {
+    if (uni[k] == 0) continue;
+    sum += (double)inter[k] / (double)uni[k];
+    ++inc;
+  }
+  return inc > 0 ? sum / (double)inc : 0.0;
+}
+
+/* metric_psnr, metrics.cpp:75-89 */
+double lm_metric_psnr(const float* a, const float* b, int64_t n, int32_t* exact) {
+  double mse = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    const double dd = (double)a[i] - (double)b[i];
+    mse += dd * dd;
+  }
+  mse /= (double)n;
+  if (mse == 0.0) {
+    if (exact) *exact = 1;
+    return 100.0;
+  }
+  if (exact) *exact = 0;
+  return 10.0 * log10(1.0 / mse);
+}
+
+/* query_map, evaluate.cpp:74-88 (scores of reconstructed rows vs one embedding) */
+void lm_query_scores(const float* rec, int64_t n, int64_t d, const float* emb, float* scores) {
+  float qn = sqrtf(lmo_dot(emb, emb, d));
+  qn = qn > 1e-8f ? qn : 1e-8f;
+  for (int64_t i = 0; i < n; ++i) {
+    float rn = sqrtf(lmo_dot(rec + i * d, rec + i * d, d));
+    rn = rn > 1e-8f ? rn : 1e-8f;
+    scores[i] = lmo_dot(rec + i * d, emb, d) / (rn * qn);
+  }
+}
+
+
 /* ------------------------------------------------------------------ std::mt19937_64 */
 /* The 64-bit Mersenne Twister with the C++ standard's parameters ([rand.predef]:
  * w=64 n=312 m=156 r=31 a=0xb5026f5aa96619e9 u=29 d=0x5555555555555555 s=17

@@ -139,6 +139,15 @@ void lm_mt64_seed(lm_mt64* r, uint64_t seed);
 uint64_t lm_mt64_next(lm_mt64* r);
 double lm_mt64_uniform01(void* r);
 
+/* ---- evaluation metrics (float, metrics.cpp:8-89, evaluate.cpp:74-88) ---- */
+double lm_metric_cos(const float* rec, const float* tgt, int64_t n, int64_t d, int32_t* flagged);
+/* intersection / union_ per class (c entries each); returns mIoU; -1 on a label >= c */
+double lm_metric_miou(const float* emb, const int32_t* labels, int64_t n, int64_t d, const float* protos,
+                      int64_t c, int64_t* inter, int64_t* uni);
+double lm_metric_psnr(const float* a, const float* b, int64_t n, int32_t* exact);
+/* query_map scores from reconstructed rows (n x d) against one embedding */
+void lm_query_scores(const float* rec, int64_t n, int64_t d, const float* embedding, float* scores);
+
 /* ---- voxel hash store (float only, voxel_hash.hpp / active_set.hpp) ---- */
 lm_voxel_key lm_voxel_of(const float p[3], float voxel_size);
 int64_t lm_hash_voxel(lm_voxel_key k, int64_t capacity);

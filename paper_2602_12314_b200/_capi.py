@@ -140,6 +140,12 @@ def _declare(L):
                                    C.POINTER(C.c_int32)],
         "latmap_session_stream_kmeans": [P, P, C.c_int64, C.c_float, P, P],
         "latmap_session_get_dict_weights": [P, P],
+        "latmap_gather_supervision": [P, P, C.c_int32, P, C.c_int64, P, C.c_int32, C.c_int32, P, P, P, C.c_int64,
+                                      C.POINTER(C.c_int64)],
+        "latmap_metric_cos": [P, P, P, C.c_int64, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int32)],
+        "latmap_metric_miou": [P, P, P, C.c_int64, C.c_int32, P, C.c_int32, P, P, C.POINTER(C.c_double)],
+        "latmap_metric_psnr": [P, P, P, C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_int32)],
+        "latmap_query_map": [P, P, C.c_int64, C.c_int32, P, P, C.c_int64, C.c_int32, C.c_float, P, P],
         "latmap_session_set_dict_weights": [P, P],
         "latmap_store_create": [P, C.c_int64, C.c_int32, C.POINTER(P)],
         "latmap_store_destroy": [P],
@@ -201,7 +207,8 @@ EXPORTED = ["latmap_ctx_create", "latmap_ctx_destroy", "latmap_ctx_set_stream", 
             "latmap_store_stats", "latmap_store_last_error", "latmap_store_insert", "latmap_store_update",
             "latmap_store_find", "latmap_store_get_records", "latmap_store_insert_global", "latmap_store_fetch_local",
             "latmap_store_sync", "latmap_weighted_kmeans", "latmap_session_stream_kmeans",
-            "latmap_session_get_dict_weights", "latmap_session_set_dict_weights"]
+            "latmap_session_get_dict_weights", "latmap_session_set_dict_weights", "latmap_gather_supervision",
+            "latmap_metric_cos", "latmap_metric_miou", "latmap_metric_psnr", "latmap_query_map"]
 
 
 def check(ctx_handle, status):

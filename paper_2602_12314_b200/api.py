@@ -29,6 +29,12 @@ def _ptr(t):
     return C.c_void_p(t.data_ptr())
 
 
+def _iptr(t, dtype=torch.int32):
+    """Device pointer of a contiguous CUDA integer tensor."""
+    assert t.is_cuda and t.dtype == dtype and t.is_contiguous(), f"expected contiguous cuda {dtype}"
+    return C.c_void_p(t.data_ptr())
+
+
 @dataclass
 class GaussianMap:
     """GaussianMapT<float> on the device (core/types.hpp:93-199)."""
@@ -260,6 +266,106 @@ def ssim(ctx, a, b, want_grad=False):
     v = C.c_float(0)
     check(ctx.h, lib().latmap_ssim(ctx.h, _ptr(a), _ptr(b), h, w, ch, _ptr(da), C.byref(v)))
     return (v.value, da) if want_grad else v.value
+
+
+# --------------------------------------------------------------------------- evaluation
+def gather_supervision(ctx, query, assignment, features, normalize=False):
+    """gather_supervision, pixel mode (objective.cpp:16-35) on the device -> (queries n x ds,
+    targets n x df, pixel_of_row n). ``normalize`` divides each target row by its norm (> 1e-12),
+    as evaluate_map does (evaluate.cpp:38-42)."""
+    q = query.reshape(-1, query.shape[-1]).contiguous()
+    asg = assignment.reshape(-1).to(torch.int32).contiguous()
+    feats = features.contiguous()
+    npx, ds = q.shape
+    df = feats.shape[1]
+    n = C.c_int64(0)
+    check(ctx.h, lib().latmap_gather_supervision(ctx.h, _ptr(q), ds, _iptr(asg), npx, _ptr(feats), df, int(normalize),
+                                                 None, None, None, 0, C.byref(n)))
+    qo = torch.empty((n.value, ds), device=q.device)
+    to = torch.empty((n.value, df), device=q.device)
+    po = torch.empty(n.value, dtype=torch.int64, device=q.device)
+    check(ctx.h, lib().latmap_gather_supervision(ctx.h, _ptr(q), ds, _iptr(asg), npx, _ptr(feats), df, int(normalize),
+                                                 _ptr(qo), _ptr(to), _iptr(po, torch.int64), n.value, C.byref(n)))
+    return qo, to, po
+
+
+def metric_cos(ctx, rec, tgt):
+    """metric_cos (io/metrics.hpp:12-13) -> (value, flagged)."""
+    if rec.shape != tgt.shape:
+        raise _capi.InvalidArgument("metric_cos: shape mismatch")
+    v, fl = C.c_double(0), C.c_int32(0)
+    check(ctx.h, lib().latmap_metric_cos(ctx.h, _ptr(rec.contiguous()), _ptr(tgt.contiguous()), rec.shape[0],
+                                         rec.shape[1], C.byref(v), C.byref(fl)))
+    return v.value, bool(fl.value)
+
+
+def metric_miou(ctx, emb, labels, prototypes):
+    """metric_miou (io/metrics.hpp:15-26) -> (miou, intersection, union) (numpy int64 per class)."""
+    lab = labels.to(torch.int32).contiguous()
+    c = prototypes.shape[0]
+    inter = np.zeros(c, np.int64)
+    uni = np.zeros(c, np.int64)
+    v = C.c_double(0)
+    check(ctx.h, lib().latmap_metric_miou(ctx.h, _ptr(emb.contiguous()), _iptr(lab), emb.shape[0], emb.shape[1],
+                                          _ptr(prototypes.contiguous()), c, inter.ctypes.data_as(C.c_void_p),
+                                          uni.ctypes.data_as(C.c_void_p), C.byref(v)))
+    return v.value, inter, uni
+
+
+def metric_psnr(ctx, rendered, observed):
+    """metric_psnr (io/metrics.hpp:28-33) -> (dB, exact)."""
+    if rendered.numel() != observed.numel():
+        raise _capi.InvalidArgument("metric_psnr: shape mismatch")
+    db, ex = C.c_double(0), C.c_int32(0)
+    check(ctx.h, lib().latmap_metric_psnr(ctx.h, _ptr(rendered.contiguous()), _ptr(observed.contiguous()),
+                                          rendered.numel(), C.byref(db), C.byref(ex)))
+    return db.value, bool(ex.value)
+
+
+def query_map(ctx, features, atoms, proj, temperature, embedding):
+    """query_map (io/evaluate.hpp:37-40): per-Gaussian cosine with one embedding (device)."""
+    n, ds = features.shape
+    k, df = atoms.shape
+    out = torch.empty(n, device=features.device)
+    check(ctx.h, lib().latmap_query_map(ctx.h, _ptr(features.contiguous()), n, ds, _ptr(atoms.contiguous()),
+                                        _ptr(proj.contiguous()), k, df, float(temperature),
+                                        _ptr(embedding.contiguous()), _ptr(out)))
+    return out
+
+
+def evaluate_map(ctx, m: GaussianMap, atoms, proj, temperature, frames, intr, prototypes=None, stride=1):
+    """evaluate_map (evaluate.cpp:10-72) over device frames: each ``frames[f]`` has pose_rot,
+    pose_trans, rgb (h x w x 3), assignment (h x w), features (n_set x df) and optionally labels
+    (h x w, -1 = unlabeled), all torch CUDA tensors. Returns the reference's EvalResult fields."""
+    if stride < 1:
+        raise _capi.InvalidArgument("evaluate_map: stride must be >= 1")
+    rows, cos_sum, psnr_sum = [], 0.0, 0.0
+    c = 0 if prototypes is None else prototypes.shape[0]
+    inter_all = np.zeros(c, np.int64)
+    uni_all = np.zeros(c, np.int64)
+    for fi in range(0, len(frames), stride):
+        fr = frames[fi]
+        out = render(ctx, m, make_pose(fr.pose_rot, fr.pose_trans), intr)
+        row = {"frame_index": fi, "psnr": metric_psnr(ctx, out.color, fr.rgb)[0], "cos_loss": 0.0, "miou": 0.0,
+               "labeled_pixels": 0}
+        psnr_sum += row["psnr"]
+        q, t, pix = gather_supervision(ctx, out.query, fr.assignment, fr.features, normalize=True)
+        if q.shape[0] > 0:
+            rec = reconstruct(ctx, q, atoms, proj, temperature)
+            row["cos_loss"] = metric_cos(ctx, rec, t)[0]
+            row["labeled_pixels"] = int(q.shape[0])
+            labels = getattr(fr, "labels", None)
+            if labels is not None and c > 0:
+                miou, inter, uni = metric_miou(ctx, rec, labels.reshape(-1)[pix], prototypes)
+                row["miou"] = miou
+                inter_all += inter
+                uni_all += uni
+        cos_sum += row["cos_loss"]
+        rows.append(row)
+    nfr = len(rows)
+    inc = uni_all > 0
+    return {"cos_loss": cos_sum / nfr if nfr else 0.0, "psnr": psnr_sum / nfr if nfr else 0.0,
+            "miou": float(np.mean(inter_all[inc] / uni_all[inc])) if inc.any() else 0.0, "frames": rows}
 
 
 @dataclass

@@ -1875,6 +1875,59 @@ latmap_status latmap_session_set_dict_weights(latmap_session* s, const float* w)
   return LATMAP_OK;
 }
 
+latmap_status latmap_gather_supervision(latmap_ctx* ctx, const float* query, int32_t ds, const int32_t* assignment,
+                                        int64_t npx, const float* features, int32_t df, int32_t normalize,
+                                        float* q_out, float* t_out, int64_t* pixel_of_row, int64_t cap,
+                                        int64_t* n_rows) {
+  if (!ctx || !n_rows || npx < 0 || ds < 1 || df < 1 || (npx > 0 && !assignment) ||
+      (q_out && (!query || !t_out || !pixel_of_row || !features)))
+    return LATMAP_ERR_INVALID_ARGUMENT;
+  CTX_CHECK(ctx, gather_supervision_dev(ctx->stream, query, ds, assignment, npx, features, df, normalize != 0, q_out,
+                                        t_out, pixel_of_row, cap, n_rows));
+  if (q_out && *n_rows > cap) return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "gather_supervision: output capacity");
+  return post_launch(ctx);
+}
+
+latmap_status latmap_metric_cos(latmap_ctx* ctx, const float* reconstructed, const float* target, int64_t n,
+                                int32_t d, double* value, int32_t* flagged) {
+  if (!ctx || !value || n < 0 || d < 1 || (n > 0 && (!reconstructed || !target))) return LATMAP_ERR_INVALID_ARGUMENT;
+  CTX_CHECK(ctx, metric_cos_dev(ctx->stream, reconstructed, target, n, d, value, flagged));
+  return post_launch(ctx);
+}
+
+latmap_status latmap_metric_miou(latmap_ctx* ctx, const float* embeddings, const int32_t* labels, int64_t n,
+                                 int32_t d, const float* prototypes, int32_t c, int64_t* intersection,
+                                 int64_t* union_, double* miou) {
+  if (!ctx || !miou || n < 0 || d < 1 || c < 0 || (c > 0 && (!intersection || !union_ || !prototypes)) ||
+      (n > 0 && (!embeddings || !labels)))
+    return LATMAP_ERR_INVALID_ARGUMENT;
+  bool bad = false;
+  CTX_CHECK(ctx, metric_miou_dev(ctx->stream, embeddings, labels, n, d, prototypes, c, intersection, union_, miou, &bad));
+  if (bad) return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "metric_miou: label id out of range");
+  return post_launch(ctx);
+}
+
+latmap_status latmap_metric_psnr(latmap_ctx* ctx, const float* rendered, const float* observed, int64_t n, double* db,
+                                 int32_t* exact) {
+  if (!ctx || !db || !exact || n < 1 || !rendered || !observed) return LATMAP_ERR_INVALID_ARGUMENT;
+  CTX_CHECK(ctx, metric_psnr_dev(ctx->stream, rendered, observed, n, db, exact));
+  return post_launch(ctx);
+}
+
+latmap_status latmap_query_map(latmap_ctx* ctx, const float* features, int64_t n, int32_t ds, const float* atoms,
+                               const float* proj, int64_t k, int32_t df, float temperature, const float* embedding,
+                               float* scores) {
+  if (!ctx || n < 0 || !embedding || !scores || (n > 0 && !features)) return LATMAP_ERR_INVALID_ARGUMENT;
+  if (n == 0) return LATMAP_OK;  // evaluate.cpp:77
+  cudaStream_t st = ctx->stream;
+  float* rec = nullptr;
+  CTX_CHECK(ctx, cudaMallocAsync(&rec, sizeof(float) * n * df, st));
+  latmap_status s = latmap_reconstruct(ctx, features, n, ds, atoms, proj, k, df, temperature, rec, nullptr);
+  if (s == LATMAP_OK) CTX_CHECK(ctx, query_scores_dev(st, rec, n, df, embedding, scores));
+  cudaFreeAsync(rec, st);
+  return s == LATMAP_OK ? post_launch(ctx) : s;
+}
+
 latmap_status latmap_selftest_umma(latmap_ctx* ctx, const float* a, const float* b, float* c, int32_t n, int32_t k,
                                    int32_t a_mn, int32_t b_mn) {
   if (!ctx || !a || !b || !c) return LATMAP_ERR_INVALID_ARGUMENT;

@@ -165,6 +165,17 @@ cudaError_t kmeans_weighted(cudaStream_t st, const float* P, const float* W, int
 cudaError_t kmeans_stream_update(cudaStream_t st, const float* batch, int64_t n, int dim, float* atoms, float* anchor,
                                  float* weights, int64_t K, double (*uni)(void*), void* user, float decay);
 
+// Evaluation (metrics.cu): device rows in, host scalars out.
+cudaError_t metric_cos_dev(cudaStream_t st, const float* rec, const float* tgt, int64_t n, int d, double* out,
+                           int32_t* flagged);
+cudaError_t metric_miou_dev(cudaStream_t st, const float* emb, const int32_t* labels, int64_t n, int d,
+                            const float* protos, int c, int64_t* inter, int64_t* uni, double* miou, bool* bad_label);
+cudaError_t metric_psnr_dev(cudaStream_t st, const float* a, const float* b, int64_t n, double* db, int32_t* exact);
+cudaError_t query_scores_dev(cudaStream_t st, const float* rec, int64_t n, int d, const float* emb, float* scores);
+cudaError_t gather_supervision_dev(cudaStream_t st, const float* query, int ds, const int32_t* asg, int64_t npx,
+                                   const float* feats, int df, bool normalize, float* q_out, float* t_out,
+                                   int64_t* pix, int64_t cap, int64_t* n_rows);
+
 int umma_selftest(cudaStream_t st, const float* A, const float* B, float* C, int N, int K, int a_mn, int b_mn);
 
 void set_launch_counter(int64_t* c);
