@@ -637,6 +637,8 @@ struct latmap_session {
   // CUDA graph of one Stage-I step (objective + Adam), replayed while the launch sequence and its
   // arguments (frame poses, buffer pointers, sizes) are unchanged
   cudaGraphExec_t step_graph = nullptr;
+  cudaGraphExec_t obj_graph = nullptr;  // objective only (want_grad): the multi-GPU path's per-rank part
+  int64_t obj_launches = 0;
   cudaStream_t cap_stream = nullptr;
   // set_frames uploads on ctx->copy_stream; up_ev[b] marks frame b's data resident. Every use of
   // frame data waits on it (an external event node when captured), so the render of frame 0 and
@@ -661,7 +663,8 @@ struct latmap_session {
   bool use_graph = true;
   void drop_graph() {
     if (step_graph) cudaGraphExecDestroy(step_graph);
-    step_graph = nullptr;
+    if (obj_graph) cudaGraphExecDestroy(obj_graph);
+    step_graph = obj_graph = nullptr;
   }
   // phase timing with CUDA events on the session stream (bench.py roofline evidence)
   struct Span {
@@ -1395,10 +1398,28 @@ latmap_status latmap_session_set_slot_offset(latmap_session* s, int32_t offset) 
   return LATMAP_OK;
 }
 
+static bool session_sized(const latmap_session* s);
+static latmap_status session_capture_step(latmap_session* s, bool with_adam);
+
 latmap_status latmap_session_objective(latmap_session* s, int32_t want_grad, latmap_loss_breakdown* out) {
   if (!s || s->nframes < 1) return LATMAP_ERR_INVALID_ARGUMENT;
   for (int attempt = 0; attempt < 3; ++attempt) {
-    latmap_status st = session_objective(s, want_grad != 0);
+    latmap_status st = LATMAP_OK;
+    if (want_grad && s->use_graph && !s->prof && session_sized(s)) {
+      // replayed objective graph (the multi-GPU step: objective -> all-reduce -> apply)
+      if ((s->step_graph || s->obj_graph) &&
+          (s->graph_exact != s->ctx->exact_blend || s->graph_dec_path != s->ctx->decoder_path))
+        s->drop_graph();
+      if (!s->obj_graph) {
+        st = session_capture_step(s, false);
+        if (st != LATMAP_OK) return st;
+      }
+      CTX_CHECK(s->ctx, cudaGraphLaunch(s->obj_graph, s->ctx->stream));
+      count_launch((int)s->obj_launches);
+      s->renders_valid = true;
+    } else {
+      st = session_objective(s, want_grad != 0);
+    }
     if (st != LATMAP_OK) return st;
     if (!out) return LATMAP_OK;
     CTX_CHECK(s->ctx, cudaStreamSynchronize(s->ctx->stream));
@@ -1414,9 +1435,13 @@ latmap_status latmap_session_apply(latmap_session* s) {
 }
 
 // Capture (objective + Adam) into s->step_graph. Requires sized tile buffers (a prior step).
-static latmap_status session_capture_step(latmap_session* s) {
+static latmap_status session_capture_step(latmap_session* s, bool with_adam) {
   latmap_ctx* ctx = s->ctx;
-  s->drop_graph();
+  if (with_adam) {
+    if (s->step_graph) cudaGraphExecDestroy(s->step_graph), s->step_graph = nullptr;
+  } else {
+    if (s->obj_graph) cudaGraphExecDestroy(s->obj_graph), s->obj_graph = nullptr;
+  }
   // capture on a private non-blocking stream (the context's stream may be the legacy default
   // stream, which cannot be captured); the graph is then launched on the context's stream
   if (!s->cap_stream) CTX_CHECK(ctx, cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking));
@@ -1432,7 +1457,7 @@ static latmap_status session_capture_step(latmap_session* s) {
     CTX_CHECK(ctx, e);
   }
   latmap_status rs = session_objective(s, true);
-  if (rs == LATMAP_OK) session_adam(s);
+  if (rs == LATMAP_OK && with_adam) session_adam(s);
   e = cudaStreamEndCapture(s->cap_stream, &g);
   ctx->stream = saved;
   const int64_t captured = g_launches.load() - l0;
@@ -1442,10 +1467,10 @@ static latmap_status session_capture_step(latmap_session* s) {
     return rs;
   }
   CTX_CHECK(ctx, e);
-  e = cudaGraphInstantiate(&s->step_graph, g, 0);
+  e = cudaGraphInstantiate(with_adam ? &s->step_graph : &s->obj_graph, g, 0);
   cudaGraphDestroy(g);
   CTX_CHECK(ctx, e);
-  s->graph_launches = captured;
+  (with_adam ? s->graph_launches : s->obj_launches) = captured;
   s->graph_exact = ctx->exact_blend;
   s->graph_dec_path = ctx->decoder_path;
   return LATMAP_OK;
@@ -1469,10 +1494,11 @@ latmap_status latmap_session_step(latmap_session* s, latmap_loss_breakdown* out)
   for (int attempt = 0; attempt < 3; ++attempt) {
     latmap_status st = LATMAP_OK;
     if (s->use_graph && !s->prof && session_sized(s)) {
-      if (s->step_graph && (s->graph_exact != s->ctx->exact_blend || s->graph_dec_path != s->ctx->decoder_path))
+      if ((s->step_graph || s->obj_graph) &&
+          (s->graph_exact != s->ctx->exact_blend || s->graph_dec_path != s->ctx->decoder_path))
         s->drop_graph();
       if (!s->step_graph) {
-        st = session_capture_step(s);
+        st = session_capture_step(s, true);
         if (st != LATMAP_OK) return st;
       }
       CTX_CHECK(s->ctx, cudaGraphLaunch(s->step_graph, s->ctx->stream));

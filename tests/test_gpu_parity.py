@@ -581,3 +581,22 @@ def test_tile_list_overflow_is_recovered(ctx, cfg0):
     la2 = a.step(read=True)  # and through the captured step
     lb2 = b.step(read=True)
     assert la2["total"] == pytest.approx(lb2["total"], rel=1e-5)
+
+
+def test_objective_graph_matches_direct(ctx, cfg0):
+    """latmap_session_objective replays a captured objective-only graph once the tile lists are
+    sized (the multi-GPU step: objective -> all-reduce -> apply); it equals the direct launches."""
+    w = cfg0
+    a = make_session(ctx, w)
+    b = make_session(ctx, w)
+    b.set_graphs(False)
+    for _ in range(3):  # first call sizes (direct), then capture, then replay
+        la = a.objective(want_grad=True)
+        lb = b.objective(want_grad=True)
+        assert la["total"] == pytest.approx(lb["total"], rel=1e-6)
+        ga, gb = a.grad_buffer().cpu().numpy(), b.grad_buffer().cpu().numpy()
+        assert np.linalg.norm(ga - gb) <= 1e-5 * np.linalg.norm(gb)
+    a.apply()
+    b.apply()
+    la, lb = a.objective(want_grad=True), b.objective(want_grad=True)
+    assert la["total"] == pytest.approx(lb["total"], rel=1e-4)
