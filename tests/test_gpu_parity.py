@@ -600,3 +600,35 @@ def test_objective_graph_matches_direct(ctx, cfg0):
     b.apply()
     la, lb = a.objective(want_grad=True), b.objective(want_grad=True)
     assert la["total"] == pytest.approx(lb["total"], rel=1e-4)
+
+
+def test_objective_ragged_multiframe_unsupervised(ctx):
+    """Ragged image (70 x 52: partial tiles on both edges), two keyframes through the multi-stream
+    pipeline, the second with no supervised pixel (decoder rows all masked, n_sup = 0): objective
+    and gradients against the oracle's total_objective."""
+    def orender(m, q, t, intr):
+        om = oracle.GaussianMap(*[np.ascontiguousarray(getattr(m, f), np.float32) for f in oracle.FIELDS])
+        out = oracle.render(om, q, t, oracle.make_intr(intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height))
+        return out["color"], out["depth"], out["alpha"]
+
+    w = synthetic.make_workload(0, orender, scale=0.22)
+    assert w.intr.width % 16 and w.intr.height % 16
+    f0 = w.frames[0]
+    f1 = synthetic.Frame(synthetic.yaw_quat(0.03), (0.01, 0.0, 0.0), f0.rgb, f0.depth,
+                         np.full_like(f0.assignment, -1), f0.features)
+    w.frames = [f0, f1]
+    s = make_session(ctx, w)
+    loss = s.objective(want_grad=True)
+    loss = s.objective(want_grad=True)  # second call: the captured objective graph
+    d = oracle.Dictionary(w.atoms.copy(), w.anchor.copy(), w.proj.copy(), np.float32(w.temperature))
+    ref, (g, dp, da) = oracle.total_objective(to_oracle_map(w.map), d, oracle_frames(w), oi(w.intr), oracle_cfg(w),
+                                              threads=THREADS)
+    for key in ("l_rgb", "l_ssim", "l_depth", "l_cos", "l_l2", "l_trust", "total"):
+        assert loss[key] == pytest.approx(ref[key], rel=2e-4, abs=1e-6), key
+    assert loss["supervised_rows"] == ref["supervised_rows"]
+    gb = s.grad_buffer().cpu().numpy()
+    n, ds = w.map.n, w.map.features.shape[1]
+    offs = np.cumsum([0, 3 * n, 4 * n, 3 * n, 3 * n, n, ds * n])
+    blocks = [g.positions, g.rotations, g.colors, g.log_scales, g.opacity_logits, g.features]
+    for i, (name, ref_b) in enumerate(zip(oracle.FIELDS, blocks)):
+        assert_close_floor(gb[offs[i]:offs[i + 1]], ref_b.reshape(-1), 1e-3, name)
