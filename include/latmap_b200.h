@@ -205,6 +205,8 @@ latmap_status latmap_session_get_map(latmap_session* s, float* positions, float*
 latmap_status latmap_session_set_dictionary(latmap_session* s, const float* atoms, const float* anchor,
                                             const float* proj);
 latmap_status latmap_session_get_dictionary(latmap_session* s, float* atoms, float* proj);
+/* DictionaryStateT::anchor (the trust-region centre; artifacts.cpp:79 save_dictionary). */
+latmap_status latmap_session_get_anchor(latmap_session* s, float* anchor);
 /* Keyframe batch (host arrays, copied H2D on the session stream). */
 latmap_status latmap_session_set_frames(latmap_session* s, int32_t nframes, const latmap_frame* frames);
 /* Batch-mean denominator (objective.cpp:77) and whether this rank adds the trust term
@@ -293,6 +295,10 @@ latmap_status latmap_store_get_records(const latmap_store* s, int64_t first, int
 /* insert_global (voxel_hash.cpp:101-115): keys + home slots on the device, probe in row order. */
 latmap_status latmap_store_insert_global(latmap_store* s, const float* recs, int64_t n, float voxel_size,
                                          int64_t* inserted);
+/* Rebuild from a global-map dump (artifacts.cpp:54-63 load_map_store): VoxelHashStore::insert of
+ * each record under its stored key, in dump order (keys n x 3 int32, recs n x record AoS). */
+latmap_status latmap_store_insert_keyed(latmap_store* s, const int32_t* keys, const float* recs, int64_t n,
+                                        int64_t* inserted);
 /* fetch_local (active_set.cpp:7-36): ascending record indices within `radius` (device radius scan +
  * ordered compaction); optional gather of the records into device memory (d_records, AoS). */
 latmap_status latmap_store_fetch_local(latmap_store* s, const float center[3], float radius, int64_t* origin,

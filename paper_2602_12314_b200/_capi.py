@@ -116,6 +116,7 @@ def _declare(L):
         "latmap_session_get_map": [P, P, P, P, P, P, P],
         "latmap_session_set_dictionary": [P, P, P, P],
         "latmap_session_get_dictionary": [P, P, P],
+        "latmap_session_get_anchor": [P, P],
         "latmap_session_set_frames": [P, C.c_int32, C.POINTER(Frame)],
         "latmap_session_set_batch": [P, C.c_int32, C.c_int32],
         "latmap_session_set_slot_offset": [P, C.c_int32],
@@ -151,6 +152,7 @@ def _declare(L):
         "latmap_store_destroy": [P],
         "latmap_store_get_records": [P, C.c_int64, C.c_int64, P, P],
         "latmap_store_insert_global": [P, P, C.c_int64, C.c_float, C.POINTER(C.c_int64)],
+        "latmap_store_insert_keyed": [P, P, P, C.c_int64, C.POINTER(C.c_int64)],
         "latmap_store_fetch_local": [P, P, C.c_float, P, C.c_int64, C.POINTER(C.c_int64), P],
         "latmap_store_sync": [P, P, P, P, C.c_int64, P, C.c_float, C.c_float, P, P, C.c_int64, P, P,
                               C.POINTER(C.c_int64)],
@@ -195,7 +197,7 @@ EXPORTED = ["latmap_ctx_create", "latmap_ctx_destroy", "latmap_ctx_set_stream", 
             "latmap_render_cache_splats", "latmap_render_cache_tiles", "latmap_reconstruct",
             "latmap_reconstruct_backward", "latmap_trust_region_penalty", "latmap_ssim", "latmap_adam_step",
             "latmap_session_create", "latmap_session_destroy", "latmap_session_set_map", "latmap_session_get_map",
-            "latmap_session_set_dictionary", "latmap_session_get_dictionary", "latmap_session_set_frames",
+            "latmap_session_set_dictionary", "latmap_session_get_dictionary", "latmap_session_get_anchor", "latmap_session_set_frames",
             "latmap_session_set_batch", "latmap_session_set_slot_offset", "latmap_session_objective",
             "latmap_session_apply", "latmap_session_step", "latmap_session_objective_ex", "latmap_session_step_dict",
             "latmap_session_export_rows", "latmap_session_import_rows", "latmap_session_size",
@@ -205,7 +207,7 @@ EXPORTED = ["latmap_ctx_create", "latmap_ctx_destroy", "latmap_ctx_set_stream", 
             "latmap_session_profile", "latmap_session_phase_times", "latmap_selftest_umma", "latmap_ctx_stream",
             "latmap_voxel_of", "latmap_hash_voxel", "latmap_store_create", "latmap_store_destroy", "latmap_store_size",
             "latmap_store_stats", "latmap_store_last_error", "latmap_store_insert", "latmap_store_update",
-            "latmap_store_find", "latmap_store_get_records", "latmap_store_insert_global", "latmap_store_fetch_local",
+            "latmap_store_find", "latmap_store_get_records", "latmap_store_insert_global", "latmap_store_insert_keyed", "latmap_store_fetch_local",
             "latmap_store_sync", "latmap_weighted_kmeans", "latmap_session_stream_kmeans",
             "latmap_session_get_dict_weights", "latmap_session_set_dict_weights", "latmap_gather_supervision",
             "latmap_metric_cos", "latmap_metric_miou", "latmap_metric_psnr", "latmap_query_map"]

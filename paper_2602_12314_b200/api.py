@@ -451,6 +451,11 @@ class Session:
         w = np.ascontiguousarray(w, np.float32)
         check(self.ctx.h, lib().latmap_session_set_dict_weights(self.h, w.ctypes.data_as(C.c_void_p)))
 
+    def get_anchor(self):
+        out = np.zeros((self.k, self.df), np.float32)
+        check(self.ctx.h, lib().latmap_session_get_anchor(self.h, self._np_ptr(out)))
+        return out
+
     def get_dictionary(self):
         atoms = np.zeros((self.k, self.df), np.float32)
         proj = np.zeros((self.ds, self.df), np.float32)
@@ -620,6 +625,7 @@ class Store:
 
     def __init__(self, ctx, capacity, query_dim):
         self.ctx, self.ds, self.rs = ctx, query_dim, 14 + query_dim
+        self.capacity = int(capacity)
         h = C.c_void_p()
         check(ctx.h, lib().latmap_store_create(ctx.h, int(capacity), int(query_dim), C.byref(h)))
         self.h = h
@@ -672,6 +678,18 @@ class Store:
         ins = C.c_int64(0)
         self._check(lib().latmap_store_insert_global(self.h, r.ctypes.data_as(C.c_void_p), r.shape[0],
                                                      float(voxel_size), C.byref(ins)))
+        return ins.value
+
+    def insert_keyed(self, keys, recs):
+        """VoxelHashStore::insert of each row under its given key, in row order (rebuilding a
+        dump, artifacts.cpp:54-63); returns the number inserted."""
+        k = np.ascontiguousarray(keys, np.int32).reshape(-1, 3)
+        r = np.ascontiguousarray(recs, np.float32).reshape(-1, self.rs)
+        if k.shape[0] != r.shape[0]:
+            raise _capi.InvalidArgument("insert_keyed: keys and records differ in count")
+        ins = C.c_int64(0)
+        self._check(lib().latmap_store_insert_keyed(self.h, k.ctypes.data_as(C.c_void_p), r.ctypes.data_as(C.c_void_p),
+                                                    r.shape[0], C.byref(ins)))
         return ins.value
 
     def fetch_local(self, center, radius, gather=False):

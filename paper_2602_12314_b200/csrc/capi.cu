@@ -1257,6 +1257,14 @@ latmap_status latmap_session_get_dictionary(latmap_session* s, float* atoms, flo
   return LATMAP_OK;
 }
 
+latmap_status latmap_session_get_anchor(latmap_session* s, float* anchor) {
+  if (!s || !anchor) return LATMAP_ERR_INVALID_ARGUMENT;
+  latmap_ctx* ctx = s->ctx;
+  CTX_CHECK(ctx, cudaMemcpyAsync(anchor, s->anchor, sizeof(float) * s->k * s->df, cudaMemcpyDeviceToHost, ctx->stream));
+  CTX_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+  return LATMAP_OK;
+}
+
 latmap_status latmap_session_set_frames(latmap_session* s, int32_t nf, const latmap_frame* frames) {
   if (!s || nf < 1 || !frames) return fail(s ? s->ctx : nullptr, LATMAP_ERR_INVALID_ARGUMENT, "total_objective: empty batch");
   latmap_ctx* ctx = s->ctx;

@@ -378,6 +378,29 @@ latmap_status latmap_store_insert_global(latmap_store* s, const float* recs, int
   return LATMAP_OK;
 }
 
+// Rebuild from a dump (artifacts.cpp:54-63 LoadedMap -> VoxelHashStore::insert per record in dump
+// order): explicit keys, so record indices follow the dump and rejections match insert().
+latmap_status latmap_store_insert_keyed(latmap_store* s, const int32_t* keys, const float* recs, int64_t n,
+                                        int64_t* inserted) {
+  if (!s || n < 0 || (n > 0 && (!recs || !keys))) return LATMAP_ERR_INVALID_ARGUMENT;
+  if (inserted) *inserted = 0;
+  if (n == 0) return LATMAP_OK;
+  if (ensure_pool(s, s->size + n) != LATMAP_OK) return LATMAP_ERR_OUT_OF_MEMORY;
+  const int64_t first = s->size;
+  int64_t ins = 0;
+  for (int64_t i = 0; i < n; ++i)
+    ins += insert_one(s, &keys[3 * i], lm::hash_voxel(&keys[3 * i], s->capacity), recs + i * s->rs, false,
+                      nullptr) >= 0;
+  std::vector<float> pos((size_t)(s->size - first) * 3);
+  for (int64_t r = first; r < s->size; ++r) std::memcpy(&pos[(r - first) * 3], s->pool + r * s->rs, 12);
+  if (!pos.empty())
+    S_CHECK(s, cudaMemcpyAsync(s->d_pos + first * 3, pos.data(), sizeof(float) * pos.size(), cudaMemcpyHostToDevice,
+                               s->st));
+  S_CHECK(s, cudaStreamSynchronize(s->st));
+  if (inserted) *inserted = ins;
+  return LATMAP_OK;
+}
+
 // fetch_local (active_set.cpp:7-36): ascending record indices of the records within `radius`,
 // optional gather of their records into a device AoS buffer (records x (14 + ds) floats).
 latmap_status latmap_store_fetch_local(latmap_store* s, const float center[3], float radius, int64_t* origin,

@@ -151,3 +151,51 @@ def test_streaming_session_loop_matches_oracle_store(ctx):
             loss = s.step(read=True)
         assert np.isfinite(loss["total"])
     assert min(ncount) > 0
+
+
+def test_map_dump_restore_round_trip(ctx, tmp_path):
+    """save_map_store -> load_map_store -> a fresh store rebuilt under the dumped keys
+    (artifacts.cpp:40-63): same records in the same order, same keys, same find() answers,
+    and fetch_local over the rebuilt store equals the original's."""
+    from paper_2602_12314_b200 import lamt
+    rng = np.random.default_rng(11)
+    r = recs(rng, 5000)
+    s = api.Store(ctx, 1 << 15, 4)
+    s.insert_global(r, 0.01)
+    lamt.save_map_store(s, str(tmp_path / "map.lamt"))
+    lamt.save_store_counters(s, str(tmp_path / "counters.json"))
+    lm = lamt.load_map_store(str(tmp_path / "map.lamt"))
+    t = lamt.restore_store(ctx, lm, 1 << 15)
+    assert t.size() == s.size()
+    a, ka = s.records()
+    b, kb = t.records()
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32)) and np.array_equal(ka, kb)
+    for k in ka[::41]:
+        assert t.find(k) == s.find(k)
+    c = np.array([0.3, -0.2, 0.1], np.float32)
+    assert np.array_equal(t.fetch_local(c, 1.0), s.fetch_local(c, 1.0))
+    # a different capacity changes the slots, not the record order
+    u = lamt.restore_store(ctx, lm, 20011)
+    assert np.array_equal(u.records()[0].view(np.uint32), a.view(np.uint32))
+    assert u.insert_keyed(ka[:3], a[:3]) == 0 and u.stats()["rejected_duplicate"] == 3
+
+
+def test_session_dictionary_dump_round_trip(ctx, tmp_path):
+    """save_dictionary of a device session -> load_dictionary -> apply to another session."""
+    from paper_2602_12314_b200 import lamt
+    g = np.random.default_rng(12)
+    k, df, ds = 16, 32, 8
+    cfg = api.default_config(softmax_temp=2.0)
+    intr = api.make_intrinsics(50, 50, 16, 16, 32, 32)
+    s1, s2 = (api.Session(ctx, cfg, 16, ds, k, df, intr) for _ in range(2))
+    atoms, anchor = g.standard_normal((2, k, df)).astype(np.float32)
+    proj = g.standard_normal((ds, df)).astype(np.float32)
+    s1.set_dictionary(atoms, anchor, proj)
+    s1.set_dict_weights(g.uniform(0, 4, k).astype(np.float32))
+    lamt.save_dictionary(s1, str(tmp_path / "dict.lamt"))
+    d = lamt.load_dictionary(str(tmp_path / "dict.lamt"))
+    assert d.temperature == 2.0 and np.array_equal(d.anchor, anchor)
+    lamt.apply_dictionary(s2, d)
+    a2, p2 = s2.get_dictionary()
+    assert np.array_equal(a2, atoms) and np.array_equal(p2, proj)
+    assert np.array_equal(s2.get_anchor(), anchor) and np.array_equal(s2.dict_weights(), s1.dict_weights())
