@@ -359,6 +359,65 @@ latmap_status latmap_query_map(latmap_ctx* ctx, const float* features, int64_t n
                                const float* proj, int64_t k, int32_t df, float temperature, const float* embedding,
                                float* scores);
 
+/* ---------------------------------------------------------------- pipeline (the step's caller) */
+/* The pipeline-level subset of latmap::Config (core/config.hpp:10-58; same defaults via
+ * latmap_default_pipeline_config). dict_init: 0 = "kmeans", 1 = "random". The objective's own
+ * fields (loss weights, learning rates, softmax_temp, dict_learn, segment_mode) stay in
+ * latmap_config. */
+typedef struct {
+  int32_t query_dim, embed_dim, dict_size;
+  int32_t stage1_iters, stage2_iters;
+  int32_t history_sample, history_capacity;
+  float voxel_size, local_radius, sync_distance;
+  int64_t hash_capacity;
+  int32_t local_mapping, keyframe_stride;
+  uint64_t seed;
+  int32_t dict_init;
+  float dict_decay;
+  int32_t trust_anchor_persistent;
+} latmap_pipeline_config;
+/* KeyframeLog (pipe/pipeline.hpp:70-80); sync = SyncStats {written_back, newborn_inserted,
+ * newborn_rejected, pruned, fetched} (store/active_set.hpp:28-34). */
+typedef struct {
+  int32_t frame_index;
+  latmap_loss_breakdown loss;
+  int64_t seeded, active_count, global_count;
+  double dict_weight_mass;
+  int32_t synced;
+  int64_t sync[5];
+  double wall_ms;
+} latmap_keyframe_log;
+typedef struct latmap_pipeline latmap_pipeline;
+void latmap_default_pipeline_config(latmap_pipeline_config* pc);
+/* select_keyframe (pipeline.cpp:14-17): 1 / 0, or -1 for stride < 1 (std::invalid_argument). */
+int32_t latmap_select_keyframe(int32_t frame_index, int32_t stride);
+/* PipelineState::PipelineState (pipeline.cpp:106-121): an empty active map (device session), an
+ * empty global store (hash_capacity), a zero dictionary with proj ~ N(0, 0.1) from
+ * std::mt19937_64(seed). Config::validate's checks (config.cpp:110-133) -> INVALID_ARGUMENT with
+ * the message on the context. */
+latmap_status latmap_pipeline_create(latmap_ctx* ctx, const latmap_config* cfg, const latmap_pipeline_config* pc,
+                                     const latmap_intrinsics* intr, latmap_pipeline** out);
+latmap_status latmap_pipeline_destroy(latmap_pipeline* p);
+/* process_keyframe (pipeline.cpp:192-312): embedding normalisation, dictionary maintenance,
+ * history-augmented batch, seeding, Stage I x stage1_iters, Stage II x stage2_iters on cached
+ * renders, history push, travel and sync. The frame is host memory (copied). Argument errors
+ * leave the state untouched; a device error mid-keyframe marks the pipeline failed (the device
+ * state cannot be rolled back as the reference's snapshot/restore does). */
+latmap_status latmap_pipeline_process_keyframe(latmap_pipeline* p, const latmap_frame* kf, int32_t frame_index,
+                                               latmap_keyframe_log* out);
+/* run_pipeline's final flush (pipeline.cpp:318-330): the whole active set marked dirty and synced
+ * at the last position; stats = SyncStats (may be NULL). */
+latmap_status latmap_pipeline_flush(latmap_pipeline* p, int64_t stats[5]);
+/* Borrowed handles (owned by the pipeline): the device map/dictionary session and the store. */
+latmap_session* latmap_pipeline_session(latmap_pipeline* p);
+latmap_store* latmap_pipeline_store(latmap_pipeline* p);
+/* PipelineState scalars: keyframes_processed, peak_active, history size, reservoir_seen, failed,
+ * traveled (float bits). */
+latmap_status latmap_pipeline_state(const latmap_pipeline* p, int64_t out[6]);
+/* ActiveSet::origin / dirty (host arrays of latmap_session_size entries). */
+latmap_status latmap_pipeline_active_set(const latmap_pipeline* p, int64_t* origin, uint8_t* dirty);
+const char* latmap_pipeline_last_error(const latmap_pipeline* p);
+
 /* ---------------------------------------------------------------- self-test */
 /* One-tile tcgen05 GEMM, C[128 x n] = A[128 x k] * B[n x k]^T (device fp32 in/out, bf16 staging),
  * with A / B staged K-major (0) or MN-major (1); pins the UMMA descriptor conventions. */

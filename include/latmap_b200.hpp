@@ -5,6 +5,7 @@
 //                                                <- dict/dictionary.hpp:63-77
 //   latmap_b200::Session::total_objective / step  <- total_objective (obj/objective.hpp:49-54) +
 //                                                   MapOptimizer::step_map/step_dict (pipe/pipeline.hpp:52-69)
+//   latmap_b200::Pipeline / select_keyframe       <- PipelineState, process_keyframe (pipe/pipeline.hpp:82-107)
 // Status codes map back to the reference's exceptions: LATMAP_ERR_INVALID_ARGUMENT ->
 // std::invalid_argument, LATMAP_ERR_STALE_CACHE -> std::runtime_error, anything else ->
 // latmap_b200::device_error. Device buffers are caller-owned raw pointers (any allocator).
@@ -261,5 +262,44 @@ class Session {
   int64_t k_ = 0;
   latmap_session* h_ = nullptr;
 };
+
+// PipelineState + process_keyframe + run_pipeline's flush (pipe/pipeline.hpp:82-107) over the
+// C-ABI pipeline; argument errors -> std::invalid_argument, device errors -> device_error.
+class Pipeline {
+ public:
+  Pipeline(Context& ctx, const latmap_config& cfg, const latmap_pipeline_config& pc, const latmap_intrinsics& intr)
+      : ctx_(&ctx) {
+    check(latmap_pipeline_create(ctx.get(), &cfg, &pc, &intr, &h_), ctx.get());
+  }
+  ~Pipeline() {
+    if (h_) latmap_pipeline_destroy(h_);
+  }
+  Pipeline(const Pipeline&) = delete;
+  Pipeline& operator=(const Pipeline&) = delete;
+  latmap_keyframe_log process_keyframe(const latmap_frame& kf, int32_t frame_index) {
+    latmap_keyframe_log row{};
+    pcheck(latmap_pipeline_process_keyframe(h_, &kf, frame_index, &row));
+    return row;
+  }
+  void flush(int64_t stats[5] = nullptr) { pcheck(latmap_pipeline_flush(h_, stats)); }
+  latmap_session* session() const { return latmap_pipeline_session(h_); }
+  latmap_store* store() const { return latmap_pipeline_store(h_); }
+
+ private:
+  void pcheck(latmap_status s) const {
+    if (s == LATMAP_OK) return;
+    const std::string msg = latmap_pipeline_last_error(h_);
+    if (s == LATMAP_ERR_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+    throw device_error(msg.empty() ? "latmap_b200: device error" : msg);
+  }
+  Context* ctx_;
+  latmap_pipeline* h_ = nullptr;
+};
+
+inline bool select_keyframe(int frame_index, int stride) {
+  const int32_t r = latmap_select_keyframe(frame_index, stride);
+  if (r < 0) throw std::invalid_argument("select_keyframe: stride must be >= 1");
+  return r != 0;
+}
 
 }  // namespace latmap_b200

@@ -69,6 +69,32 @@ class Frame(C.Structure):
                 ("features", C.c_void_p), ("n_set", C.c_int64)]
 
 
+class PipelineConfig(C.Structure):
+    """latmap_pipeline_config: the pipeline-level subset of latmap::Config (config.hpp:10-58)."""
+    _fields_ = [("query_dim", C.c_int32), ("embed_dim", C.c_int32), ("dict_size", C.c_int32),
+                ("stage1_iters", C.c_int32), ("stage2_iters", C.c_int32), ("history_sample", C.c_int32),
+                ("history_capacity", C.c_int32), ("voxel_size", C.c_float), ("local_radius", C.c_float),
+                ("sync_distance", C.c_float), ("hash_capacity", C.c_int64), ("local_mapping", C.c_int32),
+                ("keyframe_stride", C.c_int32), ("seed", C.c_uint64), ("dict_init", C.c_int32),
+                ("dict_decay", C.c_float), ("trust_anchor_persistent", C.c_int32)]
+
+
+SYNC_FIELDS = ("written_back", "newborn_inserted", "newborn_rejected", "pruned", "fetched")
+
+
+class KeyframeLog(C.Structure):
+    """KeyframeLog (pipe/pipeline.hpp:70-80)."""
+    _fields_ = [("frame_index", C.c_int32), ("loss", LossBreakdown), ("seeded", C.c_int64),
+                ("active_count", C.c_int64), ("global_count", C.c_int64), ("dict_weight_mass", C.c_double),
+                ("synced", C.c_int32), ("sync", C.c_int64 * 5), ("wall_ms", C.c_double)]
+
+    def as_dict(self):
+        return {"frame_index": self.frame_index, "loss": self.loss.as_dict(), "seeded": self.seeded,
+                "active_count": self.active_count, "global_count": self.global_count,
+                "dict_weight_mass": self.dict_weight_mass, "synced": bool(self.synced),
+                "sync": dict(zip(SYNC_FIELDS, list(self.sync))), "wall_ms": self.wall_ms}
+
+
 _lib = None
 
 
@@ -153,6 +179,13 @@ def _declare(L):
         "latmap_store_get_records": [P, C.c_int64, C.c_int64, P, P],
         "latmap_store_insert_global": [P, P, C.c_int64, C.c_float, C.POINTER(C.c_int64)],
         "latmap_store_insert_keyed": [P, P, P, C.c_int64, C.POINTER(C.c_int64)],
+        "latmap_pipeline_create": [P, C.POINTER(Config), C.POINTER(PipelineConfig), C.POINTER(Intrinsics),
+                                   C.POINTER(P)],
+        "latmap_pipeline_destroy": [P],
+        "latmap_pipeline_process_keyframe": [P, C.POINTER(Frame), C.c_int32, C.POINTER(KeyframeLog)],
+        "latmap_pipeline_flush": [P, P],
+        "latmap_pipeline_state": [P, P],
+        "latmap_pipeline_active_set": [P, P, P],
         "latmap_store_fetch_local": [P, P, C.c_float, P, C.c_int64, C.POINTER(C.c_int64), P],
         "latmap_store_sync": [P, P, P, P, C.c_int64, P, C.c_float, C.c_float, P, P, C.c_int64, P, P,
                               C.POINTER(C.c_int64)],
@@ -188,6 +221,16 @@ def _declare(L):
     L.latmap_store_find.restype = C.c_int64
     L.latmap_session_size.argtypes = [P]
     L.latmap_session_size.restype = C.c_int64
+    L.latmap_default_pipeline_config.argtypes = [C.POINTER(PipelineConfig)]
+    L.latmap_default_pipeline_config.restype = None
+    L.latmap_select_keyframe.argtypes = [C.c_int32, C.c_int32]
+    L.latmap_select_keyframe.restype = C.c_int32
+    L.latmap_pipeline_session.argtypes = [P]
+    L.latmap_pipeline_session.restype = P
+    L.latmap_pipeline_store.argtypes = [P]
+    L.latmap_pipeline_store.restype = P
+    L.latmap_pipeline_last_error.argtypes = [P]
+    L.latmap_pipeline_last_error.restype = C.c_char_p
 
 
 EXPORTED = ["latmap_ctx_create", "latmap_ctx_destroy", "latmap_ctx_set_stream", "latmap_ctx_synchronize",
@@ -210,7 +253,11 @@ EXPORTED = ["latmap_ctx_create", "latmap_ctx_destroy", "latmap_ctx_set_stream", 
             "latmap_store_find", "latmap_store_get_records", "latmap_store_insert_global", "latmap_store_insert_keyed", "latmap_store_fetch_local",
             "latmap_store_sync", "latmap_weighted_kmeans", "latmap_session_stream_kmeans",
             "latmap_session_get_dict_weights", "latmap_session_set_dict_weights", "latmap_gather_supervision",
-            "latmap_metric_cos", "latmap_metric_miou", "latmap_metric_psnr", "latmap_query_map"]
+            "latmap_metric_cos", "latmap_metric_miou", "latmap_metric_psnr", "latmap_query_map",
+            "latmap_default_pipeline_config", "latmap_select_keyframe", "latmap_pipeline_create",
+            "latmap_pipeline_destroy", "latmap_pipeline_process_keyframe", "latmap_pipeline_flush",
+            "latmap_pipeline_session", "latmap_pipeline_store", "latmap_pipeline_state", "latmap_pipeline_active_set",
+            "latmap_pipeline_last_error"]
 
 
 def check(ctx_handle, status):

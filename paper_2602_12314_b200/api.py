@@ -398,17 +398,30 @@ class Session:
 
     def __init__(self, ctx: Context, cfg: Config, n, query_dim, k, embed_dim, intr):
         self.ctx, self.cfg, self.intr = ctx, cfg, intr
-        self.n, self.ds, self.k, self.df = n, query_dim, k, embed_dim
+        self.ds, self.k, self.df = query_dim, k, embed_dim
         h = C.c_void_p()
         check(ctx.h, lib().latmap_session_create(ctx.h, C.byref(cfg), n, query_dim, k, embed_dim, C.byref(intr),
                                                  C.byref(h)))
         self.h = h
         self._keep = []
+        self._owner = None
+
+    @classmethod
+    def _borrowed(cls, owner, ctx, cfg, h, query_dim, k, embed_dim, intr):
+        """A view of a session owned by ``owner`` (a Pipeline): never destroyed here."""
+        s = cls.__new__(cls)
+        s.ctx, s.cfg, s.intr, s.ds, s.k, s.df = ctx, cfg, intr, query_dim, k, embed_dim
+        s.h, s._keep, s._owner = C.c_void_p(h), [], owner
+        return s
+
+    @property
+    def n(self):
+        return int(lib().latmap_session_size(self.h))
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and getattr(self, "_owner", None) is None:
             lib().latmap_session_destroy(self.h)
-            self.h = None
+        self.h = None
 
     @staticmethod
     def _np_ptr(a):
@@ -531,7 +544,6 @@ class Session:
         n_kept = int(km.sum()) if km is not None else self.n
         check(self.ctx.h, lib().latmap_session_import_rows(self.h, C.c_void_p(rows.data_ptr()) if n_new else None,
                                                            n_new, self._np_ptr(km), n_kept))
-        self.n = n_new
 
     def seed_candidates(self, frame=0):
         """seed_gaussians (pipeline.cpp:39-73) rows for `frame` (features zero), device [n, 14 + ds]."""
@@ -549,7 +561,6 @@ class Session:
         r = rows.contiguous()
         check(self.ctx.h, lib().latmap_session_append_rows(self.h, C.c_void_p(r.data_ptr()), int(r.shape[0]),
                                                            self._np_ptr(f)))
-        self.n += int(r.shape[0])
 
     def read_loss(self):
         out = LossBreakdown()
@@ -630,10 +641,16 @@ class Store:
         check(ctx.h, lib().latmap_store_create(ctx.h, int(capacity), int(query_dim), C.byref(h)))
         self.h = h
 
+    @classmethod
+    def _borrowed(cls, owner, ctx, h, capacity, query_dim):
+        st = cls.__new__(cls)
+        st.ctx, st.ds, st.rs, st.capacity, st.h, st._owner = ctx, query_dim, 14 + query_dim, int(capacity), C.c_void_p(h), owner
+        return st
+
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and getattr(self, "_owner", None) is None:
             lib().latmap_store_destroy(self.h)
-            self.h = None
+        self.h = None
 
     def _check(self, st):
         if st != _capi.OK:
@@ -729,3 +746,93 @@ class Store:
         w = cnt.value
         stats = dict(zip(("written_back", "newborn_inserted", "newborn_rejected", "pruned", "fetched"), st.tolist()))
         return d_out[:w].clone(), oo[:w].copy(), kept[:n].astype(bool), stats
+
+
+def default_pipeline_config(**overrides) -> _capi.PipelineConfig:
+    pc = _capi.PipelineConfig()
+    lib().latmap_default_pipeline_config(C.byref(pc))
+    for kk, vv in overrides.items():
+        if kk == "dict_init" and isinstance(vv, str):
+            vv = {"kmeans": 0, "random": 1}[vv]
+        setattr(pc, kk, vv)
+    return pc
+
+
+def select_keyframe(frame_index, stride):
+    """pipeline.cpp:14-17."""
+    r = lib().latmap_select_keyframe(int(frame_index), int(stride))
+    if r < 0:
+        raise _capi.InvalidArgument("select_keyframe: stride must be >= 1")
+    return bool(r)
+
+
+class Pipeline:
+    """PipelineState + process_keyframe (pipe/pipeline.hpp:82-107, pipeline.cpp:106-312) over the
+    device session and store; ``session`` / ``store`` are views of the pipeline's own."""
+
+    def __init__(self, ctx: Context, cfg: Config, pcfg, intr):
+        self.ctx, self.cfg, self.pcfg, self.intr = ctx, cfg, pcfg, intr
+        h = C.c_void_p()
+        check(ctx.h, lib().latmap_pipeline_create(ctx.h, C.byref(cfg), C.byref(pcfg), C.byref(intr), C.byref(h)))
+        self.h = h
+        self.session = Session._borrowed(self, ctx, cfg, lib().latmap_pipeline_session(h), pcfg.query_dim,
+                                         pcfg.dict_size, pcfg.embed_dim, intr)
+        self.store = Store._borrowed(self, ctx, lib().latmap_pipeline_store(h), pcfg.hash_capacity, pcfg.query_dim)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            for v in ("session", "store"):
+                if getattr(self, v, None) is not None:
+                    getattr(self, v).h = None
+            lib().latmap_pipeline_destroy(self.h)
+            self.h = None
+
+    def _check(self, st):
+        if st != _capi.OK:
+            msg = (lib().latmap_pipeline_last_error(self.h) or b"").decode()
+            cmsg = (lib().latmap_ctx_last_error(self.ctx.h) or b"").decode()
+            msg = msg or cmsg
+            if st == _capi.EINVAL:
+                raise _capi.InvalidArgument(msg)
+            raise _capi.LatmapError(f"latmap status {st}: {msg}")
+
+    def process_keyframe(self, kf, frame_index=None):
+        """kf: host keyframe (pose_rot (w,x,y,z), pose_trans, rgb H x W x 3, depth H x W,
+        assignment H x W, features n_set x embed_dim). Returns the KeyframeLog as a dict."""
+        fi = int(getattr(kf, "frame_index", 0) if frame_index is None else frame_index)
+        rgb = np.ascontiguousarray(kf.rgb, np.float32)
+        dep = np.ascontiguousarray(kf.depth, np.float32)
+        asg = np.ascontiguousarray(kf.assignment, np.int32)
+        fea = np.ascontiguousarray(kf.features, np.float32)
+        npx = self.intr.width * self.intr.height
+        if rgb.size != npx * 3 or dep.size != npx or asg.size != npx:
+            raise _capi.InvalidArgument("process_keyframe: image size does not match the intrinsics")
+        n_set = fea.shape[0] if fea.ndim == 2 and fea.size else 0
+        if n_set and fea.shape[1] != self.pcfg.embed_dim:
+            raise _capi.InvalidArgument("process_keyframe: embedding dimension mismatch")
+        f = Frame(make_pose(kf.pose_rot, kf.pose_trans), rgb.ctypes.data_as(C.c_void_p), dep.ctypes.data_as(C.c_void_p),
+                  asg.ctypes.data_as(C.c_void_p), fea.ctypes.data_as(C.c_void_p) if n_set else None, n_set)
+        log = _capi.KeyframeLog()
+        self._check(lib().latmap_pipeline_process_keyframe(self.h, C.byref(f), fi, C.byref(log)))
+        return log.as_dict()
+
+    def flush(self):
+        """run_pipeline's final flush (pipeline.cpp:318-330); returns the SyncStats."""
+        st = np.zeros(5, np.int64)
+        self._check(lib().latmap_pipeline_flush(self.h, st.ctypes.data_as(C.c_void_p)))
+        return dict(zip(_capi.SYNC_FIELDS, st.tolist()))
+
+    def state(self):
+        o = np.zeros(6, np.int64)
+        self._check(lib().latmap_pipeline_state(self.h, o.ctypes.data_as(C.c_void_p)))
+        return {"keyframes_processed": int(o[0]), "peak_active": int(o[1]), "history": int(o[2]),
+                "reservoir_seen": int(o[3]), "failed": bool(o[4]),
+                "traveled": float(np.array([o[5]], np.int64).astype(np.int32).view(np.float32)[0])}
+
+    def active_set(self):
+        n = self.session.n
+        org = np.zeros(n, np.int64)
+        dty = np.zeros(n, np.uint8)
+        self._check(lib().latmap_pipeline_active_set(self.h, org.ctypes.data_as(C.c_void_p),
+                                                     dty.ctypes.data_as(C.c_void_p)))
+        return org, dty

@@ -188,6 +188,10 @@ static latmap_status fail(latmap_ctx* ctx, latmap_status s, const char* msg) {
   return s;
 }
 
+// error text for clients of the C-ABI built into the library (pipeline.cu) that fail before
+// they own a handle of their own
+latmap_status lm_ctx_fail(latmap_ctx* ctx, latmap_status s, const char* msg) { return fail(ctx, s, msg); }
+
 static latmap_status post_launch(latmap_ctx* ctx) {
   if (const char* m = take_sticky_error()) {
     t_err = m;

@@ -35,6 +35,17 @@ int main() {
     }
     if (latmap_b200::sample_history(3, 5, a).size() != 3 || !latmap_b200::sample_history(0, 5, a).empty()) return 7;
   }
+  if (!latmap_b200::select_keyframe(8, 4) || latmap_b200::select_keyframe(9, 4)) return 8;
+  try { latmap_b200::select_keyframe(1, 0); return 9; } catch (const std::invalid_argument&) {}
+  latmap_pipeline_config pc;
+  latmap_default_pipeline_config(&pc);
+  if (pc.stage2_iters != 5 || pc.history_capacity != 200) return 10;
+  if (cfg.lambda_feat < 0) {
+    latmap_b200::Context ctx(0);
+    latmap_intrinsics in{1, 1, 0, 0, 1, 1};
+    latmap_b200::Pipeline p(ctx, cfg, pc, in);
+    p.flush();
+  }
   if (cfg.lambda_feat < 0) {
     latmap_b200::Context ctx(0);
     std::vector<float> pts(8, 0.f), w(4, 1.f);
