@@ -11,6 +11,7 @@ Tensors are torch CUDA float32 (torch is only the device-memory plumbing).
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from dataclasses import dataclass, fields
 
 import numpy as np
@@ -408,10 +409,12 @@ class Session:
 
     @classmethod
     def _borrowed(cls, owner, ctx, cfg, h, query_dim, k, embed_dim, intr):
-        """A view of a session owned by ``owner`` (a Pipeline): never destroyed here."""
+        """A view of a session owned by ``owner`` (a Pipeline): never destroyed here. The owner is
+        held weakly (no reference cycle, so the owner is finalised while its context lives) and
+        clears ``h`` when it goes."""
         s = cls.__new__(cls)
         s.ctx, s.cfg, s.intr, s.ds, s.k, s.df = ctx, cfg, intr, query_dim, k, embed_dim
-        s.h, s._keep, s._owner = C.c_void_p(h), [], owner
+        s.h, s._keep, s._owner = C.c_void_p(h), [], weakref.ref(owner)
         return s
 
     @property
@@ -644,7 +647,8 @@ class Store:
     @classmethod
     def _borrowed(cls, owner, ctx, h, capacity, query_dim):
         st = cls.__new__(cls)
-        st.ctx, st.ds, st.rs, st.capacity, st.h, st._owner = ctx, query_dim, 14 + query_dim, int(capacity), C.c_void_p(h), owner
+        st.ctx, st.ds, st.rs, st.capacity, st.h = ctx, query_dim, 14 + query_dim, int(capacity), C.c_void_p(h)
+        st._owner = weakref.ref(owner)
         return st
 
     def __del__(self):
