@@ -386,13 +386,28 @@ def main():
     s.set_batch(plan["global_batch"], add_trust=plan["add_trust"], slot_offset=plan["slot_offset"])
     grads = s.grad_buffer()
     parts = s.loss_buffer()
+    comm, collective = None, None
+    if world > 1:
+        # the exchange through the library's own NCCL communicator (latmap_session_allreduce);
+        # torch.distributed's all-reduce of the same buffers if NCCL cannot be loaded there
+        try:
+            uid = [api.Comm.unique_id(ctx) if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            comm = api.Comm(ctx, world, rank, uid[0])
+            collective = "latmap_session_allreduce (NCCL sum, one group)"
+        except Exception as e:  # noqa: BLE001
+            comm, collective = None, f"torch.distributed.all_reduce (library comm unavailable: {e})"
+        config["collective"] = collective
 
     def one_step(read=False):
         if world == 1:
             return s.step(read=read)
         s.objective(want_grad=True, read=False)
-        dist.all_reduce(grads)
-        dist.all_reduce(parts)
+        if comm is not None:
+            comm.session_allreduce(s)
+        else:
+            dist.all_reduce(grads)
+            dist.all_reduce(parts)
         s.apply()
         return s.read_loss() if read else None
 

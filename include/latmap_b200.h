@@ -359,6 +359,23 @@ latmap_status latmap_query_map(latmap_ctx* ctx, const float* features, int64_t n
                                const float* proj, int64_t k, int32_t df, float temperature, const float* embedding,
                                float* scores);
 
+/* ---------------------------------------------------------------- multi-GPU (NCCL) */
+/* one process per GPU, keyframes sharded across ranks, one sum all-reduce of
+ * the gradients and loss partials per iteration. NCCL is loaded at run time (libnccl.so.2);
+ * without it these return LATMAP_ERR_UNSUPPORTED. */
+typedef struct latmap_comm latmap_comm;
+/* ncclGetUniqueId on rank 0; the caller hands the 128 bytes to every rank (any channel). */
+latmap_status latmap_comm_unique_id(latmap_ctx* ctx, uint8_t id[128]);
+/* ncclCommInitRank on the context's device; collectives run on the context's stream. */
+latmap_status latmap_comm_init(latmap_ctx* ctx, int32_t nranks, int32_t rank, const uint8_t id[128],
+                               latmap_comm** out);
+latmap_status latmap_comm_destroy(latmap_comm* comm);
+/* In-place sum all-reduce of a device buffer; dtype 0 = fp32, 1 = fp64. */
+latmap_status latmap_comm_allreduce(latmap_comm* comm, void* buf, int64_t count, int32_t dtype);
+/* The sharded iteration's exchange: the session's flat gradient buffer and loss partials summed
+ * over ranks (one NCCL group), between latmap_session_objective and latmap_session_apply. */
+latmap_status latmap_session_allreduce(latmap_session* s, latmap_comm* comm);
+
 /* ---------------------------------------------------------------- pipeline (the step's caller) */
 /* The pipeline-level subset of latmap::Config (core/config.hpp:10-58; same defaults via
  * latmap_default_pipeline_config). dict_init: 0 = "kmeans", 1 = "random". The objective's own

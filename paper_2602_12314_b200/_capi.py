@@ -179,6 +179,11 @@ def _declare(L):
         "latmap_store_get_records": [P, C.c_int64, C.c_int64, P, P],
         "latmap_store_insert_global": [P, P, C.c_int64, C.c_float, C.POINTER(C.c_int64)],
         "latmap_store_insert_keyed": [P, P, P, C.c_int64, C.POINTER(C.c_int64)],
+        "latmap_comm_unique_id": [P, P],
+        "latmap_comm_init": [P, C.c_int32, C.c_int32, P, C.POINTER(P)],
+        "latmap_comm_destroy": [P],
+        "latmap_comm_allreduce": [P, P, C.c_int64, C.c_int32],
+        "latmap_session_allreduce": [P, P],
         "latmap_pipeline_create": [P, C.POINTER(Config), C.POINTER(PipelineConfig), C.POINTER(Intrinsics),
                                    C.POINTER(P)],
         "latmap_pipeline_destroy": [P],
@@ -257,7 +262,8 @@ EXPORTED = ["latmap_ctx_create", "latmap_ctx_destroy", "latmap_ctx_set_stream", 
             "latmap_default_pipeline_config", "latmap_select_keyframe", "latmap_pipeline_create",
             "latmap_pipeline_destroy", "latmap_pipeline_process_keyframe", "latmap_pipeline_flush",
             "latmap_pipeline_session", "latmap_pipeline_store", "latmap_pipeline_state", "latmap_pipeline_active_set",
-            "latmap_pipeline_last_error"]
+            "latmap_pipeline_last_error", "latmap_comm_unique_id", "latmap_comm_init",
+            "latmap_comm_destroy", "latmap_comm_allreduce", "latmap_session_allreduce"]
 
 
 def check(ctx_handle, status):

@@ -840,3 +840,39 @@ class Pipeline:
         self._check(lib().latmap_pipeline_active_set(self.h, org.ctypes.data_as(C.c_void_p),
                                                      dty.ctypes.data_as(C.c_void_p)))
         return org, dty
+
+
+class Comm:
+    """NCCL communicator of the sharded step (latmap_comm_*): rank 0 makes the unique id, the
+    caller distributes it (any channel), every rank joins with its rank."""
+
+    def __init__(self, ctx: Context, nranks, rank, uid: bytes):
+        if len(uid) != 128:
+            raise _capi.InvalidArgument("comm: unique id must be 128 bytes")
+        self.ctx, self.nranks, self.rank = ctx, int(nranks), int(rank)
+        h = C.c_void_p()
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        check(ctx.h, lib().latmap_comm_init(ctx.h, self.nranks, self.rank, buf, C.byref(h)))
+        self.h = h
+
+    @staticmethod
+    def unique_id(ctx: Context) -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(ctx.h, lib().latmap_comm_unique_id(ctx.h, buf))
+        return bytes(buf)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().latmap_comm_destroy(self.h)
+            self.h = None
+
+    def allreduce(self, t: torch.Tensor):
+        """In-place sum over ranks of a contiguous fp32 / fp64 CUDA tensor (context stream)."""
+        if t.dtype not in (torch.float32, torch.float64) or not t.is_contiguous():
+            raise _capi.InvalidArgument("comm.allreduce: contiguous fp32 or fp64 tensor expected")
+        check(self.ctx.h, lib().latmap_comm_allreduce(self.h, C.c_void_p(t.data_ptr()), t.numel(),
+                                                      0 if t.dtype == torch.float32 else 1))
+
+    def session_allreduce(self, s: Session):
+        """The sharded iteration's exchange: gradients and loss partials summed over ranks."""
+        check(self.ctx.h, lib().latmap_session_allreduce(s.h, self.h))
