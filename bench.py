@@ -207,6 +207,60 @@ def cpu_reference(cfg_id, samples, budget_s=150.0, threads=None):
 
 
 # ----------------------------------------------------------------------------- config 3
+def host_link_gbps(nbytes=256 << 20, reps=5):
+    """Pinned cudaMemcpyAsync bandwidth H2D / D2H on this box (the PCIe roofline of the store's
+    record transfers)."""
+    import torch
+
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    out = {}
+    for name, dst, src in (("h2d", d, h), ("d2h", h, d)):
+        dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            dst.copy_(src, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        out[name] = reps * nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    return out
+
+
+def streaming_hash_pass(store, st, stats, sync_ms, hbm_peak):
+    """The store's share of a config-3 frame (SURVEY.md §8(d) "Hash pass (K11)"): the device
+    radius scan over every stored position against HBM, and the record traffic of sync (184 B per
+    record written back or fetched) against the measured host link. Measured after the timed
+    region."""
+    import torch
+
+    rec_bytes = 4 * (14 + 32)
+    n = store.size()
+    c = np.asarray(st.poses[-1][1], np.float32)
+    store.fetch_local(c, st.radius)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(5):
+        store.fetch_local(c, st.radius)
+    scan_ms = (time.perf_counter() - t0) * 1000.0 / 5
+    moved = [x["written_back"] + x["newborn_inserted"] + x["fetched"] for x in stats[-len(sync_ms):]]
+    link = host_link_gbps()
+    per_frame = float(np.mean(moved)) * rec_bytes if moved else 0.0
+    sync_mean = float(np.mean(sync_ms)) if sync_ms else 0.0
+    return {"records_scanned": n, "scan_bytes": 12 * n,
+            "fetch_local_ms": scan_ms,
+            "scan_gbps": 12 * n / (scan_ms * 1e-3) / 1e9,
+            "scan_frac_hbm": 12 * n / (scan_ms * 1e-3) / 1e9 / hbm_peak,
+            "scan_note": "fetch_local wall time incl. launch, compaction and the index-list D2H",
+            "record_bytes_per_frame": per_frame, "sync_ms_per_frame": sync_mean,
+            "sync_share_of_frame": None,
+            "transfer_gbps": per_frame / (sync_mean * 1e-3) / 1e9 if sync_mean else None,
+            "transfer_note": "sync_ms covers the sync call; the written-back rows reach the pinned pool over PCIe "
+                             "afterwards on the store's writeback stream, overlapping the frame's iterations",
+            "host_link_gbps": link}
+
+
 def run_streaming(args, hbm_peak):
     """Config 3: per frame one store sync (writeback of the optimised active set into the pinned
     host pool, prune by radius, fetch the newly active records; active_set.cpp:38-128) then 10
@@ -247,15 +301,17 @@ def run_streaming(args, hbm_peak):
     s = api.Session(ctx, cfg, 0, 32, st.atoms.shape[0], st.atoms.shape[1], intr)
     s.set_dictionary(st.atoms, st.atoms, st.proj)
     origin = np.zeros(0, np.int64)
-    stats_all, active, vis_all, pairs_all = [], [], [], []
+    stats_all, active, vis_all, pairs_all, sync_ms = [], [], [], [], []
 
     def one_frame(f):
         nonlocal origin
         q, t = st.poses[f]
+        ts = time.perf_counter()
         rows = s.export_rows() if s.n else None
         d_out, origin_new, kept, stats = store.sync(rows, origin, np.ones(len(origin), np.uint8),
                                                     np.asarray(t, np.float32), st.radius, st.voxel_size)
         s.import_rows(d_out.contiguous(), kept=kept if len(origin) else None)
+        sync_ms.append((time.perf_counter() - ts) * 1000.0)  # host clock: sync returns host results
         origin = origin_new
         s.set_frames([frames[f]])
         s.set_batch(1)
@@ -287,6 +343,8 @@ def run_streaming(args, hbm_peak):
     last = s.read_loss()
     iters = args.steps * st.iters_per_frame
     moved = sum(x["fetched"] + x["written_back"] for x in stats_all)
+    hash_pass = streaming_hash_pass(store, st, stats_all, sync_ms[args.warmup:], hbm_peak)
+    hash_pass["sync_share_of_frame"] = sum(sync_ms[args.warmup:]) / ms if ms else None
     line = {"metric": METRIC, "value": 1000.0 * iters / ms, "unit": "iters/s", "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "replicas only",
             "vs_baseline": None, "dtype": "f32 render/grads, bf16 tcgen05 decoder (fp32 accum)",
@@ -299,7 +357,8 @@ def run_streaming(args, hbm_peak):
             "frames_per_s": 1000.0 * args.steps / ms, "active_mean": float(np.mean(active)),
             "visible_per_frame": float(np.mean(vis_all)), "tile_pairs_per_frame": float(np.mean(pairs_all)),
             "records_moved_per_frame": moved / max(1, args.steps),
-            "sync_stats_last": stats_all[-1] if stats_all else None, "gpu_launches": int(ctx.launches() - launches0),
+            "sync_stats_last": stats_all[-1] if stats_all else None, "hash_pass": hash_pass,
+            "gpu_launches": int(ctx.launches() - launches0),
             "clocks": clocks, "loss_last": last["total"], "setup_s": gen_s}
     print(json.dumps(line))
 

@@ -103,7 +103,10 @@ class Context:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().latmap_ctx_destroy(self.h)
+            try:
+                lib().latmap_ctx_destroy(self.h)
+            except TypeError:  # interpreter shutdown: the library handle is already gone
+                pass
             self.h = None
 
     def sync(self):
@@ -148,7 +151,10 @@ class RenderOutput:
 
     def __del__(self):
         if getattr(self, "_cache", None):
-            lib().latmap_render_cache_destroy(self._cache)
+            try:
+                lib().latmap_render_cache_destroy(self._cache)
+            except TypeError:  # interpreter shutdown: the library handle is already gone
+                pass
             self._cache = None
 
     def splats(self):
@@ -423,7 +429,10 @@ class Session:
 
     def __del__(self):
         if getattr(self, "h", None) and getattr(self, "_owner", None) is None:
-            lib().latmap_session_destroy(self.h)
+            try:
+                lib().latmap_session_destroy(self.h)
+            except TypeError:  # interpreter shutdown: the library handle is already gone
+                pass
         self.h = None
 
     @staticmethod
@@ -653,7 +662,10 @@ class Store:
 
     def __del__(self):
         if getattr(self, "h", None) and getattr(self, "_owner", None) is None:
-            lib().latmap_store_destroy(self.h)
+            try:
+                lib().latmap_store_destroy(self.h)
+            except TypeError:  # interpreter shutdown: the library handle is already gone
+                pass
         self.h = None
 
     def _check(self, st):
@@ -788,7 +800,10 @@ class Pipeline:
             for v in ("session", "store"):
                 if getattr(self, v, None) is not None:
                     getattr(self, v).h = None
-            lib().latmap_pipeline_destroy(self.h)
+            try:
+                lib().latmap_pipeline_destroy(self.h)
+            except TypeError:  # interpreter shutdown: the library handle is already gone
+                pass
             self.h = None
 
     def _check(self, st):
@@ -863,7 +878,10 @@ class Comm:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().latmap_comm_destroy(self.h)
+            try:
+                lib().latmap_comm_destroy(self.h)
+            except TypeError:  # interpreter shutdown: the library handle is already gone
+                pass
             self.h = None
 
     def allreduce(self, t: torch.Tensor):

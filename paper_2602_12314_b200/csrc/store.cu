@@ -12,6 +12,10 @@
 // order, no FMA) over the whole pool mirror with an order-preserving compaction, and the
 // gather reads the selected records from mapped host memory straight into device buffers;
 // the writeback scatter writes device records back into the pinned pool.
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -126,13 +130,26 @@ __global__ void gather_kernel(const float* __restrict__ pool, const int64_t* __r
     out[e] = pool[idx[r] * rs + c];
   }
 }
-__global__ void scatter_rec_kernel(float* __restrict__ pool, float* __restrict__ pos_mirror,
-                                   const int64_t* __restrict__ idx, int64_t n, int rs, const float* __restrict__ in) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * rs; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e / rs, c = e % rs;
-    const float v = in[e];
-    pool[idx[r] * rs + c] = v;
-    if (c < 3) pos_mirror[idx[r] * 3 + c] = v;
+// rows -> their records in the mapped host pool, 8 bytes per store when rows are 8-byte aligned
+// (even rs), else 4
+__global__ void scatter_rec_kernel(float* __restrict__ pool, const int64_t* __restrict__ idx, int64_t n, int rs,
+                                   const float* __restrict__ in) {
+  if (rs & 1) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * rs; e += (int64_t)gridDim.x * blockDim.x)
+      pool[idx[e / rs] * rs + e % rs] = in[e];
+    return;
+  }
+  const int h = rs / 2;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * h; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / h, c = e % h;
+    reinterpret_cast<float2*>(pool + idx[r] * rs)[c] = reinterpret_cast<const float2*>(in + r * rs)[c];
+  }
+}
+__global__ void pos_scatter_kernel(float* __restrict__ pos_mirror, const int64_t* __restrict__ idx, int64_t n, int rs,
+                                   const float* __restrict__ in) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * 3; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / 3, c = e % 3;
+    pos_mirror[idx[r] * 3 + c] = in[r * rs + c];
   }
 }
 // prune test for the active entries + present flags of the kept records
@@ -181,6 +198,11 @@ struct latmap_store {
   int64_t stats[5] = {0, 0, 0, 0, 0};
   float* d_pos = nullptr;  // device mirror of record positions
   int64_t d_pos_cap = 0;
+  // sync's writeback into the pinned pool runs on its own stream, overlapping the rest of the
+  // frame; every later access to the pool waits for it (wb_wait)
+  cudaStream_t wb_st = nullptr;
+  cudaEvent_t wb_ev = nullptr;
+  bool wb_pending = false;
   // scratch
   std::string err;
 };
@@ -197,8 +219,16 @@ latmap_status sfail(latmap_store* s, latmap_status code, const std::string& msg)
     if (_e != cudaSuccess) return sfail(s, LATMAP_ERR_CUDA, cudaGetErrorString(_e));  \
   } while (0)
 
+void wb_wait(const latmap_store* s) {
+  if (s->wb_pending) {
+    cudaEventSynchronize(s->wb_ev);
+    const_cast<latmap_store*>(s)->wb_pending = false;
+  }
+}
+
 latmap_status ensure_pool(latmap_store* s, int64_t need) {
   if (need <= s->pool_cap) return LATMAP_OK;
+  wb_wait(s);  // no writeback may target the pool being replaced
   int64_t cap = std::max<int64_t>(need, std::max<int64_t>(1024, s->pool_cap * 2));
   float* np = nullptr;
   S_CHECK(s, cudaHostAlloc(&np, sizeof(float) * cap * s->rs, cudaHostAllocMapped));
@@ -280,6 +310,11 @@ latmap_status latmap_store_create(latmap_ctx* ctx, int64_t capacity, int32_t que
   s->ds = query_dim;
   s->rs = 14 + query_dim;
   s->slots.resize((size_t)capacity);
+  if (cudaStreamCreateWithFlags(&s->wb_st, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&s->wb_ev, cudaEventDisableTiming) != cudaSuccess) {
+    delete s;
+    return LATMAP_ERR_CUDA;
+  }
   *out = s;
   return LATMAP_OK;
 }
@@ -289,6 +324,8 @@ latmap_status latmap_store_destroy(latmap_store* s) {
   cudaDeviceSynchronize();
   if (s->pool) cudaFreeHost(s->pool);
   if (s->d_pos) cudaFree(s->d_pos);
+  if (s->wb_ev) cudaEventDestroy(s->wb_ev);
+  if (s->wb_st) cudaStreamDestroy(s->wb_st);
   delete s;
   return LATMAP_OK;
 }
@@ -313,6 +350,7 @@ int64_t latmap_store_insert(latmap_store* s, const int32_t key[3], const float* 
 
 int32_t latmap_store_update(latmap_store* s, const int32_t key[3], const float* rec) {
   if (!s || !rec) return 0;
+  wb_wait(s);
   const int64_t hit = probe(s, key, lm::hash_voxel(key, s->capacity), false, nullptr);
   if (hit < 0) return 0;
   const int64_t r = s->slots[hit].record;
@@ -332,6 +370,7 @@ int64_t latmap_store_find(latmap_store* s, const int32_t key[3]) {
 latmap_status latmap_store_get_records(const latmap_store* s, int64_t first, int64_t count, float* out,
                                        int32_t* keys_out) {
   if (!s || first < 0 || first + count > s->size) return LATMAP_ERR_INVALID_ARGUMENT;
+  wb_wait(s);
   cudaStreamSynchronize(s->st);
   if (out) std::memcpy(out, s->pool + first * s->rs, sizeof(float) * count * s->rs);
   if (keys_out) std::memcpy(keys_out, s->keys.data() + first * 3, sizeof(int32_t) * count * 3);
@@ -407,6 +446,7 @@ latmap_status latmap_store_fetch_local(latmap_store* s, const float center[3], f
                                        int64_t cap, int64_t* count, float* d_records) {
   if (!s || !count) return LATMAP_ERR_INVALID_ARGUMENT;
   if (!(radius > 0.f)) return sfail(s, LATMAP_ERR_INVALID_ARGUMENT, "fetch_local: radius must be > 0");
+  wb_wait(s);
   *count = 0;
   if (s->size == 0) return LATMAP_OK;
   const float r2 = radius * radius;
@@ -457,10 +497,23 @@ latmap_status latmap_store_sync(latmap_store* s, const float* d_active, const in
   if (!(voxel_size > 0.f)) return sfail(s, LATMAP_ERR_INVALID_ARGUMENT, "voxel_of: voxel_size must be > 0");
   const int rs = s->rs;
   int64_t st5[5] = {0, 0, 0, 0, 0};
+  wb_wait(s);  // the previous sync's writeback
+  // LATMAP_SYNC_TRACE=1: per-step wall times (each step synchronised; development only)
+  static const bool trace = std::getenv("LATMAP_SYNC_TRACE") != nullptr;
+  auto tmark = [&, t0 = std::chrono::steady_clock::now()](const char* what) mutable {
+    if (!trace) return;
+    cudaStreamSynchronize(s->st);
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "sync %-10s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
   std::vector<int64_t> resolved((size_t)std::max<int64_t>(n, 1), -1);
   // ---- step 1: writeback. Dirty tracked entries overwrite their record in place (origin voxel
   // retained); newborns insert under the voxel of their optimised position, in row order.
   std::vector<int64_t> wb_rows, wb_idx, nb_rows;
+  float* wb_tmp = nullptr;
+  int64_t* wb_idx_dev = nullptr;
+  int64_t wb_n = 0;
   for (int64_t i = 0; i < n; ++i) {
     if (origin[i] >= 0) {
       resolved[i] = origin[i];
@@ -482,13 +535,16 @@ latmap_status latmap_store_sync(latmap_store* s, const float* d_active, const in
     S_CHECK(s, cudaMemcpyAsync(d_rows, wb_rows.data(), sizeof(int64_t) * nwb, cudaMemcpyHostToDevice, s->st));
     S_CHECK(s, cudaMemcpyAsync(d_idx2, wb_idx.data(), sizeof(int64_t) * nwb, cudaMemcpyHostToDevice, s->st));
     copy_rows_kernel<<<grid_of(nwb * rs), 256, 0, s->st>>>(d_active, d_rows, nwb, rs, d_tmp);
-    scatter_rec_kernel<<<grid_of(nwb * rs), 256, 0, s->st>>>(s->pool_dev, s->d_pos, d_idx2, nwb, rs, d_tmp);
+    // the position mirror now (the radius scan below reads it); the pool rows over PCIe on the
+    // writeback stream, overlapping everything after this sync (the rows fetched below are never
+    // written back ones: those are present or pruned)
+    pos_scatter_kernel<<<grid_of(nwb * 3), 256, 0, s->st>>>(s->d_pos, d_idx2, nwb, rs, d_tmp);
     count_launch(2);
-    S_CHECK(s, cudaFreeAsync(d_tmp, s->st));
     S_CHECK(s, cudaFreeAsync(d_rows, s->st));
-    S_CHECK(s, cudaFreeAsync(d_idx2, s->st));
+    wb_tmp = d_tmp, wb_idx_dev = d_idx2, wb_n = nwb;  // pool rows: launched when this sync is done
     st5[0] = nwb;
   }
+  tmark("writeback");
   const int64_t nnb = (int64_t)nb_rows.size();
   if (nnb > 0) {
     float* d_nb = nullptr;
@@ -530,6 +586,7 @@ latmap_status latmap_store_sync(latmap_store* s, const float* d_active, const in
     S_CHECK(s, cudaFreeAsync(d_home, s->st));
     S_CHECK(s, cudaFreeAsync(d_rows, s->st));
   }
+  tmark("newborns");
   // ---- step 2: prune in-radius tracked entries, mark their records present
   const float r2 = radius * radius;
   uint8_t* d_present = nullptr;
@@ -547,6 +604,7 @@ latmap_status latmap_store_sync(latmap_store* s, const float* d_active, const in
     count_launch();
     S_CHECK(s, cudaMemcpyAsync(kept.data(), d_kept, n, cudaMemcpyDeviceToHost, s->st));
   }
+  tmark("prune");
   // ---- step 3: fetch not-present in-radius records in ascending index order
   const int64_t nb = std::max<int64_t>(1, (s->size + kScanBlock - 1) / kScanBlock);
   int32_t* d_cnt = nullptr;
@@ -566,6 +624,7 @@ latmap_status latmap_store_sync(latmap_store* s, const float* d_active, const in
     S_CHECK(s, cudaMemcpyAsync(&fetched, d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, s->st));
   }
   S_CHECK(s, cudaStreamSynchronize(s->st));
+  tmark("scan");
   std::vector<int64_t> keep_rows;
   for (int64_t i = 0; i < n; ++i) {
     if (resolved[i] < 0) continue;  // rejected newborn drops out
@@ -604,6 +663,7 @@ latmap_status latmap_store_sync(latmap_store* s, const float* d_active, const in
                                    s->st));
     }
   }
+  tmark("assemble");
   S_CHECK(s, cudaFreeAsync(d_present, s->st));
   if (d_kept) S_CHECK(s, cudaFreeAsync(d_kept, s->st));
   if (d_res) S_CHECK(s, cudaFreeAsync(d_res, s->st));
@@ -611,6 +671,19 @@ latmap_status latmap_store_sync(latmap_store* s, const float* d_active, const in
   S_CHECK(s, cudaFreeAsync(d_total, s->st));
   S_CHECK(s, cudaFreeAsync(d_fetch, s->st));
   S_CHECK(s, cudaStreamSynchronize(s->st));
+  if (wb_n > 0) {
+    // the written-back rows reach the pinned pool over PCIe after this sync's own transfers (which
+    // would otherwise queue behind ~184 B x rows of posted writes), overlapping the caller's next
+    // work; the rows fetched above were never written back ones (those are present or pruned)
+    S_CHECK(s, cudaEventRecord(s->wb_ev, s->st));
+    S_CHECK(s, cudaStreamWaitEvent(s->wb_st, s->wb_ev, 0));
+    scatter_rec_kernel<<<grid_of(wb_n * rs / 2), 256, 0, s->wb_st>>>(s->pool_dev, wb_idx_dev, wb_n, rs, wb_tmp);
+    count_launch();
+    S_CHECK(s, cudaFreeAsync(wb_tmp, s->wb_st));
+    S_CHECK(s, cudaFreeAsync(wb_idx_dev, s->wb_st));
+    S_CHECK(s, cudaEventRecord(s->wb_ev, s->wb_st));
+    s->wb_pending = true;
+  }
   return ret;
 }
 
