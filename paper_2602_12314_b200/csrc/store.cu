@@ -203,6 +203,9 @@ struct latmap_store {
   cudaStream_t wb_st = nullptr;
   cudaEvent_t wb_ev = nullptr;
   bool wb_pending = false;
+  // pinned staging for sync's index lists (async uploads, no pageable staging copies)
+  int64_t* h_stage = nullptr;
+  int64_t h_stage_cap = 0;
   // scratch
   std::string err;
 };
@@ -325,6 +328,7 @@ latmap_status latmap_store_destroy(latmap_store* s) {
   if (s->pool) cudaFreeHost(s->pool);
   if (s->d_pos) cudaFree(s->d_pos);
   if (s->wb_ev) cudaEventDestroy(s->wb_ev);
+  if (s->h_stage) cudaFreeHost(s->h_stage);
   if (s->wb_st) cudaStreamDestroy(s->wb_st);
   delete s;
   return LATMAP_OK;
@@ -507,10 +511,23 @@ latmap_status latmap_store_sync(latmap_store* s, const float* d_active, const in
     std::fprintf(stderr, "sync %-10s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
     t0 = t1;
   };
-  std::vector<int64_t> resolved((size_t)std::max<int64_t>(n, 1), -1);
+  const int64_t nn = std::max<int64_t>(n, 1);
+  if (s->h_stage_cap < 4 * nn) {  // the previous sync ended with a stream synchronize: free to replace
+    if (s->h_stage) cudaFreeHost(s->h_stage);
+    s->h_stage = nullptr;
+    s->h_stage_cap = 0;
+    S_CHECK(s, cudaHostAlloc(&s->h_stage, sizeof(int64_t) * 4 * nn + sizeof(int64_t) * 4 * (nn / 4), 0));
+    s->h_stage_cap = 4 * nn + 4 * (nn / 4);
+  }
+  int64_t* resolved = s->h_stage;            // n entries
+  int64_t* wb_rows = s->h_stage + nn;        // <= n
+  int64_t* wb_idx = s->h_stage + 2 * nn;     // <= n
+  int64_t* keep_rows = s->h_stage + 3 * nn;  // <= n
+  std::fill(resolved, resolved + nn, int64_t(-1));
+  int64_t nwb = 0;
   // ---- step 1: writeback. Dirty tracked entries overwrite their record in place (origin voxel
   // retained); newborns insert under the voxel of their optimised position, in row order.
-  std::vector<int64_t> wb_rows, wb_idx, nb_rows;
+  std::vector<int64_t> nb_rows;
   float* wb_tmp = nullptr;
   int64_t* wb_idx_dev = nullptr;
   int64_t wb_n = 0;
@@ -518,22 +535,21 @@ latmap_status latmap_store_sync(latmap_store* s, const float* d_active, const in
     if (origin[i] >= 0) {
       resolved[i] = origin[i];
       if (dirty[i]) {
-        wb_rows.push_back(i);
-        wb_idx.push_back(origin[i]);
+        wb_rows[nwb] = i;
+        wb_idx[nwb++] = origin[i];
       }
     } else {
       nb_rows.push_back(i);
     }
   }
   int64_t *d_rows = nullptr, *d_idx2 = nullptr;
-  const int64_t nwb = (int64_t)wb_rows.size();
   if (nwb > 0) {
     float* d_tmp = nullptr;
     S_CHECK(s, cudaMallocAsync(&d_rows, sizeof(int64_t) * nwb, s->st));
     S_CHECK(s, cudaMallocAsync(&d_idx2, sizeof(int64_t) * nwb, s->st));
     S_CHECK(s, cudaMallocAsync(&d_tmp, sizeof(float) * nwb * rs, s->st));
-    S_CHECK(s, cudaMemcpyAsync(d_rows, wb_rows.data(), sizeof(int64_t) * nwb, cudaMemcpyHostToDevice, s->st));
-    S_CHECK(s, cudaMemcpyAsync(d_idx2, wb_idx.data(), sizeof(int64_t) * nwb, cudaMemcpyHostToDevice, s->st));
+    S_CHECK(s, cudaMemcpyAsync(d_rows, wb_rows, sizeof(int64_t) * nwb, cudaMemcpyHostToDevice, s->st));
+    S_CHECK(s, cudaMemcpyAsync(d_idx2, wb_idx, sizeof(int64_t) * nwb, cudaMemcpyHostToDevice, s->st));
     copy_rows_kernel<<<grid_of(nwb * rs), 256, 0, s->st>>>(d_active, d_rows, nwb, rs, d_tmp);
     // the position mirror now (the radius scan below reads it); the pool rows over PCIe on the
     // writeback stream, overlapping everything after this sync (the rows fetched below are never
@@ -598,7 +614,7 @@ latmap_status latmap_store_sync(latmap_store* s, const float* d_active, const in
   if (n > 0) {
     S_CHECK(s, cudaMallocAsync(&d_kept, n, s->st));
     S_CHECK(s, cudaMallocAsync(&d_res, sizeof(int64_t) * n, s->st));
-    S_CHECK(s, cudaMemcpyAsync(d_res, resolved.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, s->st));
+    S_CHECK(s, cudaMemcpyAsync(d_res, resolved, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s->st));
     prune_kernel<<<grid_of(n), 256, 0, s->st>>>(d_active, d_res, n, rs, center[0], center[1], center[2], r2, d_kept,
                                                 d_present);
     count_launch();
@@ -625,16 +641,16 @@ latmap_status latmap_store_sync(latmap_store* s, const float* d_active, const in
   }
   S_CHECK(s, cudaStreamSynchronize(s->st));
   tmark("scan");
-  std::vector<int64_t> keep_rows;
+  int64_t nk = 0;
   for (int64_t i = 0; i < n; ++i) {
     if (resolved[i] < 0) continue;  // rejected newborn drops out
     if (kept[i])
-      keep_rows.push_back(i);
+      keep_rows[nk++] = i;
     else
       ++st5[3];
   }
   st5[4] = fetched;
-  const int64_t total = (int64_t)keep_rows.size() + fetched;
+  const int64_t total = nk + fetched;
   *out_count = total;
   if (kept_mask)
     for (int64_t i = 0; i < n; ++i) kept_mask[i] = kept[i];
@@ -644,11 +660,10 @@ latmap_status latmap_store_sync(latmap_store* s, const float* d_active, const in
     ret = sfail(s, LATMAP_ERR_INVALID_ARGUMENT, "sync: output capacity too small");
   } else {
     // ---- assemble: kept (original order) ++ fetched (ascending)
-    const int64_t nk = (int64_t)keep_rows.size();
     if (nk > 0) {
       int64_t* d_k = nullptr;
       S_CHECK(s, cudaMallocAsync(&d_k, sizeof(int64_t) * nk, s->st));
-      S_CHECK(s, cudaMemcpyAsync(d_k, keep_rows.data(), sizeof(int64_t) * nk, cudaMemcpyHostToDevice, s->st));
+      S_CHECK(s, cudaMemcpyAsync(d_k, keep_rows, sizeof(int64_t) * nk, cudaMemcpyHostToDevice, s->st));
       copy_rows_kernel<<<grid_of(nk * rs), 256, 0, s->st>>>(d_active, d_k, nk, rs, d_out);
       count_launch();
       S_CHECK(s, cudaFreeAsync(d_k, s->st));
