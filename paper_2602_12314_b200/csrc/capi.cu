@@ -1769,7 +1769,14 @@ latmap_status latmap_session_seed_candidates(latmap_session* s, int32_t b, float
   cudaStream_t st = ctx->stream;
   const FrameDev& f = s->frames[b];
   if (!s->renders_valid) {  // render(active map, kf.pose) right before seeding (pipeline.cpp:224-226)
-    latmap_status rs = latmap_session_objective_ex(s, 0, 0, 0, nullptr);
+    // frames 0..b only (the history frames behind b are not needed here); with a loss read-back
+    // so a tile-list overflow is recovered before the candidates are taken
+    const int32_t nf = s->nframes;
+    s->nframes = b + 1;
+    latmap_loss_breakdown tmp{};
+    latmap_status rs = latmap_session_objective_ex(s, 0, 0, 0, &tmp);
+    s->nframes = nf;
+    s->renders_valid = false;  // frames after b were not rendered
     if (rs != LATMAP_OK) return rs;
   }
   wait_frame(s, b, st);
