@@ -363,6 +363,36 @@ def run_streaming(args, hbm_peak):
     print(json.dumps(line))
 
 
+# ----------------------------------------------------------------------------- launch
+def relaunch(args):
+    """`bench.py --gpus N` started as one process: re-exec under torch.distributed.run with one
+    rank per GPU (127.0.0.1 rendezvous), NCCL's INFO lines on stderr. N is capped at the visible
+    GPU count; the JSON line's n_gpus is the number of ranks that actually ran."""
+    import socket
+
+    import torch
+
+    avail = torch.cuda.device_count()
+    n = min(args.gpus, avail) if avail > 0 else 1
+    if n < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} requested, {avail} visible: running {n} rank(s)", file=sys.stderr)
+    argv = [a for a in sys.argv[1:]]
+    if n == 1:
+        os.environ["WORLD_SIZE"] = "1"
+        return main()
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + argv
+    rc = subprocess.call(cmd, env=env)
+    if rc != 0:
+        sys.exit(rc)
+
+
 # ----------------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
@@ -377,6 +407,8 @@ def main():
                     help="bf16 decoder kernels: 0 auto, 1 fused on-chip, 2 staged (experiments)")
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        return relaunch(args)
     if args.config == 3 and args.impl == "ours":
         return run_streaming(args, peaks()[0])
     rank = int(os.environ.get("RANK", "0"))
@@ -458,17 +490,17 @@ def main():
             comm, collective = None, f"torch.distributed.all_reduce (library comm unavailable: {e})"
         config["collective"] = collective
 
-    def one_step(read=False):
-        if world == 1:
-            return s.step(read=read)
-        s.objective(want_grad=True, read=False)
+    def exchange(sess):
         if comm is not None:
-            comm.session_allreduce(s)
+            comm.session_allreduce(sess)
         else:
             dist.all_reduce(grads)
             dist.all_reduce(parts)
-        s.apply()
-        return s.read_loss() if read else None
+
+    def one_step(read=False):
+        if world == 1:
+            return s.step(read=read)
+        return s.sharded_step(exchange, read=read)
 
     stream = torch.cuda.current_stream()
     first = one_step(read=True)  # sizes the tile buffers
@@ -481,6 +513,7 @@ def main():
     sampler.start()
     time.sleep(0.25)
     launches0 = ctx.launches()
+    overflow0 = s.overflow_steps()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -494,6 +527,9 @@ def main():
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
     launches = ctx.launches() - launches0
+    # sticky device count of steps whose Adam was skipped for a tile-list overflow (any rank) during
+    # the timed loop, which reads no losses: 0 means every timed step was whole
+    overflowed = s.overflow_steps() - overflow0
     clocks = sampler.stop()
     if dist:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
@@ -584,6 +620,7 @@ def main():
             "dtype": "f32" if cfg.decoder_precision == 0 else "f32 render/grads, bf16 tcgen05 decoder (fp32 accum)",
             "data": "synthetic (seeded BASELINE config; targets rendered from a perturbed map)",
             "config": config, "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
+            "overflowed_steps": int(overflowed),
             "phases": {k: round(v["ms_per_launch"], 4) for k, v in per_launch.items()},
             "phase_share": {k: round(v["share"], 4) for k, v in per_launch.items()},
             "visible_per_frame": float(np.mean(vis)), "tile_pairs_per_frame": float(np.mean(pairs)),

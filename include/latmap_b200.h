@@ -256,11 +256,41 @@ latmap_status latmap_session_append_rows(latmap_session* s, float* d_rows, int64
 /* Flat device buffers: [positions|rotations|colors|log_scales|opacity|features|proj|atoms]
  * gradient layout (for the multi-GPU all-reduce) and the loss-partials vector. */
 latmap_status latmap_session_grad_buffer(latmap_session* s, float** grads, int64_t* count);
+/* Element offset and length of each of the 8 blocks in that flat buffer (positions, rotations,
+ * colors, log_scales, opacity, features, proj, atoms); every block starts on a 16-byte boundary,
+ * so offsets are not the running sum of lengths when a length is not a multiple of 4. */
+latmap_status latmap_session_grad_layout(latmap_session* s, int64_t offsets[8], int64_t lengths[8]);
 latmap_status latmap_session_loss_buffer(latmap_session* s, double** partials, int64_t* count);
 latmap_status latmap_session_read_loss(latmap_session* s, latmap_loss_breakdown* out);
 /* Per-frame render outputs of the last objective (device pointers; parity and Stage-II reuse). */
 latmap_status latmap_session_frame_images(latmap_session* s, int32_t frame, float** color, float** depth,
                                           float** query, float** alpha);
+/* Host-only (no device): the LossBreakdown of a batch from its loss-partials vector (the layout
+ * latmap_session_loss_buffer exposes: kPart = 8 doubles per global frame slot [l1 sum, SSIM sum,
+ * depth |err| sum, valid depth count, (1 - cos) sum, |F_hat - F|^2 sum, zero-norm flag,
+ * supervised rows], then the trust penalty), with inv_b = 1 / nframes (objective.cpp:77,187-190).
+ * The sharded step's all-reduced partials assemble to the full batch's breakdown. */
+latmap_status latmap_loss_assemble(const double* partials, int32_t nframes, int32_t width, int32_t height,
+                                   const latmap_config* cfg, latmap_loss_breakdown* out);
+/* Sharded step, after objective -> latmap_session_allreduce -> apply: *any = 1 when some rank's
+ * tile lists overflowed in that objective (the flag travels in the loss partials, so every rank's
+ * Adam skipped the step). This rank's buffers are grown when its own lists overflowed; the caller
+ * repeats the iteration on every rank. Synchronises the context stream. */
+latmap_status latmap_session_check_overflow(latmap_session* s, int32_t* any);
+/* Sticky count of Adam steps skipped because a tile list overflowed (since session creation). */
+latmap_status latmap_session_overflow_steps(latmap_session* s, int64_t* count);
+/* Parity export of the bf16 tcgen05 decoders (the reference returns F_hat,
+ * proj/src/dictionary.cpp:45,52; the fused kernels never materialise it). While enabled, DEC1 /
+ * DL3 also store each row's (nu^2 = |F_hat|^2, dot = F_hat.F) as the kernels computed them. */
+latmap_status latmap_session_set_parity_export(latmap_session* s, int32_t enable);
+/* For the last frame the objective decoded: *path = 0 none, 1 fp32 SIMT, 2 fused tcgen05
+ * (DEC1/DEC2), 3 staged tcgen05 (DL1-DL5); *rows = its decoder rows (pixels). `attention` (device,
+ * rows x K, may be NULL) receives the attention P = softmax(Q W D^T / tau) the bf16 kernels used,
+ * so F_hat = P D; `row_nd` (device, rows x 2, may be NULL) the per-row (nu^2, dot). Both need a
+ * tcgen05 frame (the fused path writes its e tiles only with gradients); row_nd needs the export
+ * enabled before the objective. Synchronises the context stream. */
+latmap_status latmap_session_decoder_export(latmap_session* s, int32_t* path, int64_t* rows, float* attention,
+                                            float* row_nd);
 /* Phase timing with CUDA events on the session stream: phases 0 project+bin+sort (K1-K3b),
  * 1 raster forward (K4), 2 image losses (K5), 3 decoder+feature loss (K6/K7), 4 raster backward (K8),
  * 5 projection backward (K9), 6 Adam (K10), 7 reserved. phase_times syncs, returns the summed

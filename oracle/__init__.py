@@ -167,6 +167,8 @@ def _declare(L):
         f = getattr(L, "lm_stream_kmeans_update" + sfx)
         f.argtypes = [P, C.c_int64, C.c_int64, P, P, P, C.c_int64, C.c_void_p, C.c_void_p, ct]
     L.lm_mt64_seed.argtypes = [C.c_void_p, C.c_uint64]
+    L.lm_oracle_set_gemm_threads.argtypes = [C.c_int]
+    L.lm_oracle_set_gemm_threads.restype = None
     L.lm_mt64_next.argtypes = [C.c_void_p]
     L.lm_mt64_next.restype = C.c_uint64
     L.lm_mt64_uniform01.argtypes = [C.c_void_p]
@@ -740,3 +742,8 @@ def query_scores(rec, embedding):
     out = np.zeros(r.shape[0], np.float32)
     lib().lm_query_scores(_p(r), r.shape[0], r.shape[1], _p(e), _p(out))
     return out
+
+
+def set_gemm_threads(n):
+    """Row-split threads for the oracle's dense products (results are bit-identical for any n)."""
+    lib().lm_oracle_set_gemm_threads(int(n))

@@ -876,23 +876,76 @@ int S(lm_feature_loss)(const T* rec, const T* tgt, int64_t n, int64_t df, const 
   return 0;
 }
 
-/* ---------------- dense products (Eigen MatX stand-ins) ---------------- */
-/* C(MxN) = A(MxK) B(KxN), row-major, inner index ascending. */
-static void gemm_nn(int64_t M, int64_t N, int64_t K, const T* A, const T* B, T* C) {
-  memset(C, 0, sizeof(T) * (size_t)(M * N));
-  for (int64_t i = 0; i < M; ++i) {
-    T* c = C + i * N;
-    for (int64_t k = 0; k < K; ++k) {
-      const T a = A[i * K + k];
-      const T* b = B + k * N;
-      for (int64_t j = 0; j < N; ++j) c[j] += a * b[j];
+/* ---------------- dense products (Eigen MatX stand-ins) ----------------
+ * Every product element is summed over the inner index in ASCENDING order, one separately
+ * rounded multiply and add per term (no FMA: -ffp-contract=off); this order is the oracle's
+ * definition of Eigen's float GEMM bits. The loops are blocked (4 output rows share each B row
+ * load; 256-column / 128-inner panels stay in L1/L2) and split by output rows over
+ * lm_oracle_set_gemm_threads() threads (default 1, like the reference's Eigen without OpenMP).
+ * Neither changes the per-element order, so results are bit-identical for every thread count. */
+extern int lm_oracle_gemm_threads_value;
+#define GJ 256
+#define GK 128
+typedef struct {
+  int64_t M, N, K;
+  const T* A;
+  const T* B;
+  T* C;
+} gemm_job;
+/* C(MxN) = A(MxK) B(KxN) for rows [i0, i1). */
+static void gemm_nn_rows(void* pc, int64_t i0, int64_t i1, int tid) {
+  const gemm_job* g = (const gemm_job*)pc;
+  const int64_t N = g->N, K = g->K;
+  for (int64_t i = i0; i < i1; ++i) memset(g->C + i * N, 0, sizeof(T) * (size_t)N);
+  for (int64_t jb = 0; jb < N; jb += GJ) {
+    const int64_t je = jb + GJ < N ? jb + GJ : N, nj = je - jb;
+    for (int64_t kb = 0; kb < K; kb += GK) {
+      const int64_t ke = kb + GK < K ? kb + GK : K;
+      int64_t i = i0;
+      for (; i + 4 <= i1; i += 4) {
+        T* c0 = g->C + i * N + jb;
+        T* c1 = c0 + N;
+        T* c2 = c1 + N;
+        T* c3 = c2 + N;
+        const T* a = g->A + i * K;
+        for (int64_t k = kb; k < ke; ++k) {
+          const T a0 = a[k], a1 = a[K + k], a2 = a[2 * K + k], a3 = a[3 * K + k];
+          const T* b = g->B + k * N + jb;
+          for (int64_t j = 0; j < nj; ++j) {
+            const T bj = b[j];
+            c0[j] += a0 * bj;
+            c1[j] += a1 * bj;
+            c2[j] += a2 * bj;
+            c3[j] += a3 * bj;
+          }
+        }
+      }
+      for (; i < i1; ++i) {
+        T* c = g->C + i * N + jb;
+        for (int64_t k = kb; k < ke; ++k) {
+          const T av = g->A[i * K + k];
+          const T* b = g->B + k * N + jb;
+          for (int64_t j = 0; j < nj; ++j) c[j] += av * b[j];
+        }
+      }
     }
   }
 }
+static int gemm_threads(int64_t rows, int64_t work) {
+  int t = lm_oracle_gemm_threads_value;
+  if (work < (int64_t)1 << 22) t = 1;
+  return (int64_t)t > rows ? (int)(rows > 0 ? rows : 1) : t;
+}
+static void gemm_nn(int64_t M, int64_t N, int64_t K, const T* A, const T* B, T* C) {
+  gemm_job g = {M, N, K, A, B, C};
+  parallel_chunks(M, gemm_threads(M, M * N * K), gemm_nn_rows, &g);
+}
 static T* transpose(int64_t R, int64_t Cc, const T* A) {
   T* t = (T*)malloc(sizeof(T) * (size_t)(R * Cc));
-  for (int64_t i = 0; i < R; ++i)
-    for (int64_t j = 0; j < Cc; ++j) t[j * R + i] = A[i * Cc + j];
+  for (int64_t ib = 0; ib < R; ib += 32)
+    for (int64_t jb = 0; jb < Cc; jb += 32)
+      for (int64_t i = ib; i < ib + 32 && i < R; ++i)
+        for (int64_t j = jb; j < jb + 32 && j < Cc; ++j) t[j * R + i] = A[i * Cc + j];
   return t;
 }
 /* C(MxN) = A(MxK) B^T, B is NxK. */
@@ -901,18 +954,48 @@ static void gemm_nt(int64_t M, int64_t N, int64_t K, const T* A, const T* B, T* 
   gemm_nn(M, N, K, A, bt, C);
   free(bt);
 }
-/* C(MxN) = A^T B, A is KxM, B is KxN. */
-static void gemm_tn(int64_t M, int64_t N, int64_t K, const T* A, const T* B, T* C) {
-  memset(C, 0, sizeof(T) * (size_t)(M * N));
-  for (int64_t k = 0; k < K; ++k) {
-    const T* a = A + k * M;
-    const T* b = B + k * N;
-    for (int64_t i = 0; i < M; ++i) {
-      const T av = a[i];
-      T* c = C + i * N;
-      for (int64_t j = 0; j < N; ++j) c[j] += av * b[j];
+/* C(MxN) = A^T B, A is KxM, B is KxN: output rows [i0, i1), inner index k ascending. */
+static void gemm_tn_rows(void* pc, int64_t i0, int64_t i1, int tid) {
+  const gemm_job* g = (const gemm_job*)pc;
+  const int64_t M = g->M, N = g->N, K = g->K;
+  for (int64_t i = i0; i < i1; ++i) memset(g->C + i * N, 0, sizeof(T) * (size_t)N);
+  for (int64_t jb = 0; jb < N; jb += GJ) {
+    const int64_t je = jb + GJ < N ? jb + GJ : N, nj = je - jb;
+    for (int64_t kb = 0; kb < K; kb += GK) {
+      const int64_t ke = kb + GK < K ? kb + GK : K;
+      int64_t i = i0;
+      for (; i + 4 <= i1; i += 4) {
+        T* c0 = g->C + i * N + jb;
+        T* c1 = c0 + N;
+        T* c2 = c1 + N;
+        T* c3 = c2 + N;
+        for (int64_t k = kb; k < ke; ++k) {
+          const T* a = g->A + k * M + i;
+          const T a0 = a[0], a1 = a[1], a2 = a[2], a3 = a[3];
+          const T* b = g->B + k * N + jb;
+          for (int64_t j = 0; j < nj; ++j) {
+            const T bj = b[j];
+            c0[j] += a0 * bj;
+            c1[j] += a1 * bj;
+            c2[j] += a2 * bj;
+            c3[j] += a3 * bj;
+          }
+        }
+      }
+      for (; i < i1; ++i) {
+        T* c = g->C + i * N + jb;
+        for (int64_t k = kb; k < ke; ++k) {
+          const T av = g->A[k * M + i];
+          const T* b = g->B + k * N + jb;
+          for (int64_t j = 0; j < nj; ++j) c[j] += av * b[j];
+        }
+      }
     }
   }
+}
+static void gemm_tn(int64_t M, int64_t N, int64_t K, const T* A, const T* B, T* C) {
+  gemm_job g = {M, N, K, A, B, C};
+  parallel_chunks(M, gemm_threads(M, M * N * K), gemm_tn_rows, &g);
 }
 
 /* dictionary_checksum, dictionary.cpp:10-23 */
@@ -1391,6 +1474,8 @@ int S(lm_stream_kmeans_update)(const T* batch, int64_t n, int64_t dim, T* atoms,
 }
 
 #else /* LM_ONCE: voxel hash store, voxel_hash.cpp / active_set.cpp */
+int lm_oracle_gemm_threads_value = 1;
+void lm_oracle_set_gemm_threads(int n) { lm_oracle_gemm_threads_value = n < 1 ? 1 : (n > 256 ? 256 : n); }
 
 /* ------------------------------------------------------------------ evaluation metrics */
 static float lmo_dot(const float* a, const float* b, int64_t d) {

@@ -139,6 +139,10 @@ void lm_mt64_seed(lm_mt64* r, uint64_t seed);
 uint64_t lm_mt64_next(lm_mt64* r);
 double lm_mt64_uniform01(void* r);
 
+/* Threads for the dense products (row-split; bit-identical for every count). Default 1, like
+ * the reference's single-threaded Eigen (proj/CMakeLists.txt:11 links no OpenMP). */
+void lm_oracle_set_gemm_threads(int n);
+
 /* ---- evaluation metrics (float, metrics.cpp:8-89, evaluate.cpp:74-88) ---- */
 double lm_metric_cos(const float* rec, const float* tgt, int64_t n, int64_t d, int32_t* flagged);
 /* intersection / union_ per class (c entries each); returns mIoU; -1 on a label >= c */

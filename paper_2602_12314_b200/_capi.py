@@ -162,6 +162,8 @@ def _declare(L):
         "latmap_session_frame_images": [P, C.c_int32, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(P)],
         "latmap_session_stats": [P, P, P],
         "latmap_session_profile": [P, C.c_int32],
+        "latmap_session_set_parity_export": [P, C.c_int32],
+        "latmap_session_decoder_export": [P, C.POINTER(C.c_int32), C.POINTER(C.c_int64), P, P],
         "latmap_selftest_umma": [P, P, P, P, C.c_int32, C.c_int32, C.c_int32, C.c_int32],
         "latmap_weighted_kmeans": [P, P, P, C.c_int64, C.c_int32, C.c_int64, P, P, P, C.c_int64, C.c_int32, P, P,
                                    C.POINTER(C.c_int32)],
@@ -184,6 +186,10 @@ def _declare(L):
         "latmap_comm_destroy": [P],
         "latmap_comm_allreduce": [P, P, C.c_int64, C.c_int32],
         "latmap_session_allreduce": [P, P],
+        "latmap_loss_assemble": [P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(Config), C.POINTER(LossBreakdown)],
+        "latmap_session_check_overflow": [P, C.POINTER(C.c_int32)],
+        "latmap_session_grad_layout": [P, P, P],
+        "latmap_session_overflow_steps": [P, C.POINTER(C.c_int64)],
         "latmap_pipeline_create": [P, C.POINTER(Config), C.POINTER(PipelineConfig), C.POINTER(Intrinsics),
                                    C.POINTER(P)],
         "latmap_pipeline_destroy": [P],
@@ -252,7 +258,8 @@ EXPORTED = ["latmap_ctx_create", "latmap_ctx_destroy", "latmap_ctx_set_stream", 
             "latmap_session_set_graphs", "latmap_session_seed_candidates", "latmap_session_append_rows",
             "latmap_session_grad_buffer", "latmap_session_loss_buffer",
             "latmap_session_read_loss", "latmap_session_frame_images", "latmap_session_stats",
-            "latmap_session_profile", "latmap_session_phase_times", "latmap_selftest_umma", "latmap_ctx_stream",
+            "latmap_session_profile", "latmap_session_phase_times", "latmap_session_set_parity_export",
+            "latmap_session_decoder_export", "latmap_selftest_umma", "latmap_ctx_stream",
             "latmap_voxel_of", "latmap_hash_voxel", "latmap_store_create", "latmap_store_destroy", "latmap_store_size",
             "latmap_store_stats", "latmap_store_last_error", "latmap_store_insert", "latmap_store_update",
             "latmap_store_find", "latmap_store_get_records", "latmap_store_insert_global", "latmap_store_insert_keyed", "latmap_store_fetch_local",
@@ -263,7 +270,8 @@ EXPORTED = ["latmap_ctx_create", "latmap_ctx_destroy", "latmap_ctx_set_stream", 
             "latmap_pipeline_destroy", "latmap_pipeline_process_keyframe", "latmap_pipeline_flush",
             "latmap_pipeline_session", "latmap_pipeline_store", "latmap_pipeline_state", "latmap_pipeline_active_set",
             "latmap_pipeline_last_error", "latmap_comm_unique_id", "latmap_comm_init",
-            "latmap_comm_destroy", "latmap_comm_allreduce", "latmap_session_allreduce"]
+            "latmap_comm_destroy", "latmap_comm_allreduce", "latmap_session_allreduce", "latmap_loss_assemble",
+            "latmap_session_check_overflow", "latmap_session_overflow_steps", "latmap_session_grad_layout"]
 
 
 def check(ctx_handle, status):

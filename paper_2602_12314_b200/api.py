@@ -392,6 +392,17 @@ def adam_step(ctx, param, grad, st: AdamState, lr):
     return bool(ap.value)
 
 
+def assemble_loss(partials, width, height, cfg) -> dict:
+    """Host-side LossBreakdown of a batch from its loss-partials vector (latmap_loss_assemble;
+    nframes = (len - 8) / 8 global frame slots followed by the trust slot). No device needed."""
+    p = np.ascontiguousarray(partials, np.float64)
+    nframes = (p.size - 8) // 8
+    out = LossBreakdown()
+    check(None, lib().latmap_loss_assemble(p.ctypes.data_as(C.c_void_p), nframes, int(width), int(height),
+                                            C.byref(cfg), C.byref(out)))
+    return out.as_dict()
+
+
 def default_config(**overrides) -> Config:
     c = Config()
     lib().latmap_default_config(C.byref(c))
@@ -582,20 +593,85 @@ class Session:
     def grad_buffer(self):
         p, n = C.c_void_p(), C.c_int64()
         check(self.ctx.h, lib().latmap_session_grad_buffer(self.h, C.byref(p), C.byref(n)))
-        return _device_view(p.value, n.value, torch.float32, self.ctx.device)
+        return _device_view(p.value, n.value, torch.float32, self.ctx.device, owner=self)
 
     def loss_buffer(self):
         p, n = C.c_void_p(), C.c_int64()
         check(self.ctx.h, lib().latmap_session_loss_buffer(self.h, C.byref(p), C.byref(n)))
-        return _device_view(p.value, n.value, torch.float64, self.ctx.device)
+        return _device_view(p.value, n.value, torch.float64, self.ctx.device, owner=self)
 
     def frame_images(self, b):
         ps = [C.c_void_p() for _ in range(4)]
         check(self.ctx.h, lib().latmap_session_frame_images(self.h, b, *[C.byref(p) for p in ps]))
         h, w = self.intr.height, self.intr.width
         shapes = [(h, w, 3), (h, w), (h, w, self.ds), (h, w)]
-        return [_device_view(p.value, int(np.prod(s)), torch.float32, self.ctx.device).view(*s)
+        return [_device_view(p.value, int(np.prod(s)), torch.float32, self.ctx.device, owner=self).view(*s)
                 for p, s in zip(ps, shapes)]
+
+    GRAD_BLOCKS = ("positions", "rotations", "colors", "log_scales", "opacity_logits", "features", "proj", "atoms")
+
+    def grad_blocks(self):
+        """{block name: (offset, length)} of the flat parameter / gradient / moment buffers (blocks
+        start 16-byte aligned, so offsets are not a plain running sum)."""
+        off = np.zeros(8, np.int64)
+        ln = np.zeros(8, np.int64)
+        check(self.ctx.h, lib().latmap_session_grad_layout(self.h, off.ctypes.data_as(C.c_void_p),
+                                                          ln.ctypes.data_as(C.c_void_p)))
+        return {nm: (int(o), int(n)) for nm, o, n in zip(self.GRAD_BLOCKS, off, ln)}
+
+    def grad_block_views(self, flat=None):
+        """The flat gradient buffer (or `flat`, same layout) split into its 8 named blocks."""
+        flat = self.grad_buffer() if flat is None else flat
+        return {nm: flat[o:o + n] for nm, (o, n) in self.grad_blocks().items()}
+
+    def check_overflow(self):
+        """After objective -> all-reduce -> apply: True when some rank's tile lists overflowed (every
+        rank's Adam skipped the step; this rank's buffers are grown). Synchronises."""
+        any_ = C.c_int32()
+        check(self.ctx.h, lib().latmap_session_check_overflow(self.h, C.byref(any_)))
+        return bool(any_.value)
+
+    def overflow_steps(self):
+        """Sticky count of Adam steps skipped because a tile list overflowed."""
+        n = C.c_int64()
+        check(self.ctx.h, lib().latmap_session_overflow_steps(self.h, C.byref(n)))
+        return int(n.value)
+
+    def sharded_step(self, exchange, read=False, attempts=3):
+        """One keyframe-sharded Stage-I iteration: this rank's objective (global batch
+        mean, set_batch), ``exchange(self)`` summing gradients and loss partials over ranks (e.g.
+        Comm.session_allreduce), then the identical Adam on every rank. With ``read`` the step is
+        checked for a tile-list overflow on any rank and repeated (all ranks take the same branch:
+        the flag is part of the summed partials) and the LossBreakdown is returned."""
+        for _ in range(attempts):
+            self.objective(want_grad=True, read=False)
+            exchange(self)
+            self.apply()
+            if not read:
+                return None
+            if not self.check_overflow():
+                return self.read_loss()
+        raise _capi.LatmapError("sharded_step: tile-list overflow persisted")
+
+    DECODER_PATHS = {0: "none", 1: "fp32", 2: "tc_fused", 3: "tc_staged"}
+
+    def set_parity_export(self, enable=True):
+        """Make the bf16 tcgen05 decoders also store each row's (|F_hat|^2, F_hat.F)."""
+        check(self.ctx.h, lib().latmap_session_set_parity_export(self.h, int(bool(enable))))
+
+    def decoder_export(self, attention=True, row_nd=True):
+        """The last decoded frame's decoder path name, its attention P (rows x K, device) and
+        per-row (nu^2, dot) as the tcgen05 kernels computed them (None where not requested)."""
+        path, rows = C.c_int32(), C.c_int64()
+        check(self.ctx.h, lib().latmap_session_decoder_export(self.h, C.byref(path), C.byref(rows), None, None))
+        dev = f"cuda:{self.ctx.device}"
+        p = torch.empty((rows.value, self.k), dtype=torch.float32, device=dev) if attention else None
+        nd = torch.empty((rows.value, 2), dtype=torch.float32, device=dev) if row_nd else None
+        if attention or row_nd:
+            check(self.ctx.h, lib().latmap_session_decoder_export(
+                self.h, None, None, C.c_void_p(p.data_ptr()) if p is not None else None,
+                C.c_void_p(nd.data_ptr()) if nd is not None else None))
+        return self.DECODER_PATHS[path.value], p, nd
 
     PHASES = ("bin", "raster_fwd", "image_losses", "decoder", "raster_bwd", "project_bwd", "adam", "misc")
 
@@ -618,14 +694,19 @@ class Session:
 
 
 class _CudaArrayView:
-    def __init__(self, ptr, count, typestr):
+    """__cuda_array_interface__ over library-owned device memory. It keeps `owner` (the Session /
+    Pipeline that owns the memory) alive for as long as torch holds the view. A view must still be
+    fetched again after a row-set change (import_rows / append_rows swap the parameter set)."""
+
+    def __init__(self, ptr, count, typestr, owner=None):
+        self.owner = owner
         self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr, "data": (ptr, False), "version": 3}
 
 
-def _device_view(ptr, count, dtype, device):
+def _device_view(ptr, count, dtype, device, owner=None):
     typestr = "<f4" if dtype == torch.float32 else "<f8"
     with torch.cuda.device(device):
-        return torch.as_tensor(_CudaArrayView(ptr, count, typestr), device=f"cuda:{device}")
+        return torch.as_tensor(_CudaArrayView(ptr, count, typestr, owner), device=f"cuda:{device}")
 
 
 # ----------------------------------------------------------------------------- voxel-hash store

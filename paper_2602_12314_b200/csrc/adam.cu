@@ -81,8 +81,8 @@ __global__ void __launch_bounds__(256, 5) adam_update_kernel(float* __restrict__
                                                           float* __restrict__ m, float* __restrict__ v, Blocks B,
                                                           const int64_t* steps, const float* corr1,
                                                           const float* corr2, int32_t table_len, const int32_t* flags,
-                                                          const int64_t* overflow) {
-  if (overflow && *overflow) return;
+                                                          const double* overflow) {
+  if (overflow && *overflow != 0.0) return;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
   for (int bi = 0; bi < B.n; ++bi) {
     const AdamBlock blk = B.b[bi];
@@ -162,10 +162,13 @@ __global__ void __launch_bounds__(256, 5) adam_update_kernel(float* __restrict__
 }
 
 // Pass 3: counters (AdamState::step / skipped).
-__global__ void adam_finish_kernel(Blocks B, int64_t* steps, int64_t* skipped, int32_t* flags, const int64_t* overflow) {
+__global__ void adam_finish_kernel(Blocks B, int64_t* steps, int64_t* skipped, int32_t* flags, const double* overflow,
+                                   int64_t* overflow_steps) {
   const int i = threadIdx.x;
+  const bool ovf = overflow && *overflow != 0.0;
+  if (i == 0 && ovf && overflow_steps) *overflow_steps += 1;  // sticky: read by latmap_session_overflow_steps
   if (i >= B.n) return;
-  if (!(overflow && *overflow) && B.b[i].kind >= 0) {
+  if (!ovf && B.b[i].kind >= 0) {
     if (flags[i])
       skipped[i] += 1;
     else
@@ -178,7 +181,7 @@ __global__ void adam_finish_kernel(Blocks B, int64_t* steps, int64_t* skipped, i
 
 void adam_flat(cudaStream_t st, float* param, const float* grad, float* m, float* v, const AdamBlock* blocks,
                int nblocks, int64_t* steps, int64_t* skipped, const float* corr1, const float* corr2,
-               int32_t table_len, int32_t* flags, const int64_t* overflow) {
+               int32_t table_len, int32_t* flags, const double* overflow, int64_t* overflow_steps) {
   Blocks B;
   B.n = nblocks;
   int64_t total = 0;
@@ -189,7 +192,7 @@ void adam_flat(cudaStream_t st, float* param, const float* grad, float* m, float
   adam_check_kernel<<<148 * 4, 256, 0, st>>>(grad, B, total, flags);
   adam_update_kernel<<<148 * 5, 256, 0, st>>>(param, grad, m, v, B, steps, corr1, corr2, table_len, flags,
                                                overflow);
-  adam_finish_kernel<<<1, 32, 0, st>>>(B, steps, skipped, flags, overflow);
+  adam_finish_kernel<<<1, 32, 0, st>>>(B, steps, skipped, flags, overflow, overflow_steps);
   count_launch(3);
 }
 

@@ -574,7 +574,7 @@ latmap_status latmap_adam_step(latmap_ctx* ctx, float* param, const float* grad,
   const float* c1p = &da->c1 - *step;
   const float* c2p = &da->c2 - *step;
   adam_flat(st, param, grad, m, v, &blk, 1, d_steps, &da->skipped, c1p, c2p, (int32_t)std::min<int64_t>(t, 1 << 30),
-            da->flags, nullptr);
+            da->flags, nullptr, nullptr);
   Aux back;
   CTX_CHECK(ctx, cudaMemcpyAsync(&back, d, sizeof(Aux), cudaMemcpyDeviceToHost, st));
   CTX_CHECK(ctx, cudaFreeAsync(d, st));
@@ -623,6 +623,7 @@ struct latmap_session {
   float *sp_params = nullptr, *sp_grads = nullptr, *sp_m = nullptr, *sp_v = nullptr;
   int64_t cur_cap = 0, sp_cap = 0;  // floats per buffer of the current / spare set
   int64_t *steps = nullptr, *skipped = nullptr, *overflow = nullptr;
+  int64_t* overflow_steps = nullptr;  // sticky count of Adam steps skipped for a tile-list overflow (any rank)
   int32_t* flags = nullptr;
   float *corr1 = nullptr, *corr2 = nullptr;
   std::vector<FrameDev> frames;
@@ -733,9 +734,11 @@ struct LossWeights {
   float lambda_rgb, lambda_i1, lambda_i2, lambda_depth, lambda_feat, lambda_cos, lambda_l2, lambda_trust;
 };
 
-// LossBreakdown assembly (objective.cpp:188-190 and 247-261).
-__global__ void assemble_loss_kernel(const double* partials, int nframes, double npx, float inv_b, LossWeights wt,
-                                     latmap_loss_breakdown* out) {
+// LossBreakdown assembly (objective.cpp:188-190 and 247-261) from the per-frame partial slots
+// and the trust slot after them; shared by the device step and the host entry point
+// latmap_loss_assemble (the sharded step's all-reduced partials, and the CPU tests).
+__host__ __device__ void assemble_loss(const double* partials, int nframes, double npx, float inv_b, LossWeights wt,
+                                       latmap_loss_breakdown* out) {
   latmap_loss_breakdown L{};
   for (int b = 0; b < nframes; ++b) {
     const double* p = partials + b * kPart;
@@ -760,6 +763,11 @@ __global__ void assemble_loss_kernel(const double* partials, int nframes, double
   L.total = wt.lambda_rgb * (wt.lambda_i1 * L.l_rgb + wt.lambda_i2 * L.l_ssim) + wt.lambda_depth * L.l_depth +
             wt.lambda_feat * (wt.lambda_cos * L.l_cos + wt.lambda_l2 * L.l_l2 + wt.lambda_trust * L.l_trust);
   *out = L;
+}
+
+__global__ void assemble_loss_kernel(const double* partials, int nframes, double npx, float inv_b, LossWeights wt,
+                                     latmap_loss_breakdown* out) {
+  assemble_loss(partials, nframes, npx, inv_b, wt, out);
 }
 
 MapPtrs session_map(latmap_session* s, float* base) {
@@ -838,6 +846,8 @@ static void wait_frame(const latmap_session* s, int b, cudaStream_t st) {
 // skips the image-loss gradients and the render backward (ObjectiveOptions::map_grads);
 // use_cache skips the render when the per-frame images still hold renders of the current map
 // (ObjectiveOptions::cached_renders, Stage II of pipeline.cpp:250-259).
+__global__ void overflow_slot_kernel(const int64_t* flag, double* slot) { *slot = *flag ? 1.0 : 0.0; }
+
 latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grads = true, bool use_cache = false) {
   latmap_ctx* ctx = s->ctx;
   cudaStream_t st = ctx->stream;
@@ -965,6 +975,8 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
       seg_pool_kernel<<<gq, 256, 0, st>>>(s->query[b], f.assign, npx, s->ds, f.seg_of, s->seg_q);
       seg_mean_kernel<<<(unsigned)((f.n_sup * s->ds + 255) / 256), 256, 0, st>>>(s->seg_q, f.seg_inv, f.n_sup, s->ds);
       count_launch(2);
+      s->dec.last_path = 1;
+      s->dec.last_npx = f.n_sup;
       decoder_frame(st, s->dec, s->seg_q, f.seg_rows, f.n_sup, f.feats, f.n_set, f.stat, atoms, proj,
                     c.softmax_temp, c.lambda_cos, c.lambda_l2, c.lambda_feat * inv_b, want_grad, s->seg_dq, g_proj,
                     g_atoms, part);
@@ -977,6 +989,8 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
       s->begin(3);
       const bool fused_ok = decoder_tc_supported(s->k, s->ds, f.n_set) && ctx->decoder_path != 2;
       const bool staged_ok = s->dec.dl_mt && decoder_dl_supported(s->k, s->ds, f.n_set) && ctx->decoder_path != 1;
+      s->dec.last_path = (c.decoder_precision == 1 && fused_ok) ? 2 : (c.decoder_precision == 1 && staged_ok) ? 3 : 1;
+      s->dec.last_npx = npx;
       if (c.decoder_precision == 1 && fused_ok)
         decoder_frame_tc(st, s->dec, s->query[b], f.assign, npx, f.feats, f.n_set, f.stat, atoms, proj,
                          c.softmax_temp, c.lambda_cos, c.lambda_l2, c.lambda_feat * inv_b, want_grad, d_qry,
@@ -1016,6 +1030,10 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
     trust_region(st, atoms, s->anchor, s->k, s->df, c.trust_delta, want_grad ? g_atoms : nullptr,
                  c.lambda_feat * c.lambda_trust, tslot);
   }
+  // this rank's tile-list overflow flag joins the loss partials, so the sharded step's sum
+  // all-reduce tells every rank (and its Adam) that some rank's gradients are incomplete
+  overflow_slot_kernel<<<1, 1, 0, st>>>(s->overflow, s->partials + (size_t)s->part_frames * kPart + 1);
+  count_launch();
   return post_launch(ctx);
 }
 
@@ -1068,7 +1086,7 @@ void session_adam(latmap_session* s, bool dict_only = false) {
   else
     s->renders_valid = false;  // the map moves
   adam_flat(s->ctx->stream, s->params, s->grads, s->m, s->v, blocks, 8, s->steps, s->skipped, s->corr1, s->corr2,
-            kCorrLen, s->flags, s->overflow);
+            kCorrLen, s->flags, s->partials + (size_t)s->part_frames * kPart + 1, s->overflow_steps);
   s->end();
 }
 
@@ -1114,7 +1132,7 @@ latmap_status latmap_session_create(latmap_ctx* ctx, const latmap_config* cfg, i
   bool good = ok(cudaMalloc(&s->params, sizeof(float) * s->total)) && ok(cudaMalloc(&s->grads, sizeof(float) * s->total)) &&
               ok(cudaMalloc(&s->m, sizeof(float) * s->total)) && ok(cudaMalloc(&s->v, sizeof(float) * s->total)) &&
               ok(cudaMalloc(&s->anchor, sizeof(float) * k * df)) && ok(cudaMalloc(&s->steps, sizeof(int64_t) * 8)) &&
-              ok(cudaMalloc(&s->skipped, sizeof(int64_t) * 8)) && ok(cudaMalloc(&s->overflow, sizeof(int64_t))) &&
+              ok(cudaMalloc(&s->skipped, sizeof(int64_t) * 8)) && ok(cudaMalloc(&s->overflow, sizeof(int64_t))) && ok(cudaMalloc(&s->overflow_steps, sizeof(int64_t))) &&
               ok(cudaMalloc(&s->flags, sizeof(int32_t) * 8)) && ok(cudaMalloc(&s->corr1, sizeof(float) * kCorrLen)) &&
               ok(cudaMalloc(&s->corr2, sizeof(float) * kCorrLen)) &&
               ok(cudaMalloc(&s->d_color, sizeof(float) * npx * 3)) && ok(cudaMalloc(&s->d_depth, sizeof(float) * npx)) &&
@@ -1158,6 +1176,7 @@ latmap_status latmap_session_create(latmap_ctx* ctx, const latmap_config* cfg, i
   cudaMemset(s->m, 0, sizeof(float) * s->total);
   cudaMemset(s->v, 0, sizeof(float) * s->total);
   cudaMemset(s->grads, 0, sizeof(float) * s->total);
+  cudaMemset(s->overflow_steps, 0, sizeof(int64_t));
   cudaMemset(s->steps, 0, sizeof(int64_t) * 8);
   cudaMemset(s->skipped, 0, sizeof(int64_t) * 8);
   cudaMemset(s->flags, 0, sizeof(int32_t) * 8);
@@ -1188,14 +1207,14 @@ latmap_status latmap_session_destroy(latmap_session* s) {
   for (void* p : {(void*)s->sp_params, (void*)s->sp_grads, (void*)s->sp_m, (void*)s->sp_v})
     if (p) cudaFree(p);
   for (void* p : {(void*)s->params, (void*)s->grads, (void*)s->m, (void*)s->v, (void*)s->anchor, (void*)s->steps,
-                  (void*)s->skipped, (void*)s->overflow, (void*)s->flags, (void*)s->corr1, (void*)s->corr2,
+                  (void*)s->skipped, (void*)s->overflow, (void*)s->overflow_steps, (void*)s->flags, (void*)s->corr1, (void*)s->corr2,
                   (void*)s->d_color, (void*)s->d_depth, (void*)s->d_query, (void*)s->ssim_scratch, (void*)s->partials,
                   (void*)s->d_loss, (void*)s->dec.buf1, (void*)s->dec.buf2, (void*)s->dec.alpha_r, (void*)s->dec.beta_r,
                   (void*)s->dec.kd, (void*)s->dec.mm, (void*)s->dec.gt, (void*)s->dec.nv, (void*)s->dec.r,
                   (void*)s->dec.a, (void*)s->dec.bm, (void*)s->dec.row_stats, (void*)s->dec.r_part,
                   (void*)s->dec.a_part, (void*)s->dec.bm_part, (void*)s->dec.loss_part,
                   (void*)s->dec.e_tiles, (void*)s->dec.a_acc, (void*)s->dec.r_acc, (void*)s->dec.dl_mt,
-                  (void*)s->dec.dl_nu, (void*)s->dec.dl_part})
+                  (void*)s->dec.dl_nu, (void*)s->dec.dl_part, (void*)s->dec.row_nd})
     if (p) cudaFree(p);
   for (auto& r : s->rw) r.release();
   for (auto* p : s->color) cudaFree(p);
@@ -1852,6 +1871,77 @@ latmap_status latmap_session_frame_images(latmap_session* s, int32_t b, float** 
   if (depth) *depth = s->depth[b];
   if (query) *query = s->query[b];
   if (alpha) *alpha = s->alpha[b];
+  return LATMAP_OK;
+}
+
+latmap_status latmap_loss_assemble(const double* partials, int32_t nframes, int32_t width, int32_t height,
+                                   const latmap_config* cfg, latmap_loss_breakdown* out) {
+  if (!partials || !cfg || !out || nframes < 1 || width < 1 || height < 1) return LATMAP_ERR_INVALID_ARGUMENT;
+  const latmap_config& c = *cfg;
+  LossWeights wt{c.lambda_rgb, c.lambda_i1, c.lambda_i2, c.lambda_depth, c.lambda_feat, c.lambda_cos, c.lambda_l2,
+                 c.lambda_trust};
+  assemble_loss(partials, nframes, (double)width * height, 1.f / (float)nframes, wt, out);
+  return LATMAP_OK;
+}
+
+latmap_status latmap_session_grad_layout(latmap_session* s, int64_t offsets[8], int64_t lengths[8]) {
+  if (!s || !offsets || !lengths) return LATMAP_ERR_INVALID_ARGUMENT;
+  for (int i = 0; i < 8; ++i) offsets[i] = s->off[i], lengths[i] = s->len[i];
+  return LATMAP_OK;
+}
+
+latmap_status latmap_session_check_overflow(latmap_session* s, int32_t* any) {
+  if (!s || !any) return LATMAP_ERR_INVALID_ARGUMENT;
+  latmap_ctx* ctx = s->ctx;
+  double v = 0.0;
+  CTX_CHECK(ctx, cudaMemcpyAsync(&v, s->partials + (size_t)s->part_frames * kPart + 1, sizeof(double),
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+  CTX_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+  *any = v != 0.0;
+  session_fix_overflow(s);  // grows this rank's tile buffers when its own lists overflowed
+  return LATMAP_OK;
+}
+
+latmap_status latmap_session_overflow_steps(latmap_session* s, int64_t* count) {
+  if (!s || !count) return LATMAP_ERR_INVALID_ARGUMENT;
+  latmap_ctx* ctx = s->ctx;
+  CTX_CHECK(ctx, cudaMemcpyAsync(count, s->overflow_steps, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CTX_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+  return LATMAP_OK;
+}
+
+latmap_status latmap_session_set_parity_export(latmap_session* s, int32_t enable) {
+  if (!s) return LATMAP_ERR_INVALID_ARGUMENT;
+  latmap_ctx* ctx = s->ctx;
+  if (enable && !s->dec.row_nd) {
+    CTX_CHECK(ctx, cudaMalloc(&s->dec.row_nd, sizeof(float) * 2 * std::max<int64_t>(s->dec.n_cap, 1)));
+    CTX_CHECK(ctx, cudaMemset(s->dec.row_nd, 0, sizeof(float) * 2 * std::max<int64_t>(s->dec.n_cap, 1)));
+  } else if (!enable && s->dec.row_nd) {
+    CTX_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+    CTX_CHECK(ctx, cudaFree(s->dec.row_nd));
+    s->dec.row_nd = nullptr;
+  }
+  s->drop_graph();  // the kernels' export pointer is a captured argument
+  return LATMAP_OK;
+}
+
+latmap_status latmap_session_decoder_export(latmap_session* s, int32_t* path, int64_t* rows, float* attention,
+                                            float* row_nd) {
+  if (!s) return LATMAP_ERR_INVALID_ARGUMENT;
+  latmap_ctx* ctx = s->ctx;
+  if (path) *path = s->dec.last_path;
+  if (rows) *rows = s->dec.last_npx;
+  const bool tc = s->dec.last_path == 2 || s->dec.last_path == 3;
+  if ((attention || row_nd) && !tc)
+    return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "decoder_export: the last decoded frame did not run a tcgen05 decoder");
+  if (row_nd && !s->dec.row_nd)
+    return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "decoder_export: parity export is not enabled");
+  const int64_t n = s->dec.last_npx;
+  if (attention && n > 0) decoder_export_attention(ctx->stream, s->dec, n, attention);
+  if (row_nd && n > 0)
+    CTX_CHECK(ctx, cudaMemcpyAsync(row_nd, s->dec.row_nd, sizeof(float) * 2 * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  CTX_CHECK(ctx, cudaGetLastError());
+  CTX_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
   return LATMAP_OK;
 }
 

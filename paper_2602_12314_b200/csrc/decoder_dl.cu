@@ -369,6 +369,7 @@ struct Dl3Args {
   float inv_temp, lambda_cos, lambda_l2, scale;
   const int64_t* nsup;  // supervised rows (device)
   int want_grad;
+  float2* row_nd;       // optional parity export: per-row (nu^2, dot)
 };
 
 template <int N>
@@ -441,6 +442,7 @@ __global__ void __launch_bounds__(512, 1) dl_back_kernel(Dl3Args a) {
       be = a.scale * (-a.lambda_cos / (nug * nvg) * inv_nsup - 2.f * a.lambda_l2 * inv_nsup);
       cc = al * nu2 + be * dot;
     }
+    if (a.row_nd && role == 0 && sub == 0 && row < valid) a.row_nd[r0 + row] = make_float2(nu2, dot);
     if (!a.want_grad) continue;
     const float ps = inv_sum * a.inv_temp, al_t = al * inv_sum, wa = al * inv_sum * inv_sum, wb = be * inv_sum;
     const float* gp = a.gt + (int64_t)(asg < 0 ? 0 : asg) * K;
@@ -833,7 +835,7 @@ void launch_dl(cudaStream_t st, DecoderWork& w, const float* query, const int32_
   {
     Dl3Args d{w.e_tiles, reinterpret_cast<const uint4*>(w.dl_t), w.dl_nu, reinterpret_cast<const float4*>(w.row_stats), query, assignment, w.kd,
               w.gt, w.nv, w.dl_ae, d_query, w.r_part + 148 * (size_t)K * DS, w.loss_part, npx, K, NB, inv_temp, lambda_cos, lambda_l2,
-              scale, nsup, want_grad ? 1 : 0};
+              scale, nsup, want_grad ? 1 : 0, reinterpret_cast<float2*>(w.row_nd)};
     const size_t sm = (size_t)(K / 2) * DS * 2 + (size_t)kRows * DS * 2 + 2 * 32768;
     set_smem(dl_back_kernel<DS>, sm);
     dl_back_kernel<DS><<<2 * kBackGroups, 512, sm, st>>>(d);

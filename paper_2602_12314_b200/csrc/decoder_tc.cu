@@ -53,6 +53,7 @@ struct Dec1Args {
   double* loss_part;        // gridDim x 4
   int want_grad;
   int accum;                // add R^T into r_part (later frames of a step) instead of storing
+  float2* row_nd;           // optional parity export: per-row (nu^2, dot)
 };
 
 template <int K, int DS>
@@ -239,7 +240,10 @@ __global__ void __launch_bounds__(512, 1) dec1_kernel(Dec1Args a) {
       be = a.scale * (-a.lambda_cos / (nug * nvg) * inv_nsup - 2.f * a.lambda_l2 * inv_nsup);
       cc = al * nu2 + be * dot;
     }
-    if (qt == 0 && row < valid) a.row_stats[grow] = make_float4(mx, inv_sum, al, be);
+    if (qt == 0 && row < valid) {
+      a.row_stats[grow] = make_float4(mx, inv_sum, al, be);
+      if (a.row_nd) a.row_nd[grow] = make_float2(nu2, dot);
+    }
     // next tile's Q (consumed after this tile's MMA4 has read sQ)
     if (tile + gridDim.x < ntiles) {
       const int64_t nr0 = (tile + gridDim.x) * kRows;
@@ -682,7 +686,7 @@ void launch_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_
   const int accum = want_grad && w.tc_frames > 0 ? 1 : 0;
   Dec1Args d1{w.e_tiles, query, assignment, w.kd, w.mm, w.gt, w.nv, npx, 1.f / temperature, lambda_cos, lambda_l2,
               scale, nsup, d_query, reinterpret_cast<float4*>(w.row_stats),
-              w.r_part, w.loss_part, want_grad ? 1 : 0, accum};
+              w.r_part, w.loss_part, want_grad ? 1 : 0, accum, reinterpret_cast<float2*>(w.row_nd)};
   const size_t sm1 = (size_t)kRows * DS * 2 + (size_t)K * DS * 2 + (size_t)kRows * K * 2 + (size_t)K * K * 2 +
                      16 * 128 * 4;
   static bool attr1 = false;
@@ -775,6 +779,32 @@ void decoder_finish_tc(cudaStream_t st, DecoderWork& w, const float* atoms, cons
   sgemm(st, true, false, k, df, ds, 1.f, w.r_acc, k, proj, df, 1.f, d_atoms, df);
   sgemm(st, false, false, ds, df, k, 1.f, w.r_acc, k, atoms, df, 1.f, d_proj, df);
   w.tc_pending = false;
+}
+
+// Parity export: P[r][c] = e[r][c] * (1/sum_r), e read from the bf16 core-matrix tiles the
+// kernels wrote for the last frame (DEC1 with gradients, DL1 always), 1/sum from row_stats.y.
+__global__ void export_attention_kernel(const uint8_t* __restrict__ e_tiles, const float4* __restrict__ rs,
+                                        int64_t npx, int K, float* __restrict__ p) {
+  const int64_t chunks = npx * (K / 8);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < chunks; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / (K / 8);
+    const int c0 = (int)(i % (K / 8)) * 8;
+    const int64_t tile = r / kRows;
+    const int rr = (int)(r % kRows);
+    float v[8];
+    tc::ld_row8(e_tiles + (size_t)tile * kRows * K * 2, rr, c0, 16u * kRows, v);
+    const float inv = rs[r].y;
+    float4* dst = reinterpret_cast<float4*>(p + r * K + c0);
+    dst[0] = make_float4(v[0] * inv, v[1] * inv, v[2] * inv, v[3] * inv);
+    dst[1] = make_float4(v[4] * inv, v[5] * inv, v[6] * inv, v[7] * inv);
+  }
+}
+
+void decoder_export_attention(cudaStream_t st, const DecoderWork& w, int64_t npx, float* p_out) {
+  const int64_t chunks = npx * (w.k / 8);
+  export_attention_kernel<<<(unsigned)std::min<int64_t>((chunks + 255) / 256, 148 * 16), 256, 0, st>>>(
+      w.e_tiles, reinterpret_cast<const float4*>(w.row_stats), npx, (int)w.k, p_out);
+  count_launch();
 }
 
 }  // namespace lm

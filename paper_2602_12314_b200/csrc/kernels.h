@@ -105,6 +105,12 @@ struct DecoderWork {
   uint8_t* dl_ae = nullptr;    // ntiles x 128 x (K + NB) bf16: gram B operand (aliases buf2)
   float* dl_nu = nullptr;      // (K/256) x ntiles*128: partial e.T per 256-column unit
   float* dl_part = nullptr;    // gram partials
+  // parity export (latmap_session_set_parity_export): per-row (nu^2 = |F_hat|^2, dot = F_hat.F)
+  // as the bf16 kernels computed them, for the last decoded frame; the attention P of that frame
+  // is recoverable from e_tiles and row_stats (decoder_export_attention).
+  float* row_nd = nullptr;     // npx x 2
+  int32_t last_path = 0;       // decoder of the last decoded frame: 0 none, 1 fp32 SIMT, 2 fused tc, 3 staged tc
+  int64_t last_npx = 0;
 };
 void decoder_prepare(cudaStream_t st, DecoderWork& w, const float* atoms, const float* proj);
 // Fused feature loss + decoder backward for one frame (pixel mode). Accumulates into d_proj,
@@ -136,6 +142,9 @@ void decoder_frame_dl(cudaStream_t st, DecoderWork& w, const float* query, const
                       int64_t npx, const float* feats, int64_t n_set, const int64_t* nsup, const float* atoms,
                       float temperature, float lambda_cos, float lambda_l2, float scale, bool want_grad,
                       float* d_query, float* d_atoms, double* partials);
+// Attention P (npx x K fp32, row-major) of the last tcgen05-decoded frame: e (bf16, core-matrix
+// tiles) times 1/sum from row_stats.
+void decoder_export_attention(cudaStream_t st, const DecoderWork& w, int64_t npx, float* p_out);
 // Applies the step-accumulated A and R of the tcgen05 frames: d_atoms += A D + R^T W, d_proj += R D.
 void decoder_finish_tc(cudaStream_t st, DecoderWork& w, const float* atoms, const float* proj, float* d_proj,
                        float* d_atoms);
@@ -156,7 +165,7 @@ struct AdamBlock {
 };
 void adam_flat(cudaStream_t st, float* param, const float* grad, float* m, float* v, const AdamBlock* blocks,
                int nblocks, int64_t* steps, int64_t* skipped, const float* corr1, const float* corr2,
-               int32_t table_len, int32_t* flags, const int64_t* overflow);
+               int32_t table_len, int32_t* flags, const double* overflow, int64_t* overflow_steps);
 
 // Streaming k-means (kmeans.cu): device points / centres / atoms, host weights.
 cudaError_t kmeans_weighted(cudaStream_t st, const float* P, const float* W, int64_t n, int dim, int64_t k,

@@ -1,5 +1,5 @@
-"""tcgen05 (bf16, TMEM) decoder against the fp32 decoder path (itself pinned to the oracle in
-test_gpu_parity.py) on configs 1, 2 and 4 shapes: the fused on-chip kernels (DEC1/DEC2, K <= 256)
+"""tcgen05 (bf16, TMEM) decoder against the repo's fp32 decoder path on configs 1, 2 and 4 shapes
+(the direct pin to the CPU oracle is test_gpu_decoder_oracle.py): the fused on-chip kernels (DEC1/DEC2, K <= 256)
 and the staged large-K kernels (DL1-DL5, config 4's K = 1024, d_s = 64, 128 cells; forced on the
 config-2 shape too). bf16 bars (BASELINE north_star): loss terms
 within 2e-3 relative, decoder gradients norm-wise within 1e-2, cosine >= 0.999."""
@@ -55,13 +55,11 @@ def test_tc_decoder_matches_fp32(ctx, cfg_id, scale, path):
         assert ltc[k] == pytest.approx(l32[k], rel=2e-3, abs=1e-5), (k, ltc[k], l32[k])
     n, ds = w.map.n, w.map.features.shape[1]
     K, D = w.atoms.shape
-    offs = np.cumsum([0, 3 * n, 4 * n, 3 * n, 3 * n, n, ds * n, ds * D, K * D])
-    names = ["positions", "rotations", "colors", "log_scales", "opacity", "features", "d_proj", "d_atoms"]
-    for i, name in enumerate(names):
-        a, b = gtc[offs[i]:offs[i + 1]], g32[offs[i]:offs[i + 1]]
+    for name, (o, ln) in stc.grad_blocks().items():
+        a, b = gtc[o:o + ln], g32[o:o + ln]
         rel = np.linalg.norm(a - b) / (np.linalg.norm(b) + 1e-30)
-        assert cosine(a, b) >= 0.999 and rel <= 2e-2, (name, rel, cosine(a, b))
-        if name in ("features", "d_atoms"):
+        assert cosine(a, b) >= 0.999 and rel <= 1e-2, (name, rel, cosine(a, b))
+        if name in ("features", "atoms"):
             assert rel > 1e-7, (name, "bf16 path did not run")
 
 

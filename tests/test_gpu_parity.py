@@ -1,8 +1,9 @@
 """GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the same seeded
 inputs. Bars (BASELINE.json north_star / SURVEY.md §8(d)):
   - projected splats, tile lists and sort order: bit-exact;
-  - rendered colour / depth / query / alpha: |a-b| <= 1e-4 * max(|b|, 1e-3 * max|b|) (query in
-    fast mode, which sums on the tensor cores: floor 1e-2 * max|b|), and norm-wise <= 1e-4;
+  - rendered colour / depth / query / alpha: |a-b| <= 1e-4 * max(|b|, 1e-3 * max|b|), and
+    norm-wise <= 1e-4; the query in fast mode (tensor-core sums) adds the float summation-error
+    scale 2^-16 * sum_i w_i |f_i| per pixel (QUERY_COND below);
   - gradients: |a-b| <= 1e-3 * max(|b|, 1e-3 * ||b||_inf) per block (plus norm-wise);
   - decoded embeddings: per-row cosine >= 0.999.
 """
@@ -55,16 +56,38 @@ def gi(intr):
     return api.make_intrinsics(intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height)
 
 
-def assert_close_floor(a, b, rtol, name, floor=1e-3):
+def block_offsets(s):
+    """[(begin, end)] of the 8 flat-buffer blocks (16-byte aligned; latmap_session_grad_layout)."""
+    return [(o, o + n) for o, n in s.grad_blocks().values()]
+
+
+def assert_close_floor(a, b, rtol, name, floor=1e-3, cond=None):
+    """|a-b| <= rtol * max(|b|, floor * max|b|)  [+ cond: an extra per-element absolute allowance]."""
     a = np.asarray(a, np.float64)
     b = np.asarray(b, np.float64)
     scale = np.maximum(np.abs(b), floor * max(np.abs(b).max(), 1e-30))
-    err = np.abs(a - b) / scale
+    tol = rtol * scale if cond is None else rtol * scale + cond
+    err = np.abs(a - b) / tol
     worst = err.max() if err.size else 0.0
-    assert worst <= rtol, f"{name}: max scaled err {worst:.3e} > {rtol} (at {np.unravel_index(err.argmax(), err.shape)})"
+    assert worst <= 1.0, f"{name}: max err/tol {worst:.3e} (at {np.unravel_index(err.argmax(), err.shape)})"
     if b.size:
         nrm = np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
         assert nrm <= rtol, f"{name}: norm-wise err {nrm:.3e}"
+
+
+# Fast-mode query channels are summed on the tensor cores (3xTF32: each product exact to ~2^-21,
+# fp32 accumulation in a different order than the reference's sequential float loop). Where the
+# features cancel, |b| is far below the summed magnitude M(p) = sum_i w_i |f_i| and BOTH float sums
+# carry an absolute error of order n * 2^-24 * M(p) (n = blended splats, ~100 at config 0). The
+# bound adds that error scale, QUERY_COND * M(p) with QUERY_COND = 2^-16 (n * 2^-24 for n = 256),
+# to the 1e-4 relative / 1e-3 floor bar; M(p) is the oracle's render of the same map with |f|.
+QUERY_COND = 2.0 ** -16
+
+
+def query_magnitude(m, q, t, intr):
+    am = oracle.GaussianMap(m.positions, m.rotations, m.colors, m.log_scales, m.opacity_logits,
+                            np.abs(np.asarray(m.features, np.float32)))
+    return oracle.render(am, q, t, oi(intr), threads=THREADS)["query"]
 
 
 # ------------------------------------------------------------------------------- renderer
@@ -105,13 +128,15 @@ def test_render_images_match(ctx, cfg0, exact):
         out = api.render(ctx, api.GaussianMap.from_numpy(w.map), api.make_pose(), gi(w.intr))
     finally:
         ctx.set_exact_blend(False)
+    mag = query_magnitude(to_oracle_map(w.map), (1, 0, 0, 0), (0, 0, 0), w.intr)
     for f in ("color", "depth", "query", "alpha"):
         g = getattr(out, f).cpu().numpy()
-        # fast mode sums the query channels on the tensor cores (3xTF32, different order than the
-        # oracle's float loop): judged relative to 1% of the image's largest |value| where features
-        # cancel; exact mode keeps the tight floor
-        floor = 1e-2 if (f == "query" and not exact) else 1e-3
-        assert_close_floor(g, ref[f], 1e-4, f, floor=floor)
+        # exact mode: the tight bar alone; fast mode's query: plus the summation-error scale
+        cond = QUERY_COND * mag if (f == "query" and not exact) else None
+        assert_close_floor(g, ref[f], 1e-4, f, floor=1e-3, cond=cond)
+        if f == "query":
+            e = np.abs(g.astype(np.float64) - ref[f]) / np.maximum(mag, 1e-30)
+            print(f"query (exact={exact}): max |a-b| / M(p) = {e.max():.3e} (bound {QUERY_COND:.3e})")
         same = np.mean(g.view(np.uint32) == ref[f].astype(np.float32).view(np.uint32))
         if exact or f == "alpha":  # alpha is accumulated exactly in both modes
             assert same > 0.999, f"{f}: only {same:.5f} of values bit-identical"
@@ -126,8 +151,10 @@ def test_render_posed_camera(ctx):
     ref = oracle.render(to_oracle_map(m), q, t, oi(intr), threads=THREADS)
     out = api.render(ctx, api.GaussianMap.from_numpy(m), api.make_pose(q, t), gi(intr))
     assert np.array_equal(out.splats()["source"], ref["splats"]["source"])
+    mag = query_magnitude(to_oracle_map(m), q, t, intr)
     for f in ("color", "depth", "query", "alpha"):
-        assert_close_floor(getattr(out, f).cpu().numpy(), ref[f], 1e-4, f, floor=1e-2 if f == "query" else 1e-3)
+        assert_close_floor(getattr(out, f).cpu().numpy(), ref[f], 1e-4, f, floor=1e-3,
+                           cond=QUERY_COND * mag if f == "query" else None)
 
 
 def test_render_edge_cases(ctx):
@@ -299,19 +326,19 @@ def test_session_objective_config0(ctx, cfg0):
     assert loss["supervised_rows"] == ref["supervised_rows"]
     gb = s.grad_buffer().cpu().numpy()
     n, ds = w.map.n, w.map.features.shape[1]
-    offs = np.cumsum([0, 3 * n, 4 * n, 3 * n, 3 * n, n, ds * n, ds * w.proj.shape[1], w.atoms.size])
+    offs = block_offsets(s)
     # map gradients: against the fp32 reference path (identical render decisions)
     blocks = [g.positions, g.rotations, g.colors, g.log_scales, g.opacity_logits, g.features]
     for i, (name, ref_b) in enumerate(zip(oracle.FIELDS, blocks)):
-        assert_close_floor(gb[offs[i]:offs[i + 1]], ref_b.reshape(-1), 1e-3, name)
+        assert_close_floor(gb[offs[i][0]:offs[i][1]], ref_b.reshape(-1), 1e-3, name)
     # dictionary gradients: sums over 76.8k rows; judged against the double-precision truth on the
     # same rendered queries (the fp32 reference itself sits ~1e-3 away from it on small entries)
     _, _, q_img, _ = s.frame_images(0)
     tp, ta = dict_grads_f64(w, q_img.cpu().numpy(), w.lambdas)
-    assert_close_floor(gb[offs[6]:offs[7]], tp.reshape(-1), 1e-3, "d_proj")
-    assert_close_floor(gb[offs[7]:offs[8]], ta.reshape(-1), 1e-3, "d_atoms")
+    assert_close_floor(gb[offs[6][0]:offs[6][1]], tp.reshape(-1), 1e-3, "d_proj")
+    assert_close_floor(gb[offs[7][0]:offs[7][1]], ta.reshape(-1), 1e-3, "d_atoms")
     # and the fp32 reference agrees with the GPU norm-wise
-    for name, got, r in (("d_proj", gb[offs[6]:offs[7]], dp), ("d_atoms", gb[offs[7]:offs[8]], da)):
+    for name, got, r in (("d_proj", gb[offs[6][0]:offs[6][1]], dp), ("d_atoms", gb[offs[7][0]:offs[7][1]], da)):
         nrm = np.linalg.norm(got - r.reshape(-1)) / np.linalg.norm(r)
         assert nrm < 1e-3, (name, nrm)
 
@@ -462,11 +489,11 @@ def test_session_segment_supervision_config0(ctx, cfg0):
         assert loss[key] == pytest.approx(ref[key], rel=2e-4, abs=1e-6), key
     gb = s.grad_buffer().cpu().numpy()
     n, ds = w.map.n, w.map.features.shape[1]
-    offs = np.cumsum([0, 3 * n, 4 * n, 3 * n, 3 * n, n, ds * n, ds * w.proj.shape[1], w.atoms.size])
+    offs = block_offsets(s)
     blocks = [g.positions, g.rotations, g.colors, g.log_scales, g.opacity_logits, g.features]
     for i, (name, ref_b) in enumerate(zip(oracle.FIELDS, blocks)):
-        assert_close_floor(gb[offs[i]:offs[i + 1]], ref_b.reshape(-1), 1e-3, name)
-    for name, got, r in (("d_proj", gb[offs[6]:offs[7]], dp), ("d_atoms", gb[offs[7]:offs[8]], da)):
+        assert_close_floor(gb[offs[i][0]:offs[i][1]], ref_b.reshape(-1), 1e-3, name)
+    for name, got, r in (("d_proj", gb[offs[6][0]:offs[6][1]], dp), ("d_atoms", gb[offs[7][0]:offs[7][1]], da)):
         assert_close_floor(got, r.reshape(-1), 1e-3, name)
 
 
@@ -628,7 +655,7 @@ def test_objective_ragged_multiframe_unsupervised(ctx):
     assert loss["supervised_rows"] == ref["supervised_rows"]
     gb = s.grad_buffer().cpu().numpy()
     n, ds = w.map.n, w.map.features.shape[1]
-    offs = np.cumsum([0, 3 * n, 4 * n, 3 * n, 3 * n, n, ds * n])
+    offs = block_offsets(s)
     blocks = [g.positions, g.rotations, g.colors, g.log_scales, g.opacity_logits, g.features]
     for i, (name, ref_b) in enumerate(zip(oracle.FIELDS, blocks)):
-        assert_close_floor(gb[offs[i]:offs[i + 1]], ref_b.reshape(-1), 1e-3, name)
+        assert_close_floor(gb[offs[i][0]:offs[i][1]], ref_b.reshape(-1), 1e-3, name)
