@@ -26,8 +26,11 @@ static inline T lm_fabs(T x) { return fabs(x); }
 #else
 typedef float T;
 #define S(x) x##_f32
-/* std::exp(float) restated as the correctly rounded (float)exp((double)x). */
-static inline T lm_exp(T x) { return (float)exp((double)x); }
+/* std::exp(float) is what the reference calls (render.cpp:193,303, types.hpp:252-255): the C
+ * library's expf, the same function the compiled reference (oracle/_ref) uses on this image.
+ * (Round 1 used the correctly rounded (float)exp((double)x); libm differs from it on ~7e-5 of
+ * inputs.) */
+static inline T lm_exp(T x) { return expf(x); }
 /* float sqrt / abs stay in float (Eigen's array().sqrt(), std::abs on float). */
 static inline T lm_sqrt(T x) { return sqrtf(x); }
 static inline T lm_fabs(T x) { return fabsf(x); }
@@ -1520,7 +1523,7 @@ double lm_metric_miou(const float* emb, const int32_t* labels, int64_t n, int64_
     }
     float s = 0.f;
     for (int64_t k = 0; k < c; ++k) {
-      sc[k] = (float)exp((double)(sc[k] - m));
+      sc[k] = expf(sc[k] - m);
       s += sc[k];
     }
     int64_t pred = 0;

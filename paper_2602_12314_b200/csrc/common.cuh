@@ -1,5 +1,6 @@
 // common.cuh — shared device helpers for the latent-map step kernels (sm_100a).
 #pragma once
+#include "expf_ref.h"
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -18,9 +19,9 @@ __device__ __forceinline__ double dm(double a, double b) { return __dmul_rn(a, b
 __device__ __forceinline__ double da(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double ds_(double a, double b) { return __dsub_rn(a, b); }
 
-// std::exp(float) restated as the correctly rounded (float)exp((double)x) — the
-// oracle's definition; CUDA's double exp is accurate to < 1 ulp of double.
-__device__ __forceinline__ float exp_exact(float x) { return __double2float_rn(exp((double)x)); }
+// std::exp(float) bit for bit as the reference evaluates it on the CPU (glibc expf, restated in
+// expf_ref.h; checked on all 2^32 inputs) — the oracle calls the same libm function.
+__device__ __forceinline__ float exp_exact(float x) { return expf_ref(x); }
 
 // sigmoid, core/types.hpp:252-255
 __device__ __forceinline__ float sigmoid_exact(float x) {
