@@ -116,6 +116,12 @@ latmap_status latmap_ctx_set_exact_blend(latmap_ctx* ctx, int32_t exact);
  * proj/src/dictionary.cpp:25-83); results agree within the bf16 tolerances either way. */
 latmap_status latmap_ctx_set_decoder_path(latmap_ctx* ctx, int32_t path);
 const char* latmap_ctx_last_error(const latmap_ctx* ctx);
+/* Device memory for callers that hold only this header (the Eigen-typed drop-in layer):
+ * alloc / free (free synchronises the context stream) and copies on the context stream,
+ * direction 0 host->device, 1 device->host (synchronous), 2 device->device. */
+latmap_status latmap_device_alloc(latmap_ctx* ctx, int64_t bytes, void** out);
+latmap_status latmap_device_free(latmap_ctx* ctx, void* p);
+latmap_status latmap_copy(latmap_ctx* ctx, void* dst, const void* src, int64_t bytes, int32_t direction);
 /* The cudaStream_t the context's calls are ordered on (as void*). */
 void* latmap_ctx_stream(const latmap_ctx* ctx);
 /* Kernels launched by this context since creation (evidence for the bench). */
@@ -178,6 +184,25 @@ latmap_status latmap_trust_region_penalty(latmap_ctx* ctx, const float* atoms, c
 /* ssim, obj/losses.hpp:12-13; d_a optional (overwritten). Returns the mean SSIM in *value. */
 latmap_status latmap_ssim(latmap_ctx* ctx, const float* a, const float* b, int32_t h, int32_t w,
                           int32_t channels, float* d_a, float* value);
+
+/* rgb_loss, obj/losses.hpp:33-34 (losses.cpp:200-224): lambda_i1 mean|a - b| + lambda_i2 (1 - SSIM)/2
+ * over H x W x channels images (device). grad (device, may be NULL) receives the gradient w.r.t.
+ * `rendered`; value / l1 / ssim_loss are host floats (l1, ssim_loss may be NULL). */
+latmap_status latmap_rgb_loss(latmap_ctx* ctx, const float* rendered, const float* observed, int32_t h, int32_t w,
+                              int32_t channels, float lambda_i1, float lambda_i2, float* grad, float* value,
+                              float* l1, float* ssim_loss);
+/* depth_loss, obj/losses.hpp:38-40 (losses.cpp:226-255): mean |rendered - observed| over pixels
+ * with observed > 0 and alpha > 0.5; *flagged = 1 (value 0, grad all zero) when none qualifies.
+ * n = H x W; grad (device, may be NULL). */
+latmap_status latmap_depth_loss(latmap_ctx* ctx, const float* rendered, const float* observed, const float* alpha,
+                                int64_t n, float* grad, float* value, int32_t* flagged);
+/* feature_loss, obj/losses.hpp:43-58 (losses.cpp:257-294): terms = {value, cos_term, l2_term,
+ * trust_term} (host); d_reconstructed (n x embed_dim) and d_atoms_trust (k x embed_dim,
+ * lambda_trust-scaled) are device outputs, either may be NULL. */
+latmap_status latmap_feature_loss(latmap_ctx* ctx, const float* reconstructed, const float* target, int64_t n,
+                                  int32_t embed_dim, const float* atoms, const float* anchor, int64_t k, float delta,
+                                  float lambda_cos, float lambda_l2, float lambda_trust, float* d_reconstructed,
+                                  float* d_atoms_trust, float terms[4], int32_t* zero_norm_flagged);
 
 /* ---------------------------------------------------------------- optimiser */
 /* adam_step, obj/adam.hpp:61-79 on one device block. *step / *skipped are the host-side
@@ -470,6 +495,9 @@ const char* latmap_pipeline_last_error(const latmap_pipeline* p);
  * with A / B staged K-major (0) or MN-major (1); pins the UMMA descriptor conventions. */
 latmap_status latmap_selftest_umma(latmap_ctx* ctx, const float* a, const float* b, float* c, int32_t n,
                                    int32_t k, int32_t a_mn, int32_t b_mn);
+/* out[i] = the kernels' std::exp(float) (glibc expf restated, csrc/expf_ref.h) of the float whose
+ * bit pattern is first + i (device out, n floats): pins it to libm on every input. */
+latmap_status latmap_selftest_expf(latmap_ctx* ctx, uint64_t first, int64_t n, float* out);
 
 #ifdef __cplusplus
 }

@@ -169,6 +169,8 @@ def _declare(L):
     L.lm_mt64_seed.argtypes = [C.c_void_p, C.c_uint64]
     L.lm_oracle_set_gemm_threads.argtypes = [C.c_int]
     L.lm_oracle_set_gemm_threads.restype = None
+    L.lm_expf_bits.argtypes = [C.c_uint64, C.c_int64, C.c_void_p, C.c_int]
+    L.lm_expf_bits.restype = None
     L.lm_mt64_next.argtypes = [C.c_void_p]
     L.lm_mt64_next.restype = C.c_uint64
     L.lm_mt64_uniform01.argtypes = [C.c_void_p]
@@ -747,3 +749,10 @@ def query_scores(rec, embedding):
 def set_gemm_threads(n):
     """Row-split threads for the oracle's dense products (results are bit-identical for any n)."""
     lib().lm_oracle_set_gemm_threads(int(n))
+
+
+def expf_bits(first, n, threads=1):
+    """libm expf (the reference's std::exp(float)) of the floats with bit patterns first + i."""
+    out = np.empty(int(n), np.float32)
+    lib().lm_expf_bits(int(first), int(n), out.ctypes.data_as(C.c_void_p), int(threads))
+    return out

@@ -1477,6 +1477,52 @@ int S(lm_stream_kmeans_update)(const T* batch, int64_t n, int64_t dim, T* atoms,
 }
 
 #else /* LM_ONCE: voxel hash store, voxel_hash.cpp / active_set.cpp */
+/* libm expf (what the reference's std::exp(float) calls) of the floats with bit patterns
+ * first .. first + n - 1, split over threads: the checker of the device's restated expf. */
+typedef struct {
+  uint64_t first;
+  float* out;
+} expf_job;
+typedef struct {
+  void (*fn)(void*, int64_t, int64_t, int);
+  void* ctx;
+  int64_t b, e;
+  int tid;
+} once_job;
+static void* once_tramp(void* p) {
+  once_job* j = (once_job*)p;
+  j->fn(j->ctx, j->b, j->e, j->tid);
+  return NULL;
+}
+static void parallel_chunks_once(int64_t total, int threads, void (*fn)(void*, int64_t, int64_t, int), void* ctx) {
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  pthread_t th[256];
+  once_job jobs[256];
+  const int64_t chunk = (total + threads - 1) / threads;
+  int nt = 0;
+  for (int t = 0; t < threads; ++t) {
+    const int64_t b = t * chunk, e = b + chunk < total ? b + chunk : total;
+    if (b >= e) break;
+    jobs[nt] = (once_job){fn, ctx, b, e, t};
+    pthread_create(&th[nt], NULL, once_tramp, &jobs[nt]);
+    ++nt;
+  }
+  for (int t = 0; t < nt; ++t) pthread_join(th[t], NULL);
+}
+static void expf_chunk(void* pc, int64_t b, int64_t e, int tid) {
+  const expf_job* j = (const expf_job*)pc;
+  for (int64_t i = b; i < e; ++i) {
+    const uint32_t u = (uint32_t)(j->first + (uint64_t)i);
+    float x;
+    memcpy(&x, &u, 4);
+    j->out[i] = expf(x);
+  }
+}
+void lm_expf_bits(uint64_t first, int64_t n, float* out, int threads) {
+  expf_job j = {first, out};
+  parallel_chunks_once(n, threads, expf_chunk, &j);
+}
 int lm_oracle_gemm_threads_value = 1;
 void lm_oracle_set_gemm_threads(int n) { lm_oracle_gemm_threads_value = n < 1 ? 1 : (n > 256 ? 256 : n); }
 

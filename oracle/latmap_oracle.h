@@ -142,6 +142,8 @@ double lm_mt64_uniform01(void* r);
 /* Threads for the dense products (row-split; bit-identical for every count). Default 1, like
  * the reference's single-threaded Eigen (proj/CMakeLists.txt:11 links no OpenMP). */
 void lm_oracle_set_gemm_threads(int n);
+/* libm expf of the floats with bit patterns first .. first + n - 1 (threads split the range). */
+void lm_expf_bits(uint64_t first, int64_t n, float* out, int threads);
 
 /* ---- evaluation metrics (float, metrics.cpp:8-89, evaluate.cpp:74-88) ---- */
 double lm_metric_cos(const float* rec, const float* tgt, int64_t n, int64_t d, int32_t* flagged);

@@ -165,6 +165,14 @@ def _declare(L):
         "latmap_session_set_parity_export": [P, C.c_int32],
         "latmap_session_decoder_export": [P, C.POINTER(C.c_int32), C.POINTER(C.c_int64), P, P],
         "latmap_selftest_umma": [P, P, P, P, C.c_int32, C.c_int32, C.c_int32, C.c_int32],
+        "latmap_selftest_expf": [P, C.c_uint64, C.c_int64, P],
+        "latmap_device_alloc": [P, C.c_int64, C.POINTER(P)],
+        "latmap_device_free": [P, P],
+        "latmap_copy": [P, P, P, C.c_int64, C.c_int32],
+        "latmap_rgb_loss": [P, P, P, C.c_int32, C.c_int32, C.c_int32, C.c_float, C.c_float, P, P, P, P],
+        "latmap_depth_loss": [P, P, P, P, C.c_int64, P, P, P],
+        "latmap_feature_loss": [P, P, P, C.c_int64, C.c_int32, P, P, C.c_int64, C.c_float, C.c_float, C.c_float,
+                                C.c_float, P, P, P, P],
         "latmap_weighted_kmeans": [P, P, P, C.c_int64, C.c_int32, C.c_int64, P, P, P, C.c_int64, C.c_int32, P, P,
                                    C.POINTER(C.c_int32)],
         "latmap_session_stream_kmeans": [P, P, C.c_int64, C.c_float, P, P],
@@ -259,7 +267,9 @@ EXPORTED = ["latmap_ctx_create", "latmap_ctx_destroy", "latmap_ctx_set_stream", 
             "latmap_session_grad_buffer", "latmap_session_loss_buffer",
             "latmap_session_read_loss", "latmap_session_frame_images", "latmap_session_stats",
             "latmap_session_profile", "latmap_session_phase_times", "latmap_session_set_parity_export",
-            "latmap_session_decoder_export", "latmap_selftest_umma", "latmap_ctx_stream",
+            "latmap_session_decoder_export", "latmap_selftest_umma", "latmap_selftest_expf", "latmap_rgb_loss", "latmap_depth_loss", "latmap_device_alloc",
+            "latmap_device_free", "latmap_copy",
+            "latmap_feature_loss", "latmap_ctx_stream",
             "latmap_voxel_of", "latmap_hash_voxel", "latmap_store_create", "latmap_store_destroy", "latmap_store_size",
             "latmap_store_stats", "latmap_store_last_error", "latmap_store_insert", "latmap_store_update",
             "latmap_store_find", "latmap_store_get_records", "latmap_store_insert_global", "latmap_store_insert_keyed", "latmap_store_fetch_local",

@@ -275,6 +275,49 @@ def ssim(ctx, a, b, want_grad=False):
     return (v.value, da) if want_grad else v.value
 
 
+def rgb_loss(ctx, rendered, observed, lambda_i1, lambda_i2, want_grad=True):
+    """rgb_loss (obj/losses.hpp:33-34): {value, l1, ssim_loss, grad} on HxWxC device images."""
+    if rendered.shape != observed.shape:
+        raise _capi.InvalidArgument("rgb_loss: image shapes differ")
+    h, w = rendered.shape[:2]
+    ch = rendered.shape[2] if rendered.dim() == 3 else 1
+    g = torch.empty_like(rendered) if want_grad else None
+    v, l1, ss = C.c_float(), C.c_float(), C.c_float()
+    check(ctx.h, lib().latmap_rgb_loss(ctx.h, _ptr(rendered), _ptr(observed), h, w, ch, float(lambda_i1),
+                                       float(lambda_i2), _ptr(g), C.byref(v), C.byref(l1), C.byref(ss)))
+    return {"value": v.value, "l1": l1.value, "ssim_loss": ss.value, "grad": g}
+
+
+def depth_loss(ctx, rendered, observed, alpha, want_grad=True):
+    """depth_loss (obj/losses.hpp:38-40): {value, flagged, grad} on HxW device images."""
+    if rendered.shape != observed.shape or rendered.shape != alpha.shape:
+        raise _capi.InvalidArgument("depth_loss: image shapes differ")
+    g = torch.empty_like(rendered) if want_grad else None
+    v, fl = C.c_float(), C.c_int32()
+    check(ctx.h, lib().latmap_depth_loss(ctx.h, _ptr(rendered), _ptr(observed), _ptr(alpha), rendered.numel(),
+                                         _ptr(g), C.byref(v), C.byref(fl)))
+    return {"value": v.value, "flagged": bool(fl.value), "grad": g}
+
+
+def feature_loss(ctx, reconstructed, target, atoms, anchor, delta, lambda_cos, lambda_l2, lambda_trust,
+                 want_grad=True):
+    """feature_loss (obj/losses.hpp:43-58): {value, cos_term, l2_term, trust_term,
+    zero_norm_flagged, d_reconstructed, d_atoms_trust} on device rows."""
+    if reconstructed.shape != target.shape:
+        raise _capi.InvalidArgument("feature_loss: shape mismatch")
+    n, df = reconstructed.shape
+    k = atoms.shape[0]
+    dr = torch.empty_like(reconstructed) if want_grad else None
+    dt = torch.empty_like(atoms) if want_grad else None
+    terms = (C.c_float * 4)()
+    fl = C.c_int32()
+    check(ctx.h, lib().latmap_feature_loss(ctx.h, _ptr(reconstructed), _ptr(target), n, df, _ptr(atoms), _ptr(anchor),
+                                           k, float(delta), float(lambda_cos), float(lambda_l2), float(lambda_trust),
+                                           _ptr(dr), _ptr(dt), terms, C.byref(fl)))
+    return {"value": terms[0], "cos_term": terms[1], "l2_term": terms[2], "trust_term": terms[3],
+            "zero_norm_flagged": bool(fl.value), "d_reconstructed": dr, "d_atoms_trust": dt}
+
+
 # --------------------------------------------------------------------------- evaluation
 def gather_supervision(ctx, query, assignment, features, normalize=False):
     """gather_supervision, pixel mode (objective.cpp:16-35) on the device -> (queries n x ds,

@@ -546,6 +546,76 @@ static void corr_tables(std::vector<float>& c1, std::vector<float>& c2, int len)
 }
 static const int kCorrLen = 1 << 16;
 
+latmap_status latmap_device_alloc(latmap_ctx* ctx, int64_t bytes, void** out) {
+  if (!ctx || !out || bytes < 0) return LATMAP_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  if (bytes == 0) return LATMAP_OK;
+  cudaError_t e = cudaMalloc(out, (size_t)bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    return fail(ctx, LATMAP_ERR_OUT_OF_MEMORY, "device_alloc: out of device memory");
+  }
+  CTX_CHECK(ctx, e);
+  return LATMAP_OK;
+}
+
+latmap_status latmap_device_free(latmap_ctx* ctx, void* p) {
+  if (!ctx) return LATMAP_ERR_INVALID_ARGUMENT;
+  if (p) {
+    CTX_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+    CTX_CHECK(ctx, cudaFree(p));
+  }
+  return LATMAP_OK;
+}
+
+latmap_status latmap_copy(latmap_ctx* ctx, void* dst, const void* src, int64_t bytes, int32_t direction) {
+  if (!ctx || bytes < 0 || direction < 0 || direction > 2 || (bytes > 0 && (!dst || !src)))
+    return LATMAP_ERR_INVALID_ARGUMENT;
+  if (bytes == 0) return LATMAP_OK;
+  const cudaMemcpyKind kind =
+      direction == 0 ? cudaMemcpyHostToDevice : (direction == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice);
+  CTX_CHECK(ctx, cudaMemcpyAsync(dst, src, (size_t)bytes, kind, ctx->stream));
+  if (direction == 1) CTX_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
+  return LATMAP_OK;
+}
+
+latmap_status latmap_rgb_loss(latmap_ctx* ctx, const float* rendered, const float* observed, int32_t h, int32_t w,
+                              int32_t channels, float lambda_i1, float lambda_i2, float* grad, float* value,
+                              float* l1, float* ssim_loss) {
+  if (!ctx || h < 0 || w < 0 || channels < 1 || !value || ((int64_t)h * w > 0 && (!rendered || !observed)))
+    return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "rgb_loss: invalid arguments");
+  float out[3];
+  CTX_CHECK(ctx, rgb_loss_dev(ctx->stream, rendered, observed, h, w, channels, lambda_i1, lambda_i2, grad, out));
+  *value = out[0];
+  if (l1) *l1 = out[1];
+  if (ssim_loss) *ssim_loss = out[2];
+  return post_launch(ctx);
+}
+
+latmap_status latmap_depth_loss(latmap_ctx* ctx, const float* rendered, const float* observed, const float* alpha,
+                                int64_t n, float* grad, float* value, int32_t* flagged) {
+  if (!ctx || n < 0 || !value || !flagged || (n > 0 && (!rendered || !observed || !alpha)))
+    return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "depth_loss: invalid arguments");
+  int fl = 0;
+  CTX_CHECK(ctx, depth_loss_dev(ctx->stream, rendered, observed, alpha, n, grad, value, &fl));
+  *flagged = fl;
+  return post_launch(ctx);
+}
+
+latmap_status latmap_feature_loss(latmap_ctx* ctx, const float* reconstructed, const float* target, int64_t n,
+                                  int32_t embed_dim, const float* atoms, const float* anchor, int64_t k, float delta,
+                                  float lambda_cos, float lambda_l2, float lambda_trust, float* d_reconstructed,
+                                  float* d_atoms_trust, float terms[4], int32_t* zero_norm_flagged) {
+  if (!ctx || n < 0 || embed_dim < 1 || k < 0 || !terms || !zero_norm_flagged ||
+      (n > 0 && (!reconstructed || !target)) || (k > 0 && (!atoms || !anchor)))
+    return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "feature_loss: invalid arguments");
+  int fl = 0;
+  CTX_CHECK(ctx, feature_loss_dev(ctx->stream, reconstructed, target, n, embed_dim, atoms, anchor, k, delta, lambda_cos,
+                                  lambda_l2, lambda_trust, d_reconstructed, d_atoms_trust, terms, &fl));
+  *zero_norm_flagged = fl;
+  return post_launch(ctx);
+}
+
 latmap_status latmap_adam_step(latmap_ctx* ctx, float* param, const float* grad, float* m, float* v, int64_t count,
                                int64_t* step, int64_t* skipped, float lr, int32_t* applied) {
   if (!ctx || !param || !grad || !m || !v || !step || !skipped) return LATMAP_ERR_INVALID_ARGUMENT;
@@ -2067,6 +2137,12 @@ latmap_status latmap_selftest_umma(latmap_ctx* ctx, const float* a, const float*
                                    int32_t a_mn, int32_t b_mn) {
   if (!ctx || !a || !b || !c) return LATMAP_ERR_INVALID_ARGUMENT;
   if (umma_selftest(ctx->stream, a, b, c, n, k, a_mn, b_mn)) return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "bad shape");
+  return post_launch(ctx);
+}
+
+latmap_status latmap_selftest_expf(latmap_ctx* ctx, uint64_t first, int64_t n, float* out) {
+  if (!ctx || n < 0 || (n > 0 && !out)) return LATMAP_ERR_INVALID_ARGUMENT;
+  if (n > 0) expf_selftest(ctx->stream, first, n, out);
   return post_launch(ctx);
 }
 

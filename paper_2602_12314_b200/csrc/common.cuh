@@ -22,6 +22,12 @@ __device__ __forceinline__ double ds_(double a, double b) { return __dsub_rn(a, 
 // std::exp(float) bit for bit as the reference evaluates it on the CPU (glibc expf, restated in
 // expf_ref.h; checked on all 2^32 inputs) — the oracle calls the same libm function.
 __device__ __forceinline__ float exp_exact(float x) { return expf_ref(x); }
+// the same with the 2^(i/32) table staged in shared memory (load_exp_table; inner loops)
+__device__ __forceinline__ float exp_exact(float x, const uint64_t* s_tab) { return expf_ref(x, s_tab); }
+// stage kExp2Tab32 into a 32-entry shared array (threads 0..31; caller synchronises)
+__device__ __forceinline__ void load_exp_table(uint64_t* s_tab) {
+  if (threadIdx.x < 32) s_tab[threadIdx.x] = kExp2Tab32[threadIdx.x];
+}
 
 // sigmoid, core/types.hpp:252-255
 __device__ __forceinline__ float sigmoid_exact(float x) {

@@ -88,30 +88,38 @@ LM_EXPF_HD float lm_bits_float(uint32_t u) {
 #endif
 }
 
-LM_EXPF_HD float expf_ref(float x) {
+// `tab` (optional, device): a copy of the table in shared memory for kernels that evaluate the
+// exponential in their inner loop (an LDS instead of an L1 load); nullptr reads kExp2Tab32.
+LM_EXPF_HD float expf_ref(float x, const uint64_t* tab = nullptr) {
+  // branch-free: out-of-range / NaN inputs run the main path on a clamped argument and the
+  // special results are selected at the end (the blend evaluates whole warps of exponentials)
   const uint32_t ux = lm_float_bits(x);
-  if (ux == 0xc27c65d9u) return lm_bits_float(0x11fa2993u);  // x = -0x1.f8cbb2p+5: libm 0x1.f45326p-92
-  if (ux == 0x4202422fu) return lm_bits_float(0x56fc9f1cu);  // x =  0x1.04845ep+5: libm 0x1.f93e38p+46
-  if (!(x >= -0x1.9fe368p+6f)) return x != x ? x + x : 0.f;   // underflow (and -inf) -> 0; NaN stays NaN
-  if (x > 0x1.62e42ep+6f) return x + 0x1p127f * 0x1p127f;     // overflow -> +inf
+  const bool under = !(x >= -0x1.9fe368p+6f);  // libm underflows to 0 below this (and -inf, NaN)
+  const bool over = x > 0x1.62e42ep+6f;        // and overflows to +inf above this
+  const float xc = under ? -0x1.9fe368p+6f : (over ? 0x1.62e42ep+6f : x);
   const double kInvLn2N = 0x1.71547652b82fep+0 * 32, kShift = 0x1.8p+52;
   const double kC0 = 0x1.c6af84b912394p-5 / 32 / 32 / 32, kC1 = 0x1.ebfce50fac4f3p-3 / 32 / 32,
                kC2 = 0x1.62e42ff0c52d6p-1 / 32;
 #ifdef __CUDA_ARCH__
   // explicit roundings: no contraction of the k rounding (z is used twice) on the device
-  const double z = __dmul_rn(kInvLn2N, (double)x);
+  const double z = __dmul_rn(kInvLn2N, (double)xc);
   double kd = __dadd_rn(z, kShift);  // round to nearest integer (it sits in the low mantissa bits)
   const uint64_t ki = lm_double_to_bits(kd);
   kd = __dsub_rn(kd, kShift);
   const double r = __dsub_rn(z, kd);
 #else
-  const double z = kInvLn2N * (double)x;
+  const double z = kInvLn2N * (double)xc;
   double kd = z + kShift;
   const uint64_t ki = lm_double_to_bits(kd);
   kd -= kShift;
   const double r = z - kd;
 #endif
+#ifdef __CUDA_ARCH__
+  const uint64_t t = (tab ? tab[ki & 31] : expf_tab((uint32_t)(ki & 31))) + (ki << 47);
+#else
+  (void)tab;
   const uint64_t t = expf_tab((uint32_t)(ki & 31)) + (ki << 47);
+#endif
   const double s = lm_bits_to_double(t);
   // the cubic with fused multiply-adds on host and device (fused or not, every float result is
   // the same; the tests check this form)
@@ -120,7 +128,13 @@ LM_EXPF_HD float expf_ref(float x) {
   double y = fma(kC2, r, 1.0);
   y = fma(p, r2, y);
   y = y * s;
-  return (float)y;
+  float res = (float)y;
+  res = under ? (x != x ? x : 0.f) : res;
+  res = over ? __builtin_huge_valf() : res;
+  // the two inputs libm rounds the other way (found by the exhaustive check)
+  res = ux == 0xc27c65d9u ? lm_bits_float(0x11fa2993u) : res;  // x = -0x1.f8cbb2p+5: 0x1.f45326p-92
+  res = ux == 0x4202422fu ? lm_bits_float(0x56fc9f1cu) : res;  // x =  0x1.04845ep+5: 0x1.f93e38p+46
+  return res;
 }
 
 }  // namespace lm

@@ -67,6 +67,16 @@ void image_losses(cudaStream_t st, const float* color, const float* depth, const
 double ssim_host(cudaStream_t st, const float* a, const float* b, int h, int w, int c, float* d_a,
                  float* scratch);
 size_t ssim_scratch_floats(int h, int w, int c);
+// Standalone loss operators (losses.hpp:12-58): device images / rows in, host scalars out; the
+// gradient pointers may be NULL. out = {value, l1, ssim_loss} / {value, cos, l2, trust}.
+cudaError_t rgb_loss_dev(cudaStream_t st, const float* rendered, const float* observed, int h, int w, int ch,
+                         float lambda_i1, float lambda_i2, float* grad, float out[3]);
+cudaError_t depth_loss_dev(cudaStream_t st, const float* rendered, const float* observed, const float* alpha,
+                           int64_t n, float* grad, float* value, int* flagged);
+cudaError_t feature_loss_dev(cudaStream_t st, const float* rec, const float* tgt, int64_t n, int df,
+                             const float* atoms, const float* anchor, int64_t k, float delta, float lambda_cos,
+                             float lambda_l2, float lambda_trust, float* d_rec, float* d_atoms_trust, float out[4],
+                             int* zero_norm_flagged);
 
 // Generic SIMT SGEMM: C = alpha * op(A) * op(B) + beta * C, row-major; split-K via atomics when
 // `split` > 1 (then beta must be applied by the caller beforehand, beta ignored).
@@ -185,6 +195,7 @@ cudaError_t gather_supervision_dev(cudaStream_t st, const float* query, int ds, 
                                    const float* feats, int df, bool normalize, float* q_out, float* t_out,
                                    int64_t* pix, int64_t cap, int64_t* n_rows);
 
+void expf_selftest(cudaStream_t st, uint64_t first, int64_t n, float* out);
 int umma_selftest(cudaStream_t st, const float* A, const float* B, float* C, int N, int K, int a_mn, int b_mn);
 
 void set_launch_counter(int64_t* c);

@@ -392,4 +392,173 @@ void image_losses(cudaStream_t st, const float* color, const float* depth, const
   }
 }
 
+
+// ---------------------------------------------------------------- standalone losses (C-ABI)
+// rgb_loss / depth_loss / feature_loss, obj/losses.hpp:12-58 (proj/src/losses.cpp:200-294), as
+// separate device operators on caller-owned images / rows. The step fuses these into the frame
+// loop (image_losses above, the decoders' epilogues); these are the reference's operator API.
+namespace {
+
+__global__ void __launch_bounds__(256) rgb_l1_kernel(const float* __restrict__ a, const float* __restrict__ b,
+                                                     int64_t n, float lambda_i1, float* grad, double* sum) {
+  double l1 = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float d = fs(a[i], b[i]);
+    l1 += (double)fabsf(d);
+    if (grad) grad[i] = fd(fm(lambda_i1, d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f)), (float)n);
+  }
+  block_add_double(l1, sum);
+}
+
+__global__ void __launch_bounds__(256) depth_sum_kernel(const float* __restrict__ r, const float* __restrict__ o,
+                                                        const float* __restrict__ al, int64_t n, double* acc) {
+  double sum = 0.0, cnt = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (o[i] > 0.f && al[i] > 0.5f) {
+      sum += (double)fabsf(fs(r[i], o[i]));
+      cnt += 1.0;
+    }
+  block_add_double(sum, &acc[0]);
+  block_add_double(cnt, &acc[1]);
+}
+
+__global__ void depth_grad_kernel(const float* __restrict__ r, const float* __restrict__ o,
+                                  const float* __restrict__ al, int64_t n, const double* acc, float* grad) {
+  const float valid = (float)acc[1];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float g = 0.f;
+    if (valid > 0.f && o[i] > 0.f && al[i] > 0.5f) {
+      const float d = fs(r[i], o[i]);
+      g = fd(d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f), valid);
+    }
+    grad[i] = g;
+  }
+}
+
+// one warp per row: |u|, |v|, u.v, |u - v|^2 (float, lane-strided), then the row gradient
+// dF = lambda_cos (-(v / (|u||v|) - dot u / (|u|^3 |v|))) / n + lambda_l2 2 (u - v) / n
+__global__ void __launch_bounds__(256) feature_rows_kernel(const float* __restrict__ u, const float* __restrict__ v,
+                                                           int64_t n, int df, float lambda_cos, float lambda_l2,
+                                                           float* d_rec, double* acc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  double cos_acc = 0.0, l2_acc = 0.0, flag = 0.0;
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
+    const float* ur = u + r * df;
+    const float* vr = v + r * df;
+    float uu = 0.f, vv = 0.f, uv = 0.f, dd = 0.f;
+    for (int c = lane; c < df; c += 32) {
+      const float a = ur[c], b = vr[c];
+      uu = fmaf(a, a, uu);
+      vv = fmaf(b, b, vv);
+      uv = fmaf(a, b, uv);
+      const float e = a - b;
+      dd = fmaf(e, e, dd);
+    }
+    uu = warp_sum(uu);
+    vv = warp_sum(vv);
+    uv = warp_sum(uv);
+    dd = warp_sum(dd);
+    const float eps = 1e-8f, nu = sqrtf(uu), nv = sqrtf(vv);
+    const float nug = fmaxf(nu, eps), nvg = fmaxf(nv, eps);
+    if (lane == 0) {
+      if (nu < eps || nv < eps) flag = 1.0;
+      cos_acc += 1.0 - (double)(uv / (nug * nvg));
+      l2_acc += (double)dd;
+    }
+    if (d_rec) {
+      const float inv_n = 1.f / (float)n;
+      const float a_u = lambda_cos * uv / (nug * nug * nug * nvg) * inv_n + 2.f * lambda_l2 * inv_n;
+      const float a_v = -lambda_cos / (nug * nvg) * inv_n - 2.f * lambda_l2 * inv_n;
+      float* gr = d_rec + r * df;
+      for (int c = lane; c < df; c += 32) gr[c] = fmaf(a_u, ur[c], a_v * vr[c]);
+    }
+  }
+  block_add_double(cos_acc, &acc[0]);
+  block_add_double(l2_acc, &acc[1]);
+  block_add_double(flag, &acc[2]);
+}
+
+}  // namespace
+
+cudaError_t rgb_loss_dev(cudaStream_t st, const float* rendered, const float* observed, int h, int w, int ch,
+                         float lambda_i1, float lambda_i2, float* grad, float out[3]) {
+  const int64_t n = (int64_t)h * w * ch;
+  double* acc = nullptr;
+  float* scratch = nullptr;
+  cudaError_t e = cudaMallocAsync(&acc, sizeof(double) * 2, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&scratch, sizeof(float) * std::max<size_t>(ssim_scratch_floats(h, w, ch), 1), st);
+  if (e != cudaSuccess) return e;
+  cudaMemsetAsync(acc, 0, sizeof(double) * 2, st);
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  if (n > 0) {
+    rgb_l1_kernel<<<grid, 256, 0, st>>>(rendered, observed, n, lambda_i1, grad, &acc[0]);
+    count_launch();
+    // SSIM always (losses.cpp:217); its adjoint is added into grad scaled by -lambda_i2 / 2
+    ssim_run(st, rendered, observed, h, w, ch, grad, lambda_i2 * -0.5f, true, scratch, &acc[1]);
+  }
+  double hv[2] = {0, 0};
+  cudaMemcpyAsync(hv, acc, sizeof(hv), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(acc, st);
+  cudaFreeAsync(scratch, st);
+  e = cudaStreamSynchronize(st);
+  const float l1 = n > 0 ? (float)(hv[0] / (double)n) : 0.f;
+  const float ss = n > 0 ? (float)(hv[1] / (double)n) : 1.f;
+  out[1] = l1;
+  out[2] = (1.f - ss) / 2.f;
+  out[0] = lambda_i1 * out[1] + lambda_i2 * out[2];
+  return e;
+}
+
+cudaError_t depth_loss_dev(cudaStream_t st, const float* rendered, const float* observed, const float* alpha,
+                           int64_t n, float* grad, float* value, int* flagged) {
+  double* acc = nullptr;
+  cudaError_t e = cudaMallocAsync(&acc, sizeof(double) * 2, st);
+  if (e != cudaSuccess) return e;
+  cudaMemsetAsync(acc, 0, sizeof(double) * 2, st);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
+  if (n > 0) {
+    depth_sum_kernel<<<grid, 256, 0, st>>>(rendered, observed, alpha, n, acc);
+    count_launch();
+    if (grad) {
+      depth_grad_kernel<<<grid, 256, 0, st>>>(rendered, observed, alpha, n, acc, grad);
+      count_launch();
+    }
+  }
+  double hv[2] = {0, 0};
+  cudaMemcpyAsync(hv, acc, sizeof(hv), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(acc, st);
+  e = cudaStreamSynchronize(st);
+  *flagged = hv[1] == 0.0;
+  *value = hv[1] > 0.0 ? (float)(hv[0] / hv[1]) : 0.f;
+  return e;
+}
+
+cudaError_t feature_loss_dev(cudaStream_t st, const float* rec, const float* tgt, int64_t n, int df,
+                             const float* atoms, const float* anchor, int64_t k, float delta, float lambda_cos,
+                             float lambda_l2, float lambda_trust, float* d_rec, float* d_atoms_trust, float out[4],
+                             int* zero_norm_flagged) {
+  double* acc = nullptr;
+  cudaError_t e = cudaMallocAsync(&acc, sizeof(double) * 4, st);
+  if (e != cudaSuccess) return e;
+  cudaMemsetAsync(acc, 0, sizeof(double) * 4, st);
+  if (n > 0) {
+    const int grid = (int)std::min<int64_t>((n + 7) / 8, 148 * 16);
+    feature_rows_kernel<<<grid, 256, 0, st>>>(rec, tgt, n, df, lambda_cos, lambda_l2, d_rec, acc);
+    count_launch();
+  }
+  if (d_atoms_trust) cudaMemsetAsync(d_atoms_trust, 0, sizeof(float) * k * df, st);
+  trust_region(st, atoms, anchor, k, df, delta, d_atoms_trust, lambda_trust, &acc[3]);
+  double hv[4] = {0, 0, 0, 0};
+  cudaMemcpyAsync(hv, acc, sizeof(hv), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(acc, st);
+  e = cudaStreamSynchronize(st);
+  out[1] = n > 0 ? (float)(hv[0] / (double)n) : 0.f;  // cos_term
+  out[2] = n > 0 ? (float)(hv[1] / (double)n) : 0.f;  // l2_term
+  out[3] = (float)hv[3];                              // trust_term
+  out[0] = lambda_cos * out[1] + lambda_l2 * out[2] + lambda_trust * out[3];
+  *zero_norm_flagged = hv[2] != 0.0;
+  return e;
+}
+
 }  // namespace lm

@@ -579,7 +579,9 @@ __global__ void __launch_bounds__(kTilePixels) raster_fwd_kernel(RasterArgs a) {
   __shared__ float s_col[kFwdBatch * 3];
   __shared__ float s_feat[kFwdBatch * DSP];
   __shared__ int32_t s_max;
+  __shared__ uint64_t s_etab[32];
   if (a.counters[2]) return;
+  load_exp_table(s_etab);  // published by the first __syncthreads_and of the batch loop
   const int tile = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
   const int px = (tile % a.tiles_x) * kTile + (threadIdx.x % kTile);
   const int py = (tile / a.tiles_x) * kTile + (threadIdx.x / kTile);
@@ -615,7 +617,7 @@ __global__ void __launch_bounds__(kTilePixels) raster_fwd_kernel(RasterArgs a) {
         const float dx = fs(fx, s.mean_x);
         const float dy = fs(fy, s.mean_y);
         const float rho = fa(fa(fm(fm(s.a00, dx), dx), fm(fm(fm(2.f, s.a01), dx), dy)), fm(fm(s.a11, dy), dy));
-        float al = fm(s.alpha, exp_exact(fm(-0.5f, rho)));
+        float al = fm(s.alpha, exp_exact(fm(-0.5f, rho), s_etab));
         if (al > kAlphaMax) al = kAlphaMax;
         const float w = fm(al, T);
         if (EXACT) {
@@ -724,7 +726,9 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_fwd_mma_kernel(RasterAr
   __shared__ float4 s_sp[FB][3];            // {mean_x, mean_y, a00, 2 a01} {a11, alpha, depth, -} {bbox}
   __shared__ float s_col[FB * 3];
   __shared__ int32_t s_max;
+  __shared__ uint64_t s_etab[32];
   if (a.counters[2]) return;
+  load_exp_table(s_etab);  // published by the batch loop's barriers before first use
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, cq = lane & 3;
   const int tile = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
@@ -829,7 +833,7 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_fwd_mma_kernel(RasterAr
             const float dx = fs(fx, s0.x);
             const float dy = fs(fy, s0.y);
             const float rho = fa(fa(fm(fm(s0.z, dx), dx), fm(fm(s0.w, dx), dy)), fm(fm(s1.x, dy), dy));
-            float al = fm(s1.y, exp_exact(fm(-0.5f, rho)));
+            float al = fm(s1.y, exp_exact(fm(-0.5f, rho), s_etab));
             alv[u] = al > kAlphaMax ? kAlphaMax : al;
           }
         }

@@ -3,6 +3,7 @@
 // C[128 x N] = A[128 x K] * B[N x K]^T with either operand staged K-major or MN-major.
 #include <cuda_runtime.h>
 
+#include "expf_ref.h"
 #include "kernels.h"
 #include "tc_common.cuh"
 
@@ -73,6 +74,16 @@ int umma_selftest(cudaStream_t st, const float* A, const float* B, float* C, int
   umma_probe_kernel<<<1, 128, smem, st>>>(A, B, C, N, K, a_mn, b_mn);
   count_launch();
   return 0;
+}
+
+// exp_exact (expf_ref.h) on the float with bit pattern first + i, i < n
+__global__ void expf_probe_kernel(uint64_t first, int64_t n, float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = expf_ref(__uint_as_float((uint32_t)(first + (uint64_t)i)));
+}
+void expf_selftest(cudaStream_t st, uint64_t first, int64_t n, float* out) {
+  expf_probe_kernel<<<148 * 16, 256, 0, st>>>(first, n, out);
+  count_launch();
 }
 
 }  // namespace lm
