@@ -78,6 +78,7 @@ def lib():
                                                 C.c_int32]
         L.latmap_ref_session_create.restype = P
         L.latmap_ref_session_step.argtypes = [P, C.POINTER(Loss)]
+        L.latmap_ref_session_objective.argtypes = [P, C.POINTER(Loss)]
         L.latmap_ref_session_get.argtypes = [P, P, P, P]
         L.latmap_ref_session_destroy.argtypes = [P]
         _lib = L
@@ -192,6 +193,12 @@ class Session:
     def step(self):
         loss = Loss()
         _check(lib().latmap_ref_session_step(self.h, C.byref(loss)))
+        return loss.as_dict()
+
+    def objective(self):
+        """total_objective with gradients, no optimiser step."""
+        loss = Loss()
+        _check(lib().latmap_ref_session_objective(self.h, C.byref(loss)))
         return loss.as_dict()
 
     def get(self):

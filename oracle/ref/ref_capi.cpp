@@ -248,6 +248,24 @@ int latmap_ref_session_step(void* h, latmap_ref_loss* loss) {
   }
 }
 
+// total_objective alone (with gradients) on the session's state, no optimiser step.
+int latmap_ref_session_objective(void* h, latmap_ref_loss* loss) {
+  auto* s = static_cast<Session*>(h);
+  try {
+    std::vector<const Keyframe*> batch;
+    for (const auto& f : s->frames) batch.push_back(&f);
+    ObjectiveOptions<float> opts;
+    opts.threads = s->threads;
+    ObjectiveGrads<float> g;
+    const LossBreakdown<float> l = total_objective(s->map, s->dict, batch, s->intr, s->cfg, &g, opts);
+    if (loss) copy_loss(l, loss);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
 // The map after the session's steps, flat like the map gradients; the dictionary's atoms / proj.
 int latmap_ref_session_get(void* h, float* map_flat, float* atoms, float* proj) {
   auto* s = static_cast<Session*>(h);
