@@ -495,6 +495,8 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="sharded", choices=["sharded", "allreduce"],
+                    help="N>1: ZeRO-1 sharded Adam (default) or all-reduce + replicated Adam")
     ap.add_argument("--cpu-full-frame", action="store_true",
                     help="reference arm: also time one whole keyframe to check the row-band model")
     ap.add_argument("--profile-phases", type=int, default=1)
@@ -586,8 +588,16 @@ def main():
             comm, collective = None, f"torch.distributed.all_reduce (library comm unavailable: {e})"
         config["collective"] = collective
 
+    sharded_adam = args.exchange == "sharded" and comm is not None
+    if world > 1:
+        config["exchange"] = ("ZeRO-1: reduce-scatter grads, shard check, all-reduce loss partials, Adam on the "
+                              "rank's shard, all-gather params (latmap_session_exchange_sharded)" if sharded_adam
+                              else "all-reduce grads + loss partials, replicated Adam")
+
     def exchange(sess):
-        if comm is not None:
+        if sharded_adam:
+            comm.session_exchange_sharded(sess)
+        elif comm is not None:
             comm.session_allreduce(sess)
         else:
             dist.all_reduce(grads)
@@ -596,7 +606,7 @@ def main():
     def one_step(read=False):
         if world == 1:
             return s.step(read=read)
-        return s.sharded_step(exchange, read=read)
+        return s.sharded_step(exchange, read=read, apply=not sharded_adam)
 
     stream = torch.cuda.current_stream()
     first = one_step(read=True)  # sizes the tile buffers

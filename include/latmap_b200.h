@@ -293,7 +293,8 @@ latmap_status latmap_session_frame_images(latmap_session* s, int32_t frame, floa
 /* Host-only (no device): the LossBreakdown of a batch from its loss-partials vector (the layout
  * latmap_session_loss_buffer exposes: kPart = 8 doubles per global frame slot [l1 sum, SSIM sum,
  * depth |err| sum, valid depth count, (1 - cos) sum, |F_hat - F|^2 sum, zero-norm flag,
- * supervised rows], then the trust penalty), with inv_b = 1 / nframes (objective.cpp:77,187-190).
+ * supervised rows], then a 16-double tail: trust penalty, overflow flag, the 8 Adam blocks' skip
+ * flags), with inv_b = 1 / nframes (objective.cpp:77,187-190).
  * The sharded step's all-reduced partials assemble to the full batch's breakdown. */
 latmap_status latmap_loss_assemble(const double* partials, int32_t nframes, int32_t width, int32_t height,
                                    const latmap_config* cfg, latmap_loss_breakdown* out);
@@ -304,6 +305,18 @@ latmap_status latmap_loss_assemble(const double* partials, int32_t nframes, int3
 latmap_status latmap_session_check_overflow(latmap_session* s, int32_t* any);
 /* Sticky count of Adam steps skipped because a tile list overflowed (since session creation). */
 latmap_status latmap_session_overflow_steps(latmap_session* s, int64_t* count);
+/* Sharded optimiser step (ZeRO-1 over the keyframe-sharded objective). The flat buffers split into
+ * nranks 4-aligned shards; rank r owns [*begin, *end). */
+latmap_status latmap_session_shard_range(const latmap_session* s, int32_t nranks, int32_t rank, int64_t* begin,
+                                         int64_t* end);
+/* Per-block non-finite flags (adam.hpp:65-68) of the gradient range [begin, end) into the loss
+ * partials' tail (slots 2..9 after the trust and overflow slots); the partials all-reduce ORs them. */
+latmap_status latmap_session_shard_check(latmap_session* s, int64_t begin, int64_t end);
+/* MapOptimizer::step_map + step_dict restricted to the flat range [begin, end), taking the skip
+ * flags from the (all-reduced) partials tail; step counters advance as in the full step. */
+latmap_status latmap_session_apply_range(latmap_session* s, int64_t begin, int64_t end);
+/* The flat parameter buffer (device; same layout as the gradients). */
+latmap_status latmap_session_params_buffer(latmap_session* s, float** params, int64_t* count);
 /* Parity export of the bf16 tcgen05 decoders (the reference returns F_hat,
  * proj/src/dictionary.cpp:45,52; the fused kernels never materialise it). While enabled, DEC1 /
  * DL3 also store each row's (nu^2 = |F_hat|^2, dot = F_hat.F) as the kernels computed them. */
@@ -430,6 +443,9 @@ latmap_status latmap_comm_allreduce(latmap_comm* comm, void* buf, int64_t count,
 /* The sharded iteration's exchange: the session's flat gradient buffer and loss partials summed
  * over ranks (one NCCL group), between latmap_session_objective and latmap_session_apply. */
 latmap_status latmap_session_allreduce(latmap_session* s, latmap_comm* comm);
+/* The sharded exchange + step: reduce-scatter of the gradients, shard check, all-reduce of the loss
+ * partials, Adam on this rank's shard, all-gather of the parameters (replaces allreduce + apply). */
+latmap_status latmap_session_exchange_sharded(latmap_session* s, latmap_comm* comm);
 
 /* ---------------------------------------------------------------- pipeline (the step's caller) */
 /* The pipeline-level subset of latmap::Config (core/config.hpp:10-58; same defaults via

@@ -197,6 +197,11 @@ def _declare(L):
         "latmap_loss_assemble": [P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(Config), C.POINTER(LossBreakdown)],
         "latmap_session_check_overflow": [P, C.POINTER(C.c_int32)],
         "latmap_session_grad_layout": [P, P, P],
+        "latmap_session_shard_range": [P, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
+        "latmap_session_shard_check": [P, C.c_int64, C.c_int64],
+        "latmap_session_apply_range": [P, C.c_int64, C.c_int64],
+        "latmap_session_params_buffer": [P, C.POINTER(P), C.POINTER(C.c_int64)],
+        "latmap_session_exchange_sharded": [P, P],
         "latmap_session_overflow_steps": [P, C.POINTER(C.c_int64)],
         "latmap_pipeline_create": [P, C.POINTER(Config), C.POINTER(PipelineConfig), C.POINTER(Intrinsics),
                                    C.POINTER(P)],
@@ -281,7 +286,9 @@ EXPORTED = ["latmap_ctx_create", "latmap_ctx_destroy", "latmap_ctx_set_stream", 
             "latmap_pipeline_session", "latmap_pipeline_store", "latmap_pipeline_state", "latmap_pipeline_active_set",
             "latmap_pipeline_last_error", "latmap_comm_unique_id", "latmap_comm_init",
             "latmap_comm_destroy", "latmap_comm_allreduce", "latmap_session_allreduce", "latmap_loss_assemble",
-            "latmap_session_check_overflow", "latmap_session_overflow_steps", "latmap_session_grad_layout"]
+            "latmap_session_check_overflow", "latmap_session_overflow_steps", "latmap_session_grad_layout",
+            "latmap_session_shard_range", "latmap_session_shard_check", "latmap_session_apply_range",
+            "latmap_session_params_buffer", "latmap_session_exchange_sharded"]
 
 
 def check(ctx_handle, status):

@@ -435,11 +435,14 @@ def adam_step(ctx, param, grad, st: AdamState, lr):
     return bool(ap.value)
 
 
+LOSS_TAIL = 16  # partials tail after the 8-double frame slots: trust, overflow, 8 Adam skip flags
+
+
 def assemble_loss(partials, width, height, cfg) -> dict:
     """Host-side LossBreakdown of a batch from its loss-partials vector (latmap_loss_assemble;
-    nframes = (len - 8) / 8 global frame slots followed by the trust slot). No device needed."""
+    nframes = (len - 16) / 8 global frame slots followed by the 16-double tail). No device needed."""
     p = np.ascontiguousarray(partials, np.float64)
-    nframes = (p.size - 8) // 8
+    nframes = (p.size - LOSS_TAIL) // 8
     out = LossBreakdown()
     check(None, lib().latmap_loss_assemble(p.ctypes.data_as(C.c_void_p), nframes, int(width), int(height),
                                             C.byref(cfg), C.byref(out)))
@@ -680,7 +683,24 @@ class Session:
         check(self.ctx.h, lib().latmap_session_overflow_steps(self.h, C.byref(n)))
         return int(n.value)
 
-    def sharded_step(self, exchange, read=False, attempts=3):
+    def shard_range(self, nranks, rank):
+        b, e = C.c_int64(), C.c_int64()
+        check(self.ctx.h, lib().latmap_session_shard_range(self.h, int(nranks), int(rank), C.byref(b), C.byref(e)))
+        return b.value, e.value
+
+    def shard_check(self, begin, end):
+        check(self.ctx.h, lib().latmap_session_shard_check(self.h, int(begin), int(end)))
+
+    def apply_range(self, begin, end):
+        """Adam on the flat range [begin, end) with the all-reduced skip flags (sharded step)."""
+        check(self.ctx.h, lib().latmap_session_apply_range(self.h, int(begin), int(end)))
+
+    def params_buffer(self):
+        p, n = C.c_void_p(), C.c_int64()
+        check(self.ctx.h, lib().latmap_session_params_buffer(self.h, C.byref(p), C.byref(n)))
+        return _device_view(p.value, n.value, torch.float32, self.ctx.device, owner=self)
+
+    def sharded_step(self, exchange, read=False, attempts=3, apply=True):
         """One keyframe-sharded Stage-I iteration: this rank's objective (global batch
         mean, set_batch), ``exchange(self)`` summing gradients and loss partials over ranks (e.g.
         Comm.session_allreduce), then the identical Adam on every rank. With ``read`` the step is
@@ -689,7 +709,8 @@ class Session:
         for _ in range(attempts):
             self.objective(want_grad=True, read=False)
             exchange(self)
-            self.apply()
+            if apply:
+                self.apply()
             if not read:
                 return None
             if not self.check_overflow():
@@ -1018,3 +1039,8 @@ class Comm:
     def session_allreduce(self, s: Session):
         """The sharded iteration's exchange: gradients and loss partials summed over ranks."""
         check(self.ctx.h, lib().latmap_session_allreduce(s.h, self.h))
+
+    def session_exchange_sharded(self, s: Session):
+        """ZeRO-1 exchange + step: reduce-scatter, shard check, partials all-reduce, Adam on the
+        shard, all-gather (replaces session_allreduce + Session.apply)."""
+        check(self.ctx.h, lib().latmap_session_exchange_sharded(s.h, self.h))

@@ -179,9 +179,26 @@ __global__ void adam_finish_kernel(Blocks B, int64_t* steps, int64_t* skipped, i
 
 }  // namespace
 
+namespace {
+// Sharded step: the per-block non-finite flags of this rank's gradient shard [begin, end), as
+// doubles in the loss-partials tail (summed over ranks by the partials all-reduce).
+__global__ void adam_check_range_kernel(const float* __restrict__ grad, Blocks B, int64_t begin, int64_t end,
+                                        double* flags_out) {
+  for (int64_t e = begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < end; e += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(grad[e])) {
+      const int b = find_block(B, e);
+      if (b >= 0) flags_out[b] = 1.0;
+    }
+}
+__global__ void adam_flags_from_kernel(const double* ext, int32_t* flags, int n) {
+  if (threadIdx.x < n) flags[threadIdx.x] = ext[threadIdx.x] != 0.0 ? 1 : 0;
+}
+}  // namespace
+
 void adam_flat(cudaStream_t st, float* param, const float* grad, float* m, float* v, const AdamBlock* blocks,
                int nblocks, int64_t* steps, int64_t* skipped, const float* corr1, const float* corr2,
-               int32_t table_len, int32_t* flags, const double* overflow, int64_t* overflow_steps) {
+               int32_t table_len, int32_t* flags, const double* overflow, int64_t* overflow_steps, int64_t begin,
+               int64_t end, const double* ext_flags) {
   Blocks B;
   B.n = nblocks;
   int64_t total = 0;
@@ -189,11 +206,35 @@ void adam_flat(cudaStream_t st, float* param, const float* grad, float* m, float
     B.b[i] = blocks[i];
     total = std::max(total, blocks[i].offset + blocks[i].count);
   }
-  adam_check_kernel<<<148 * 4, 256, 0, st>>>(grad, B, total, flags);
+  if (end < 0) end = total;
+  // clip every block to [begin, end): counts may become 0, the block index (and with it the
+  // step counter and skip flag of the reference's AdamState) is kept
+  for (int i = 0; i < nblocks; ++i) {
+    const int64_t b0 = std::max(B.b[i].offset, begin), b1 = std::min(B.b[i].offset + B.b[i].count, end);
+    B.b[i].offset = b0;
+    B.b[i].count = std::max<int64_t>(0, b1 - b0);
+  }
+  if (ext_flags) {
+    adam_flags_from_kernel<<<1, 32, 0, st>>>(ext_flags, flags, nblocks);
+  } else {
+    adam_check_kernel<<<148 * 4, 256, 0, st>>>(grad, B, total, flags);
+  }
   adam_update_kernel<<<148 * 5, 256, 0, st>>>(param, grad, m, v, B, steps, corr1, corr2, table_len, flags,
                                                overflow);
   adam_finish_kernel<<<1, 32, 0, st>>>(B, steps, skipped, flags, overflow, overflow_steps);
   count_launch(3);
+}
+
+void adam_check_range(cudaStream_t st, const float* grad, const AdamBlock* blocks, int nblocks, int64_t begin,
+                      int64_t end, double* flags_out) {
+  Blocks B;
+  B.n = nblocks;
+  for (int i = 0; i < nblocks; ++i) B.b[i] = blocks[i];
+  if (end > begin) {
+    adam_check_range_kernel<<<(unsigned)std::min<int64_t>((end - begin + 255) / 256, 148 * 4), 256, 0, st>>>(
+        grad, B, begin, end, flags_out);
+    count_launch();
+  }
 }
 
 }  // namespace lm

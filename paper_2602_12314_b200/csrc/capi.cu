@@ -676,6 +676,13 @@ struct FrameDev {
   float rcw[9], rwc[9];
 };
 constexpr int kPart = 8;  // per-frame loss partial slots (see losses.cu / decoder.cu)
+// partials tail after the frame slots: [0] trust penalty, [1] tile-list overflow flag, [2..9] the
+// 8 Adam blocks' non-finite flags of the sharded step (all summed by the partials all-reduce)
+constexpr int kTail = 16;
+constexpr int kTailOverflow = 1, kTailBlockFlags = 2;
+// slack after the flat parameter / gradient / moment buffers: the sharded step's reduce-scatter
+// and all-gather address nranks equal 4-aligned shards (<= 4 * 64 floats past the last block)
+constexpr int64_t kShardSlack = 256;
 }  // namespace
 
 // session parameter blocks start on 16-byte boundaries (vector loads / cp.async of rows)
@@ -864,7 +871,7 @@ latmap_status session_alloc_frames(latmap_session* s, int nf) {
   const int need_part = std::max(nf, s->global_batch);
   if (need_part > s->part_frames) {
     if (s->partials) cudaFree(s->partials);
-    CTX_CHECK(ctx, cudaMalloc(&s->partials, sizeof(double) * ((size_t)need_part * kPart + 8)));
+    CTX_CHECK(ctx, cudaMalloc(&s->partials, sizeof(double) * ((size_t)need_part * kPart + kTail)));
     s->part_frames = need_part;
   }
   return LATMAP_OK;
@@ -934,7 +941,7 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
   float* atoms = s->params + s->off[7];
   float* g_proj = s->grads + s->off[6];
   float* g_atoms = s->grads + s->off[7];
-  CTX_CHECK(ctx, cudaMemsetAsync(s->partials, 0, sizeof(double) * ((size_t)s->part_frames * kPart + 8), st));
+  CTX_CHECK(ctx, cudaMemsetAsync(s->partials, 0, sizeof(double) * ((size_t)s->part_frames * kPart + kTail), st));
   if (want_grad) CTX_CHECK(ctx, cudaMemsetAsync(s->grads, 0, sizeof(float) * s->total, st));
   // size the tile-pair buffers the first time a frame is seen
   bool sized = false;
@@ -1102,7 +1109,7 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
   }
   // this rank's tile-list overflow flag joins the loss partials, so the sharded step's sum
   // all-reduce tells every rank (and its Adam) that some rank's gradients are incomplete
-  overflow_slot_kernel<<<1, 1, 0, st>>>(s->overflow, s->partials + (size_t)s->part_frames * kPart + 1);
+  overflow_slot_kernel<<<1, 1, 0, st>>>(s->overflow, s->partials + (size_t)s->part_frames * kPart + kTailOverflow);
   count_launch();
   return post_launch(ctx);
 }
@@ -1138,7 +1145,8 @@ latmap_status session_assemble(latmap_session* s, latmap_loss_breakdown* out) {
 }
 
 // MapOptimizer::step_map + step_dict (pipeline.cpp:75-95); dict_only = step_dict alone (Stage II).
-void session_adam(latmap_session* s, bool dict_only = false) {
+void session_adam(latmap_session* s, bool dict_only = false, int64_t begin = 0, int64_t end = -1,
+                  const double* ext_flags = nullptr) {
   const latmap_config& c = s->cfg;
   s->begin(6);
   AdamBlock blocks[8] = {
@@ -1156,7 +1164,8 @@ void session_adam(latmap_session* s, bool dict_only = false) {
   else
     s->renders_valid = false;  // the map moves
   adam_flat(s->ctx->stream, s->params, s->grads, s->m, s->v, blocks, 8, s->steps, s->skipped, s->corr1, s->corr2,
-            kCorrLen, s->flags, s->partials + (size_t)s->part_frames * kPart + 1, s->overflow_steps);
+            kCorrLen, s->flags, s->partials + (size_t)s->part_frames * kPart + kTailOverflow, s->overflow_steps, begin,
+            end, ext_flags);
   s->end();
 }
 
@@ -1199,8 +1208,9 @@ latmap_status latmap_session_create(latmap_ctx* ctx, const latmap_config* cfg, i
   s->total = s->off[8];
   const size_t npx = (size_t)intr->width * intr->height;
   auto ok = [&](cudaError_t e) { return e == cudaSuccess; };
-  bool good = ok(cudaMalloc(&s->params, sizeof(float) * s->total)) && ok(cudaMalloc(&s->grads, sizeof(float) * s->total)) &&
-              ok(cudaMalloc(&s->m, sizeof(float) * s->total)) && ok(cudaMalloc(&s->v, sizeof(float) * s->total)) &&
+  const int64_t flat_cap = s->total + kShardSlack;
+  bool good = ok(cudaMalloc(&s->params, sizeof(float) * flat_cap)) && ok(cudaMalloc(&s->grads, sizeof(float) * flat_cap)) &&
+              ok(cudaMalloc(&s->m, sizeof(float) * flat_cap)) && ok(cudaMalloc(&s->v, sizeof(float) * flat_cap)) &&
               ok(cudaMalloc(&s->anchor, sizeof(float) * k * df)) && ok(cudaMalloc(&s->steps, sizeof(int64_t) * 8)) &&
               ok(cudaMalloc(&s->skipped, sizeof(int64_t) * 8)) && ok(cudaMalloc(&s->overflow, sizeof(int64_t))) && ok(cudaMalloc(&s->overflow_steps, sizeof(int64_t))) &&
               ok(cudaMalloc(&s->flags, sizeof(int32_t) * 8)) && ok(cudaMalloc(&s->corr1, sizeof(float) * kCorrLen)) &&
@@ -1242,10 +1252,10 @@ latmap_status latmap_session_create(latmap_ctx* ctx, const latmap_config* cfg, i
     return LATMAP_ERR_OUT_OF_MEMORY;
   }
   s->dict_w.assign((size_t)k, 0.f);
-  s->cur_cap = std::max<int64_t>(s->total, 1);
-  cudaMemset(s->m, 0, sizeof(float) * s->total);
-  cudaMemset(s->v, 0, sizeof(float) * s->total);
-  cudaMemset(s->grads, 0, sizeof(float) * s->total);
+  s->cur_cap = flat_cap;
+  cudaMemset(s->m, 0, sizeof(float) * flat_cap);
+  cudaMemset(s->v, 0, sizeof(float) * flat_cap);
+  cudaMemset(s->grads, 0, sizeof(float) * flat_cap);
   cudaMemset(s->overflow_steps, 0, sizeof(int64_t));
   cudaMemset(s->steps, 0, sizeof(int64_t) * 8);
   cudaMemset(s->skipped, 0, sizeof(int64_t) * 8);
@@ -1734,12 +1744,12 @@ latmap_status latmap_session_import_rows(latmap_session* s, const float* d_rows,
   off[0] = 0;
   for (int i = 0; i < 8; ++i) off[i + 1] = pad4(off[i] + sizes[i]);
   const int64_t total = off[8];
-  if (s->sp_cap < total) {  // grow the spare set with headroom (the active set drifts frame to frame)
+  if (s->sp_cap < total + kShardSlack) {  // grow the spare set with headroom (the active set drifts frame to frame)
     for (float* p : {s->sp_params, s->sp_grads, s->sp_m, s->sp_v})
       if (p) cudaFree(p);
     s->sp_params = s->sp_grads = s->sp_m = s->sp_v = nullptr;
     s->sp_cap = 0;
-    const int64_t cap = std::max<int64_t>(total + total / 4, 1);
+    const int64_t cap = total + std::max<int64_t>(total / 4, kShardSlack);
     CTX_CHECK(ctx, cudaMalloc(&s->sp_params, sizeof(float) * cap));
     CTX_CHECK(ctx, cudaMalloc(&s->sp_grads, sizeof(float) * cap));
     CTX_CHECK(ctx, cudaMalloc(&s->sp_m, sizeof(float) * cap));
@@ -1925,7 +1935,7 @@ latmap_status latmap_session_grad_buffer(latmap_session* s, float** grads, int64
 latmap_status latmap_session_loss_buffer(latmap_session* s, double** partials, int64_t* count) {
   if (!s || !partials || !count) return LATMAP_ERR_INVALID_ARGUMENT;
   *partials = s->partials;
-  *count = (int64_t)s->part_frames * kPart + 8;
+  *count = (int64_t)s->part_frames * kPart + kTail;
   return LATMAP_OK;
 }
 
@@ -1943,6 +1953,48 @@ latmap_status latmap_session_frame_images(latmap_session* s, int32_t b, float** 
   if (alpha) *alpha = s->alpha[b];
   return LATMAP_OK;
 }
+
+// ------------------------------------------------------------------ sharded step (ZeRO-1)
+// The keyframe-sharded iteration with the optimiser state split across ranks: reduce-scatter of
+// the gradients (each rank owns one 4-aligned shard of the flat buffer), the shard's per-block
+// non-finite flags joined to the loss partials (their all-reduce ORs them, so every rank skips the
+// same blocks, adam.hpp:65-68), Adam on the shard only, all-gather of the parameters. The step
+// counters stay replicated (every rank applies the same skip decisions).
+latmap_status latmap_session_shard_range(const latmap_session* s, int32_t nranks, int32_t rank, int64_t* begin,
+                                         int64_t* end) {
+  if (!s || nranks < 1 || rank < 0 || rank >= nranks || !begin || !end || nranks * 4 > kShardSlack)
+    return LATMAP_ERR_INVALID_ARGUMENT;
+  const int64_t shard = (s->total + 4 * nranks - 1) / (4 * nranks) * 4;
+  *begin = std::min<int64_t>(s->total, (int64_t)rank * shard);
+  *end = std::min<int64_t>(s->total, *begin + shard);
+  return LATMAP_OK;
+}
+
+latmap_status latmap_session_shard_check(latmap_session* s, int64_t begin, int64_t end) {
+  if (!s || begin < 0 || end < begin || end > s->total) return LATMAP_ERR_INVALID_ARGUMENT;
+  const latmap_config& c = s->cfg;
+  const AdamBlock blocks[8] = {{s->off[0], s->len[0], 0.f, 0}, {s->off[1], s->len[1], 0.f, 1},
+                               {s->off[2], s->len[2], 0.f, 0}, {s->off[3], s->len[3], 0.f, 0},
+                               {s->off[4], s->len[4], 0.f, 0}, {s->off[5], s->len[5], 0.f, 0},
+                               {s->off[6], s->len[6], 0.f, 0}, {s->off[7], s->len[7], 0.f, c.dict_learn ? 0 : -1}};
+  adam_check_range(s->ctx->stream, s->grads, blocks, 8, begin, end,
+                   s->partials + (size_t)s->part_frames * kPart + kTailBlockFlags);
+  return post_launch(s->ctx);
+}
+
+latmap_status latmap_session_apply_range(latmap_session* s, int64_t begin, int64_t end) {
+  if (!s || begin < 0 || end < begin || end > s->total) return LATMAP_ERR_INVALID_ARGUMENT;
+  session_adam(s, false, begin, end, s->partials + (size_t)s->part_frames * kPart + kTailBlockFlags);
+  return post_launch(s->ctx);
+}
+
+latmap_status latmap_session_params_buffer(latmap_session* s, float** params, int64_t* count) {
+  if (!s || !params || !count) return LATMAP_ERR_INVALID_ARGUMENT;
+  *params = s->params;
+  *count = s->total;
+  return LATMAP_OK;
+}
+
 
 latmap_status latmap_loss_assemble(const double* partials, int32_t nframes, int32_t width, int32_t height,
                                    const latmap_config* cfg, latmap_loss_breakdown* out) {
@@ -1964,7 +2016,7 @@ latmap_status latmap_session_check_overflow(latmap_session* s, int32_t* any) {
   if (!s || !any) return LATMAP_ERR_INVALID_ARGUMENT;
   latmap_ctx* ctx = s->ctx;
   double v = 0.0;
-  CTX_CHECK(ctx, cudaMemcpyAsync(&v, s->partials + (size_t)s->part_frames * kPart + 1, sizeof(double),
+  CTX_CHECK(ctx, cudaMemcpyAsync(&v, s->partials + (size_t)s->part_frames * kPart + kTailOverflow, sizeof(double),
                                  cudaMemcpyDeviceToHost, ctx->stream));
   CTX_CHECK(ctx, cudaStreamSynchronize(ctx->stream));
   *any = v != 0.0;

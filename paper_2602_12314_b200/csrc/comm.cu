@@ -28,6 +28,8 @@ struct NcclApi {
   decltype(&ncclCommInitRank) comm_init_rank = nullptr;
   decltype(&ncclCommDestroy) comm_destroy = nullptr;
   decltype(&ncclAllReduce) all_reduce = nullptr;
+  decltype(&ncclReduceScatter) reduce_scatter = nullptr;
+  decltype(&ncclAllGather) all_gather = nullptr;
   decltype(&ncclGroupStart) group_start = nullptr;
   decltype(&ncclGroupEnd) group_end = nullptr;
   decltype(&ncclGetErrorString) error_string = nullptr;
@@ -52,6 +54,8 @@ const NcclApi& nccl() {
     LM_SYM(comm_init_rank, "ncclCommInitRank");
     LM_SYM(comm_destroy, "ncclCommDestroy");
     LM_SYM(all_reduce, "ncclAllReduce");
+    LM_SYM(reduce_scatter, "ncclReduceScatter");
+    LM_SYM(all_gather, "ncclAllGather");
     LM_SYM(group_start, "ncclGroupStart");
     LM_SYM(group_end, "ncclGroupEnd");
     LM_SYM(error_string, "ncclGetErrorString");
@@ -135,6 +139,42 @@ latmap_status latmap_session_allreduce(latmap_session* s, latmap_comm* c) {
   const ncclResult_t r2 = n.group_end();
   if (r != ncclSuccess || r2 != ncclSuccess)
     return lm_ctx_fail(c->ctx, LATMAP_ERR_CUDA, n.error_string(r != ncclSuccess ? r : r2));
+  return LATMAP_OK;
+}
+
+
+// The sharded (ZeRO-1) exchange + optimiser step: after latmap_session_objective on every rank,
+//   reduce-scatter(gradients) -> this rank's shard summed over ranks (in place)
+//   shard check -> per-block non-finite flags into the partials tail
+//   all-reduce(loss partials)  -> LossBreakdown terms, overflow flag and block flags for every rank
+//   Adam on the shard (latmap_session_apply_range)
+//   all-gather(parameters)     -> every rank holds the full updated map and dictionary.
+// The same bytes cross NVLink as one all-reduce, while Adam touches 1/nranks of the state.
+latmap_status latmap_session_exchange_sharded(latmap_session* s, latmap_comm* c) {
+  if (!s || !c) return LATMAP_ERR_INVALID_ARGUMENT;
+  int64_t b = 0, e = 0;
+  latmap_status st = latmap_session_shard_range(s, c->nranks, c->rank, &b, &e);
+  if (st != LATMAP_OK) return lm_ctx_fail(c->ctx, st, "exchange_sharded: too many ranks for the shard slack");
+  float *g = nullptr, *prm = nullptr;
+  double* part = nullptr;
+  int64_t ng = 0, np = 0, nprm = 0;
+  st = latmap_session_grad_buffer(s, &g, &ng);
+  if (st == LATMAP_OK) st = latmap_session_loss_buffer(s, &part, &np);
+  if (st == LATMAP_OK) st = latmap_session_params_buffer(s, &prm, &nprm);
+  if (st != LATMAP_OK) return st;
+  const int64_t shard = (ng + 4 * c->nranks - 1) / (4 * c->nranks) * 4;
+  const NcclApi& n = nccl();
+  cudaStream_t stream = static_cast<cudaStream_t>(latmap_ctx_stream(c->ctx));
+  ncclResult_t r = n.reduce_scatter(g, g + (size_t)c->rank * shard, (size_t)shard, ncclFloat32, ncclSum, c->comm, stream);
+  if (r != ncclSuccess) return lm_ctx_fail(c->ctx, LATMAP_ERR_CUDA, n.error_string(r));
+  st = latmap_session_shard_check(s, b, e);
+  if (st != LATMAP_OK) return st;
+  r = n.all_reduce(part, part, (size_t)np, ncclFloat64, ncclSum, c->comm, stream);
+  if (r != ncclSuccess) return lm_ctx_fail(c->ctx, LATMAP_ERR_CUDA, n.error_string(r));
+  st = latmap_session_apply_range(s, b, e);
+  if (st != LATMAP_OK) return st;
+  r = n.all_gather(prm + (size_t)c->rank * shard, prm, (size_t)shard, ncclFloat32, c->comm, stream);
+  if (r != ncclSuccess) return lm_ctx_fail(c->ctx, LATMAP_ERR_CUDA, n.error_string(r));
   return LATMAP_OK;
 }
 

@@ -175,7 +175,11 @@ struct AdamBlock {
 };
 void adam_flat(cudaStream_t st, float* param, const float* grad, float* m, float* v, const AdamBlock* blocks,
                int nblocks, int64_t* steps, int64_t* skipped, const float* corr1, const float* corr2,
-               int32_t table_len, int32_t* flags, const double* overflow, int64_t* overflow_steps);
+               int32_t table_len, int32_t* flags, const double* overflow, int64_t* overflow_steps,
+               int64_t begin = 0, int64_t end = -1, const double* ext_flags = nullptr);
+// Sharded step: per-block non-finite flags of grad[begin, end) into flags_out[block] (doubles, 1 = bad).
+void adam_check_range(cudaStream_t st, const float* grad, const AdamBlock* blocks, int nblocks, int64_t begin,
+                      int64_t end, double* flags_out);
 
 // Streaming k-means (kmeans.cu): device points / centres / atoms, host weights.
 cudaError_t kmeans_weighted(cudaStream_t st, const float* P, const float* W, int64_t n, int dim, int64_t k,

@@ -106,3 +106,64 @@ def test_sharded_step_applies_identical_adam(ctx):
     assert torch.equal(a, b)  # identical Adam input -> identical parameters on every rank
     rel = float(torch.linalg.norm(a - ref_params) / torch.linalg.norm(ref_params))
     assert rel < 1e-5, rel
+
+
+@pytest.mark.parametrize("inject_nan", [False, True])
+def test_zero1_sharded_adam_equals_replicated(ctx, inject_nan):
+    """The ZeRO-1 step (latmap_session_exchange_sharded's pieces, NCCL replaced by device adds and
+    copies on one GPU): reduce-scatter -> shard check -> partials all-reduce (block skip flags
+    OR-ed) -> Adam on each rank's shard -> all-gather. Bit-identical to every rank applying the
+    replicated Adam to the same summed gradients, including a whole-block skip for a non-finite
+    gradient found in only one rank's shard (adam.hpp:65-68)."""
+    w = synthetic.make_workload(2, gpu_render(ctx), scale=0.25)
+    nf = len(w.frames)
+    ranks = []
+    for r in range(2):
+        plan = rank_plan(nf, 2, r)
+        s, _ = session(ctx, w, [w.frames[i] for i in plan["frames"]], 1)
+        s.set_batch(plan["global_batch"], add_trust=plan["add_trust"], slot_offset=plan["slot_offset"])
+        ranks.append(s)
+    rep, _ = session(ctx, w, [w.frames[i] for i in rank_plan(nf, 2, 0)["frames"]], 1)
+    rep.set_batch(nf, add_trust=True, slot_offset=0)
+    for s in ranks + [rep]:
+        s.objective(want_grad=True, read=False)
+    g = ranks[0].grad_buffer() + ranks[1].grad_buffer()
+    p = ranks[0].loss_buffer() + ranks[1].loss_buffer()
+    total = g.numel()
+    (b0, e0), (b1, e1) = ranks[0].shard_range(2, 0), ranks[1].shard_range(2, 1)
+    assert b0 == 0 and e0 == b1 and e1 == total and b1 % 4 == 0
+    bad_block = None
+    if inject_nan:  # a non-finite gradient in rank 1's shard only
+        bad_block = next(nm for nm, (o, n) in ranks[1].grad_blocks().items() if o <= b1 + 1 < o + n)
+        g[b1 + 1] = float("nan")
+    init = ranks[0].params_buffer().clone()
+    # replicated: every rank applies Adam to the all-reduced gradients
+    rep.grad_buffer().copy_(g)
+    rep.loss_buffer().copy_(p)
+    rep.apply()
+    # sharded: reduce-scatter (each rank keeps the summed gradients of its shard) ...
+    tail = p.numel() - 16
+    for s in ranks:
+        s.grad_buffer().copy_(g)
+        s.loss_buffer().copy_(p)
+    ranks[0].shard_check(b0, e0)
+    ranks[1].shard_check(b1, e1)
+    # ... partials all-reduce: the per-block skip flags of the two shards OR-ed ...
+    flags = ranks[0].loss_buffer()[tail + 2:tail + 10] + ranks[1].loss_buffer()[tail + 2:tail + 10]
+    assert bool(flags.any().item()) == inject_nan
+    for s in ranks:
+        s.loss_buffer()[tail + 2:tail + 10] = flags
+    # ... Adam on each shard, then all-gather of the parameters
+    ranks[0].apply_range(b0, e0)
+    ranks[1].apply_range(b1, e1)
+    p0, p1 = ranks[0].params_buffer(), ranks[1].params_buffer()
+    p0[b1:e1] = p1[b1:e1]
+    p1[b0:e0] = p0[b0:e0]
+    torch.cuda.synchronize()
+    ref = rep.params_buffer()
+    assert torch.equal(p0, ref) and torch.equal(p1, ref)
+    if inject_nan:  # that whole block was skipped on both ranks (also the part in rank 0's shard)
+        o, n = ranks[0].grad_blocks()[bad_block]
+        assert torch.equal(p0[o:o + n], init[o:o + n]) and o < b1, bad_block
+    else:
+        assert not torch.equal(p0, init)

@@ -127,7 +127,7 @@ def _assembly_worker(rank, world, port, out):
     intr, m, d, frames = _problem()
     plan = rank_plan(len(frames), world, rank)
     cfg = oracle.Config()
-    part = np.zeros(len(frames) * KPART + 8, np.float64)
+    part = np.zeros(len(frames) * KPART + 16, np.float64)
     for i, gi in enumerate(plan["frames"]):
         slot = plan["slot_offset"] + i
         part[slot * KPART:(slot + 1) * KPART], trust = _frame_partials(m, d, frames[gi], intr, cfg)
