@@ -305,6 +305,11 @@ latmap_status latmap_loss_assemble(const double* partials, int32_t nframes, int3
 latmap_status latmap_session_check_overflow(latmap_session* s, int32_t* any);
 /* Sticky count of Adam steps skipped because a tile list overflowed (since session creation). */
 latmap_status latmap_session_overflow_steps(latmap_session* s, int64_t* count);
+/* process_keyframe's transaction (pipeline.cpp:155-190, 294-306): save the device state (map rows,
+ * dictionary incl. anchor and weights, Adam moments and counters) and restore it after a failure.
+ * One saved state per session; restore re-homes the flat buffers when the row count changed. */
+latmap_status latmap_session_save_state(latmap_session* s);
+latmap_status latmap_session_restore_state(latmap_session* s);
 /* Sharded optimiser step (ZeRO-1 over the keyframe-sharded objective). The flat buffers split into
  * nranks 4-aligned shards; rank r owns [*begin, *end). */
 latmap_status latmap_session_shard_range(const latmap_session* s, int32_t nranks, int32_t rank, int64_t* begin,
@@ -505,6 +510,9 @@ latmap_status latmap_pipeline_state(const latmap_pipeline* p, int64_t out[6]);
 /* ActiveSet::origin / dirty (host arrays of latmap_session_size entries). */
 latmap_status latmap_pipeline_active_set(const latmap_pipeline* p, int64_t* origin, uint8_t* dirty);
 const char* latmap_pipeline_last_error(const latmap_pipeline* p);
+/* Test hook: make the next process_keyframe fail (LATMAP_ERR_CUDA, "injected fault") at stage
+ * 1 after seeding, 2 after Stage I/II, 3 after the sync (0 = off); the keyframe is rolled back. */
+latmap_status latmap_pipeline_inject_fault(latmap_pipeline* p, int32_t stage);
 
 /* ---------------------------------------------------------------- self-test */
 /* One-tile tcgen05 GEMM, C[128 x n] = A[128 x k] * B[n x k]^T (device fp32 in/out, bf16 staging),

@@ -980,6 +980,11 @@ class Pipeline:
         self._check(lib().latmap_pipeline_process_keyframe(self.h, C.byref(f), fi, C.byref(log)))
         return log.as_dict()
 
+    def inject_fault(self, stage):
+        """Test hook: the next process_keyframe fails at stage 1 (after seeding), 2 (after Stage
+        I/II) or 3 (after the sync) and is rolled back (latmap_pipeline_inject_fault)."""
+        self._check(lib().latmap_pipeline_inject_fault(self.h, int(stage)))
+
     def flush(self):
         """run_pipeline's final flush (pipeline.cpp:318-330); returns the SyncStats."""
         st = np.zeros(5, np.int64)

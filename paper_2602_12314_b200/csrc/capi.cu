@@ -739,6 +739,16 @@ struct latmap_session {
   std::vector<cudaEvent_t> evD, evB;
   float *d_color2 = nullptr, *d_depth2 = nullptr, *d_query2 = nullptr;
   std::vector<float> dict_w;  // DictionaryState::weights (host; k-means maintenance only)
+  // latmap_session_save_state / restore_state: the map, dictionary and MapOptimizer state at the
+  // start of a keyframe (process_keyframe's StateSnapshot, pipeline.cpp:155-190)
+  struct Snapshot {
+    bool valid = false;
+    int64_t n = 0, total = 0, off[9] = {}, len[8] = {};
+    float *params = nullptr, *m = nullptr, *v = nullptr, *anchor = nullptr;
+    int64_t cap = 0;
+    int64_t steps[8] = {}, skipped[8] = {};
+    std::vector<float> dict_w;
+  } snap;
   int64_t graph_launches = 0;
   bool graph_exact = false;
   int32_t graph_dec_path = 0;
@@ -1294,7 +1304,8 @@ latmap_status latmap_session_destroy(latmap_session* s) {
                   (void*)s->dec.a, (void*)s->dec.bm, (void*)s->dec.row_stats, (void*)s->dec.r_part,
                   (void*)s->dec.a_part, (void*)s->dec.bm_part, (void*)s->dec.loss_part,
                   (void*)s->dec.e_tiles, (void*)s->dec.a_acc, (void*)s->dec.r_acc, (void*)s->dec.dl_mt,
-                  (void*)s->dec.dl_nu, (void*)s->dec.dl_part, (void*)s->dec.row_nd})
+                  (void*)s->dec.dl_nu, (void*)s->dec.dl_part, (void*)s->dec.row_nd, (void*)s->snap.params,
+                  (void*)s->snap.m, (void*)s->snap.v, (void*)s->snap.anchor})
     if (p) cudaFree(p);
   for (auto& r : s->rw) r.release();
   for (auto* p : s->color) cudaFree(p);
@@ -1995,6 +2006,79 @@ latmap_status latmap_session_params_buffer(latmap_session* s, float** params, in
   return LATMAP_OK;
 }
 
+
+// ------------------------------------------------------------------ keyframe transactions
+// process_keyframe's snapshot / restore (pipeline.cpp:155-190, 294-306) for the device state:
+// map rows, dictionary (proj, atoms, anchor, weights) and the Adam moments and counters.
+latmap_status latmap_session_save_state(latmap_session* s) {
+  if (!s) return LATMAP_ERR_INVALID_ARGUMENT;
+  latmap_ctx* ctx = s->ctx;
+  cudaStream_t st = ctx->stream;
+  auto& sn = s->snap;
+  if (sn.cap < s->total) {
+    for (float** p : {&sn.params, &sn.m, &sn.v})
+      if (*p) cudaFree(*p), *p = nullptr;
+    sn.cap = 0;
+    const int64_t cap = s->total + s->total / 4 + 1024;
+    CTX_CHECK(ctx, cudaMalloc(&sn.params, sizeof(float) * cap));
+    CTX_CHECK(ctx, cudaMalloc(&sn.m, sizeof(float) * cap));
+    CTX_CHECK(ctx, cudaMalloc(&sn.v, sizeof(float) * cap));
+    sn.cap = cap;
+  }
+  if (!sn.anchor) CTX_CHECK(ctx, cudaMalloc(&sn.anchor, sizeof(float) * s->k * s->df));
+  CTX_CHECK(ctx, cudaMemcpyAsync(sn.params, s->params, sizeof(float) * s->total, cudaMemcpyDeviceToDevice, st));
+  CTX_CHECK(ctx, cudaMemcpyAsync(sn.m, s->m, sizeof(float) * s->total, cudaMemcpyDeviceToDevice, st));
+  CTX_CHECK(ctx, cudaMemcpyAsync(sn.v, s->v, sizeof(float) * s->total, cudaMemcpyDeviceToDevice, st));
+  CTX_CHECK(ctx, cudaMemcpyAsync(sn.anchor, s->anchor, sizeof(float) * s->k * s->df, cudaMemcpyDeviceToDevice, st));
+  CTX_CHECK(ctx, cudaMemcpyAsync(sn.steps, s->steps, sizeof(sn.steps), cudaMemcpyDeviceToHost, st));
+  CTX_CHECK(ctx, cudaMemcpyAsync(sn.skipped, s->skipped, sizeof(sn.skipped), cudaMemcpyDeviceToHost, st));
+  CTX_CHECK(ctx, cudaStreamSynchronize(st));
+  sn.n = s->n, sn.total = s->total;
+  std::copy(s->off, s->off + 9, sn.off);
+  std::copy(s->len, s->len + 8, sn.len);
+  sn.dict_w = s->dict_w;
+  sn.valid = true;
+  return LATMAP_OK;
+}
+
+latmap_status latmap_session_restore_state(latmap_session* s) {
+  if (!s || !s->snap.valid) return s ? fail(s->ctx, LATMAP_ERR_INVALID_ARGUMENT, "restore_state: no saved state")
+                                     : LATMAP_ERR_INVALID_ARGUMENT;
+  latmap_ctx* ctx = s->ctx;
+  cudaStream_t st = ctx->stream;
+  auto& sn = s->snap;
+  CTX_CHECK(ctx, cudaStreamSynchronize(st));
+  if (s->cur_cap < sn.total + kShardSlack) {  // the row set grew and shrank since: re-home the flat buffers
+    for (float** p : {&s->params, &s->grads, &s->m, &s->v}) {
+      if (*p) CTX_CHECK(ctx, cudaFree(*p));
+      *p = nullptr;
+    }
+    const int64_t cap = sn.total + kShardSlack;
+    CTX_CHECK(ctx, cudaMalloc(&s->params, sizeof(float) * cap));
+    CTX_CHECK(ctx, cudaMalloc(&s->grads, sizeof(float) * cap));
+    CTX_CHECK(ctx, cudaMalloc(&s->m, sizeof(float) * cap));
+    CTX_CHECK(ctx, cudaMalloc(&s->v, sizeof(float) * cap));
+    s->cur_cap = cap;
+  }
+  CTX_CHECK(ctx, cudaMemcpyAsync(s->params, sn.params, sizeof(float) * sn.total, cudaMemcpyDeviceToDevice, st));
+  CTX_CHECK(ctx, cudaMemcpyAsync(s->m, sn.m, sizeof(float) * sn.total, cudaMemcpyDeviceToDevice, st));
+  CTX_CHECK(ctx, cudaMemcpyAsync(s->v, sn.v, sizeof(float) * sn.total, cudaMemcpyDeviceToDevice, st));
+  CTX_CHECK(ctx, cudaMemsetAsync(s->grads, 0, sizeof(float) * (sn.total + kShardSlack), st));
+  CTX_CHECK(ctx, cudaMemcpyAsync(s->anchor, sn.anchor, sizeof(float) * s->k * s->df, cudaMemcpyDeviceToDevice, st));
+  CTX_CHECK(ctx, cudaMemcpyAsync(s->steps, sn.steps, sizeof(sn.steps), cudaMemcpyHostToDevice, st));
+  CTX_CHECK(ctx, cudaMemcpyAsync(s->skipped, sn.skipped, sizeof(sn.skipped), cudaMemcpyHostToDevice, st));
+  CTX_CHECK(ctx, cudaMemsetAsync(s->flags, 0, sizeof(int32_t) * 8, st));
+  s->n = sn.n, s->total = sn.total;
+  std::copy(sn.off, sn.off + 9, s->off);
+  std::copy(sn.len, sn.len + 8, s->len);
+  s->dict_w = sn.dict_w;
+  for (auto& r : s->rw)
+    if (r.w.pair_cap > 1) CTX_CHECK(ctx, r.ensure(s->n, s->intr.width, s->intr.height, r.w.pair_cap));
+  s->renders_valid = false;
+  s->drop_graph();
+  CTX_CHECK(ctx, cudaStreamSynchronize(st));
+  return LATMAP_OK;
+}
 
 latmap_status latmap_loss_assemble(const double* partials, int32_t nframes, int32_t width, int32_t height,
                                    const latmap_config* cfg, latmap_loss_breakdown* out) {

@@ -68,6 +68,7 @@ struct latmap_pipeline {
   std::vector<uint8_t> kept;
   bool failed = false;
   std::string err;
+  int32_t fault_stage = 0;  // test hook (latmap_pipeline_inject_fault): fail the next keyframe at this point
 };
 
 namespace {
@@ -77,9 +78,8 @@ latmap_status pfail(latmap_pipeline* p, latmap_status st, const std::string& msg
   return st;
 }
 
-// A device-side failure after the keyframe began mutating the session: the reference restores
-// its snapshot (pipeline.cpp:302-312); the device state here cannot be rolled back, so the
-// pipeline refuses further work instead of continuing from a half-applied keyframe.
+// A device-side failure: inside process_keyframe the caller restores the keyframe's snapshot
+// (and clears the flag); elsewhere (flush) the pipeline refuses further work.
 latmap_status poison(latmap_pipeline* p, latmap_status st, const char* where, bool store_err = false) {
   p->failed = true;
   const char* m = store_err ? latmap_store_last_error(p->store) : latmap_ctx_last_error(p->ctx);
@@ -284,11 +284,18 @@ latmap_status latmap_pipeline_active_set(const latmap_pipeline* p, int64_t* orig
   return LATMAP_OK;
 }
 
-// process_keyframe / process_keyframe_inner (pipeline.cpp:192-312)
-latmap_status latmap_pipeline_process_keyframe(latmap_pipeline* p, const latmap_frame* kf, int32_t frame_index,
-                                               latmap_keyframe_log* out) {
-  if (!p || !kf) return LATMAP_ERR_INVALID_ARGUMENT;
-  if (p->failed) return pfail(p, LATMAP_ERR_INVALID_ARGUMENT, "pipeline: state lost after a failed keyframe (" + p->err + ")");
+}  // extern "C"
+
+namespace {
+latmap_status injected(latmap_pipeline* p, int32_t stage) {
+  if (p->fault_stage != stage) return LATMAP_OK;
+  p->fault_stage = 0;
+  return pfail(p, LATMAP_ERR_CUDA, "injected fault (latmap_pipeline_inject_fault stage " + std::to_string(stage) + ")");
+}
+
+// process_keyframe_inner (pipeline.cpp:192-290)
+latmap_status process_keyframe_inner(latmap_pipeline* p, const latmap_frame* kf, int32_t frame_index,
+                                     latmap_keyframe_log* out) {
   const auto t0 = std::chrono::steady_clock::now();
   const int64_t npx = (int64_t)p->intr.width * p->intr.height;
   const int32_t ed = p->pc.embed_dim, qd = p->pc.query_dim;
@@ -378,6 +385,7 @@ latmap_status latmap_pipeline_process_keyframe(latmap_pipeline* p, const latmap_
     p->origin.resize(p->origin.size() + (size_t)n, -1);
     p->dirty.resize(p->dirty.size() + (size_t)n, 1);
   }
+  if (latmap_status fst = injected(p, 1)) return fst;
 
   // 4. Stage I, 5. Stage II (pipeline.cpp:232-266)
   bool have_loss = false;
@@ -391,6 +399,7 @@ latmap_status latmap_pipeline_process_keyframe(latmap_pipeline* p, const latmap_
     have_loss = true;
   }
   if (!have_loss) PL_TRY(latmap_session_objective_ex(p->s, 0, 0, 0, &row.loss), "objective");
+  if (latmap_status fst = injected(p, 2)) return fst;
 
   // 6. history push (HistoryBuffer::push)
   if ((int)p->hist.size() < p->pc.history_capacity) {
@@ -414,6 +423,7 @@ latmap_status latmap_pipeline_process_keyframe(latmap_pipeline* p, const latmap_
     p->traveled = 0.f;
     row.synced = 1;
   }
+  if (latmap_status fst = injected(p, 3)) return fst;
 
   ++p->keyframes_processed;
   const int64_t na = latmap_session_size(p->s);
@@ -427,6 +437,54 @@ latmap_status latmap_pipeline_process_keyframe(latmap_pipeline* p, const latmap_
   row.dict_weight_mass = double(mass);
   row.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   if (out) *out = row;
+  return LATMAP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+// process_keyframe (pipeline.cpp:292-312): the keyframe runs as a transaction. The state the
+// reference snapshots (ActiveSet rows / origin / dirty, DictionaryState, MapOptimizer, travel,
+// counters, persistent anchor, rng; pipeline.cpp:155-190) is saved first and restored when the
+// keyframe fails, so the pipeline continues from the state before it. As in the reference the
+// history buffer and the store are not part of the snapshot.
+latmap_status latmap_pipeline_process_keyframe(latmap_pipeline* p, const latmap_frame* kf, int32_t frame_index,
+                                               latmap_keyframe_log* out) {
+  if (!p || !kf) return LATMAP_ERR_INVALID_ARGUMENT;
+  if (p->failed) return pfail(p, LATMAP_ERR_INVALID_ARGUMENT, "pipeline: state lost after a failed keyframe (" + p->err + ")");
+  struct Host {
+    std::mt19937_64 rng;
+    float traveled;
+    bool have_last;
+    float last[3];
+    int32_t keyframes_processed;
+    int64_t peak_active, reservoir_seen;
+    bool anchor_init;
+    std::vector<float> persistent_anchor;
+    std::vector<int64_t> origin;
+    std::vector<uint8_t> dirty;
+  } snap{p->rng, p->traveled, p->have_last, {p->last[0], p->last[1], p->last[2]}, p->keyframes_processed,
+         p->peak_active, p->reservoir_seen, p->anchor_init, p->persistent_anchor, p->origin, p->dirty};
+  if (latmap_session_save_state(p->s) != LATMAP_OK) return poison(p, LATMAP_ERR_CUDA, "process_keyframe snapshot");
+  const latmap_status st = process_keyframe_inner(p, kf, frame_index, out);
+  if (st == LATMAP_OK) return LATMAP_OK;
+  const std::string why = p->err;
+  if (latmap_session_restore_state(p->s) != LATMAP_OK) return poison(p, st, "process_keyframe restore");
+  p->rng = snap.rng, p->traveled = snap.traveled, p->have_last = snap.have_last;
+  std::copy(snap.last, snap.last + 3, p->last);
+  p->keyframes_processed = snap.keyframes_processed, p->peak_active = snap.peak_active;
+  p->reservoir_seen = snap.reservoir_seen, p->anchor_init = snap.anchor_init;
+  p->persistent_anchor = std::move(snap.persistent_anchor);
+  p->origin = std::move(snap.origin), p->dirty = std::move(snap.dirty);
+  p->failed = false;  // the inner failure poisoned the pipeline; the restore un-poisons it
+  p->err = why;
+  return st;
+}
+
+latmap_status latmap_pipeline_inject_fault(latmap_pipeline* p, int32_t stage) {
+  if (!p || stage < 0 || stage > 3) return LATMAP_ERR_INVALID_ARGUMENT;
+  p->fault_stage = stage;
   return LATMAP_OK;
 }
 

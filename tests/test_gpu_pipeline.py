@@ -260,3 +260,52 @@ def test_run_pipeline_over_lamt_dataset(ctx, tmp_path):
     assert (p.active_set()[0] >= 0).all()  # every kept row now has a store record
     line = pl.log_csv_row(res["log"][0])
     assert len(line.split(",")) == len(pl.log_csv_header().split(","))
+
+
+@pytest.mark.parametrize("stage", [1, 2, 3])
+def test_process_keyframe_rolls_back_a_failed_keyframe(ctx, stage):
+    """process_keyframe is a transaction (pipeline.cpp:292-306): a keyframe that fails after it
+    started mutating the state (seeding appended rows, Stage I/II stepped the map, dictionary and
+    moments, the sync re-homed the active set) leaves the ActiveSet rows / origin / dirty, the
+    dictionary, the counters and the travel exactly as before it, and the pipeline continues; the
+    repeated keyframe then matches a run that never failed. As in the reference the history
+    buffer and the store are outside the snapshot (pipeline.cpp:155-169)."""
+    intr, frames = make_scene(ctx, nframes=4)
+    cfg, pc = small_lr_config(), pipeline_config()
+    p = api.Pipeline(ctx, cfg, pc, intr)
+    for kf in frames[:2]:
+        p.process_keyframe(kf)
+
+    def snapshot():
+        s = p.session
+        rows = s.export_rows().cpu().numpy().copy() if s.n else None
+        atoms, proj = s.get_dictionary()
+        st = p.state()
+        st.pop("history")
+        org, dty = p.active_set()
+        return rows, atoms, proj, s.get_anchor(), s.dict_weights(), st, org, dty
+
+    before = snapshot()
+    p.inject_fault(stage)
+    with pytest.raises(api._capi.LatmapError, match="injected fault"):
+        p.process_keyframe(frames[2])
+    after = snapshot()
+    assert not p.state()["failed"]
+    for a, b in zip(before, after):
+        if isinstance(a, dict):
+            assert a == b
+        elif a is None:
+            assert b is None
+        else:
+            assert np.array_equal(np.asarray(a).view(np.uint8), np.asarray(b).view(np.uint8))
+    got = p.process_keyframe(frames[2])
+    # a pipeline that never failed
+    q = api.Pipeline(ctx, cfg, pc, intr)
+    for kf in frames[:2]:
+        q.process_keyframe(kf)
+    ref = q.process_keyframe(frames[2])
+    for k in ("seeded", "active_count", "synced"):
+        assert got[k] == ref[k], k
+    if stage != 3:  # a rolled-back sync already moved records into the store
+        assert got["global_count"] == ref["global_count"]
+    assert got["loss"]["total"] == pytest.approx(ref["loss"]["total"], rel=1e-3)
