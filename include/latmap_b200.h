@@ -115,6 +115,13 @@ latmap_status latmap_ctx_set_exact_blend(latmap_ctx* ctx, int32_t exact);
  * Replaces no reference interface (the reference has one fp32 CPU decoder,
  * proj/src/dictionary.cpp:25-83); results agree within the bf16 tolerances either way. */
 latmap_status latmap_ctx_set_decoder_path(latmap_ctx* ctx, int32_t path);
+/* Deterministic mode: every gradient reduction in a fixed order instead of float atomics, so
+ * gradients are bit-identical run to run (the reference's guarantee, render.cpp:272-273,358,
+ * test_render.cpp:142-151). The render backward writes one partial row per (splat, tile) pair and
+ * sums a splat's rows in the row-major order of its tile rectangle; the decoders' split-K /
+ * per-CTA partial reductions run unsplit; segment pooling sums in raster order. Slower; off by
+ * default. Loss values are sums in double (reported to double rounding). */
+latmap_status latmap_ctx_set_deterministic(latmap_ctx* ctx, int32_t on);
 const char* latmap_ctx_last_error(const latmap_ctx* ctx);
 /* Device memory for callers that hold only this header (the Eigen-typed drop-in layer):
  * alloc / free (free synchronises the context stream) and copies on the context stream,

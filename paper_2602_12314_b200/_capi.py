@@ -203,6 +203,7 @@ def _declare(L):
         "latmap_session_params_buffer": [P, C.POINTER(P), C.POINTER(C.c_int64)],
         "latmap_session_exchange_sharded": [P, P],
         "latmap_session_save_state": [P],
+        "latmap_ctx_set_deterministic": [P, C.c_int32],
         "latmap_session_restore_state": [P],
         "latmap_pipeline_inject_fault": [P, C.c_int32],
         "latmap_session_overflow_steps": [P, C.POINTER(C.c_int64)],
@@ -292,7 +293,7 @@ EXPORTED = ["latmap_ctx_create", "latmap_ctx_destroy", "latmap_ctx_set_stream", 
             "latmap_session_check_overflow", "latmap_session_overflow_steps", "latmap_session_grad_layout",
             "latmap_session_shard_range", "latmap_session_shard_check", "latmap_session_apply_range",
             "latmap_session_params_buffer", "latmap_session_exchange_sharded", "latmap_session_save_state",
-            "latmap_session_restore_state", "latmap_pipeline_inject_fault"]
+            "latmap_session_restore_state", "latmap_pipeline_inject_fault", "latmap_ctx_set_deterministic"]
 
 
 def check(ctx_handle, status):

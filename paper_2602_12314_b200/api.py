@@ -115,6 +115,10 @@ class Context:
     def set_exact_blend(self, exact=True):
         check(self.h, lib().latmap_ctx_set_exact_blend(self.h, int(bool(exact))))
 
+    def set_deterministic(self, on=True):
+        """Fixed-order gradient reductions: bit-identical gradients run to run (slower)."""
+        check(self.h, lib().latmap_ctx_set_deterministic(self.h, int(bool(on))))
+
     def set_decoder_path(self, path):
         """bf16 decoder kernels: 0 auto, 1 fused on-chip (DEC1/DEC2), 2 staged (DL1-DL5)."""
         check(self.h, lib().latmap_ctx_set_decoder_path(self.h, int(path)))

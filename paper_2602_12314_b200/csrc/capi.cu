@@ -159,6 +159,8 @@ struct latmap_ctx {
   std::string err;
   int64_t launches0 = 0;
   bool exact_blend = false;  // parity mode: separately rounded accumulation in the forward blend
+  bool deterministic = false;  // fixed-order gradient reductions (bit-reproducible backward)
+  DetScratch det;              // the deterministic render backward's per-(splat, tile) rows
   int32_t decoder_path = 0;  // bf16 decoder: 0 auto, 1 fused on-chip (DEC1/DEC2), 2 staged (DL1-DL5)
   cudaStream_t copy_stream = nullptr;  // keyframe uploads (overlap the step's render of earlier frames)
 };
@@ -265,6 +267,7 @@ latmap_status latmap_ctx_create(int32_t device, void* stream, latmap_ctx** out) 
 latmap_status latmap_ctx_destroy(latmap_ctx* ctx) {
   if (!ctx) return LATMAP_ERR_INVALID_ARGUMENT;
   cudaStreamSynchronize(ctx->stream);
+  ctx->det.release();
   if (ctx->copy_stream) {
     cudaStreamSynchronize(ctx->copy_stream);
     cudaStreamDestroy(ctx->copy_stream);
@@ -282,6 +285,13 @@ latmap_status latmap_ctx_set_stream(latmap_ctx* ctx, void* stream) {
 latmap_status latmap_ctx_set_exact_blend(latmap_ctx* ctx, int32_t exact) {
   if (!ctx) return LATMAP_ERR_INVALID_ARGUMENT;
   ctx->exact_blend = exact != 0;
+  return LATMAP_OK;
+}
+
+latmap_status latmap_ctx_set_deterministic(latmap_ctx* ctx, int32_t on) {
+  if (!ctx) return LATMAP_ERR_INVALID_ARGUMENT;
+  ctx->deterministic = on != 0;
+  if (!on) ctx->det.release();
   return LATMAP_OK;
 }
 
@@ -403,8 +413,9 @@ latmap_status latmap_render_backward(latmap_ctx* ctx, const latmap_map* map, con
   pose_mats(*pose, rcw, rwc);
   auto& b = const_cast<latmap_render_cache*>(cache)->bufs;
   CTX_CHECK(ctx, cudaMemsetAsync(b.geo_acc, 0, sizeof(float) * 8 * map->n, ctx->stream));
+  set_deterministic(ctx->deterministic);
   render_backward(ctx->stream, map_ptrs(map), rcw, rwc, pose->translation, to_intr(*intr), b.w, d_color, d_depth,
-                  d_query, b.geo_acc, map_ptrs(grads));
+                  d_query, b.geo_acc, map_ptrs(grads), true, ctx->deterministic ? &ctx->det : nullptr);
   return post_launch(ctx);
 }
 
@@ -489,6 +500,7 @@ latmap_status latmap_reconstruct_backward(latmap_ctx* ctx, const float* q, const
                                           float temperature, const float* d_rec, float* d_q, float* d_proj,
                                           float* d_atoms) {
   if (!ctx || !q || !attention || !d_rec || !d_q || !d_proj || !d_atoms) return LATMAP_ERR_INVALID_ARGUMENT;
+  set_deterministic(ctx->deterministic);
   cudaStream_t st = ctx->stream;
   if (n == 0) {
     CTX_CHECK(ctx, cudaMemsetAsync(d_proj, 0, sizeof(float) * ds * df, st));
@@ -751,6 +763,7 @@ struct latmap_session {
   } snap;
   int64_t graph_launches = 0;
   bool graph_exact = false;
+  bool graph_det = false;
   int32_t graph_dec_path = 0;
   bool use_graph = true;
   void drop_graph() {
@@ -897,6 +910,25 @@ __global__ void seg_pool_kernel(const float* __restrict__ query, const int32_t* 
     const int a = assign[p];
     if (a < 0) continue;
     atomicAdd(&qsum[(size_t)seg_of[a] * ds + (e % ds)], query[e]);
+  }
+}
+// deterministic variant: block (row r, channel chunk) sums its segment's pixels in raster order
+// (per-thread strided partials, then a fixed-order combination)
+__global__ void seg_pool_det_kernel(const float* __restrict__ query, const int32_t* __restrict__ assign, int64_t npx,
+                                    int ds, const int32_t* __restrict__ seg_of, float* __restrict__ qsum) {
+  __shared__ float part[256];
+  const int r = blockIdx.x, c = blockIdx.y;
+  float acc = 0.f;
+  for (int64_t p = threadIdx.x; p < npx; p += blockDim.x) {
+    const int a = assign[p];
+    if (a >= 0 && seg_of[a] == r) acc += query[p * ds + c];
+  }
+  part[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (unsigned t = 0; t < blockDim.x; ++t) s += part[t];
+    qsum[(size_t)r * ds + c] = s;
   }
 }
 __global__ void seg_mean_kernel(float* q, const float* __restrict__ inv, int64_t rows, int ds) {
@@ -1059,7 +1091,11 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
       s->begin(3);
       const unsigned gq = (unsigned)std::min<int64_t>((npx * s->ds + 255) / 256, 148 * 16);
       CTX_CHECK(ctx, cudaMemsetAsync(s->seg_q, 0, sizeof(float) * f.n_sup * s->ds, st));
-      seg_pool_kernel<<<gq, 256, 0, st>>>(s->query[b], f.assign, npx, s->ds, f.seg_of, s->seg_q);
+      if (deterministic())
+        seg_pool_det_kernel<<<dim3((unsigned)f.n_sup, (unsigned)s->ds), 256, 0, st>>>(s->query[b], f.assign, npx, s->ds,
+                                                                                   f.seg_of, s->seg_q);
+      else
+        seg_pool_kernel<<<gq, 256, 0, st>>>(s->query[b], f.assign, npx, s->ds, f.seg_of, s->seg_q);
       seg_mean_kernel<<<(unsigned)((f.n_sup * s->ds + 255) / 256), 256, 0, st>>>(s->seg_q, f.seg_inv, f.n_sup, s->ds);
       count_launch(2);
       s->dec.last_path = 1;
@@ -1100,7 +1136,7 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
       }
       s->begin(4);
       render_backward(bs, map, f.rcw, f.rwc, f.pose.translation, in, rb.w, d_col, d_dep, have_sup ? d_qry : nullptr,
-                      rb.geo_acc, gmap, false);
+                      rb.geo_acc, gmap, false, deterministic() ? &ctx->det : nullptr);
       s->end();
       s->begin(5);
       render_project_backward(bs, map, f.rcw, f.rwc, f.pose.translation, in, rb.w, rb.geo_acc, gmap);
@@ -1525,12 +1561,14 @@ static latmap_status session_capture_step(latmap_session* s, bool with_adam);
 
 latmap_status latmap_session_objective(latmap_session* s, int32_t want_grad, latmap_loss_breakdown* out) {
   if (!s || s->nframes < 1) return LATMAP_ERR_INVALID_ARGUMENT;
+  set_deterministic(s->ctx->deterministic);
   for (int attempt = 0; attempt < 3; ++attempt) {
     latmap_status st = LATMAP_OK;
     if (want_grad && s->use_graph && !s->prof && session_sized(s)) {
       // replayed objective graph (the multi-GPU step: objective -> all-reduce -> apply)
       if ((s->step_graph || s->obj_graph) &&
-          (s->graph_exact != s->ctx->exact_blend || s->graph_dec_path != s->ctx->decoder_path))
+          (s->graph_exact != s->ctx->exact_blend || s->graph_dec_path != s->ctx->decoder_path ||
+           s->graph_det != s->ctx->deterministic))
         s->drop_graph();
       if (!s->obj_graph) {
         st = session_capture_step(s, false);
@@ -1594,6 +1632,7 @@ static latmap_status session_capture_step(latmap_session* s, bool with_adam) {
   CTX_CHECK(ctx, e);
   (with_adam ? s->graph_launches : s->obj_launches) = captured;
   s->graph_exact = ctx->exact_blend;
+  s->graph_det = ctx->deterministic;
   s->graph_dec_path = ctx->decoder_path;
   return LATMAP_OK;
 }
@@ -1613,11 +1652,13 @@ latmap_status latmap_session_set_graphs(latmap_session* s, int32_t enable) {
 
 latmap_status latmap_session_step(latmap_session* s, latmap_loss_breakdown* out) {
   if (!s || s->nframes < 1) return LATMAP_ERR_INVALID_ARGUMENT;
+  set_deterministic(s->ctx->deterministic);
   for (int attempt = 0; attempt < 3; ++attempt) {
     latmap_status st = LATMAP_OK;
     if (s->use_graph && !s->prof && session_sized(s)) {
       if ((s->step_graph || s->obj_graph) &&
-          (s->graph_exact != s->ctx->exact_blend || s->graph_dec_path != s->ctx->decoder_path))
+          (s->graph_exact != s->ctx->exact_blend || s->graph_dec_path != s->ctx->decoder_path ||
+           s->graph_det != s->ctx->deterministic))
         s->drop_graph();
       if (!s->step_graph) {
         st = session_capture_step(s, true);
@@ -1642,6 +1683,7 @@ latmap_status latmap_session_step(latmap_session* s, latmap_loss_breakdown* out)
 latmap_status latmap_session_objective_ex(latmap_session* s, int32_t want_grad, int32_t map_grads,
                                           int32_t use_cached_renders, latmap_loss_breakdown* out) {
   if (!s || s->nframes < 1) return LATMAP_ERR_INVALID_ARGUMENT;
+  set_deterministic(s->ctx->deterministic);
   for (int attempt = 0; attempt < 3; ++attempt) {
     latmap_status st = session_objective(s, want_grad != 0, map_grads != 0, use_cached_renders != 0);
     if (st != LATMAP_OK) return st;
@@ -1655,6 +1697,7 @@ latmap_status latmap_session_objective_ex(latmap_session* s, int32_t want_grad, 
 
 latmap_status latmap_session_step_dict(latmap_session* s, latmap_loss_breakdown* out) {
   if (!s || s->nframes < 1) return LATMAP_ERR_INVALID_ARGUMENT;
+  set_deterministic(s->ctx->deterministic);
   for (int attempt = 0; attempt < 3; ++attempt) {
     latmap_status st = session_objective(s, true, false, true);
     if (st != LATMAP_OK) return st;

@@ -390,7 +390,7 @@ void sgemm(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, f
   if (split < 1) split = 1;
   // small output grids with long reductions: split K across CTAs (atomics into C); C is
   // pre-zeroed for beta == 0, accumulated into for beta == 1.
-  if (split == 1 && gx * gy < 148 && K >= 256 && (beta == 0.f || beta == 1.f)) {
+  if (split == 1 && !deterministic() && gx * gy < 148 && K >= 256 && (beta == 0.f || beta == 1.f)) {
     const int64_t want = (296 + gx * gy - 1) / (gx * gy);
     split = (int)std::max<int64_t>(1, std::min<int64_t>(want, K / 128));
     if (split > 1 && beta == 0.f) zero_block(st, C, M, N, ldc);
@@ -406,7 +406,9 @@ void sgemm(cudaStream_t st, bool ta, bool tb, int64_t M, int64_t N, int64_t K, f
   count_launch();
 }
 
+// split-K factor of the long reductions (atomics); 1 in deterministic mode (fixed order)
 static int split_for(int64_t M, int64_t N, int64_t K) {
+  if (deterministic()) return 1;
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   int64_t s = (148 * 4 + tiles - 1) / tiles;
   s = std::min<int64_t>(s, std::max<int64_t>(1, K / 512));
@@ -451,7 +453,7 @@ void decoder_frame(cudaStream_t st, DecoderWork& w, const float* query, const in
   // Bm^T (n_set x K)
   cudaMemsetAsync(w.bm, 0, sizeof(float) * n_set * k, st);
   {
-    const int64_t rpb = 512;
+    const int64_t rpb = deterministic() ? std::max<int64_t>(npx, 1) : 512;  // one row block: one writer
     dim3 g((unsigned)((k + 127) / 128), (unsigned)((npx + rpb - 1) / rpb));
     bm_accum_kernel<<<g, 128, 0, st>>>(w.buf1, w.beta_r, assignment, npx, (int)k, rpb, w.bm);
     count_launch();
@@ -521,11 +523,15 @@ void reconstruct_backward(cudaStream_t st, const float* q, const float* att, int
   sgemm(st, false, false, n, df, ds, 1.f, q, ds, proj, df, 0.f, s_ndf, df);
   cudaMemsetAsync(d_atoms, 0, sizeof(float) * k * df, st);
   sgemm(st, true, false, k, df, n, 1.f, att, k, d_rec, df, 0.f, d_atoms, df, split_for(k, df, n));
-  sgemm(st, true, false, k, df, n, 1.f, s_nk, k, s_ndf, df, 0.f, d_atoms, df, std::max(2, split_for(k, df, n)));
+  if (deterministic())  // accumulate with beta = 1 (no split: one writer per element)
+    sgemm(st, true, false, k, df, n, 1.f, s_nk, k, s_ndf, df, 1.f, d_atoms, df, 1);
+  else
+    sgemm(st, true, false, k, df, n, 1.f, s_nk, k, s_ndf, df, 0.f, d_atoms, df, std::max(2, split_for(k, df, n)));
   // d_qw = d_logits D ; d_proj = Q^T d_qw ; d_q = d_qw W^T (dictionary.cpp:79-81)
   sgemm(st, false, false, n, df, k, 1.f, s_nk, k, atoms, df, 0.f, s_ndf, df);
   cudaMemsetAsync(d_proj, 0, sizeof(float) * ds * df, st);
-  sgemm(st, true, false, ds, df, n, 1.f, q, ds, s_ndf, df, 0.f, d_proj, df, std::max(2, split_for(ds, df, n)));
+  sgemm(st, true, false, ds, df, n, 1.f, q, ds, s_ndf, df, 0.f, d_proj, df,
+        deterministic() ? 1 : std::max(2, split_for(ds, df, n)));
   sgemm(st, false, true, n, ds, df, 1.f, s_ndf, df, proj, df, 0.f, d_q, ds);
   (void)s_kdf;
 }

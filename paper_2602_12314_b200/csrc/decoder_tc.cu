@@ -573,7 +573,7 @@ __global__ void __launch_bounds__(256) dec_reduce_kernel(const float* __restrict
       stride = (size_t)K * DS / 4;
       ng = groups1;
     }
-    const int per = (ng + kRedSplit - 1) / kRedSplit, g0 = split * per, g1 = min(ng, g0 + per);
+    const int per = (ng + (int)gridDim.y - 1) / (int)gridDim.y, g0 = split * per, g1 = min(ng, g0 + per);
     float4 acc[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -752,7 +752,7 @@ void decoder_frame_tc(cudaStream_t st, DecoderWork& w, const float* query, const
   } else {
     cudaMemsetAsync(w.bm, 0, sizeof(float) * n_set * k, st);
     const int64_t quads = k * 64 / 4;
-    dec_reduce_kernel<<<dim3((unsigned)((quads + 255) / 256), kRedSplit), 256, 0, st>>>(
+    dec_reduce_kernel<<<dim3((unsigned)((quads + 255) / 256), deterministic() ? 1 : kRedSplit), 256, 0, st>>>(
         nullptr, w.bm_part, nullptr, nullptr, (int)k, ds, (int)n_set, 148, 74, nullptr, w.bm, nullptr, nullptr, 0, 1);
     count_launch();
     decoder_bm_embed(st, w.bm, feats, n_set, k, df, d_atoms);
@@ -769,7 +769,7 @@ void decoder_finish_tc(cudaStream_t st, DecoderWork& w, const float* atoms, cons
   const int ds = w.ds, df = w.df;
   if (w.tc_frames > 0) {  // the fused frames' step-summed A and R partials
     const int64_t quads = (k * k + k * ds) / 4;
-    dec_reduce_kernel<<<dim3((unsigned)((quads + 255) / 256), kRedSplit), 256, 0, st>>>(
+    dec_reduce_kernel<<<dim3((unsigned)((quads + 255) / 256), deterministic() ? 1 : kRedSplit), 256, 0, st>>>(
         w.a_part, nullptr, w.r_part, nullptr, (int)k, ds, 0, 148, 74, w.a_acc, nullptr, w.r_acc, nullptr, 1, 0);
     count_launch();
     w.tc_frames = 0;

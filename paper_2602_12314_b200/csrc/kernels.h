@@ -49,11 +49,25 @@ void render_blend(cudaStream_t st, const MapPtrs& map, const Intr& intr, RenderW
                   float* query, float* alpha, bool exact = false);
 void project_single(cudaStream_t st, const float* d_in11, const float rot_cw[9], const float origin[3],
                     const Intr& intr, float* d_out8);
+// Deterministic backward scratch: per-splat pair counts / offsets and the per-(splat, tile)
+// partial rows K8 writes instead of float atomics; reduced in a fixed order.
+struct DetScratch {
+  int64_t *cnt = nullptr, *off = nullptr, *blocks = nullptr;
+  float* part = nullptr;
+  int64_t n_cap = 0, part_cap = 0;
+  cudaError_t ensure(int64_t n, int64_t pairs, int ds);
+  void release();
+};
 // Backward: blend replay + reverse sweep (K8) -> projection backward (K9). Accumulates.
 void render_backward(cudaStream_t st, const MapPtrs& map, const float rot_cw[9], const float rot_wc[9],
                      const float origin[3], const Intr& intr, const RenderWork& w, const float* d_color,
                      const float* d_depth, const float* d_query, float* geo_acc, const MapPtrs& grads,
-                     bool project = true);
+                     bool project = true, DetScratch* det = nullptr);
+// Deterministic reductions for the calling host thread (set by the C-ABI entry points from the
+// context): gradient sums in a fixed order instead of float atomics (render backward, the
+// decoders' partial reductions, segment pooling).
+void set_deterministic(bool on);
+bool deterministic();
 // K9 only (after render_backward(..., project=false)).
 void render_project_backward(cudaStream_t st, const MapPtrs& map, const float rot_cw[9], const float rot_wc[9],
                              const float origin[3], const Intr& intr, const RenderWork& w, float* geo_acc,

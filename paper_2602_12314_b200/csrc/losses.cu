@@ -277,21 +277,30 @@ __global__ void ssim_adj_h_kernel(const float* __restrict__ tmp, const float* __
 // ssim_global, losses.cpp:85-129 (images smaller than the window). One block.
 __global__ void ssim_global_kernel(const float* a, const float* b, int h, int w, int ch, float* d_a, float out_scale,
                                    bool accumulate, double* sum_out) {
+  // fixed-order block reductions (per-thread partials, summed by thread 0 in thread order), so the
+  // result does not depend on warp scheduling
+  __shared__ double part[256][3];
   __shared__ double red[5];
   const float c1 = 0.01f * 0.01f, c2 = 0.03f * 0.03f;
   const int n = h * w;
   double total = 0.0;
-  for (int c = 0; c < ch; ++c) {
-    if (threadIdx.x < 5) red[threadIdx.x] = 0.0;
+  auto block_sum = [&](double x, double y, double z, double* out) {
+    part[threadIdx.x][0] = x, part[threadIdx.x][1] = y, part[threadIdx.x][2] = z;
     __syncthreads();
+    if (threadIdx.x == 0) {
+      double sx = 0, sy = 0, sz = 0;
+      for (unsigned t = 0; t < blockDim.x; ++t) sx += part[t][0], sy += part[t][1], sz += part[t][2];
+      out[0] = sx, out[1] = sy, out[2] = sz;
+    }
+    __syncthreads();
+  };
+  for (int c = 0; c < ch; ++c) {
     double sx = 0, sy = 0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       sx += a[i * ch + c];
       sy += b[i * ch + c];
     }
-    atomicAdd(&red[0], sx);
-    atomicAdd(&red[1], sy);
-    __syncthreads();
+    block_sum(sx, sy, 0.0, red);
     const float mx = (float)(red[0] / n), my = (float)(red[1] / n);
     double vx = 0, vy = 0, cv = 0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -300,10 +309,7 @@ __global__ void ssim_global_kernel(const float* a, const float* b, int h, int w,
       vy += dy * dy;
       cv += dx * dy;
     }
-    atomicAdd(&red[2], vx);
-    atomicAdd(&red[3], vy);
-    atomicAdd(&red[4], cv);
-    __syncthreads();
+    block_sum(vx, vy, cv, red + 2);
     const float fvx = (float)(red[2] / n), fvy = (float)(red[3] / n), fcv = (float)(red[4] / n);
     const float a1 = 2.f * mx * my + c1, a2 = 2.f * fcv + c2;
     const float b1 = mx * mx + my * my + c1, b2 = fvx + fvy + c2;

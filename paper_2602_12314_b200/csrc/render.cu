@@ -682,9 +682,15 @@ struct RasterBwdArgs {
   float* g_feat;   // N x ds
   const int32_t* order;
   const int64_t* counters;
+  // deterministic mode (nullptr = float atomics): per (splat, tile) partial rows, splat-major,
+  // tiles of a splat in row-major order: row = splat_off[src] + rank(tile in the splat's rect)
+  float* pair_part;
+  const int64_t* splat_off;
 };
 
 constexpr int kBwdBatch = 16;  // splats per batch (one MMA M tile)
+// deterministic partial row: [geo 8 | colour 3, pad | features ds padded to 4]
+__host__ __device__ constexpr int det_width(int ds) { return 12 + (ds + 3) / 4 * 4; }
 
 __device__ __forceinline__ uint32_t to_tf32(float x) {
   uint32_t r;
@@ -1306,11 +1312,19 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
     {
       constexpr int SL = 5 + DSP / 4;  // slots per splat
       const bool vf = (a.ds & 3) == 0 && (reinterpret_cast<uintptr_t>(a.g_feat) & 15) == 0;
+      const int DW = det_width(a.ds);
       for (int e = tid; e < cnt * SL; e += blockDim.x) {
         const int j = e / SL, k = e % SL;
         const float* ac = s_acc + j * NACC;
         const float* row = raw + j * RP;
         const size_t src = __float_as_uint(row[15]);
+        float* det = nullptr;  // this (splat, tile) pair's partial row (deterministic mode)
+        if (a.pair_part) {
+          const int4 bb = f4_as_i4(*reinterpret_cast<const float4*>(row + 8));
+          const int rtx0 = bb.x / kTile, rtx1 = bb.y / kTile, rty0 = bb.z / kTile;
+          const int rank = (ty0 / kTile - rty0) * (rtx1 - rtx0 + 1) + (tx0 / kTile - rtx0);
+          det = a.pair_part + (size_t)(a.splat_off[src] + rank) * DW;
+        }
         if (k < 2) {
           // moments M0..M5 of the drho rows -> dmean_u, dmean_v, dA00, dA01 | dA11, dz, dg
           const float up = row[0] - ((float)tx0 + 7.5f), vp = row[1] - ((float)ty0 + 7.5f);
@@ -1323,16 +1337,23 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
           } else {
             v = make_float4(M[5] - 2.f * vp * M[2] + vp * vp * M[0], ac[3], ac[NU + 8], 0.f);
           }
-          if (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f)
+          if (det)
+            reinterpret_cast<float4*>(det)[k] = v;
+          else if (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f)
             atomicAdd(reinterpret_cast<float4*>(a.geo_acc + src * 8) + k, v);
         } else if (k < 5) {
           const float val = ac[k - 2];
-          if (val != 0.f) atomicAdd(&a.g_col[src * 3 + (k - 2)], val);
+          if (det)
+            det[8 + (k - 2)] = val;
+          else if (val != 0.f)
+            atomicAdd(&a.g_col[src * 3 + (k - 2)], val);
         } else {
           const int c0 = 4 * (k - 5);
           if (c0 < a.ds) {
             const float4 v = make_float4(ac[4 + c0], ac[5 + c0], ac[6 + c0], ac[7 + c0]);
-            if (vf) {
+            if (det) {
+              reinterpret_cast<float4*>(det + 12)[k - 5] = v;
+            } else if (vf) {
               if (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f)
                 atomicAdd(reinterpret_cast<float4*>(a.g_feat + src * a.ds + c0), v);
             } else {
@@ -1614,14 +1635,137 @@ void render_blend(cudaStream_t st, const MapPtrs& map, const Intr& intr, RenderW
   count_launch();
 }
 
+// ---- deterministic backward (K8 writes per-(splat, tile) partial rows; these kernels place and
+// reduce them in a fixed order: a splat's tiles in row-major order of its tile rectangle)
+__global__ void det_count_kernel(const SplatRec* __restrict__ rec, int64_t n, int64_t* __restrict__ cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int4 bb = reinterpret_cast<const int4*>(rec + i)[2];
+    cnt[i] = (bb.x > bb.y || bb.z > bb.w) ? 0
+                                           : (int64_t)(bb.y / kTile - bb.x / kTile + 1) * (bb.w / kTile - bb.z / kTile + 1);
+  }
+}
+// exclusive scan in place, 1024 elements per block: local scan + block totals
+__global__ void __launch_bounds__(1024) det_scan_local_kernel(int64_t* __restrict__ v, int64_t n,
+                                                               int64_t* __restrict__ block_sum) {
+  __shared__ int64_t s[1024];
+  const int64_t i = blockIdx.x * 1024 + threadIdx.x;
+  const int64_t x = i < n ? v[i] : 0;
+  s[threadIdx.x] = x;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const int64_t t = threadIdx.x >= (unsigned)o ? s[threadIdx.x - o] : 0;
+    __syncthreads();
+    s[threadIdx.x] += t;
+    __syncthreads();
+  }
+  if (i < n) v[i] = s[threadIdx.x] - x;
+  if (threadIdx.x == 1023) block_sum[blockIdx.x] = s[1023];
+}
+__global__ void det_scan_blocks_kernel(int64_t* block_sum, int64_t nb) {  // one thread: nb is small
+  int64_t run = 0;
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t x = block_sum[b];
+    block_sum[b] = run;
+    run += x;
+  }
+}
+__global__ void det_scan_add_kernel(int64_t* __restrict__ v, int64_t n, const int64_t* __restrict__ block_sum) {
+  const int64_t i = blockIdx.x * 1024 + threadIdx.x;
+  if (i < n) v[i] += block_sum[blockIdx.x];
+}
+// per (splat, float4 slot): sum the splat's rows in order; geo -> geo_acc (store), colour and
+// features added into the map gradients (one writer per element)
+__global__ void det_reduce_kernel(const float* __restrict__ part, const int64_t* __restrict__ off,
+                                  const int64_t* __restrict__ cnt, int64_t n, int ds, float* __restrict__ geo_acc,
+                                  float* __restrict__ g_col, float* __restrict__ g_feat) {
+  const int DW = det_width(ds), slots = DW / 4;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * slots; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / slots;
+    const int q = (int)(e % slots);
+    const int64_t c = cnt[i];
+    if (c == 0) continue;
+    const float4* p = reinterpret_cast<const float4*>(part + (size_t)off[i] * DW) + q;
+    float4 acc = p[0];
+    for (int64_t r = 1; r < c; ++r) {
+      const float4 v = p[(size_t)r * (DW / 4)];
+      acc.x += v.x, acc.y += v.y, acc.z += v.z, acc.w += v.w;
+    }
+    if (q < 2) {
+      reinterpret_cast<float4*>(geo_acc + i * 8)[q] = acc;
+    } else if (q == 2) {
+      g_col[i * 3 + 0] += acc.x, g_col[i * 3 + 1] += acc.y, g_col[i * 3 + 2] += acc.z;
+    } else {
+      const int c0 = 4 * (q - 3);
+      const float vv[4] = {acc.x, acc.y, acc.z, acc.w};
+      for (int k = 0; k < 4 && c0 + k < ds; ++k) g_feat[i * ds + c0 + k] += vv[k];
+    }
+  }
+}
+
+namespace {
+thread_local bool t_deterministic = false;
+}
+void set_deterministic(bool on) { t_deterministic = on; }
+bool deterministic() { return t_deterministic; }
+
+cudaError_t DetScratch::ensure(int64_t n, int64_t pairs, int ds) {
+  cudaError_t e = cudaSuccess;
+  if (n > n_cap) {
+    if (cnt) cudaFree(cnt), cnt = nullptr;
+    if (off) cudaFree(off), off = nullptr;
+    if (blocks) cudaFree(blocks), blocks = nullptr;
+    n_cap = 0;
+    const int64_t nb = (n + 1023) / 1024;
+    if ((e = cudaMalloc(&cnt, sizeof(int64_t) * n)) || (e = cudaMalloc(&off, sizeof(int64_t) * n)) ||
+        (e = cudaMalloc(&blocks, sizeof(int64_t) * nb)))
+      return e;
+    n_cap = n;
+  }
+  const int64_t need = pairs * det_width(ds);
+  if (need > part_cap) {
+    if (part) cudaFree(part), part = nullptr;
+    part_cap = 0;
+    if ((e = cudaMalloc(&part, sizeof(float) * need))) return e;
+    part_cap = need;
+  }
+  return e;
+}
+
+void DetScratch::release() {
+  for (void* p : {(void*)cnt, (void*)off, (void*)blocks, (void*)part})
+    if (p) cudaFree(p);
+  cnt = off = blocks = nullptr;
+  part = nullptr;
+  n_cap = part_cap = 0;
+}
+
 void render_backward(cudaStream_t st, const MapPtrs& map, const float rot_cw[9], const float rot_wc[9],
                      const float origin[3], const Intr& intr, const RenderWork& w, const float* d_color,
                      const float* d_depth, const float* d_query, float* geo_acc, const MapPtrs& grads,
-                     bool project) {
+                     bool project, DetScratch* det) {
   const int ntiles = w.tiles_x * w.tiles_y;
   RasterBwdArgs a{w.rec, map.col, map.feat, map.ds, w.tile_offset, w.keys, w.tiles_x, intr.width, intr.height,
                   w.px_last, w.px_T, w.tile_max_last, d_color, d_depth, d_query, geo_acc, grads.col, grads.feat,
-                  w.tile_order, w.counters};
+                  w.tile_order, w.counters, nullptr, nullptr};
+  if (det && map.n > 0) {
+    // rows of every (splat, tile) pair (capacity: the tile-pair arrays), zeroed: pairs no tile
+    // processed (beyond a tile's last blended entry, empty tiles) contribute nothing
+    if (det->ensure(map.n, w.pair_cap, map.ds) != cudaSuccess) {
+      set_sticky_error("render_backward: deterministic scratch allocation failed");
+      return;
+    }
+    const unsigned g = (unsigned)std::min<int64_t>((map.n + 255) / 256, 148 * 8);
+    det_count_kernel<<<g, 256, 0, st>>>(w.rec, map.n, det->cnt);
+    cudaMemcpyAsync(det->off, det->cnt, sizeof(int64_t) * map.n, cudaMemcpyDeviceToDevice, st);
+    const int64_t nb = (map.n + 1023) / 1024;
+    det_scan_local_kernel<<<(unsigned)nb, 1024, 0, st>>>(det->off, map.n, det->blocks);
+    det_scan_blocks_kernel<<<1, 1, 0, st>>>(det->blocks, nb);
+    det_scan_add_kernel<<<(unsigned)nb, 1024, 0, st>>>(det->off, map.n, det->blocks);
+    cudaMemsetAsync(det->part, 0, sizeof(float) * w.pair_cap * det_width(map.ds), st);
+    count_launch(4);
+    a.pair_part = det->part;
+    a.splat_off = det->off;
+  }
   switch (pad_ds(map.ds)) {
     case 4: launch_bwd<4>(st, ntiles, a); break;
     case 8: launch_bwd<8>(st, ntiles, a); break;
@@ -1631,6 +1775,12 @@ void render_backward(cudaStream_t st, const MapPtrs& map, const float rot_cw[9],
     default: break;
   }
   count_launch();
+  if (a.pair_part) {
+    const int64_t work = map.n * (det_width(map.ds) / 4);
+    det_reduce_kernel<<<(unsigned)std::min<int64_t>((work + 255) / 256, 148 * 16), 256, 0, st>>>(
+        det->part, det->off, det->cnt, map.n, map.ds, geo_acc, grads.col, grads.feat);
+    count_launch();
+  }
   if (!project) return;
   render_project_backward(st, map, rot_cw, rot_wc, origin, intr, w, geo_acc, grads);
 }

@@ -472,12 +472,18 @@ def test_export_import_rows_keep_and_append(ctx, cfg0):
     _moved_like("colors", after["colors"], nm.colors, g2.colors, 2.5e-3, 2)
 
 
-def test_session_segment_supervision_config0(ctx, cfg0):
+@pytest.mark.parametrize("det", [False, True])
+def test_session_segment_supervision_config0(ctx, cfg0, det):
     """feature_supervision = "segment" (objective.cpp:37-64, 147-157): queries pooled per present
-    assignment row, the row gradient shared equally by the segment's pixels."""
+    assignment row, the row gradient shared equally by the segment's pixels (also in the
+    deterministic mode, whose pooling sums each segment in raster order)."""
     w = cfg0
     s = make_session(ctx, w, segment_mode=1, decoder_precision=0)
-    loss = s.objective(want_grad=True)
+    ctx.set_deterministic(det)
+    try:
+        loss = s.objective(want_grad=True)
+    finally:
+        ctx.set_deterministic(False)
     d = oracle.Dictionary(w.atoms.copy(), w.anchor.copy(), w.proj.copy(), np.float32(w.temperature))
     cfg = oracle_cfg(w)
     cfg.segment_mode = True
