@@ -2,7 +2,7 @@
  * latmap_b200.h — C-ABI of the B200-native latent-map optimisation step.
  *
  * Drop-in boundary for the reference operator API in
- * /root/reference/proj/include/latmap/** (LatentAM CPU reference). Every entry
+ * /root/reference/proj/include/latmap/ (LatentAM CPU reference). Every entry
  * point names the reference interface it replaces (file:line, relative to
  * /root/reference/proj/). Conventions:
  *   - extern "C", plain pointers and sizes, no C++ types, no exceptions;

@@ -67,6 +67,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 __device__ __forceinline__ int4 f4_as_i4(float4 v) {
   return make_int4(__float_as_int(v.x), __float_as_int(v.y), __float_as_int(v.z), __float_as_int(v.w));
 }
+__device__ __forceinline__ float4 i4_as_f4(int4 v) {
+  return make_float4(__int_as_float(v.x), __int_as_float(v.y), __int_as_float(v.z), __int_as_float(v.w));
+}
 
 // 2^x and 1/x on the SFU (approximate; used only where gradient accuracy suffices)
 __device__ __forceinline__ float ex2_approx(float x) {

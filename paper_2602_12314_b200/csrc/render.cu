@@ -937,32 +937,39 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_fwd_mma_kernel(RasterAr
 // ~fp32 accurate):  [dcolor, dz, dfeat] = W^T U  (U = per-pixel upstream [uc, uz, uq]),
 // and the drho moments  sum drho * [1, x, y, x^2, xy, y^2]  (+ sum dg), from which
 // dmean and dA (render.cpp:345-352) follow per splat in closed form.
-// Batches are staged with cp.async one batch ahead (record, colour, features of 16 splats,
-// issued by 16 lanes of warp 0), and a warp whose 8x4 pixel block meets none of the batch's
-// bboxes, or whose pixels all stopped before the batch, skips the batch entirely.
+// Two barriers per batch. Phase 1: the warps' sweep and tensor-core reductions of batch i,
+// the tf32 split of batch i+1 (staged one batch earlier) and the cp.async staging of batch
+// i+2 (record, colour, features; 16 lanes of warp 0). Phase 2: each (splat, output slot) sums
+// its entries over the active warps' partials and forms the closed-form gradients. A warp
+// whose 8x4 pixel block meets none of the batch's bboxes, or whose pixels all stopped before
+// the batch, skips the batch's sweep and contributes nothing.
 template <int DSP>
-__global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArgs a) {
+__global__ void __launch_bounds__(kTilePixels, DSP >= 64 ? 1 : 2) raster_bwd_kernel(RasterBwdArgs a) {
   constexpr int NU = ((4 + DSP) + 7) / 8 * 8;  // U columns: uc0..2, uz, uq[DSP], pad
   constexpr int NT = NU / 8;                   // n-tiles of the W^T U product
   // U row pitch = 8 mod 16 plus a column XOR swizzle on row bit 2: both the row-fragment
-  // (value MMA) and the column-fragment (W^T U MMA) loads are bank-conflict free
+  // (value MMA) and the column-fragment (W^T U MMA) loads are bank conflict free
   constexpr int UP = NU % 16 == 8 ? NU : NU + 8;
-  constexpr int WP = 36;                       // per-warp [splat][pixel] pitch (floats)
-  constexpr int NACC = NU + 8 + 8;             // per-splat accumulators: W^T U | drho moments | dg
+  constexpr int NACC = NU + 8 + 8;             // per-splat partial entries: W^T U | drho moments | dg
   constexpr int NUP = NU + 4;                  // splat-row pitch (B-fragment loads hit distinct banks)
   constexpr int PP = (NACC + 23) / 32 * 32 + 8;  // per-warp partial pitch (= 8 mod 32)
+  // per-warp [splat][pixel] pitch: 32 with an XOR swizzle of the pixel index by the splat row
+  // (conflict-free row writes and fragment reads), 36 padded when the partials need the room
+  constexpr int WP = 16 * PP <= 3 * kBwdBatch * 32 ? 32 : 36;
   // raw staging row (floats): [SplatRec 12 | colour 3 | source bits | features DSP (padded to 4)]
-  constexpr int RP = 16 + (DSP + 3) / 4 * 4;
+  constexpr int RP = 16 + (DSP + 3) / 4 * 4 + ((DSP + 3) / 4 % 2 == 0 ? 4 : 0);
   static_assert(16 * PP <= 3 * kBwdBatch * WP, "warp partials must fit the warp's staging area");
   auto uidx = [](int p, int c) { return p * UP + (c ^ (((p >> 2) & 1) << 2)); };
+  auto widx = [](int j, int p) { return j * WP + (WP == 32 ? (p ^ ((j & 7) << 2)) : p); };
   extern __shared__ __align__(16) float s_dyn[];
   float* s_u = s_dyn;                                          // [256][UP] per-pixel upstream rows
   float* s_wbase = s_dyn + kTilePixels * UP;                   // [8 warps][3][16 * WP]: W, drho, dg
-  __shared__ __align__(16) float s_fh[kBwdBatch * NUP];      // splat rows [c0 c1 c2 z f...], tf32 hi
-  __shared__ __align__(16) float s_fl[kBwdBatch * NUP];      //   ... and tf32 lo
-  __shared__ __align__(16) float s_raw[2][kBwdBatch * RP];   // cp.async staging, double-buffered
-  __shared__ __align__(16) float4 s_sp[kBwdBatch][3];        // {mx,my,q00,q01} {q11,alpha} {bbox}
-  __shared__ float s_acc[kBwdBatch * NACC];
+  __shared__ __align__(16) float s_fh[2][kBwdBatch * NUP];   // splat rows [c0 c1 c2 z f...], tf32 hi
+  __shared__ __align__(16) float s_fl[2][kBwdBatch * NUP];   //   ... and tf32 lo
+  __shared__ __align__(16) float s_raw[2][kBwdBatch * RP];   // cp.async staging
+  // per splat: {mx, my, q00', 2q01'} {q11', alpha, A00, A01} {x0, x1 - x0, y0, y1 - y0}
+  // {A10, A11, source bits, -}; a padding row has x0 = INT_MAX / 2 (meets no pixel)
+  __shared__ __align__(16) float4 s_sp[2][4][kBwdBatch];  // [slot][field][splat]
   __shared__ int32_t s_wact[8];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tile = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
@@ -973,11 +980,14 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
   const int start = a.offset[tile];
   const int tend = start + a.tile_max_last[tile];
   if (tend <= start) return;
+  const int nbatch = (tend - start + kBwdBatch - 1) / kBwdBatch;
+  auto batch_lo = [&](int b) { return max(start, tend - kBwdBatch * (b + 1)); };
+  auto batch_hi = [&](int b) { return tend - kBwdBatch * b; };
   const bool vec_feat = (a.ds & 3) == 0 && (reinterpret_cast<uintptr_t>(a.feats) & 15) == 0;
-  // warp 0, lanes 0..15: stage splat `lane` of the batch [lo, lo + cnt) into raw buffer `buf`
-  auto stage = [&](int buf, int lo, int cnt, uint32_t src) {
+  // warp 0, lanes 0..15: stage splat `lane` of batch b (source src) into raw buffer `buf`
+  auto stage = [&](int buf, int b, uint32_t src) {
     float* row = s_raw[buf] + lane * RP;
-    if (lane < cnt) {
+    if (lane < batch_hi(b) - batch_lo(b)) {
       const float4* rg = reinterpret_cast<const float4*>(a.rec + src);
       cp_async16(row, rg);
       cp_async16(row + 4, rg + 1);
@@ -998,7 +1008,45 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
       reinterpret_cast<int32_t*>(row)[8] = 1;  // empty bbox (x0 > x1)
     }
   };
+  auto src_of = [&](int b) -> uint32_t {  // lanes < 16: source of splat `lane` of batch b
+    if (b >= nbatch) return 0u;
+    const int lo = batch_lo(b);
+    return lane < batch_hi(b) - lo ? (uint32_t)a.keys[lo + lane] : 0u;
+  };
+  constexpr float kNegHalfLog2e = -0.72134752044448170f;  // -0.5 * log2(e)
+  // split staged raw buffer `buf` into the tf32 hi/lo splat rows and per-splat terms of slot `sb`
+  auto split_batch = [&](int buf, int sb) {
+    const float* raw = s_raw[buf];
+    for (int e = tid; e < kBwdBatch * NU; e += kTilePixels) {
+      const int j = e / NU, c = e % NU;
+      const float* row = raw + j * RP;
+      const float v = c < 3 ? row[12 + c] : (c == 3 ? row[2] : (c - 4 < DSP ? row[16 + c - 4] : 0.f));
+      uint32_t h, l;
+      split_tf32(v, h, l);
+      s_fh[sb][j * NUP + c] = __uint_as_float(h);
+      s_fl[sb][j * NUP + c] = __uint_as_float(l);
+    }
+    if (tid < kBwdBatch) {
+      const float* row = raw + tid * RP;
+      s_sp[sb][0][tid] = make_float4(row[0], row[1], kNegHalfLog2e * row[4], kNegHalfLog2e * (2.f * row[5]));
+      s_sp[sb][1][tid] = make_float4(kNegHalfLog2e * row[7], row[3], row[4], row[5]);
+      int4 bb = *reinterpret_cast<const int4*>(row + 8);
+      bb.y -= bb.x;
+      bb.w -= bb.z;
+      if (bb.y < 0 || bb.w < 0) bb = make_int4(0x3fffffff, 0, 0x3fffffff, 0);
+      s_sp[sb][2][tid] = i4_as_f4(bb);
+      s_sp[sb][3][tid] = make_float4(row[6], row[7], row[15], 0.f);
+    }
+  };
   const size_t p = inside ? (size_t)py * a.width + px : 0;
+  // prologue: stage batches 0 and 1, fetch the sources of batch 2
+  uint32_t nsrc = 0;
+  if (warp == 0 && lane < kBwdBatch) {
+    stage(0, 0, src_of(0));
+    if (nbatch > 1) stage(1, 1, src_of(1));
+    cp_async_commit();
+    nsrc = src_of(2);
+  }
   // per-pixel upstream row U[p] = [uc0, uc1, uc2, uz, uq...] (zero outside the image)
   int last = 0;
   float T = 1.f;
@@ -1018,8 +1066,11 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
     s_u[uidx(tid, 1)] = uc1;
     s_u[uidx(tid, 2)] = uc2;
     s_u[uidx(tid, 3)] = uz;
+    if constexpr (NU - (4 + DSP) == 4)  // the 4 pad columns are one swizzled float4
+      *reinterpret_cast<float4*>(s_u + uidx(tid, 4 + DSP)) = make_float4(0.f, 0.f, 0.f, 0.f);
+    else
 #pragma unroll
-    for (int c = 4 + DSP; c < NU; ++c) s_u[uidx(tid, c)] = 0.f;
+      for (int c = 4 + DSP; c < NU; ++c) s_u[uidx(tid, c)] = 0.f;
     // query gradients: the tile's 16 pixel rows are contiguous runs of 16 * ds floats, read
     // cooperatively (coalesced 16-byte loads when ds % 4 == 0)
     const bool vq = a.d_query && (a.ds & 3) == 0 && (reinterpret_cast<uintptr_t>(a.d_query) & 15) == 0;
@@ -1028,13 +1079,11 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
       for (int i = tid; i < kTilePixels * (DSP / 4); i += kTilePixels) {
         const int pl = i / (DSP / 4), c4 = i % (DSP / 4);
         const int qx = tx0 + tile_dx(pl), qy = ty0 + tile_dy(pl);
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        float* dst = s_u + uidx(pl, 4 + 4 * c4);  // the swizzle keeps 4-column groups contiguous
         if (c4 < q4 && qx < a.width && qy < a.height)
-          v = reinterpret_cast<const float4*>(a.d_query)[((size_t)qy * a.width + qx) * q4 + c4];
-        s_u[uidx(pl, 4 + 4 * c4)] = v.x;
-        s_u[uidx(pl, 5 + 4 * c4)] = v.y;
-        s_u[uidx(pl, 6 + 4 * c4)] = v.z;
-        s_u[uidx(pl, 7 + 4 * c4)] = v.w;
+          cp_async16(dst, reinterpret_cast<const float4*>(a.d_query) + ((size_t)qy * a.width + qx) * q4 + c4);
+        else
+          *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
       }
     } else {
 #pragma unroll
@@ -1073,61 +1122,32 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
   float* sw_w = s_wbase + (warp * 3 + 0) * kBwdBatch * WP;
   float* sw_r = s_wbase + (warp * 3 + 1) * kBwdBatch * WP;
   float* sw_g = s_wbase + (warp * 3 + 2) * kBwdBatch * WP;
-  constexpr float kNegHalfLog2e = -0.72134752044448170f;  // -0.5 * log2(e)
-  // prologue: stage batch 0, fetch the sources of batch 1
-  uint32_t nsrc = 0;
-  {
-    const int lo0 = max(start, tend - kBwdBatch);
-    if (warp == 0 && lane < kBwdBatch) {
-      const int cnt0 = tend - lo0;
-      stage(0, lo0, cnt0, lane < cnt0 ? (uint32_t)a.keys[lo0 + lane] : 0u);
-      cp_async_commit();
-      const int lo1 = max(start, lo0 - kBwdBatch);
-      if (lane < lo0 - lo1) nsrc = (uint32_t)a.keys[lo1 + lane];
-    }
-  }
-  int it = 0;
-  for (int hi = tend; hi > start; hi -= kBwdBatch, ++it) {
-    const int lo = max(start, hi - kBwdBatch);
-    const int cnt = hi - lo;
+  cp_async_wait_all();
+  __syncthreads();
+  split_batch(0, 0);
+  __syncthreads();
+  for (int it = 0; it < nbatch; ++it) {
+    const int lo = batch_lo(it);
+    const int cnt = batch_hi(it) - lo;
     const int cur = it & 1;
-    const float* raw = s_raw[cur];
-    cp_async_wait_all();
-    __syncthreads();
-    // ---- split the staged batch into tf32 hi/lo splat rows and the prescaled per-splat terms
-    for (int e = tid; e < kBwdBatch * NU; e += blockDim.x) {
-      const int j = e / NU, c = e % NU;
-      const float* row = raw + j * RP;
-      const float v = c < 3 ? row[12 + c] : (c == 3 ? row[2] : (c - 4 < DSP ? row[16 + c - 4] : 0.f));
-      uint32_t h, l;
-      split_tf32(v, h, l);
-      s_fh[j * NUP + c] = __uint_as_float(h);
-      s_fl[j * NUP + c] = __uint_as_float(l);
+    // ======== phase 1
+    // stage batch it+2 into the raw buffer batch it used (split in the previous phase 1)
+    if (warp == 0 && lane < kBwdBatch && it + 2 < nbatch) {
+      stage(cur, it + 2, nsrc);
+      cp_async_commit();
+      nsrc = src_of(it + 3);
     }
-    if (tid < kBwdBatch) {
-      const float* row = raw + tid * RP;
-      s_sp[tid][0] = make_float4(row[0], row[1], kNegHalfLog2e * row[4], kNegHalfLog2e * (2.f * row[5]));
-      s_sp[tid][1] = make_float4(kNegHalfLog2e * row[7], row[3], 0.f, 0.f);
-      s_sp[tid][2] = *reinterpret_cast<const float4*>(row + 8);
-    }
-    // ---- prefetch the next batch into the other buffer (free: last read before the barrier)
-    if (warp == 0 && lane < kBwdBatch) {
-      const int nhi = lo, nlo = max(start, lo - kBwdBatch);
-      if (nhi > start) {
-        stage(cur ^ 1, nlo, nhi - nlo, nsrc);
-        cp_async_commit();
-        const int nnlo = max(start, nlo - kBwdBatch);
-        nsrc = lane < nlo - nnlo ? (uint32_t)a.keys[nnlo + lane] : 0u;
-      }
-    }
-    __syncthreads();
-    // ---- warp activity: some pixel of the block still blends at this batch and some bbox meets it
+    // split batch it+1 (landed before the previous barrier) for the next phase 1
+    if (it + 1 < nbatch) split_batch(cur ^ 1, cur ^ 1);
+    const float* fh = s_fh[cur];
+    const float* fl = s_fl[cur];
+    // warp activity: some pixel of the block still blends at this batch and some bbox meets it
     bool act = (lo - start) < warp_last;
     if (act) {
       bool meets = false;
       if (lane < cnt) {
-        const int4 bb = f4_as_i4(s_sp[lane][2]);
-        meets = bb.x <= bx0 + 7 && bb.y >= bx0 && bb.z <= by0 + 3 && bb.w >= by0;
+        const int4 bb = f4_as_i4(s_sp[cur][2][lane]);
+        meets = bb.x <= bx0 + 7 && bb.x + bb.y >= bx0 && bb.z <= by0 + 3 && bb.z + bb.w >= by0;
       }
       act = __any_sync(0xffffffffu, meets);
     }
@@ -1156,8 +1176,8 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
 #pragma unroll
           for (int nt = 0; nt < 2; ++nt) {
             const int fo = (8 * nt + g) * NUP + 8 * ks + cq;
-            const uint32_t bh[2] = {__float_as_uint(s_fh[fo]), __float_as_uint(s_fh[fo + 4])};
-            const uint32_t bl[2] = {__float_as_uint(s_fl[fo]), __float_as_uint(s_fl[fo + 4])};
+            const uint32_t bh[2] = {__float_as_uint(fh[fo]), __float_as_uint(fh[fo + 4])};
+            const uint32_t bl[2] = {__float_as_uint(fl[fo]), __float_as_uint(fl[fo + 4])};
 #pragma unroll
             for (int mt = 0; mt < 2; ++mt) {
               mma_tf32(va[mt][nt], ul[mt], bh);
@@ -1170,11 +1190,11 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
         for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
           for (int nt = 0; nt < 2; ++nt) {
-            float* d = sw_g + (8 * nt + 2 * cq) * WP + 16 * mt + g;
-            d[0] = va[mt][nt][0];
-            d[WP] = va[mt][nt][1];
-            d[8] = va[mt][nt][2];
-            d[WP + 8] = va[mt][nt][3];
+            const int r = 8 * nt + 2 * cq, c = 16 * mt + g;
+            sw_g[widx(r, c)] = va[mt][nt][0];
+            sw_g[widx(r + 1, c)] = va[mt][nt][1];
+            sw_g[widx(r, c + 8)] = va[mt][nt][2];
+            sw_g[widx(r + 1, c + 8)] = va[mt][nt][3];
           }
         __syncwarp();
       }
@@ -1182,7 +1202,7 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
       // independently (ILP), then the transmittance recovery / d_alpha chain runs serially.
       // The set of blended (pixel, splat) pairs comes from the forward (px_last), so alpha' only
       // needs gradient accuracy here (SFU exp2 / reciprocal).
-      const int rel = lo - start;
+      const int jl = last - (lo - start);  // splats j < jl of this batch are in the pixel's blend list
 #pragma unroll
       for (int j4 = kBwdBatch - 4; j4 >= 0; j4 -= 4) {
         float alv[4], ex[4], rv[4];
@@ -1191,16 +1211,15 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
 #pragma unroll
         for (int u = 3; u >= 0; --u) {
           const int j = j4 + u;
-          const int4 bb = f4_as_i4(s_sp[j][2]);
-          ok[u] = j < cnt && rel + j < last && (unsigned)(px - bb.x) <= (unsigned)(bb.y - bb.x) &&
-                  (unsigned)(py - bb.z) <= (unsigned)(bb.w - bb.z);
+          const int4 bb = f4_as_i4(s_sp[cur][2][j]);
+          ok[u] = j < jl && (unsigned)(px - bb.x) <= (unsigned)bb.y && (unsigned)(py - bb.z) <= (unsigned)bb.w;
           any |= ok[u];
         }
         if (__any_sync(0xffffffffu, any)) {
 #pragma unroll
           for (int u = 3; u >= 0; --u) {
-            const float4 s0 = s_sp[j4 + u][0];
-            const float4 s1 = s_sp[j4 + u][1];
+            const float4 s0 = s_sp[cur][0][j4 + u];
+            const float4 s1 = s_sp[cur][1][j4 + u];
             const float dx = fx - s0.x;
             const float dy = fy - s0.y;
             const float pw = fmaf(dx, fmaf(s0.z, dx, s0.w * dy), s1.x * dy * dy);
@@ -1219,7 +1238,7 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
           if (ok[u]) {
             const float Tb = T * rv[u];
             w = alv[u] * Tb;
-            const float value = sw_g[j * WP + lane];
+            const float value = sw_g[widx(j, lane)];
             const float d_alpha = Tb * value - s_after * rv[u];
             s_after = fmaf(w, value, s_after);
             if (unc[u]) {
@@ -1228,9 +1247,9 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
             }
             T = Tb;
           }
-          sw_w[j * WP + lane] = w;
-          sw_r[j * WP + lane] = drho;
-          sw_g[j * WP + lane] = dg;
+          sw_w[widx(j, lane)] = w;
+          sw_r[widx(j, lane)] = drho;
+          sw_g[widx(j, lane)] = dg;
         }
       }
       __syncwarp();
@@ -1244,10 +1263,10 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
       for (int ks = 0; ks < 4; ++ks) {
         // A = W^T (rows: splats j, cols: pixels) ; split into tf32 hi/lo
         uint32_t ah[4], al_[4];
-        split_tf32(sw_w[g * WP + 8 * ks + cq], ah[0], al_[0]);
-        split_tf32(sw_w[(g + 8) * WP + 8 * ks + cq], ah[1], al_[1]);
-        split_tf32(sw_w[g * WP + 8 * ks + cq + 4], ah[2], al_[2]);
-        split_tf32(sw_w[(g + 8) * WP + 8 * ks + cq + 4], ah[3], al_[3]);
+        split_tf32(sw_w[widx(g, 8 * ks + cq)], ah[0], al_[0]);
+        split_tf32(sw_w[widx(g + 8, 8 * ks + cq)], ah[1], al_[1]);
+        split_tf32(sw_w[widx(g, 8 * ks + cq + 4)], ah[2], al_[2]);
+        split_tf32(sw_w[widx(g + 8, 8 * ks + cq + 4)], ah[3], al_[3]);
         const int prow = 32 * warp + 8 * ks + cq;  // pixel (k index) of b0; b1 is +4
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
@@ -1263,10 +1282,10 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
         for (int mt = 0; mt < 2; ++mt) {
           const float* src = mt ? sw_g : sw_r;
           uint32_t rh[4], rl[4];
-          split_tf32(src[g * WP + 8 * ks + cq], rh[0], rl[0]);
-          split_tf32(src[(g + 8) * WP + 8 * ks + cq], rh[1], rl[1]);
-          split_tf32(src[g * WP + 8 * ks + cq + 4], rh[2], rl[2]);
-          split_tf32(src[(g + 8) * WP + 8 * ks + cq + 4], rh[3], rl[3]);
+          split_tf32(src[widx(g, 8 * ks + cq)], rh[0], rl[0]);
+          split_tf32(src[widx(g + 8, 8 * ks + cq)], rh[1], rl[1]);
+          split_tf32(src[widx(g, 8 * ks + cq + 4)], rh[2], rl[2]);
+          split_tf32(src[widx(g + 8, 8 * ks + cq + 4)], rh[3], rl[3]);
           mma_tf32(dmo[mt], rh, xb[ks]);
           mma_tf32(dmo[mt], rl, xb[ks]);
         }
@@ -1287,84 +1306,106 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_bwd_kernel(RasterBwdArg
       }
     }
     __syncthreads();
-
-    // ---- cross-warp sum over the active warps (fixed entries per thread)
+    // ======== phase 2: per-splat sums of the active warps' partials (fixed warp order), closed
+    // forms and global accumulation. Threads [0, 4 * DSP) own one float4 feature column of one
+    // splat each; warp 7 owns the geometry + colour row of every splat (two lanes per splat, one
+    // per half of the warps). All partial reads are 16-byte.
     {
       int wm = 0;
 #pragma unroll
       for (int w8 = 0; w8 < 8; ++w8) wm |= s_wact[w8] << w8;
-#pragma unroll
-      for (int k = 0; k < (kBwdBatch * NACC + kTilePixels - 1) / kTilePixels; ++k) {
-        const int e = tid + k * kTilePixels;
-        if (e < kBwdBatch * NACC) {
-          const int j = e / NACC, c = e % NACC;
-          float v = 0.f;
+      constexpr int WS = 3 * kBwdBatch * WP;  // warp stride of the partial areas
+      constexpr int FC = DSP / 4;             // float4 feature columns per splat
+      const int DW = det_width(a.ds);
+      auto det_row = [&](int j, size_t src) -> float* {  // (splat, tile) partial row, deterministic mode
+        const int4 bb = f4_as_i4(s_sp[cur][2][j]);
+        const int rtx0 = bb.x / kTile, rtx1 = (bb.x + bb.y) / kTile, rty0 = bb.z / kTile;
+        const int rank = (ty0 / kTile - rty0) * (rtx1 - rtx0 + 1) + (tx0 / kTile - rtx0);
+        return a.pair_part + (size_t)(a.splat_off[src] + rank) * DW;
+      };
+      auto add4 = [](float4& v, const float* q) {
+        const float4 t = *reinterpret_cast<const float4*>(q);
+        v.x += t.x, v.y += t.y, v.z += t.z, v.w += t.w;
+      };
+      const bool vf = (a.ds & 3) == 0 && (reinterpret_cast<uintptr_t>(a.g_feat) & 15) == 0;
+      for (int e = tid; e < kBwdBatch * FC; e += kTilePixels) {
+        const int j = e / FC, c0 = 4 * (e % FC);
+        if (j < cnt && c0 < a.ds) {
+          const float* pj = s_wbase + j * PP + 4 + c0;
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
           for (int w8 = 0; w8 < 8; ++w8)
-            if (wm & (1 << w8)) v += s_wbase[w8 * 3 * kBwdBatch * WP + j * PP + c];
-          s_acc[e] = v;
-        }
-      }
-    }
-    __syncthreads();
-    // ---- per-splat closed forms + global accumulation: per splat 2 x float4 geometry
-    // (dmean, dA, dz, dg), 3 colour and ds/4 x float4 feature reductions (vector REDs)
-    {
-      constexpr int SL = 5 + DSP / 4;  // slots per splat
-      const bool vf = (a.ds & 3) == 0 && (reinterpret_cast<uintptr_t>(a.g_feat) & 15) == 0;
-      const int DW = det_width(a.ds);
-      for (int e = tid; e < cnt * SL; e += blockDim.x) {
-        const int j = e / SL, k = e % SL;
-        const float* ac = s_acc + j * NACC;
-        const float* row = raw + j * RP;
-        const size_t src = __float_as_uint(row[15]);
-        float* det = nullptr;  // this (splat, tile) pair's partial row (deterministic mode)
-        if (a.pair_part) {
-          const int4 bb = f4_as_i4(*reinterpret_cast<const float4*>(row + 8));
-          const int rtx0 = bb.x / kTile, rtx1 = bb.y / kTile, rty0 = bb.z / kTile;
-          const int rank = (ty0 / kTile - rty0) * (rtx1 - rtx0 + 1) + (tx0 / kTile - rtx0);
-          det = a.pair_part + (size_t)(a.splat_off[src] + rank) * DW;
-        }
-        if (k < 2) {
-          // moments M0..M5 of the drho rows -> dmean_u, dmean_v, dA00, dA01 | dA11, dz, dg
-          const float up = row[0] - ((float)tx0 + 7.5f), vp = row[1] - ((float)ty0 + 7.5f);
-          const float* M = ac + NU;
-          float4 v;
-          if (k == 0) {
-            const float sdx = M[1] - up * M[0], sdy = M[2] - vp * M[0];
-            v = make_float4(-2.f * (row[4] * sdx + row[5] * sdy), -2.f * (row[6] * sdx + row[7] * sdy),
-                            M[3] - 2.f * up * M[1] + up * up * M[0], M[4] - vp * M[1] - up * M[2] + up * vp * M[0]);
+            if (wm & (1 << w8)) add4(v, pj + w8 * WS);
+          const size_t src = __float_as_uint(s_sp[cur][3][j].z);
+          if (a.pair_part) {
+            reinterpret_cast<float4*>(det_row(j, src) + 12)[c0 / 4] = v;
+          } else if (vf) {
+            if (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f)
+              atomicAdd(reinterpret_cast<float4*>(a.g_feat + src * a.ds + c0), v);
           } else {
-            v = make_float4(M[5] - 2.f * vp * M[2] + vp * vp * M[0], ac[3], ac[NU + 8], 0.f);
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+            for (int c = 0; c < 4 && c0 + c < a.ds; ++c)
+              if (vv[c] != 0.f) atomicAdd(&a.g_feat[src * a.ds + c0 + c], vv[c]);
           }
-          if (det)
-            reinterpret_cast<float4*>(det)[k] = v;
-          else if (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f)
-            atomicAdd(reinterpret_cast<float4*>(a.geo_acc + src * 8) + k, v);
-        } else if (k < 5) {
-          const float val = ac[k - 2];
-          if (det)
-            det[8 + (k - 2)] = val;
-          else if (val != 0.f)
-            atomicAdd(&a.g_col[src * 3 + (k - 2)], val);
-        } else {
-          const int c0 = 4 * (k - 5);
-          if (c0 < a.ds) {
-            const float4 v = make_float4(ac[4 + c0], ac[5 + c0], ac[6 + c0], ac[7 + c0]);
-            if (det) {
-              reinterpret_cast<float4*>(det + 12)[k - 5] = v;
-            } else if (vf) {
-              if (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f)
-                atomicAdd(reinterpret_cast<float4*>(a.g_feat + src * a.ds + c0), v);
-            } else {
-              const float vv[4] = {v.x, v.y, v.z, v.w};
-              for (int c = 0; c < 4 && c0 + c < a.ds; ++c)
-                if (vv[c] != 0.f) atomicAdd(&a.g_feat[src * a.ds + c0 + c], vv[c]);
-            }
+        }
+      }
+      if (warp == 7) {
+        const int j = lane & 15, h = lane >> 4;  // lane pair (j, j + 16): warps 0-3 and 4-7
+        // [c0 c1 c2 z] | drho moments M0..M3 | M4 M5 - - | dg moment, - - -
+        float4 cz = make_float4(0.f, 0.f, 0.f, 0.f), ma = cz, mb = cz, mg = cz;
+        const float* pj = s_wbase + j * PP;
+#pragma unroll
+        for (int w4 = 0; w4 < 4; ++w4) {
+          const int w8 = 4 * h + w4;
+          if (wm & (1 << w8)) {
+            const float* q = pj + w8 * WS;
+            add4(cz, q);
+            add4(ma, q + NU);
+            add4(mb, q + NU + 4);
+            add4(mg, q + NU + 8);
+          }
+        }
+        auto xadd = [](float4& v) {
+          v.x += __shfl_xor_sync(0xffffffffu, v.x, 16);
+          v.y += __shfl_xor_sync(0xffffffffu, v.y, 16);
+          v.z += __shfl_xor_sync(0xffffffffu, v.z, 16);
+          v.w += __shfl_xor_sync(0xffffffffu, v.w, 16);
+        };
+        xadd(cz);
+        xadd(ma);
+        xadd(mb);
+        mg.x += __shfl_xor_sync(0xffffffffu, mg.x, 16);
+        if (h == 0 && j < cnt) {
+          const float4 sp0 = s_sp[cur][0][j], sp1 = s_sp[cur][1][j], sp3 = s_sp[cur][3][j];
+          const size_t src = __float_as_uint(sp3.z);
+          // moments M0..M5 of the drho rows -> dmean_u, dmean_v, dA00, dA01 | dA11, dz, dg
+          const float up = sp0.x - ((float)tx0 + 7.5f), vp = sp0.y - ((float)ty0 + 7.5f);
+          const float m0 = ma.x, m1 = ma.y, m2 = ma.z, m3 = ma.w, m4 = mb.x, m5 = mb.y;
+          const float sdx = m1 - up * m0, sdy = m2 - vp * m0;
+          const float4 g0 = make_float4(-2.f * (sp1.z * sdx + sp1.w * sdy), -2.f * (sp3.x * sdx + sp3.y * sdy),
+                                        m3 - 2.f * up * m1 + up * up * m0, m4 - vp * m1 - up * m2 + up * vp * m0);
+          const float4 g1 = make_float4(m5 - 2.f * vp * m2 + vp * vp * m0, cz.w, mg.x, 0.f);
+          if (a.pair_part) {
+            float* det = det_row(j, src);
+            reinterpret_cast<float4*>(det)[0] = g0;
+            reinterpret_cast<float4*>(det)[1] = g1;
+            det[8] = cz.x;
+            det[9] = cz.y;
+            det[10] = cz.z;
+          } else {
+            if (g0.x != 0.f || g0.y != 0.f || g0.z != 0.f || g0.w != 0.f)
+              atomicAdd(reinterpret_cast<float4*>(a.geo_acc + src * 8), g0);
+            if (g1.x != 0.f || g1.y != 0.f || g1.z != 0.f)
+              atomicAdd(reinterpret_cast<float4*>(a.geo_acc + src * 8) + 1, g1);
+            if (cz.x != 0.f) atomicAdd(&a.g_col[src * 3 + 0], cz.x);
+            if (cz.y != 0.f) atomicAdd(&a.g_col[src * 3 + 1], cz.y);
+            if (cz.z != 0.f) atomicAdd(&a.g_col[src * 3 + 2], cz.z);
           }
         }
       }
     }
+    cp_async_wait_all();  // batch it+2 (issuing lanes of warp 0), visible after the barrier
+    __syncthreads();
   }
 }
 
@@ -1532,7 +1573,9 @@ template <int DSP>
 void launch_bwd(cudaStream_t st, int ntiles, const RasterBwdArgs& a) {
   constexpr int NU = ((4 + DSP) + 7) / 8 * 8;
   constexpr int UP = NU % 16 == 8 ? NU : NU + 8;
-  const size_t smem = sizeof(float) * ((size_t)kTilePixels * UP + 8 * 3 * kBwdBatch * 36);
+  constexpr int NACC = NU + 16, PP = (NACC + 23) / 32 * 32 + 8;
+  constexpr int WP = 16 * PP <= 3 * kBwdBatch * 32 ? 32 : 36;  // as in raster_bwd_kernel
+  const size_t smem = sizeof(float) * ((size_t)kTilePixels * UP + 8 * 3 * kBwdBatch * WP);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(raster_bwd_kernel<DSP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
