@@ -1282,6 +1282,7 @@ latmap_status latmap_session_create(latmap_ctx* ctx, const latmap_config* cfg, i
            ok(cudaMalloc(&d.bm_part, sizeof(float) * 74 * k * 64)) &&
            ok(cudaMalloc(&d.loss_part, sizeof(double) * 148 * 4)) &&
            ok(cudaMalloc(&d.e_tiles, (size_t)((npx + 127) / 128) * 128 * k * 2)) &&
+           (!decoder_tc_supported(k, ds, 1) || ok(cudaMalloc(&d.tc_img, (size_t)(k * ds + k * k) * 2))) &&
            ok(cudaMalloc(&d.a_acc, sizeof(float) * k * k)) && ok(cudaMalloc(&d.r_acc, sizeof(float) * ds * k));
     if (good && decoder_dl_supported(k, ds, 1)) {
       d.dl_t = d.buf1;
@@ -1339,7 +1340,7 @@ latmap_status latmap_session_destroy(latmap_session* s) {
                   (void*)s->dec.kd, (void*)s->dec.mm, (void*)s->dec.gt, (void*)s->dec.nv, (void*)s->dec.r,
                   (void*)s->dec.a, (void*)s->dec.bm, (void*)s->dec.row_stats, (void*)s->dec.r_part,
                   (void*)s->dec.a_part, (void*)s->dec.bm_part, (void*)s->dec.loss_part,
-                  (void*)s->dec.e_tiles, (void*)s->dec.a_acc, (void*)s->dec.r_acc, (void*)s->dec.dl_mt,
+                  (void*)s->dec.e_tiles, (void*)s->dec.tc_img, (void*)s->dec.a_acc, (void*)s->dec.r_acc, (void*)s->dec.dl_mt,
                   (void*)s->dec.dl_nu, (void*)s->dec.dl_part, (void*)s->dec.row_nd, (void*)s->snap.params,
                   (void*)s->snap.m, (void*)s->snap.v, (void*)s->snap.anchor})
     if (p) cudaFree(p);

@@ -419,6 +419,7 @@ void decoder_prepare(cudaStream_t st, DecoderWork& w, const float* atoms, const 
   // Kd = D W^T (K x ds), M = D D^T (K x K)
   sgemm(st, false, true, w.k, w.ds, w.df, 1.f, atoms, w.df, proj, w.df, 0.f, w.kd, w.ds);
   sgemm(st, false, true, w.k, w.k, w.df, 1.f, atoms, w.df, atoms, w.df, 0.f, w.mm, w.k);
+  decoder_tc_images(st, w);
   if (w.a_acc) cudaMemsetAsync(w.a_acc, 0, sizeof(float) * w.k * w.k, st);
   if (w.r_acc) cudaMemsetAsync(w.r_acc, 0, sizeof(float) * w.ds * w.k, st);
   w.tc_pending = false;

@@ -54,6 +54,7 @@ struct Dec1Args {
   int want_grad;
   int accum;                // add R^T into r_part (later frames of a step) instead of storing
   float2* row_nd;           // optional parity export: per-row (nu^2, dot)
+  const uint8_t* img;       // bf16 core-matrix images of Kd then M (decoder_prepare), or null
 };
 
 template <int K, int DS>
@@ -70,7 +71,7 @@ __global__ void __launch_bounds__(512, 1) dec1_kernel(Dec1Args a) {
   uint8_t* sP = sKd + K * DS * 2;                  // 128 x K  (e, then dS)
   uint8_t* sM = sP + kRows * K * 2;                // K x K
   float* s_red = reinterpret_cast<float*>(sM + K * K * 2);  // [4 quantities][4 quarters][128]
-  __shared__ uint64_t bar[3];
+  __shared__ uint64_t bar[4];  // MMA1, MMA2, MMA3/4 completion; [3] the Kd / M image load
   __shared__ uint32_t s_taddr;
   __shared__ double s_loss[16][3];
 
@@ -80,11 +81,18 @@ __global__ void __launch_bounds__(512, 1) dec1_kernel(Dec1Args a) {
   const int c0 = qt * QC;
   auto red = [&](int q, int quarter) -> float& { return s_red[(q * 4 + quarter) * 128 + row]; };
 
-  tc::load_tile_bf16(sKd, a.kd, K, DS, K, tid, NT);
-  tc::load_tile_bf16(sM, a.mm, K, K, K, tid, NT);
+  if (!a.img) {
+    tc::load_tile_bf16(sKd, a.kd, K, DS, K, tid, NT);
+    tc::load_tile_bf16(sM, a.mm, K, K, K, tid, NT);
+  }
   if (tid == 0) {
-    for (int i = 0; i < 3; ++i) tc::mbar_init(&bar[i], 1);
+    for (int i = 0; i < 4; ++i) tc::mbar_init(&bar[i], 1);
     tc::fence_mbar_init();
+    if (a.img) {  // the step's operand images (144 KB at K = 256): two bulk copies, waited before MMA1
+      tc::mbar_expect_tx(&bar[3], (uint32_t)(K * DS * 2 + K * K * 2));
+      tc::bulk_g2s(sKd, a.img, (uint32_t)(K * DS * 2), &bar[3]);
+      tc::bulk_g2s(sM, a.img + K * DS * 2, (uint32_t)(K * K * 2), &bar[3]);
+    }
   }
   if (warp == 0) tc::tmem_alloc<kTmemCols>(&s_taddr);
   tc::fence_async_smem();
@@ -137,6 +145,7 @@ __global__ void __launch_bounds__(512, 1) dec1_kernel(Dec1Args a) {
     __syncthreads();
     // ---- MMA1: S = Q Kd^T  -> TMEM[0, K)
     if (tid == 0) {
+      if (a.img && first) tc::mbar_wait(&bar[3], 0);
       tc::tc_fence_after();
 #pragma unroll
       for (int ks = 0; ks < DS / 16; ++ks)
@@ -193,10 +202,19 @@ __global__ void __launch_bounds__(512, 1) dec1_kernel(Dec1Args a) {
                      tc::make_sdesc(aM + ks * 2 * (16 * K), 16 * K, 128), idesc1, ks > 0);
       tc::mma_commit(&bar[1]);
     }
-    // warm L1 with the target-score row slice (overlaps MMA2)
-    const int32_t asg_prev = __shfl_up_sync(0xffffffffu, asg, 1);  // all lanes take part
-    if (lane == 0 || asg != asg_prev)
-      for (int i = 0; i < QC; i += 32) asm volatile("prefetch.global.L1 [%0];" ::"l"(grow_ptr + i));
+    // dot = P.G[a] needs only e (read-only for MMA2 too) and the target-score row: computed
+    // while MMA2 runs
+    float dot = 0.f;
+#pragma unroll
+    for (int c = 0; c < QC; c += 8) {
+      float e[8];
+      tc::ld_row8(sP, row, c0 + c, kCS, e);
+      const float4 g0 = __ldg(reinterpret_cast<const float4*>(grow_ptr + c));
+      const float4 g1 = __ldg(reinterpret_cast<const float4*>(grow_ptr + c + 4));
+      const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) dot = fmaf(e[j], gv[j], dot);
+    }
     tc::mbar_wait(&bar[1], ph[1]);
     ph[1] ^= 1;
     tc::tc_fence_after();
@@ -207,19 +225,13 @@ __global__ void __launch_bounds__(512, 1) dec1_kernel(Dec1Args a) {
     tc::tmem_wait_ld();
 #pragma unroll
     for (int c = 0; c < QC; c += 32) tc::tmem_reg_fence32(tv + c);
-    float nu2 = 0.f, dot = 0.f;
+    float nu2 = 0.f;
 #pragma unroll
     for (int c = 0; c < QC; c += 8) {
       float e[8];
       tc::ld_row8(sP, row, c0 + c, kCS, e);
-      const float4 g0 = __ldg(reinterpret_cast<const float4*>(grow_ptr + c));
-      const float4 g1 = __ldg(reinterpret_cast<const float4*>(grow_ptr + c + 4));
-      const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        nu2 = fmaf(e[j], tv[c + j], nu2);
-        dot = fmaf(e[j], gv[j], dot);
-      }
+      for (int j = 0; j < 8; ++j) nu2 = fmaf(e[j], tv[c + j], nu2);
     }
     red(2, qt) = nu2;
     red(3, qt) = dot;
@@ -686,7 +698,7 @@ void launch_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_
   const int accum = want_grad && w.tc_frames > 0 ? 1 : 0;
   Dec1Args d1{w.e_tiles, query, assignment, w.kd, w.mm, w.gt, w.nv, npx, 1.f / temperature, lambda_cos, lambda_l2,
               scale, nsup, d_query, reinterpret_cast<float4*>(w.row_stats),
-              w.r_part, w.loss_part, want_grad ? 1 : 0, accum, reinterpret_cast<float2*>(w.row_nd)};
+              w.r_part, w.loss_part, want_grad ? 1 : 0, accum, reinterpret_cast<float2*>(w.row_nd), w.tc_img};
   const size_t sm1 = (size_t)kRows * DS * 2 + (size_t)K * DS * 2 + (size_t)kRows * K * 2 + (size_t)K * K * 2 +
                      16 * 128 * 4;
   static bool attr1 = false;
@@ -719,6 +731,19 @@ void launch_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_
 }
 
 }  // namespace
+
+__global__ void tc_image_kernel(uint8_t* img, const float* __restrict__ kd, const float* __restrict__ mm, int K,
+                                int DS) {
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nthr = gridDim.x * blockDim.x;
+  tc::load_tile_bf16(img, kd, K, DS, K, tid, nthr);
+  tc::load_tile_bf16(img + (size_t)K * DS * 2, mm, K, K, K, tid, nthr);
+}
+
+void decoder_tc_images(cudaStream_t st, DecoderWork& w) {
+  if (!w.tc_img) return;
+  tc_image_kernel<<<32, 256, 0, st>>>(w.tc_img, w.kd, w.mm, (int)w.k, w.ds);
+  count_launch();
+}
 
 bool decoder_tc_supported(int64_t k, int ds, int64_t n_set) {
   return (k == 128 || k == 256) && ds == 32 && n_set <= 64;

@@ -119,6 +119,7 @@ struct DecoderWork {
   float* bm_part = nullptr;    // 74 x K x 64
   double* loss_part = nullptr; // 148 x 4
   uint8_t* e_tiles = nullptr;  // ceil(npx/128) x 128 x K bf16 (DEC1 -> DEC2)
+  uint8_t* tc_img = nullptr;   // bf16 core-matrix images of Kd (K x ds) then M (K x K): DEC1's operands, per step
   float* a_acc = nullptr;      // K x K: sum over the step's frames of P^T diag(alpha) P
   float* r_acc = nullptr;      // ds x K: sum over the step's frames of Q^T dS
   bool tc_pending = false;     // a_acc / r_acc hold contributions not yet applied
@@ -137,6 +138,7 @@ struct DecoderWork {
   int64_t last_npx = 0;
 };
 void decoder_prepare(cudaStream_t st, DecoderWork& w, const float* atoms, const float* proj);
+void decoder_tc_images(cudaStream_t st, DecoderWork& w);  // Kd / M -> tc_img (fused tcgen05 path)
 // Fused feature loss + decoder backward for one frame (pixel mode). Accumulates into d_proj,
 // d_atoms (scaled by lambda_feat * inv_b) and writes d_query (HxWxds, scaled likewise).
 // nsup: device int64, the supervised-row count (inv_nsup = 1 / nsup, 0 without supervision).

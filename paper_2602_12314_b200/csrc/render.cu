@@ -718,7 +718,7 @@ __device__ __forceinline__ void mma_tf32(float* d, const uint32_t* a, const uint
 // W (32 pixels x 16 splats, from the scalar pass) multiply the splats' features F (16 x DSP),
 // Q += W F as 3xTF32 m16n8k8 MMAs (~fp32 accurate, different summation order than the scalar loop).
 template <int DSP>
-__global__ void __launch_bounds__(kTilePixels, 2) raster_fwd_mma_kernel(RasterArgs a) {
+__global__ void __launch_bounds__(kTilePixels, DSP >= 64 ? 1 : 2) raster_fwd_mma_kernel(RasterArgs a) {
   constexpr int FB = 128;           // splats per shared-memory batch
   constexpr int FP = DSP + 8;       // feature pitch: B-fragment loads hit distinct banks
   constexpr int WP = 40;            // per-warp [splat][pixel] weight pitch
@@ -729,7 +729,7 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_fwd_mma_kernel(RasterAr
   float* s_fl = s_fh + FB * FP;             // [FB][FP] tf32 lo
   float* s_w = s_fl + FB * FP;              // [8 warps][16][WP]
   float* s_raw = s_w + 8 * 16 * WP;         // [FB][RP] cp.async staging of the next batch
-  __shared__ float4 s_sp[FB][3];            // {mean_x, mean_y, a00, 2 a01} {a11, alpha, depth, -} {bbox}
+  __shared__ float4 s_sp[FB][3];            // {mean_x, mean_y, a00, 2 a01} {a11, alpha, depth, -} {x0, x1-x0, y0, y1-y0}
   __shared__ float s_col[FB * 3];
   __shared__ int32_t s_max;
   __shared__ uint64_t s_etab[32];
@@ -777,6 +777,8 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_fwd_mma_kernel(RasterAr
   int last = end - start;
   const float fx = (float)px, fy = (float)py;
   float* sw = s_w + warp * 16 * WP;
+  // this warp's pixel block: columns bx0 .. bx0 + 7, rows by0 .. by0 + 3
+  const int bx0 = tx0 + (warp & 1) * 8, by0 = ty0 + (warp >> 1) * 4;
   for (int base = start; base < end; base += FB) {
     cp_async_wait_all();
     if (__syncthreads_and(done)) break;
@@ -802,7 +804,10 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_fwd_mma_kernel(RasterAr
       const float4 r1 = *reinterpret_cast<const float4*>(row + 4);  // a00, a01, a10, a11
       s_sp[tid][0] = make_float4(r0.x, r0.y, r1.x, fm(2.f, r1.y));  // 2 a01: exact
       s_sp[tid][1] = make_float4(r1.w, r0.w, r0.z, 0.f);
-      s_sp[tid][2] = *reinterpret_cast<const float4*>(row + 8);
+      int4 bb = *reinterpret_cast<const int4*>(row + 8);
+      bb.y -= bb.x;  // extents: one unsigned compare per axis in the per-pixel test
+      bb.w -= bb.z;
+      s_sp[tid][2] = i4_as_f4(bb);
       s_col[tid * 3 + 0] = row[12];
       s_col[tid * 3 + 1] = row[13];
       s_col[tid * 3 + 2] = row[14];
@@ -816,8 +821,22 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_fwd_mma_kernel(RasterAr
     }
     for (int sb = 0; sb < cnt; sb += 16) {
       if (__all_sync(0xffffffffu, done)) break;
+      // splats of the sub-batch whose bbox meets the warp's 8x4 block (any other has no pixel of
+      // the warp in its bbox: every blend weight is 0 and the sub-batch is skipped or zero-filled)
+      bool meets = false;
+      if (lane < 16 && sb + lane < cnt) {
+        const int4 bb = f4_as_i4(s_sp[sb + lane][2]);
+        meets = bb.x <= bx0 + 7 && bb.x + bb.y >= bx0 && bb.z <= by0 + 3 && bb.z + bb.w >= by0;
+      }
+      const uint32_t wmask = __ballot_sync(0xffffffffu, meets);
+      if (wmask == 0u) continue;
 #pragma unroll
       for (int j4 = 0; j4 < 16; j4 += 4) {
+        if (((wmask >> j4) & 15u) == 0u) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) sw[(j4 + u) * WP + lane] = 0.f;
+          continue;
+        }
         // alpha' of four splats evaluated independently (ILP over the exact exp), then the
         // transmittance chain in order
         float alv[4];
@@ -827,8 +846,7 @@ __global__ void __launch_bounds__(kTilePixels, 2) raster_fwd_mma_kernel(RasterAr
         for (int u = 0; u < 4; ++u) {
           const int j = sb + j4 + u;
           const int4 bb = f4_as_i4(s_sp[j][2]);
-          ok[u] = !done && j < cnt && (unsigned)(px - bb.x) <= (unsigned)(bb.y - bb.x) &&
-                  (unsigned)(py - bb.z) <= (unsigned)(bb.w - bb.z);
+          ok[u] = !done && j < cnt && (unsigned)(px - bb.x) <= (unsigned)bb.y && (unsigned)(py - bb.z) <= (unsigned)bb.w;
           any |= ok[u];
         }
         if (__any_sync(0xffffffffu, any)) {
@@ -1142,15 +1160,16 @@ __global__ void __launch_bounds__(kTilePixels, DSP >= 64 ? 1 : 2) raster_bwd_ker
     const float* fh = s_fh[cur];
     const float* fl = s_fl[cur];
     // warp activity: some pixel of the block still blends at this batch and some bbox meets it
-    bool act = (lo - start) < warp_last;
-    if (act) {
+    uint32_t wmask = 0u;  // splats of the batch whose bbox meets the warp's block
+    if ((lo - start) < warp_last) {
       bool meets = false;
       if (lane < cnt) {
         const int4 bb = f4_as_i4(s_sp[cur][2][lane]);
         meets = bb.x <= bx0 + 7 && bb.x + bb.y >= bx0 && bb.z <= by0 + 3 && bb.z + bb.w >= by0;
       }
-      act = __any_sync(0xffffffffu, meets);
+      wmask = __ballot_sync(0xffffffffu, meets);
     }
+    const bool act = wmask != 0u;
     if (lane == 0) s_wact[warp] = act ? 1 : 0;
     if (act) {
       // ---- value[p][j] = U[p] . [c_j, z_j, f_j] for the warp's 32 pixels x 16 splats on the tensor
