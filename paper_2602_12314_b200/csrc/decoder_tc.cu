@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(512, 1) dec1_kernel(Dec1Args a) {
     tc::mbar_wait(&bar[0], ph[0]);
     ph[0] ^= 1;
     tc::tc_fence_after();
+    uint8_t* e_out = a.want_grad ? a.e_tiles + (size_t)tile * kRows * K * 2 + (size_t)(row >> 6) * 64 * K * 2 : nullptr;
     // ---- softmax: row max, then e = exp(S - max) (bf16) and the row sum
     float sv[QC];
 #pragma unroll
@@ -183,6 +184,8 @@ __global__ void __launch_bounds__(512, 1) dec1_kernel(Dec1Args a) {
       u.z = tc::pack_bf16(tc::ex2(fmaf(sv[c + 4], cl, -mxl)), tc::ex2(fmaf(sv[c + 5], cl, -mxl)));
       u.w = tc::pack_bf16(tc::ex2(fmaf(sv[c + 6], cl, -mxl)), tc::ex2(fmaf(sv[c + 7], cl, -mxl)));
       *reinterpret_cast<uint4*>(sP + tc::core_off(row, c0 + c, 128u, kCS)) = u;
+      if (e_out)  // DEC2's copy, half-major: rows 0-63 then 64-127, each a contiguous 64-row tile
+        *reinterpret_cast<uint4*>(e_out + tc::core_off(row & 63, c0 + c, 128u, 16u * 64)) = u;
       const uint32_t w4[4] = {u.x, u.y, u.z, u.w};  // sum the bf16-rounded e the MMA consumes
 #pragma unroll
       for (int j = 0; j < 4; ++j) sum += __uint_as_float(w4[j] << 16) + __uint_as_float(w4[j] & 0xffff0000u);
@@ -192,10 +195,9 @@ __global__ void __launch_bounds__(512, 1) dec1_kernel(Dec1Args a) {
     tc::tc_fence_before();
     __syncthreads();
     const float inv_sum = 1.f / ((red(1, 0) + red(1, 1)) + (red(1, 2) + red(1, 3)));
-    // ---- MMA2: t = e M -> TMEM[0, K) (S is dead); e also streams to HBM for DEC2
+    // ---- MMA2: t = e M -> TMEM[0, K) (S is dead)
     if (tid == 0) {
       tc::tc_fence_after();
-      if (a.want_grad) tc::bulk_s2g(a.e_tiles + (size_t)tile * kRows * K * 2, sP, kRows * K * 2);
 #pragma unroll 4
       for (int ks = 0; ks < K / 16; ++ks)
         tc::mma_bf16(tmem, tc::make_sdesc(aP + ks * 2 * 2048, 2048, 128),
@@ -266,9 +268,8 @@ __global__ void __launch_bounds__(512, 1) dec1_kernel(Dec1Args a) {
       __syncthreads();
       continue;
     }
-    // ---- dS = P (al t + be g - c) / tau  (bf16, overwrites e in sP once its copy-out is read)
-    if (tid == 0) tc::bulk_wait_read();
-    __syncthreads();
+    // ---- dS = P (al t + be g - c) / tau  (bf16, overwrites e in sP: every thread rewrites only
+    // the chunks it wrote and read itself, and MMA2 -- the last async reader -- has completed)
     const float ps = inv_sum * a.inv_temp;  // P = e * inv_sum
     const float al_t = al * inv_sum;        // al * t = al * inv_sum * (e M)
 #pragma unroll
@@ -375,32 +376,40 @@ struct Dec2Args {
 // DEC2: A[:, role half] = e^T diag(alpha / sum^2) e and (role 0) Bm = e^T Ohb with
 // Ohb[r][s] = beta_r / sum_r [a_r == s], streaming the e tiles DEC1 exported -- no
 // recomputation of S or exp. Warp-specialised: warp 8 (one elected lane) issues the TMA bulk
-// loads of the e tiles and the MMAs; warps 0-7 build the scaled B operands. The e tiles and the
-// B operands are double-buffered, so the build of tile i overlaps the MMAs of tile i-1, and the
-// load of tile i+1 overlaps both.
-//   bar_ld[b]    : e tile landed in sE[b]            (TMA complete_tx)
-//   bar_built[b] : 8 builder warps filled sAP/sOh[b]  (8 arrivals)
-//   bar_mma[b]   : MMAs reading sE/sAP/sOh[b] done    (tcgen05.commit)
-// A load into sE[b] is issued only after the MMAs of the tile that last used b completed, so a
-// builder that sees bar_ld[b] may also overwrite sAP/sOh[b].
+// loads and the MMAs; warps 0-7 build the scaled B operands. The unit of the pipeline is a
+// half tile (64 pixel rows, one contiguous bulk copy: DEC1 exports each tile half-major, every
+// half in the 64-row core-matrix layout) in a ring of kStages stages, so three loads are in
+// flight while a fourth stage is built and multiplied.
+//   bar_ld[s]    : half tile landed in sE[s]            (TMA complete_tx)
+//   bar_built[s] : 8 builder warps filled sAP/sOh[s]     (8 arrivals)
+//   bar_mma[s]   : MMAs reading sE/sAP/sOh[s] done       (tcgen05.commit)
+// The load of half tile i into stage s is issued only after the MMAs of half tile i - kStages
+// (the last user of s) completed, so a builder that sees bar_ld[s] may also overwrite sAP/sOh[s].
+constexpr int kHalf = kRows / 2;  // pixel rows per pipeline unit
+constexpr int kStages = 4;
+template <int K>
+constexpr size_t dec2_smem() {
+  return (size_t)kStages * ((size_t)kHalf * K * 2 + (size_t)kHalf * (K / 2) * 2 + (size_t)kHalf * 64 * 2);
+}
+
 template <int K>
 __global__ void __launch_bounds__(288, 1) dec2_kernel(Dec2Args a) {
   constexpr int MH = K / 128, NH = K / 2, NB = 64;
   constexpr int kColA = 0, kColB = MH * NH;
   constexpr int kTmemCols = kColB + MH * NB <= 256 ? 256 : 512;
-  constexpr uint32_t kCS = 16u * kRows;
+  constexpr uint32_t kCH = 16u * kHalf;  // column-group stride of the 64-row half tiles
   constexpr uint32_t kTileBytes = kRows * K * 2;
-  constexpr uint32_t kAPBytes = kRows * NH * 2, kOhBytes = kRows * NB * 2;
+  constexpr uint32_t kEB = kHalf * K * 2, kAPB = kHalf * NH * 2, kOhB = kHalf * NB * 2;
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sE0 = smem;                       // 2 x (128 x K)
-  uint8_t* sAP0 = smem + 2 * kTileBytes;     // 2 x (128 x NH)
-  uint8_t* sOh0 = sAP0 + 2 * kAPBytes;       // 2 x (128 x NB)
-  __shared__ uint64_t bar_ld[2], bar_built[2], bar_mma[2];
+  uint8_t* sE0 = smem;                     // kStages x (64 x K)
+  uint8_t* sAP0 = smem + kStages * kEB;    // kStages x (64 x NH)
+  uint8_t* sOh0 = sAP0 + kStages * kAPB;   // kStages x (64 x NB)
+  __shared__ uint64_t bar_ld[kStages], bar_built[kStages], bar_mma[kStages];
   __shared__ uint32_t s_taddr;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int role = blockIdx.x & 1, group = blockIdx.x >> 1, ngroups = gridDim.x >> 1;
   if (tid == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kStages; ++i) {
       tc::mbar_init(&bar_ld[i], 1);
       tc::mbar_init(&bar_built[i], 8);
       tc::mbar_init(&bar_mma[i], 1);
@@ -414,98 +423,108 @@ __global__ void __launch_bounds__(288, 1) dec2_kernel(Dec2Args a) {
   const uint32_t tmem = s_taddr;
   const int64_t ntiles = (a.npx + kRows - 1) / kRows;
   const int nmine = group < ntiles ? (int)((ntiles - 1 - group) / ngroups + 1) : 0;
+  const int nh = 2 * nmine;  // half tiles of this CTA
   if (warp == 8) {
     // ---------------- producer: TMA loads + MMA issue (one lane)
-    if (lane == 0 && nmine > 0) {
+    if (lane == 0 && nh > 0) {
       const uint32_t aAP0 = tc::smem_u32(sAP0), aOh0 = tc::smem_u32(sOh0), aE0 = tc::smem_u32(sE0);
-      for (int i = 0; i < 2 && i < nmine; ++i) {
-        tc::mbar_expect_tx(&bar_ld[i], kTileBytes);
-        tc::bulk_g2s(sE0 + i * kTileBytes, a.e_tiles + (size_t)(group + (int64_t)i * ngroups) * kTileBytes,
-                     kTileBytes, &bar_ld[i]);
-      }
-      for (int it = 0; it < nmine; ++it) {
-        const int buf = it & 1;
-        tc::mbar_wait(&bar_built[buf], (it >> 1) & 1);
+      auto load = [&](int i) {  // DEC1 wrote each tile half-major: one contiguous copy per half tile
+        const int s = i % kStages;
+        const uint8_t* src = a.e_tiles + (size_t)(group + (int64_t)(i >> 1) * ngroups) * kTileBytes + (i & 1) * kEB;
+        tc::mbar_expect_tx(&bar_ld[s], kEB);
+        tc::bulk_g2s(sE0 + s * kEB, src, kEB, &bar_ld[s]);
+      };
+      for (int i = 0; i < kStages - 1 && i < nh; ++i) load(i);
+      for (int it = 0; it < nh; ++it) {
+        const int s = it % kStages;
+        tc::mbar_wait(&bar_built[s], (it / kStages) & 1);
         tc::tc_fence_after();
-        const uint32_t aE = aE0 + buf * kTileBytes, aAP = aAP0 + buf * kAPBytes, aOh = aOh0 + buf * kOhBytes;
+        const uint32_t aE = aE0 + s * kEB, aAP = aAP0 + s * kAPB, aOh = aOh0 + s * kOhB;
         for (int mh = 0; mh < MH; ++mh) {
 #pragma unroll
-          for (int ks = 0; ks < kRows / 16; ++ks)
-            tc::mma_bf16(tmem + kColA + mh * NH, tc::make_sdesc(aE + mh * 16 * 2048 + ks * 2 * 128, 128, 2048),
-                         tc::make_sdesc(aAP + ks * 2 * 128, 128, 2048), tc::make_idesc_bf16(128, NH, 1, 1),
+          for (int ks = 0; ks < kHalf / 16; ++ks)
+            tc::mma_bf16(tmem + kColA + mh * NH, tc::make_sdesc(aE + mh * 16 * kCH + ks * 2 * 128, 128, kCH),
+                         tc::make_sdesc(aAP + ks * 2 * 128, 128, kCH), tc::make_idesc_bf16(128, NH, 1, 1),
                          it > 0 || ks > 0);
           if (role == 0) {
 #pragma unroll
-            for (int ks = 0; ks < kRows / 16; ++ks)
-              tc::mma_bf16(tmem + kColB + mh * NB, tc::make_sdesc(aE + mh * 16 * 2048 + ks * 2 * 128, 128, 2048),
-                           tc::make_sdesc(aOh + ks * 2 * 128, 128, 2048), tc::make_idesc_bf16(128, NB, 1, 1),
+            for (int ks = 0; ks < kHalf / 16; ++ks)
+              tc::mma_bf16(tmem + kColB + mh * NB, tc::make_sdesc(aE + mh * 16 * kCH + ks * 2 * 128, 128, kCH),
+                           tc::make_sdesc(aOh + ks * 2 * 128, 128, kCH), tc::make_idesc_bf16(128, NB, 1, 1),
                            it > 0 || ks > 0);
           }
         }
-        tc::mma_commit(&bar_mma[buf]);
-        // refill the other buffer with tile it+1 once the MMAs of tile it-1 (its last user) are done
-        if (it >= 1 && it + 1 < nmine) {
-          tc::mbar_wait(&bar_mma[buf ^ 1], ((it - 1) >> 1) & 1);
-          tc::mbar_expect_tx(&bar_ld[buf ^ 1], kTileBytes);
-          tc::bulk_g2s(sE0 + (buf ^ 1) * kTileBytes,
-                       a.e_tiles + (size_t)(group + (int64_t)(it + 1) * ngroups) * kTileBytes, kTileBytes,
-                       &bar_ld[buf ^ 1]);
+        tc::mma_commit(&bar_mma[s]);
+        // refill: half tile it + kStages - 1 into the stage half tile it - 1 used
+        const int nx = it + kStages - 1;
+        if (nx < nh) {
+          if (it >= 1) tc::mbar_wait(&bar_mma[(it - 1) % kStages], ((it - 1) / kStages) & 1);
+          load(nx);
         }
       }
     }
   } else {
-    // ---------------- builders: B operands (alpha / sum^2) e[:, role half] and the beta / sum one-hot
-    const int g = warp & 3, h = warp >> 2;  // TMEM lane group, column half (of the role's NH)
-    const int row = 32 * g + lane;
-    for (int it = 0; it < nmine; ++it) {
-      const int buf = it & 1;
-      const int64_t tile = group + (int64_t)it * ngroups;
-      const int64_t r0 = tile * kRows;
-      const int valid = (int)(a.npx - r0 < kRows ? a.npx - r0 : kRows);
-      float4 st = make_float4(0.f, 0.f, 0.f, 0.f);
-      int32_t asg = -1;
-      if (row < valid) {
-        st = a.row_stats[r0 + row];
-        asg = a.assign[r0 + row];
+    // ---------------- builders: B operands (alpha / sum^2) e[:, role half] and the beta / sum one-hot.
+    // Thread = (row of the half tile, quarter of the columns); the row statistics of half tile
+    // it + 1 are fetched while half tile it is built.
+    const int row = tid & (kHalf - 1), q = tid / kHalf;
+    auto fetch = [&](int i, float4& st, int32_t& asg) {  // asg = -2 marks a row past npx
+      const int64_t r = (group + (int64_t)(i >> 1) * ngroups) * kRows + (i & 1) * kHalf + row;
+      st = make_float4(0.f, 0.f, 0.f, 0.f);
+      asg = -2;
+      if (r < a.npx) {
+        st = a.row_stats[r];
+        asg = a.assign[r];
       }
-      const float wa = st.z * st.y * st.y;  // alpha / sum^2
+    };
+    float4 st_n;
+    int32_t asg_n;
+    if (nh > 0) fetch(0, st_n, asg_n);
+    for (int it = 0; it < nh; ++it) {
+      const int s = it % kStages;
+      const float4 st = st_n;
+      const int32_t asg = asg_n;
+      if (it + 1 < nh) fetch(it + 1, st_n, asg_n);
+      const float wa = st.z * st.y * st.y;  // alpha / sum^2 (0 for rows past npx)
       const float wb = st.w * st.y;         // beta / sum
-      tc::mbar_wait(&bar_ld[buf], (it >> 1) & 1);
-      const uint8_t* E = sE0 + buf * kTileBytes;
-      uint8_t* AP = sAP0 + buf * kAPBytes;
+      tc::mbar_wait(&bar_ld[s], (it / kStages) & 1);
+      const uint8_t* E = sE0 + s * kEB;
+      uint8_t* AP = sAP0 + s * kAPB;
 #pragma unroll
-      for (int c = h * (NH / 2); c < (h + 1) * (NH / 2); c += 8) {
+      for (int c = q * (NH / 4); c < (q + 1) * (NH / 4); c += 8) {
         float v[8];
-        tc::ld_row8(E, row, role * NH + c, kCS, v);
+        tc::ld_row8(E, row, role * NH + c, kCH, v);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = row < valid ? v[j] * wa : 0.f;
-        tc::st_row8(AP, row, c, kCS, v);
+        for (int j = 0; j < 8; ++j) v[j] = asg != -2 ? v[j] * wa : 0.f;
+        tc::st_row8(AP, row, c, kCH, v);
       }
       if (role == 0) {
-        uint8_t* Oh = sOh0 + buf * kOhBytes;
+        uint8_t* Oh = sOh0 + s * kOhB;
 #pragma unroll
-        for (int c = h * (NB / 2); c < (h + 1) * (NB / 2); c += 8) {
+        for (int c = q * (NB / 4); c < (q + 1) * (NB / 4); c += 8) {
           float v[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) v[j] = (asg == c + j) ? wb : 0.f;
-          tc::st_row8(Oh, row, c, kCS, v);
+          tc::st_row8(Oh, row, c, kCH, v);
         }
       }
       tc::fence_async_smem();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&bar_built[buf]);
+      if (lane == 0) tc::mbar_arrive(&bar_built[s]);
     }
-    // all MMAs complete once the last tile's commit arrives
-    if (nmine > 0) {
-      tc::mbar_wait(&bar_mma[(nmine - 1) & 1], ((nmine - 1) >> 1) & 1);
+    // all MMAs complete once the last half tile's commit arrives
+    if (nh > 0) {
+      tc::mbar_wait(&bar_mma[(nh - 1) % kStages], ((nh - 1) / kStages) & 1);
       tc::tc_fence_after();
     }
-    // drain: lane `row` of half mh holds A[mh*128 + row][role*NH + c], Bm[mh*128 + row][c]
+    // drain: lane `row` of TMEM lane group g, column half h of the role's NH
+    const int g = warp & 3, h = warp >> 2;
+    const int trow = 32 * g + lane;
     for (int mh = 0; mh < MH; ++mh) {
-      float* dst = a.a_part + (((size_t)group * 2 + role) * K + mh * 128 + row) * NH;
+      float* dst = a.a_part + (((size_t)group * 2 + role) * K + mh * 128 + trow) * NH;
       for (int c = h * (NH / 2); c < (h + 1) * (NH / 2); c += 16) {
         float v[16];
-        if (nmine == 0) {
+        if (nh == 0) {
           for (int i = 0; i < 16; ++i) v[i] = 0.f;
         } else {
           tc::tmem_ld16(tmem + ((uint32_t)(32 * g) << 16) + kColA + mh * NH + c, v);
@@ -521,10 +540,10 @@ __global__ void __launch_bounds__(288, 1) dec2_kernel(Dec2Args a) {
         }
       }
       if (role == 0) {
-        float* db = a.bm_part + ((size_t)group * K + mh * 128 + row) * NB;
+        float* db = a.bm_part + ((size_t)group * K + mh * 128 + trow) * NB;
         for (int c = h * (NB / 2); c < (h + 1) * (NB / 2); c += 16) {
           float v[16];
-          if (nmine == 0) {
+          if (nh == 0) {
             for (int i = 0; i < 16; ++i) v[i] = 0.f;
           } else {
             tc::tmem_ld16(tmem + ((uint32_t)(32 * g) << 16) + kColB + mh * NB + c, v);
@@ -715,7 +734,7 @@ void launch_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_
     return;
   }
   Dec2Args d2{w.e_tiles, assignment, reinterpret_cast<const float4*>(w.row_stats), npx, w.a_part, w.bm_part, accum};
-  const size_t sm2 = 2 * ((size_t)kRows * K * 2 + (size_t)kRows * (K / 2) * 2 + (size_t)kRows * 64 * 2);
+  const size_t sm2 = dec2_smem<K>();
   static bool attr2 = false;
   if (!attr2) {
     cudaFuncSetAttribute(dec2_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
@@ -809,7 +828,7 @@ void decoder_finish_tc(cudaStream_t st, DecoderWork& w, const float* atoms, cons
 // Parity export: P[r][c] = e[r][c] * (1/sum_r), e read from the bf16 core-matrix tiles the
 // kernels wrote for the last frame (DEC1 with gradients, DL1 always), 1/sum from row_stats.y.
 __global__ void export_attention_kernel(const uint8_t* __restrict__ e_tiles, const float4* __restrict__ rs,
-                                        int64_t npx, int K, float* __restrict__ p) {
+                                        int64_t npx, int K, int half_major, float* __restrict__ p) {
   const int64_t chunks = npx * (K / 8);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < chunks; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / (K / 8);
@@ -817,7 +836,11 @@ __global__ void export_attention_kernel(const uint8_t* __restrict__ e_tiles, con
     const int64_t tile = r / kRows;
     const int rr = (int)(r % kRows);
     float v[8];
-    tc::ld_row8(e_tiles + (size_t)tile * kRows * K * 2, rr, c0, 16u * kRows, v);
+    if (half_major)  // DEC1's export: two 64-row halves, each contiguous
+      tc::ld_row8(e_tiles + (size_t)tile * kRows * K * 2 + (size_t)(rr / kHalf) * kHalf * K * 2, rr % kHalf, c0,
+                  16u * kHalf, v);
+    else
+      tc::ld_row8(e_tiles + (size_t)tile * kRows * K * 2, rr, c0, 16u * kRows, v);
     const float inv = rs[r].y;
     float4* dst = reinterpret_cast<float4*>(p + r * K + c0);
     dst[0] = make_float4(v[0] * inv, v[1] * inv, v[2] * inv, v[3] * inv);
@@ -828,7 +851,7 @@ __global__ void export_attention_kernel(const uint8_t* __restrict__ e_tiles, con
 void decoder_export_attention(cudaStream_t st, const DecoderWork& w, int64_t npx, float* p_out) {
   const int64_t chunks = npx * (w.k / 8);
   export_attention_kernel<<<(unsigned)std::min<int64_t>((chunks + 255) / 256, 148 * 16), 256, 0, st>>>(
-      w.e_tiles, reinterpret_cast<const float4*>(w.row_stats), npx, (int)w.k, p_out);
+      w.e_tiles, reinterpret_cast<const float4*>(w.row_stats), npx, (int)w.k, w.last_path == 2 ? 1 : 0, p_out);
   count_launch();
 }
 
