@@ -406,11 +406,18 @@ __device__ void tile_radix_sort(uint64_t* __restrict__ g, int n, uint64_t* s_a, 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ept = (n + kSortThreads - 1) / kSortThreads;
   for (int i = tid; i < n; i += kSortThreads) s_a[i] = g[i];
+  __syncthreads();
   const uint32_t lt = (1u << lane) - 1u;
   uint32_t* s_w = s_h;  // [16 warps][257] (padded: conflict-free column walks)
 #pragma unroll 1
   for (int pass = 0; pass < 4; ++pass) {
     const int shift = 32 + 8 * pass;
+    {  // a digit shared by every key (the exponent byte, typically) leaves the order unchanged
+      const uint32_t d0 = (uint32_t)(s_a[0] >> shift) & 255u;
+      bool differs = false;
+      for (int i = tid; i < n; i += kSortThreads) differs |= ((uint32_t)(s_a[i] >> shift) & 255u) != d0;
+      if (!__syncthreads_or(differs)) continue;
+    }
     for (int i = tid; i < 257 * 16; i += kSortThreads) s_w[i] = 0u;
     __syncthreads();
     uint64_t k[8];
@@ -422,7 +429,13 @@ __device__ void tile_radix_sort(uint64_t* __restrict__ g, int n, uint64_t* s_a, 
       const int i = (warp * ept + r) * 32 + lane;
       k[r] = i < n ? s_a[i] : 0ull;
       d[r] = i < n ? (int)((k[r] >> shift) & 255u) : 256;
-      const uint32_t peers = __match_any_sync(0xffffffffu, d[r]);
+      uint32_t peers = 0xffffffffu;  // lanes with the same 9-bit digit (ballots: cheaper than match.any)
+#pragma unroll
+      for (int b = 0; b < 9; ++b) {
+        const bool bit = (d[r] >> b) & 1;
+        const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+        peers &= bit ? bal : ~bal;
+      }
       const bool ok = d[r] < 256;
       loc[r] = __popc(peers & lt) + (ok ? s_w[warp * 257 + (ok ? d[r] : 0)] : 0u);
       __syncwarp();
@@ -1644,7 +1657,7 @@ void render_forward(cudaStream_t st, const MapPtrs& map, const float rot_cw[9], 
     cudaMemsetAsync(query, 0, sizeof(float) * npx * map.ds, st);
     cudaMemsetAsync(alpha, 0, sizeof(float) * npx, st);
   }
-  const int grid1 = 148 * 2;
+  const int grid1 = 148 * 4;  // 64 registers: 4 CTAs of 256 per SM
   const size_t hist_smem = ntiles <= kHistMax ? sizeof(int32_t) * ntiles : 0;
   if (map.n > 0) {
     project_kernel<<<grid1, 256, hist_smem, st>>>(map, cam, w.rec, w.dkey, w.tile_count, w.counters);
