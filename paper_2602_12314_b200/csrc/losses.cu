@@ -83,6 +83,73 @@ __global__ void __launch_bounds__(256) l1_depth_kernel(const float* __restrict__
   block_add_double(dcount, &partials[3]);
 }
 
+// Pass 1, four pixels per thread (16-byte loads and stores; npx % 4 == 0, aligned buffers). With
+// fold_color the objective weight is applied here with the same two roundings finalize applies
+// (objective.cpp:164-165), so d_color is final and finalize only touches d_depth.
+__global__ void __launch_bounds__(256) l1_depth4_kernel(const float4* __restrict__ color, const float4* __restrict__ depth,
+                                                        const float4* __restrict__ alpha, const float4* __restrict__ rgb_t,
+                                                        const float4* __restrict__ depth_t, int64_t n4, float lambda_i1,
+                                                        float n_rgb, bool want_grad, bool fold_color, float rgb_scale,
+                                                        float4* d_color, float4* d_depth, double* partials) {
+  double l1 = 0.0, dsum = 0.0, dcount = 0.0;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n4; p += (int64_t)gridDim.x * blockDim.x) {
+    const float4 c0 = color[3 * p], c1 = color[3 * p + 1], c2 = color[3 * p + 2];
+    const float4 t0 = rgb_t[3 * p], t1 = rgb_t[3 * p + 1], t2 = rgb_t[3 * p + 2];
+    const float4 dp = depth[p], al = alpha[p], dt = depth_t[p];
+    const float cv[12] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w, c2.x, c2.y, c2.z, c2.w};
+    const float tv[12] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w, t2.x, t2.y, t2.z, t2.w};
+    float g[12];
+#pragma unroll
+    for (int i = 0; i < 12; ++i) {
+      const float d = fs(cv[i], tv[i]);
+      l1 += (double)fabsf(d);
+      const float sg = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
+      g[i] = fd(fm(lambda_i1, sg), n_rgb);
+      if (fold_color) g[i] = fm(g[i], rgb_scale);
+    }
+    const float dv[4] = {dp.x, dp.y, dp.z, dp.w}, av[4] = {al.x, al.y, al.z, al.w}, ov[4] = {dt.x, dt.y, dt.z, dt.w};
+    float gd[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float o = ov[j];
+      const bool valid = o > 0.f && av[j] > 0.5f;
+      float sg = 0.f;
+      if (valid) {
+        const float d = fs(dv[j], o);
+        dsum += (double)fabsf(d);
+        dcount += 1.0;
+        sg = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
+      }
+      gd[j] = sg;
+    }
+    if (want_grad) {
+      d_color[3 * p] = make_float4(g[0], g[1], g[2], g[3]);
+      d_color[3 * p + 1] = make_float4(g[4], g[5], g[6], g[7]);
+      d_color[3 * p + 2] = make_float4(g[8], g[9], g[10], g[11]);
+      d_depth[p] = make_float4(gd[0], gd[1], gd[2], gd[3]);
+    }
+  }
+  block_add_double(l1, &partials[0]);
+  block_add_double(dsum, &partials[2]);
+  block_add_double(dcount, &partials[3]);
+}
+
+// d_depth only (d_color already final): four pixels per thread.
+__global__ void finalize_depth4_kernel(float4* d_depth, int64_t n4, float depth_scale, const double* partials) {
+  const double valid = partials[3];
+  const float fv = (float)valid;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n4; p += (int64_t)gridDim.x * blockDim.x) {
+    float4 v = d_depth[p];
+    if (valid > 0.0) {
+      v.x = fm(fd(v.x, fv), depth_scale), v.y = fm(fd(v.y, fv), depth_scale);
+      v.z = fm(fd(v.z, fv), depth_scale), v.w = fm(fd(v.w, fv), depth_scale);
+    } else {
+      v = make_float4(0.f, 0.f, 0.f, 0.f);  // depth flagged: no gradient (objective.cpp:165-169)
+    }
+    d_depth[p] = v;
+  }
+}
+
 // Fold the objective weights into the upstream images (objective.cpp:164-170).
 __global__ void finalize_upstream_kernel(float* d_color, float* d_depth, int64_t npx, float rgb_scale,
                                          float depth_scale, const double* partials) {
@@ -162,63 +229,69 @@ __global__ void __launch_bounds__(256) ssim_v_kernel(const float* __restrict__ h
 
 // SSIM value only (no gradient requested): both separable passes fused per 32x8 output tile
 // with a 5-pixel reflect-101 halo in shared memory, the same per-pixel float expressions as
-// ssim_h_kernel + ssim_v_kernel (so the same values), one pass over the two images.
+// ssim_h_kernel + ssim_v_kernel (so the same values), one pass over the two images. The halos
+// of all channels (ch <= 3) are loaded together: one reflected index per halo pixel.
 constexpr int kSTX = 32, kSTY = 8, kSHX = kSTX + 2 * kRad, kSHY = kSTY + 2 * kRad;
 __global__ void __launch_bounds__(256) ssim_fused_kernel(const float* __restrict__ a, const float* __restrict__ b,
                                                          int h, int w, int ch, SsimKernel K, double* sum_out) {
-  __shared__ float s_a[kSHY][kSHX], s_b[kSHY][kSHX];
+  __shared__ float s_a[3][kSHY][kSHX], s_b[3][kSHY][kSHX];
   __shared__ float s_h[5][kSHY][kSTX];
   const float c1 = 0.01f * 0.01f, c2 = 0.03f * 0.03f;
   const int x0 = blockIdx.x * kSTX, y0 = blockIdx.y * kSTY;
   const int tid = threadIdx.x;
   double acc = 0.0;
-  for (int c = 0; c < ch; ++c) {
+  for (int cb = 0; cb < ch; cb += 3) {
+    const int nc = min(3, ch - cb);
     for (int i = tid; i < kSHY * kSHX; i += blockDim.x) {
       const int yy = i / kSHX, xx = i % kSHX;
       const int gy = refl(min(y0 - kRad + yy, h - 1 + kRad), h), gx = refl(min(x0 - kRad + xx, w - 1 + kRad), w);
-      const int64_t q = ((int64_t)gy * w + gx) * ch + c;
-      s_a[yy][xx] = a[q];
-      s_b[yy][xx] = b[q];
-    }
-    __syncthreads();
-    for (int i = tid; i < kSHY * kSTX; i += blockDim.x) {
-      const int yy = i / kSTX, xx = i % kSTX;
-      float s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0;
-#pragma unroll
-      for (int k = -kRad; k <= kRad; ++k) {
-        const float av = s_a[yy][xx + kRad + k], bv = s_b[yy][xx + kRad + k], kw = K.k[k + kRad];
-        s0 += kw * av;
-        s1 += kw * bv;
-        s2 += kw * (av * av);
-        s3 += kw * (bv * bv);
-        s4 += kw * (av * bv);
+      const int64_t q = ((int64_t)gy * w + gx) * ch + cb;
+      for (int c = 0; c < nc; ++c) {
+        s_a[c][yy][xx] = a[q + c];
+        s_b[c][yy][xx] = b[q + c];
       }
-      s_h[0][yy][xx] = s0;
-      s_h[1][yy][xx] = s1;
-      s_h[2][yy][xx] = s2;
-      s_h[3][yy][xx] = s3;
-      s_h[4][yy][xx] = s4;
     }
     __syncthreads();
-    {
-      const int yy = tid / kSTX, xx = tid % kSTX;
-      const int y = y0 + yy, x = x0 + xx;
-      if (y < h && x < w) {
-        float q[5] = {0, 0, 0, 0, 0};
+    for (int c = 0; c < nc; ++c) {
+      for (int i = tid; i < kSHY * kSTX; i += blockDim.x) {
+        const int yy = i / kSTX, xx = i % kSTX;
+        float s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0;
 #pragma unroll
         for (int k = -kRad; k <= kRad; ++k) {
-          const float kw = K.k[k + kRad];
-#pragma unroll
-          for (int t = 0; t < 5; ++t) q[t] += kw * s_h[t][yy + kRad + k][xx];
+          const float av = s_a[c][yy][xx + kRad + k], bv = s_b[c][yy][xx + kRad + k], kw = K.k[k + kRad];
+          s0 += kw * av;
+          s1 += kw * bv;
+          s2 += kw * (av * av);
+          s3 += kw * (bv * bv);
+          s4 += kw * (av * bv);
         }
-        const float mx = q[0], my = q[1];
-        const float sx2 = q[2] - mx * mx, sy2 = q[3] - my * my, sxy = q[4] - mx * my;
-        const float a1 = 2.f * mx * my + c1, a2 = 2.f * sxy + c2;
-        const float b1 = mx * mx + my * my + c1, b2 = sx2 + sy2 + c2;
-        acc += (double)((a1 * a2) / (b1 * b2));
+        s_h[0][yy][xx] = s0;
+        s_h[1][yy][xx] = s1;
+        s_h[2][yy][xx] = s2;
+        s_h[3][yy][xx] = s3;
+        s_h[4][yy][xx] = s4;
       }
+      __syncthreads();
+      {
+        const int yy = tid / kSTX, xx = tid % kSTX;
+        const int y = y0 + yy, x = x0 + xx;
+        if (y < h && x < w) {
+          float q[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+          for (int k = -kRad; k <= kRad; ++k) {
+            const float kw = K.k[k + kRad];
+#pragma unroll
+            for (int t = 0; t < 5; ++t) q[t] += kw * s_h[t][yy + kRad + k][xx];
+          }
+          const float mx = q[0], my = q[1];
+          const float sx2 = q[2] - mx * mx, sy2 = q[3] - my * my, sxy = q[4] - mx * my;
+          const float a1 = 2.f * mx * my + c1, a2 = 2.f * sxy + c2;
+          const float b1 = mx * mx + my * my + c1, b2 = sx2 + sy2 + c2;
+          acc += (double)((a1 * a2) / (b1 * b2));
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
   block_add_double(acc, sum_out);
 }
@@ -385,15 +458,34 @@ void image_losses(cudaStream_t st, const float* color, const float* depth, const
                   float* ssim_scratch) {
   const int64_t npx = (int64_t)h * w;
   const int grid = (int)std::min<int64_t>((npx + 255) / 256, 148 * 8);
-  l1_depth_kernel<<<grid, 256, 0, st>>>(color, depth, alpha, rgb_t, depth_t, npx, lambda_i1, (float)(npx * 3),
-                                        want_grad, d_color, d_depth, partials);
-  count_launch();
   // SSIM forward always runs (losses.cpp:217); its gradient only matters when lambda_i2 != 0.
   const bool ssim_grad = want_grad && lambda_i2 != 0.f;
+  auto al16 = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  const bool vec = npx % 4 == 0 && al16(color) && al16(depth) && al16(alpha) && al16(rgb_t) && al16(depth_t) &&
+                   al16(d_color) && al16(d_depth) && (!want_grad || (d_color && d_depth));
+  if (vec) {
+    const int64_t n4 = npx / 4;
+    const int g4 = (int)std::min<int64_t>((n4 + 255) / 256, 148 * 8);
+    l1_depth4_kernel<<<g4, 256, 0, st>>>(reinterpret_cast<const float4*>(color), reinterpret_cast<const float4*>(depth),
+                                         reinterpret_cast<const float4*>(alpha), reinterpret_cast<const float4*>(rgb_t),
+                                         reinterpret_cast<const float4*>(depth_t), n4, lambda_i1, (float)(npx * 3),
+                                         want_grad, !ssim_grad, rgb_scale, reinterpret_cast<float4*>(d_color),
+                                         reinterpret_cast<float4*>(d_depth), partials);
+  } else {
+    l1_depth_kernel<<<grid, 256, 0, st>>>(color, depth, alpha, rgb_t, depth_t, npx, lambda_i1, (float)(npx * 3),
+                                          want_grad, d_color, d_depth, partials);
+  }
+  count_launch();
   ssim_run(st, color, rgb_t, h, w, 3, ssim_grad ? d_color : nullptr, lambda_i2 * -0.5f, true, ssim_scratch,
            &partials[1]);
   if (want_grad) {
-    finalize_upstream_kernel<<<grid, 256, 0, st>>>(d_color, d_depth, npx, rgb_scale, depth_scale, partials);
+    if (vec && !ssim_grad) {
+      const int64_t n4 = npx / 4;
+      finalize_depth4_kernel<<<(int)std::min<int64_t>((n4 + 255) / 256, 148 * 8), 256, 0, st>>>(
+          reinterpret_cast<float4*>(d_depth), n4, depth_scale, partials);
+    } else {
+      finalize_upstream_kernel<<<grid, 256, 0, st>>>(d_color, d_depth, npx, rgb_scale, depth_scale, partials);
+    }
     count_launch();
   }
 }
