@@ -1451,7 +1451,7 @@ struct ProjBwdArgs {
 };
 
 // K9: projection backward (render.cpp:368-429), one thread per listed Gaussian.
-__global__ void __launch_bounds__(256) project_bwd_kernel(ProjBwdArgs a) {
+__global__ void __launch_bounds__(256, 4) project_bwd_kernel(ProjBwdArgs a) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= a.map.n) return;
   const float4* rv = reinterpret_cast<const float4*>(a.rec + i);
