@@ -115,6 +115,9 @@ latmap_status latmap_ctx_set_exact_blend(latmap_ctx* ctx, int32_t exact);
  * Replaces no reference interface (the reference has one fp32 CPU decoder,
  * proj/src/dictionary.cpp:25-83); results agree within the bf16 tolerances either way. */
 latmap_status latmap_ctx_set_decoder_path(latmap_ctx* ctx, int32_t path);
+/* Standalone reconstruct precision (latmap_reconstruct, latmap_query_map): 0 fp32 (default),
+ * 1 bf16 tcgen05 where the shape is supported. */
+latmap_status latmap_ctx_set_reconstruct_precision(latmap_ctx* ctx, int32_t precision);
 /* Deterministic mode: every gradient reduction in a fixed order instead of float atomics, so
  * gradients are bit-identical run to run (the reference's guarantee, render.cpp:272-273,358,
  * test_render.cpp:142-151). The render backward writes one partial row per (splat, tile) pair and
@@ -172,7 +175,11 @@ latmap_status latmap_render_cache_tiles(latmap_ctx* ctx, const latmap_render_cac
 
 /* ---------------------------------------------------------------- decoder (device pointers) */
 /* reconstruct, dict/dictionary.hpp:63-65: out = softmax(Q W D^T / temperature) D.
- * attention (n x K) optional (AttentionCache::attention). */
+ * attention (n x K) optional (AttentionCache::attention). With the context's reconstruct
+ * precision set to 1, no attention requested, K in {256, 512, 768, 1024}, query_dim in {32, 64}
+ * and embed_dim a multiple of 256, the product runs on the tensor cores (bf16 operands, fp32
+ * accumulation: the precision of the configs' bf16 decoder); otherwise in fp32. query_map and
+ * evaluation go through this entry point. */
 latmap_status latmap_reconstruct(latmap_ctx* ctx, const float* queries, int64_t n, int32_t query_dim,
                                  const float* atoms, const float* proj, int64_t k, int32_t embed_dim,
                                  float temperature, float* out, float* attention);

@@ -118,6 +118,7 @@ def _declare(L):
         "latmap_ctx_synchronize": [P],
         "latmap_ctx_set_exact_blend": [P, C.c_int32],
         "latmap_ctx_set_decoder_path": [P, C.c_int32],
+        "latmap_ctx_set_reconstruct_precision": [P, C.c_int32],
         "latmap_project_gaussian": [P, P, P, P, C.c_float, C.POINTER(Pose), C.POINTER(Intrinsics),
                                     C.POINTER(C.c_int32), P, P, P],
         "latmap_render_cache_create": [P, C.POINTER(P)],
@@ -262,7 +263,7 @@ def _declare(L):
 
 
 EXPORTED = ["latmap_ctx_create", "latmap_ctx_destroy", "latmap_ctx_set_stream", "latmap_ctx_synchronize",
-            "latmap_ctx_set_exact_blend", "latmap_ctx_set_decoder_path",
+            "latmap_ctx_set_exact_blend", "latmap_ctx_set_decoder_path", "latmap_ctx_set_reconstruct_precision",
             "latmap_ctx_last_error", "latmap_ctx_launch_count", "latmap_default_config", "latmap_project_gaussian",
             "latmap_render_cache_create", "latmap_render_cache_destroy", "latmap_render", "latmap_render_backward",
             "latmap_render_cache_splats", "latmap_render_cache_tiles", "latmap_reconstruct",

@@ -123,6 +123,11 @@ class Context:
         """bf16 decoder kernels: 0 auto, 1 fused on-chip (DEC1/DEC2), 2 staged (DL1-DL5)."""
         check(self.h, lib().latmap_ctx_set_decoder_path(self.h, int(path)))
 
+    def set_reconstruct_precision(self, precision):
+        """Standalone reconstruct / query_map / evaluation: 0 fp32, 1 bf16 tcgen05 (K in 256..1024,
+        d_s in {32, 64}, D a multiple of 256; other shapes stay fp32)."""
+        check(self.h, lib().latmap_ctx_set_reconstruct_precision(self.h, int(precision)))
+
     def weighted_kmeans(self, points, weights, k, uniform, warm=None, max_iters=10):
         """weighted_kmeans (stream_kmeans.cpp:94-157) on the device -> (centers, weights, iterations).
 

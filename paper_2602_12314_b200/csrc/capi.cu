@@ -162,6 +162,7 @@ struct latmap_ctx {
   bool deterministic = false;  // fixed-order gradient reductions (bit-reproducible backward)
   DetScratch det;              // the deterministic render backward's per-(splat, tile) rows
   int32_t decoder_path = 0;  // bf16 decoder: 0 auto, 1 fused on-chip (DEC1/DEC2), 2 staged (DL1-DL5)
+  int32_t reconstruct_precision = 0;  // standalone reconstruct: 0 fp32 SIMT, 1 bf16 tcgen05 where supported
   cudaStream_t copy_stream = nullptr;  // keyframe uploads (overlap the step's render of earlier frames)
 };
 
@@ -298,6 +299,12 @@ latmap_status latmap_ctx_set_deterministic(latmap_ctx* ctx, int32_t on) {
 latmap_status latmap_ctx_set_decoder_path(latmap_ctx* ctx, int32_t path) {
   if (!ctx || path < 0 || path > 2) return LATMAP_ERR_INVALID_ARGUMENT;
   ctx->decoder_path = path;
+  return LATMAP_OK;
+}
+
+latmap_status latmap_ctx_set_reconstruct_precision(latmap_ctx* ctx, int32_t precision) {
+  if (!ctx || precision < 0 || precision > 1) return LATMAP_ERR_INVALID_ARGUMENT;
+  ctx->reconstruct_precision = precision;
   return LATMAP_OK;
 }
 
@@ -486,6 +493,10 @@ latmap_status latmap_reconstruct(latmap_ctx* ctx, const float* q, int64_t n, int
   if (!(temperature > 0.f)) return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "reconstruct: temperature must be > 0");
   if (n == 0) return LATMAP_OK;
   cudaStream_t st = ctx->stream;
+  if (ctx->reconstruct_precision == 1 && !attention && reconstruct_tc_supported(k, ds, df)) {
+    CTX_CHECK(ctx, reconstruct_tc(st, q, n, ds, atoms, proj, k, df, temperature, out));
+    return post_launch(ctx);
+  }
   float *qw = nullptr, *att = attention;
   CTX_CHECK(ctx, cudaMallocAsync(&qw, sizeof(float) * n * df, st));
   if (!att) CTX_CHECK(ctx, cudaMallocAsync(&att, sizeof(float) * n * k, st));

@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(512, 1) dl_softmax_kernel(Dl1Args a) {
       float4* dq = reinterpret_cast<float4*>(a.d_query + r0 * DS);
       for (int i = tid; i < valid * DS / 4; i += 512) dq[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    const int32_t asg = row < valid ? a.assign[r0 + row] : -1;
+    const int32_t asg = row < valid && a.assign ? a.assign[r0 + row] : -1;  // no assignment: reconstruct only
     const float* gp = a.gt + (int64_t)(asg < 0 ? 0 : asg) * K;
     uint8_t* et = a.e_tiles + (size_t)tile * kRows * K * 2;
     tc::fence_async_smem();
@@ -349,6 +349,132 @@ __global__ void dl_tile_m_kernel(const float* __restrict__ mm, int K, uint8_t* _
   }
 }
 
+// D (K x N fp32, row-major) -> B-operand blocks of dl_rec_kernel: block (nc, ks) holds
+// B[n][k] = D[k][n] for n in [256 nc, 256 nc + 256), k in [64 ks, 64 ks + 64).
+__global__ void dl_tile_dt_kernel(const float* __restrict__ d, int K, int N, uint8_t* __restrict__ bt) {
+  const int KB = K / 64;
+  const int64_t chunks = (int64_t)N * K / 8;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < chunks; q += (int64_t)gridDim.x * blockDim.x) {
+    const int n = (int)(q / (K / 8)), k0 = (int)(q % (K / 8)) * 8;
+    const int nc = n / 256, nl = n % 256, ks = k0 / 64, kl = k0 % 64;
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = d[(size_t)(k0 + i) * N + n];
+    tc::st_row8(bt + ((size_t)nc * KB + ks) * kT_B, nl, kl, 4096u, v);
+  }
+}
+
+// Standalone reconstruct (dictionary.cpp:25-53), F_hat = (e D) / sum: DL1's bf16 e tiles times
+// D on tcgen05, 128 x 256 output units through the same 4-stage TMA pipeline and double-
+// buffered TMEM accumulator as dl_t_kernel; the epilogue scales each row by 1/sum (DL1's row
+// statistics) and writes fp32 rows.
+struct DlRecArgs {
+  const uint8_t* e_tiles;  // ntiles x (128 x K bf16)
+  const uint8_t* bt;       // (N/256) x (K/64) blocks of 256 x 64 bf16: D^T
+  const float4* rs;        // npx: (max S, 1/sum, -, -)
+  float* out;              // npx x N
+  int64_t npx;
+  int K, N;
+};
+
+__global__ void __launch_bounds__(192, 1) dl_rec_kernel(DlRecArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t full[kT_Stages], empty[kT_Stages], accf[2], acce[2];
+  __shared__ uint32_t s_taddr;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int K = a.K, KB = K / 64, NC = a.N / 256;
+  const int64_t ntiles = (a.npx + kRows - 1) / kRows, units = ntiles * NC;
+  auto sA = [&](int s) { return smem + s * (kT_A + kT_B); };
+  auto sB = [&](int s) { return smem + s * (kT_A + kT_B) + kT_A; };
+  if (tid == 0) {
+    for (int i = 0; i < kT_Stages; ++i) {
+      tc::mbar_init(&full[i], 1);
+      tc::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&accf[i], 1);
+      tc::mbar_init(&acce[i], 128);
+    }
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc<512>(&s_taddr);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = s_taddr;
+  if (warp == 4) {
+    if (lane == 0) {  // producer: the e block and the D^T block of each k-step
+      int st = 0;
+      uint32_t ph = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const int64_t t = u / NC;
+        const int nc = (int)(u % NC);
+        const uint8_t* ea = a.e_tiles + (size_t)t * kRows * K * 2;
+        const uint8_t* bb = a.bt + (size_t)nc * KB * kT_B;
+        for (int ks = 0; ks < KB; ++ks) {
+          tc::mbar_wait(&empty[st], ph ^ 1);
+          tc::mbar_expect_tx(&full[st], kT_A + kT_B);
+          tc::bulk_g2s(sA(st), ea + (size_t)ks * kT_A, kT_A, &full[st]);
+          tc::bulk_g2s(sB(st), bb + (size_t)ks * kT_B, kT_B, &full[st]);
+          if (++st == kT_Stages) st = 0, ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {  // MMA issuer
+      const uint32_t idesc = tc::make_idesc_bf16(128, 256, 0, 0);
+      int st = 0;
+      uint32_t ph = 0;
+      int i = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+        const int buf = i & 1;
+        tc::mbar_wait(&acce[buf], ((i >> 1) & 1) ^ 1);
+        tc::tc_fence_after();
+        for (int ks = 0; ks < KB; ++ks) {
+          tc::mbar_wait(&full[st], ph);
+          tc::tc_fence_after();
+          const uint32_t aa = tc::smem_u32(sA(st)), ab = tc::smem_u32(sB(st));
+#pragma unroll
+          for (int k16 = 0; k16 < 4; ++k16)
+            tc::mma_bf16(tmem + buf * 256, tc::make_sdesc(aa + k16 * 2 * kCS, kCS, 128),
+                         tc::make_sdesc(ab + k16 * 2 * 4096, 4096, 128), idesc, (ks | k16) != 0);
+          tc::mma_commit(&empty[st]);
+          if (++st == kT_Stages) st = 0, ph ^= 1;
+        }
+        tc::mma_commit(&accf[buf]);
+      }
+    }
+  } else {  // epilogue: warps 0-3, one row per thread
+    const int row = 32 * warp + lane;
+    int i = 0;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+      const int buf = i & 1;
+      const int64_t t = u / NC;
+      const int nc = (int)(u % NC);
+      const int64_t r = t * kRows + row;
+      const float inv = r < a.npx ? a.rs[r].y : 0.f;
+      tc::mbar_wait(&accf[buf], (i >> 1) & 1);
+      tc::tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < 256; c += 32) {
+        float v[32];
+        tc::tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + buf * 256 + c, v);
+        if (r < a.npx) {
+          float4* dst = reinterpret_cast<float4*>(a.out + r * a.N + nc * 256 + c);
+#pragma unroll
+          for (int f = 0; f < 8; ++f)
+            dst[f] = make_float4(v[4 * f] * inv, v[4 * f + 1] * inv, v[4 * f + 2] * inv, v[4 * f + 3] * inv);
+        }
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&acce[buf]);
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free<512>(tmem);
+}
+
 // ------------------------------------------------------------------------------------------ DL3
 struct Dl3Args {
   const uint8_t* e_tiles;
@@ -422,7 +548,7 @@ __global__ void __launch_bounds__(512, 1) dl_back_kernel(Dl3Args a) {
     const int valid = (int)(a.npx - r0 < kRows ? a.npx - r0 : kRows);
     if (a.want_grad) tc::load_tile_bf16(sQ, a.query + r0 * DS, kRows, DS, valid, tid, 512);
     // per-row loss quantities (objective.cpp:100-185 via the factored algebra)
-    const int32_t asg = row < valid ? a.assign[r0 + row] : -1;
+    const int32_t asg = row < valid && a.assign ? a.assign[r0 + row] : -1;  // no assignment: reconstruct only
     const float4 st = row < valid ? a.rs[r0 + row] : make_float4(0.f, 0.f, 0.f, 0.f);
     const float inv_sum = st.y, dot = st.z;
     float nu2 = 0.f;
@@ -798,11 +924,19 @@ bool half_tile_map(CUtensorMap* m, const void* base, int ncg, int64_t ntiles, in
 
 template <typename F>
 void set_smem(F* f, size_t bytes) {
-  static size_t done = 0;  // per kernel instantiation
-  if (done < bytes) {
-    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    done = bytes;
-  }
+  // per kernel (not per function type: the DS instantiations of a kernel share one type, and an
+  // attribute set for one must not cap the other)
+  static std::vector<std::pair<const void*, size_t>> done;
+  for (auto& d : done)
+    if (d.first == reinterpret_cast<const void*>(f)) {
+      if (d.second < bytes) {
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        d.second = bytes;
+      }
+      return;
+    }
+  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  done.emplace_back(reinterpret_cast<const void*>(f), bytes);
 }
 
 template <int DS>
@@ -877,6 +1011,49 @@ void launch_dl(cudaStream_t st, DecoderWork& w, const float* query, const int32_
 }
 
 }  // namespace
+
+bool reconstruct_tc_supported(int64_t k, int ds, int df) {
+  return k >= 256 && k <= 1024 && k % 256 == 0 && (ds == 32 || ds == 64) && df >= 256 && df % 256 == 0;
+}
+
+cudaError_t reconstruct_tc(cudaStream_t st, const float* q, int64_t n, int ds, const float* atoms, const float* proj,
+                           int64_t k, int df, float temperature, float* out) {
+  if (n == 0) return cudaSuccess;
+  const int K = (int)k;
+  const int64_t ntiles = (n + kRows - 1) / kRows;
+  float *kd = nullptr, *rs = nullptr;
+  uint8_t *et = nullptr, *bt = nullptr;
+  cudaError_t e;
+  if ((e = cudaMallocAsync(&kd, sizeof(float) * k * ds, st)) || (e = cudaMallocAsync(&rs, sizeof(float) * 4 * n, st)) ||
+      (e = cudaMallocAsync(&et, (size_t)ntiles * kRows * K * 2, st)) ||
+      (e = cudaMallocAsync(&bt, (size_t)K * df * 2, st)))
+    return e;
+  sgemm(st, false, true, k, ds, df, 1.f, atoms, df, proj, df, 0.f, kd, ds);  // Kd = D W^T
+  dl_tile_dt_kernel<<<(unsigned)std::min<int64_t>(((int64_t)K * df / 8 + 255) / 256, 148 * 8), 256, 0, st>>>(
+      atoms, K, df, bt);
+  count_launch();
+  Dl1Args d1{et, q, nullptr, kd, nullptr, n, K, 1.f / temperature, reinterpret_cast<float4*>(rs), nullptr, 0};
+  const size_t sm1 = (size_t)K * ds * 2 + (size_t)kRows * ds * 2;
+  if (ds == 64) {
+    set_smem(dl_softmax_kernel<64>, sm1);
+    dl_softmax_kernel<64><<<148, 512, sm1, st>>>(d1);
+  } else {
+    set_smem(dl_softmax_kernel<32>, sm1);
+    dl_softmax_kernel<32><<<148, 512, sm1, st>>>(d1);
+  }
+  count_launch();
+  DlRecArgs dr{et, bt, reinterpret_cast<const float4*>(rs), out, n, K, df};
+  const size_t sm = (size_t)kT_Stages * (kT_A + kT_B);
+  set_smem(dl_rec_kernel, sm);
+  const int64_t units = ntiles * (df / 256);
+  dl_rec_kernel<<<(unsigned)std::min<int64_t>(148, units), 192, sm, st>>>(dr);
+  count_launch();
+  cudaFreeAsync(kd, st);
+  cudaFreeAsync(rs, st);
+  cudaFreeAsync(et, st);
+  cudaFreeAsync(bt, st);
+  return cudaGetLastError();
+}
 
 bool decoder_dl_supported(int64_t k, int ds, int64_t n_set) {
   return k >= 256 && k <= 1024 && k % 256 == 0 && (ds == 32 || ds == 64) && n_set >= 1 && n_set <= 256;

@@ -155,6 +155,12 @@ void decoder_bm_embed(cudaStream_t st, const float* bmt, const float* feats, int
                       float* d_atoms);
 // tcgen05 / TMEM path (bf16 operands, fp32 accumulation) for K in {128, 256}, d_s = 32, n_set <= 64.
 bool decoder_tc_supported(int64_t k, int ds, int64_t n_set);
+// Standalone reconstruct on tcgen05 (bf16 operands, fp32 accumulation; decoder_dl.cu):
+// out (n x df) = softmax(Q W D^T / temperature) D, for K in {256, ..., 1024}, ds in {32, 64},
+// df a multiple of 256.
+bool reconstruct_tc_supported(int64_t k, int ds, int df);
+cudaError_t reconstruct_tc(cudaStream_t st, const float* q, int64_t n, int ds, const float* atoms, const float* proj,
+                           int64_t k, int df, float temperature, float* out);
 void decoder_frame_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_t* assignment,
                       int64_t npx, const float* feats, int64_t n_set, const int64_t* nsup, const float* atoms,
                       const float* proj, float temperature, float lambda_cos, float lambda_l2, float scale,
