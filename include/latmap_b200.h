@@ -281,6 +281,10 @@ latmap_status latmap_session_step_dict(latmap_session* s, latmap_loss_breakdown*
 latmap_status latmap_session_export_rows(latmap_session* s, float* d_rows);
 latmap_status latmap_session_import_rows(latmap_session* s, const float* d_rows, int64_t n_new, const uint8_t* kept,
                                          int64_t n_kept);
+/* import_rows with the kept mask on the device (one byte per old row, d_kept NULL = none carry
+ * over) and n_kept its number of set entries (as latmap_store_sync_device reports them). */
+latmap_status latmap_session_import_rows_device(latmap_session* s, const float* d_rows, int64_t n_new,
+                                                const uint8_t* d_kept, int64_t n_kept);
 int64_t latmap_session_size(const latmap_session* s);
 /* seed_gaussians (pipeline.cpp:39-73) for frame b against a render of the current map: the
  * stride-2 pixels with observed depth > 0 whose rendered alpha < 0.5 or |rendered - observed
@@ -398,6 +402,22 @@ latmap_status latmap_store_sync(latmap_store* s, const float* d_active, const in
                                 int64_t n, const float center[3], float radius, float voxel_size, float* d_out,
                                 int64_t* out_origin, int64_t cap, uint8_t* kept_mask, int64_t stats[5],
                                 int64_t* out_count);
+/* fetch_local (active_set.cpp:7-36) with device outputs: d_origin (ascending record indices,
+ * may be NULL to count only), d_records (optional AoS gather); the store's persistent scratch,
+ * one count readback. count = NULL (with d_origin and d_records NULL): the scan only, no
+ * readback, nothing waits (used to time the radius scan on the device). */
+latmap_status latmap_store_fetch_local_device(latmap_store* s, const float center[3], float radius, int64_t* d_origin,
+                                              int64_t cap, float* d_records, int64_t* count);
+/* sync with every per-row array on the device: d_origin (int64), d_dirty (uint8, NULL = all
+ * dirty), d_kept (uint8 out) and d_out_origin (int64 out) are device buffers. Same results as
+ * latmap_store_sync bit for bit; the row selections are device compactions and the counts come
+ * back once (twice when newborns are present: their inserts follow the host probe order).
+ * The pool writeback of the written-back rows runs on the store's writeback stream, overlapping
+ * the caller's next work; every later store call waits for it. */
+latmap_status latmap_store_sync_device(latmap_store* s, const float* d_active, const int64_t* d_origin,
+                                       const uint8_t* d_dirty, int64_t n, const float center[3], float radius,
+                                       float voxel_size, float* d_out, int64_t* d_out_origin, int64_t cap,
+                                       uint8_t* d_kept, int64_t stats[5], int64_t* out_count);
 
 /* ---------------------------------------------------------------- streaming k-means */
 /* std::uniform_real_distribution<double>(0, 1) drawn from the caller's generator (the pipeline's

@@ -157,6 +157,7 @@ def _declare(L):
         "latmap_session_append_rows": [P, P, C.c_int64, P],
         "latmap_session_export_rows": [P, P],
         "latmap_session_import_rows": [P, P, C.c_int64, P, C.c_int64],
+        "latmap_session_import_rows_device": [P, P, C.c_int64, P, C.c_int64],
         "latmap_session_grad_buffer": [P, C.POINTER(P), C.POINTER(C.c_int64)],
         "latmap_session_loss_buffer": [P, C.POINTER(P), C.POINTER(C.c_int64)],
         "latmap_session_read_loss": [P, C.POINTER(LossBreakdown)],
@@ -218,6 +219,9 @@ def _declare(L):
         "latmap_store_fetch_local": [P, P, C.c_float, P, C.c_int64, C.POINTER(C.c_int64), P],
         "latmap_store_sync": [P, P, P, P, C.c_int64, P, C.c_float, C.c_float, P, P, C.c_int64, P, P,
                               C.POINTER(C.c_int64)],
+        "latmap_store_fetch_local_device": [P, P, C.c_float, P, C.c_int64, P, C.POINTER(C.c_int64)],
+        "latmap_store_sync_device": [P, P, P, P, C.c_int64, P, C.c_float, C.c_float, P, P, C.c_int64, P, P,
+                                     C.POINTER(C.c_int64)],
         "latmap_session_phase_times": [P, P, P],
     }
     for name, args in sig.items():
@@ -272,7 +276,8 @@ EXPORTED = ["latmap_ctx_create", "latmap_ctx_destroy", "latmap_ctx_set_stream", 
             "latmap_session_set_dictionary", "latmap_session_get_dictionary", "latmap_session_get_anchor", "latmap_session_set_frames",
             "latmap_session_set_batch", "latmap_session_set_slot_offset", "latmap_session_objective",
             "latmap_session_apply", "latmap_session_step", "latmap_session_objective_ex", "latmap_session_step_dict",
-            "latmap_session_export_rows", "latmap_session_import_rows", "latmap_session_size",
+            "latmap_session_export_rows", "latmap_session_import_rows", "latmap_session_import_rows_device",
+            "latmap_session_size",
             "latmap_session_set_graphs", "latmap_session_seed_candidates", "latmap_session_append_rows",
             "latmap_session_grad_buffer", "latmap_session_loss_buffer",
             "latmap_session_read_loss", "latmap_session_frame_images", "latmap_session_stats",
@@ -283,7 +288,7 @@ EXPORTED = ["latmap_ctx_create", "latmap_ctx_destroy", "latmap_ctx_set_stream", 
             "latmap_voxel_of", "latmap_hash_voxel", "latmap_store_create", "latmap_store_destroy", "latmap_store_size",
             "latmap_store_stats", "latmap_store_last_error", "latmap_store_insert", "latmap_store_update",
             "latmap_store_find", "latmap_store_get_records", "latmap_store_insert_global", "latmap_store_insert_keyed", "latmap_store_fetch_local",
-            "latmap_store_sync", "latmap_weighted_kmeans", "latmap_session_stream_kmeans",
+            "latmap_store_sync", "latmap_store_sync_device", "latmap_store_fetch_local_device", "latmap_weighted_kmeans", "latmap_session_stream_kmeans",
             "latmap_session_get_dict_weights", "latmap_session_set_dict_weights", "latmap_gather_supervision",
             "latmap_metric_cos", "latmap_metric_miou", "latmap_metric_psnr", "latmap_query_map",
             "latmap_default_pipeline_config", "latmap_select_keyframe", "latmap_pipeline_create",

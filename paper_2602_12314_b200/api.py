@@ -623,6 +623,15 @@ class Session:
         check(self.ctx.h, lib().latmap_session_import_rows(self.h, C.c_void_p(rows.data_ptr()) if n_new else None,
                                                            n_new, self._np_ptr(km), n_kept))
 
+    def import_rows_device(self, rows, kept, n_kept):
+        """import_rows with the kept mask on the device (torch uint8/bool, one entry per old row) and
+        its count known: no host pass over the rows."""
+        n_new = int(rows.shape[0])
+        km = None if kept is None else kept.to(torch.uint8).contiguous()
+        check(self.ctx.h, lib().latmap_session_import_rows_device(
+            self.h, C.c_void_p(rows.data_ptr()) if n_new else None, n_new,
+            C.c_void_p(km.data_ptr()) if km is not None and km.numel() else None, int(n_kept) if km is not None else 0))
+
     def seed_candidates(self, frame=0):
         """seed_gaussians (pipeline.cpp:39-73) rows for `frame` (features zero), device [n, 14 + ds]."""
         w, h = self.intr.width, self.intr.height
@@ -916,6 +925,55 @@ class Store:
         w = cnt.value
         stats = dict(zip(("written_back", "newborn_inserted", "newborn_rejected", "pruned", "fetched"), st.tolist()))
         return d_out[:w].clone(), oo[:w].copy(), kept[:n].astype(bool), stats
+
+    def radius_scan(self, center, radius):
+        """The device radius scan of fetch_local only (no readback, nothing waits)."""
+        c = np.ascontiguousarray(center, np.float32)
+        self._check(lib().latmap_store_fetch_local_device(self.h, c.ctypes.data_as(C.c_void_p), float(radius), None, 0,
+                                                          None, None))
+
+    def fetch_local_device(self, center, radius, gather=False):
+        """fetch_local with device outputs: (origin int64 CUDA, records or None)."""
+        c = np.ascontiguousarray(center, np.float32)
+        cnt = C.c_int64(0)
+        self._check(lib().latmap_store_fetch_local_device(self.h, c.ctypes.data_as(C.c_void_p), float(radius), None, 0,
+                                                          None, C.byref(cnt)))
+        n = cnt.value
+        dev = f"cuda:{self.ctx.device}"
+        org = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+        rec = torch.empty((max(n, 1), self.rs), device=dev) if gather else None
+        self._check(lib().latmap_store_fetch_local_device(self.h, c.ctypes.data_as(C.c_void_p), float(radius),
+                                                          C.c_void_p(org.data_ptr()), n,
+                                                          C.c_void_p(rec.data_ptr()) if gather else None,
+                                                          C.byref(cnt)))
+        return (org[:n], rec[:n]) if gather else org[:n]
+
+    def sync_device(self, d_active, d_origin, d_dirty, center, radius, voxel_size):
+        """sync with the per-row arrays on the device (latmap_store_sync_device): d_origin torch
+        int64 CUDA (n), d_dirty torch uint8 CUDA (n) or None (every row dirty). Returns device
+        (d_out, out_origin, kept) views and the stats dict; the output buffers are reused by the
+        next call."""
+        n = 0 if d_active is None else d_active.shape[0]
+        c = np.ascontiguousarray(center, np.float32)
+        cap = self.size() + n + 1
+        dev = f"cuda:{self.ctx.device}"
+        if getattr(self, "_ddout", None) is None or self._ddout.shape[0] < cap:
+            self._ddout = torch.empty((cap + cap // 8, self.rs), device=dev)
+            self._ddorg = torch.empty(cap + cap // 8, dtype=torch.int64, device=dev)
+        if getattr(self, "_dkept", None) is None or self._dkept.numel() < max(n, 1):
+            self._dkept = torch.empty(max(n, 1) + max(n, 1) // 4, dtype=torch.uint8, device=dev)
+        st = np.zeros(5, np.int64)
+        cnt = C.c_int64(0)
+        org = d_origin.contiguous() if n else None
+        dty = d_dirty.to(torch.uint8).contiguous() if (n and d_dirty is not None) else None
+        self._check(lib().latmap_store_sync_device(
+            self.h, C.c_void_p(d_active.data_ptr()) if n else None, C.c_void_p(org.data_ptr()) if n else None,
+            C.c_void_p(dty.data_ptr()) if dty is not None else None, n, c.ctypes.data_as(C.c_void_p), float(radius),
+            float(voxel_size), C.c_void_p(self._ddout.data_ptr()), C.c_void_p(self._ddorg.data_ptr()), cap,
+            C.c_void_p(self._dkept.data_ptr()), st.ctypes.data_as(C.c_void_p), C.byref(cnt)))
+        w = cnt.value
+        stats = dict(zip(("written_back", "newborn_inserted", "newborn_rejected", "pruned", "fetched"), st.tolist()))
+        return self._ddout[:w], self._ddorg[:w], self._dkept[:n], stats
 
 
 def default_pipeline_config(**overrides) -> _capi.PipelineConfig:

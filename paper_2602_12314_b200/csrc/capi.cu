@@ -1617,6 +1617,11 @@ static latmap_status session_capture_step(latmap_session* s, bool with_adam) {
   // capture on a private non-blocking stream (the context's stream may be the legacy default
   // stream, which cannot be captured); the graph is then launched on the context's stream
   if (!s->cap_stream) CTX_CHECK(ctx, cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking));
+  if (ctx->deterministic) {  // the fixed-order backward's scratch: allocated here, not inside the capture
+    int64_t pairs = 1;
+    for (int b = 0; b < s->nframes; ++b) pairs = std::max<int64_t>(pairs, s->rw[b].w.pair_cap);
+    CTX_CHECK(ctx, ctx->det.ensure(std::max<int64_t>(s->n, 1), pairs, s->ds));
+  }
   cudaStream_t saved = ctx->stream;
   // order the capture after everything already queued on the context stream
   CTX_CHECK(ctx, cudaStreamSynchronize(saved));
@@ -1787,22 +1792,12 @@ latmap_status latmap_session_export_rows(latmap_session* s, float* d_rows) {
   return post_launch(s->ctx);
 }
 
-latmap_status latmap_session_import_rows(latmap_session* s, const float* d_rows, int64_t n_new, const uint8_t* kept,
-                                         int64_t n_kept) {
-  if (!s || n_new < 0 || (n_new > 0 && !d_rows)) return LATMAP_ERR_INVALID_ARGUMENT;
+namespace {
+// import_rows with the kept-row list already on the device (d_idx: n_kept ascending old rows)
+latmap_status import_rows_impl(latmap_session* s, const float* d_rows, int64_t n_new, const int64_t* d_idx_kept,
+                               int64_t n_kept) {
   latmap_ctx* ctx = s->ctx;
   cudaStream_t st = ctx->stream;
-  // rows of the old map whose Adam moments carry over, in order (MapOptimizer::keep_map_rows)
-  std::vector<int64_t> idx;
-  if (kept) {
-    for (int64_t i = 0; i < s->n; ++i)
-      if (kept[i]) idx.push_back(i);
-  } else {
-    for (int64_t i = 0; i < s->n; ++i) idx.push_back(i);
-  }
-  if ((kept && (int64_t)idx.size() != n_kept) || (int64_t)idx.size() > n_new)
-    return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "import_rows: kept rows do not match the new row count");
-  n_kept = (int64_t)idx.size();
   const int ds = s->ds;
   const int64_t sizes[8] = {3 * n_new, 4 * n_new, 3 * n_new, 3 * n_new, n_new, (int64_t)ds * n_new,
                             (int64_t)ds * s->df, s->k * s->df};
@@ -1823,10 +1818,7 @@ latmap_status latmap_session_import_rows(latmap_session* s, const float* d_rows,
     s->sp_cap = cap;
   }
   float *np = s->sp_params, *ng = s->sp_grads, *nm = s->sp_m, *nv = s->sp_v;
-  int64_t* d_idx = nullptr;
-  CTX_CHECK(ctx, cudaMallocAsync(&d_idx, sizeof(int64_t) * std::max<size_t>(idx.size(), 1), st));
-  if (!idx.empty())
-    CTX_CHECK(ctx, cudaMemcpyAsync(d_idx, idx.data(), sizeof(int64_t) * idx.size(), cudaMemcpyHostToDevice, st));
+  const int64_t* d_idx = d_idx_kept;
   MapOff so, d_o;
   for (int i = 0; i < 6; ++i) so.o[i] = s->off[i], d_o.o[i] = off[i];
   if (n_new > 0) {
@@ -1841,7 +1833,6 @@ latmap_status latmap_session_import_rows(latmap_session* s, const float* d_rows,
   CTX_CHECK(ctx, cudaMemcpyAsync(nm + off[6], s->m + s->off[6], sizeof(float) * dict, cudaMemcpyDeviceToDevice, st));
   CTX_CHECK(ctx, cudaMemcpyAsync(nv + off[6], s->v + s->off[6], sizeof(float) * dict, cudaMemcpyDeviceToDevice, st));
   CTX_CHECK(ctx, cudaMemsetAsync(ng, 0, sizeof(float) * std::max<int64_t>(total, 1), st));
-  CTX_CHECK(ctx, cudaFreeAsync(d_idx, st));
   // swap: the old set (stream-ordered behind the copies above) becomes the next spare
   std::swap(s->params, s->sp_params), std::swap(s->grads, s->sp_grads), std::swap(s->m, s->sp_m),
       std::swap(s->v, s->sp_v), std::swap(s->cur_cap, s->sp_cap);
@@ -1857,6 +1848,52 @@ latmap_status latmap_session_import_rows(latmap_session* s, const float* d_rows,
   s->renders_valid = false;
   s->drop_graph();
   return LATMAP_OK;
+}
+}  // namespace
+
+latmap_status latmap_session_import_rows(latmap_session* s, const float* d_rows, int64_t n_new, const uint8_t* kept,
+                                         int64_t n_kept) {
+  if (!s || n_new < 0 || (n_new > 0 && !d_rows)) return LATMAP_ERR_INVALID_ARGUMENT;
+  latmap_ctx* ctx = s->ctx;
+  cudaStream_t st = ctx->stream;
+  // rows of the old map whose Adam moments carry over, in order (MapOptimizer::keep_map_rows)
+  std::vector<int64_t> idx;
+  if (kept) {
+    for (int64_t i = 0; i < s->n; ++i)
+      if (kept[i]) idx.push_back(i);
+  } else {
+    for (int64_t i = 0; i < s->n; ++i) idx.push_back(i);
+  }
+  if ((kept && (int64_t)idx.size() != n_kept) || (int64_t)idx.size() > n_new)
+    return fail(ctx, LATMAP_ERR_INVALID_ARGUMENT, "import_rows: kept rows do not match the new row count");
+  int64_t* d_idx = nullptr;
+  CTX_CHECK(ctx, cudaMallocAsync(&d_idx, sizeof(int64_t) * std::max<size_t>(idx.size(), 1), st));
+  if (!idx.empty())
+    CTX_CHECK(ctx, cudaMemcpyAsync(d_idx, idx.data(), sizeof(int64_t) * idx.size(), cudaMemcpyHostToDevice, st));
+  const latmap_status r = import_rows_impl(s, d_rows, n_new, d_idx, (int64_t)idx.size());
+  cudaFreeAsync(d_idx, st);
+  return r;
+}
+
+latmap_status latmap_session_import_rows_device(latmap_session* s, const float* d_rows, int64_t n_new,
+                                                const uint8_t* d_kept, int64_t n_kept) {
+  if (!s || n_new < 0 || (n_new > 0 && !d_rows) || n_kept < 0 || n_kept > n_new || n_kept > s->n ||
+      (n_kept > 0 && !d_kept))
+    return LATMAP_ERR_INVALID_ARGUMENT;
+  latmap_ctx* ctx = s->ctx;
+  cudaStream_t st = ctx->stream;
+  int64_t* d_idx = nullptr;
+  int32_t* d_blk = nullptr;
+  int64_t* d_cnt = nullptr;
+  CTX_CHECK(ctx, cudaMallocAsync(&d_idx, sizeof(int64_t) * std::max<int64_t>(s->n, 1), st));
+  CTX_CHECK(ctx, cudaMallocAsync(&d_blk, sizeof(int32_t) * (compact_blocks(s->n) + 1), st));
+  CTX_CHECK(ctx, cudaMallocAsync(&d_cnt, sizeof(int64_t), st));
+  if (d_kept && s->n > 0) CTX_CHECK(ctx, compact_mask(st, d_kept, s->n, d_idx, d_blk, d_cnt));
+  const latmap_status r = import_rows_impl(s, d_rows, n_new, d_idx, d_kept ? n_kept : 0);
+  cudaFreeAsync(d_idx, st);
+  cudaFreeAsync(d_blk, st);
+  cudaFreeAsync(d_cnt, st);
+  return r;
 }
 
 int64_t latmap_session_size(const latmap_session* s) { return s ? s->n : -1; }

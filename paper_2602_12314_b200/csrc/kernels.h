@@ -159,6 +159,11 @@ bool decoder_tc_supported(int64_t k, int ds, int64_t n_set);
 // out (n x df) = softmax(Q W D^T / temperature) D, for K in {256, ..., 1024}, ds in {32, 64},
 // df a multiple of 256.
 bool reconstruct_tc_supported(int64_t k, int ds, int df);
+// Order-preserving compaction of a device byte mask: out_idx = ascending i with mask[i] != 0,
+// *count (device) = their number; blocks: compact_blocks(n) int32 scratch (store.cu).
+int64_t compact_blocks(int64_t n);
+cudaError_t compact_mask(cudaStream_t st, const uint8_t* mask, int64_t n, int64_t* out_idx, int32_t* blocks,
+                         int64_t* count);
 cudaError_t reconstruct_tc(cudaStream_t st, const float* q, int64_t n, int ds, const float* atoms, const float* proj,
                            int64_t k, int df, float temperature, float* out);
 void decoder_frame_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_t* assignment,

@@ -74,27 +74,43 @@ __global__ void __launch_bounds__(kScanBlock) radius_count_kernel(const float* _
   if (threadIdx.x == 0) block_counts[blockIdx.x] = c;
 }
 
-// K11c: exclusive scan of the block counts (one block, loops over chunks).
+// K11c: exclusive scan of the block counts (one block of 1024 threads, chunks of 1024 counts:
+// warp shuffles, then one scan of the 32 warp totals).
 __global__ void __launch_bounds__(1024) block_scan_kernel(int32_t* counts, int64_t nblocks, int64_t* total) {
-  __shared__ int64_t s[1024];
-  int64_t carry = 0;
+  __shared__ int64_t s_w[32];
+  __shared__ int64_t s_carry;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
   for (int64_t base = 0; base < nblocks; base += 1024) {
     const int64_t i = base + threadIdx.x;
     const int64_t v = i < nblocks ? counts[i] : 0;
-    s[threadIdx.x] = v;
-    __syncthreads();
-    for (int o = 1; o < 1024; o <<= 1) {
-      const int64_t t = threadIdx.x >= (unsigned)o ? s[threadIdx.x - o] : 0;
-      __syncthreads();
-      s[threadIdx.x] += t;
-      __syncthreads();
+    int64_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += t;
     }
-    if (i < nblocks) counts[i] = (int32_t)(carry + s[threadIdx.x] - v);
-    const int64_t blk = s[1023];
+    if (lane == 31) s_w[w] = x;
     __syncthreads();
-    carry += blk;
+    if (w == 0) {
+      int64_t y = s_w[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t t = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= o) y += t;
+      }
+      s_w[lane] = y;  // inclusive warp totals
+    }
+    __syncthreads();
+    const int64_t carry = s_carry;
+    const int64_t excl = carry + (w ? s_w[w - 1] : 0) + x - v;
+    if (i < nblocks) counts[i] = (int32_t)excl;
+    __syncthreads();
+    if (threadIdx.x == 1023) s_carry = carry + s_w[31];
+    __syncthreads();
   }
-  if (threadIdx.x == 0) *total = carry;
+  if (threadIdx.x == 0) *total = s_carry;
 }
 
 // K11d: order-preserving compaction of the hits (ascending record index).
@@ -120,6 +136,100 @@ __global__ void __launch_bounds__(kScanBlock) radius_emit_kernel(const float* __
   }
   __syncthreads();
   if (hit) out[block_offsets[blockIdx.x] + s_warp[w] + __popc(m & ((1u << lane) - 1u))] = i;
+}
+
+// K11b' single-pass radius compaction (decoupled look-back): each block takes the next ticket,
+// tests kRcEach consecutive records per thread (kRcPer per block), publishes its hit count, adds the
+// counts of the blocks before it (flag P: inclusive prefix, A: own count only) and emits its hits
+// in ascending record order. status[] (one word per block: flag << 62 | value) and the ticket
+// are zeroed before the launch; the last block writes the total.
+constexpr int kRcThreads = 512, kRcEach = 8, kRcPer = kRcEach * kRcThreads;
+__global__ void __launch_bounds__(kRcThreads) radius_compact_kernel(const float* __restrict__ pos, int64_t n, float cx,
+                                                                    float cy, float cz, float r2,
+                                                                    const uint8_t* __restrict__ present,
+                                                                    unsigned long long* status, int* ticket,
+                                                                    int64_t* __restrict__ out, int64_t* total) {
+  __shared__ int s_bid;
+  __shared__ int32_t s_warp[kRcThreads / 32];
+  __shared__ long long s_prefix;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) s_bid = atomicAdd(ticket, 1);
+  __syncthreads();
+  const int64_t bid = s_bid;
+  const int64_t i0 = bid * kRcPer + kRcEach * (int64_t)tid;
+  bool hit[kRcEach];
+  if (i0 + kRcEach - 1 < n) {
+    const float4* p4 = reinterpret_cast<const float4*>(pos + 3 * i0);
+    float v[3 * kRcEach];
+#pragma unroll
+    for (int q = 0; q < 3 * kRcEach / 4; ++q) {
+      const float4 t = p4[q];
+      v[4 * q] = t.x, v[4 * q + 1] = t.y, v[4 * q + 2] = t.z, v[4 * q + 3] = t.w;
+    }
+#pragma unroll
+    for (int k = 0; k < kRcEach; ++k) hit[k] = (!present || !present[i0 + k]) && in_radius(v + 3 * k, cx, cy, cz, r2);
+  } else {
+#pragma unroll
+    for (int k = 0; k < kRcEach; ++k)
+      hit[k] = i0 + k < n && (!present || !present[i0 + k]) && in_radius(pos + 3 * (i0 + k), cx, cy, cz, r2);
+  }
+  int c = 0;
+#pragma unroll
+  for (int k = 0; k < kRcEach; ++k) c += (int)hit[k];
+  int x = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += t;
+  }
+  if (lane == 31) s_warp[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int y = lane < kRcThreads / 32 ? s_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= o) y += t;
+    }
+    if (lane < kRcThreads / 32) s_warp[lane] = y;  // inclusive warp totals
+  }
+  __syncthreads();
+  const int agg = s_warp[kRcThreads / 32 - 1];
+  constexpr unsigned long long kA = 1ull << 62, kP = 2ull << 62, kMask = (1ull << 62) - 1;
+  if (tid == 0) atomicExch(&status[bid], (bid == 0 ? kP : kA) | (unsigned long long)agg);
+  if (w == 0 && bid > 0) {  // warp look-back over windows of 32 predecessors
+    long long prefix = 0;
+    for (int64_t j = bid - 1;;) {
+      const int64_t jj = j - lane;
+      const unsigned long long st = jj >= 0 ? atomicAdd(&status[jj], 0ull) : kP;  // before block 0: P, 0
+      const unsigned f = (unsigned)(st >> 62);
+      if (__any_sync(0xffffffffu, f == 0)) continue;  // a predecessor has not published yet
+      const unsigned pm = __ballot_sync(0xffffffffu, f == 2);
+      const int first = pm ? __ffs(pm) - 1 : 32;  // the nearest predecessor with an inclusive prefix
+      long long v = lane <= first ? (long long)(st & kMask) : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      prefix += v;
+      if (pm) break;
+      j -= 32;
+    }
+    if (lane == 0) {
+      atomicExch(&status[bid], kP | (unsigned long long)(prefix + agg));
+      s_prefix = prefix;
+    }
+  } else if (tid == 0) {
+    s_prefix = 0;
+  }
+  if (tid == 0 && (bid + 1) * kRcPer >= n) {
+    __threadfence();
+  }
+  __syncthreads();
+  if (tid == 0 && (bid + 1) * kRcPer >= n) *total = s_prefix + agg;
+  __syncthreads();
+  int64_t o = s_prefix + (w ? s_warp[w - 1] : 0) + x - c;
+#pragma unroll
+  for (int k = 0; k < kRcEach; ++k)
+    if (hit[k]) out[o++] = i0 + k;
 }
 
 // K11e: gather records (mapped host pool -> device AoS) and scatter (device AoS -> mapped pool).
@@ -171,11 +281,131 @@ __global__ void copy_rows_kernel(const float* __restrict__ in, const int64_t* __
   }
 }
 
+// ---- device-resident sync (latmap_store_sync_device): row selections as order-preserving
+// compactions, counts kept on the device until the end.
+// sel: 0 written-back rows (tracked and dirty), 1 newborn rows (untracked), 2 kept rows
+__device__ __forceinline__ bool sel_row(int mode, int64_t i, const int64_t* __restrict__ origin,
+                                        const uint8_t* __restrict__ dirty, const uint8_t* __restrict__ kept) {
+  if (mode == 0) return origin[i] >= 0 && (!dirty || dirty[i]);
+  if (mode == 1) return origin[i] < 0;
+  return kept[i] != 0;
+}
+__global__ void __launch_bounds__(kScanBlock) sel_count_kernel(int mode, int64_t n, const int64_t* __restrict__ origin,
+                                                               const uint8_t* __restrict__ dirty,
+                                                               const uint8_t* __restrict__ kept,
+                                                               int32_t* __restrict__ block_counts) {
+  const int64_t i = blockIdx.x * (int64_t)kScanBlock + threadIdx.x;
+  const int c = __syncthreads_count(i < n && sel_row(mode, i, origin, dirty, kept));
+  if (threadIdx.x == 0) block_counts[blockIdx.x] = c;
+}
+// rows in ascending order -> out_rows; out_val (optional) = origin[row]
+__global__ void __launch_bounds__(kScanBlock) sel_emit_kernel(int mode, int64_t n, const int64_t* __restrict__ origin,
+                                                              const uint8_t* __restrict__ dirty,
+                                                              const uint8_t* __restrict__ kept,
+                                                              const int32_t* __restrict__ block_offsets,
+                                                              int64_t* __restrict__ out_rows, int64_t* __restrict__ out_val) {
+  __shared__ int32_t s_warp[kScanBlock / 32];
+  const int64_t i = blockIdx.x * (int64_t)kScanBlock + threadIdx.x;
+  const bool hit = i < n && sel_row(mode, i, origin, dirty, kept);
+  const unsigned m = __ballot_sync(0xffffffffu, hit);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) s_warp[w] = __popc(m);
+  __syncthreads();
+  if (w == 0) {
+    int v = s_warp[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += t;
+    }
+    s_warp[lane] = v - s_warp[lane];
+  }
+  __syncthreads();
+  if (hit) {
+    const int64_t j = block_offsets[blockIdx.x] + s_warp[w] + __popc(m & ((1u << lane) - 1u));
+    out_rows[j] = i;
+    if (out_val) out_val[j] = origin[i];
+  }
+}
+__global__ void copy_i64_kernel(const int64_t* __restrict__ in, int64_t n, int64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+__global__ void scatter_i64_kernel(const int64_t* __restrict__ rows, const int64_t* __restrict__ vals, int64_t n,
+                                   int64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[rows[i]] = vals[i];
+}
+// copy_rows / gather / pos_scatter with the row count (and an output row offset) read on the device
+__global__ void copy_rows_dev_kernel(const float* __restrict__ in, const int64_t* __restrict__ rows,
+                                     const int64_t* __restrict__ count, int64_t cap_rows, int rs, float* __restrict__ out) {
+  const int64_t n = min(*count, cap_rows);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * rs; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / rs, c = e % rs;
+    out[e] = in[rows[r] * rs + c];
+  }
+}
+__global__ void pos_scatter_dev_kernel(float* __restrict__ pos_mirror, const int64_t* __restrict__ idx,
+                                       const int64_t* __restrict__ count, int rs, const float* __restrict__ in) {
+  const int64_t n = *count;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * 3; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / 3, c = e % 3;
+    pos_mirror[idx[r] * 3 + c] = in[r * rs + c];
+  }
+}
+__global__ void scatter_rec_dev_kernel(float* __restrict__ pool, const int64_t* __restrict__ idx,
+                                       const int64_t* __restrict__ count, int rs, const float* __restrict__ in) {
+  const int64_t n = *count;
+  if (rs & 1) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * rs; e += (int64_t)gridDim.x * blockDim.x)
+      pool[idx[e / rs] * rs + e % rs] = in[e];
+    return;
+  }
+  const int h = rs / 2;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * h; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / h, c = e % h;
+    reinterpret_cast<float2*>(pool + idx[r] * rs)[c] = reinterpret_cast<const float2*>(in + r * rs)[c];
+  }
+}
+// assemble: d_out = kept rows (in row order) ++ fetched records (ascending index); out_origin
+// likewise. cnt = {nk, fetched}; nothing is written when nk + fetched > cap.
+__global__ void assemble_kernel(const float* __restrict__ active, const int64_t* __restrict__ keep_rows,
+                                const int64_t* __restrict__ resolved, const float* __restrict__ pool,
+                                const int64_t* __restrict__ fetch, const int64_t* __restrict__ cnt, int64_t cap,
+                                int rs, float* __restrict__ out, int64_t* __restrict__ out_origin) {
+  const int64_t nk = cnt[0], nf = cnt[1];
+  if (nk + nf > cap) return;
+  const int64_t total = (nk + nf) * rs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / rs, c = e % rs;
+    if (r < nk) {
+      const int64_t row = keep_rows[r];
+      out[e] = active[row * rs + c];
+      if (c == 0 && out_origin) out_origin[r] = resolved[row];
+    } else {
+      const int64_t rec = fetch[r - nk];
+      out[e] = pool[rec * rs + c];
+      if (c == 0 && out_origin) out_origin[r] = rec;
+    }
+  }
+}
+
 inline unsigned grid_of(int64_t n, int per = 256) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + per - 1) / per, 148 * 16));
 }
 
 }  // namespace
+
+int64_t compact_blocks(int64_t n) { return std::max<int64_t>(1, (n + kScanBlock - 1) / kScanBlock); }
+
+cudaError_t compact_mask(cudaStream_t st, const uint8_t* mask, int64_t n, int64_t* out_idx, int32_t* blocks,
+                         int64_t* count) {
+  const int64_t nb = compact_blocks(n);
+  sel_count_kernel<<<(unsigned)nb, kScanBlock, 0, st>>>(2, n, nullptr, nullptr, mask, blocks);
+  block_scan_kernel<<<1, 1024, 0, st>>>(blocks, nb, count);
+  sel_emit_kernel<<<(unsigned)nb, kScanBlock, 0, st>>>(2, n, nullptr, nullptr, mask, blocks, out_idx, nullptr);
+  count_launch(3);
+  return cudaGetLastError();
+}
 
 }  // namespace lm
 
@@ -206,6 +436,21 @@ struct latmap_store {
   // pinned staging for sync's index lists (async uploads, no pageable staging copies)
   int64_t* h_stage = nullptr;
   int64_t h_stage_cap = 0;
+  // device-resident sync scratch (grow-only): rows [n] x 4 lists, present [pool], fetch [pool],
+  // block counts, counters {nwb, nnb, nk, fetched, ...}; a pinned readback of the counters
+  int64_t *dv_res = nullptr, *dv_wb_rows = nullptr, *dv_wb_idx = nullptr, *dv_rows2 = nullptr;
+  int64_t dv_n_cap = 0;
+  uint8_t* dv_present = nullptr;
+  int64_t* dv_fetch = nullptr;
+  int64_t dv_pool_cap = 0;
+  int32_t* dv_cnt = nullptr;
+  int64_t dv_cnt_cap = 0;
+  int64_t* dv_counts = nullptr;  // [0] nwb [1] nnb [2] nk [3] fetched [4] scan total (device)
+  unsigned long long* dv_status = nullptr;  // radius_compact_kernel look-back words (+ ticket)
+  int64_t dv_status_cap = 0;
+  int64_t* h_counts = nullptr;   // pinned copy of dv_counts
+  float* dv_wb_tmp = nullptr;    // written-back rows staged for the pool scatter (wb stream)
+  int64_t dv_tmp_cap = 0;
   // scratch
   std::string err;
 };
@@ -329,6 +574,11 @@ latmap_status latmap_store_destroy(latmap_store* s) {
   if (s->d_pos) cudaFree(s->d_pos);
   if (s->wb_ev) cudaEventDestroy(s->wb_ev);
   if (s->h_stage) cudaFreeHost(s->h_stage);
+  for (void* p : {(void*)s->dv_res, (void*)s->dv_wb_rows, (void*)s->dv_wb_idx, (void*)s->dv_rows2,
+                  (void*)s->dv_present, (void*)s->dv_fetch, (void*)s->dv_cnt, (void*)s->dv_counts, (void*)s->dv_status,
+                  (void*)s->dv_wb_tmp})
+    if (p) cudaFree(p);
+  if (s->h_counts) cudaFreeHost(s->h_counts);
   if (s->wb_st) cudaStreamDestroy(s->wb_st);
   delete s;
   return LATMAP_OK;
@@ -700,6 +950,251 @@ latmap_status latmap_store_sync(latmap_store* s, const float* d_active, const in
     s->wb_pending = true;
   }
   return ret;
+}
+
+
+namespace {
+// order-preserving radius compaction of the pool positions into out (ascending), count -> *total
+latmap_status radius_compact(latmap_store* s, const float center[3], float r2, const uint8_t* present, int64_t* out,
+                             int64_t* total) {
+  const int64_t ps = s->size;
+  const int64_t nb = (ps + kRcPer - 1) / kRcPer;
+  if (s->dv_status_cap < nb + 1) {
+    if (s->dv_status) cudaFree(s->dv_status);
+    s->dv_status_cap = nb + 1 + nb / 4;
+    S_CHECK(s, cudaMalloc(&s->dv_status, sizeof(unsigned long long) * s->dv_status_cap));
+  }
+  S_CHECK(s, cudaMemsetAsync(s->dv_status, 0, sizeof(unsigned long long) * (nb + 1), s->st));
+  radius_compact_kernel<<<(unsigned)nb, kRcThreads, 0, s->st>>>(
+      s->d_pos, ps, center[0], center[1], center[2], r2, present, s->dv_status,
+      reinterpret_cast<int*>(s->dv_status + nb), out, total);
+  count_launch();
+  return LATMAP_OK;
+}
+}  // namespace
+
+// sync (active_set.cpp:38-128) with every per-row array on the device: origin / dirty / kept /
+// out_origin are device buffers, the row selections are order-preserving device compactions and
+// the counts come back once (plus once more when newborns need the host's probe order).
+latmap_status latmap_store_sync_device(latmap_store* s, const float* d_active, const int64_t* d_origin,
+                                       const uint8_t* d_dirty, int64_t n, const float center[3], float radius,
+                                       float voxel_size, float* d_out, int64_t* d_out_origin, int64_t cap,
+                                       uint8_t* d_kept, int64_t stats_out[5], int64_t* out_count) {
+  if (!s || !center || !out_count || n < 0 || (n > 0 && (!d_active || !d_origin || !d_kept)))
+    return LATMAP_ERR_INVALID_ARGUMENT;
+  if (!(voxel_size > 0.f)) return sfail(s, LATMAP_ERR_INVALID_ARGUMENT, "voxel_of: voxel_size must be > 0");
+  const int rs = s->rs;
+  cudaStream_t st = s->st;
+  wb_wait(s);  // the previous sync's writeback (it reads dv_wb_tmp / dv_wb_idx / dv_counts)
+  int64_t st5[5] = {0, 0, 0, 0, 0};
+  const int64_t nn = std::max<int64_t>(n, 1);
+  auto grow64 = [&](int64_t*& p, int64_t need) -> cudaError_t {
+    if (p) cudaFree(p);
+    return cudaMalloc(&p, sizeof(int64_t) * need);
+  };
+  if (s->dv_n_cap < nn) {
+    S_CHECK(s, grow64(s->dv_res, nn + nn / 4));
+    S_CHECK(s, grow64(s->dv_wb_rows, nn + nn / 4));
+    S_CHECK(s, grow64(s->dv_wb_idx, nn + nn / 4));
+    S_CHECK(s, grow64(s->dv_rows2, nn + nn / 4));
+    if (s->dv_wb_tmp) cudaFree(s->dv_wb_tmp);
+    S_CHECK(s, cudaMalloc(&s->dv_wb_tmp, sizeof(float) * (nn + nn / 4) * rs));
+    s->dv_n_cap = nn + nn / 4;
+  }
+  if (!s->dv_counts) {
+    S_CHECK(s, cudaMalloc(&s->dv_counts, sizeof(int64_t) * 8));
+    S_CHECK(s, cudaHostAlloc(&s->h_counts, sizeof(int64_t) * 8, 0));
+  }
+  auto ensure_blocks = [&](int64_t rows) -> cudaError_t {
+    const int64_t nb = compact_blocks(rows) + 1;
+    if (s->dv_cnt_cap >= nb) return cudaSuccess;
+    if (s->dv_cnt) cudaFree(s->dv_cnt);
+    s->dv_cnt_cap = nb + nb / 4;
+    return cudaMalloc(&s->dv_cnt, sizeof(int32_t) * s->dv_cnt_cap);
+  };
+  S_CHECK(s, ensure_blocks(n));
+  S_CHECK(s, cudaMemsetAsync(s->dv_counts, 0, sizeof(int64_t) * 8, st));
+  const int64_t nbn = compact_blocks(n);
+  if (n > 0) {
+    copy_i64_kernel<<<grid_of(n), 256, 0, st>>>(d_origin, n, s->dv_res);  // resolved = origin (newborns: -1)
+    // newborn rows (row order) and written-back rows with their records
+    sel_count_kernel<<<(unsigned)nbn, kScanBlock, 0, st>>>(1, n, d_origin, d_dirty, nullptr, s->dv_cnt);
+    block_scan_kernel<<<1, 1024, 0, st>>>(s->dv_cnt, nbn, s->dv_counts + 1);
+    sel_emit_kernel<<<(unsigned)nbn, kScanBlock, 0, st>>>(1, n, d_origin, d_dirty, nullptr, s->dv_cnt, s->dv_rows2,
+                                                          nullptr);
+    sel_count_kernel<<<(unsigned)nbn, kScanBlock, 0, st>>>(0, n, d_origin, d_dirty, nullptr, s->dv_cnt);
+    block_scan_kernel<<<1, 1024, 0, st>>>(s->dv_cnt, nbn, s->dv_counts + 0);
+    sel_emit_kernel<<<(unsigned)nbn, kScanBlock, 0, st>>>(0, n, d_origin, d_dirty, nullptr, s->dv_cnt, s->dv_wb_rows,
+                                                          s->dv_wb_idx);
+    copy_rows_dev_kernel<<<grid_of(n * rs), 256, 0, st>>>(d_active, s->dv_wb_rows, s->dv_counts + 0, n, rs,
+                                                          s->dv_wb_tmp);
+    pos_scatter_dev_kernel<<<grid_of(n * 3), 256, 0, st>>>(s->d_pos, s->dv_wb_idx, s->dv_counts + 0, rs,
+                                                           s->dv_wb_tmp);
+    count_launch(9);
+  }
+  S_CHECK(s, cudaMemcpyAsync(s->h_counts, s->dv_counts, sizeof(int64_t) * 2, cudaMemcpyDeviceToHost, st));
+  S_CHECK(s, cudaStreamSynchronize(st));
+  const int64_t nwb = s->h_counts[0], nnb = s->h_counts[1];
+  st5[0] = nwb;
+  int64_t ins = 0;
+  if (nnb > 0) {
+    // newborns insert under the voxel of their optimised position in row order (the host probe
+    // sequence defines record indices and rejections, active_set.cpp:56-70)
+    std::vector<int64_t> rows((size_t)nnb);
+    float* d_nb = nullptr;
+    int32_t* d_keys = nullptr;
+    int64_t *d_home = nullptr, *d_pairs = nullptr;
+    S_CHECK(s, cudaMemcpyAsync(rows.data(), s->dv_rows2, sizeof(int64_t) * nnb, cudaMemcpyDeviceToHost, st));
+    S_CHECK(s, cudaMallocAsync(&d_nb, sizeof(float) * nnb * rs, st));
+    S_CHECK(s, cudaMallocAsync(&d_keys, sizeof(int32_t) * nnb * 3, st));
+    S_CHECK(s, cudaMallocAsync(&d_home, sizeof(int64_t) * nnb, st));
+    S_CHECK(s, cudaMallocAsync(&d_pairs, sizeof(int64_t) * nnb * 2, st));
+    copy_rows_kernel<<<grid_of(nnb * rs), 256, 0, st>>>(d_active, s->dv_rows2, nnb, rs, d_nb);
+    keys_kernel<<<grid_of(nnb), 256, 0, st>>>(d_nb, nnb, rs, voxel_size, s->capacity, d_keys, d_home);
+    count_launch(2);
+    std::vector<float> nb((size_t)nnb * rs);
+    std::vector<int32_t> keys((size_t)nnb * 3);
+    std::vector<int64_t> home((size_t)nnb);
+    S_CHECK(s, cudaMemcpyAsync(nb.data(), d_nb, sizeof(float) * nnb * rs, cudaMemcpyDeviceToHost, st));
+    S_CHECK(s, cudaMemcpyAsync(keys.data(), d_keys, sizeof(int32_t) * nnb * 3, cudaMemcpyDeviceToHost, st));
+    S_CHECK(s, cudaMemcpyAsync(home.data(), d_home, sizeof(int64_t) * nnb, cudaMemcpyDeviceToHost, st));
+    S_CHECK(s, cudaStreamSynchronize(st));
+    if (ensure_pool(s, s->size + nnb) != LATMAP_OK) return LATMAP_ERR_OUT_OF_MEMORY;
+    const int64_t first = s->size;
+    std::vector<int64_t> pr;  // (row, record) of the inserted newborns
+    for (int64_t j = 0; j < nnb; ++j) {
+      const int64_t r = insert_one(s, &keys[3 * j], home[j], &nb[j * rs], false, nullptr);
+      if (r >= 0) {
+        pr.push_back(rows[j]);
+        pr.push_back(r);
+        ++ins;
+      }
+    }
+    st5[1] = ins;
+    st5[2] = nnb - ins;
+    if (ins > 0) {
+      std::vector<int64_t> rr((size_t)ins), rv((size_t)ins);
+      for (int64_t j = 0; j < ins; ++j) rr[j] = pr[2 * j], rv[j] = pr[2 * j + 1];
+      S_CHECK(s, cudaMemcpyAsync(d_pairs, rr.data(), sizeof(int64_t) * ins, cudaMemcpyHostToDevice, st));
+      S_CHECK(s, cudaMemcpyAsync(d_pairs + nnb, rv.data(), sizeof(int64_t) * ins, cudaMemcpyHostToDevice, st));
+      scatter_i64_kernel<<<grid_of(ins), 256, 0, st>>>(d_pairs, d_pairs + nnb, ins, s->dv_res);
+      count_launch();
+    }
+    std::vector<float> pos((size_t)(s->size - first) * 3);
+    for (int64_t r = first; r < s->size; ++r) std::memcpy(&pos[(r - first) * 3], s->pool + r * rs, 12);
+    if (!pos.empty())
+      S_CHECK(s, cudaMemcpyAsync(s->d_pos + first * 3, pos.data(), sizeof(float) * pos.size(), cudaMemcpyHostToDevice,
+                                 st));
+    S_CHECK(s, cudaStreamSynchronize(st));  // host staging vectors go out of scope
+    S_CHECK(s, cudaFreeAsync(d_nb, st));
+    S_CHECK(s, cudaFreeAsync(d_keys, st));
+    S_CHECK(s, cudaFreeAsync(d_home, st));
+    S_CHECK(s, cudaFreeAsync(d_pairs, st));
+  }
+  // pool-sized scratch (the pool may have grown by the newborns)
+  const int64_t ps = std::max<int64_t>(s->size, 1);
+  if (s->dv_pool_cap < ps) {
+    if (s->dv_present) cudaFree(s->dv_present);
+    S_CHECK(s, grow64(s->dv_fetch, ps + ps / 4));
+    S_CHECK(s, cudaMalloc(&s->dv_present, ps + ps / 4));
+    s->dv_pool_cap = ps + ps / 4;
+  }
+  S_CHECK(s, ensure_blocks(s->size));
+  // prune in-radius tracked entries, mark their records present; kept rows (row order)
+  const float r2 = radius * radius;
+  S_CHECK(s, cudaMemsetAsync(s->dv_present, 0, ps, st));
+  if (n > 0) {
+    prune_kernel<<<grid_of(n), 256, 0, st>>>(d_active, s->dv_res, n, rs, center[0], center[1], center[2], r2, d_kept,
+                                             s->dv_present);
+    sel_count_kernel<<<(unsigned)nbn, kScanBlock, 0, st>>>(2, n, nullptr, nullptr, d_kept, s->dv_cnt);
+    block_scan_kernel<<<1, 1024, 0, st>>>(s->dv_cnt, nbn, s->dv_counts + 2);
+    sel_emit_kernel<<<(unsigned)nbn, kScanBlock, 0, st>>>(2, n, nullptr, nullptr, d_kept, s->dv_cnt, s->dv_rows2,
+                                                          nullptr);
+    count_launch(4);
+  }
+  // fetch: not-present in-radius records, ascending index
+  if (s->size > 0) {
+    const latmap_status rc = radius_compact(s, center, r2, s->dv_present, s->dv_fetch, s->dv_counts + 3);
+    if (rc != LATMAP_OK) return rc;
+  }
+  // assemble (nothing written when the output capacity is too small)
+  if (d_out && cap > 0) {
+    assemble_kernel<<<grid_of((n + s->size) * rs), 256, 0, st>>>(d_active, s->dv_rows2, s->dv_res, s->pool_dev,
+                                                                 s->dv_fetch, s->dv_counts + 2, cap, rs, d_out,
+                                                                 d_out_origin);
+    count_launch();
+  }
+  S_CHECK(s, cudaMemcpyAsync(s->h_counts, s->dv_counts, sizeof(int64_t) * 4, cudaMemcpyDeviceToHost, st));
+  S_CHECK(s, cudaStreamSynchronize(st));
+  const int64_t nk = s->h_counts[2], fetched = s->h_counts[3];
+  st5[3] = (n - nnb + ins) - nk;
+  st5[4] = fetched;
+  *out_count = nk + fetched;
+  if (stats_out) std::memcpy(stats_out, st5, sizeof(st5));
+  latmap_status ret = LATMAP_OK;
+  if (nk + fetched > cap) ret = sfail(s, LATMAP_ERR_INVALID_ARGUMENT, "sync: output capacity too small");
+  if (nwb > 0) {  // written-back rows to the pinned pool over PCIe, overlapping the caller's next work
+    S_CHECK(s, cudaEventRecord(s->wb_ev, st));
+    S_CHECK(s, cudaStreamWaitEvent(s->wb_st, s->wb_ev, 0));
+    scatter_rec_dev_kernel<<<grid_of(nwb * rs / 2), 256, 0, s->wb_st>>>(s->pool_dev, s->dv_wb_idx, s->dv_counts + 0,
+                                                                       rs, s->dv_wb_tmp);
+    count_launch();
+    S_CHECK(s, cudaEventRecord(s->wb_ev, s->wb_st));
+    s->wb_pending = true;
+  }
+  return ret;
+}
+
+
+// fetch_local with device outputs (d_origin: ascending record indices, d_records optional AoS
+// gather) and the store's persistent scratch: the radius scan (count, scan, emit) and one count
+// readback. *count = hits (also when > cap: nothing is written then).
+latmap_status latmap_store_fetch_local_device(latmap_store* s, const float center[3], float radius, int64_t* d_origin,
+                                              int64_t cap, float* d_records, int64_t* count) {
+  if (!s || !center || (!count && (d_origin || d_records))) return LATMAP_ERR_INVALID_ARGUMENT;
+  if (!(radius > 0.f)) return sfail(s, LATMAP_ERR_INVALID_ARGUMENT, "fetch_local: radius must be > 0");
+  wb_wait(s);
+  if (count) *count = 0;
+  if (s->size == 0) return LATMAP_OK;
+  cudaStream_t st = s->st;
+  const int64_t ps = s->size;
+  if (!s->dv_counts) {
+    S_CHECK(s, cudaMalloc(&s->dv_counts, sizeof(int64_t) * 8));
+    S_CHECK(s, cudaHostAlloc(&s->h_counts, sizeof(int64_t) * 8, 0));
+  }
+  const int64_t nb = compact_blocks(ps);
+  if (s->dv_cnt_cap < nb + 1) {
+    if (s->dv_cnt) cudaFree(s->dv_cnt);
+    s->dv_cnt_cap = nb + 1 + nb / 4;
+    S_CHECK(s, cudaMalloc(&s->dv_cnt, sizeof(int32_t) * s->dv_cnt_cap));
+  }
+  if (s->dv_pool_cap < ps) {
+    if (s->dv_present) cudaFree(s->dv_present);
+    if (s->dv_fetch) cudaFree(s->dv_fetch);
+    S_CHECK(s, cudaMalloc(&s->dv_fetch, sizeof(int64_t) * (ps + ps / 4)));
+    S_CHECK(s, cudaMalloc(&s->dv_present, ps + ps / 4));
+    s->dv_pool_cap = ps + ps / 4;
+  }
+  const float r2 = radius * radius;
+  // emit straight into the caller's buffer when it can hold every record, else into scratch
+  int64_t* out = d_origin && cap >= ps ? d_origin : s->dv_fetch;
+  {
+    const latmap_status rc = radius_compact(s, center, r2, nullptr, out, s->dv_counts + 4);
+    if (rc != LATMAP_OK) return rc;
+  }
+  if (!count) return LATMAP_OK;  // scan only: the count stays on the device (timing)
+  S_CHECK(s, cudaMemcpyAsync(s->h_counts + 4, s->dv_counts + 4, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  S_CHECK(s, cudaStreamSynchronize(st));
+  const int64_t total = s->h_counts[4];
+  *count = total;
+  if (d_origin && total > cap) return sfail(s, LATMAP_ERR_INVALID_ARGUMENT, "fetch_local: output capacity too small");
+  if (d_origin && out != d_origin && total > 0)
+    S_CHECK(s, cudaMemcpyAsync(d_origin, out, sizeof(int64_t) * total, cudaMemcpyDeviceToDevice, st));
+  if (d_records && total > 0) {
+    gather_kernel<<<grid_of(total * s->rs), 256, 0, st>>>(s->pool_dev, out, total, s->rs, d_records);
+    count_launch();
+  }
+  return LATMAP_OK;
 }
 
 }  // extern "C"

@@ -199,3 +199,123 @@ def test_session_dictionary_dump_round_trip(ctx, tmp_path):
     a2, p2 = s2.get_dictionary()
     assert np.array_equal(a2, atoms) and np.array_equal(p2, proj)
     assert np.array_equal(s2.get_anchor(), anchor) and np.array_equal(s2.dict_weights(), s1.dict_weights())
+
+
+def test_sync_device_matches_host_sync(ctx):
+    """latmap_store_sync_device (per-row arrays on the device, device compactions) against the host
+    sync on the same sequence: outputs, origins, kept masks, stats and the stored records bit for
+    bit, with newborns (some rejected), tracked moves across voxels and a drifting centre; one
+    frame with every row dirty (d_dirty = None)."""
+    rng = np.random.default_rng(5)
+    a, b = api.Store(ctx, 1 << 16, 4), api.Store(ctx, 1 << 16, 4)
+    base = recs(rng, 4000)
+    a.insert_global(base, 0.05)
+    b.insert_global(base, 0.05)
+    center = np.zeros(3, np.float32)
+    org, act_t = a.fetch_local(center, 1.0, gather=True)
+    b.fetch_local(center, 1.0)
+    act = act_t.cpu().numpy()
+    for step in range(6):
+        act = act.copy()
+        moved = rng.random(len(act)) < 0.3
+        act[moved, :3] += rng.normal(0, 0.05, (moved.sum(), 3)).astype(np.float32)
+        act[moved, 7:] += 0.1
+        dirty = moved.astype(np.uint8)
+        nb = 0 if step == 2 else 60
+        if nb:
+            born = recs(rng, nb, extent=1.5)
+            born[:10, :3] = act[:10, :3]
+            act = np.concatenate([act, born])
+            org = np.concatenate([org, -np.ones(nb, np.int64)])
+            dirty = np.concatenate([dirty, np.ones(nb, np.uint8)])
+        all_dirty = step == 4
+        if all_dirty:
+            dirty = np.ones(len(org), np.uint8)
+        center = (center + rng.normal(0, 0.3, 3)).astype(np.float32)
+        d_act = torch.as_tensor(act, device="cuda")
+        h_out, h_org, h_kept, h_st = a.sync(d_act, org, dirty, center, 1.0, 0.05)
+        d_out, d_org, d_kept, d_st = b.sync_device(d_act, torch.as_tensor(org, device="cuda"),
+                                                   None if all_dirty else torch.as_tensor(dirty, device="cuda"),
+                                                   center, 1.0, 0.05)
+        assert d_st == h_st, (step, d_st, h_st)
+        assert np.array_equal(d_org.cpu().numpy(), h_org)
+        assert np.array_equal(d_kept.cpu().numpy().astype(bool), h_kept)
+        assert np.array_equal(d_out.cpu().numpy().view(np.uint32), h_out.cpu().numpy().view(np.uint32))
+        assert a.size() == b.size()
+        assert np.array_equal(a.records()[0].view(np.uint32), b.records()[0].view(np.uint32))
+        act, org = h_out.cpu().numpy(), h_org
+
+
+def test_import_rows_device_matches_host(ctx):
+    """Session.import_rows_device (kept mask on the device) == import_rows (host mask): in
+    deterministic mode, one Stage-I step, the row import, and a second step (whose Adam update
+    depends on the carried moments) give bit-identical maps. Also: deterministic mode switched on
+    after a graph-captured step (its scratch must be sized outside the re-capture)."""
+    from paper_2602_12314_b200 import synthetic
+
+    st = synthetic.make_streaming(n_global=1_000_000, nframes=1, scale=0.1, device="cuda")
+    intr = api.make_intrinsics(st.intr.fx, st.intr.fy, st.intr.cx, st.intr.cy, st.intr.width, st.intr.height)
+    store = api.Store(ctx, st.capacity, 32)
+    store.insert_global(st.records, st.voxel_size)
+    q, t = st.poses[0]
+    org, rows = store.fetch_local(np.asarray(t, np.float32), st.radius, gather=True)
+    gm = api.GaussianMap(rows[:, 0:3].contiguous(), rows[:, 3:7].contiguous(), rows[:, 7:10].contiguous(),
+                         rows[:, 10:13].contiguous(), rows[:, 13].contiguous(), rows[:, 14:].contiguous())
+    out = api.render(ctx, gm, api.make_pose(q, t), intr)
+    frame = synthetic.Frame(q, t, out.color.cpu().numpy() * 0.9, out.depth.cpu().numpy(), st.assignments[0],
+                            st.features[0])
+    cfg = api.default_config(**st.lambdas)
+    rng = np.random.default_rng(1)
+    kept = rng.random(len(org)) < 0.7
+    new_rows = torch.cat([rows[torch.as_tensor(kept, device="cuda")], rows[:100]]).contiguous()
+    res = []
+    for dev in (False, True):
+        s = api.Session(ctx, cfg, 0, 32, 256, 1024, intr)
+        s.set_dictionary(st.atoms, st.atoms, st.proj)
+        s.import_rows(rows.contiguous())
+        s.set_frames([frame])
+        s.set_batch(1)
+        ctx.set_deterministic(True)
+        try:
+            s.step(read=True)
+            s.step(read=True)  # graph-captured
+            if dev:
+                s.import_rows_device(new_rows, torch.as_tensor(kept, device="cuda"), int(kept.sum()))
+            else:
+                s.import_rows(new_rows, kept=kept)
+            s.step(read=True)
+            s.step(read=True)
+        finally:
+            ctx.set_deterministic(False)
+        res.append(s.params_buffer().clone())
+        del s
+    assert torch.equal(res[0], res[1])
+    # deterministic mode switched on after a graph-captured step: the fixed-order scratch is sized
+    # before the re-capture (an allocation inside a capture fails)
+    s = api.Session(ctx, cfg, 0, 32, 256, 1024, intr)
+    s.set_dictionary(st.atoms, st.atoms, st.proj)
+    s.import_rows(rows.contiguous())
+    s.set_frames([frame])
+    s.set_batch(1)
+    s.step(read=True)
+    s.step(read=True)
+    ctx.set_deterministic(True)
+    try:
+        assert np.isfinite(s.step(read=True)["total"])
+    finally:
+        ctx.set_deterministic(False)
+
+
+def test_fetch_local_device_matches_host(ctx):
+    """fetch_local_device (single-pass look-back compaction) == fetch_local: the ascending record
+    list and the gathered records, over a 300k-record store at several radii (block boundaries,
+    empty and full results)."""
+    rng = np.random.default_rng(9)
+    s = api.Store(ctx, 1 << 20, 4)
+    s.insert_global(recs(rng, 300_000, extent=4.0), 0.01)
+    for radius in (0.05, 0.7, 2.0, 100.0):
+        c = rng.normal(0, 1, 3).astype(np.float32)
+        h_org, h_rec = s.fetch_local(c, radius, gather=True)
+        d_org, d_rec = s.fetch_local_device(c, radius, gather=True)
+        assert np.array_equal(d_org.cpu().numpy(), h_org), radius
+        assert torch.equal(d_rec, h_rec), radius
