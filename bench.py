@@ -97,6 +97,20 @@ def ncu_traffic():
     return out
 
 
+def ncu_warp_instructions():
+    """Executed warp instructions per launch of each phase's kernels (same capture), or {}."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            k = json.load(f)["kernels"]
+    except Exception:
+        return {}
+    out = {}
+    for v in k.values():
+        if v.get("phase") and v.get("warp_instructions_per_launch"):
+            out[v["phase"]] = out.get(v["phase"], 0.0) + v["warp_instructions_per_launch"]
+    return out
+
+
 # ----------------------------------------------------------------------------- workload
 def gpu_render_fn(ctx):
     import torch
@@ -736,6 +750,14 @@ def main():
             roof = {"kernel": dom, "bound": "hbm", "achieved": by / t_launch / 1e9, "peak": hbm, "unit": "GB/s",
                     "frac": by / t_launch / 1e9 / hbm, "traffic": traffic.get(dom), "algorithmic_per_launch": by,
                     "peak_source": f"{src} HBM copy"}
+            wi = ncu_warp_instructions().get(dom) if args.config == 2 else None
+            if wi:  # the rasteriser is issue-bound: its instruction issue rate against the SMs' peak
+                clk = (clocks or {}).get("sm_mhz") or 1965.0
+                peak_i = 148 * 4 * clk * 1e6  # one warp instruction per scheduler per clock
+                roof["issue"] = {"warp_instructions_per_launch": wi, "achieved": wi / t_launch, "peak": peak_i,
+                                 "unit": "warp instructions/s", "frac": wi / t_launch / peak_i,
+                                 "source": "smsp__inst_executed.sum of the committed ncu --set full capture "
+                                           "(profiles/ncu_traffic.json); time per launch measured live"}
         else:
             roof = {"kernel": dom, "bound": "hbm", "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None,
                     "traffic": None}

@@ -1,4 +1,5 @@
-"""Per-launch DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum) of the step's kernels from
+"""Per-launch DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum) and executed warp
+instructions (smsp__inst_executed.sum) of the step's kernels from
 ncu --set full reports -> profiles/ncu_traffic.json, read by bench.py for the roofline `traffic` key.
 
   python tools/ncu_traffic.py OUT.json REPORT.ncu-rep [REPORT.ncu-rep ...]
@@ -30,11 +31,13 @@ def main():
                 b += float(d[k]) * scale[dict(zip(h, units))[k]]
             tu = dict(zip(h, units))["gpu__time_duration.sum"]
             us = float(d["gpu__time_duration.sum"]) * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}[tu]
-            per_kernel.setdefault(name, []).append((b, us))
+            wi = float(d.get("smsp__inst_executed.sum", "0") or 0)
+            per_kernel.setdefault(name, []).append((b, us, wi))
     res = {"source": reps, "kernels": {}}
     for name, v in per_kernel.items():
         res["kernels"][name] = {"bytes_per_launch": sum(x[0] for x in v) / len(v),
                                 "ncu_us_per_launch": sum(x[1] for x in v) / len(v), "launches": len(v),
+                                "warp_instructions_per_launch": sum(x[2] for x in v) / len(v),
                                 "phase": next((p for k, p in PHASE.items() if k in name), None)}
     json.dump(res, open(out, "w"), indent=1)
     print(json.dumps(res["kernels"], indent=1))
