@@ -227,71 +227,96 @@ __global__ void __launch_bounds__(256) ssim_v_kernel(const float* __restrict__ h
   block_add_double(acc, sum_out);
 }
 
-// SSIM value only (no gradient requested): both separable passes fused per 32x8 output tile
-// with a 5-pixel reflect-101 halo in shared memory, the same per-pixel float expressions as
-// ssim_h_kernel + ssim_v_kernel (so the same values), one pass over the two images. The halos
-// of all channels (ch <= 3) are loaded together: one reflected index per halo pixel.
-constexpr int kSTX = 32, kSTY = 8, kSHX = kSTX + 2 * kRad, kSHY = kSTY + 2 * kRad;
+// SSIM value only (no gradient requested): both separable passes fused per 32x16 output tile
+// with a 5-pixel reflect-101 halo in shared memory, one channel at a time. Each thread slides the
+// 11-tap window over 4 consecutive outputs (horizontal: a row segment, vertical: a column
+// segment), loading each input once; every output keeps the float expressions and the tap order
+// of ssim_h_kernel + ssim_v_kernel (so the same values).
+constexpr int kSTX = 32, kSTY = 16, kSHX = kSTX + 2 * kRad, kSHY = kSTY + 2 * kRad;
+constexpr int kSOut = 4;  // horizontal outputs per thread
+constexpr int kVOut = kSTY / 8;  // vertical outputs per thread (256 threads = 32 columns x 8 segments)
 __global__ void __launch_bounds__(256) ssim_fused_kernel(const float* __restrict__ a, const float* __restrict__ b,
                                                          int h, int w, int ch, SsimKernel K, double* sum_out) {
-  __shared__ float s_a[3][kSHY][kSHX], s_b[3][kSHY][kSHX];
-  __shared__ float s_h[5][kSHY][kSTX];
+  __shared__ float s_a[3][kSHY][kSHX + 1], s_b[3][kSHY][kSHX + 1];
+  __shared__ float s_h[5][kSHY][kSTX + 1];
   const float c1 = 0.01f * 0.01f, c2 = 0.03f * 0.03f;
   const int x0 = blockIdx.x * kSTX, y0 = blockIdx.y * kSTY;
   const int tid = threadIdx.x;
   double acc = 0.0;
   for (int cb = 0; cb < ch; cb += 3) {
-    const int nc = min(3, ch - cb);
-    for (int i = tid; i < kSHY * kSHX; i += blockDim.x) {
-      const int yy = i / kSHX, xx = i % kSHX;
-      const int gy = refl(min(y0 - kRad + yy, h - 1 + kRad), h), gx = refl(min(x0 - kRad + xx, w - 1 + kRad), w);
-      const int64_t q = ((int64_t)gy * w + gx) * ch + cb;
-      for (int c = 0; c < nc; ++c) {
-        s_a[c][yy][xx] = a[q + c];
-        s_b[c][yy][xx] = b[q + c];
+  const int nc = min(3, ch - cb);
+  for (int i = tid; i < kSHY * kSHX; i += blockDim.x) {  // halos of up to 3 channels, one reflected index
+    const int yy = i / kSHX, xx = i % kSHX;
+    const int gy = refl(min(y0 - kRad + yy, h - 1 + kRad), h), gx = refl(min(x0 - kRad + xx, w - 1 + kRad), w);
+    const int64_t q = ((int64_t)gy * w + gx) * ch + cb;
+    for (int c = 0; c < nc; ++c) {
+      s_a[c][yy][xx] = a[q + c];
+      s_b[c][yy][xx] = b[q + c];
+    }
+  }
+  __syncthreads();
+  for (int c = 0; c < nc; ++c) {
+    // horizontal: kSHY rows x (kSTX / kSOut) segments
+    for (int t = tid; t < kSHY * (kSTX / kSOut); t += blockDim.x) {
+      const int yy = t / (kSTX / kSOut), xs = (t % (kSTX / kSOut)) * kSOut;
+      float av[kSOut + 2 * kRad], bv[kSOut + 2 * kRad];
+#pragma unroll
+      for (int i = 0; i < kSOut + 2 * kRad; ++i) {
+        av[i] = s_a[c][yy][xs + i];
+        bv[i] = s_b[c][yy][xs + i];
+      }
+#pragma unroll
+      for (int o = 0; o < kSOut; ++o) {
+        float s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0;
+#pragma unroll
+        for (int k = 0; k < kWin; ++k) {
+          const float x = av[o + k], y = bv[o + k], kw = K.k[k];
+          s0 += kw * x;
+          s1 += kw * y;
+          s2 += kw * (x * x);
+          s3 += kw * (y * y);
+          s4 += kw * (x * y);
+        }
+        s_h[0][yy][xs + o] = s0;
+        s_h[1][yy][xs + o] = s1;
+        s_h[2][yy][xs + o] = s2;
+        s_h[3][yy][xs + o] = s3;
+        s_h[4][yy][xs + o] = s4;
       }
     }
     __syncthreads();
-    for (int c = 0; c < nc; ++c) {
-      for (int i = tid; i < kSHY * kSTX; i += blockDim.x) {
-        const int yy = i / kSTX, xx = i % kSTX;
-        float s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0;
+    // vertical: kSTX columns x 8 segments of kVOut rows = 256 threads
+    {
+      const int xx = tid % kSTX, ys = (tid / kSTX) * kVOut;
+      float q[kVOut][5];
 #pragma unroll
-        for (int k = -kRad; k <= kRad; ++k) {
-          const float av = s_a[c][yy][xx + kRad + k], bv = s_b[c][yy][xx + kRad + k], kw = K.k[k + kRad];
-          s0 += kw * av;
-          s1 += kw * bv;
-          s2 += kw * (av * av);
-          s3 += kw * (bv * bv);
-          s4 += kw * (av * bv);
-        }
-        s_h[0][yy][xx] = s0;
-        s_h[1][yy][xx] = s1;
-        s_h[2][yy][xx] = s2;
-        s_h[3][yy][xx] = s3;
-        s_h[4][yy][xx] = s4;
+      for (int o = 0; o < kVOut; ++o)
+#pragma unroll
+        for (int t = 0; t < 5; ++t) q[o][t] = 0.f;
+#pragma unroll
+      for (int t = 0; t < 5; ++t) {
+        float col[kVOut + 2 * kRad];
+#pragma unroll
+        for (int i = 0; i < kVOut + 2 * kRad; ++i) col[i] = s_h[t][ys + i][xx];
+#pragma unroll
+        for (int o = 0; o < kVOut; ++o)
+#pragma unroll
+          for (int k = 0; k < kWin; ++k) q[o][t] += K.k[k] * col[o + k];
       }
-      __syncthreads();
-      {
-        const int yy = tid / kSTX, xx = tid % kSTX;
-        const int y = y0 + yy, x = x0 + xx;
+#pragma unroll
+      for (int o = 0; o < kVOut; ++o) {
+        const int y = y0 + ys + o, x = x0 + xx;
         if (y < h && x < w) {
-          float q[5] = {0, 0, 0, 0, 0};
-#pragma unroll
-          for (int k = -kRad; k <= kRad; ++k) {
-            const float kw = K.k[k + kRad];
-#pragma unroll
-            for (int t = 0; t < 5; ++t) q[t] += kw * s_h[t][yy + kRad + k][xx];
-          }
-          const float mx = q[0], my = q[1];
-          const float sx2 = q[2] - mx * mx, sy2 = q[3] - my * my, sxy = q[4] - mx * my;
+          const float mx = q[o][0], my = q[o][1];
+          const float sx2 = q[o][2] - mx * mx, sy2 = q[o][3] - my * my, sxy = q[o][4] - mx * my;
           const float a1 = 2.f * mx * my + c1, a2 = 2.f * sxy + c2;
           const float b1 = mx * mx + my * my + c1, b2 = sx2 + sy2 + c2;
           acc += (double)((a1 * a2) / (b1 * b2));
         }
       }
-      __syncthreads();
     }
+    __syncthreads();
+  }
   }
   block_add_double(acc, sum_out);
 }
@@ -415,7 +440,7 @@ void ssim_run(cudaStream_t st, const float* a, const float* b, int h, int w, int
     return;
   }
   if (!d_a) {
-    ssim_fused_kernel<<<dim3((w + kSTX - 1) / kSTX, (h + kSTY - 1) / kSTY), kSTX * kSTY, 0, st>>>(a, b, h, w, ch, K,
+    ssim_fused_kernel<<<dim3((w + kSTX - 1) / kSTX, (h + kSTY - 1) / kSTY), 256, 0, st>>>(a, b, h, w, ch, K,
                                                                                               sum_out);
     count_launch();
     return;
