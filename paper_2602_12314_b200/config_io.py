@@ -9,6 +9,10 @@ and then rounded to float32, where ``std::stof`` rounds the text directly. The t
 """
 from __future__ import annotations
 
+import math
+import re
+from fractions import Fraction
+
 import numpy as np
 
 from ._capi import InvalidArgument
@@ -39,14 +43,95 @@ def default_config() -> dict:
     return {n: (float(np.float32(d)) if k == "float" else d) for n, k, d in FIELDS}
 
 
+_DEC = re.compile(r"[+-]?(\d+\.?\d*|\.\d+)([eE][+-]?\d+)?")
+_HEX = re.compile(r"[+-]?0[xX]([0-9a-fA-F]+\.?[0-9a-fA-F]*|\.[0-9a-fA-F]+)([pP][+-]?\d+)?")
+_SPECIAL = re.compile(r"[+-]?(inf|infinity|nan(\([0-9A-Za-z_]*\))?)", re.IGNORECASE)
+_FLT_MIN = 2.0 ** -126
+
+
+def _exact_value(v):
+    """The exact rational value of a decimal or hexadecimal strtof literal."""
+    if _HEX.fullmatch(v):
+        sign = -1 if v[0] == "-" else 1
+        body = v.lstrip("+-")[2:]
+        mant, _, exp = body.partition("p") if "p" in body else body.partition("P")
+        ip, _, fp = mant.partition(".")
+        digits = (ip or "0") + fp
+        return sign * Fraction(int(digits, 16), 16 ** len(fp)) * Fraction(2) ** int(exp or "0")
+    return Fraction(v)
+
+
+def _round_f32(f):
+    """Round an exact rational to the nearest float32, ties to even (strtof's result); +-inf past
+    the rounding boundary of FLT_MAX."""
+    big = Fraction(2) ** 128  # the next "float" past FLT_MAX, for the rounding decision
+    mag = abs(f)
+    fmax = Fraction(float(np.finfo(np.float32).max))
+    if mag > fmax:
+        mid = (fmax + big) / 2
+        r = math.inf if mag >= mid else float(fmax)  # a tie rounds to the even side: 2^128
+        return -r if f < 0 else r
+    d = float(mag)  # correctly rounded to double
+    with np.errstate(over="ignore"):
+        r = float(np.float32(d))
+    if r != d:  # double rounding is only possible on a float32 midpoint: decide on the exact value
+        nb = float(np.nextafter(np.float32(r), np.float32(0) if r > d else np.float32(np.finfo(np.float32).max)))
+        a, b = (nb, r) if nb < r else (r, nb)
+        mid = (Fraction(a) + Fraction(b)) / 2
+        if mag < mid:
+            r = a
+        elif mag > mid:
+            r = b
+        else:
+            r = a if int(np.float32(a).view(np.uint32)) % 2 == 0 else b
+    return -r if f < 0 else r
+
+
+def parse_float(v):
+    """std::stof with the whole string consumed (config.cpp:28-33), as glibc strtof parses it:
+    leading whitespace, decimal and hexadecimal literals, inf / infinity / nan(...). Raises
+    std::out_of_range (OverflowError) when the value overflows float, or when it rounds inexactly
+    to a subnormal or zero (strtof's ERANGE; checked against this image's std::stof)."""
+    t = v.lstrip(" \t\n\v\f\r")
+    if _SPECIAL.fullmatch(t):
+        return float(np.float32(float(t.lower().split("(")[0])))
+    if not (_DEC.fullmatch(t) or _HEX.fullmatch(t)):
+        raise InvalidArgument(f"bad float value '{v}'")
+    f = _exact_value(t)
+    if f == 0:
+        return -0.0 if t.startswith("-") else 0.0
+    r = _round_f32(f)
+    if not math.isfinite(r):
+        raise OverflowError(f"float value out of range '{v}'")  # std::out_of_range
+    if abs(r) < _FLT_MIN:
+        # underflow (ERANGE) when the subnormal result is inexact. glibc's hexadecimal path first
+        # forms a 24-bit mantissa (round bit = the 25th bit, sticky = anything beyond) and then
+        # tests only the mantissa bits shifted out below 2^-149 and the sticky bit -- not that
+        # round bit (measured: 0x1.000001p-149 parses, 0x1.00000000001p-149 is out of range)
+        if _HEX.fullmatch(t):
+            mag = abs(f)
+            e = mag.numerator.bit_length() - mag.denominator.bit_length()
+            if Fraction(2) ** e > mag:
+                e -= 1
+            elif Fraction(2) ** (e + 1) <= mag:
+                e += 1
+            unit = Fraction(2) ** (e - 23)
+            m24 = int(mag / unit)
+            rem = mag - m24 * unit
+            sticky = rem != 0 and rem != unit / 2
+            drop = -126 - e
+            dropped = m24 if drop >= 24 else m24 % (1 << drop) if drop > 0 else 0
+            inexact = dropped != 0 or sticky
+        else:
+            inexact = Fraction(r) != f
+        if inexact:
+            raise OverflowError(f"float value out of range '{v}'")  # std::out_of_range
+    return r
+
+
 def _parse(kind, v):
     if kind == "float":
-        try:
-            if "_" in v:
-                raise ValueError
-            return float(np.float32(float(v)))
-        except ValueError:
-            raise InvalidArgument(f"bad float value '{v}'") from None
+        return parse_float(v)
     if kind in _RANGE:
         try:
             if "_" in v:
