@@ -12,7 +12,9 @@
 // order, no FMA) over the whole pool mirror with an order-preserving compaction, and the
 // gather reads the selected records from mapped host memory straight into device buffers;
 // the writeback scatter writes device records back into the pinned pool.
+#include <algorithm>
 #include <chrono>
+#include <functional>
 #include <cstdio>
 #include <cstdlib>
 
@@ -781,6 +783,30 @@ latmap_status latmap_store_sync(latmap_store* s, const float* d_active, const in
   float* wb_tmp = nullptr;
   int64_t* wb_idx_dev = nullptr;
   int64_t wb_n = 0;
+  // every device temporary of this call, and an exit guard: an error return launches the
+  // deferred pool writeback (the position mirror already holds those rows) and frees what is
+  // still allocated, then synchronizes, so the pool, the mirror and h_stage stay consistent
+  std::vector<void*> live;
+  auto amalloc = [&](auto** p, size_t bytes) {
+    const cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(p), bytes, s->st);
+    if (e == cudaSuccess) live.push_back(*p);
+    return e;
+  };
+  auto afree = [&](void* p) {
+    live.erase(std::remove(live.begin(), live.end(), p), live.end());
+    return cudaFreeAsync(p, s->st);
+  };
+  struct ExitGuard {
+    std::function<void()> f;
+    ~ExitGuard() {
+      if (f) f();
+    }
+  } guard{[&]() {
+    if (wb_n > 0 && wb_tmp && wb_idx_dev)
+      scatter_rec_kernel<<<grid_of(wb_n * rs / 2), 256, 0, s->st>>>(s->pool_dev, wb_idx_dev, wb_n, rs, wb_tmp);
+    for (void* p : live) cudaFreeAsync(p, s->st);
+    cudaStreamSynchronize(s->st);
+  }};
   for (int64_t i = 0; i < n; ++i) {
     if (origin[i] >= 0) {
       resolved[i] = origin[i];
@@ -795,9 +821,9 @@ latmap_status latmap_store_sync(latmap_store* s, const float* d_active, const in
   int64_t *d_rows = nullptr, *d_idx2 = nullptr;
   if (nwb > 0) {
     float* d_tmp = nullptr;
-    S_CHECK(s, cudaMallocAsync(&d_rows, sizeof(int64_t) * nwb, s->st));
-    S_CHECK(s, cudaMallocAsync(&d_idx2, sizeof(int64_t) * nwb, s->st));
-    S_CHECK(s, cudaMallocAsync(&d_tmp, sizeof(float) * nwb * rs, s->st));
+    S_CHECK(s, amalloc(&d_rows, sizeof(int64_t) * nwb));
+    S_CHECK(s, amalloc(&d_idx2, sizeof(int64_t) * nwb));
+    S_CHECK(s, amalloc(&d_tmp, sizeof(float) * nwb * rs));
     S_CHECK(s, cudaMemcpyAsync(d_rows, wb_rows, sizeof(int64_t) * nwb, cudaMemcpyHostToDevice, s->st));
     S_CHECK(s, cudaMemcpyAsync(d_idx2, wb_idx, sizeof(int64_t) * nwb, cudaMemcpyHostToDevice, s->st));
     copy_rows_kernel<<<grid_of(nwb * rs), 256, 0, s->st>>>(d_active, d_rows, nwb, rs, d_tmp);
@@ -806,7 +832,7 @@ latmap_status latmap_store_sync(latmap_store* s, const float* d_active, const in
     // written back ones: those are present or pruned)
     pos_scatter_kernel<<<grid_of(nwb * 3), 256, 0, s->st>>>(s->d_pos, d_idx2, nwb, rs, d_tmp);
     count_launch(2);
-    S_CHECK(s, cudaFreeAsync(d_rows, s->st));
+    S_CHECK(s, afree(d_rows));
     wb_tmp = d_tmp, wb_idx_dev = d_idx2, wb_n = nwb;  // pool rows: launched when this sync is done
     st5[0] = nwb;
   }
@@ -816,10 +842,10 @@ latmap_status latmap_store_sync(latmap_store* s, const float* d_active, const in
     float* d_nb = nullptr;
     int32_t* d_keys = nullptr;
     int64_t* d_home = nullptr;
-    S_CHECK(s, cudaMallocAsync(&d_rows, sizeof(int64_t) * nnb, s->st));
-    S_CHECK(s, cudaMallocAsync(&d_nb, sizeof(float) * nnb * rs, s->st));
-    S_CHECK(s, cudaMallocAsync(&d_keys, sizeof(int32_t) * nnb * 3, s->st));
-    S_CHECK(s, cudaMallocAsync(&d_home, sizeof(int64_t) * nnb, s->st));
+    S_CHECK(s, amalloc(&d_rows, sizeof(int64_t) * nnb));
+    S_CHECK(s, amalloc(&d_nb, sizeof(float) * nnb * rs));
+    S_CHECK(s, amalloc(&d_keys, sizeof(int32_t) * nnb * 3));
+    S_CHECK(s, amalloc(&d_home, sizeof(int64_t) * nnb));
     S_CHECK(s, cudaMemcpyAsync(d_rows, nb_rows.data(), sizeof(int64_t) * nnb, cudaMemcpyHostToDevice, s->st));
     copy_rows_kernel<<<grid_of(nnb * rs), 256, 0, s->st>>>(d_active, d_rows, nnb, rs, d_nb);
     keys_kernel<<<grid_of(nnb), 256, 0, s->st>>>(d_nb, nnb, rs, voxel_size, s->capacity, d_keys, d_home);
@@ -847,10 +873,10 @@ latmap_status latmap_store_sync(latmap_store* s, const float* d_active, const in
     if (!pos.empty())
       S_CHECK(s, cudaMemcpyAsync(s->d_pos + first * 3, pos.data(), sizeof(float) * pos.size(), cudaMemcpyHostToDevice,
                                  s->st));
-    S_CHECK(s, cudaFreeAsync(d_nb, s->st));
-    S_CHECK(s, cudaFreeAsync(d_keys, s->st));
-    S_CHECK(s, cudaFreeAsync(d_home, s->st));
-    S_CHECK(s, cudaFreeAsync(d_rows, s->st));
+    S_CHECK(s, afree(d_nb));
+    S_CHECK(s, afree(d_keys));
+    S_CHECK(s, afree(d_home));
+    S_CHECK(s, afree(d_rows));
   }
   tmark("newborns");
   // ---- step 2: prune in-radius tracked entries, mark their records present
@@ -858,12 +884,12 @@ latmap_status latmap_store_sync(latmap_store* s, const float* d_active, const in
   uint8_t* d_present = nullptr;
   uint8_t* d_kept = nullptr;
   int64_t* d_res = nullptr;
-  S_CHECK(s, cudaMallocAsync(&d_present, std::max<int64_t>(s->size, 1), s->st));
+  S_CHECK(s, amalloc(&d_present, std::max<int64_t>(s->size, 1)));
   S_CHECK(s, cudaMemsetAsync(d_present, 0, std::max<int64_t>(s->size, 1), s->st));
   std::vector<uint8_t> kept((size_t)std::max<int64_t>(n, 1), 0);
   if (n > 0) {
-    S_CHECK(s, cudaMallocAsync(&d_kept, n, s->st));
-    S_CHECK(s, cudaMallocAsync(&d_res, sizeof(int64_t) * n, s->st));
+    S_CHECK(s, amalloc(&d_kept, n));
+    S_CHECK(s, amalloc(&d_res, sizeof(int64_t) * n));
     S_CHECK(s, cudaMemcpyAsync(d_res, resolved, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s->st));
     prune_kernel<<<grid_of(n), 256, 0, s->st>>>(d_active, d_res, n, rs, center[0], center[1], center[2], r2, d_kept,
                                                 d_present);
@@ -876,9 +902,9 @@ latmap_status latmap_store_sync(latmap_store* s, const float* d_active, const in
   int32_t* d_cnt = nullptr;
   int64_t* d_total = nullptr;
   int64_t* d_fetch = nullptr;
-  S_CHECK(s, cudaMallocAsync(&d_cnt, sizeof(int32_t) * nb, s->st));
-  S_CHECK(s, cudaMallocAsync(&d_total, sizeof(int64_t), s->st));
-  S_CHECK(s, cudaMallocAsync(&d_fetch, sizeof(int64_t) * std::max<int64_t>(s->size, 1), s->st));
+  S_CHECK(s, amalloc(&d_cnt, sizeof(int32_t) * nb));
+  S_CHECK(s, amalloc(&d_total, sizeof(int64_t)));
+  S_CHECK(s, amalloc(&d_fetch, sizeof(int64_t) * std::max<int64_t>(s->size, 1)));
   int64_t fetched = 0;
   if (s->size > 0) {
     radius_count_kernel<<<(unsigned)nb, kScanBlock, 0, s->st>>>(s->d_pos, s->size, center[0], center[1], center[2],
@@ -912,11 +938,11 @@ latmap_status latmap_store_sync(latmap_store* s, const float* d_active, const in
     // ---- assemble: kept (original order) ++ fetched (ascending)
     if (nk > 0) {
       int64_t* d_k = nullptr;
-      S_CHECK(s, cudaMallocAsync(&d_k, sizeof(int64_t) * nk, s->st));
+      S_CHECK(s, amalloc(&d_k, sizeof(int64_t) * nk));
       S_CHECK(s, cudaMemcpyAsync(d_k, keep_rows, sizeof(int64_t) * nk, cudaMemcpyHostToDevice, s->st));
       copy_rows_kernel<<<grid_of(nk * rs), 256, 0, s->st>>>(d_active, d_k, nk, rs, d_out);
       count_launch();
-      S_CHECK(s, cudaFreeAsync(d_k, s->st));
+      S_CHECK(s, afree(d_k));
       if (out_origin)
         for (int64_t j = 0; j < nk; ++j) out_origin[j] = resolved[keep_rows[j]];
     }
@@ -929,13 +955,14 @@ latmap_status latmap_store_sync(latmap_store* s, const float* d_active, const in
     }
   }
   tmark("assemble");
-  S_CHECK(s, cudaFreeAsync(d_present, s->st));
-  if (d_kept) S_CHECK(s, cudaFreeAsync(d_kept, s->st));
-  if (d_res) S_CHECK(s, cudaFreeAsync(d_res, s->st));
-  S_CHECK(s, cudaFreeAsync(d_cnt, s->st));
-  S_CHECK(s, cudaFreeAsync(d_total, s->st));
-  S_CHECK(s, cudaFreeAsync(d_fetch, s->st));
+  S_CHECK(s, afree(d_present));
+  if (d_kept) S_CHECK(s, afree(d_kept));
+  if (d_res) S_CHECK(s, afree(d_res));
+  S_CHECK(s, afree(d_cnt));
+  S_CHECK(s, afree(d_total));
+  S_CHECK(s, afree(d_fetch));
   S_CHECK(s, cudaStreamSynchronize(s->st));
+  guard.f = nullptr;  // success: nothing to undo
   if (wb_n > 0) {
     // the written-back rows reach the pinned pool over PCIe after this sync's own transfers (which
     // would otherwise queue behind ~184 B x rows of posted writes), overlapping the caller's next
