@@ -1046,6 +1046,12 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
     }
   }
   const bool pipe = ahead && want_grad && map_grads;
+  // projection backward of every frame in one pass after the frame loop (LATMAP_PB_MULTI=0: per frame)
+  static const bool pb_multi_env = [] {
+    const char* e = std::getenv("LATMAP_PB_MULTI");
+    return !(e && e[0] == '0');
+  }();
+  const bool pb_multi = pb_multi_env && nf > 1;
   if (pipe) {
     if (!s->bstream) CTX_CHECK(ctx, cudaStreamCreateWithFlags(&s->bstream, cudaStreamNonBlocking));
     while ((int)s->evD.size() < nf) {
@@ -1149,13 +1155,31 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
       render_backward(bs, map, f.rcw, f.rwc, f.pose.translation, in, rb.w, d_col, d_dep, have_sup ? d_qry : nullptr,
                       rb.geo_acc, gmap, false, deterministic() ? &ctx->det : nullptr);
       s->end();
-      s->begin(5);
-      render_project_backward(bs, map, f.rcw, f.rwc, f.pose.translation, in, rb.w, rb.geo_acc, gmap);
-      s->end();
+      if (!pb_multi) {
+        s->begin(5);
+        render_project_backward(bs, map, f.rcw, f.rwc, f.pose.translation, in, rb.w, rb.geo_acc, gmap);
+        s->end();
+      }
       if (pipe) CTX_CHECK(ctx, cudaEventRecord(s->evB[b], s->bstream));
     }
   }
   if (pipe) CTX_CHECK(ctx, cudaStreamWaitEvent(st, s->evB[nf - 1], 0));  // join: every backward done
+  if (want_grad && map_grads && pb_multi) {
+    // K9 over all frames in one pass: parameters and gradients read once, frame order kept
+    std::vector<const float*> rcw(nf), rwc(nf), org(nf);
+    std::vector<const RenderWork*> ws(nf);
+    std::vector<float*> geo(nf);
+    for (int b = 0; b < nf; ++b) {
+      rcw[b] = s->frames[b].rcw;
+      rwc[b] = s->frames[b].rwc;
+      org[b] = s->frames[b].pose.translation;
+      ws[b] = &s->rw[b].w;
+      geo[b] = s->rw[b].geo_acc;
+    }
+    s->begin(5);
+    render_project_backward_multi(st, map, nf, rcw.data(), rwc.data(), org.data(), in, ws.data(), geo.data(), gmap);
+    s->end();
+  }
   s->renders_valid = true;
   if (want_grad) decoder_finish_tc(st, s->dec, atoms, proj, g_proj, g_atoms);
   // trust term enters once (objective.cpp:247-256)

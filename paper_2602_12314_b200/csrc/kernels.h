@@ -72,6 +72,10 @@ bool deterministic();
 void render_project_backward(cudaStream_t st, const MapPtrs& map, const float rot_cw[9], const float rot_wc[9],
                              const float origin[3], const Intr& intr, const RenderWork& w, float* geo_acc,
                              const MapPtrs& grads);
+// K9 over nf frames in one pass (frame order kept: the same gradient bits as nf K9 launches).
+void render_project_backward_multi(cudaStream_t st, const MapPtrs& map, int nf, const float* const* rot_cw,
+                                   const float* const* rot_wc, const float* const* origin, const Intr& intr,
+                                   const RenderWork* const* w, float* const* geo_acc, const MapPtrs& grads);
 
 // Image-space losses (K5). partials[...] are double accumulators (see capi.cu).
 void image_losses(cudaStream_t st, const float* color, const float* depth, const float* alpha,

@@ -1450,65 +1450,36 @@ struct ProjBwdArgs {
   float fx, fy, cx, cy;
 };
 
-// K9: projection backward (render.cpp:368-429), one thread per listed Gaussian.
-__global__ void __launch_bounds__(256, 4) project_bwd_kernel(ProjBwdArgs a) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= a.map.n) return;
-  const float4* rv = reinterpret_cast<const float4*>(a.rec + i);
-  // every load is issued before the culled test (one memory round trip instead of two; a culled
-  // Gaussian's extra bytes cost less than the serialised latency): 16-byte loads of the record,
-  // the accumulators (re-zeroed below for the next frame), the quaternion
-  const int4 bb = reinterpret_cast<const int4*>(a.rec + i)[2];
-  const float4 r0 = ld_early4(rv), r1 = ld_early4(rv + 1);
-  float4* acc4 = reinterpret_cast<float4*>(a.geo_acc + 8 * i);
-  const float4 g0 = ld_early4(acc4), g1 = ld_early4(acc4 + 1);
-  const float ac[7] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z};
-  const float pv[3] = {ld_early(a.map.pos + 3 * i), ld_early(a.map.pos + 3 * i + 1), ld_early(a.map.pos + 3 * i + 2)};
-  const float4 q4 = (reinterpret_cast<uintptr_t>(a.map.rot) & 15) == 0
-                        ? ld_early4(reinterpret_cast<const float4*>(a.map.rot) + i)
-                        : make_float4(a.map.rot[4 * i], a.map.rot[4 * i + 1], a.map.rot[4 * i + 2], a.map.rot[4 * i + 3]);
-  const float lv[3] = {ld_early(a.map.lsc + 3 * i), ld_early(a.map.lsc + 3 * i + 1), ld_early(a.map.lsc + 3 * i + 2)};
-  const float* p = pv;
-  const float q[4] = {q4.x, q4.y, q4.z, q4.w};
-  const float* ls = lv;
-  // the gradient read-modify-writes: loads issued here, independent of the math below
-  const float go = ld_early(a.grads.opa + i);
-  const float gl[3] = {ld_early(a.grads.lsc + 3 * i), ld_early(a.grads.lsc + 3 * i + 1), ld_early(a.grads.lsc + 3 * i + 2)};
-  const float gr[4] = {ld_early(a.grads.rot + 4 * i), ld_early(a.grads.rot + 4 * i + 1), ld_early(a.grads.rot + 4 * i + 2),
-                       ld_early(a.grads.rot + 4 * i + 3)};
-  const float gp[3] = {ld_early(a.grads.pos + 3 * i), ld_early(a.grads.pos + 3 * i + 1), ld_early(a.grads.pos + 3 * i + 2)};
-  // culled (empty bbox): no accumulation happened, nothing is written. The test only guards the
-  // stores, so the loads above are all in flight together (an early exit lets the compiler sink
-  // them behind it: two serialised round trips)
-  const bool vis = bb.x <= bb.y;
-  if (vis) {
-    acc4[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-    acc4[1] = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  const float d0 = p[0] - a.o[0], d1 = p[1] - a.o[1], d2 = p[2] - a.o[2];
+// One frame's projection-backward contribution of one Gaussian (render.cpp:368-429), from the
+// Gaussian's frame-independent terms (position p, normalised quaternion qh = (w, x, y, z) with its
+// norm qn, rotation rg, scales sc), the frame's record (r0 = mean, depth, alpha; r1 = cov_inv)
+// and accumulators ac = (dmean_u, dmean_v, dA00, dA01, dA11, dz, dg).
+struct PbContrib {
+  float opa, lsc[3], rot[4], pos[3];
+};
+__device__ __forceinline__ PbContrib proj_bwd_frame(const float* p, const float* qh, float qn, const float* rg,
+                                                    const float* sc, float4 r0, float4 r1, const float* ac,
+                                                    const float* rcw, const float* rwc, const float* o, float fx,
+                                                    float fy) {
+  PbContrib out;
+  const float qw = qh[0], qx = qh[1], qy = qh[2], qz = qh[3];
+  const float d0 = p[0] - o[0], d1 = p[1] - o[1], d2 = p[2] - o[2];
   float pc[3];
-  for (int r = 0; r < 3; ++r) pc[r] = a.rcw[3 * r] * d0 + a.rcw[3 * r + 1] * d1 + a.rcw[3 * r + 2] * d2;
-  const float qn = sqrtf(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
-  const float qw = q[0] / qn, qx = q[1] / qn, qy = q[2] / qn, qz = q[3] / qn;
-  float rg[9] = {1.f - 2.f * (qy * qy + qz * qz), 2.f * (qx * qy - qw * qz), 2.f * (qx * qz + qw * qy),
-                 2.f * (qx * qy + qw * qz), 1.f - 2.f * (qx * qx + qz * qz), 2.f * (qy * qz - qw * qx),
-                 2.f * (qx * qz - qw * qy), 2.f * (qy * qz + qw * qx), 1.f - 2.f * (qx * qx + qy * qy)};
-  const float sc[3] = {expf(ls[0]), expf(ls[1]), expf(ls[2])};
+  for (int r = 0; r < 3; ++r) pc[r] = rcw[3 * r] * d0 + rcw[3 * r + 1] * d1 + rcw[3 * r + 2] * d2;
   float rcg[9], m[9];
   for (int r = 0; r < 3; ++r)
     for (int c = 0; c < 3; ++c) {
-      rcg[3 * r + c] = a.rcw[3 * r] * rg[c] + a.rcw[3 * r + 1] * rg[3 + c] + a.rcw[3 * r + 2] * rg[6 + c];
+      rcg[3 * r + c] = rcw[3 * r] * rg[c] + rcw[3 * r + 1] * rg[3 + c] + rcw[3 * r + 2] * rg[6 + c];
       m[3 * r + c] = rcg[3 * r + c] * sc[c];
     }
   float cc[9];
   for (int r = 0; r < 3; ++r)
     for (int c = 0; c < 3; ++c) cc[3 * r + c] = m[3 * r] * m[3 * c] + m[3 * r + 1] * m[3 * c + 1] + m[3 * r + 2] * m[3 * c + 2];
   const float x = pc[0], y = pc[1], z = pc[2];
-  const float fx = a.fx, fy = a.fy;
   const float J[6] = {fx / z, 0.f, -fx * x / (z * z), 0.f, fy / z, -fy * y / (z * z)};
   const float A[4] = {r1.x, r1.y, r1.z, r1.w};  // cov_inv from the forward record (identical values)
   const float alpha = r0.w;
-  if (vis) a.grads.opa[i] = go + ac[6] * alpha * (1.f - alpha);
+  out.opa = ac[6] * alpha * (1.f - alpha);
   const float dA[4] = {ac[2], ac[3], ac[3], ac[4]};
   float t1[4], dc[4];
   for (int r = 0; r < 2; ++r)
@@ -1533,10 +1504,8 @@ __global__ void __launch_bounds__(256, 4) project_bwd_kernel(ProjBwdArgs a) {
   float drg[9];
   for (int r = 0; r < 3; ++r)
     for (int c = 0; c < 3; ++c)
-      drg[3 * r + c] = (a.rcw[r] * dm_[c] + a.rcw[3 + r] * dm_[3 + c] + a.rcw[6 + r] * dm_[6 + c]) * sc[c];
-  if (vis)
-    for (int c = 0; c < 3; ++c)
-      a.grads.lsc[3 * i + c] = gl[c] + (rcg[c] * dm_[c] + rcg[3 + c] * dm_[3 + c] + rcg[6 + c] * dm_[6 + c]) * sc[c];
+      drg[3 * r + c] = (rcw[r] * dm_[c] + rcw[3 + r] * dm_[3 + c] + rcw[6 + r] * dm_[6 + c]) * sc[c];
+  for (int c = 0; c < 3; ++c) out.lsc[c] = (rcg[c] * dm_[c] + rcg[3 + c] * dm_[3 + c] + rcg[6 + c] * dm_[6 + c]) * sc[c];
   const float dw[9] = {0.f, -qz, qy, qz, 0.f, -qx, -qy, qx, 0.f};
   const float dxm[9] = {0.f, qy, qz, qy, -2.f * qx, -qw, qz, qw, -2.f * qx};
   const float dym[9] = {-2.f * qy, qx, qw, qx, 0.f, qz, -qw, qz, -2.f * qy};
@@ -1549,10 +1518,8 @@ __global__ void __launch_bounds__(256, 4) project_bwd_kernel(ProjBwdArgs a) {
     dq[3] += dzm[r] * drg[r];
   }
   for (int r = 0; r < 4; ++r) dq[r] *= 2.f;
-  const float qh[4] = {qw, qx, qy, qz};
   const float qd = qh[0] * dq[0] + qh[1] * dq[1] + qh[2] * dq[2] + qh[3] * dq[3];
-  if (vis)
-    for (int r = 0; r < 4; ++r) a.grads.rot[4 * i + r] = gr[r] + (dq[r] - qh[r] * qd) / qn;
+  for (int r = 0; r < 4; ++r) out.rot[r] = (dq[r] - qh[r] * qd) / qn;
   float dp[3] = {0.f, 0.f, 0.f};
   const float z2 = z * z, z3 = z2 * z;
   dp[0] += ac[0] * fx / z;
@@ -1563,9 +1530,129 @@ __global__ void __launch_bounds__(256, 4) project_bwd_kernel(ProjBwdArgs a) {
   dp[1] += djac[5] * (-fy / z2);
   dp[2] += djac[0] * (-fx / z2) + djac[2] * (2.f * fx * x / z3) + djac[4] * (-fy / z2) + djac[5] * (2.f * fy * y / z3);
   dp[2] += ac[5];
-  if (vis)
-    for (int r = 0; r < 3; ++r)
-      a.grads.pos[3 * i + r] = gp[r] + (a.rwc[3 * r] * dp[0] + a.rwc[3 * r + 1] * dp[1] + a.rwc[3 * r + 2] * dp[2]);
+  for (int r = 0; r < 3; ++r) out.pos[r] = rwc[3 * r] * dp[0] + rwc[3 * r + 1] * dp[1] + rwc[3 * r + 2] * dp[2];
+  return out;
+}
+
+// The frame-independent terms of a Gaussian: normalised quaternion, its rotation, scales.
+__device__ __forceinline__ void proj_bwd_common(const float* q, const float* ls, float* qh, float& qn, float* rg,
+                                                float* sc) {
+  qn = sqrtf(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+  const float qw = q[0] / qn, qx = q[1] / qn, qy = q[2] / qn, qz = q[3] / qn;
+  qh[0] = qw, qh[1] = qx, qh[2] = qy, qh[3] = qz;
+  rg[0] = 1.f - 2.f * (qy * qy + qz * qz), rg[1] = 2.f * (qx * qy - qw * qz), rg[2] = 2.f * (qx * qz + qw * qy);
+  rg[3] = 2.f * (qx * qy + qw * qz), rg[4] = 1.f - 2.f * (qx * qx + qz * qz), rg[5] = 2.f * (qy * qz - qw * qx);
+  rg[6] = 2.f * (qx * qz - qw * qy), rg[7] = 2.f * (qy * qz + qw * qx), rg[8] = 1.f - 2.f * (qx * qx + qy * qy);
+  sc[0] = expf(ls[0]), sc[1] = expf(ls[1]), sc[2] = expf(ls[2]);
+}
+
+// K9: projection backward (render.cpp:368-429), one thread per Gaussian. The gradient adds
+// are __fadd_rn (no contraction), so the multi-frame kernel below reproduces them bit for bit.
+__global__ void __launch_bounds__(256, 4) project_bwd_kernel(ProjBwdArgs a) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= a.map.n) return;
+  const float4* rv = reinterpret_cast<const float4*>(a.rec + i);
+  // every load is issued before the culled test (one memory round trip instead of two; a culled
+  // Gaussian's extra bytes cost less than the serialised latency): 16-byte loads of the record,
+  // the accumulators (re-zeroed below for the next frame), the quaternion
+  const int4 bb = reinterpret_cast<const int4*>(a.rec + i)[2];
+  const float4 r0 = ld_early4(rv), r1 = ld_early4(rv + 1);
+  float4* acc4 = reinterpret_cast<float4*>(a.geo_acc + 8 * i);
+  const float4 g0 = ld_early4(acc4), g1 = ld_early4(acc4 + 1);
+  const float ac[7] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z};
+  const float pv[3] = {ld_early(a.map.pos + 3 * i), ld_early(a.map.pos + 3 * i + 1), ld_early(a.map.pos + 3 * i + 2)};
+  const float4 q4 = (reinterpret_cast<uintptr_t>(a.map.rot) & 15) == 0
+                        ? ld_early4(reinterpret_cast<const float4*>(a.map.rot) + i)
+                        : make_float4(a.map.rot[4 * i], a.map.rot[4 * i + 1], a.map.rot[4 * i + 2], a.map.rot[4 * i + 3]);
+  const float lv[3] = {ld_early(a.map.lsc + 3 * i), ld_early(a.map.lsc + 3 * i + 1), ld_early(a.map.lsc + 3 * i + 2)};
+  const float q[4] = {q4.x, q4.y, q4.z, q4.w};
+  // the gradient read-modify-writes: loads issued here, independent of the math below
+  const float go = ld_early(a.grads.opa + i);
+  const float gl[3] = {ld_early(a.grads.lsc + 3 * i), ld_early(a.grads.lsc + 3 * i + 1), ld_early(a.grads.lsc + 3 * i + 2)};
+  const float gr[4] = {ld_early(a.grads.rot + 4 * i), ld_early(a.grads.rot + 4 * i + 1), ld_early(a.grads.rot + 4 * i + 2),
+                       ld_early(a.grads.rot + 4 * i + 3)};
+  const float gp[3] = {ld_early(a.grads.pos + 3 * i), ld_early(a.grads.pos + 3 * i + 1), ld_early(a.grads.pos + 3 * i + 2)};
+  // culled (empty bbox): no accumulation happened, nothing is written. The test only guards the
+  // stores, so the loads above are all in flight together
+  const bool vis = bb.x <= bb.y;
+  if (!vis) return;
+  acc4[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+  acc4[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  float qh[4], qn, rg[9], sc[3];
+  proj_bwd_common(q, lv, qh, qn, rg, sc);
+  const PbContrib c = proj_bwd_frame(pv, qh, qn, rg, sc, r0, r1, ac, a.rcw, a.rwc, a.o, a.fx, a.fy);
+  a.grads.opa[i] = __fadd_rn(go, c.opa);
+  for (int k = 0; k < 3; ++k) a.grads.lsc[3 * i + k] = __fadd_rn(gl[k], c.lsc[k]);
+  for (int k = 0; k < 4; ++k) a.grads.rot[4 * i + k] = __fadd_rn(gr[k], c.rot[k]);
+  for (int k = 0; k < 3; ++k) a.grads.pos[3 * i + k] = __fadd_rn(gp[k], c.pos[k]);
+}
+
+// K9 over a step's frames at once: the gradients are read and written once, with the same float
+// additions in the same order as frame-by-frame K9.
+constexpr int kPbFrames = 8;
+struct ProjBwdMultiArgs {
+  MapPtrs map;
+  MapPtrs grads;
+  int nf;
+  const SplatRec* rec[kPbFrames];
+  float* geo_acc[kPbFrames];
+  float rcw[kPbFrames][9], rwc[kPbFrames][9], o[kPbFrames][3];
+  float fx[kPbFrames], fy[kPbFrames];
+};
+// One thread per Gaussian, frames in order; the next frame's record and accumulators are loaded
+// while the current frame's contribution is computed.
+__global__ void __launch_bounds__(256, 3) project_bwd_multi_kernel(ProjBwdMultiArgs a) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= a.map.n) return;
+  const float pv[3] = {ld_early(a.map.pos + 3 * i), ld_early(a.map.pos + 3 * i + 1), ld_early(a.map.pos + 3 * i + 2)};
+  const float4 q4 = (reinterpret_cast<uintptr_t>(a.map.rot) & 15) == 0
+                        ? ld_early4(reinterpret_cast<const float4*>(a.map.rot) + i)
+                        : make_float4(a.map.rot[4 * i], a.map.rot[4 * i + 1], a.map.rot[4 * i + 2], a.map.rot[4 * i + 3]);
+  const float lv[3] = {ld_early(a.map.lsc + 3 * i), ld_early(a.map.lsc + 3 * i + 1), ld_early(a.map.lsc + 3 * i + 2)};
+  const float q[4] = {q4.x, q4.y, q4.z, q4.w};
+  float go = ld_early(a.grads.opa + i);
+  float gl[3] = {ld_early(a.grads.lsc + 3 * i), ld_early(a.grads.lsc + 3 * i + 1), ld_early(a.grads.lsc + 3 * i + 2)};
+  float gr[4] = {ld_early(a.grads.rot + 4 * i), ld_early(a.grads.rot + 4 * i + 1), ld_early(a.grads.rot + 4 * i + 2),
+                 ld_early(a.grads.rot + 4 * i + 3)};
+  float gp[3] = {ld_early(a.grads.pos + 3 * i), ld_early(a.grads.pos + 3 * i + 1), ld_early(a.grads.pos + 3 * i + 2)};
+  float qh[4], qn, rg[9], sc[3];
+  proj_bwd_common(q, lv, qh, qn, rg, sc);
+  bool any = false;
+  auto load = [&](int b, int4& bb, float4& r0, float4& r1, float4& g0, float4& g1) {
+    const float4* rv = reinterpret_cast<const float4*>(a.rec[b] + i);
+    bb = reinterpret_cast<const int4*>(a.rec[b] + i)[2];
+    r0 = ld_early4(rv);
+    r1 = ld_early4(rv + 1);
+    const float4* acc4 = reinterpret_cast<const float4*>(a.geo_acc[b] + 8 * i);
+    g0 = ld_early4(acc4);
+    g1 = ld_early4(acc4 + 1);
+  };
+  int4 bb;
+  float4 r0, r1, g0, g1;
+  load(0, bb, r0, r1, g0, g1);
+  for (int b = 0; b < a.nf; ++b) {
+    int4 nbb = bb;
+    float4 nr0 = r0, nr1 = r1, ng0 = g0, ng1 = g1;
+    if (b + 1 < a.nf) load(b + 1, nbb, nr0, nr1, ng0, ng1);
+    if (bb.x <= bb.y) {  // visible in frame b
+      any = true;
+      float4* acc4 = reinterpret_cast<float4*>(a.geo_acc[b] + 8 * i);
+      acc4[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+      acc4[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+      const float ac[7] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z};
+      const PbContrib c = proj_bwd_frame(pv, qh, qn, rg, sc, r0, r1, ac, a.rcw[b], a.rwc[b], a.o[b], a.fx[b], a.fy[b]);
+      go = __fadd_rn(go, c.opa);
+      for (int k = 0; k < 3; ++k) gl[k] = __fadd_rn(gl[k], c.lsc[k]);
+      for (int k = 0; k < 4; ++k) gr[k] = __fadd_rn(gr[k], c.rot[k]);
+      for (int k = 0; k < 3; ++k) gp[k] = __fadd_rn(gp[k], c.pos[k]);
+    }
+    bb = nbb, r0 = nr0, r1 = nr1, g0 = ng0, g1 = ng1;
+  }
+  if (!any) return;
+  a.grads.opa[i] = go;
+  for (int k = 0; k < 3; ++k) a.grads.lsc[3 * i + k] = gl[k];
+  for (int k = 0; k < 4; ++k) a.grads.rot[4 * i + k] = gr[k];
+  for (int k = 0; k < 3; ++k) a.grads.pos[3 * i + k] = gp[k];
 }
 
 // project_gaussian (render.cpp:118-132): one Gaussian, returns cov2d (not its inverse).
@@ -1858,6 +1945,28 @@ void render_backward(cudaStream_t st, const MapPtrs& map, const float rot_cw[9],
   }
   if (!project) return;
   render_project_backward(st, map, rot_cw, rot_wc, origin, intr, w, geo_acc, grads);
+}
+
+void render_project_backward_multi(cudaStream_t st, const MapPtrs& map, int nf, const float* const* rot_cw,
+                                   const float* const* rot_wc, const float* const* origin, const Intr& intr,
+                                   const RenderWork* const* w, float* const* geo_acc, const MapPtrs& grads) {
+  if (map.n <= 0) return;
+  for (int f0 = 0; f0 < nf; f0 += kPbFrames) {
+    ProjBwdMultiArgs pa;
+    pa.map = map;
+    pa.grads = grads;
+    pa.nf = std::min(kPbFrames, nf - f0);
+    for (int b = 0; b < pa.nf; ++b) {
+      pa.rec[b] = w[f0 + b]->rec;
+      pa.geo_acc[b] = geo_acc[f0 + b];
+      for (int i = 0; i < 9; ++i) pa.rcw[b][i] = rot_cw[f0 + b][i], pa.rwc[b][i] = rot_wc[f0 + b][i];
+      for (int i = 0; i < 3; ++i) pa.o[b][i] = origin[f0 + b][i];
+      pa.fx[b] = intr.fx;
+      pa.fy[b] = intr.fy;
+    }
+    project_bwd_multi_kernel<<<(unsigned)((map.n + 255) / 256), 256, 0, st>>>(pa);
+    count_launch();
+  }
 }
 
 void render_project_backward(cudaStream_t st, const MapPtrs& map, const float rot_cw[9], const float rot_wc[9],
