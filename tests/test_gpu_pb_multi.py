@@ -1,7 +1,8 @@
 """The projection backward of all keyframes in one pass (render_project_backward_multi, the
 session default) against one K9 launch per frame (LATMAP_PB_MULTI=0): the same float additions
-in the same frame order, so in deterministic mode the gradient buffers are bit-identical.
-Each variant runs in its own process (the switch is read once)."""
+in the same frame order, so in deterministic mode the rendered images, the loss terms and the
+gradient buffers are bit-identical. Each variant runs in its own process (the switch is read
+once)."""
 import os
 import subprocess
 import sys
@@ -31,7 +32,10 @@ s.set_map(w.map); s.set_dictionary(w.atoms, w.anchor, w.proj); s.set_frames(w.fr
 ctx.set_deterministic(True)
 s.objective(want_grad=True)
 s.objective(want_grad=True)
-np.save(sys.argv[1], s.grad_buffer().cpu().numpy())
+loss = s.objective(want_grad=True)
+imgs = [t.cpu().numpy().ravel() for b in range(len(w.frames)) for t in s.frame_images(b) if t is not None]
+np.save(sys.argv[1], np.concatenate([s.grad_buffer().cpu().numpy()] + imgs
+                                    + [np.array([loss[k] for k in ("l_rgb", "l_depth", "l_cos", "total")], np.float32)]))
 """
 
 
