@@ -305,6 +305,11 @@ latmap_status latmap_session_grad_buffer(latmap_session* s, float** grads, int64
 latmap_status latmap_session_grad_layout(latmap_session* s, int64_t offsets[8], int64_t lengths[8]);
 latmap_status latmap_session_loss_buffer(latmap_session* s, double** partials, int64_t* count);
 latmap_status latmap_session_read_loss(latmap_session* s, latmap_loss_breakdown* out);
+/* The step's loss partials (latmap_session_loss_buffer's layout) copied D2H on the context stream
+ * into host_partials (page-locked for an asynchronous copy) without waiting: after the stream
+ * reaches this point, latmap_loss_assemble(host_partials, *count, ...) gives the LossBreakdown.
+ * Lets a training loop read every step's loss one step late instead of stalling each step. */
+latmap_status latmap_session_read_loss_async(latmap_session* s, double* host_partials, int64_t cap, int64_t* count);
 /* Per-frame render outputs of the last objective (device pointers; parity and Stage-II reuse). */
 latmap_status latmap_session_frame_images(latmap_session* s, int32_t frame, float** color, float** depth,
                                           float** query, float** alpha);

@@ -158,6 +158,7 @@ def _declare(L):
         "latmap_session_export_rows": [P, P],
         "latmap_session_import_rows": [P, P, C.c_int64, P, C.c_int64],
         "latmap_session_import_rows_device": [P, P, C.c_int64, P, C.c_int64],
+        "latmap_session_read_loss_async": [P, P, C.c_int64, C.POINTER(C.c_int64)],
         "latmap_session_grad_buffer": [P, C.POINTER(P), C.POINTER(C.c_int64)],
         "latmap_session_loss_buffer": [P, C.POINTER(P), C.POINTER(C.c_int64)],
         "latmap_session_read_loss": [P, C.POINTER(LossBreakdown)],
@@ -276,7 +277,7 @@ EXPORTED = ["latmap_ctx_create", "latmap_ctx_destroy", "latmap_ctx_set_stream", 
             "latmap_session_set_dictionary", "latmap_session_get_dictionary", "latmap_session_get_anchor", "latmap_session_set_frames",
             "latmap_session_set_batch", "latmap_session_set_slot_offset", "latmap_session_objective",
             "latmap_session_apply", "latmap_session_step", "latmap_session_objective_ex", "latmap_session_step_dict",
-            "latmap_session_export_rows", "latmap_session_import_rows", "latmap_session_import_rows_device",
+            "latmap_session_export_rows", "latmap_session_import_rows", "latmap_session_import_rows_device", "latmap_session_read_loss_async",
             "latmap_session_size",
             "latmap_session_set_graphs", "latmap_session_seed_candidates", "latmap_session_append_rows",
             "latmap_session_grad_buffer", "latmap_session_loss_buffer",

@@ -649,6 +649,15 @@ class Session:
         check(self.ctx.h, lib().latmap_session_append_rows(self.h, C.c_void_p(r.data_ptr()), int(r.shape[0]),
                                                            self._np_ptr(f)))
 
+    def read_loss_async(self, buf):
+        """Enqueue the D2H copy of the step's loss partials into ``buf`` (pinned float64 numpy) on
+        the context stream; after the stream passes this point, ``assemble_loss(buf[:n], ...)``
+        gives the LossBreakdown. Returns n."""
+        cnt = C.c_int64(0)
+        check(self.ctx.h, lib().latmap_session_read_loss_async(self.h, buf.ctypes.data_as(C.c_void_p), buf.size,
+                                                               C.byref(cnt)))
+        return cnt.value
+
     def read_loss(self):
         out = LossBreakdown()
         check(self.ctx.h, lib().latmap_session_read_loss(self.h, C.byref(out)))

@@ -2071,6 +2071,16 @@ latmap_status latmap_session_read_loss(latmap_session* s, latmap_loss_breakdown*
   return session_assemble(s, out);
 }
 
+latmap_status latmap_session_read_loss_async(latmap_session* s, double* host_partials, int64_t cap, int64_t* count) {
+  if (!s || !host_partials || !count) return LATMAP_ERR_INVALID_ARGUMENT;
+  const int64_t n = (int64_t)s->part_frames * kPart + kTail;
+  *count = n;
+  if (cap < n) return fail(s->ctx, LATMAP_ERR_INVALID_ARGUMENT, "read_loss_async: buffer too small");
+  CTX_CHECK(s->ctx, cudaMemcpyAsync(host_partials, s->partials, sizeof(double) * n, cudaMemcpyDeviceToHost,
+                                    s->ctx->stream));
+  return LATMAP_OK;
+}
+
 latmap_status latmap_session_frame_images(latmap_session* s, int32_t b, float** color, float** depth, float** query,
                                           float** alpha) {
   if (!s || b < 0 || b >= s->nframes) return LATMAP_ERR_INVALID_ARGUMENT;
