@@ -49,12 +49,35 @@ class Config(C.Structure):
                                                         ("num_threads", C.c_int32)]
 
 
+class PipelineConfig(C.Structure):
+    """latmap_ref_pipeline_config: the pipeline fields of latmap::Config, api.PipelineConfig's order."""
+    _fields_ = [("query_dim", C.c_int32), ("embed_dim", C.c_int32), ("dict_size", C.c_int32),
+                ("stage1_iters", C.c_int32), ("stage2_iters", C.c_int32), ("history_sample", C.c_int32),
+                ("history_capacity", C.c_int32), ("voxel_size", C.c_float), ("local_radius", C.c_float),
+                ("sync_distance", C.c_float), ("hash_capacity", C.c_int64), ("local_mapping", C.c_int32),
+                ("keyframe_stride", C.c_int32), ("seed", C.c_uint64), ("dict_init", C.c_int32),
+                ("dict_decay", C.c_float), ("trust_anchor_persistent", C.c_int32)]
+
+
 class Loss(C.Structure):
     _fields_ = [(f, C.c_float) for f in ("l_rgb", "l_ssim", "l_depth", "l_cos", "l_l2", "l_trust", "total")] + [
         ("supervised_rows", C.c_int64), ("depth_empty", C.c_int32), ("zero_norm_flagged", C.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class KeyframeLog(C.Structure):
+    _fields_ = [("frame_index", C.c_int32), ("loss", Loss), ("seeded", C.c_int64), ("active_count", C.c_int64),
+                ("global_count", C.c_int64), ("dict_weight_mass", C.c_double), ("synced", C.c_int32),
+                ("sync", C.c_int64 * 5)]
+
+    def as_dict(self):
+        return {"frame_index": self.frame_index, "loss": self.loss.as_dict(), "seeded": self.seeded,
+                "active_count": self.active_count, "global_count": self.global_count,
+                "dict_weight_mass": self.dict_weight_mass, "synced": bool(self.synced),
+                "sync": dict(zip(("written_back", "newborn_inserted", "newborn_rejected", "pruned", "fetched"),
+                                 list(self.sync)))}
 
 
 def available() -> bool:
@@ -81,6 +104,13 @@ def lib():
         L.latmap_ref_session_objective.argtypes = [P, C.POINTER(Loss)]
         L.latmap_ref_session_get.argtypes = [P, P, P, P]
         L.latmap_ref_session_destroy.argtypes = [P]
+        L.latmap_ref_pipeline_create.argtypes = [C.POINTER(Config), C.POINTER(PipelineConfig), C.POINTER(Intr)]
+        L.latmap_ref_pipeline_create.restype = P
+        L.latmap_ref_pipeline_process.argtypes = [P, C.POINTER(Frame), C.c_int32, C.POINTER(KeyframeLog)]
+        L.latmap_ref_pipeline_flush.argtypes = [P, P]
+        L.latmap_ref_pipeline_get.argtypes = [P, P, P, P, P, P]
+        L.latmap_ref_pipeline_get.restype = C.c_int64
+        L.latmap_ref_pipeline_destroy.argtypes = [P]
         _lib = L
     return _lib
 
@@ -213,5 +243,48 @@ class Session:
             try:
                 lib().latmap_ref_session_destroy(self.h)
             except Exception:  # noqa: BLE001  interpreter shutdown
+                pass
+            self.h = None
+
+
+class Pipeline:
+    """The reference's keyframe pipeline (PipelineState / process_keyframe and run_pipeline's final
+    flush, pipeline.cpp:106-330) on host arrays."""
+
+    def __init__(self, cfg: Config, pc: PipelineConfig, intr):
+        self.pc = pc
+        self.intr = _intr(intr)
+        self.h = lib().latmap_ref_pipeline_create(C.byref(cfg), C.byref(pc), C.byref(self.intr))
+        if not self.h:
+            raise RuntimeError(lib().latmap_ref_last_error().decode())
+
+    def process_keyframe(self, kf):
+        keep = _Keep()
+        fr = _frames([kf], keep)
+        log = KeyframeLog()
+        _check(lib().latmap_ref_pipeline_process(self.h, fr, int(getattr(kf, "frame_index", 0)), C.byref(log)))
+        return log.as_dict()
+
+    def flush(self):
+        st = np.zeros(5, np.int64)
+        _check(lib().latmap_ref_pipeline_flush(self.h, _p(st)))
+        return dict(zip(("written_back", "newborn_inserted", "newborn_rejected", "pruned", "fetched"), st.tolist()))
+
+    def state(self):
+        n = lib().latmap_ref_pipeline_get(self.h, None, None, None, None, None)
+        org = np.zeros(max(n, 1), np.int64)
+        k, ds, df = self.pc.dict_size, self.pc.query_dim, self.pc.embed_dim
+        atoms = np.zeros((k, df), np.float32)
+        proj = np.zeros((ds, df), np.float32)
+        w = np.zeros(k, np.float32)
+        size = C.c_int64(0)
+        lib().latmap_ref_pipeline_get(self.h, _p(org), _p(atoms), _p(proj), _p(w), C.byref(size))
+        return {"origin": org[:n], "atoms": atoms, "proj": proj, "weights": w, "store_size": size.value}
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            try:
+                lib().latmap_ref_pipeline_destroy(self.h)
+            except Exception:  # noqa: BLE001
                 pass
             self.h = None

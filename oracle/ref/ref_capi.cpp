@@ -51,6 +51,26 @@ struct latmap_ref_loss {
   int64_t supervised_rows;
   int32_t depth_empty, zero_norm_flagged;
 };
+// The pipeline fields of latmap::Config (config.hpp:10-63), as api.PipelineConfig orders them.
+struct latmap_ref_pipeline_config {
+  int32_t query_dim, embed_dim, dict_size, stage1_iters, stage2_iters, history_sample, history_capacity;
+  float voxel_size, local_radius, sync_distance;
+  int64_t hash_capacity;
+  int32_t local_mapping, keyframe_stride;
+  uint64_t seed;
+  int32_t dict_init;  // 0 kmeans, 1 random
+  float dict_decay;
+  int32_t trust_anchor_persistent;
+};
+// KeyframeLog (pipe/pipeline.hpp:70-80) without the wall time.
+struct latmap_ref_keyframe_log {
+  int32_t frame_index;
+  latmap_ref_loss loss;
+  int64_t seeded, active_count, global_count;
+  double dict_weight_mass;
+  int32_t synced;
+  int64_t sync[5];  // written_back, newborn_inserted, newborn_rejected, pruned, fetched
+};
 
 }  // extern "C"
 
@@ -279,5 +299,91 @@ int latmap_ref_session_get(void* h, float* map_flat, float* atoms, float* proj) 
 }
 
 void latmap_ref_session_destroy(void* h) { delete static_cast<Session*>(h); }
+
+
+// ---- the reference's keyframe pipeline (PipelineState / process_keyframe / run_pipeline's final
+// flush, pipeline.cpp:106-330), for an independent check of csrc/pipeline.cu
+void* latmap_ref_pipeline_create(const latmap_ref_config* c, const latmap_ref_pipeline_config* pc,
+                                 const latmap_ref_intr* in) {
+  try {
+    Config cfg = make_config(*c, pc->query_dim, pc->embed_dim, pc->dict_size);
+    cfg.stage1_iters = pc->stage1_iters, cfg.stage2_iters = pc->stage2_iters;
+    cfg.history_sample = pc->history_sample, cfg.history_capacity = pc->history_capacity;
+    cfg.voxel_size = pc->voxel_size, cfg.local_radius = pc->local_radius, cfg.sync_distance = pc->sync_distance;
+    cfg.hash_capacity = pc->hash_capacity, cfg.local_mapping = pc->local_mapping != 0;
+    cfg.keyframe_stride = pc->keyframe_stride, cfg.seed = pc->seed;
+    cfg.dict_init = pc->dict_init == 1 ? "random" : "kmeans";
+    cfg.dict_decay = pc->dict_decay, cfg.trust_anchor_persistent = pc->trust_anchor_persistent != 0;
+    return new PipelineState(cfg, make_intr(*in));
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+int latmap_ref_pipeline_process(void* h, const latmap_ref_frame* f, int32_t frame_index,
+                                latmap_ref_keyframe_log* out) {
+  auto* st = static_cast<PipelineState*>(h);
+  try {
+    Keyframe kf = make_frame(*f, latmap_ref_intr{st->intr.fx, st->intr.fy, st->intr.cx, st->intr.cy, st->intr.width,
+                                                 st->intr.height},
+                             st->cfg.embed_dim);
+    kf.frame_index = frame_index;
+    const KeyframeLog row = process_keyframe(*st, std::move(kf));
+    if (out) {
+      out->frame_index = row.frame_index;
+      copy_loss(row.loss, &out->loss);
+      out->seeded = row.seeded, out->active_count = row.active_count, out->global_count = row.global_count;
+      out->dict_weight_mass = row.dict_weight_mass;
+      out->synced = row.synced;
+      out->sync[0] = row.sync.written_back, out->sync[1] = row.sync.newborn_inserted;
+      out->sync[2] = row.sync.newborn_rejected, out->sync[3] = row.sync.pruned, out->sync[4] = row.sync.fetched;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// run_pipeline's final flush (pipeline.cpp:320-330); stats[5] as SyncStats
+int latmap_ref_pipeline_flush(void* h, int64_t* stats) {
+  auto* st = static_cast<PipelineState*>(h);
+  try {
+    SyncStats ss;
+    if (st->active.size() > 0) {
+      std::vector<uint8_t> kept;
+      st->active.mark_all_dirty();
+      const Vec3f center = st->have_last_pos ? st->last_pos : Vec3f::Zero();
+      ActiveSet next = sync(st->store, st->active, center, st->cfg.local_radius, st->cfg.voxel_size, &ss, &kept);
+      st->opt.keep_map_rows(kept);
+      st->active = std::move(next);
+    }
+    if (stats) {
+      stats[0] = ss.written_back, stats[1] = ss.newborn_inserted, stats[2] = ss.newborn_rejected;
+      stats[3] = ss.pruned, stats[4] = ss.fetched;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// active-set origins, the dictionary (atoms, proj, per-atom weights) and the store size
+int64_t latmap_ref_pipeline_get(void* h, int64_t* origin, float* atoms, float* proj, float* weights,
+                                int64_t* store_size) {
+  auto* st = static_cast<PipelineState*>(h);
+  const int64_t n = (int64_t)st->active.origin.size();
+  if (origin) std::memcpy(origin, st->active.origin.data(), sizeof(int64_t) * n);
+  if (atoms) std::memcpy(atoms, st->dict.atoms.data(), sizeof(float) * st->dict.atoms.size());
+  if (proj) std::memcpy(proj, st->dict.proj.data(), sizeof(float) * st->dict.proj.size());
+  if (weights)
+    for (Eigen::Index i = 0; i < st->dict.weights.size(); ++i) weights[i] = (float)st->dict.weights[i];
+  if (store_size) *store_size = st->store.size();
+  return n;
+}
+
+void latmap_ref_pipeline_destroy(void* h) { delete static_cast<PipelineState*>(h); }
 
 }  // extern "C"

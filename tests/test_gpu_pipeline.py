@@ -309,3 +309,49 @@ def test_process_keyframe_rolls_back_a_failed_keyframe(ctx, stage):
     if stage != 3:  # a rolled-back sync already moved records into the store
         assert got["global_count"] == ref["global_count"]
     assert got["loss"]["total"] == pytest.approx(ref["loss"]["total"], rel=1e-3)
+
+
+def test_pipeline_matches_reference_pipeline(ctx):
+    """api.Pipeline against the REFERENCE's own pipeline (oracle/_ref: PipelineState,
+    process_keyframe and run_pipeline's final flush compiled from proj/src/pipeline.cpp) on the
+    same keyframes and configuration -- an independent check of csrc/pipeline.cu. Blend decisions
+    are made bit-exact (exact blend mode) so seeding sees the reference's images; the Stage-I
+    gradients differ from the reference's by float summation order only, and small learning
+    rates keep that noise away from the seeding thresholds. Counts, sync statistics and active
+    origins must match exactly; losses and the dictionary to float noise."""
+    from oracle import ref
+
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    intr, frames = make_scene(ctx)
+    cfg, pc = small_lr_config(), pipeline_config()
+    ctx.set_exact_blend(True)
+    try:
+        p = api.Pipeline(ctx, cfg, pc, intr)
+        got = [p.process_keyframe(kf) for kf in frames]
+        fl = p.flush()
+    finally:
+        ctx.set_exact_blend(False)
+    rcfg = ref.make_config(num_threads=8, dict_learn=bool(cfg.dict_learn), segment_mode=bool(cfg.segment_mode),
+                           **{f: getattr(cfg, f) for f in ref.CFG_FIELDS})
+    rpc = ref.PipelineConfig(*[getattr(pc, f) for f, _ in ref.PipelineConfig._fields_])
+    rp = ref.Pipeline(rcfg, rpc, intr)
+    want = [rp.process_keyframe(kf) for kf in frames]
+    rfl = rp.flush()
+    assert any(r["synced"] for r in want) and any(r["seeded"] for r in want)
+    for a, b in zip(got, want):
+        assert (a["seeded"], a["synced"], a["active_count"], a["global_count"]) == (
+            b["seeded"], b["synced"], b["active_count"], b["global_count"]), (a, b)
+        if a["synced"]:
+            assert a["sync"] == b["sync"]
+        assert a["loss"]["supervised_rows"] == b["loss"]["supervised_rows"]
+        for key in ("l_rgb", "l_depth", "l_cos", "l_l2", "total"):
+            assert a["loss"][key] == pytest.approx(b["loss"][key], rel=2e-3, abs=1e-6), key
+        assert a["dict_weight_mass"] == pytest.approx(b["dict_weight_mass"], rel=1e-5)
+    assert fl == rfl
+    rs = rp.state()
+    assert np.array_equal(p.active_set()[0], rs["origin"])
+    assert p.store.size() == rs["store_size"]
+    atoms, proj = p.session.get_dictionary()
+    np.testing.assert_allclose(atoms, rs["atoms"], rtol=1e-3, atol=1e-5)
+    np.testing.assert_allclose(proj, rs["proj"], rtol=1e-3, atol=1e-5)
