@@ -25,6 +25,8 @@ namespace lm {
 
 namespace {
 
+constexpr float kNegHalfLog2eF = -0.72134752044448170f;  // -0.5 * log2(e)
+
 struct Cam {
   float r[9];  // rot_cw (world -> camera), row-major
   float o[3];  // camera origin (pose translation)
@@ -630,7 +632,8 @@ __global__ void __launch_bounds__(kTilePixels) raster_fwd_kernel(RasterArgs a) {
         const float dx = fs(fx, s.mean_x);
         const float dy = fs(fy, s.mean_y);
         const float rho = fa(fa(fm(fm(s.a00, dx), dx), fm(fm(fm(2.f, s.a01), dx), dy)), fm(fm(s.a11, dy), dy));
-        float al = fm(s.alpha, exp_exact(fm(-0.5f, rho), s_etab));
+        // exact mode: libm expf restated (bit-exact blend decisions); fast mode: the SFU exp2
+        float al = EXACT ? fm(s.alpha, exp_exact(fm(-0.5f, rho), s_etab)) : fm(s.alpha, ex2_approx(fm(kNegHalfLog2eF, rho)));
         if (al > kAlphaMax) al = kAlphaMax;
         const float w = fm(al, T);
         if (EXACT) {
@@ -745,9 +748,7 @@ __global__ void __launch_bounds__(kTilePixels, DSP >= 64 ? 1 : 2) raster_fwd_mma
   __shared__ float4 s_sp[FB][3];            // {mean_x, mean_y, a00, 2 a01} {a11, alpha, depth, -} {x0, x1-x0, y0, y1-y0}
   __shared__ float s_col[FB * 3];
   __shared__ int32_t s_max;
-  __shared__ uint64_t s_etab[32];
   if (a.counters[2]) return;
-  load_exp_table(s_etab);  // published by the batch loop's barriers before first use
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, cq = lane & 3;
   const int tile = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
@@ -870,7 +871,9 @@ __global__ void __launch_bounds__(kTilePixels, DSP >= 64 ? 1 : 2) raster_fwd_mma
             const float dx = fs(fx, s0.x);
             const float dy = fs(fy, s0.y);
             const float rho = fa(fa(fm(fm(s0.z, dx), dx), fm(fm(s0.w, dx), dy)), fm(fm(s1.x, dy), dy));
-            float al = fm(s1.y, exp_exact(fm(-0.5f, rho), s_etab));
+            // fast mode: exp(-rho/2) on the SFU (ex2.approx, ~2^-22 relative); the exact-mode kernel
+            // (raster_fwd_kernel<DSP, true>) restates libm expf for bit-exact blend decisions
+            float al = fm(s1.y, ex2_approx(fm(kNegHalfLog2eF, rho)));
             alv[u] = al > kAlphaMax ? kAlphaMax : al;
           }
         }

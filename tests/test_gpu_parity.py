@@ -138,8 +138,10 @@ def test_render_images_match(ctx, cfg0, exact):
             e = np.abs(g.astype(np.float64) - ref[f]) / np.maximum(mag, 1e-30)
             print(f"query (exact={exact}): max |a-b| / M(p) = {e.max():.3e} (bound {QUERY_COND:.3e})")
         same = np.mean(g.view(np.uint32) == ref[f].astype(np.float32).view(np.uint32))
-        if exact or f == "alpha":  # alpha is accumulated exactly in both modes
+        if exact:  # exact mode: libm expf and the reference's op order -> the reference's bits
             assert same > 0.999, f"{f}: only {same:.5f} of values bit-identical"
+        elif f == "alpha":  # fast mode: exp on the SFU (ex2.approx): alpha within ~1e-6 relative
+            np.testing.assert_allclose(g, ref[f], rtol=1e-5, atol=1e-6)
 
 
 def test_render_posed_camera(ctx):
