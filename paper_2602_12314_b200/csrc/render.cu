@@ -816,8 +816,9 @@ __global__ void __launch_bounds__(kTilePixels, DSP >= 64 ? 1 : 2) raster_fwd_mma
       const float* row = s_raw + tid * RP;
       const float4 r0 = *reinterpret_cast<const float4*>(row);      // mean_x, mean_y, depth, alpha
       const float4 r1 = *reinterpret_cast<const float4*>(row + 4);  // a00, a01, a10, a11
-      s_sp[tid][0] = make_float4(r0.x, r0.y, r1.x, fm(2.f, r1.y));  // 2 a01: exact
-      s_sp[tid][1] = make_float4(r1.w, r0.w, r0.z, 0.f);
+      // the conic prescaled by -log2(e)/2: the exp2 argument is one FMA chain per pixel
+      s_sp[tid][0] = make_float4(r0.x, r0.y, kNegHalfLog2eF * r1.x, kNegHalfLog2eF * (2.f * r1.y));
+      s_sp[tid][1] = make_float4(kNegHalfLog2eF * r1.w, r0.w, r0.z, 0.f);
       int4 bb = *reinterpret_cast<const int4*>(row + 8);
       bb.y -= bb.x;  // extents: one unsigned compare per axis in the per-pixel test
       bb.w -= bb.z;
@@ -868,12 +869,13 @@ __global__ void __launch_bounds__(kTilePixels, DSP >= 64 ? 1 : 2) raster_fwd_mma
           for (int u = 0; u < 4; ++u) {
             const float4 s0 = s_sp[sb + j4 + u][0];
             const float4 s1 = s_sp[sb + j4 + u][1];
-            const float dx = fs(fx, s0.x);
-            const float dy = fs(fy, s0.y);
-            const float rho = fa(fa(fm(fm(s0.z, dx), dx), fm(fm(s0.w, dx), dy)), fm(fm(s1.x, dy), dy));
-            // fast mode: exp(-rho/2) on the SFU (ex2.approx, ~2^-22 relative); the exact-mode kernel
-            // (raster_fwd_kernel<DSP, true>) restates libm expf for bit-exact blend decisions
-            float al = fm(s1.y, ex2_approx(fm(kNegHalfLog2eF, rho)));
+            const float dx = fx - s0.x;
+            const float dy = fy - s0.y;
+            // fast mode: exp(-rho/2) on the SFU (ex2.approx, ~2^-22 relative), the argument as one
+            // FMA chain over the prescaled conic -- what the backward replays; the exact-mode kernel
+            // (raster_fwd_kernel<DSP, true>) keeps the reference's op order and libm expf
+            const float pw = fmaf(dx, fmaf(s0.z, dx, s0.w * dy), s1.x * dy * dy);
+            float al = s1.y * ex2_approx(pw);
             alv[u] = al > kAlphaMax ? kAlphaMax : al;
           }
         }
