@@ -373,41 +373,49 @@ struct Dec2Args {
   int accum;       // add A into a_part (later frames of a step) instead of storing
 };
 
-// DEC2: A[:, role half] = e^T diag(alpha / sum^2) e and (role 0) Bm = e^T Ohb with
-// Ohb[r][s] = beta_r / sum_r [a_r == s], streaming the e tiles DEC1 exported -- no
-// recomputation of S or exp. Warp-specialised: warp 8 (one elected lane) issues the TMA bulk
-// loads and the MMAs; warps 0-7 build the scaled B operands. The unit of the pipeline is a
-// half tile (64 pixel rows, one contiguous bulk copy: DEC1 exports each tile half-major, every
-// half in the 64-row core-matrix layout) in a ring of kStages stages, so three loads are in
-// flight while a fourth stage is built and multiplied.
+// DEC2: A = e^T diag(alpha / sum^2) e and Bm = e^T Ohb (Ohb[r][s] = beta_r / sum_r [a_r == s]),
+// streaming the e tiles DEC1 exported -- no recomputation of S or exp. One CTA per group of
+// tiles (kDec2Groups); A is symmetric, so at K = 256 only its blocks A00, A01, A11 are
+// accumulated (3 x 128 TMEM columns, Bm's two 128-row halves take the other 128) and the drain
+// writes A10 = A01^T. Warp-specialised: warp 8 (one elected lane) issues the TMA bulk loads and
+// the MMAs; warps 0-7 build the scaled B operands (alpha / sum^2) e over all K columns and the
+// one-hot Ohb. The pipeline unit is a half tile (64 pixel rows, one contiguous 32 KB copy: DEC1
+// exports each tile half-major) in a ring of kStages stages.
 //   bar_ld[s]    : half tile landed in sE[s]            (TMA complete_tx)
 //   bar_built[s] : 8 builder warps filled sAP/sOh[s]     (8 arrivals)
 //   bar_mma[s]   : MMAs reading sE/sAP/sOh[s] done       (tcgen05.commit)
 // The load of half tile i into stage s is issued only after the MMAs of half tile i - kStages
 // (the last user of s) completed, so a builder that sees bar_ld[s] may also overwrite sAP/sOh[s].
 constexpr int kHalf = kRows / 2;  // pixel rows per pipeline unit
-constexpr int kStages = 4;
+constexpr int kDec2Groups = 148;
+template <int K>
+constexpr int dec2_stages() {
+  return K == 256 ? 3 : 4;
+}
 template <int K>
 constexpr size_t dec2_smem() {
-  return (size_t)kStages * ((size_t)kHalf * K * 2 + (size_t)kHalf * (K / 2) * 2 + (size_t)kHalf * 64 * 2);
+  return (size_t)dec2_stages<K>() * ((size_t)kHalf * K * 2 * 2 + (size_t)kHalf * 64 * 2);
 }
 
 template <int K>
 __global__ void __launch_bounds__(288, 1) dec2_kernel(Dec2Args a) {
-  constexpr int MH = K / 128, NH = K / 2, NB = 64;
-  constexpr int kColA = 0, kColB = MH * NH;
+  constexpr int kStages = dec2_stages<K>();
+  constexpr int MH = K / 128, NB = 64;
+  // TMEM: the A blocks (128 columns each: A00 | A01 | A11 at K = 256, A at K = 128), then Bm
+  constexpr int NBLK = MH == 2 ? 3 : 1;
+  constexpr int kColB = NBLK * 128;
   constexpr int kTmemCols = kColB + MH * NB <= 256 ? 256 : 512;
   constexpr uint32_t kCH = 16u * kHalf;  // column-group stride of the 64-row half tiles
   constexpr uint32_t kTileBytes = kRows * K * 2;
-  constexpr uint32_t kEB = kHalf * K * 2, kAPB = kHalf * NH * 2, kOhB = kHalf * NB * 2;
+  constexpr uint32_t kEB = kHalf * K * 2, kAPB = kHalf * K * 2, kOhB = kHalf * NB * 2;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sE0 = smem;                     // kStages x (64 x K)
-  uint8_t* sAP0 = smem + kStages * kEB;    // kStages x (64 x NH)
+  uint8_t* sAP0 = smem + kStages * kEB;    // kStages x (64 x K)
   uint8_t* sOh0 = sAP0 + kStages * kAPB;   // kStages x (64 x NB)
   __shared__ uint64_t bar_ld[kStages], bar_built[kStages], bar_mma[kStages];
   __shared__ uint32_t s_taddr;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int role = blockIdx.x & 1, group = blockIdx.x >> 1, ngroups = gridDim.x >> 1;
+  const int group = blockIdx.x, ngroups = gridDim.x;
   if (tid == 0) {
     for (int i = 0; i < kStages; ++i) {
       tc::mbar_init(&bar_ld[i], 1);
@@ -435,23 +443,27 @@ __global__ void __launch_bounds__(288, 1) dec2_kernel(Dec2Args a) {
         tc::bulk_g2s(sE0 + s * kEB, src, kEB, &bar_ld[s]);
       };
       for (int i = 0; i < kStages - 1 && i < nh; ++i) load(i);
+      const uint32_t idA = tc::make_idesc_bf16(128, 128, 1, 1), idB = tc::make_idesc_bf16(128, NB, 1, 1);
       for (int it = 0; it < nh; ++it) {
         const int s = it % kStages;
         tc::mbar_wait(&bar_built[s], (it / kStages) & 1);
         tc::tc_fence_after();
         const uint32_t aE = aE0 + s * kEB, aAP = aAP0 + s * kAPB, aOh = aOh0 + s * kOhB;
-        for (int mh = 0; mh < MH; ++mh) {
+        // MN-major operands: 128 atoms = 16 column groups of the half tile
 #pragma unroll
-          for (int ks = 0; ks < kHalf / 16; ++ks)
-            tc::mma_bf16(tmem + kColA + mh * NH, tc::make_sdesc(aE + mh * 16 * kCH + ks * 2 * 128, 128, kCH),
-                         tc::make_sdesc(aAP + ks * 2 * 128, 128, kCH), tc::make_idesc_bf16(128, NH, 1, 1),
-                         it > 0 || ks > 0);
-          if (role == 0) {
-#pragma unroll
-            for (int ks = 0; ks < kHalf / 16; ++ks)
-              tc::mma_bf16(tmem + kColB + mh * NB, tc::make_sdesc(aE + mh * 16 * kCH + ks * 2 * 128, 128, kCH),
-                           tc::make_sdesc(aOh + ks * 2 * 128, 128, kCH), tc::make_idesc_bf16(128, NB, 1, 1),
-                           it > 0 || ks > 0);
+        for (int ks = 0; ks < kHalf / 16; ++ks) {
+          const uint32_t acc = it > 0 || ks > 0;
+          const uint64_t e0 = tc::make_sdesc(aE + ks * 2 * 128, 128, kCH);
+          const uint64_t p0 = tc::make_sdesc(aAP + ks * 2 * 128, 128, kCH);
+          const uint64_t oh = tc::make_sdesc(aOh + ks * 2 * 128, 128, kCH);
+          tc::mma_bf16(tmem + 0, e0, p0, idA, acc);  // A00 (A at K = 128)
+          tc::mma_bf16(tmem + kColB, e0, oh, idB, acc);  // Bm rows 0..127
+          if constexpr (MH == 2) {
+            const uint64_t e1 = tc::make_sdesc(aE + 16 * kCH + ks * 2 * 128, 128, kCH);
+            const uint64_t p1 = tc::make_sdesc(aAP + 16 * kCH + ks * 2 * 128, 128, kCH);
+            tc::mma_bf16(tmem + 128, e0, p1, idA, acc);       // A01
+            tc::mma_bf16(tmem + 256, e1, p1, idA, acc);       // A11
+            tc::mma_bf16(tmem + kColB + NB, e1, oh, idB, acc);  // Bm rows 128..255
           }
         }
         tc::mma_commit(&bar_mma[s]);
@@ -464,7 +476,7 @@ __global__ void __launch_bounds__(288, 1) dec2_kernel(Dec2Args a) {
       }
     }
   } else {
-    // ---------------- builders: B operands (alpha / sum^2) e[:, role half] and the beta / sum one-hot.
+    // ---------------- builders: (alpha / sum^2) e over all K columns and the beta / sum one-hot.
     // Thread = (row of the half tile, quarter of the columns); the row statistics of half tile
     // it + 1 are fetched while half tile it is built.
     const int row = tid & (kHalf - 1), q = tid / kHalf;
@@ -485,28 +497,26 @@ __global__ void __launch_bounds__(288, 1) dec2_kernel(Dec2Args a) {
       const float4 st = st_n;
       const int32_t asg = asg_n;
       if (it + 1 < nh) fetch(it + 1, st_n, asg_n);
-      const float wa = st.z * st.y * st.y;  // alpha / sum^2 (0 for rows past npx)
+      const float wa = st.z * st.y * st.y;  // alpha / sum^2
       const float wb = st.w * st.y;         // beta / sum
       tc::mbar_wait(&bar_ld[s], (it / kStages) & 1);
       const uint8_t* E = sE0 + s * kEB;
       uint8_t* AP = sAP0 + s * kAPB;
 #pragma unroll
-      for (int c = q * (NH / 4); c < (q + 1) * (NH / 4); c += 8) {
+      for (int c = q * (K / 4); c < (q + 1) * (K / 4); c += 8) {
         float v[8];
-        tc::ld_row8(E, row, role * NH + c, kCH, v);
+        tc::ld_row8(E, row, c, kCH, v);
 #pragma unroll
         for (int j = 0; j < 8; ++j) v[j] = asg != -2 ? v[j] * wa : 0.f;
         tc::st_row8(AP, row, c, kCH, v);
       }
-      if (role == 0) {
-        uint8_t* Oh = sOh0 + s * kOhB;
+      uint8_t* Oh = sOh0 + s * kOhB;
 #pragma unroll
-        for (int c = q * (NB / 4); c < (q + 1) * (NB / 4); c += 8) {
-          float v[8];
+      for (int c = q * (NB / 4); c < (q + 1) * (NB / 4); c += 8) {
+        float v[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) v[j] = (asg == c + j) ? wb : 0.f;
-          tc::st_row8(Oh, row, c, kCH, v);
-        }
+        for (int j = 0; j < 8; ++j) v[j] = (asg == c + j) ? wb : 0.f;
+        tc::st_row8(Oh, row, c, kCH, v);
       }
       tc::fence_async_smem();
       __syncwarp();
@@ -517,40 +527,56 @@ __global__ void __launch_bounds__(288, 1) dec2_kernel(Dec2Args a) {
       tc::mbar_wait(&bar_mma[(nh - 1) % kStages], ((nh - 1) / kStages) & 1);
       tc::tc_fence_after();
     }
-    // drain: lane `row` of TMEM lane group g, column half h of the role's NH
+    // drain into the partial layout [group][column half][row][column within the half] (K x K/2
+    // per half): TMEM lane group g holds rows 32g + lane of every block; the two warps of a lane
+    // group take alternate 16-column chunks
+    constexpr int NHALF = K / 2;
     const int g = warp & 3, h = warp >> 2;
     const int trow = 32 * g + lane;
-    for (int mh = 0; mh < MH; ++mh) {
-      float* dst = a.a_part + (((size_t)group * 2 + role) * K + mh * 128 + trow) * NH;
-      for (int c = h * (NH / 2); c < (h + 1) * (NH / 2); c += 16) {
+    const uint32_t tl = tmem + ((uint32_t)(32 * g) << 16);
+    auto put = [&](int i, int col, const float* v) {  // 16 values of A[i][col .. col+15]
+      const int half = col / NHALF, jj = col % NHALF;
+      float* dst = a.a_part + (((size_t)group * 2 + half) * K + i) * NHALF + jj;
+      for (int u = 0; u < 16; u += 4) {
+        float4 o = make_float4(v[u], v[u + 1], v[u + 2], v[u + 3]);
+        if (a.accum) {
+          const float4 p = *reinterpret_cast<const float4*>(dst + u);
+          o.x += p.x, o.y += p.y, o.z += p.z, o.w += p.w;
+        }
+        *reinterpret_cast<float4*>(dst + u) = o;
+      }
+    };
+    for (int blk = 0; blk < NBLK; ++blk) {
+      // blk 0: A00 (rows 0.., cols 0..); 1: A01 (rows 0.., cols 128..); 2: A11 (rows 128.., cols 128..)
+      const int r0 = blk == 2 ? 128 : 0, cb = blk == 0 ? 0 : 128;
+      for (int c = 16 * h; c < 128; c += 32) {
         float v[16];
         if (nh == 0) {
           for (int i = 0; i < 16; ++i) v[i] = 0.f;
         } else {
-          tc::tmem_ld16(tmem + ((uint32_t)(32 * g) << 16) + kColA + mh * NH + c, v);
+          tc::tmem_ld16(tl + blk * 128 + c, v);
         }
-        for (int i = 0; i < 16; i += 4) {
-          float4* d4 = reinterpret_cast<float4*>(dst + c + i);
-          float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-          if (a.accum) {
-            const float4 p = *d4;
-            o.x += p.x, o.y += p.y, o.z += p.z, o.w += p.w;
+        put(r0 + trow, cb + c, v);
+        if (blk == 1) {  // A10 = A01^T: rows 128 + c + u, column trow (lanes: consecutive columns)
+          for (int u = 0; u < 16; ++u) {
+            const int i = 128 + c + u;
+            float* dst = a.a_part + (((size_t)group * 2 + 0) * K + i) * NHALF + trow;
+            *dst = a.accum ? *dst + v[u] : v[u];
           }
-          *d4 = o;
         }
       }
-      if (role == 0) {
-        float* db = a.bm_part + ((size_t)group * K + mh * 128 + trow) * NB;
-        for (int c = h * (NB / 2); c < (h + 1) * (NB / 2); c += 16) {
-          float v[16];
-          if (nh == 0) {
-            for (int i = 0; i < 16; ++i) v[i] = 0.f;
-          } else {
-            tc::tmem_ld16(tmem + ((uint32_t)(32 * g) << 16) + kColB + mh * NB + c, v);
-          }
-          for (int i = 0; i < 16; i += 4)
-            *reinterpret_cast<float4*>(db + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    }
+    for (int mh = 0; mh < MH; ++mh) {
+      float* db = a.bm_part + ((size_t)group * K + mh * 128 + trow) * NB;
+      for (int c = 16 * h; c < NB; c += 32) {
+        float v[16];
+        if (nh == 0) {
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        } else {
+          tc::tmem_ld16(tl + kColB + mh * NB + c, v);
         }
+        for (int i = 0; i < 16; i += 4)
+          *reinterpret_cast<float4*>(db + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
       }
     }
   }
@@ -713,7 +739,7 @@ void launch_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_
                const float* feats, int64_t n_set, const int64_t* nsup, float temperature, float lambda_cos, float lambda_l2,
                float scale, bool want_grad, float* d_query, double* partials) {
   const int g1 = 148;
-  const int g2 = 148;  // 74 groups x 2 roles
+  const int g2 = kDec2Groups;  // one CTA per group
   const int accum = want_grad && w.tc_frames > 0 ? 1 : 0;
   Dec1Args d1{w.e_tiles, query, assignment, w.kd, w.mm, w.gt, w.nv, npx, 1.f / temperature, lambda_cos, lambda_l2,
               scale, nsup, d_query, reinterpret_cast<float4*>(w.row_stats),
@@ -770,7 +796,8 @@ bool decoder_tc_supported(int64_t k, int ds, int64_t n_set) {
 
 size_t decoder_tc_scratch_floats(int64_t k, int ds, int64_t npx) {
   // row_stats (4/row) + r_part + a_part + bm_part + loss_part (as floats x2)
-  return (size_t)npx * 4 + 148 * (size_t)k * ds + 74 * 2 * (size_t)k * (k / 2) + 74 * (size_t)k * 64 + 148 * 4 * 2;
+  return (size_t)npx * 4 + 148 * (size_t)k * ds + kDec2Groups * (size_t)k * k + kDec2Groups * (size_t)k * 64 +
+         148 * 4 * 2;
 }
 
 void decoder_frame_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_t* assignment, int64_t npx,
@@ -791,13 +818,15 @@ void decoder_frame_tc(cudaStream_t st, DecoderWork& w, const float* query, const
   // d_atoms += Bm E for this frame's embedding table; A and R accumulate over the step's frames
   // and enter once in decoder_finish_tc (they multiply the same D, W in every frame)
   if (df % 4 == 0 && (reinterpret_cast<uintptr_t>(feats) & 15) == 0 && (reinterpret_cast<uintptr_t>(d_atoms) & 15) == 0) {
-    bm_embed_fused_kernel<<<(unsigned)(k / 2), 256, 0, st>>>(w.bm_part, 74, (int)k, feats, (int)n_set, df, d_atoms);
+    bm_embed_fused_kernel<<<(unsigned)(k / 2), 256, 0, st>>>(w.bm_part, kDec2Groups, (int)k, feats, (int)n_set, df,
+                                                           d_atoms);
     count_launch();
   } else {
     cudaMemsetAsync(w.bm, 0, sizeof(float) * n_set * k, st);
     const int64_t quads = k * 64 / 4;
     dec_reduce_kernel<<<dim3((unsigned)((quads + 255) / 256), deterministic() ? 1 : kRedSplit), 256, 0, st>>>(
-        nullptr, w.bm_part, nullptr, nullptr, (int)k, ds, (int)n_set, 148, 74, nullptr, w.bm, nullptr, nullptr, 0, 1);
+        nullptr, w.bm_part, nullptr, nullptr, (int)k, ds, (int)n_set, 148, kDec2Groups, nullptr, w.bm, nullptr, nullptr,
+        0, 1);
     count_launch();
     decoder_bm_embed(st, w.bm, feats, n_set, k, df, d_atoms);
   }
@@ -814,7 +843,7 @@ void decoder_finish_tc(cudaStream_t st, DecoderWork& w, const float* atoms, cons
   if (w.tc_frames > 0) {  // the fused frames' step-summed A and R partials
     const int64_t quads = (k * k + k * ds) / 4;
     dec_reduce_kernel<<<dim3((unsigned)((quads + 255) / 256), deterministic() ? 1 : kRedSplit), 256, 0, st>>>(
-        w.a_part, nullptr, w.r_part, nullptr, (int)k, ds, 0, 148, 74, w.a_acc, nullptr, w.r_acc, nullptr, 1, 0);
+        w.a_part, nullptr, w.r_part, nullptr, (int)k, ds, 0, 148, kDec2Groups, w.a_acc, nullptr, w.r_acc, nullptr, 1, 0);
     count_launch();
     w.tc_frames = 0;
   }
