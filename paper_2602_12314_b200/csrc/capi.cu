@@ -1313,7 +1313,7 @@ latmap_status latmap_session_create(latmap_ctx* ctx, const latmap_config* cfg, i
   if (good && cfg->decoder_precision == 1) {
     good = ok(cudaMalloc(&d.row_stats, sizeof(float) * 4 * npx)) &&
            ok(cudaMalloc(&d.r_part, sizeof(float) * 2 * 148 * k * ds)) &&
-           ok(cudaMalloc(&d.a_part, sizeof(float) * 148 * k * (k + 2))) &&
+           ok(cudaMalloc(&d.a_part, sizeof(float) * 8 * 148 * k * k + 1024)) &&  // 8 per-frame slots (decoder_tc.cu)
            ok(cudaMalloc(&d.bm_part, sizeof(float) * 148 * k * 64)) &&
            ok(cudaMalloc(&d.loss_part, sizeof(double) * 148 * 4)) &&
            ok(cudaMalloc(&d.e_tiles, (size_t)((npx + 127) / 128) * 128 * k * 2)) &&

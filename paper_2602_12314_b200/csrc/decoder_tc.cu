@@ -368,9 +368,9 @@ struct Dec2Args {
   const int32_t* assign;
   const float4* row_stats;   // (max, 1/sum, alpha, beta)
   int64_t npx;
-  float* a_part;   // (gridDim/2) x 2 roles x K x (K/2), summed over the step's frames
+  float* a_part;   // this frame's slot: gridDim x 2 halves x K x (K/2)
   float* bm_part;  // (gridDim/2) x K x 64  (role 0 only)
-  int accum;       // add A into a_part (later frames of a step) instead of storing
+  int accum;       // add A into the slot (frames past the last slot) instead of storing
 };
 
 // DEC2: A = e^T diag(alpha / sum^2) e and Bm = e^T Ohb (Ohb[r][s] = beta_r / sum_r [a_r == s]),
@@ -388,6 +388,7 @@ struct Dec2Args {
 // (the last user of s) completed, so a builder that sees bar_ld[s] may also overwrite sAP/sOh[s].
 constexpr int kHalf = kRows / 2;  // pixel rows per pipeline unit
 constexpr int kDec2Groups = 148;
+constexpr int kDec2Slots = 8;  // per-frame A partial slots (see launch_tc)
 template <int K>
 constexpr int dec2_stages() {
   return K == 256 ? 3 : 4;
@@ -759,7 +760,12 @@ void launch_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_
     count_launch();
     return;
   }
-  Dec2Args d2{w.e_tiles, assignment, reinterpret_cast<const float4*>(w.row_stats), npx, w.a_part, w.bm_part, accum};
+  // A partials: one slot per frame of the step (plain stores; decoder_finish_tc sums the slots),
+  // the last slot accumulating when a step has more frames than slots
+  const int slot = std::min(w.tc_frames, kDec2Slots - 1);
+  const int accum2 = want_grad && w.tc_frames >= kDec2Slots ? 1 : 0;
+  Dec2Args d2{w.e_tiles, assignment, reinterpret_cast<const float4*>(w.row_stats), npx,
+              w.a_part + (size_t)slot * kDec2Groups * K * K, w.bm_part, accum2};
   const size_t sm2 = dec2_smem<K>();
   static bool attr2 = false;
   if (!attr2) {
@@ -796,8 +802,8 @@ bool decoder_tc_supported(int64_t k, int ds, int64_t n_set) {
 
 size_t decoder_tc_scratch_floats(int64_t k, int ds, int64_t npx) {
   // row_stats (4/row) + r_part + a_part + bm_part + loss_part (as floats x2)
-  return (size_t)npx * 4 + 148 * (size_t)k * ds + kDec2Groups * (size_t)k * k + kDec2Groups * (size_t)k * 64 +
-         148 * 4 * 2;
+  return (size_t)npx * 4 + 148 * (size_t)k * ds + kDec2Slots * kDec2Groups * (size_t)k * k +
+         kDec2Groups * (size_t)k * 64 + 148 * 4 * 2;
 }
 
 void decoder_frame_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_t* assignment, int64_t npx,
@@ -840,10 +846,11 @@ void decoder_finish_tc(cudaStream_t st, DecoderWork& w, const float* atoms, cons
   if (!w.tc_pending) return;
   const int64_t k = w.k;
   const int ds = w.ds, df = w.df;
-  if (w.tc_frames > 0) {  // the fused frames' step-summed A and R partials
+  if (w.tc_frames > 0) {  // the fused frames' A partials (one slot per frame) and step-summed R partials
     const int64_t quads = (k * k + k * ds) / 4;
+    const int ngroups_a = kDec2Groups * std::min(w.tc_frames, kDec2Slots);
     dec_reduce_kernel<<<dim3((unsigned)((quads + 255) / 256), deterministic() ? 1 : kRedSplit), 256, 0, st>>>(
-        w.a_part, nullptr, w.r_part, nullptr, (int)k, ds, 0, 148, kDec2Groups, w.a_acc, nullptr, w.r_acc, nullptr, 1, 0);
+        w.a_part, nullptr, w.r_part, nullptr, (int)k, ds, 0, 148, ngroups_a, w.a_acc, nullptr, w.r_acc, nullptr, 1, 0);
     count_launch();
     w.tc_frames = 0;
   }

@@ -119,7 +119,7 @@ struct DecoderWork {
   // tcgen05 path scratch (decoder_tc.cu)
   float* row_stats = nullptr;  // npx x 4: max S, 1/sum, alpha, beta
   float* r_part = nullptr;     // 2 x 148 x K x ds (fused path step sums, staged path per frame)
-  float* a_part = nullptr;     // 74 x 2 x K x K/2
+  float* a_part = nullptr;     // 8 frame slots x 148 groups x 2 halves x K x K/2
   float* bm_part = nullptr;    // 74 x K x 64
   double* loss_part = nullptr; // 148 x 4
   uint8_t* e_tiles = nullptr;  // ceil(npx/128) x 128 x K bf16 (DEC1 -> DEC2)
