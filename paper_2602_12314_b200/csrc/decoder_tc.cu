@@ -591,6 +591,30 @@ __global__ void __launch_bounds__(288, 1) dec2_kernel(Dec2Args a) {
 // from (groups x 2 roles x K x K/2) and R^T (K x DS) -> R (DS x K) into the accumulators. Each thread owns 4 consecutive partial entries (float4 loads) and a
 // 1/kRedSplit share of the groups; the shares meet in global atomics (distinct addresses).
 // Block (0, 0) also folds the loss partials into the frame's slots.
+// One warp folds DEC1's per-CTA loss partials (groups x 4 doubles: cos, l2, non-finite flag) into
+// the frame's slots: lane-strided sums, then a fixed xor tree (the same order every run).
+__device__ __forceinline__ void fold_loss_partials(const double* __restrict__ loss_part, int groups,
+                                                   double* partials) {
+  const int lane = threadIdx.x & 31;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (int gi = lane; gi < groups; gi += 32) {
+    s0 += loss_part[gi * 4 + 0];
+    s1 += loss_part[gi * 4 + 1];
+    s2 += loss_part[gi * 4 + 2];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
+  if (lane == 0) {
+    partials[4] += s0;
+    partials[5] += s1;
+    partials[6] = fmax(partials[6], s2 > 0.0 ? 1.0 : 0.0);
+  }
+}
+
 constexpr int kRedSplit = 4;
 __global__ void __launch_bounds__(256) dec_reduce_kernel(const float* __restrict__ a_part,
                                                          const float* __restrict__ bm_part,
@@ -602,15 +626,7 @@ __global__ void __launch_bounds__(256) dec_reduce_kernel(const float* __restrict
   const int64_t qa = do_ar ? (int64_t)K * K / 4 : 0, qb = do_bm ? (int64_t)K * 64 / 4 : 0,
                 qr = do_ar ? (int64_t)K * DS / 4 : 0;
   const int split = blockIdx.y;
-  if (loss_part && blockIdx.x == 0 && split == 0 && threadIdx.x < 3) {
-    const int which = threadIdx.x;
-    double s = 0.0;
-    for (int gi = 0; gi < groups1; ++gi) s += loss_part[gi * 4 + which];
-    if (which == 2)
-      partials[6] = fmax(partials[6], s > 0.0 ? 1.0 : 0.0);
-    else
-      partials[4 + which] += s;
-  }
+  if (loss_part && blockIdx.x == 0 && split == 0 && threadIdx.x < 32) fold_loss_partials(loss_part, groups1, partials);
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < qa + qb + qr;
        q += (int64_t)gridDim.x * blockDim.x) {
     const float4* src;
@@ -679,11 +695,14 @@ __global__ void __launch_bounds__(256) dec_reduce_kernel(const float* __restrict
 // the two output rows with two threads per float4 column (half the sets each).
 __global__ void __launch_bounds__(256) bm_embed_fused_kernel(const float* __restrict__ bm_part, int groups, int K,
                                                              const float* __restrict__ feats, int n_set, int df,
-                                                             float* __restrict__ d_atoms) {
+                                                             float* __restrict__ d_atoms,
+                                                             const double* __restrict__ loss_part, int loss_groups,
+                                                             double* partials) {
   __shared__ float s_half[2][128];
   __shared__ float s_bm[2][64];
   __shared__ float4 s_out[2][128];
   const int tid = threadIdx.x, k0 = blockIdx.x * 2;
+  if (loss_part && blockIdx.x == 0 && tid < 32) fold_loss_partials(loss_part, loss_groups, partials);
   {
     const int pair = tid & 127, hf = tid >> 7;  // (key, set) pair, half of the groups
     const int kk = pair >> 6, sidx = pair & 63;
@@ -774,10 +793,7 @@ void launch_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_
   }
   dec2_kernel<K><<<g2, 288, sm2, st>>>(d2);
   count_launch();
-  // loss partials of this frame
-  dec_reduce_kernel<<<dim3(1, 1), 32, 0, st>>>(nullptr, nullptr, nullptr, w.loss_part, 0, 0, 0, g1, 0, nullptr,
-                                               nullptr, nullptr, partials, 0, 0);
-  count_launch();
+  // this frame's loss partials are folded by the Bm embed that follows (decoder_frame_tc)
   w.tc_frames += 1;
 }
 
@@ -825,14 +841,14 @@ void decoder_frame_tc(cudaStream_t st, DecoderWork& w, const float* query, const
   // and enter once in decoder_finish_tc (they multiply the same D, W in every frame)
   if (df % 4 == 0 && (reinterpret_cast<uintptr_t>(feats) & 15) == 0 && (reinterpret_cast<uintptr_t>(d_atoms) & 15) == 0) {
     bm_embed_fused_kernel<<<(unsigned)(k / 2), 256, 0, st>>>(w.bm_part, kDec2Groups, (int)k, feats, (int)n_set, df,
-                                                           d_atoms);
+                                                           d_atoms, w.loss_part, 148, partials);
     count_launch();
   } else {
     cudaMemsetAsync(w.bm, 0, sizeof(float) * n_set * k, st);
     const int64_t quads = k * 64 / 4;
     dec_reduce_kernel<<<dim3((unsigned)((quads + 255) / 256), deterministic() ? 1 : kRedSplit), 256, 0, st>>>(
-        nullptr, w.bm_part, nullptr, nullptr, (int)k, ds, (int)n_set, 148, kDec2Groups, nullptr, w.bm, nullptr, nullptr,
-        0, 1);
+        nullptr, w.bm_part, nullptr, w.loss_part, (int)k, ds, (int)n_set, 148, kDec2Groups, nullptr, w.bm, nullptr,
+        partials, 0, 1);
     count_launch();
     decoder_bm_embed(st, w.bm, feats, n_set, k, df, d_atoms);
   }
