@@ -648,13 +648,13 @@ __global__ void __launch_bounds__(256) dec_reduce_kernel(const float* __restrict
       ng = groups1;
     }
     const int per = (ng + (int)gridDim.y - 1) / (int)gridDim.y, g0 = split * per, g1 = min(ng, g0 + per);
-    float4 acc[4];
+    float4 acc[8];  // 8 independent 16-byte loads in flight per thread (the slots stream from HBM)
 #pragma unroll
-    for (int u = 0; u < 4; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int u = 0; u < 8; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
     int gi = g0;
-    for (; gi + 4 <= g1; gi += 4) {
+    for (; gi + 8 <= g1; gi += 8) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 8; ++u) {
         const float4 v = __ldg(src + (size_t)(gi + u) * stride);
         acc[u].x += v.x; acc[u].y += v.y; acc[u].z += v.z; acc[u].w += v.w;
       }
@@ -662,6 +662,10 @@ __global__ void __launch_bounds__(256) dec_reduce_kernel(const float* __restrict
     for (; gi < g1; ++gi) {
       const float4 v = __ldg(src + (size_t)gi * stride);
       acc[0].x += v.x; acc[0].y += v.y; acc[0].z += v.z; acc[0].w += v.w;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      acc[u].x += acc[u + 4].x; acc[u].y += acc[u + 4].y; acc[u].z += acc[u + 4].z; acc[u].w += acc[u + 4].w;
     }
     const float4 t = make_float4((acc[0].x + acc[1].x) + (acc[2].x + acc[3].x),
                                  (acc[0].y + acc[1].y) + (acc[2].y + acc[3].y),
@@ -865,7 +869,7 @@ void decoder_finish_tc(cudaStream_t st, DecoderWork& w, const float* atoms, cons
   if (w.tc_frames > 0) {  // the fused frames' A partials (one slot per frame) and step-summed R partials
     const int64_t quads = (k * k + k * ds) / 4;
     const int ngroups_a = kDec2Groups * std::min(w.tc_frames, kDec2Slots);
-    dec_reduce_kernel<<<dim3((unsigned)((quads + 255) / 256), deterministic() ? 1 : kRedSplit), 256, 0, st>>>(
+    dec_reduce_kernel<<<dim3((unsigned)((quads + 255) / 256), deterministic() ? 1 : 2 * kRedSplit), 256, 0, st>>>(
         w.a_part, nullptr, w.r_part, nullptr, (int)k, ds, 0, 148, ngroups_a, w.a_acc, nullptr, w.r_acc, nullptr, 1, 0);
     count_launch();
     w.tc_frames = 0;
