@@ -26,27 +26,24 @@ __device__ __forceinline__ int find_block(const Blocks& B, int64_t e) {
   return -1;
 }
 
-// Pass 1: per-block all-finite check (adam.hpp:65-68), 16-byte loads.
-__global__ void adam_check_kernel(const float* __restrict__ grad, Blocks B, int64_t total, int32_t* flags) {
-  const int64_t n4 = total / 4;
-  const float4* g4 = reinterpret_cast<const float4*>(grad);
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n4; q += (int64_t)gridDim.x * blockDim.x) {
-    const float4 v = g4[q];
-    if (!(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w))) {
-      const float vv[4] = {v.x, v.y, v.z, v.w};
-      for (int i = 0; i < 4; ++i)
-        if (!isfinite(vv[i])) {
-          const int b = find_block(B, 4 * q + i);
-          if (b >= 0) flags[b] = 1;
-        }
+// Pass 1: per-block all-finite check (adam.hpp:65-68) over the active blocks only (kind >= 0),
+// 16-byte loads over each block's 4-aligned interior.
+__global__ void adam_check_kernel(const float* __restrict__ grad, Blocks B, int32_t* flags) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+  for (int bi = 0; bi < B.n; ++bi) {
+    const AdamBlock blk = B.b[bi];
+    if (blk.kind < 0 || blk.count <= 0) continue;
+    const int64_t e0 = blk.offset, e1 = blk.offset + blk.count;
+    const int64_t a0 = (e0 + 3) / 4 * 4, a1 = max(a0, e1 / 4 * 4);
+    bool bad = false;
+    for (int64_t q = a0 / 4 + tid; q < a1 / 4; q += nth) {
+      const float4 v = reinterpret_cast<const float4*>(grad)[q];
+      bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
     }
+    for (int64_t e = e0 + tid; e < min(a0, e1); e += nth) bad |= !isfinite(grad[e]);
+    for (int64_t e = max(a1, e0) + tid; e < e1; e += nth) bad |= !isfinite(grad[e]);
+    if (bad) flags[bi] = 1;
   }
-  for (int64_t e = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x)
-    if (!isfinite(grad[e])) {
-      const int b = find_block(B, e);
-      if (b >= 0) flags[b] = 1;
-    }
 }
 
 __device__ __forceinline__ float adam_elem(float& p, float g, float& m, float& v, float lr, float c1, float c2) {
@@ -217,7 +214,7 @@ void adam_flat(cudaStream_t st, float* param, const float* grad, float* m, float
   if (ext_flags) {
     adam_flags_from_kernel<<<1, 32, 0, st>>>(ext_flags, flags, nblocks);
   } else {
-    adam_check_kernel<<<148 * 4, 256, 0, st>>>(grad, B, total, flags);
+    adam_check_kernel<<<148 * 4, 256, 0, st>>>(grad, B, flags);
   }
   adam_update_kernel<<<148 * 5, 256, 0, st>>>(param, grad, m, v, B, steps, corr1, corr2, table_len, flags,
                                                overflow);

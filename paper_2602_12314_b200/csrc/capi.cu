@@ -760,6 +760,12 @@ struct latmap_session {
   // alternate between two slots (slot 1 below), reused once frame b-2's backward is done (evB)
   cudaStream_t bstream = nullptr;
   std::vector<cudaEvent_t> evD, evB;
+  // latmap_session_step: the colour and feature Adam blocks depend only on the render backward
+  // (K8 writes their gradients directly), so once the last frame's K8 is done they are updated on
+  // rstream while K9 (geometry gradients), the decoder's step-end reduce and the trust term run
+  // on the context stream; session_adam then updates the remaining blocks (LATMAP_EARLY_CF=0: off)
+  bool early_cf = false, cf_done = false;
+  cudaEvent_t ev_cf = nullptr;
   float *d_color2 = nullptr, *d_depth2 = nullptr, *d_query2 = nullptr;
   std::vector<float> dict_w;  // DictionaryState::weights (host; k-means maintenance only)
   // latmap_session_save_state / restore_state: the map, dictionary and MapOptimizer state at the
@@ -978,6 +984,10 @@ static void wait_frame(const latmap_session* s, int b, cudaStream_t st) {
 // (ObjectiveOptions::cached_renders, Stage II of pipeline.cpp:250-259).
 __global__ void overflow_slot_kernel(const int64_t* flag, double* slot) { *slot = *flag ? 1.0 : 0.0; }
 
+constexpr unsigned kAdamAll = 0xffu, kAdamDict = 0xc0u, kAdamColourFeature = (1u << 2) | (1u << 5);
+void session_adam_blocks(latmap_session* s, cudaStream_t st, unsigned mask, int64_t begin = 0, int64_t end = -1,
+                         const double* ext_flags = nullptr);
+
 latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grads = true, bool use_cache = false) {
   latmap_ctx* ctx = s->ctx;
   cudaStream_t st = ctx->stream;
@@ -1164,6 +1174,18 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
     }
   }
   if (pipe) CTX_CHECK(ctx, cudaStreamWaitEvent(st, s->evB[nf - 1], 0));  // join: every backward done
+  s->cf_done = false;
+  if (pipe && s->early_cf) {
+    if (!s->ev_cf) CTX_CHECK(ctx, cudaEventCreateWithFlags(&s->ev_cf, cudaEventDisableTiming));
+    CTX_CHECK(ctx, cudaStreamWaitEvent(s->rstream, s->evB[nf - 1], 0));
+    // every frame's tile-list overflow flag is final (all renders are done): Adam skips on it
+    overflow_slot_kernel<<<1, 1, 0, s->rstream>>>(s->overflow,
+                                                  s->partials + (size_t)s->part_frames * kPart + kTailOverflow);
+    count_launch();
+    session_adam_blocks(s, s->rstream, kAdamColourFeature);
+    CTX_CHECK(ctx, cudaEventRecord(s->ev_cf, s->rstream));
+    s->cf_done = true;
+  }
   if (want_grad && map_grads && pb_multi) {
     // K9 over all frames in one pass: parameters and gradients read once, frame order kept
     std::vector<const float*> rcw(nf), rwc(nf), org(nf);
@@ -1228,8 +1250,22 @@ latmap_status session_assemble(latmap_session* s, latmap_loss_breakdown* out) {
 // MapOptimizer::step_map + step_dict (pipeline.cpp:75-95); dict_only = step_dict alone (Stage II).
 void session_adam(latmap_session* s, bool dict_only = false, int64_t begin = 0, int64_t end = -1,
                   const double* ext_flags = nullptr) {
-  const latmap_config& c = s->cfg;
   s->begin(6);
+  unsigned mask = dict_only ? kAdamDict : kAdamAll;
+  if (s->cf_done && !dict_only && begin == 0 && end < 0 && !ext_flags) {  // colour + feature done early
+    cudaStreamWaitEvent(s->ctx->stream, s->ev_cf, 0);
+    mask &= ~kAdamColourFeature;
+  }
+  s->cf_done = false;
+  session_adam_blocks(s, s->ctx->stream, mask, begin, end, ext_flags);
+  if (!dict_only) s->renders_valid = false;  // the map moves
+  s->end();
+}
+
+// MapOptimizer blocks selected by `mask` (bit i = block i of the flat buffers).
+void session_adam_blocks(latmap_session* s, cudaStream_t st, unsigned mask, int64_t begin, int64_t end,
+                         const double* ext_flags) {
+  const latmap_config& c = s->cfg;
   AdamBlock blocks[8] = {
       {s->off[0], s->len[0], c.lr_position * c.scene_extent, 0},  // pipeline.cpp:76
       {s->off[1], s->len[1], c.lr_rotation, 1},
@@ -1240,14 +1276,12 @@ void session_adam(latmap_session* s, bool dict_only = false, int64_t begin = 0, 
       {s->off[6], s->len[6], c.lr_proj, 0},                       // pipeline.cpp:93
       {s->off[7], s->len[7], c.lr_dict, c.dict_learn ? 0 : -1},  // pipeline.cpp:94
   };
-  if (dict_only)
-    for (int i = 0; i < 6; ++i) blocks[i].kind = -1;
-  else
-    s->renders_valid = false;  // the map moves
-  adam_flat(s->ctx->stream, s->params, s->grads, s->m, s->v, blocks, 8, s->steps, s->skipped, s->corr1, s->corr2,
-            kCorrLen, s->flags, s->partials + (size_t)s->part_frames * kPart + kTailOverflow, s->overflow_steps, begin,
-            end, ext_flags);
-  s->end();
+  for (int i = 0; i < 8; ++i)
+    if (!(mask >> i & 1u)) blocks[i].kind = -1;
+  // the sticky overflow-step counter is advanced once per step: by the call holding block 0
+  adam_flat(st, s->params, s->grads, s->m, s->v, blocks, 8, s->steps, s->skipped, s->corr1, s->corr2, kCorrLen,
+            s->flags, s->partials + (size_t)s->part_frames * kPart + kTailOverflow,
+            (mask & 1u) || mask == kAdamDict ? s->overflow_steps : nullptr, begin, end, ext_flags);
 }
 
 // Grow the tile-pair buffers after an overflow; returns true when something was resized.
@@ -1357,6 +1391,7 @@ latmap_status latmap_session_destroy(latmap_session* s) {
   if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
   if (s->rstream) cudaStreamSynchronize(s->rstream), cudaStreamDestroy(s->rstream);
   if (s->rend_start) cudaEventDestroy(s->rend_start);
+  if (s->ev_cf) cudaEventDestroy(s->ev_cf);
   for (cudaEvent_t e : s->rend_ev) cudaEventDestroy(e);
   if (s->bstream) cudaStreamSynchronize(s->bstream), cudaStreamDestroy(s->bstream);
   for (cudaEvent_t e : s->evD) cudaEventDestroy(e);
@@ -1691,9 +1726,25 @@ latmap_status latmap_session_set_graphs(latmap_session* s, int32_t enable) {
   return LATMAP_OK;
 }
 
+static bool early_cf_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("LATMAP_EARLY_CF");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// RAII: the colour / feature Adam blocks may run early inside this step's objective
+struct EarlyCf {
+  latmap_session* s;
+  explicit EarlyCf(latmap_session* s_) : s(s_) { s->early_cf = early_cf_enabled(); }
+  ~EarlyCf() { s->early_cf = false; }
+};
+
 latmap_status latmap_session_step(latmap_session* s, latmap_loss_breakdown* out) {
   if (!s || s->nframes < 1) return LATMAP_ERR_INVALID_ARGUMENT;
   set_deterministic(s->ctx->deterministic);
+  EarlyCf early(s);
   for (int attempt = 0; attempt < 3; ++attempt) {
     latmap_status st = LATMAP_OK;
     if (s->use_graph && !s->prof && session_sized(s)) {
