@@ -753,6 +753,7 @@ struct latmap_session {
   // renders of every frame run ahead on rstream (they only read the map); frame b's losses,
   // decoder and backward on the context stream wait on rend_ev[b]
   cudaStream_t rstream = nullptr;
+  cudaStream_t rstream2 = nullptr;  // odd frames (LATMAP_RSTREAMS=1: every render on rstream)
   cudaEvent_t rend_start = nullptr;
   std::vector<cudaEvent_t> rend_ev;
   // frame b's render backward runs on bstream behind its losses + decoder (evD[b]) while frame
@@ -1036,6 +1037,11 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
   const bool ahead = !cached_all && !s->prof && nf > 1;
   if (ahead) {
     if (!s->rstream) CTX_CHECK(ctx, cudaStreamCreateWithFlags(&s->rstream, cudaStreamNonBlocking));
+    static const int nrs = [] {
+      const char* e = std::getenv("LATMAP_RSTREAMS");
+      return e && e[0] == '1' ? 1 : 2;
+    }();
+    if (nrs == 2 && !s->rstream2) CTX_CHECK(ctx, cudaStreamCreateWithFlags(&s->rstream2, cudaStreamNonBlocking));
     if (!s->rend_start) CTX_CHECK(ctx, cudaEventCreateWithFlags(&s->rend_start, cudaEventDisableTiming));
     while ((int)s->rend_ev.size() < nf) {
       cudaEvent_t e;
@@ -1045,14 +1051,17 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
     // after the memsets / previous step's update above; joined back frame by frame below
     CTX_CHECK(ctx, cudaEventRecord(s->rend_start, st));
     CTX_CHECK(ctx, cudaStreamWaitEvent(s->rstream, s->rend_start, 0));
+    if (s->rstream2) CTX_CHECK(ctx, cudaStreamWaitEvent(s->rstream2, s->rend_start, 0));
+    // two render streams: frame b+1's binning (small, latency-bound launches) overlaps frame b's
     for (int b = 0; b < nf; ++b) {
       FrameDev& f = s->frames[b];
       RenderBufs& rb = s->rw[b];
+      cudaStream_t rs = (b & 1) && s->rstream2 ? s->rstream2 : s->rstream;
       rb.w.step_overflow = s->overflow;
-      render_forward(s->rstream, map, f.rcw, f.pose.translation, in, rb.w, s->color[b], s->depth[b], s->query[b],
+      render_forward(rs, map, f.rcw, f.pose.translation, in, rb.w, s->color[b], s->depth[b], s->query[b],
                      s->alpha[b], false, false, false);
-      render_blend(s->rstream, map, in, rb.w, s->color[b], s->depth[b], s->query[b], s->alpha[b], ctx->exact_blend);
-      CTX_CHECK(ctx, cudaEventRecord(s->rend_ev[b], s->rstream));
+      render_blend(rs, map, in, rb.w, s->color[b], s->depth[b], s->query[b], s->alpha[b], ctx->exact_blend);
+      CTX_CHECK(ctx, cudaEventRecord(s->rend_ev[b], rs));
     }
   }
   const bool pipe = ahead && want_grad && map_grads;
@@ -1390,6 +1399,7 @@ latmap_status latmap_session_destroy(latmap_session* s) {
   s->drop_graph();
   if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
   if (s->rstream) cudaStreamSynchronize(s->rstream), cudaStreamDestroy(s->rstream);
+  if (s->rstream2) cudaStreamSynchronize(s->rstream2), cudaStreamDestroy(s->rstream2);
   if (s->rend_start) cudaEventDestroy(s->rend_start);
   if (s->ev_cf) cudaEventDestroy(s->ev_cf);
   for (cudaEvent_t e : s->rend_ev) cudaEventDestroy(e);
