@@ -222,9 +222,9 @@ __global__ void row_norms_kernel(const float* __restrict__ x, int64_t n, int d, 
 }
 
 // Per-frame target scores and norms: G[s][k] = E[s] . D[k] (G = E D^T), nv[s] = |E[s]|.
-// CTA = 8 target rows x 32 keys (E rows staged in shared memory); each warp takes 4 keys at a
+// CTA = 4 target rows x 32 keys (E rows staged in shared memory); each warp takes 4 keys at a
 // time with 4 x (df / 128) independent float4 loads of D in flight per lane. Requires df % 4 == 0.
-constexpr int kTsRows = 8, kTsKeys = 32;
+constexpr int kTsRows = 4, kTsKeys = 32;  // 4 rows: twice the CTAs of 8 (48 -> 96 at n_set = 48)
 __global__ void __launch_bounds__(256) target_scores_kernel(const float* __restrict__ feats,
                                                             const float* __restrict__ atoms, int64_t n_set, int k,
                                                             int df, float* __restrict__ gt, float* __restrict__ nv) {

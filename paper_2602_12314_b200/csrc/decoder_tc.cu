@@ -694,25 +694,24 @@ __global__ void __launch_bounds__(256) dec_reduce_kernel(const float* __restrict
 }
 
 // This frame's d_atoms += Bm E from DEC2's per-group Bm partials (groups x K x 64), without
-// materialising Bm^T. CTA = 2 keys, 256 threads: phase 1 sums the partials of each (key, set)
-// pair with two threads (half the groups each, 8 independent loads in flight); phase 2 forms
-// the two output rows with two threads per float4 column (half the sets each).
+// materialising Bm^T. CTA = one key (K CTAs), 256 threads: phase 1 sums the partials of each
+// (key, set) pair with four threads (a quarter of the groups each, 8 independent loads in
+// flight); phase 2 forms the output row with two threads per float4 column (half the sets each).
 __global__ void __launch_bounds__(256) bm_embed_fused_kernel(const float* __restrict__ bm_part, int groups, int K,
                                                              const float* __restrict__ feats, int n_set, int df,
                                                              float* __restrict__ d_atoms,
                                                              const double* __restrict__ loss_part, int loss_groups,
                                                              double* partials) {
-  __shared__ float s_half[2][128];
-  __shared__ float s_bm[2][64];
-  __shared__ float4 s_out[2][128];
-  const int tid = threadIdx.x, k0 = blockIdx.x * 2;
+  __shared__ float s_q[4][64];
+  __shared__ float s_bm[64];
+  __shared__ float4 s_out[128];
+  const int tid = threadIdx.x, k0 = blockIdx.x;
   if (loss_part && blockIdx.x == 0 && tid < 32) fold_loss_partials(loss_part, loss_groups, partials);
   {
-    const int pair = tid & 127, hf = tid >> 7;  // (key, set) pair, half of the groups
-    const int kk = pair >> 6, sidx = pair & 63;
-    const float* src = bm_part + (size_t)(k0 + kk) * 64 + sidx;
+    const int sidx = tid & 63, qq = tid >> 6;  // set, quarter of the groups
+    const float* src = bm_part + (size_t)k0 * 64 + sidx;
     const size_t gs = (size_t)K * 64;
-    const int g0 = hf ? groups / 2 : 0, g1 = hf ? groups : groups / 2;
+    const int per = (groups + 3) / 4, g0 = min(groups, qq * per), g1 = min(groups, g0 + per);
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     int g = g0;
     for (; g + 8 <= g1; g += 8) {
@@ -720,39 +719,31 @@ __global__ void __launch_bounds__(256) bm_embed_fused_kernel(const float* __rest
       for (int u = 0; u < 8; ++u) acc[u] += __ldg(src + (size_t)(g + u) * gs);
     }
     for (; g < g1; ++g) acc[0] += __ldg(src + (size_t)g * gs);
-    s_half[hf][pair] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+    s_q[qq][sidx] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
   }
   __syncthreads();
-  if (tid < 128) s_bm[tid >> 6][tid & 63] = s_half[0][tid] + s_half[1][tid];
+  if (tid < 64) s_bm[tid] = (s_q[0][tid] + s_q[1][tid]) + (s_q[2][tid] + s_q[3][tid]);
   __syncthreads();
   const int hs = tid >> 7, s0 = hs ? n_set / 2 : 0, s1 = hs ? n_set : n_set / 2;
   for (int cb = 0; cb < df / 4; cb += 128) {
     const int c4 = cb + (tid & 127);
-    float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+    float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f);
     if (c4 < df / 4) {
 #pragma unroll 8
       for (int sidx = s0; sidx < s1; ++sidx) {
         const float4 e = __ldg(reinterpret_cast<const float4*>(feats + (size_t)sidx * df) + c4);
-        const float b0 = s_bm[0][sidx], b1 = s_bm[1][sidx];
+        const float b0 = s_bm[sidx];
         a0.x = fmaf(b0, e.x, a0.x), a0.y = fmaf(b0, e.y, a0.y), a0.z = fmaf(b0, e.z, a0.z), a0.w = fmaf(b0, e.w, a0.w);
-        a1.x = fmaf(b1, e.x, a1.x), a1.y = fmaf(b1, e.y, a1.y), a1.z = fmaf(b1, e.z, a1.z), a1.w = fmaf(b1, e.w, a1.w);
       }
     }
-    if (hs == 1) {
-      s_out[0][tid & 127] = a0;
-      s_out[1][tid & 127] = a1;
-    }
+    if (hs == 1) s_out[tid & 127] = a0;
     __syncthreads();
     if (hs == 0 && c4 < df / 4) {
-      const float4 p0 = s_out[0][tid], p1 = s_out[1][tid];
+      const float4 p0 = s_out[tid];
       float4* d0 = reinterpret_cast<float4*>(d_atoms + (size_t)k0 * df) + c4;
-      float4* d1 = reinterpret_cast<float4*>(d_atoms + (size_t)(k0 + 1) * df) + c4;
       float4 o = *d0;
       o.x += a0.x + p0.x, o.y += a0.y + p0.y, o.z += a0.z + p0.z, o.w += a0.w + p0.w;
       *d0 = o;
-      o = *d1;
-      o.x += a1.x + p1.x, o.y += a1.y + p1.y, o.z += a1.z + p1.z, o.w += a1.w + p1.w;
-      *d1 = o;
     }
     __syncthreads();
   }
@@ -844,7 +835,7 @@ void decoder_frame_tc(cudaStream_t st, DecoderWork& w, const float* query, const
   // d_atoms += Bm E for this frame's embedding table; A and R accumulate over the step's frames
   // and enter once in decoder_finish_tc (they multiply the same D, W in every frame)
   if (df % 4 == 0 && (reinterpret_cast<uintptr_t>(feats) & 15) == 0 && (reinterpret_cast<uintptr_t>(d_atoms) & 15) == 0) {
-    bm_embed_fused_kernel<<<(unsigned)(k / 2), 256, 0, st>>>(w.bm_part, kDec2Groups, (int)k, feats, (int)n_set, df,
+    bm_embed_fused_kernel<<<(unsigned)k, 256, 0, st>>>(w.bm_part, kDec2Groups, (int)k, feats, (int)n_set, df,
                                                            d_atoms, w.loss_part, 148, partials);
     count_launch();
   } else {
