@@ -767,6 +767,11 @@ struct latmap_session {
   // on the context stream; session_adam then updates the remaining blocks (LATMAP_EARLY_CF=0: off)
   bool early_cf = false, cf_done = false;
   cudaEvent_t ev_cf = nullptr;
+  // frame b's image losses (colour / depth / SSIM and their gradient images) run on lstream,
+  // beside the decoder on the context stream; K8 waits for both (evL[b], evD[b])
+  // (LATMAP_LSTREAM=0: on the context stream)
+  cudaStream_t lstream = nullptr;
+  std::vector<cudaEvent_t> evL;
   float *d_color2 = nullptr, *d_depth2 = nullptr, *d_query2 = nullptr;
   std::vector<float> dict_w;  // DictionaryState::weights (host; k-means maintenance only)
   // latmap_session_save_state / restore_state: the map, dictionary and MapOptimizer state at the
@@ -1080,6 +1085,16 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
       s->evD.push_back(e1);
       s->evB.push_back(e2);
     }
+    static const bool lstream_env = [] {
+      const char* e = std::getenv("LATMAP_LSTREAM");
+      return !(e && e[0] == '0');
+    }();
+    if (lstream_env && !s->lstream) CTX_CHECK(ctx, cudaStreamCreateWithFlags(&s->lstream, cudaStreamNonBlocking));
+    while (s->lstream && (int)s->evL.size() < nf) {
+      cudaEvent_t e;
+      CTX_CHECK(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      s->evL.push_back(e);
+    }
     if (!s->d_color2) {
       CTX_CHECK(ctx, cudaMalloc(&s->d_color2, sizeof(float) * npx * 3));
       CTX_CHECK(ctx, cudaMalloc(&s->d_depth2, sizeof(float) * npx));
@@ -1109,12 +1124,20 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
       s->end();
     }
     const bool map_grad = want_grad && map_grads;
+    const bool lsplit = pipe && s->lstream;
+    cudaStream_t ls = lsplit ? s->lstream : st;
+    if (lsplit) {
+      if (b >= 2) CTX_CHECK(ctx, cudaStreamWaitEvent(ls, s->evB[b - 2], 0));  // gradient-image slot free
+      CTX_CHECK(ctx, cudaStreamWaitEvent(ls, s->rend_ev[b], 0));
+      wait_frame(s, b, st);  // the decoder's frame data
+    }
     s->begin(2);
-    wait_frame(s, b, st);
-    image_losses(st, s->color[b], s->depth[b], s->alpha[b], f.rgb, f.depth, h, w, c.lambda_i1, c.lambda_i2,
+    wait_frame(s, b, ls);
+    image_losses(ls, s->color[b], s->depth[b], s->alpha[b], f.rgb, f.depth, h, w, c.lambda_i1, c.lambda_i2,
                  c.lambda_rgb * inv_b, c.lambda_depth * inv_b, map_grad, d_col, d_dep, part,
                  s->ssim_scratch);
     s->end();
+    if (lsplit) CTX_CHECK(ctx, cudaEventRecord(s->evL[b], ls));
     if (c.segment_mode)
       set_double_kernel<<<1, 1, 0, st>>>(part + 7, (double)f.n_sup);
     else
@@ -1168,6 +1191,7 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
       if (pipe) {
         CTX_CHECK(ctx, cudaEventRecord(s->evD[b], st));
         CTX_CHECK(ctx, cudaStreamWaitEvent(s->bstream, s->evD[b], 0));
+        if (lsplit) CTX_CHECK(ctx, cudaStreamWaitEvent(s->bstream, s->evL[b], 0));
         bs = s->bstream;
       }
       s->begin(4);
@@ -1402,6 +1426,8 @@ latmap_status latmap_session_destroy(latmap_session* s) {
   if (s->rstream2) cudaStreamSynchronize(s->rstream2), cudaStreamDestroy(s->rstream2);
   if (s->rend_start) cudaEventDestroy(s->rend_start);
   if (s->ev_cf) cudaEventDestroy(s->ev_cf);
+  for (cudaEvent_t e : s->evL) cudaEventDestroy(e);
+  if (s->lstream) cudaStreamSynchronize(s->lstream), cudaStreamDestroy(s->lstream);
   for (cudaEvent_t e : s->rend_ev) cudaEventDestroy(e);
   if (s->bstream) cudaStreamSynchronize(s->bstream), cudaStreamDestroy(s->bstream);
   for (cudaEvent_t e : s->evD) cudaEventDestroy(e);

@@ -1,11 +1,16 @@
-"""Early colour / feature Adam (latmap_session_step): once the last frame's render backward is
+"""Stream scheduling of the Stage-I step against the plain schedule, bit for bit.
+
+Early colour / feature Adam (latmap_session_step): once the last frame's render backward is
 done, the colour and feature blocks -- whose gradients K8 writes directly -- are updated on the
 render stream while the projection backward, the decoder's step-end reduce and the trust term
 run on the context stream; the remaining blocks follow (csrc/capi.cu session_objective /
 session_adam). Against LATMAP_EARLY_CF=0 (all eight blocks after the objective) the step is the
 same arithmetic, so in deterministic mode the parameters, the gradient buffer and the losses are
-bit-identical after several steps, through the captured graph and through direct launches. Each
-variant runs in its own process (the switch is read once)."""
+bit-identical after several steps, through the captured graph and through direct launches. The
+comparison run also puts every render on one render stream (LATMAP_RSTREAMS=1) and the image
+losses back on the context stream (LATMAP_LSTREAM=0), so the two-render-stream and loss-stream
+schedules are covered by the same equality. Each variant runs in its own process (the switches
+are read once)."""
 import os
 import subprocess
 import sys
@@ -50,7 +55,7 @@ def test_early_colour_feature_adam_bit_identical(tmp_path, graphs):
     outs = []
     for mode in ("1", "0"):
         f = tmp_path / f"p{mode}.npy"
-        env = dict(os.environ, LATMAP_EARLY_CF=mode)
+        env = dict(os.environ, LATMAP_EARLY_CF=mode, LATMAP_LSTREAM=mode, LATMAP_RSTREAMS="2" if mode == "1" else "1")
         subprocess.run([sys.executable, "-c", SCRIPT % ROOT, str(f), graphs], env=env, check=True, timeout=600)
         outs.append(np.load(f))
     assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
