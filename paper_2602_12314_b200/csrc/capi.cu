@@ -1125,6 +1125,7 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
     }
     const bool map_grad = want_grad && map_grads;
     const bool lsplit = pipe && s->lstream;
+    bool evd_early = false;  // evD[b] recorded inside the decoder, right after DEC1
     cudaStream_t ls = lsplit ? s->lstream : st;
     if (lsplit) {
       if (b >= 2) CTX_CHECK(ctx, cudaStreamWaitEvent(ls, s->evB[b - 2], 0));  // gradient-image slot free
@@ -1173,10 +1174,14 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
       const bool staged_ok = s->dec.dl_mt && decoder_dl_supported(s->k, s->ds, f.n_set) && ctx->decoder_path != 1;
       s->dec.last_path = (c.decoder_precision == 1 && fused_ok) ? 2 : (c.decoder_precision == 1 && staged_ok) ? 3 : 1;
       s->dec.last_npx = npx;
-      if (c.decoder_precision == 1 && fused_ok)
+      if (c.decoder_precision == 1 && fused_ok) {
+        // K8 of this frame may start once DEC1 has written d_query: DEC2 and the Bm embed overlap it
+        if (pipe && map_grads) s->dec.ev_dq = s->evD[b], evd_early = true;
         decoder_frame_tc(st, s->dec, s->query[b], f.assign, npx, f.feats, f.n_set, f.stat, atoms, proj,
                          c.softmax_temp, c.lambda_cos, c.lambda_l2, c.lambda_feat * inv_b, want_grad, d_qry,
                          g_proj, g_atoms, part);
+        s->dec.ev_dq = nullptr;
+      }
       else if (c.decoder_precision == 1 && staged_ok)
         decoder_frame_dl(st, s->dec, s->query[b], f.assign, npx, f.feats, f.n_set, f.stat, atoms, c.softmax_temp,
                          c.lambda_cos, c.lambda_l2, c.lambda_feat * inv_b, want_grad, d_qry, g_atoms, part);
@@ -1189,7 +1194,7 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
       // geo_acc is zero here: zeroed at allocation, and project_bwd re-zeroes every entry it reads
       cudaStream_t bs = st;
       if (pipe) {
-        CTX_CHECK(ctx, cudaEventRecord(s->evD[b], st));
+        if (!evd_early) CTX_CHECK(ctx, cudaEventRecord(s->evD[b], st));
         CTX_CHECK(ctx, cudaStreamWaitEvent(s->bstream, s->evD[b], 0));
         if (lsplit) CTX_CHECK(ctx, cudaStreamWaitEvent(s->bstream, s->evL[b], 0));
         bs = s->bstream;

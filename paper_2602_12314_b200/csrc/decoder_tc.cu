@@ -768,6 +768,7 @@ void launch_tc(cudaStream_t st, DecoderWork& w, const float* query, const int32_
   }
   dec1_kernel<K, DS><<<g1, 512, sm1, st>>>(d1);
   count_launch();
+  if (w.ev_dq) cudaEventRecord(w.ev_dq, st);  // the render backward needs only d_query
   if (!want_grad) {
     dec_reduce_kernel<<<dim3(1, 1), 32, 0, st>>>(nullptr, nullptr, nullptr, w.loss_part, 0, 0, 0, g1, 0, nullptr,
                                                  nullptr, nullptr, partials, 0, 0);

@@ -128,6 +128,7 @@ struct DecoderWork {
   float* r_acc = nullptr;      // ds x K: sum over the step's frames of Q^T dS
   bool tc_pending = false;     // a_acc / r_acc hold contributions not yet applied
   int tc_frames = 0;           // fused-path frames whose A / R partials are summed in a_part / r_part
+  cudaEvent_t ev_dq = nullptr; // optional: recorded right after DEC1 (d_query complete; DEC2 still to run)
   // staged large-K tcgen05 path scratch (decoder_dl.cu)
   uint8_t* dl_mt = nullptr;    // K x K bf16: M in the B-operand blocks of the T GEMM
   float* dl_t = nullptr;       // ntiles x 128 x K fp16: T = e M (aliases buf1)
