@@ -1011,7 +1011,6 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
   float* g_proj = s->grads + s->off[6];
   float* g_atoms = s->grads + s->off[7];
   CTX_CHECK(ctx, cudaMemsetAsync(s->partials, 0, sizeof(double) * ((size_t)s->part_frames * kPart + kTail), st));
-  if (want_grad) CTX_CHECK(ctx, cudaMemsetAsync(s->grads, 0, sizeof(float) * s->total, st));
   // size the tile-pair buffers the first time a frame is seen
   bool sized = false;
   for (int b = 0; b < nf; ++b) {
@@ -1034,9 +1033,16 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
     }
   }
   CTX_CHECK(ctx, cudaMemsetAsync(s->overflow, 0, sizeof(int64_t), st));
-  decoder_prepare(st, s->dec, atoms, proj);
-  if (s->cfg.decoder_precision == 1 && (ctx->decoder_path == 2 || !decoder_tc_supported(s->k, s->ds, s->dec.nset_cap)))
-    decoder_dl_prepare(st, s->dec);  // M in the staged path's operand blocks
+  // the gradient clear and the decoder's per-step operands are queued after the renders fork
+  // off (below): the renders need neither
+  auto prepare_rest = [&]() -> latmap_status {
+    if (want_grad) CTX_CHECK(ctx, cudaMemsetAsync(s->grads, 0, sizeof(float) * s->total, st));
+    decoder_prepare(st, s->dec, atoms, proj);
+    if (s->cfg.decoder_precision == 1 &&
+        (ctx->decoder_path == 2 || !decoder_tc_supported(s->k, s->ds, s->dec.nset_cap)))
+      decoder_dl_prepare(st, s->dec);  // M in the staged path's operand blocks
+    return LATMAP_OK;
+  };
   const bool cached_all = use_cache && s->renders_valid;
   // side-stream renders: off while phases are profiled (per-phase events need one stream)
   const bool ahead = !cached_all && !s->prof && nf > 1;
@@ -1068,6 +1074,10 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
       render_blend(rs, map, in, rb.w, s->color[b], s->depth[b], s->query[b], s->alpha[b], ctx->exact_blend);
       CTX_CHECK(ctx, cudaEventRecord(s->rend_ev[b], rs));
     }
+  }
+  {
+    const latmap_status ps = prepare_rest();
+    if (ps != LATMAP_OK) return ps;
   }
   const bool pipe = ahead && want_grad && map_grads;
   // projection backward of every frame in one pass after the frame loop (LATMAP_PB_MULTI=0: per frame)
