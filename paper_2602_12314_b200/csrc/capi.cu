@@ -1221,6 +1221,15 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
       if (pipe) CTX_CHECK(ctx, cudaEventRecord(s->evB[b], s->bstream));
     }
   }
+  // the dictionary's step-end terms need only the decoder (this stream): queued before the join,
+  // they overlap the last frames' render backward
+  if (want_grad) decoder_finish_tc(st, s->dec, atoms, proj, g_proj, g_atoms);
+  // trust term enters once (objective.cpp:247-256)
+  if (s->add_trust) {
+    double* tslot = s->partials + (size_t)s->part_frames * kPart;
+    trust_region(st, atoms, s->anchor, s->k, s->df, c.trust_delta, want_grad ? g_atoms : nullptr,
+                 c.lambda_feat * c.lambda_trust, tslot);
+  }
   if (pipe) CTX_CHECK(ctx, cudaStreamWaitEvent(st, s->evB[nf - 1], 0));  // join: every backward done
   s->cf_done = false;
   if (pipe && s->early_cf) {
@@ -1251,13 +1260,6 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
     s->end();
   }
   s->renders_valid = true;
-  if (want_grad) decoder_finish_tc(st, s->dec, atoms, proj, g_proj, g_atoms);
-  // trust term enters once (objective.cpp:247-256)
-  if (s->add_trust) {
-    double* tslot = s->partials + (size_t)s->part_frames * kPart;
-    trust_region(st, atoms, s->anchor, s->k, s->df, c.trust_delta, want_grad ? g_atoms : nullptr,
-                 c.lambda_feat * c.lambda_trust, tslot);
-  }
   // this rank's tile-list overflow flag joins the loss partials, so the sharded step's sum
   // all-reduce tells every rank (and its Adam) that some rank's gradients are incomplete
   overflow_slot_kernel<<<1, 1, 0, st>>>(s->overflow, s->partials + (size_t)s->part_frames * kPart + kTailOverflow);
