@@ -1079,7 +1079,9 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
     const latmap_status ps = prepare_rest();
     if (ps != LATMAP_OK) return ps;
   }
-  const bool pipe = ahead && want_grad && map_grads;
+  // the backward stream (and the early colour/feature Adam) fork off even for a single keyframe
+  // when the decoder is a tcgen05 one: K8 then overlaps the decoder's tail (DEC2 / DL4)
+  const bool pipe = !cached_all && !s->prof && want_grad && map_grads && (nf > 1 || s->cfg.decoder_precision == 1);
   // projection backward of every frame in one pass after the frame loop (LATMAP_PB_MULTI=0: per frame)
   static const bool pb_multi_env = [] {
     const char* e = std::getenv("LATMAP_PB_MULTI");
@@ -1087,6 +1089,7 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
   }();
   const bool pb_multi = pb_multi_env && nf > 1;
   if (pipe) {
+    if (!s->rstream) CTX_CHECK(ctx, cudaStreamCreateWithFlags(&s->rstream, cudaStreamNonBlocking));
     if (!s->bstream) CTX_CHECK(ctx, cudaStreamCreateWithFlags(&s->bstream, cudaStreamNonBlocking));
     while ((int)s->evD.size() < nf) {
       cudaEvent_t e1, e2;
@@ -1134,7 +1137,7 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
       s->end();
     }
     const bool map_grad = want_grad && map_grads;
-    const bool lsplit = pipe && s->lstream;
+    const bool lsplit = pipe && ahead && s->lstream;  // (the loss stream waits on the render streams' events)
     bool evd_early = false;  // evD[b] recorded inside the decoder, right after DEC1
     cudaStream_t ls = lsplit ? s->lstream : st;
     if (lsplit) {
@@ -1192,9 +1195,12 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
                          g_proj, g_atoms, part);
         s->dec.ev_dq = nullptr;
       }
-      else if (c.decoder_precision == 1 && staged_ok)
+      else if (c.decoder_precision == 1 && staged_ok) {
+        if (pipe && map_grads) s->dec.ev_dq = s->evD[b], evd_early = true;  // recorded after DL3 (d_query)
         decoder_frame_dl(st, s->dec, s->query[b], f.assign, npx, f.feats, f.n_set, f.stat, atoms, c.softmax_temp,
                          c.lambda_cos, c.lambda_l2, c.lambda_feat * inv_b, want_grad, d_qry, g_atoms, part);
+        s->dec.ev_dq = nullptr;
+      }
       else
         decoder_frame(st, s->dec, s->query[b], f.assign, npx, f.feats, f.n_set, f.stat, atoms, proj, c.softmax_temp,
                       c.lambda_cos, c.lambda_l2, c.lambda_feat * inv_b, want_grad, d_qry, g_proj, g_atoms, part);

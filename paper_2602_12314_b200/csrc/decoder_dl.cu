@@ -975,6 +975,7 @@ void launch_dl(cudaStream_t st, DecoderWork& w, const float* query, const int32_
     dl_back_kernel<DS><<<2 * kBackGroups, 512, sm, st>>>(d);
     count_launch();
   }
+  if (w.ev_dq) cudaEventRecord(w.ev_dq, st);  // d_query complete: the render backward may start (DL4 overlaps it)
   if (!want_grad) {
     dl_reduce_kernel<<<1, 32, 0, st>>>(nullptr, 0, 0, 0, 0, 0, nullptr, 0, 0, w.loss_part, 2 * kBackGroups,
                                         nullptr, nullptr, nullptr, partials);
