@@ -1103,6 +1103,11 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
       return !(e && e[0] == '0');
     }();
     if (lstream_env && !s->lstream) CTX_CHECK(ctx, cudaStreamCreateWithFlags(&s->lstream, cudaStreamNonBlocking));
+    while (s->lstream && (int)s->rend_ev.size() < nf) {
+      cudaEvent_t e;
+      CTX_CHECK(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      s->rend_ev.push_back(e);
+    }
     while (s->lstream && (int)s->evL.size() < nf) {
       cudaEvent_t e;
       CTX_CHECK(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1135,9 +1140,11 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
       s->begin(1);
       render_blend(st, map, in, rb.w, s->color[b], s->depth[b], s->query[b], s->alpha[b], ctx->exact_blend);
       s->end();
+      // the loss stream's render dependency when the render ran on this stream (single keyframe)
+      if (pipe && s->lstream) CTX_CHECK(ctx, cudaEventRecord(s->rend_ev[b], st));
     }
     const bool map_grad = want_grad && map_grads;
-    const bool lsplit = pipe && ahead && s->lstream;  // (the loss stream waits on the render streams' events)
+    const bool lsplit = pipe && s->lstream && (ahead || !cached);
     bool evd_early = false;  // evD[b] recorded inside the decoder, right after DEC1
     cudaStream_t ls = lsplit ? s->lstream : st;
     if (lsplit) {
