@@ -767,6 +767,7 @@ struct latmap_session {
   // on the context stream; session_adam then updates the remaining blocks (LATMAP_EARLY_CF=0: off)
   bool early_cf = false, cf_done = false;
   cudaEvent_t ev_cf = nullptr;
+  cudaEvent_t ev_pf = nullptr, ev_pj = nullptr;  // single-keyframe step: preparation fork / join
   // frame b's image losses (colour / depth / SSIM and their gradient images) run on lstream,
   // beside the decoder on the context stream; K8 waits for both (evL[b], evD[b])
   // (LATMAP_LSTREAM=0: on the context stream)
@@ -1035,12 +1036,12 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
   CTX_CHECK(ctx, cudaMemsetAsync(s->overflow, 0, sizeof(int64_t), st));
   // the gradient clear and the decoder's per-step operands are queued after the renders fork
   // off (below): the renders need neither
-  auto prepare_rest = [&]() -> latmap_status {
-    if (want_grad) CTX_CHECK(ctx, cudaMemsetAsync(s->grads, 0, sizeof(float) * s->total, st));
-    decoder_prepare(st, s->dec, atoms, proj);
+  auto prepare_rest = [&](cudaStream_t ps) -> latmap_status {
+    if (want_grad) CTX_CHECK(ctx, cudaMemsetAsync(s->grads, 0, sizeof(float) * s->total, ps));
+    decoder_prepare(ps, s->dec, atoms, proj);
     if (s->cfg.decoder_precision == 1 &&
         (ctx->decoder_path == 2 || !decoder_tc_supported(s->k, s->ds, s->dec.nset_cap)))
-      decoder_dl_prepare(st, s->dec);  // M in the staged path's operand blocks
+      decoder_dl_prepare(ps, s->dec);  // M in the staged path's operand blocks
     return LATMAP_OK;
   };
   const bool cached_all = use_cache && s->renders_valid;
@@ -1074,10 +1075,6 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
       render_blend(rs, map, in, rb.w, s->color[b], s->depth[b], s->query[b], s->alpha[b], ctx->exact_blend);
       CTX_CHECK(ctx, cudaEventRecord(s->rend_ev[b], rs));
     }
-  }
-  {
-    const latmap_status ps = prepare_rest();
-    if (ps != LATMAP_OK) return ps;
   }
   // the backward stream (and the early colour/feature Adam) fork off even for a single keyframe
   // when the decoder is a tcgen05 one: K8 then overlaps the decoder's tail (DEC2 / DL4)
@@ -1119,6 +1116,22 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
       CTX_CHECK(ctx, cudaMalloc(&s->d_query2, sizeof(float) * npx * s->ds));
     }
   }
+  // single keyframe: the render runs on this stream next, so the preparation goes to the (idle)
+  // backward stream and is joined after the render
+  bool prep_forked = false;
+  if (pipe && !ahead) {
+    if (!s->ev_pf) CTX_CHECK(ctx, cudaEventCreateWithFlags(&s->ev_pf, cudaEventDisableTiming));
+    if (!s->ev_pj) CTX_CHECK(ctx, cudaEventCreateWithFlags(&s->ev_pj, cudaEventDisableTiming));
+    CTX_CHECK(ctx, cudaEventRecord(s->ev_pf, st));
+    CTX_CHECK(ctx, cudaStreamWaitEvent(s->bstream, s->ev_pf, 0));
+    const latmap_status ps = prepare_rest(s->bstream);
+    if (ps != LATMAP_OK) return ps;
+    CTX_CHECK(ctx, cudaEventRecord(s->ev_pj, s->bstream));
+    prep_forked = true;
+  } else {
+    const latmap_status ps = prepare_rest(st);
+    if (ps != LATMAP_OK) return ps;
+  }
   for (int b = 0; b < nf; ++b) {
     FrameDev& f = s->frames[b];
     RenderBufs& rb = s->rw[b];
@@ -1143,6 +1156,7 @@ latmap_status session_objective(latmap_session* s, bool want_grad, bool map_grad
       // the loss stream's render dependency when the render ran on this stream (single keyframe)
       if (pipe && s->lstream) CTX_CHECK(ctx, cudaEventRecord(s->rend_ev[b], st));
     }
+    if (prep_forked && b == 0) CTX_CHECK(ctx, cudaStreamWaitEvent(st, s->ev_pj, 0));  // gradients cleared, operands ready
     const bool map_grad = want_grad && map_grads;
     const bool lsplit = pipe && s->lstream && (ahead || !cached);
     bool evd_early = false;  // evD[b] recorded inside the decoder, right after DEC1
@@ -1456,6 +1470,8 @@ latmap_status latmap_session_destroy(latmap_session* s) {
   if (s->rstream2) cudaStreamSynchronize(s->rstream2), cudaStreamDestroy(s->rstream2);
   if (s->rend_start) cudaEventDestroy(s->rend_start);
   if (s->ev_cf) cudaEventDestroy(s->ev_cf);
+  if (s->ev_pf) cudaEventDestroy(s->ev_pf);
+  if (s->ev_pj) cudaEventDestroy(s->ev_pj);
   for (cudaEvent_t e : s->evL) cudaEventDestroy(e);
   if (s->lstream) cudaStreamSynchronize(s->lstream), cudaStreamDestroy(s->lstream);
   for (cudaEvent_t e : s->rend_ev) cudaEventDestroy(e);
